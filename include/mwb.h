@@ -1,0 +1,166 @@
+/*
+ * mwb.h — C ABI of the B200 (sm_100a) confocal DAS/DMAS imaging path.
+ *
+ * This is the drop-in boundary below the reference's Python imaging entry
+ * points (package `mwbeam`, /root/reference/pkg/src/mwbeam).  Every entry
+ * point takes plain device pointers, sizes and a cudaStream_t passed as
+ * `void*`; nothing here allocates on the hot path and no torch type appears
+ * in a signature.  All functions return 0 on success and a negative code on
+ * error; `mwb_last_error()` returns a thread-local message for the last
+ * failure on the calling thread.
+ *
+ * Replaced reference interfaces (file:line relative to /root/reference):
+ *   mwb_energies           <- pkg/src/mwbeam/beamform.py:169-212  _multistatic_energies
+ *                             (also das_energy / dmas_energy, beamform.py:242-253,
+ *                              and the 64-point batching of image(), beamform.py:325-336)
+ *   mwb_enumerate_lattice  <- pkg/src/mwbeam/beamform.py:268-280  _region_cells
+ *                             + the skip filter of image(), beamform.py:309-315
+ *                             + cell centres, beamform.py:321-323
+ *   mwb_select_roi         <- pkg/src/mwbeam/coarse2fine.py:169-256 select_roi
+ *   mwb_argmax_dense       <- pkg/src/mwbeam/beamform.py:101-104  EnergyMap.argmax_cell
+ *                             (also fused into mwb_energies through `argmax_key`)
+ */
+#ifndef MWB_H
+#define MWB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* beamformer kind (reference BeamformerKind, beamform.py:41-50) */
+#define MWB_DAS 0
+#define MWB_DMAS 1
+
+/* interpolation (reference _check_interpolation, beamform.py:131-133) */
+#define MWB_INTERP_LINEAR 0
+#define MWB_INTERP_NEAREST 1
+
+/* status codes */
+#define MWB_OK 0
+#define MWB_EINVAL (-1)
+#define MWB_ECUDA (-2)
+#define MWB_ERANGE (-3)
+
+/* select_roi termination codes (reference MetricTrace.termination strings) */
+#define MWB_TERM_NONE 0
+#define MWB_TERM_DEGENERATE 1       /* "degenerate"       coarse2fine.py:189-192 */
+#define MWB_TERM_REGION_FLOOR 2     /* "region-floor"     coarse2fine.py:202-205 */
+#define MWB_TERM_N_MIN 3            /* "n-min"            coarse2fine.py:227-229 */
+#define MWB_TERM_DISTANCE 4         /* "distance-metrics" coarse2fine.py:250-252 */
+#define MWB_TERM_EMPTY (-1)         /* ValueError         coarse2fine.py:187-188 */
+#define MWB_TERM_OVERFLOW (-2)      /* more than MWB_MAX_ITERS iterations */
+
+#define MWB_MAX_ITERS 64
+
+/* one select_roi iteration (reference IterationRecord, coarse2fine.py:127-152).
+ * Regions are inclusive cell bounds {x0, y0, x1, y1}. has_stats: 0 = None
+ * (empty quadrant), 1 = {"mu","var"} (first iteration), 2 = full metric parts. */
+typedef struct mwb_iter_record {
+  int32_t iteration;
+  int32_t quadrant_counts[4];
+  int32_t selected;
+  int32_t satisfied;
+  int32_t has_stats[4];
+  int32_t clamped[4];
+  int32_t selected_region[4];
+  int32_t expanded_region[4];
+  int32_t _pad;
+  double scores[4];
+  double mu[4];
+  double var[4];
+  double delta_raw[4];
+  double delta[4];
+  double w;
+  double b;
+} mwb_iter_record_t;
+
+/* select_roi trace (reference MetricTrace, coarse2fine.py:155-166) */
+typedef struct mwb_trace {
+  int32_t termination;
+  int32_t n_records;
+  int32_t final_region[4];
+  int32_t _pad[2];
+  mwb_iter_record_t records[MWB_MAX_ITERS];
+} mwb_trace_t;
+
+const char* mwb_last_error(void);
+int mwb_version(void);
+/* sizeof(mwb_trace_t), for binding-layout checks */
+int64_t mwb_trace_bytes(void);
+
+/*
+ * Synthesized DAS/DMAS energies of a list of focal points over S scans that
+ * share one antenna geometry.
+ *
+ *   sig        device fp32 [S][n_chan][ld]; populated channels only (all-zero
+ *              channels contribute exactly 0 in the reference and are dropped);
+ *              samples n_samples..ld-1 must be zero; ld % 4 == 0.
+ *   scan_stride  floats between scans (multiple of 4).
+ *   chan_txrx  device int32 [n_chan][2] transmitter/receiver antenna index.
+ *   ant_xyz    device fp64 [n_ant][3] antenna positions (m).
+ *   inv_scale  1 / (propagation_speed * sample_interval)  (samples per metre).
+ *   pts_xyz    device fp64 [n_pts][3] focal points (z = 0 for the 2-D slice).
+ *   out_idx    device int32 [n_pts] output slot of each point (NULL = identity).
+ *   d_count    device int32 scalar overriding n_pts (<= n_pts) or NULL; lets a
+ *              device-side enumerator feed this launch without a host sync.
+ *   kind       MWB_DAS / MWB_DMAS;  interp MWB_INTERP_*.
+ *   k0, window energy is summed over aligned samples k in [k0, k0+window);
+ *              the reference's full-record sum is k0 = 0, window = n_samples.
+ *   out        device fp32, out[s*out_stride + out_idx[p]].
+ *   argmax_key device uint64 [S] or NULL: atomicMax of (ordered(value)<<32 |
+ *              ~slot), i.e. the max energy with ties to the lowest slot.
+ *   flags      device int32 or NULL: bit 0 set when a non-finite energy occurs.
+ *   mode       0 = shared-memory staged (TMA bulk copies), 1 = L1/L2 gather.
+ */
+int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
+                 int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
+                 double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
+                 const int32_t* d_count, int kind, int interp, int k0, int window, float* out,
+                 int64_t out_stride, uint64_t* argmax_key, int32_t* flags, int mode,
+                 void* stream);
+
+/* Workspace (bytes) for mwb_enumerate_lattice on an nx x ny grid at `stride`. */
+int64_t mwb_lattice_workspace_bytes(int nx, int ny, int stride);
+
+/*
+ * Enumerate the stride-`stride` lattice cells of region {x0,y0,x1,y1} (or of
+ * the region stored at d_region when non-NULL), keep cells with mask[ix*ny+iy]
+ * (mask may be NULL) and drop cells with ix%skip==0 && iy%skip==0 when
+ * skip_stride > 0.  Writes fp64 cell centres origin + (i + 0.5) * res
+ * (pts_xyz, z = 0), the dense slot ix*ny+iy (out_idx), the count (d_count)
+ * and sets valid[slot] = 1.  Points come out in 16x16-lattice-tile order.
+ */
+int mwb_enumerate_lattice(double ox, double oy, double res, int nx, int ny, int x0, int y0,
+                          int x1, int y1, const int32_t* d_region, int stride,
+                          const uint8_t* mask, int skip_stride, double* pts_xyz,
+                          int32_t* out_idx, int32_t* d_count, uint8_t* valid, void* workspace,
+                          void* stream);
+
+/*
+ * Device-resident iterative quadrant selection on a dense nx x ny energy map
+ * whose valid cells lie on multiples of `lattice`.  Region {x0,y0,x1,y1} is
+ * the breast region.  Writes the final region to d_region_out (int32[4]) and
+ * the full trace to d_trace (mwb_trace_t).  One CTA, no host sync.
+ */
+int mwb_select_roi(const float* dense, const uint8_t* valid, int nx, int ny, int lattice,
+                   int x0, int y0, int x1, int y1, double frame_fraction, int n_min,
+                   int32_t* d_region_out, mwb_trace_t* d_trace, void* stream);
+
+/* argmax over a dense map (valid cells only); key as in mwb_energies. */
+int mwb_argmax_dense(const float* dense, const uint8_t* valid, int n, uint64_t* key,
+                     void* stream);
+
+/*
+ * Roofline microbenchmarks run on the device: which = 0 shared-memory LDS.32
+ * bandwidth (bytes), 1 FFMA2 (flops), 2 scalar FFMA (flops).  Writes the work
+ * done by one launch to *work and the elapsed milliseconds to *ms.
+ */
+int mwb_microbench(int which, double* work, float* ms, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MWB_H */

@@ -1,0 +1,116 @@
+"""Device residency of scans, masks and workspaces.
+
+A scan is uploaded once per (frozen) dataset object: the populated channels
+(any nonzero sample) are compacted in the reference's row-major (i, j) channel
+order into an fp32 ``[C][ld]`` buffer with a zero tail (ld = N rounded up to
+4 samples, so every TMA bulk copy is 16-byte aligned).  All-zero channels are
+dropped because they add exactly 0 to DAS and DMAS in the reference
+(beamform.py:199-212).  Device buffers are torch tensors; only raw pointers
+cross into ``libmwb.so``.
+"""
+
+from __future__ import annotations
+
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 imaging path needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def round4(n: int) -> int:
+    return max(4, (int(n) + 3) // 4 * 4)
+
+
+@dataclass
+class DeviceScan:
+    sig: torch.Tensor  # (C, ld) float32
+    chan: torch.Tensor  # (C, 2) int32
+    ant: torch.Tensor  # (M, 3) float64
+    inv_scale: float
+    n_samples: int
+    ld: int
+    n_ant: int
+    chan_host: np.ndarray  # (C, 2) int32
+
+    @property
+    def n_chan(self) -> int:
+        return int(self.chan_host.shape[0])
+
+
+def compact_channels(signals: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Populated channels of an (M, M, N) array: (C, N) float32 and (C, 2) pairs.
+
+    A dataset with no populated channel keeps channel (0, 0) (all zeros) so the
+    launch shape stays valid; its energies are exactly 0, as in the reference.
+    """
+    m, _, n = signals.shape
+    flat = signals.reshape(m * m, n)
+    keep = np.flatnonzero(np.any(flat != 0.0, axis=1)) if n > 0 else np.zeros(0, dtype=np.int64)
+    if keep.size == 0:
+        keep = np.zeros(1, dtype=np.int64)
+    pairs = np.stack([keep // m, keep % m], axis=1).astype(np.int32)
+    return flat[keep].astype(np.float32), pairs
+
+
+_SCANS: dict[int, tuple[weakref.ref, DeviceScan]] = {}
+
+
+def _build_scan(ds) -> DeviceScan:
+    geom = ds.geometry
+    sig = np.asarray(ds.signals)
+    m, _, n = sig.shape
+    comp, pairs = compact_channels(sig)
+    ld = round4(n)
+    dev = device()
+    host = np.zeros((comp.shape[0], ld), dtype=np.float32)
+    host[:, :n] = comp
+    scale = float(geom.propagation_speed) * float(geom.sample_interval)
+    return DeviceScan(
+        sig=torch.from_numpy(host).to(dev),
+        chan=torch.from_numpy(pairs).to(dev),
+        ant=torch.from_numpy(np.ascontiguousarray(geom.antennas, dtype=np.float64)).to(dev),
+        inv_scale=1.0 / scale,
+        n_samples=n,
+        ld=ld,
+        n_ant=m,
+        chan_host=pairs,
+    )
+
+
+def scan_for(ds) -> DeviceScan:
+    """Device copy of ``ds``; cached while ``ds`` lives if its signals are read-only."""
+    sig = np.asarray(ds.signals)
+    cacheable = not sig.flags.writeable
+    key = id(ds)
+    if cacheable:
+        hit = _SCANS.get(key)
+        if hit is not None and hit[0]() is ds:
+            return hit[1]
+    scan = _build_scan(ds)
+    if cacheable:
+        try:
+            ref = weakref.ref(ds, lambda _r, k=key: _SCANS.pop(k, None))
+        except TypeError:
+            return scan
+        _SCANS[key] = (ref, scan)
+    return scan
+
+
+def upload_mask(mask: np.ndarray | None, dims: tuple[int, int]) -> torch.Tensor | None:
+    if mask is None:
+        return None
+    m = np.asarray(mask, dtype=bool)
+    if m.shape != tuple(dims):
+        raise ValueError(f"mask must have the grid's dims {tuple(dims)}, got {m.shape}")
+    return torch.from_numpy(np.ascontiguousarray(m).view(np.uint8)).to(device())

@@ -1,0 +1,124 @@
+"""ctypes binding of ``libmwb.so`` (the C ABI in include/mwb.h).
+
+There is no CPU fallback: if the library is missing or a call fails, a
+``RuntimeError`` carrying ``mwb_last_error()`` is raised.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from ._build import LIB
+
+MWB_DAS = 0
+MWB_DMAS = 1
+INTERP = {"linear": 0, "nearest": 1}
+MAX_ITERS = 64
+
+TERMINATION = {
+    0: "",
+    1: "degenerate",
+    2: "region-floor",
+    3: "n-min",
+    4: "distance-metrics",
+    -1: "empty",
+    -2: "overflow",
+}
+
+
+class IterRecord(C.Structure):
+    _fields_ = [
+        ("iteration", C.c_int32),
+        ("quadrant_counts", C.c_int32 * 4),
+        ("selected", C.c_int32),
+        ("satisfied", C.c_int32),
+        ("has_stats", C.c_int32 * 4),
+        ("clamped", C.c_int32 * 4),
+        ("selected_region", C.c_int32 * 4),
+        ("expanded_region", C.c_int32 * 4),
+        ("_pad", C.c_int32),
+        ("scores", C.c_double * 4),
+        ("mu", C.c_double * 4),
+        ("var", C.c_double * 4),
+        ("delta_raw", C.c_double * 4),
+        ("delta", C.c_double * 4),
+        ("w", C.c_double),
+        ("b", C.c_double),
+    ]
+
+
+class Trace(C.Structure):
+    _fields_ = [
+        ("termination", C.c_int32),
+        ("n_records", C.c_int32),
+        ("final_region", C.c_int32 * 4),
+        ("_pad", C.c_int32 * 2),
+        ("records", IterRecord * MAX_ITERS),
+    ]
+
+
+TRACE_BYTES = C.sizeof(Trace)
+
+_P = C.c_void_p
+_I = C.c_int
+_I64 = C.c_int64
+_D = C.c_double
+
+_SIGNATURES = {
+    "mwb_last_error": ([], C.c_char_p),
+    "mwb_version": ([], _I),
+    "mwb_trace_bytes": ([], _I64),
+    "mwb_energies": (
+        [_P, _I, _I64, _I, _I, _I, _P, _P, _I, _D, _P, _P, _I, _P, _I, _I, _I, _I, _P, _I64, _P, _P, _I, _P],
+        _I,
+    ),
+    "mwb_lattice_workspace_bytes": ([_I, _I, _I], _I64),
+    "mwb_enumerate_lattice": (
+        [_D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _P, _P, _P, _P, _P],
+        _I,
+    ),
+    "mwb_select_roi": ([_P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P], _I),
+    "mwb_argmax_dense": ([_P, _P, _I, _P, _P], _I),
+    "mwb_microbench": ([_I, C.POINTER(C.c_double), C.POINTER(C.c_float), _P], _I),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+_lib: C.CDLL | None = None
+
+
+def load(path: Path | str | None = None) -> C.CDLL:
+    """Load (once) and type the shared library; raise if it is absent."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB
+    if not p.exists():
+        raise RuntimeError(
+            f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the GPU path has no CPU fallback)"
+        )
+    lib = C.CDLL(str(p))
+    for name, (args, res) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        msg = load().mwb_last_error()
+        raise RuntimeError(f"{what} failed ({status}): {msg.decode() if msg else ''}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def ptr(t) -> int | None:
+    """Raw device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()

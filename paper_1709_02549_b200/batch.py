@@ -1,0 +1,183 @@
+"""Batched multi-scan imaging (BASELINE configs[3]: 4096 scans x 256^2, DAS + DMAS).
+
+The reference images one dataset per ``image()`` call
+(/root/reference/pkg/src/mwbeam/beamform.py:283-342).  Here S scans that
+share an antenna geometry and a grid are imaged by one launch per kind: the
+focal-point list is enumerated once on the device, every CTA stages a tile's
+channel spans for several scans in turn (reusing its per-point distance
+table), and each scan's argmax (the detected tumour cell, ties to the lowest
+(ix, iy)) is fused into the epilogue.
+
+``BatchImager.run_device`` works on device-resident scans (throughput);
+``BatchImager.__call__`` is the end-to-end host API: pinned host scans in,
+host energy maps out, with chunked H2D / compute / D2H overlapped on three
+CUDA streams.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _native as nat
+from .beamform import _kind_code, _Status, _window
+from .geometry import ArrayGeometry, ImagingGrid
+
+
+@dataclass
+class BatchResult:
+    maps: dict  # kind -> (S, nx, ny) float32 (host or device)
+    argmax: dict  # kind -> (S, 2) int cells
+
+
+class BatchImager:
+    def __init__(self, geometry: ArrayGeometry, pairs, n_samples: int, grid: ImagingGrid, window=None,
+                 mask: np.ndarray | None = None, interpolation: str = "linear", mode: str = "smem"):
+        dev = dv.device()
+        self.grid = grid
+        self.n_samples = int(n_samples)
+        self.ld = dv.round4(n_samples)
+        self.k0, self.w = _window(self.n_samples, window)
+        self.interp = nat.INTERP[interpolation]
+        self.mode = {"smem": 0, "gather": 1}[mode]
+        pairs = np.asarray(pairs, dtype=np.int32).reshape(-1, 2)
+        m = geometry.n_antennas
+        if pairs.size == 0 or pairs.min() < 0 or pairs.max() >= m:
+            raise ValueError("pairs must index the geometry's antennas")
+        self.scan = dv.DeviceScan(
+            sig=torch.empty(0, device=dev),
+            chan=torch.from_numpy(pairs).to(dev),
+            ant=torch.from_numpy(np.ascontiguousarray(geometry.antennas, dtype=np.float64)).to(dev),
+            inv_scale=1.0 / (float(geometry.propagation_speed) * float(geometry.sample_interval)),
+            n_samples=self.n_samples,
+            ld=self.ld,
+            n_ant=m,
+            chan_host=pairs,
+        )
+        nx, ny = grid.dims
+        # enumerate the grid once (device), read the point count once
+        emask = dv.upload_mask(mask, (nx, ny))
+        p_max = nx * ny
+        self.pts = torch.empty((p_max, 3), dtype=torch.float64, device=dev)
+        self.oidx = torch.empty(p_max, dtype=torch.int32, device=dev)
+        self.valid = torch.zeros(p_max, dtype=torch.uint8, device=dev)
+        st = _Status()
+        ws = torch.empty(int(nat.load().mwb_lattice_workspace_bytes(nx, ny, 1)), dtype=torch.uint8, device=dev)
+        nat.call("mwb_enumerate_lattice", grid.origin[0], grid.origin[1], grid.resolution, nx, ny, 0, 0, nx - 1,
+                 ny - 1, None, 1, nat.ptr(emask), 0, self.pts.data_ptr(), self.oidx.data_ptr(), st.count_ptr(0),
+                 self.valid.data_ptr(), ws.data_ptr(), dv.stream_handle())
+        _, counts, _ = st.read()
+        self.n_pts = int(counts[0])
+        self.valid_host = self.valid.view(nx, ny).cpu().numpy().astype(bool)
+
+    @property
+    def n_chan(self) -> int:
+        return self.scan.n_chan
+
+    def launches_per_kind(self) -> int:
+        return 1
+
+    def run_device(self, sig: torch.Tensor, kind, out: torch.Tensor, keys: torch.Tensor | None = None,
+                   flags: torch.Tensor | None = None) -> None:
+        """Image S device-resident scans ``sig`` (S, C, ld) fp32 into ``out`` (S, nx*ny) fp32.
+
+        ``keys`` (S,) int64 receives the per-scan argmax key (zero it first).
+        Stream ordered, no host synchronisation.
+        """
+        s = int(sig.shape[0])
+        if sig.dtype != torch.float32 or sig.shape[1:] != (self.n_chan, self.ld) or not sig.is_contiguous():
+            raise ValueError(f"sig must be contiguous float32 (S, {self.n_chan}, {self.ld})")
+        nxny = self.grid.dims[0] * self.grid.dims[1]
+        if out.shape != (s, nxny) or out.dtype != torch.float32:
+            raise ValueError(f"out must be float32 (S, {nxny})")
+        if self.w == 0 or s == 0:
+            out.zero_()
+            return
+        nat.call(
+            "mwb_energies", sig.data_ptr(), s, self.n_chan * self.ld, self.n_chan, self.ld, self.n_samples,
+            self.scan.chan.data_ptr(), self.scan.ant.data_ptr(), self.scan.n_ant, self.scan.inv_scale,
+            self.pts.data_ptr(), self.oidx.data_ptr(), self.n_pts, None, _kind_code(kind), self.interp, self.k0,
+            self.w, out.data_ptr(), nxny, nat.ptr(keys), nat.ptr(flags), self.mode, dv.stream_handle(),
+        )
+
+    def decode_keys(self, keys: np.ndarray) -> np.ndarray:
+        ny = self.grid.dims[1]
+        slot = 0xFFFFFFFF - (keys.astype(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        return np.stack([slot // ny, slot % ny], axis=1)
+
+    def to_device_layout(self, host: np.ndarray | torch.Tensor) -> torch.Tensor:
+        """(S, C, N) host scans -> (S, C, ld) fp32 device tensor."""
+        t = torch.as_tensor(host)
+        if t.dtype != torch.float32:
+            t = t.float()
+        dev = dv.device()
+        if self.ld == self.n_samples:
+            return t.to(dev, non_blocking=True).contiguous()
+        out = torch.zeros((t.shape[0], t.shape[1], self.ld), dtype=torch.float32, device=dev)
+        out[:, :, : self.n_samples] = t.to(dev)
+        return out
+
+    def __call__(self, signals, kinds=("das", "dmas"), chunk: int = 256, out=None) -> BatchResult:
+        """End-to-end: host (S, C, N) fp32 scans (pinned torch tensor or numpy) ->
+        host (S, nx, ny) fp32 maps per kind + per-scan argmax cells.
+
+        Inputs are copied in chunks on a copy stream, imaged on a compute
+        stream and copied back on a third stream, so PCIe traffic in both
+        directions overlaps the kernels.
+        """
+        host = torch.as_tensor(signals)
+        if host.dtype != torch.float32 or host.dim() != 3 or host.shape[1:] != (self.n_chan, self.n_samples):
+            raise ValueError(f"signals must be float32 (S, {self.n_chan}, {self.n_samples})")
+        if self.ld != self.n_samples:
+            raise ValueError("the end-to-end path needs n_samples % 4 == 0")
+        s_total = int(host.shape[0])
+        nx, ny = self.grid.dims
+        kinds = list(kinds)
+        if out is None:
+            out = {k: torch.empty((s_total, nx * ny), dtype=torch.float32, pin_memory=host.is_pinned())
+                   for k in kinds}
+        dev = dv.device()
+        chunk = max(1, min(chunk, s_total))
+        n_chunks = (s_total + chunk - 1) // chunk
+        nbuf = 2
+        dev_in = [torch.empty((chunk, self.n_chan, self.ld), dtype=torch.float32, device=dev) for _ in range(nbuf)]
+        dev_out = [{k: torch.empty((chunk, nx * ny), dtype=torch.float32, device=dev) for k in kinds}
+                   for _ in range(nbuf)]
+        keys = torch.zeros((len(kinds), s_total), dtype=torch.int64, device=dev)
+        s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+        for st in (s_in, s_cmp, s_out):
+            st.wait_stream(main)
+        ev_in = [torch.cuda.Event() for _ in range(n_chunks)]
+        ev_cmp = [torch.cuda.Event() for _ in range(n_chunks)]
+        ev_out = [torch.cuda.Event() for _ in range(n_chunks)]
+        for i in range(n_chunks):
+            a, b = i * chunk, min(s_total, (i + 1) * chunk)
+            n = b - a
+            buf = i % nbuf
+            with torch.cuda.stream(s_in):
+                if i >= nbuf:
+                    s_in.wait_event(ev_cmp[i - nbuf])
+                dev_in[buf][:n].copy_(host[a:b], non_blocking=True)
+                ev_in[i].record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev_in[i])
+                if i >= nbuf:
+                    s_cmp.wait_event(ev_out[i - nbuf])
+                for ki, k in enumerate(kinds):
+                    self.run_device(dev_in[buf][:n], k, dev_out[buf][k][:n], keys[ki, a:b])
+                ev_cmp[i].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_cmp[i])
+                for k in kinds:
+                    out[k][a:b].copy_(dev_out[buf][k][:n], non_blocking=True)
+                ev_out[i].record(s_out)
+        main.wait_stream(s_out)
+        main.wait_stream(s_cmp)
+        keys_h = keys.cpu().numpy().view(np.uint64)
+        main.synchronize()
+        maps = {k: out[k].view(s_total, nx, ny) for k in kinds}
+        return BatchResult(maps=maps, argmax={k: self.decode_keys(keys_h[ki]) for ki, k in enumerate(kinds)})

@@ -1,0 +1,410 @@
+"""Drop-in DAS/DMAS imaging on the B200.
+
+Public functions keep the signatures of the reference module
+/root/reference/pkg/src/mwbeam/beamform.py:
+
+* ``image(ds, kind, grid, region, stride, mask, threads, skip, interpolation)``
+  (beamform.py:283-342) — one device pass: the lattice/mask/skip enumeration
+  (beamform.py:268-280, 309-323) and the energy kernel
+  (``_multistatic_energies``, beamform.py:169-212) run as CUDA kernels from
+  ``libmwb.so``; the result is a dense-backed ``EnergyMap``.
+* ``das_energy`` / ``dmas_energy`` / ``point_energy`` (beamform.py:242-265) —
+  the same kernel on a one-point list, so ``image(...)[cell] ==
+  das_energy(ds, grid.cell_center(*cell))`` bit for bit.
+* ``EnergyMap`` (beamform.py:78-128) and ``EVAL_COUNTER`` (beamform.py:53-75).
+
+Extensions (keyword-only): ``window=(k0, W)`` sums the energy over aligned
+samples [k0, k0+W) instead of the full record (BASELINE configs use a 32- or
+48-sample window); ``mode="gather"`` selects the L1/L2-gather kernel variant
+used for the shared-memory-vs-L2 comparison.  ``threads`` is accepted and
+ignored: results never depend on it.  Arithmetic is fp32 (delays fp64).
+"""
+
+from __future__ import annotations
+
+import threading
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _native as nat
+from .geometry import ImagingGrid, Region, delay_multistatic
+
+_MODES = {"smem": 0, "gather": 1}
+
+
+class BeamformerKind(Enum):
+    DAS = "das"
+    DMAS = "dmas"
+
+    @classmethod
+    def parse(cls, name: str) -> "BeamformerKind":
+        try:
+            return cls(name.strip().lower())
+        except ValueError:
+            raise ValueError(f"unknown beamformer kind: {name!r}") from None
+
+
+def _kind(kind) -> BeamformerKind:
+    if isinstance(kind, BeamformerKind):
+        return kind
+    if isinstance(kind, str):
+        return BeamformerKind.parse(kind)
+    value = getattr(kind, "value", None)  # the reference's own enum
+    if isinstance(value, str):
+        return BeamformerKind.parse(value)
+    raise ValueError(f"unknown beamformer kind: {kind!r}")
+
+
+def _kind_code(kind) -> int:
+    return nat.MWB_DAS if _kind(kind) is BeamformerKind.DAS else nat.MWB_DMAS
+
+
+class EvalCounter:
+    """Thread-safe count of focal points evaluated (kernel invocations)."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._n = 0
+
+    def add(self, n: int) -> None:
+        with self._lock:
+            self._n += int(n)
+
+    @property
+    def value(self) -> int:
+        with self._lock:
+            return self._n
+
+    def reset(self) -> None:
+        with self._lock:
+            self._n = 0
+
+
+EVAL_COUNTER = EvalCounter()
+
+
+class EnergyMap:
+    """Sparse map ``(ix, iy) -> energy`` (reference beamform.py:78-128).
+
+    Maps produced by the GPU path are backed by a dense (nx, ny) fp32 array
+    plus a validity mask; the ``entries`` dict is materialised on first use.
+    Entry order is the reference's: ix-major for ``image()``; for framework
+    composites the coarse entries first, then the fine ones.
+    """
+
+    def __init__(self, grid: ImagingGrid, entries: dict | None = None, stride: int = 1, roi: Region | None = None):
+        self.grid = grid
+        self.stride = stride
+        self.roi = roi
+        self._entries = entries if entries is not None else {}
+        self._values: np.ndarray | None = None
+        self._valid: np.ndarray | None = None
+        self._split: int = 0
+        if self._entries:
+            vals = np.fromiter(self._entries.values(), dtype=np.float64, count=len(self._entries))
+            if not np.isfinite(vals).all():
+                raise ValueError("energy map contains non-finite values")
+
+    @classmethod
+    def _from_dense(cls, grid, values: np.ndarray, valid: np.ndarray, stride: int = 1, roi=None, split: int = 0):
+        em = cls.__new__(cls)
+        em.grid, em.stride, em.roi = grid, stride, roi
+        em._entries = None
+        em._values = values
+        em._valid = valid
+        em._split = split
+        if valid.any() and not np.isfinite(values[valid]).all():
+            raise ValueError("energy map contains non-finite values")
+        return em
+
+    # -- entries -----------------------------------------------------------
+    def _cells_in_order(self) -> tuple[np.ndarray, np.ndarray]:
+        ix, iy = np.nonzero(self._valid)
+        if self._split > 1:
+            lat = (ix % self._split == 0) & (iy % self._split == 0)
+            order = np.concatenate([np.flatnonzero(lat), np.flatnonzero(~lat)])
+            ix, iy = ix[order], iy[order]
+        return ix, iy
+
+    @property
+    def entries(self) -> dict:
+        if self._entries is None:
+            ix, iy = self._cells_in_order()
+            vals = self._values[ix, iy].astype(np.float64)
+            self._entries = dict(zip(zip(ix.tolist(), iy.tolist()), vals.tolist()))
+        return self._entries
+
+    @entries.setter
+    def entries(self, value: dict) -> None:
+        self._entries = value
+        self._values = self._valid = None
+
+    def __len__(self) -> int:
+        if self._entries is None:
+            return int(self._valid.sum())
+        return len(self._entries)
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, EnergyMap):
+            return NotImplemented
+        return (
+            self.grid == other.grid
+            and self.stride == other.stride
+            and self.roi == other.roi
+            and self.entries == other.entries
+        )
+
+    __hash__ = None
+
+    def __repr__(self) -> str:
+        return f"EnergyMap(grid={self.grid!r}, entries=<{len(self)}>, stride={self.stride}, roi={self.roi!r})"
+
+    # -- queries -----------------------------------------------------------
+    def argmax_cell(self) -> tuple[int, int]:
+        """Max energy; ties go to the lowest ix, then the lowest iy (beamform.py:101-104)."""
+        if self._entries is None:
+            if not self._valid.any():
+                raise ValueError("energy map is empty")
+            score = np.where(self._valid, self._values.astype(np.float64), -np.inf)
+            flat = int(np.argmax(score))  # first max in C order = lowest (ix, iy)
+            return divmod(flat, self.grid.dims[1])
+        if not self._entries:
+            raise ValueError("energy map is empty")
+        return max(self._entries, key=lambda k: (self._entries[k], (-k[0], -k[1])))
+
+    def argmax_position(self) -> tuple[float, float]:
+        return self.grid.cell_center(*self.argmax_cell())
+
+    def values_in(self, region: Region) -> np.ndarray:
+        (x0, y0), (x1, y1) = region.min_cell, region.max_cell
+        if self._entries is None and self._split <= 1:
+            v = self._valid[x0 : x1 + 1, y0 : y1 + 1]
+            return self._values[x0 : x1 + 1, y0 : y1 + 1][v].astype(np.float64)
+        return np.array([e for (ix, iy), e in self.entries.items() if x0 <= ix <= x1 and y0 <= iy <= y1])
+
+    def dense(self, fill: float = np.nan) -> np.ndarray:
+        """(nx, ny) array; each stride-D value is held over its D x D block,
+        explicit entries win, uncovered cells get ``fill`` (beamform.py:116-128)."""
+        nx, ny = self.grid.dims
+        if self._entries is not None:
+            vals = np.zeros((nx, ny))
+            valid = np.zeros((nx, ny), dtype=bool)
+            for (ix, iy), v in self._entries.items():
+                vals[ix, iy] = v
+                valid[ix, iy] = True
+        else:
+            vals, valid = self._values.astype(np.float64), self._valid
+        out = np.full((nx, ny), fill, dtype=np.float64)
+        d = self.stride
+        if d > 1:
+            lat_valid = valid[::d, ::d]
+            hold_valid = np.repeat(np.repeat(lat_valid, d, 0), d, 1)[:nx, :ny]
+            hold_vals = np.repeat(np.repeat(vals[::d, ::d], d, 0), d, 1)[:nx, :ny]
+            out[hold_valid] = hold_vals[hold_valid]
+        out[valid] = vals[valid]
+        return out
+
+
+def _check_interpolation(interpolation: str) -> None:
+    if interpolation not in ("linear", "nearest"):
+        raise ValueError(f"unknown interpolation: {interpolation!r}")
+
+
+def _window(ds_samples: int, window) -> tuple[int, int]:
+    if window is None:
+        return 0, int(ds_samples)
+    k0, w = (int(v) for v in window)
+    if k0 < 0 or w < 0:
+        raise ValueError("window must be (k0 >= 0, W >= 0)")
+    return k0, w
+
+
+def aligned_channel(ds, i: int, j: int, r, interpolation: str = "linear") -> np.ndarray:
+    """Channel (i, j) aligned to focal point ``r`` (host helper, beamform.py:136-166).
+
+    Not part of the GPU imaging path: a single-channel utility kept for API
+    parity (the reference uses it in tests and examples).
+    """
+    _check_interpolation(interpolation)
+    n = delay_multistatic(ds.geometry, i, j, r)
+    if interpolation == "nearest":
+        n = float(np.rint(n))
+    y = np.asarray(ds.signals[i, j], dtype=np.float64)
+    i0 = int(np.floor(n))
+    f = n - i0
+    ext = np.concatenate([y, np.zeros(max(i0, 0) + 2)])
+    if i0 < 0:
+        ext = np.concatenate([np.zeros(-i0), y, np.zeros(2)])
+        i0 = 0
+    return (1.0 - f) * ext[i0 : i0 + y.size] + f * ext[i0 + 1 : i0 + 1 + y.size]
+
+
+# ---------------------------------------------------------------------------
+# device launches
+# ---------------------------------------------------------------------------
+class _Status:
+    """One small device block: [argmax key u64 | count i32, flags i32 | ...]."""
+
+    def __init__(self, n_keys: int = 1):
+        self.t = torch.zeros(n_keys + 2, dtype=torch.int64, device=dv.device())
+        self.n_keys = n_keys
+
+    @property
+    def key_ptr(self) -> int:
+        return self.t.data_ptr()
+
+    def count_ptr(self, i: int = 0) -> int:
+        return self.t.data_ptr() + 8 * self.n_keys + 4 * i
+
+    @property
+    def flags_ptr(self) -> int:
+        return self.t.data_ptr() + 8 * self.n_keys + 8
+
+    def read(self) -> tuple[np.ndarray, np.ndarray, int]:
+        h = self.t.cpu().numpy()
+        keys = h[: self.n_keys].view(np.uint64)
+        tail = h[self.n_keys :].view(np.int32)
+        return keys, tail[:2], int(tail[2])
+
+
+def launch_energies(scan: dv.DeviceScan, pts: torch.Tensor, n_pts: int, kind: int, interp: int, k0: int, w: int,
+                    out: torch.Tensor, out_stride: int = 0, out_idx: torch.Tensor | None = None,
+                    d_count: int | None = None, key_ptr: int | None = None, flags_ptr: int | None = None,
+                    mode: int = 0, n_scans: int = 1, sig: torch.Tensor | None = None, scan_stride: int = 0) -> None:
+    sig = scan.sig if sig is None else sig
+    nat.call(
+        "mwb_energies",
+        sig.data_ptr(), n_scans, scan_stride, scan.n_chan, scan.ld, scan.n_samples,
+        scan.chan.data_ptr(), scan.ant.data_ptr(), scan.n_ant, scan.inv_scale,
+        pts.data_ptr(), nat.ptr(out_idx), n_pts, d_count, kind, interp, k0, w,
+        out.data_ptr(), out_stride, key_ptr, flags_ptr, mode, dv.stream_handle(),
+    )
+
+
+def lattice_pass(scan: dv.DeviceScan, grid: ImagingGrid, stride: int, mask_t: torch.Tensor | None,
+                 skip_stride: int, kind: int, interp: int, k0: int, w: int, dense: torch.Tensor,
+                 valid: torch.Tensor, status: _Status, count_slot: int, bounds=None,
+                 d_region: torch.Tensor | None = None, mode: int = 0) -> None:
+    """Enumerate a lattice on the device and evaluate it into ``dense`` (no host sync)."""
+    nx, ny = grid.dims
+    p_max = ((nx + stride - 1) // stride) * ((ny + stride - 1) // stride)
+    dev = dv.device()
+    pts = torch.empty((p_max, 3), dtype=torch.float64, device=dev)
+    oidx = torch.empty(p_max, dtype=torch.int32, device=dev)
+    ws = torch.empty(int(nat.load().mwb_lattice_workspace_bytes(nx, ny, stride)), dtype=torch.uint8, device=dev)
+    x0, y0, x1, y1 = bounds if bounds is not None else (0, 0, nx - 1, ny - 1)
+    res = grid.resolution
+    nat.call(
+        "mwb_enumerate_lattice", grid.origin[0], grid.origin[1], res, nx, ny, x0, y0, x1, y1,
+        nat.ptr(d_region), stride, nat.ptr(mask_t), skip_stride, pts.data_ptr(), oidx.data_ptr(),
+        status.count_ptr(count_slot), valid.data_ptr(), ws.data_ptr(), dv.stream_handle(),
+    )
+    if w == 0:
+        return
+    launch_energies(scan, pts, p_max, kind, interp, k0, w, dense, 0, oidx, status.count_ptr(count_slot),
+                    status.key_ptr, status.flags_ptr, mode)
+
+
+def energies(ds, points, kind, interpolation: str = "linear", *, window=None, mode: str = "smem") -> np.ndarray:
+    """Energies of an arbitrary (P, 2) or (P, 3) list of focal points [m] (fp64 result)."""
+    _check_interpolation(interpolation)
+    pts = np.asarray(points, dtype=np.float64)
+    if pts.ndim != 2 or pts.shape[1] not in (2, 3):
+        raise ValueError("points must be (P, 2) or (P, 3)")
+    if not np.isfinite(pts).all():
+        raise ValueError("focal points must be finite")
+    n = pts.shape[0]
+    if n == 0:
+        return np.zeros(0)
+    p3 = np.zeros((n, 3))
+    p3[:, : pts.shape[1]] = pts
+    scan = dv.scan_for(ds)
+    k0, w = _window(scan.n_samples, window)
+    if w == 0:
+        return np.zeros(n)
+    dev = dv.device()
+    pts_t = torch.from_numpy(p3).to(dev)
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    launch_energies(scan, pts_t, n, _kind_code(kind), nat.INTERP[interpolation], k0, w, out, mode=_MODES[mode])
+    return out.cpu().numpy().astype(np.float64)
+
+
+def das_energy(ds, r, interpolation: str = "linear", *, window=None) -> float:
+    """Multistatic DAS synthesized energy at focal point ``r`` (beamform.py:242-246)."""
+    _check_interpolation(interpolation)
+    pt = np.asarray(r, dtype=np.float64)[:2].reshape(1, 2)
+    return float(energies(ds, pt, BeamformerKind.DAS, interpolation, window=window)[0])
+
+
+def dmas_energy(ds, r, interpolation: str = "linear", *, window=None) -> float:
+    """Multistatic DMAS synthesized energy at focal point ``r`` (beamform.py:249-253)."""
+    _check_interpolation(interpolation)
+    pt = np.asarray(r, dtype=np.float64)[:2].reshape(1, 2)
+    return float(energies(ds, pt, BeamformerKind.DMAS, interpolation, window=window)[0])
+
+
+def point_energy(ds, kind, r) -> float:
+    return das_energy(ds, r) if _kind(kind) is BeamformerKind.DAS else dmas_energy(ds, r)
+
+
+def _eval_mask(grid: ImagingGrid, mask, skip) -> np.ndarray | None:
+    nx, ny = grid.dims
+    if mask is not None:
+        m = np.asarray(mask, dtype=bool)
+        if m.shape != (nx, ny):
+            raise ValueError(f"mask must have the grid's dims {(nx, ny)}, got {m.shape}")
+    else:
+        m = None
+    if skip:
+        m = np.ones((nx, ny), dtype=bool) if m is None else m.copy()
+        cells = np.array([(int(a), int(b)) for a, b in skip], dtype=np.int64).reshape(-1, 2)
+        inside = (cells[:, 0] >= 0) & (cells[:, 0] < nx) & (cells[:, 1] >= 0) & (cells[:, 1] < ny)
+        cells = cells[inside]
+        m[cells[:, 0], cells[:, 1]] = False
+    return m
+
+
+def image(
+    ds,
+    kind,
+    grid: ImagingGrid,
+    region: Region | None = None,
+    stride: int = 1,
+    mask: np.ndarray | None = None,
+    threads: int = 1,
+    skip: set[tuple[int, int]] | None = None,
+    interpolation: str = "linear",
+    *,
+    window=None,
+    mode: str = "smem",
+) -> EnergyMap:
+    """Evaluate the kernel on the stride-D lattice of ``region`` (beamform.py:283-342)."""
+    _check_interpolation(interpolation)
+    kcode = _kind_code(kind)
+    if stride < 1:
+        raise ValueError("stride must be >= 1")
+    if region is None:
+        region = grid.full_region()
+    if not grid.full_region().contains_region(region):
+        raise ValueError("region lies outside the grid")
+    emask = _eval_mask(grid, mask, skip)
+    scan = dv.scan_for(ds)
+    k0, w = _window(scan.n_samples, window)
+    nx, ny = grid.dims
+    dev = dv.device()
+    dense = torch.zeros(nx * ny, dtype=torch.float32, device=dev)
+    valid = torch.zeros(nx * ny, dtype=torch.uint8, device=dev)
+    status = _Status()
+    lattice_pass(scan, grid, stride, dv.upload_mask(emask, (nx, ny)), 0, kcode, nat.INTERP[interpolation], k0, w,
+                 dense, valid, status, 0, bounds=region.bounds(), mode=_MODES[mode])
+    _, counts, flags = status.read()
+    if flags & 1:
+        raise ValueError("energy map contains non-finite values")
+    n = int(counts[0])
+    vals = dense.view(nx, ny).cpu().numpy()
+    vmask = valid.view(nx, ny).cpu().numpy().astype(bool)
+    EVAL_COUNTER.add(n)
+    return EnergyMap._from_dense(grid, vals, vmask, stride)

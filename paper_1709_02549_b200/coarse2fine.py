@@ -1,0 +1,457 @@
+"""Coarse-to-fine segment-selection framework, device resident.
+
+Drop-in for /root/reference/pkg/src/mwbeam/coarse2fine.py:
+
+* ``run_framework`` (coarse2fine.py:301-350): coarse lattice pass -> device
+  ``select_roi`` kernel -> fine pass over the ROI read from device memory ->
+  composite argmax fused into the energy epilogue.  One host synchronisation,
+  at the end, to fetch the map, the trace and the counters.
+* ``select_roi`` (coarse2fine.py:169-256) on any ``EnergyMap``: uploads the map
+  and runs the same device kernel.
+* ``consistency_check`` (coarse2fine.py:353-402), ``breast_mask`` (259-268),
+  ``decision_metric`` / ``class_distances`` (67-109), ``Manual`` /
+  ``Automatic`` / ``auto_decimation_factor`` (24-64), ``FrameworkConfig``,
+  ``IterationRecord``, ``MetricTrace``, ``FrameworkReport``, ``CheckVerdict``
+  with the reference's fields and ``to_dict`` keys.
+
+``elapsed`` timings are CUDA-event device times of the three phases.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _native as nat
+from .beamform import (
+    EVAL_COUNTER,
+    BeamformerKind,
+    EnergyMap,
+    _check_interpolation,
+    _kind_code,
+    _Status,
+    _window,
+    lattice_pass,
+)
+from .geometry import ImagingGrid, Region
+
+
+@dataclass(frozen=True)
+class Manual:
+    """Fixed spatial decimation factor."""
+
+    factor: int
+
+    def __post_init__(self):
+        if self.factor < 1:
+            raise ValueError("manual decimation factor must be >= 1")
+
+
+@dataclass(frozen=True)
+class Automatic:
+    """Decimation derived from the smallest tumour diameter to detect."""
+
+    min_tumor_diameter: float
+
+    def __post_init__(self):
+        if not self.min_tumor_diameter > 0:
+            raise ValueError("min_tumor_diameter must be > 0")
+
+
+DecimationMode = Manual | Automatic
+
+
+def auto_decimation_factor(min_tumor_diameter: float, resolution: float) -> int:
+    """Largest stride that keeps a coarse point inside the inscribed square
+    (side d/sqrt 2) of any tumour of diameter d (coarse2fine.py:49-58)."""
+    if not (min_tumor_diameter > 0 and resolution > 0):
+        raise ValueError("min_tumor_diameter and resolution must be > 0")
+    return max(1, math.floor((min_tumor_diameter / math.sqrt(2.0)) / resolution))
+
+
+def decimation_factor(mode, resolution: float) -> int:
+    if isinstance(mode, Manual) or hasattr(mode, "factor"):
+        return int(mode.factor)
+    return auto_decimation_factor(mode.min_tumor_diameter, resolution)
+
+
+def _mean_var_parts(vals: np.ndarray, sigma_prev_sq: float) -> tuple[float, dict]:
+    if vals.size == 0:
+        raise ValueError("decision_metric needs a nonempty value set")
+    mu = float(vals.mean())
+    var = float(vals.var())
+    if var == 0.0:
+        return mu, {"mu": mu, "var": var, "delta_raw": 0.0, "delta": 0.0, "clamped": False}
+    raw = (var - sigma_prev_sq) / var
+    delta = min(max(raw, 0.0), 1.0)
+    return (1.0 - delta) * mu + delta * var, {
+        "mu": mu,
+        "var": var,
+        "delta_raw": raw,
+        "delta": delta,
+        "clamped": delta != raw,
+    }
+
+
+def decision_metric(energies_current, sigma_prev_sq: float) -> float:
+    """Eq. (5): (1-Δ)μ + Δσ², Δ = clamp((σ² − σ²_prev)/σ², 0, 1); σ² = 0 -> μ."""
+    value, _ = _mean_var_parts(np.asarray(energies_current, dtype=np.float64), sigma_prev_sq)
+    return value
+
+
+def class_distances(class_a, class_b) -> tuple[float, float]:
+    """Eqs. (6)-(7) for scalar energies: within-class W and between-class B."""
+    a = np.asarray(class_a, dtype=np.float64)
+    b = np.asarray(class_b, dtype=np.float64)
+    if a.size == 0 or b.size == 0:
+        raise ValueError("class_distances needs nonempty classes")
+    ma, mb = a.mean(), b.mean()
+    w = float(((a - ma) ** 2).sum() + ((b - mb) ** 2).sum())
+    g = np.concatenate([a, b]).mean()
+    return w, float(a.size * (ma - g) ** 2 + b.size * (mb - g) ** 2)
+
+
+@dataclass(frozen=True)
+class FrameworkConfig:
+    frame_fraction: float = 0.25
+    n_min: int = 4
+    min_tumor_diameter: float = 0.01
+
+    def __post_init__(self):
+        if not 0.0 <= self.frame_fraction < 1.0:
+            raise ValueError("frame_fraction must be in [0, 1)")
+        if self.n_min < 1:
+            raise ValueError("n_min must be >= 1")
+        if not self.min_tumor_diameter > 0:
+            raise ValueError("min_tumor_diameter must be > 0")
+
+
+@dataclass
+class IterationRecord:
+    iteration: int
+    quadrant_counts: list[int]
+    scores: list[float]
+    stats: list[dict | None]
+    selected: int
+    selected_region: Region
+    expanded_region: Region
+    w: float
+    b: float
+    satisfied: bool
+
+    def to_dict(self) -> dict:
+        return {
+            "iteration": self.iteration,
+            "quadrant_counts": self.quadrant_counts,
+            "scores": self.scores,
+            "stats": self.stats,
+            "selected": self.selected,
+            "selected_region": self.selected_region.to_dict(),
+            "expanded_region": self.expanded_region.to_dict(),
+            "W": self.w,
+            "B": self.b,
+            "satisfied": self.satisfied,
+        }
+
+
+@dataclass
+class MetricTrace:
+    records: list[IterationRecord] = field(default_factory=list)
+    termination: str = ""
+    warning: str | None = None
+
+    def to_dict(self) -> dict:
+        return {
+            "records": [r.to_dict() for r in self.records],
+            "termination": self.termination,
+            "warning": self.warning,
+        }
+
+
+def breast_mask(grid: ImagingGrid) -> np.ndarray:
+    """Cells whose centres lie in the circle inscribed in the grid (coarse2fine.py:259-268)."""
+    nx, ny = grid.dims
+    cx, cy = grid.center()
+    radius = min(nx, ny) * grid.resolution / 2.0
+    px = grid.origin[0] + (np.arange(nx) + 0.5) * grid.resolution
+    py = grid.origin[1] + (np.arange(ny) + 0.5) * grid.resolution
+    return (px[:, None] - cx) ** 2 + (py[None, :] - cy) ** 2 <= radius**2
+
+
+_MASKS: dict[tuple, tuple[np.ndarray, torch.Tensor]] = {}
+
+
+def _breast_mask_device(grid: ImagingGrid) -> tuple[np.ndarray, torch.Tensor]:
+    key = (grid.origin, grid.extent, grid.resolution, torch.cuda.current_device())
+    hit = _MASKS.get(key)
+    if hit is None:
+        m = breast_mask(grid)
+        hit = (m, dv.upload_mask(m, grid.dims))
+        if len(_MASKS) > 64:
+            _MASKS.clear()
+        _MASKS[key] = hit
+    return hit
+
+
+@dataclass
+class FrameworkReport:
+    decimation_factor: int
+    iterations: int
+    final_region: Region
+    coarse_points_evaluated: int
+    fine_points_evaluated: int
+    full_equivalent_points: int
+    reduction_ratio: float
+    elapsed: dict[str, float]
+    trace: MetricTrace
+    argmax_cell: tuple[int, int]
+    argmax_position: tuple[float, float]
+
+    def to_dict(self) -> dict:
+        return {
+            "decimation_factor": self.decimation_factor,
+            "iterations": self.iterations,
+            "final_region": self.final_region.to_dict(),
+            "coarse_points_evaluated": self.coarse_points_evaluated,
+            "fine_points_evaluated": self.fine_points_evaluated,
+            "full_equivalent_points": self.full_equivalent_points,
+            "reduction_ratio": self.reduction_ratio,
+            "elapsed": self.elapsed,
+            "trace": self.trace.to_dict(),
+            "argmax_cell": list(self.argmax_cell),
+            "argmax_position": list(self.argmax_position),
+        }
+
+
+# ---------------------------------------------------------------------------
+# trace decoding
+# ---------------------------------------------------------------------------
+def _region(b) -> Region:
+    return Region((int(b[0]), int(b[1])), (int(b[2]), int(b[3])))
+
+
+def decode_trace(raw: bytes) -> tuple[Region, MetricTrace, int]:
+    tr = nat.Trace.from_buffer_copy(raw)
+    code = int(tr.termination)
+    if code == -1:
+        raise ValueError("coarse map has no entries in the breast region")
+    if code == -2:
+        raise RuntimeError(f"select_roi exceeded {nat.MAX_ITERS} iterations")
+    trace = MetricTrace()
+    trace.termination = nat.TERMINATION[code]
+    if code == 1:
+        trace.warning = "energy map has no discriminating signal"
+    for i in range(int(tr.n_records)):
+        r = tr.records[i]
+        stats: list[dict | None] = []
+        for k in range(4):
+            h = int(r.has_stats[k])
+            if h == 0:
+                stats.append(None)
+            elif h == 1:
+                stats.append({"mu": float(r.mu[k]), "var": float(r.var[k])})
+            else:
+                stats.append({
+                    "mu": float(r.mu[k]),
+                    "var": float(r.var[k]),
+                    "delta_raw": float(r.delta_raw[k]),
+                    "delta": float(r.delta[k]),
+                    "clamped": bool(r.clamped[k]),
+                })
+        trace.records.append(IterationRecord(
+            iteration=int(r.iteration),
+            quadrant_counts=[int(c) for c in r.quadrant_counts],
+            scores=[float(s) for s in r.scores],
+            stats=stats,
+            selected=int(r.selected),
+            selected_region=_region(r.selected_region),
+            expanded_region=_region(r.expanded_region),
+            w=float(r.w),
+            b=float(r.b),
+            satisfied=bool(r.satisfied),
+        ))
+    return _region(tr.final_region), trace, code
+
+
+def _launch_select(dense: torch.Tensor, valid: torch.Tensor, grid: ImagingGrid, lattice: int, breast: Region,
+                   cfg: FrameworkConfig, region_out: torch.Tensor, trace_buf: torch.Tensor) -> None:
+    nx, ny = grid.dims
+    x0, y0, x1, y1 = breast.bounds()
+    nat.call("mwb_select_roi", dense.data_ptr(), valid.data_ptr(), nx, ny, lattice, x0, y0, x1, y1,
+             float(cfg.frame_fraction), int(cfg.n_min), region_out.data_ptr(), trace_buf.data_ptr(),
+             dv.stream_handle())
+
+
+def select_roi(coarse: EnergyMap, breast_region: Region, cfg: FrameworkConfig = FrameworkConfig()) -> tuple[Region, MetricTrace]:
+    """Iterative quadrant selection (coarse2fine.py:169-256), run by the device kernel."""
+    grid = coarse.grid
+    nx, ny = grid.dims
+    if not grid.full_region().contains_region(breast_region):
+        raise ValueError("breast region lies outside the grid")
+    if coarse._entries is None:
+        vals, valid = coarse._values.astype(np.float32), coarse._valid
+    else:
+        vals = np.zeros((nx, ny), dtype=np.float32)
+        valid = np.zeros((nx, ny), dtype=bool)
+        for (ix, iy), v in coarse._entries.items():
+            if 0 <= ix < nx and 0 <= iy < ny:
+                vals[ix, iy] = v
+                valid[ix, iy] = True
+    (x0, y0), (x1, y1) = breast_region.min_cell, breast_region.max_cell
+    if not valid[x0 : x1 + 1, y0 : y1 + 1].any():
+        raise ValueError("coarse map has no entries in the breast region")
+    d = max(1, int(coarse.stride))
+    ix, iy = np.nonzero(valid)
+    lattice = d if (d > 1 and not ((ix % d).any() or (iy % d).any())) else 1
+    dev = dv.device()
+    dense_t = torch.from_numpy(np.ascontiguousarray(vals).reshape(-1)).to(dev)
+    valid_t = torch.from_numpy(np.ascontiguousarray(valid).view(np.uint8).reshape(-1)).to(dev)
+    region_t = torch.zeros(4, dtype=torch.int32, device=dev)
+    trace_t = torch.zeros(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
+    _launch_select(dense_t, valid_t, grid, lattice, breast_region, cfg, region_t, trace_t)
+    final, trace, _ = decode_trace(trace_t.cpu().numpy().tobytes())
+    return final, trace
+
+
+class _FrameworkRun:
+    """Device state of one framework run (buffers live until ``finish``)."""
+
+    def __init__(self, ds, kind, grid: ImagingGrid, d: int, cfg: FrameworkConfig, interpolation: str, window, mode: int):
+        self.grid, self.d, self.cfg = grid, d, cfg
+        self.kcode = _kind_code(kind)
+        self.interp = nat.INTERP[interpolation]
+        self.scan = dv.scan_for(ds)
+        self.k0, self.w = _window(self.scan.n_samples, window)
+        self.mode = mode
+        nx, ny = grid.dims
+        self.mask_np, self.mask_t = _breast_mask_device(grid)
+        dev = dv.device()
+        self.dense = torch.zeros(nx * ny, dtype=torch.float32, device=dev)
+        self.valid = torch.zeros(nx * ny, dtype=torch.uint8, device=dev)
+        self.status = _Status()
+        self.region_t = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.trace_t = torch.zeros(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    def enqueue(self) -> None:
+        g, d = self.grid, self.d
+        ev = self.events
+        ev[0].record()
+        lattice_pass(self.scan, g, d, self.mask_t, 0, self.kcode, self.interp, self.k0, self.w,
+                     self.dense, self.valid, self.status, 0, mode=self.mode)
+        ev[1].record()
+        _launch_select(self.dense, self.valid, g, d, g.full_region(), self.cfg, self.region_t, self.trace_t)
+        ev[2].record()
+        lattice_pass(self.scan, g, 1, self.mask_t, d, self.kcode, self.interp, self.k0, self.w,
+                     self.dense, self.valid, self.status, 1, d_region=self.region_t, mode=self.mode)
+        ev[3].record()
+
+    def finish(self) -> tuple[EnergyMap, FrameworkReport]:
+        nx, ny = self.grid.dims
+        keys, counts, flags = self.status.read()  # synchronises the stream
+        raw = self.trace_t.cpu().numpy().tobytes()
+        vals = self.dense.view(nx, ny).cpu().numpy()
+        vmask = self.valid.view(nx, ny).cpu().numpy().astype(bool)
+        if flags & 1:
+            raise ValueError("energy map contains non-finite values")
+        final, trace, _ = decode_trace(raw)
+        n_coarse, n_fine = int(counts[0]), int(counts[1])
+        EVAL_COUNTER.add(n_coarse)
+        EVAL_COUNTER.add(n_fine)
+        composite = EnergyMap._from_dense(self.grid, vals, vmask, stride=self.d, roi=final, split=self.d)
+        ev = self.events
+        t_c = ev[0].elapsed_time(ev[1]) / 1e3
+        t_s = ev[1].elapsed_time(ev[2]) / 1e3
+        t_f = ev[2].elapsed_time(ev[3]) / 1e3
+        full_equivalent = int(self.mask_np.sum())
+        slot = 0xFFFFFFFF - (int(keys[0]) & 0xFFFFFFFF)
+        cell = (slot // ny, slot % ny) if int(keys[0]) != 0 else composite.argmax_cell()
+        report = FrameworkReport(
+            decimation_factor=self.d,
+            iterations=len(trace.records),
+            final_region=final,
+            coarse_points_evaluated=n_coarse,
+            fine_points_evaluated=n_fine,
+            full_equivalent_points=full_equivalent,
+            reduction_ratio=full_equivalent / (n_coarse + n_fine),
+            elapsed={"coarse": t_c, "select": t_s, "fine": t_f, "total": t_c + t_s + t_f},
+            trace=trace,
+            argmax_cell=cell,
+            argmax_position=self.grid.cell_center(*cell),
+        )
+        return composite, report
+
+
+def run_framework(
+    ds,
+    kind,
+    grid: ImagingGrid,
+    mode,
+    cfg: FrameworkConfig = FrameworkConfig(),
+    threads: int = 1,
+    *,
+    interpolation: str = "linear",
+    window=None,
+    kernel_mode: str = "smem",
+) -> tuple[EnergyMap, FrameworkReport]:
+    """Coarse pass, ROI selection, fine pass, composite (coarse2fine.py:301-350)."""
+    _check_interpolation(interpolation)
+    d = decimation_factor(mode, grid.resolution)
+    mask = breast_mask(grid)
+    if not mask[::d, ::d].any():
+        raise ValueError("no coarse focal points inside the breast mask")
+    run = _FrameworkRun(ds, kind, grid, d, cfg, interpolation, window, {"smem": 0, "gather": 1}[kernel_mode])
+    run.enqueue()
+    return run.finish()
+
+
+@dataclass
+class CheckVerdict:
+    """Outcome of running the framework with two decimation factors."""
+
+    confirmed: bool
+    overlap: Region | None
+    region_a: Region
+    region_b: Region
+
+    def to_dict(self) -> dict:
+        return {
+            "confirmed": self.confirmed,
+            "overlap": self.overlap.to_dict() if self.overlap else None,
+            "region_a": self.region_a.to_dict(),
+            "region_b": self.region_b.to_dict(),
+        }
+
+
+def consistency_check(
+    ds,
+    kind,
+    grid: ImagingGrid,
+    d1: int,
+    d2: int,
+    cfg: FrameworkConfig = FrameworkConfig(),
+    threads: int = 1,
+) -> tuple[CheckVerdict, FrameworkReport, FrameworkReport]:
+    """Confirmed when the final regions of two decimation factors overlap
+    (coarse2fine.py:371-402).  Both runs are enqueued back to back on the
+    stream before the single synchronisation."""
+    if d1 == d2:
+        raise ValueError("consistency check needs two different decimation factors")
+    limit = auto_decimation_factor(cfg.min_tumor_diameter, grid.resolution)
+    for dd in (d1, d2):
+        if dd < 1 or dd > limit:
+            raise ValueError(f"decimation factor {dd} outside acceptable range [1, {limit}]")
+    mask = breast_mask(grid)
+    for dd in (d1, d2):
+        if not mask[::dd, ::dd].any():
+            raise ValueError("no coarse focal points inside the breast mask")
+    runs = [_FrameworkRun(ds, kind, grid, dd, cfg, "linear", None, 0) for dd in (d1, d2)]
+    for r in runs:
+        r.enqueue()
+    (_, rep_a), (_, rep_b) = (r.finish() for r in runs)
+    inter = rep_a.final_region.intersection(rep_b.final_region)
+    return CheckVerdict(inter is not None, inter, rep_a.final_region, rep_b.final_region), rep_a, rep_b
