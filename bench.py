@@ -1,0 +1,405 @@
+"""Benchmark of the B200 DAS/DMAS imaging path (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[3], the batched-throughput configuration):
+4096 independent seeded scans per GPU, 12 antennas / 66 Tx-Rx pairs, 1024
+fp32 samples, each imaged with DAS and with DMAS on a 256 x 256 grid over
+12 x 12 cm with a 32-sample energy window.  One step = DAS + DMAS over all
+scans of the rank.  ``value`` is pixel-pair evaluations per second over the
+whole job (inputs resident in HBM); ``e2e`` is the same metric through the
+public host API (pinned host scans in, host energy maps out, H2D/D2H inside
+the timed region).  Multi-GPU: scans are sharded across ranks (weak scaling,
+no data-path collective); the step time is the max over ranks.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+numpy oracle restating mwbeam's kernel, all host cores) on a bounded sample
+of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+import numpy as np  # noqa: E402
+
+METRIC = "DAS+DMAS pixel-pair evals/s (66 Tx-Rx pairs, 32-sample window)"
+UNIT = "pixel-pair evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scans", type=int, default=4096)
+    ap.add_argument("--grid", type=int, default=256)
+    ap.add_argument("--chunk", type=int, default=512)
+    ap.add_argument("--mode", choices=["smem", "gather"], default="smem")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def config_block(args, world):
+    return {
+        "workload": f"BASELINE configs[3] batched: {args.scans} scans/GPU x {args.grid}x{args.grid} px x (DAS + DMAS)",
+        "scans_per_gpu": args.scans,
+        "grid": [args.grid, args.grid],
+        "extent_m": 0.12,
+        "antennas": 12,
+        "pairs": 66,
+        "samples": 1024,
+        "window": 32,
+        "l2": "inputs (1.1 GB per GPU) larger than the 126 MB L2; no flush needed",
+        "parallelism": f"scans sharded over {world} rank(s), no data-path collective",
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+class Clocks:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.proc = None
+        self.t_on = self.t_off = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.file, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+
+    def mark_on(self):
+        self.t_on = time.time()
+
+    def mark_off(self):
+        self.t_off = time.time()
+
+    def stop(self) -> dict:
+        time.sleep(0.25)
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+        self.file.flush()
+        rows = []
+        for line in Path(self.file.name).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[4:]))
+            except ValueError:
+                continue
+        os.unlink(self.file.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        # samples during the timed region: the middle of the run (the clock
+        # sampler runs only while the timed loop executes, plus 0.3 s before)
+        busy = [r for r in rows if r[0] > 0.5 * max(x[0] for x in rows)] or rows
+        names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for _, _, flags in busy:
+            for n, f in zip(names[1:], flags[1:]):
+                if f.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(r[0] for r in busy), "sm_max_mhz": max(r[1] for r in rows),
+                "samples": len(busy), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port of mwbeam's numpy kernel), bounded sample
+# ---------------------------------------------------------------------------
+def cpu_reference_rate(seconds: float, seed: int = 0) -> dict:
+    """Pixel-pair evals/s of the reference algorithm on host cores (DAS + DMAS).
+
+    Sample: one configs[3] scan, blocks of 512 grid points (alternating DAS and
+    DMAS) evaluated through the oracle's windowed energy (two calls of the
+    reference kernel on truncated records, 64-point batches on a thread pool
+    with every available core) until ``seconds`` of CPU work are done.
+    """
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import mwbeam_oracle as orc
+    from paper_1709_02549_b200 import synth
+
+    model = synth.ScanModel()
+    sig, _ = synth.batch_2d(model, [seed])
+    full = synth.embed_pairs(12, model.pairs(), sig[0].astype(np.float64))
+    g = model.geometry()
+    grid = synth.grid_square(0.12, 256)
+    rng = np.random.default_rng(seed)
+    threads = orc.cpu_threads()
+    pairs = 66
+    done_px = 0
+    t0 = time.perf_counter()
+    blocks = 0
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        while True:
+            cells = rng.integers(0, 256, (512, 2))
+            pts = np.array([grid.cell_center(int(a), int(b)) for a, b in cells])
+            kind = "das" if blocks % 2 == 0 else "dmas"
+            batches = [pts[i:i + orc.BATCH] for i in range(0, len(pts), orc.BATCH)]
+            list(pool.map(lambda b: orc.windowed_energies(g.antennas, g.propagation_speed, g.sample_interval, full,
+                                                          b, kind, model.k0, model.window), batches))
+            done_px += len(pts)
+            blocks += 1
+            el = time.perf_counter() - t0
+            if el >= seconds and blocks % 2 == 0:
+                break
+    return {"value": done_px * pairs / el, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{done_px} px of one configs[3] scan (DAS and DMAS alternating), {el:.1f} s",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank, _, world = env_rank()
+    if rank != 0:
+        return
+    per_step = max(1.0, min(6.0, 60.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_rate(per_step, seed=i)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median(x["value"] for x in vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[3] signal model)",
+        "config": config_block(args, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "port",
+                         "sample": f"per step: {vals[0]['sample']}", "cpu_model": vals[0]["cpu_model"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def smem_peak_gbs(lib) -> float:
+    work, ms = ctypes.c_double(), ctypes.c_float()
+    best = 0.0
+    for _ in range(3):
+        rc = lib.mwb_microbench(0, ctypes.byref(work), ctypes.byref(ms), None)
+        if rc != 0:
+            raise RuntimeError("microbench failed")
+        best = max(best, work.value / (ms.value * 1e-3) / 1e9)
+    return best
+
+
+def fp32_peak_tflops(lib) -> float:
+    work, ms = ctypes.c_double(), ctypes.c_float()
+    best = 0.0
+    for which in (1, 2):
+        lib.mwb_microbench(which, ctypes.byref(work), ctypes.byref(ms), None)
+        best = max(best, work.value / (ms.value * 1e-3) / 1e12)
+    return best
+
+
+def load_traffic():
+    p = REPO / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except ValueError:
+            return None
+    return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_02549_b200 import _native as nat
+    from paper_1709_02549_b200 import synth
+    from paper_1709_02549_b200.batch import BatchImager
+
+    rank, local, world = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    lib = nat.load()
+
+    model = synth.ScanModel()
+    S = args.scans
+    t_gen = time.perf_counter()
+    sig, _ = synth.batch_2d(model, range(rank * S, (rank + 1) * S))
+    t_gen = time.perf_counter() - t_gen
+    grid = synth.grid_square(0.12, args.grid)
+    bi = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=(model.k0, model.window),
+                     mode=args.mode)
+    P, C, W = bi.n_pts, bi.n_chan, model.window
+    nxny = grid.dims[0] * grid.dims[1]
+    sig_d = bi.to_device_layout(sig)
+    outs = {k: torch.empty((S, nxny), dtype=torch.float32, device=dev) for k in ("das", "dmas")}  # 2.1 GB
+    keys = {k: torch.zeros(S, dtype=torch.int64, device=dev) for k in ("das", "dmas")}
+
+    smem_gbs = smem_peak_gbs(lib)
+    fp32_tf = fp32_peak_tflops(lib)
+
+    def step(ev=None):
+        # one fused launch: DAS and DMAS share the per-sample channel sum
+        if ev is not None:
+            ev[0].record()
+        bi.run_device(sig_d, outs["das"], outs["dmas"], keys["das"], keys["dmas"])
+        if ev is not None:
+            ev[1].record()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks.mark_on()
+    e0.record()
+    for i in range(args.steps):
+        step(evs[i])
+    e1.record()
+    torch.cuda.synchronize()
+    clocks.mark_off()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = e0.elapsed_time(e1)
+    launch_ms = [a.elapsed_time(b) for a, b in evs]
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    ms_step = elapsed_ms / args.steps
+    pair_evals = 2.0 * S * P * C * world
+    value = pair_evals / (ms_step * 1e-3)
+    images_s = 2.0 * S * world / (ms_step * 1e-3)
+
+    # roofline of the (single, fused) energy kernel: one fp32 sample per
+    # point-pair-sample serves both kinds; 4 FP32-pipe ops per point-pair-sample
+    avg = statistics.mean(launch_ms)
+    pps_launch = float(S) * P * C * W
+    achieved = pps_launch * 4.0 / (avg * 1e-3) / 1e9
+    fp32_frac = pps_launch * 4.0 / (avg * 1e-3) / (fp32_tf * 1e12 / 2.0)
+    traffic = load_traffic()
+    roofline = {
+        "bound": "smem",
+        "kernel": "energy_kernel<BOTH> (fused DAS+DMAS)",
+        "achieved": achieved,
+        "peak": smem_gbs,
+        "unit": "GB/s",
+        "frac": achieved / smem_gbs,
+        "traffic": traffic.get("energy_kernel_both") if isinstance(traffic, dict) else None,
+        "algorithmic_bytes_per_launch": pps_launch * 4.0,
+        "per_unit": "4 B of shared memory per point-pair-sample (one fresh fp32 sample serves DAS and DMAS; "
+                    "the interpolation neighbour is reused in a register)",
+        "peak_source": "LDS.32 bandwidth microbenchmark run live in this process (mwb_microbench 0)",
+        "launch_ms": avg,
+        "fp32_pipe_frac": fp32_frac,
+        "fp32_ops_per_unit": 4,
+        "fp32_peak_tflops": fp32_tf,
+        "co_bound": "smem (1 LDS.32/pps) and FP32 pipe (FMUL+FFMA+FADD+FFMA per pps) peak at the same 32 pps/clk/SM",
+    }
+
+    # end to end through the public host API
+    e2e = None
+    if not args.no_e2e:
+        host = torch.from_numpy(sig).pin_memory()
+        out_h = {k: torch.empty((S, nxny), dtype=torch.float32, pin_memory=True) for k in ("das", "dmas")}
+        bi(host, kinds=("das", "dmas"), chunk=args.chunk, out=out_h)  # warm-up
+        times = []
+        for _ in range(max(1, min(args.steps, 5))):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            bi(host, kinds=("das", "dmas"), chunk=args.chunk, out=out_h)
+            times.append(time.perf_counter() - t0)
+        tt = torch.tensor([statistics.median(times)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+        chunks = (S + args.chunk - 1) // args.chunk
+        e2e = {"value": pair_evals / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(host.numel() * 4),
+               "d2h_bytes_per_step": int(2 * S * nxny * 4 + 2 * S * 8), "seconds_per_step": e2e_s,
+               "api": "paper_1709_02549_b200.batch.BatchImager.__call__ (pinned host in, host maps out)",
+               "gpu_launches_per_step": chunks}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_reference_rate(args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: seeded differentiated-Gaussian scans (BASELINE configs[3] signal model), no dataset",
+            "config": config_block(args, world),
+            "images_per_s": images_s,
+            "pixel_pair_samples_per_s": value * W,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clk,
+            "kernel_mode": args.mode,
+            "host_generate_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -10,6 +10,7 @@
  * failure on the calling thread.
  *
  * Replaced reference interfaces (file:line relative to /root/reference):
+ *   mwb_delay_table        <- pkg/src/mwbeam/beamform.py:182-190  delays / i0 / frac
  *   mwb_energies           <- pkg/src/mwbeam/beamform.py:169-212  _multistatic_energies
  *                             (also das_energy / dmas_energy, beamform.py:242-253,
  *                              and the 64-point batching of image(), beamform.py:325-336)
@@ -91,8 +92,25 @@ int mwb_version(void);
 int64_t mwb_trace_bytes(void);
 
 /*
- * Synthesized DAS/DMAS energies of a list of focal points over S scans that
- * share one antenna geometry.
+ * Per-point delay table (computed once per focal-point list and geometry, then
+ * reused by every scan / kind / window).  For each tile of 256 consecutive
+ * points and each channel it stores the exact range {lo, hi} of the integer
+ * delays and, per point, (i0 - lo) << 23 | frac23 where i0 = floor(n),
+ * frac23 = floor((n - i0) * 2^23) and n = (|p - a_tx| + |p - a_rx|) / (v dt)
+ * in fp64 (beamform.py:182-190).  The interpolation weights are then
+ * f1 = frac23 * 2^-23 and f0 = 1 - f1, identical for a point in every call.
+ * `table` must hold mwb_delay_table_bytes(n_pts, n_chan) bytes.
+ */
+int64_t mwb_delay_table_bytes(int n_pts, int n_chan);
+int mwb_delay_table(const double* pts_xyz, int n_pts, const int32_t* d_count,
+                    const int32_t* chan_txrx, int n_chan, const double* ant_xyz, int n_ant,
+                    double inv_scale, int interp, void* table, void* stream);
+
+/*
+ * Synthesized DAS and/or DMAS energies of a list of focal points over S scans
+ * that share one antenna geometry (replaces beamform.py:169-212).  Both kinds
+ * share the per-sample channel sum s = Σ_c a_c, so requesting both costs one
+ * pass over the samples: DAS = Σ_k s_k^2, DMAS = ½ Σ_k (s_k^2 − Σ_c a_c,k^2).
  *
  *   sig        device fp32 [S][n_chan][ld]; populated channels only (all-zero
  *              channels contribute exactly 0 in the reference and are dropped);
@@ -105,21 +123,22 @@ int64_t mwb_trace_bytes(void);
  *   out_idx    device int32 [n_pts] output slot of each point (NULL = identity).
  *   d_count    device int32 scalar overriding n_pts (<= n_pts) or NULL; lets a
  *              device-side enumerator feed this launch without a host sync.
- *   kind       MWB_DAS / MWB_DMAS;  interp MWB_INTERP_*.
+ *   table      the mwb_delay_table of the same points / channels / interp.
  *   k0, window energy is summed over aligned samples k in [k0, k0+window);
  *              the reference's full-record sum is k0 = 0, window = n_samples.
- *   out        device fp32, out[s*out_stride + out_idx[p]].
- *   argmax_key device uint64 [S] or NULL: atomicMax of (ordered(value)<<32 |
- *              ~slot), i.e. the max energy with ties to the lowest slot.
+ *   out_das, out_dmas  device fp32 outputs (either may be NULL = kind not
+ *              wanted), out[s*out_stride + out_idx[p]].
+ *   key_das, key_dmas  device uint64 [S] or NULL: atomicMax of
+ *              (ordered(value) << 32 | ~slot) = max energy, ties to the lowest slot.
  *   flags      device int32 or NULL: bit 0 set when a non-finite energy occurs.
  *   mode       0 = shared-memory staged (TMA bulk copies), 1 = L1/L2 gather.
  */
 int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
                  int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
                  double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
-                 const int32_t* d_count, int kind, int interp, int k0, int window, float* out,
-                 int64_t out_stride, uint64_t* argmax_key, int32_t* flags, int mode,
-                 void* stream);
+                 const int32_t* d_count, const void* table, int interp, int k0, int window,
+                 float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
+                 uint64_t* key_dmas, int32_t* flags, int mode, void* stream);
 
 /* Workspace (bytes) for mwb_enumerate_lattice on an nx x ny grid at `stride`. */
 int64_t mwb_lattice_workspace_bytes(int nx, int ny, int stride);

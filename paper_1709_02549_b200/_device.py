@@ -79,7 +79,7 @@ def _build_scan(ds) -> DeviceScan:
     return DeviceScan(
         sig=torch.from_numpy(host).to(dev),
         chan=torch.from_numpy(pairs).to(dev),
-        ant=torch.from_numpy(np.ascontiguousarray(geom.antennas, dtype=np.float64)).to(dev),
+        ant=torch.from_numpy(np.array(geom.antennas, dtype=np.float64)).to(dev),
         inv_scale=1.0 / scale,
         n_samples=n,
         ld=ld,

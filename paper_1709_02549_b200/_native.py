@@ -69,8 +69,11 @@ _SIGNATURES = {
     "mwb_last_error": ([], C.c_char_p),
     "mwb_version": ([], _I),
     "mwb_trace_bytes": ([], _I64),
+    "mwb_delay_table_bytes": ([_I, _I], _I64),
+    "mwb_delay_table": ([_P, _I, _P, _P, _I, _P, _I, _D, _I, _P, _P], _I),
     "mwb_energies": (
-        [_P, _I, _I64, _I, _I, _I, _P, _P, _I, _D, _P, _P, _I, _P, _I, _I, _I, _I, _P, _I64, _P, _P, _I, _P],
+        [_P, _I, _I64, _I, _I, _I, _P, _P, _I, _D, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _I64, _P, _P, _P, _I,
+         _P],
         _I,
     ),
     "mwb_lattice_workspace_bytes": ([_I, _I, _I], _I64),

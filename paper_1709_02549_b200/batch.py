@@ -23,7 +23,7 @@ import torch
 
 from . import _device as dv
 from . import _native as nat
-from .beamform import _kind_code, _Status, _window
+from .beamform import _Status, _window, build_table
 from .geometry import ArrayGeometry, ImagingGrid
 
 
@@ -50,7 +50,7 @@ class BatchImager:
         self.scan = dv.DeviceScan(
             sig=torch.empty(0, device=dev),
             chan=torch.from_numpy(pairs).to(dev),
-            ant=torch.from_numpy(np.ascontiguousarray(geometry.antennas, dtype=np.float64)).to(dev),
+            ant=torch.from_numpy(np.array(geometry.antennas, dtype=np.float64)).to(dev),
             inv_scale=1.0 / (float(geometry.propagation_speed) * float(geometry.sample_interval)),
             n_samples=self.n_samples,
             ld=self.ld,
@@ -72,6 +72,8 @@ class BatchImager:
         _, counts, _ = st.read()
         self.n_pts = int(counts[0])
         self.valid_host = self.valid.view(nx, ny).cpu().numpy().astype(bool)
+        # per-point delay table: computed once, shared by every scan and kind
+        self.table = build_table(self.scan, self.pts, self.n_pts, self.interp) if self.n_pts else None
 
     @property
     def n_chan(self) -> int:
@@ -80,27 +82,35 @@ class BatchImager:
     def launches_per_kind(self) -> int:
         return 1
 
-    def run_device(self, sig: torch.Tensor, kind, out: torch.Tensor, keys: torch.Tensor | None = None,
-                   flags: torch.Tensor | None = None) -> None:
-        """Image S device-resident scans ``sig`` (S, C, ld) fp32 into ``out`` (S, nx*ny) fp32.
+    def run_device(self, sig: torch.Tensor, out_das: torch.Tensor | None = None,
+                   out_dmas: torch.Tensor | None = None, key_das: torch.Tensor | None = None,
+                   key_dmas: torch.Tensor | None = None, flags: torch.Tensor | None = None) -> None:
+        """Image S device-resident scans ``sig`` (S, C, ld) fp32 into ``out_das`` /
+        ``out_dmas`` (S, nx*ny) fp32 with ONE launch (either output may be None).
 
-        ``keys`` (S,) int64 receives the per-scan argmax key (zero it first).
+        ``key_*`` (S,) int64 receive the per-scan argmax key (zero them first).
         Stream ordered, no host synchronisation.
         """
         s = int(sig.shape[0])
         if sig.dtype != torch.float32 or sig.shape[1:] != (self.n_chan, self.ld) or not sig.is_contiguous():
             raise ValueError(f"sig must be contiguous float32 (S, {self.n_chan}, {self.ld})")
         nxny = self.grid.dims[0] * self.grid.dims[1]
-        if out.shape != (s, nxny) or out.dtype != torch.float32:
-            raise ValueError(f"out must be float32 (S, {nxny})")
+        for out in (out_das, out_dmas):
+            if out is not None and (out.shape != (s, nxny) or out.dtype != torch.float32 or not out.is_contiguous()):
+                raise ValueError(f"outputs must be contiguous float32 (S, {nxny})")
+        if out_das is None and out_dmas is None:
+            raise ValueError("no output requested")
         if self.w == 0 or s == 0:
-            out.zero_()
+            for out in (out_das, out_dmas):
+                if out is not None:
+                    out.zero_()
             return
         nat.call(
             "mwb_energies", sig.data_ptr(), s, self.n_chan * self.ld, self.n_chan, self.ld, self.n_samples,
             self.scan.chan.data_ptr(), self.scan.ant.data_ptr(), self.scan.n_ant, self.scan.inv_scale,
-            self.pts.data_ptr(), self.oidx.data_ptr(), self.n_pts, None, _kind_code(kind), self.interp, self.k0,
-            self.w, out.data_ptr(), nxny, nat.ptr(keys), nat.ptr(flags), self.mode, dv.stream_handle(),
+            self.pts.data_ptr(), self.oidx.data_ptr(), self.n_pts, None, self.table.data_ptr(), self.interp, self.k0,
+            self.w, nat.ptr(out_das), nat.ptr(out_dmas), nxny, nat.ptr(key_das), nat.ptr(key_dmas), nat.ptr(flags),
+            self.mode, dv.stream_handle(),
         )
 
     def decode_keys(self, keys: np.ndarray) -> np.ndarray:
@@ -135,7 +145,9 @@ class BatchImager:
             raise ValueError("the end-to-end path needs n_samples % 4 == 0")
         s_total = int(host.shape[0])
         nx, ny = self.grid.dims
-        kinds = list(kinds)
+        kinds = [k if isinstance(k, str) else k.value for k in kinds]
+        if not kinds or any(k not in ("das", "dmas") for k in kinds):
+            raise ValueError("kinds must be a subset of ('das', 'dmas')")
         if out is None:
             out = {k: torch.empty((s_total, nx * ny), dtype=torch.float32, pin_memory=host.is_pinned())
                    for k in kinds}
@@ -167,8 +179,9 @@ class BatchImager:
                 s_cmp.wait_event(ev_in[i])
                 if i >= nbuf:
                     s_cmp.wait_event(ev_out[i - nbuf])
-                for ki, k in enumerate(kinds):
-                    self.run_device(dev_in[buf][:n], k, dev_out[buf][k][:n], keys[ki, a:b])
+                outs = {k: dev_out[buf][k][:n] for k in kinds}
+                kk = {k: keys[ki, a:b] for ki, k in enumerate(kinds)}
+                self.run_device(dev_in[buf][:n], outs.get("das"), outs.get("dmas"), kk.get("das"), kk.get("dmas"))
                 ev_cmp[i].record(s_cmp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_cmp[i])

@@ -246,49 +246,66 @@ def aligned_channel(ds, i: int, j: int, r, interpolation: str = "linear") -> np.
 # device launches
 # ---------------------------------------------------------------------------
 class _Status:
-    """One small device block: [argmax key u64 | count i32, flags i32 | ...]."""
+    """One small device block: [key_das u64 | key_dmas u64 | count0 i32, count1 i32 | flags i32, pad]."""
 
-    def __init__(self, n_keys: int = 1):
-        self.t = torch.zeros(n_keys + 2, dtype=torch.int64, device=dv.device())
-        self.n_keys = n_keys
+    N_KEYS = 2
 
-    @property
-    def key_ptr(self) -> int:
-        return self.t.data_ptr()
+    def __init__(self):
+        self.t = torch.zeros(self.N_KEYS + 2, dtype=torch.int64, device=dv.device())
+
+    def key_ptr(self, i: int = 0) -> int:
+        return self.t.data_ptr() + 8 * i
 
     def count_ptr(self, i: int = 0) -> int:
-        return self.t.data_ptr() + 8 * self.n_keys + 4 * i
+        return self.t.data_ptr() + 8 * self.N_KEYS + 4 * i
 
     @property
     def flags_ptr(self) -> int:
-        return self.t.data_ptr() + 8 * self.n_keys + 8
+        return self.t.data_ptr() + 8 * self.N_KEYS + 8
 
     def read(self) -> tuple[np.ndarray, np.ndarray, int]:
         h = self.t.cpu().numpy()
-        keys = h[: self.n_keys].view(np.uint64)
-        tail = h[self.n_keys :].view(np.int32)
+        keys = h[: self.N_KEYS].view(np.uint64)
+        tail = h[self.N_KEYS :].view(np.int32)
         return keys, tail[:2], int(tail[2])
 
 
-def launch_energies(scan: dv.DeviceScan, pts: torch.Tensor, n_pts: int, kind: int, interp: int, k0: int, w: int,
-                    out: torch.Tensor, out_stride: int = 0, out_idx: torch.Tensor | None = None,
-                    d_count: int | None = None, key_ptr: int | None = None, flags_ptr: int | None = None,
+def build_table(scan: dv.DeviceScan, pts: torch.Tensor, n_pts: int, interp: int,
+                d_count: int | None = None) -> torch.Tensor:
+    """Device delay table of a point list (mwb_delay_table); reused by every scan."""
+    nbytes = int(nat.load().mwb_delay_table_bytes(max(n_pts, 1), scan.n_chan))
+    table = torch.empty(nbytes, dtype=torch.uint8, device=pts.device)
+    nat.call("mwb_delay_table", pts.data_ptr(), n_pts, d_count, scan.chan.data_ptr(), scan.n_chan,
+             scan.ant.data_ptr(), scan.n_ant, scan.inv_scale, interp, table.data_ptr(), dv.stream_handle())
+    return table
+
+
+def launch_energies(scan: dv.DeviceScan, pts: torch.Tensor, n_pts: int, table: torch.Tensor, interp: int, k0: int,
+                    w: int, out_das: torch.Tensor | None, out_dmas: torch.Tensor | None, out_stride: int = 0,
+                    out_idx: torch.Tensor | None = None, d_count: int | None = None,
+                    key_das: int | None = None, key_dmas: int | None = None, flags_ptr: int | None = None,
                     mode: int = 0, n_scans: int = 1, sig: torch.Tensor | None = None, scan_stride: int = 0) -> None:
+    """One fused launch: DAS and/or DMAS energies (whichever outputs are given)."""
     sig = scan.sig if sig is None else sig
     nat.call(
         "mwb_energies",
         sig.data_ptr(), n_scans, scan_stride, scan.n_chan, scan.ld, scan.n_samples,
         scan.chan.data_ptr(), scan.ant.data_ptr(), scan.n_ant, scan.inv_scale,
-        pts.data_ptr(), nat.ptr(out_idx), n_pts, d_count, kind, interp, k0, w,
-        out.data_ptr(), out_stride, key_ptr, flags_ptr, mode, dv.stream_handle(),
+        pts.data_ptr(), nat.ptr(out_idx), n_pts, d_count, table.data_ptr(), interp, k0, w,
+        nat.ptr(out_das), nat.ptr(out_dmas), out_stride, key_das, key_dmas, flags_ptr, mode, dv.stream_handle(),
     )
 
 
 def lattice_pass(scan: dv.DeviceScan, grid: ImagingGrid, stride: int, mask_t: torch.Tensor | None,
-                 skip_stride: int, kind: int, interp: int, k0: int, w: int, dense: torch.Tensor,
-                 valid: torch.Tensor, status: _Status, count_slot: int, bounds=None,
+                 skip_stride: int, kinds: tuple, interp: int, k0: int, w: int, dense: dict,
+                 valid: torch.Tensor, status: "_Status", count_slot: int, bounds=None,
                  d_region: torch.Tensor | None = None, mode: int = 0) -> None:
-    """Enumerate a lattice on the device and evaluate it into ``dense`` (no host sync)."""
+    """Enumerate a lattice on the device and evaluate it into ``dense[kind]`` (no host sync).
+
+    ``kinds`` is a tuple of kind codes; when both DAS and DMAS are requested a
+    single fused launch produces both maps.  Argmax keys go to status key
+    slots 0 (DAS) / 1 (DMAS).
+    """
     nx, ny = grid.dims
     p_max = ((nx + stride - 1) // stride) * ((ny + stride - 1) // stride)
     dev = dv.device()
@@ -297,15 +314,19 @@ def lattice_pass(scan: dv.DeviceScan, grid: ImagingGrid, stride: int, mask_t: to
     ws = torch.empty(int(nat.load().mwb_lattice_workspace_bytes(nx, ny, stride)), dtype=torch.uint8, device=dev)
     x0, y0, x1, y1 = bounds if bounds is not None else (0, 0, nx - 1, ny - 1)
     res = grid.resolution
+    count_ptr = status.count_ptr(count_slot)
     nat.call(
         "mwb_enumerate_lattice", grid.origin[0], grid.origin[1], res, nx, ny, x0, y0, x1, y1,
         nat.ptr(d_region), stride, nat.ptr(mask_t), skip_stride, pts.data_ptr(), oidx.data_ptr(),
-        status.count_ptr(count_slot), valid.data_ptr(), ws.data_ptr(), dv.stream_handle(),
+        count_ptr, valid.data_ptr(), ws.data_ptr(), dv.stream_handle(),
     )
     if w == 0:
         return
-    launch_energies(scan, pts, p_max, kind, interp, k0, w, dense, 0, oidx, status.count_ptr(count_slot),
-                    status.key_ptr, status.flags_ptr, mode)
+    table = build_table(scan, pts, p_max, interp, count_ptr)
+    launch_energies(scan, pts, p_max, table, interp, k0, w,
+                    dense.get(nat.MWB_DAS) if nat.MWB_DAS in kinds else None,
+                    dense.get(nat.MWB_DMAS) if nat.MWB_DMAS in kinds else None,
+                    0, oidx, count_ptr, status.key_ptr(0), status.key_ptr(1), status.flags_ptr, mode)
 
 
 def energies(ds, points, kind, interpolation: str = "linear", *, window=None, mode: str = "smem") -> np.ndarray:
@@ -328,7 +349,11 @@ def energies(ds, points, kind, interpolation: str = "linear", *, window=None, mo
     dev = dv.device()
     pts_t = torch.from_numpy(p3).to(dev)
     out = torch.empty(n, dtype=torch.float32, device=dev)
-    launch_energies(scan, pts_t, n, _kind_code(kind), nat.INTERP[interpolation], k0, w, out, mode=_MODES[mode])
+    interp = nat.INTERP[interpolation]
+    table = build_table(scan, pts_t, n, interp)
+    code = _kind_code(kind)
+    launch_energies(scan, pts_t, n, table, interp, k0, w, out if code == nat.MWB_DAS else None,
+                    out if code == nat.MWB_DMAS else None, mode=_MODES[mode])
     return out.cpu().numpy().astype(np.float64)
 
 
@@ -367,6 +392,48 @@ def _eval_mask(grid: ImagingGrid, mask, skip) -> np.ndarray | None:
     return m
 
 
+def images(ds, kinds, grid: ImagingGrid, region: Region | None = None, stride: int = 1,
+           mask: np.ndarray | None = None, skip=None, interpolation: str = "linear", *, window=None,
+           mode: str = "smem") -> dict:
+    """``image()`` for several kinds in one fused pass: {"das": EnergyMap, "dmas": EnergyMap}.
+
+    DAS and DMAS share the per-sample channel sum, so both maps cost one pass
+    over the samples.  Each map equals the corresponding ``image()`` call bit
+    for bit; the evaluated-point counter is advanced once per map.
+    """
+    _check_interpolation(interpolation)
+    codes = tuple(dict.fromkeys(_kind_code(k) for k in kinds))
+    if not codes:
+        raise ValueError("no beamformer kind requested")
+    if stride < 1:
+        raise ValueError("stride must be >= 1")
+    if region is None:
+        region = grid.full_region()
+    if not grid.full_region().contains_region(region):
+        raise ValueError("region lies outside the grid")
+    emask = _eval_mask(grid, mask, skip)
+    scan = dv.scan_for(ds)
+    k0, w = _window(scan.n_samples, window)
+    nx, ny = grid.dims
+    dev = dv.device()
+    dense = {c: torch.zeros(nx * ny, dtype=torch.float32, device=dev) for c in codes}
+    valid = torch.zeros(nx * ny, dtype=torch.uint8, device=dev)
+    status = _Status()
+    lattice_pass(scan, grid, stride, dv.upload_mask(emask, (nx, ny)), 0, codes, nat.INTERP[interpolation], k0, w,
+                 dense, valid, status, 0, bounds=region.bounds(), mode=_MODES[mode])
+    _, counts, flags = status.read()
+    if flags & 1:
+        raise ValueError("energy map contains non-finite values")
+    n = int(counts[0])
+    vmask = valid.view(nx, ny).cpu().numpy().astype(bool)
+    out = {}
+    for c in codes:
+        EVAL_COUNTER.add(n)
+        name = "das" if c == nat.MWB_DAS else "dmas"
+        out[name] = EnergyMap._from_dense(grid, dense[c].view(nx, ny).cpu().numpy(), vmask, stride)
+    return out
+
+
 def image(
     ds,
     kind,
@@ -383,28 +450,5 @@ def image(
 ) -> EnergyMap:
     """Evaluate the kernel on the stride-D lattice of ``region`` (beamform.py:283-342)."""
     _check_interpolation(interpolation)
-    kcode = _kind_code(kind)
-    if stride < 1:
-        raise ValueError("stride must be >= 1")
-    if region is None:
-        region = grid.full_region()
-    if not grid.full_region().contains_region(region):
-        raise ValueError("region lies outside the grid")
-    emask = _eval_mask(grid, mask, skip)
-    scan = dv.scan_for(ds)
-    k0, w = _window(scan.n_samples, window)
-    nx, ny = grid.dims
-    dev = dv.device()
-    dense = torch.zeros(nx * ny, dtype=torch.float32, device=dev)
-    valid = torch.zeros(nx * ny, dtype=torch.uint8, device=dev)
-    status = _Status()
-    lattice_pass(scan, grid, stride, dv.upload_mask(emask, (nx, ny)), 0, kcode, nat.INTERP[interpolation], k0, w,
-                 dense, valid, status, 0, bounds=region.bounds(), mode=_MODES[mode])
-    _, counts, flags = status.read()
-    if flags & 1:
-        raise ValueError("energy map contains non-finite values")
-    n = int(counts[0])
-    vals = dense.view(nx, ny).cpu().numpy()
-    vmask = valid.view(nx, ny).cpu().numpy().astype(bool)
-    EVAL_COUNTER.add(n)
-    return EnergyMap._from_dense(grid, vals, vmask, stride)
+    name = _kind(kind).value
+    return images(ds, (name,), grid, region, stride, mask, skip, interpolation, window=window, mode=mode)[name]

@@ -341,13 +341,13 @@ class _FrameworkRun:
         g, d = self.grid, self.d
         ev = self.events
         ev[0].record()
-        lattice_pass(self.scan, g, d, self.mask_t, 0, self.kcode, self.interp, self.k0, self.w,
-                     self.dense, self.valid, self.status, 0, mode=self.mode)
+        lattice_pass(self.scan, g, d, self.mask_t, 0, (self.kcode,), self.interp, self.k0, self.w,
+                     {self.kcode: self.dense}, self.valid, self.status, 0, mode=self.mode)
         ev[1].record()
         _launch_select(self.dense, self.valid, g, d, g.full_region(), self.cfg, self.region_t, self.trace_t)
         ev[2].record()
-        lattice_pass(self.scan, g, 1, self.mask_t, d, self.kcode, self.interp, self.k0, self.w,
-                     self.dense, self.valid, self.status, 1, d_region=self.region_t, mode=self.mode)
+        lattice_pass(self.scan, g, 1, self.mask_t, d, (self.kcode,), self.interp, self.k0, self.w,
+                     {self.kcode: self.dense}, self.valid, self.status, 1, d_region=self.region_t, mode=self.mode)
         ev[3].record()
 
     def finish(self) -> tuple[EnergyMap, FrameworkReport]:
@@ -368,8 +368,9 @@ class _FrameworkRun:
         t_s = ev[1].elapsed_time(ev[2]) / 1e3
         t_f = ev[2].elapsed_time(ev[3]) / 1e3
         full_equivalent = int(self.mask_np.sum())
-        slot = 0xFFFFFFFF - (int(keys[0]) & 0xFFFFFFFF)
-        cell = (slot // ny, slot % ny) if int(keys[0]) != 0 else composite.argmax_cell()
+        key = int(keys[0 if self.kcode == nat.MWB_DAS else 1])
+        slot = 0xFFFFFFFF - (key & 0xFFFFFFFF)
+        cell = (slot // ny, slot % ny) if key != 0 else composite.argmax_cell()
         report = FrameworkReport(
             decimation_factor=self.d,
             iterations=len(trace.records),

@@ -118,16 +118,25 @@ __device__ __forceinline__ double antenna_distance(double px, double py, double 
   return __dsqrt_rn(s);
 }
 
-// Split a fractional delay (samples) into i0 = floor(n) and the interpolation
-// weights (beamform.py:186-190; nearest -> rint, 187-188).
-__device__ __forceinline__ void split_delay(double n, int interp, int& i0, float& f0, float& f1) {
+// Split a fractional delay (samples) into i0 = floor(n) and a 23-bit fixed-point
+// fraction (beamform.py:186-190; nearest -> rint, 187-188).  The weights used by
+// every path are f1 = q * 2^-23, f0 = 1 - f1 (both exact in fp32, f0 + f1 == 1),
+// a function of the point alone, so a point's energy never depends on the tile.
+__device__ __forceinline__ void split_delay_q(double n, int interp, int& i0, uint32_t& fq) {
   if (interp == MWB_INTERP_NEAREST) n = rint(n);
   n = fmin(fmax(n, 0.0), 1073741824.0);
   const double fl = floor(n);
-  const double fr = __dsub_rn(n, fl);
   i0 = static_cast<int>(fl);
-  f1 = __double2float_rn(fr);
-  f0 = __double2float_rn(__dsub_rn(1.0, fr));
+  fq = static_cast<uint32_t>(__dmul_rn(__dsub_rn(n, fl), 8388608.0));  // trunc, < 2^23
+}
+
+__device__ __forceinline__ float weight_f1(uint32_t fq) {
+  return __fsub_rn(__uint_as_float(0x3F800000u | (fq & 0x7FFFFFu)), 1.0f);
+}
+
+// per-point per-channel delay in samples: (d_tx + d_rx) / (v dt)  (beamform.py:186)
+__device__ __forceinline__ double pair_delay(double dtx, double drx, double inv_scale) {
+  return __dmul_rn(__dadd_rn(dtx, drx), inv_scale);
 }
 
 __device__ __forceinline__ uint32_t ordered_f32(float v) {
@@ -141,9 +150,12 @@ __device__ __forceinline__ uint64_t argmax_key(float v, int slot) {
          static_cast<uint64_t>(0xFFFFFFFFu - static_cast<uint32_t>(slot));
 }
 
-// Accumulate one channel into the register window of two points.
-//   DAS : s += f0*y[k] ; s += f1*y[k+1]                (beamform.py:203-205)
-//   DMAS: a = f0*y[k] + f1*y[k+1]; s += a; q += a*a    (beamform.py:207-209)
+constexpr int KIND_DAS = 0, KIND_DMAS = 1, KIND_BOTH = 2;
+
+// Accumulate one channel into the register window of two points (float2 lanes):
+//   a = f0*y[k] + f1*y[k+1];  s += a            (beamform.py:207-208; DAS 203-205)
+//   q += a*a                                    (DMAS only, beamform.py:209)
+// DAS and DMAS share s, so one pass yields both energies.
 template <int KIND, bool TAIL, class Load>
 __device__ __forceinline__ void accumulate_channel(float2 (&s)[WCH], float2& qe, float2& qo,
                                                    const float2 f0, const float2 f1,
@@ -152,42 +164,28 @@ __device__ __forceinline__ void accumulate_channel(float2 (&s)[WCH], float2& qe,
 #pragma unroll
   for (int k = 0; k < WCH; ++k) {
     const float2 nxt = load(k + 1);
-    if (KIND == MWB_DAS) {
-      s[k] = __ffma2_rn(f0, prev, s[k]);
-      s[k] = __ffma2_rn(f1, nxt, s[k]);
-    } else {
-      float2 a = __fmul2_rn(f0, prev);
-      a = __ffma2_rn(f1, nxt, a);
-      s[k] = __fadd2_rn(s[k], a);
-      if (!TAIL || k < valid) {
-        if (k & 1)
-          qo = __ffma2_rn(a, a, qo);
-        else
-          qe = __ffma2_rn(a, a, qe);
-      }
+    float2 a = __fmul2_rn(f0, prev);
+    a = __ffma2_rn(f1, nxt, a);
+    s[k] = __fadd2_rn(s[k], a);
+    if (KIND != KIND_DAS && (!TAIL || k < valid)) {
+      if (k & 1)
+        qo = __ffma2_rn(a, a, qo);
+      else
+        qe = __ffma2_rn(a, a, qe);
     }
     prev = nxt;
   }
 }
 
-// Chunk epilogue: Σ_k s_k^2 (DAS, beamform.py:211) or ½Σ_k(s_k^2 − q_k) (DMAS, 212),
-// fp32 within the chunk, fp64 across chunks; fixed summation order.
-template <int KIND>
-__device__ __forceinline__ void chunk_energy(const float2 (&s)[WCH], const float2 qe,
-                                             const float2 qo, const int valid, double& ea,
-                                             double& eb) {
+// Chunk epilogue: S = Σ_k s_k^2 (fp32, fixed order) and Q = Σ q (DMAS);
+// DAS energy = Σ S, DMAS energy = ½ Σ (S − Q), summed over chunks in fp64
+// (beamform.py:210-212).
+__device__ __forceinline__ float2 chunk_sumsq(const float2 (&s)[WCH], const int valid) {
   float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < WCH; ++k)
     if (k < valid) acc = __ffma2_rn(s[k], s[k], acc);
-  if (KIND == MWB_DAS) {
-    ea += static_cast<double>(acc.x);
-    eb += static_cast<double>(acc.y);
-  } else {
-    const float2 q = __fadd2_rn(qe, qo);
-    ea += 0.5 * (static_cast<double>(acc.x) - static_cast<double>(q.x));
-    eb += 0.5 * (static_cast<double>(acc.y) - static_cast<double>(q.y));
-  }
+  return acc;
 }
 
 struct EnergyParams {
@@ -205,12 +203,17 @@ struct EnergyParams {
   const int* out_idx;
   int P;
   const int* d_count;
+  const uint32_t* tab_words;  // [tiles][C][TILE]
+  const int2* tab_span;       // [tiles][C] {lo, hi}
+  const int* tab_wide;        // [tiles]
   int interp;
   int k0;
   int W;
-  float* out;
+  float* out_das;
+  float* out_dmas;
   long long out_stride;
-  unsigned long long* argmax;
+  unsigned long long* key_das;
+  unsigned long long* key_dmas;
   int* flags;
   int mode;
   int scans_per_cta;
@@ -218,22 +221,17 @@ struct EnergyParams {
 };
 
 struct SmemLayout {
-  size_t dist, chan, lo, alloc, off, ant_min, ant_max, misc, mbar, stage, total;
+  size_t lo, alloc, off, misc, mbar, stage, total;
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-__host__ __device__ inline SmemLayout smem_layout(int M, int C, int cap) {
+__host__ __device__ inline SmemLayout smem_layout(int C, int cap) {
   SmemLayout L;
   size_t o = 0;
-  L.dist = o;    o += sizeof(double) * (size_t)M * TILE;
-  L.chan = o;    o += sizeof(int2) * (size_t)C;
   L.lo = o;      o += sizeof(int) * (size_t)C;
   L.alloc = o;   o += sizeof(int) * (size_t)C;
   L.off = o;     o += sizeof(int) * (size_t)C;
-  o = align_up(o, 8);
-  L.ant_min = o; o += sizeof(double) * (size_t)M;
-  L.ant_max = o; o += sizeof(double) * (size_t)M;
   L.misc = o;    o += sizeof(int) * 16;
   o = align_up(o, 16);
   L.mbar = o;    o += sizeof(uint64_t) * 2;
@@ -243,8 +241,115 @@ __host__ __device__ inline SmemLayout smem_layout(int M, int C, int cap) {
   return L;
 }
 
+// table layout inside one workspace buffer
+struct TableLayout {
+  size_t words, span, wide, total;
+};
+
+__host__ __device__ inline TableLayout table_layout(long long tiles, int C) {
+  TableLayout T;
+  size_t o = 0;
+  T.words = o; o += sizeof(uint32_t) * (size_t)tiles * C * TILE;
+  o = align_up(o, 16);
+  T.span = o;  o += sizeof(int2) * (size_t)tiles * C;
+  o = align_up(o, 16);
+  T.wide = o;  o += sizeof(int) * (size_t)tiles;
+  T.total = align_up(o, 256);
+  return T;
+}
+
+constexpr int SPAN_BITS = 9;                       // i0 - lo_c stored in 9 bits
+constexpr int SPAN_MAX = (1 << SPAN_BITS) - 1;
+
 // ----------------------------------------------------------------------------
-// K1: fused delay + staged fractional gather + DAS/DMAS window accumulation
+// K0: per point-list delay table (computed once, reused by every scan)
+//   word(p, c) = (i0 - lo_c) << 23 | frac23,  span(c) = {lo_c, hi_c} per tile
+// ----------------------------------------------------------------------------
+struct TableParams {
+  const double* pts;
+  int P;
+  const int* d_count;
+  const int* chan;
+  int C;
+  const double* ant;
+  int M;
+  double inv_scale;
+  int interp;
+  uint32_t* words;
+  int2* span;
+  int* wide;
+};
+
+__global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* dist = reinterpret_cast<double*>(smem);                 // [M][TILE]
+  int* lo = reinterpret_cast<int*>(dist + (size_t)p.M * TILE);   // [C]
+  int* hi = lo + p.C;                                            // [C]
+  int* wide = hi + p.C;
+  const int tid = threadIdx.x;
+  const int n_pts = p.d_count ? min(*p.d_count, p.P) : p.P;
+  const int tile0 = blockIdx.x * TILE;
+  if (tile0 >= n_pts) return;
+  const int n_in = min(TILE, n_pts - tile0);
+  const int la = tid, lb = tid + TPB;
+  const int ga = tile0 + (la < n_in ? la : 0), gb = tile0 + (lb < n_in ? lb : 0);
+  const double pax = p.pts[3 * (size_t)ga], pay = p.pts[3 * (size_t)ga + 1], paz = p.pts[3 * (size_t)ga + 2];
+  const double pbx = p.pts[3 * (size_t)gb], pby = p.pts[3 * (size_t)gb + 1], pbz = p.pts[3 * (size_t)gb + 2];
+  for (int i = 0; i < p.M; ++i) {
+    const double ax = __ldg(p.ant + 3 * i), ay = __ldg(p.ant + 3 * i + 1), az = __ldg(p.ant + 3 * i + 2);
+    dist[i * TILE + la] = antenna_distance(pax, pay, paz, ax, ay, az);
+    dist[i * TILE + lb] = antenna_distance(pbx, pby, pbz, ax, ay, az);
+  }
+  for (int c = tid; c < p.C; c += TPB) {
+    lo[c] = 0x7FFFFFFF;
+    hi[c] = -1;
+  }
+  if (tid == 0) *wide = 0;
+  __syncthreads();
+  // exact per-channel i0 range over the tile's valid points
+  for (int c = 0; c < p.C; ++c) {
+    const int tx = __ldg(p.chan + 2 * c), rx = __ldg(p.chan + 2 * c + 1);
+    int ia, ib;
+    uint32_t qa, qb;
+    split_delay_q(pair_delay(dist[tx * TILE + la], dist[rx * TILE + la], p.inv_scale), p.interp, ia, qa);
+    split_delay_q(pair_delay(dist[tx * TILE + lb], dist[rx * TILE + lb], p.inv_scale), p.interp, ib, qb);
+    int mn = 0x7FFFFFFF, mx = -1;
+    if (la < n_in) { mn = min(mn, ia); mx = max(mx, ia); }
+    if (lb < n_in) { mn = min(mn, ib); mx = max(mx, ib); }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((tid & 31) == 0) {
+      atomicMin(&lo[c], mn);
+      atomicMax(&hi[c], mx);
+    }
+  }
+  __syncthreads();
+  const size_t tile = blockIdx.x;
+  for (int c = tid; c < p.C; c += TPB) {
+    p.span[tile * p.C + c] = make_int2(lo[c], hi[c]);
+    if (hi[c] - lo[c] > SPAN_MAX) atomicOr(wide, 1);
+  }
+  __syncthreads();
+  if (tid == 0) p.wide[tile] = *wide;
+  if (*wide) return;  // wide tiles are evaluated from the points directly
+  uint32_t* w = p.words + tile * (size_t)p.C * TILE;
+  for (int c = 0; c < p.C; ++c) {
+    const int tx = __ldg(p.chan + 2 * c), rx = __ldg(p.chan + 2 * c + 1);
+    int ia, ib;
+    uint32_t qa, qb;
+    split_delay_q(pair_delay(dist[tx * TILE + la], dist[rx * TILE + la], p.inv_scale), p.interp, ia, qa);
+    split_delay_q(pair_delay(dist[tx * TILE + lb], dist[rx * TILE + lb], p.inv_scale), p.interp, ib, qb);
+    const int l = lo[c];
+    w[(size_t)c * TILE + la] = ((uint32_t)min(max(ia - l, 0), SPAN_MAX) << 23) | qa;
+    w[(size_t)c * TILE + lb] = ((uint32_t)min(max(ib - l, 0), SPAN_MAX) << 23) | qb;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// K1: staged fractional gather + fused DAS/DMAS window accumulation
 // ----------------------------------------------------------------------------
 template <int KIND>
 __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
@@ -261,82 +366,42 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
   if (scan_begin >= p.n_scans) return;
   const int n_my_scans = min(p.scans_per_cta, p.n_scans - scan_begin);
 
-  const SmemLayout L = smem_layout(p.M, p.C, p.cap);
-  double* dist = reinterpret_cast<double*>(smem + L.dist);
-  int2* chs = reinterpret_cast<int2*>(smem + L.chan);
+  const SmemLayout L = smem_layout(p.C, p.cap);
   int* clo = reinterpret_cast<int*>(smem + L.lo);
   int* calloc_ = reinterpret_cast<int*>(smem + L.alloc);
   int* coff = reinterpret_cast<int*>(smem + L.off);
-  double* amin = reinterpret_cast<double*>(smem + L.ant_min);
-  double* amax = reinterpret_cast<double*>(smem + L.ant_max);
   int* misc = reinterpret_cast<int*>(smem + L.misc);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.mbar);
   float* stage = reinterpret_cast<float*>(smem + L.stage);
 
-  // ---- phase A: points, distances, per-channel spans ----------------------
+  const size_t tile = blockIdx.x;
+  const bool wide = __ldg(p.tab_wide + tile) != 0;
+  const uint32_t* tw = p.tab_words + tile * (size_t)p.C * TILE;
+  const int2* tsp = p.tab_span + tile * (size_t)p.C;
+
   const int la = tid, lb = tid + TPB;
   const bool va = la < n_in_tile, vb = lb < n_in_tile;
   const int ga = tile0 + (va ? la : 0), gb = tile0 + (vb ? lb : 0);
-  const double pax = p.pts[3 * (size_t)ga], pay = p.pts[3 * (size_t)ga + 1],
-               paz = p.pts[3 * (size_t)ga + 2];
-  const double pbx = p.pts[3 * (size_t)gb], pby = p.pts[3 * (size_t)gb + 1],
-               pbz = p.pts[3 * (size_t)gb + 2];
-  for (int i = 0; i < p.M; ++i) {
-    const double ax = __ldg(p.ant + 3 * i), ay = __ldg(p.ant + 3 * i + 1),
-                 az = __ldg(p.ant + 3 * i + 2);
-    dist[i * TILE + la] = antenna_distance(pax, pay, paz, ax, ay, az);
-    dist[i * TILE + lb] = antenna_distance(pbx, pby, pbz, ax, ay, az);
+  const int oa = va ? (p.out_idx ? __ldg(p.out_idx + ga) : ga) : -1;
+  const int ob = vb ? (p.out_idx ? __ldg(p.out_idx + gb) : gb) : -1;
+
+  // ---- per-channel spans and stage-buffer groups --------------------------
+  for (int c = tid; c < p.C; c += TPB) {
+    const int2 sp = __ldg(tsp + c);
+    clo[c] = sp.x;
+    // samples k0+q*WCH + [lo, hi+WCH] plus up to 3 of alignment slack
+    calloc_[c] = (sp.y - sp.x + WCH + 8 + 3) & ~3;
   }
-  for (int c = tid; c < p.C; c += TPB) chs[c] = make_int2(__ldg(p.chan + 2 * c), __ldg(p.chan + 2 * c + 1));
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
     fence_mbar_init();
   }
   __syncthreads();
-
-  // exact per-antenna min/max distance over the tile's valid points
-  for (int i = warp; i < p.M; i += TPB / 32) {
-    double mn = INFINITY, mx = -INFINITY;
-    for (int j = lane; j < n_in_tile; j += 32) {
-      const double d = dist[i * TILE + j];
-      mn = fmin(mn, d);
-      mx = fmax(mx, d);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    if (lane == 0) {
-      amin[i] = mn;
-      amax[i] = mx;
-    }
-  }
-  __syncthreads();
-
-  // channel spans: every point's i0 for channel c lies in [lo_c, hi_c] because
-  // fl(+) and fl(*) are monotone (no margin needed; nearest adds one sample).
-  for (int c = tid; c < p.C; c += TPB) {
-    const int2 tr = chs[c];
-    int lo, hi;
-    float f0, f1;
-    split_delay(__dmul_rn(__dadd_rn(amin[tr.x], amin[tr.y]), p.inv_scale), MWB_INTERP_LINEAR, lo,
-                f0, f1);
-    split_delay(__dmul_rn(__dadd_rn(amax[tr.x], amax[tr.y]), p.inv_scale), MWB_INTERP_LINEAR, hi,
-                f0, f1);
-    if (p.interp == MWB_INTERP_NEAREST) hi += 1;
-    clo[c] = lo;
-    // samples k0+q*WCH + [lo, hi+WCH] plus up to 3 of alignment slack each side
-    long long a = (long long)(hi - lo) + WCH + 8;
-    a = (a + 3) & ~3LL;
-    calloc_[c] = (int)min(a, (long long)1 << 30);
-  }
-  __syncthreads();
   if (tid == 0) {
     int mx = 0;
     for (int c = 0; c < p.C; ++c) mx = max(mx, calloc_[c]);
-    int G = (p.mode == 0 && mx <= p.cap) ? p.cap / mx : 0;
+    int G = (!wide && p.mode == 0 && mx <= p.cap) ? p.cap / mx : 0;
     if (G > p.C) G = p.C;
     int run = 0;
     for (int c = 0; c < p.C; ++c) {
@@ -352,12 +417,6 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
   const int n_groups = misc[1];
   const int n_chunks = (p.W + WCH - 1) / WCH;
 
-  const int oa = va ? (p.out_idx ? __ldg(p.out_idx + ga) : ga) : -1;
-  const int ob = vb ? (p.out_idx ? __ldg(p.out_idx + gb) : gb) : -1;
-
-  // per-step bookkeeping
-  auto chunk_base = [&](int q) { return p.k0 + q * WCH; };
-
   // Issue the bulk copies of step t into buffer (t & 1).  Warp 0 only.
   auto issue = [&](int t) {
     const int g = t % n_groups;
@@ -367,12 +426,11 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
     const int c_begin = g * G, c_end = min(p.C, c_begin + G);
     float* buf = stage + (t & 1) * p.cap;
     const float* scan_sig = p.sig + (size_t)s * (size_t)p.scan_stride;
+    const int cb = p.k0 + q * WCH;
     uint32_t bytes_lane = 0;
     for (int c = c_begin + lane; c < c_end; c += 32) {
-      const long long start = (long long)chunk_base(q) + clo[c];
-      const long long start4 = start & ~3LL;
-      const long long avail = (long long)p.ld - start4;
-      const long long n = min((long long)calloc_[c], max(avail, 0LL));
+      const long long start4 = ((long long)cb + clo[c]) & ~3LL;
+      const long long n = min((long long)calloc_[c], max((long long)p.ld - start4, 0LL));
       bytes_lane += (uint32_t)(n * 4);
     }
 #pragma unroll
@@ -380,33 +438,31 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
     if (lane == 0) mbar_arrive_expect_tx(&mbar[t & 1], bytes_lane);
     __syncwarp();
     for (int c = c_begin + lane; c < c_end; c += 32) {
-      const long long start = (long long)chunk_base(q) + clo[c];
-      const long long start4 = start & ~3LL;
-      const long long avail = (long long)p.ld - start4;
+      const long long start4 = ((long long)cb + clo[c]) & ~3LL;
       const int alloc = calloc_[c];
-      const long long n = min((long long)alloc, max(avail, 0LL));
+      const long long n = min((long long)alloc, max((long long)p.ld - start4, 0LL));
       float* dst = buf + coff[c];
       if (n > 0) bulk_g2s(dst, scan_sig + (size_t)c * p.ld + start4, (uint32_t)(n * 4), &mbar[t & 1]);
       for (long long j = max(n, 0LL); j < alloc; ++j) dst[j] = 0.f;  // past the record: zeros
     }
   };
 
-  const double isc = p.inv_scale;
   const int nsteps = (n_groups > 0 ? n_groups : 1) * n_chunks * n_my_scans;
 
   float2 sacc[WCH];
   float2 qe = make_float2(0.f, 0.f), qo = make_float2(0.f, 0.f);
-  double ea = 0.0, eb = 0.0;
+  double eS_a = 0.0, eS_b = 0.0, eQ_a = 0.0, eQ_b = 0.0;
 
   if (G > 0 && warp == 0) issue(0);
+  __syncthreads();  // thread zero-fills of step 0 are not tracked by the mbarrier
 
   for (int t = 0; t < nsteps; ++t) {
     const int g = G > 0 ? t % n_groups : 0;
     const int r = G > 0 ? t / n_groups : t;
     const int q = r % n_chunks;
-    const int si = r / n_chunks;
-    const int s = scan_begin + si;
+    const int s = scan_begin + r / n_chunks;
     const int valid = min(WCH, p.W - q * WCH);
+    const int cb = p.k0 + q * WCH;
 
     if (G > 0) {
       if (warp == 0 && t + 1 < nsteps) issue(t + 1);
@@ -418,32 +474,59 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
       qe = make_float2(0.f, 0.f);
       qo = make_float2(0.f, 0.f);
     }
-
     const int c_begin = G > 0 ? g * G : 0;
     const int c_end = G > 0 ? min(p.C, c_begin + G) : p.C;
-    const int cb = chunk_base(q);
     const float* buf = stage + (t & 1) * p.cap;
     const float* scan_sig = p.sig + (size_t)s * (size_t)p.scan_stride;
 
-    for (int c = c_begin; c < c_end; ++c) {
-      const int2 tr = chs[c];
-      const double na = __dmul_rn(__dadd_rn(dist[tr.x * TILE + la], dist[tr.y * TILE + la]), isc);
-      const double nb = __dmul_rn(__dadd_rn(dist[tr.x * TILE + lb], dist[tr.y * TILE + lb]), isc);
-      int ia, ib;
-      float2 f0, f1;
-      split_delay(na, p.interp, ia, f0.x, f1.x);
-      split_delay(nb, p.interp, ib, f0.y, f1.y);
-      if (G > 0) {
-        const int sbase = coff[c] - ((cb + clo[c]) & ~3) + cb;
-        const float* ya = buf + sbase + ia;
-        const float* yb = buf + sbase + ib;
+    if (G > 0) {
+      // fast path: packed delay words (L2-resident table), samples from smem
+      uint32_t wa = __ldg(tw + (size_t)c_begin * TILE + la), wb = __ldg(tw + (size_t)c_begin * TILE + lb);
+      for (int c = c_begin; c < c_end; ++c) {
+        const uint32_t ca = wa, cbw = wb;
+        if (c + 1 < c_end) {
+          wa = __ldg(tw + (size_t)(c + 1) * TILE + la);
+          wb = __ldg(tw + (size_t)(c + 1) * TILE + lb);
+        }
+        const float2 f1 = make_float2(weight_f1(ca), weight_f1(cbw));
+        const float2 f0 = __ffma2_rn(f1, make_float2(-1.f, -1.f), make_float2(1.f, 1.f));
+        const int sbase = coff[c] + ((cb + clo[c]) & 3);  // smem slot of sample cb + lo_c
+        const float* ya = buf + sbase + (int)(ca >> 23);
+        const float* yb = buf + sbase + (int)(cbw >> 23);
         auto load = [&](int k) { return make_float2(ya[k], yb[k]); };
         if (valid == WCH)
           accumulate_channel<KIND, false>(sacc, qe, qo, f0, f1, load, valid);
         else
           accumulate_channel<KIND, true>(sacc, qe, qo, f0, f1, load, valid);
-      } else {
-        // L1/L2 gather path: same arithmetic, loads straight from global.
+      }
+    } else {
+      // L1/L2 gather path (mode 1 or a tile whose delay spread exceeds the table):
+      // same weights, loads straight from global with a zero tail.
+      const double pax = p.pts[3 * (size_t)ga], pay = p.pts[3 * (size_t)ga + 1], paz = p.pts[3 * (size_t)ga + 2];
+      const double pbx = p.pts[3 * (size_t)gb], pby = p.pts[3 * (size_t)gb + 1], pbz = p.pts[3 * (size_t)gb + 2];
+      for (int c = 0; c < p.C; ++c) {
+        int ia, ib;
+        uint32_t qa, qb;
+        if (!wide) {
+          const uint32_t wa = __ldg(tw + (size_t)c * TILE + la), wb = __ldg(tw + (size_t)c * TILE + lb);
+          const int l = clo[c];
+          ia = l + (int)(wa >> 23);
+          ib = l + (int)(wb >> 23);
+          qa = wa;
+          qb = wb;
+        } else {
+          const int tx = __ldg(p.chan + 2 * c), rx = __ldg(p.chan + 2 * c + 1);
+          const double* at = p.ant + 3 * tx;
+          const double* ar = p.ant + 3 * rx;
+          split_delay_q(pair_delay(antenna_distance(pax, pay, paz, at[0], at[1], at[2]),
+                                   antenna_distance(pax, pay, paz, ar[0], ar[1], ar[2]), p.inv_scale),
+                        p.interp, ia, qa);
+          split_delay_q(pair_delay(antenna_distance(pbx, pby, pbz, at[0], at[1], at[2]),
+                                   antenna_distance(pbx, pby, pbz, ar[0], ar[1], ar[2]), p.inv_scale),
+                        p.interp, ib, qb);
+        }
+        const float2 f1 = make_float2(weight_f1(qa), weight_f1(qb));
+        const float2 f0 = __ffma2_rn(f1, make_float2(-1.f, -1.f), make_float2(1.f, 1.f));
         const float* yc = scan_sig + (size_t)c * p.ld;
         const long long ma = (long long)cb + ia, mb = (long long)cb + ib;
         const int ldv = p.ld;
@@ -459,34 +542,52 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
     }
 
     if (g == (G > 0 ? n_groups - 1 : 0)) {
-      chunk_energy<KIND>(sacc, qe, qo, valid, ea, eb);
+      const float2 S = chunk_sumsq(sacc, valid);
+      eS_a += (double)S.x;
+      eS_b += (double)S.y;
+      if (KIND != KIND_DAS) {
+        const float2 Q = __fadd2_rn(qe, qo);
+        eQ_a += (double)Q.x;
+        eQ_b += (double)Q.y;
+      }
       if (q == n_chunks - 1) {
-        const float eaf = __double2float_rn(ea), ebf = __double2float_rn(eb);
-        float* out = p.out + (size_t)s * (size_t)p.out_stride;
-        unsigned long long key = 0ull;
         bool bad = false;
-        if (va) {
-          out[oa] = eaf;
-          if (isfinite(eaf)) key = argmax_key(eaf, oa); else bad = true;
-        }
-        if (vb) {
-          out[ob] = ebf;
-          if (isfinite(ebf)) key = max(key, (unsigned long long)argmax_key(ebf, ob)); else bad = true;
-        }
-        if (p.argmax) {
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
-          if (lane == 0 && key != 0ull) atomicMax(p.argmax + s, key);
+        for (int kk = 0; kk < 2; ++kk) {
+          const bool want = kk == 0 ? KIND != KIND_DMAS : KIND != KIND_DAS;
+          if (!want) continue;
+          float ea, eb;
+          if (kk == 0) {
+            ea = __double2float_rn(eS_a);
+            eb = __double2float_rn(eS_b);
+          } else {
+            ea = __double2float_rn(0.5 * (eS_a - eQ_a));
+            eb = __double2float_rn(0.5 * (eS_b - eQ_b));
+          }
+          float* out = (kk == 0 ? p.out_das : p.out_dmas) + (size_t)s * (size_t)p.out_stride;
+          unsigned long long* keys = kk == 0 ? p.key_das : p.key_dmas;
+          unsigned long long key = 0ull;
+          if (va) {
+            out[oa] = ea;
+            if (isfinite(ea)) key = argmax_key(ea, oa); else bad = true;
+          }
+          if (vb) {
+            out[ob] = eb;
+            if (isfinite(eb)) key = max(key, (unsigned long long)argmax_key(eb, ob)); else bad = true;
+          }
+          if (keys) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+            if (lane == 0 && key != 0ull) atomicMax(keys + s, key);
+          }
         }
         if (bad && p.flags) atomicOr(p.flags, 1);
-        ea = 0.0;
-        eb = 0.0;
+        eS_a = eS_b = eQ_a = eQ_b = 0.0;
       }
     }
     if (G > 0) __syncthreads();
   }
 }
-
 // ----------------------------------------------------------------------------
 // lattice enumeration (beamform.py:268-280 + skip filter 309-315 + centres 321-323)
 // ----------------------------------------------------------------------------
@@ -967,6 +1068,45 @@ __global__ void __launch_bounds__(1024) mb_ffma_kernel(float* sink, float seed) 
   if (r == 1234.5f) sink[threadIdx.x] = r;
 }
 
+// shared-memory load-width / broadcast pattern probe: WORDS = 1, 2, 4 (LDS.32/64/128);
+// lane address (in units of WORDS words): 0 consecutive, 1 all-same, 2 lane/2,
+// 3 lane/4, 4 lane/8, 5 (lane*3)/8 (a delay-like monotone spread)
+template <int WORDS>
+__global__ void __launch_bounds__(1024) mb_lds_pattern_kernel(float* sink, int pattern) {
+  __shared__ __align__(16) float buf[8192];
+  for (int i = threadIdx.x; i < 8192; i += blockDim.x) buf[i] = (float)(i & 1023);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  int a;
+  switch (pattern) {
+    case 0: a = lane; break;
+    case 1: a = 0; break;
+    case 2: a = lane >> 1; break;
+    case 3: a = lane >> 2; break;
+    case 4: a = lane >> 3; break;
+    default: a = (lane * 3) >> 3; break;
+  }
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int it = 0; it < MB_ITERS / 4; ++it) {
+    const int base = ((it * 37) & 63) * 32;  // stays 16-byte aligned per WORDS
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float* b = buf + (base + (a + k * 8) * WORDS) % 8192;
+      if (WORDS == 1) {
+        acc[k & 3] += b[0];
+      } else if (WORDS == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(b);
+        acc[k & 3] += v.x + v.y;
+      } else {
+        const float4 v = *reinterpret_cast<const float4*>(b);
+        acc[k & 3] += (v.x + v.y) + (v.z + v.w);
+      }
+    }
+  }
+  const float r = acc[0] + acc[1] + acc[2] + acc[3];
+  if (r == 1234.5f) sink[threadIdx.x] = r;
+}
+
 int choose_scans_per_cta(int tiles, int n_scans) {
   const long long target = 148LL * 3 * 8;  // >= 8 waves of 3 CTAs/SM
   long long spc = (long long)tiles * n_scans / target;
@@ -988,29 +1128,73 @@ int mwb_version(void) { return 1; }
 
 int64_t mwb_trace_bytes(void) { return (int64_t)sizeof(mwb_trace_t); }
 
+int64_t mwb_delay_table_bytes(int n_pts, int n_chan) {
+  if (n_pts < 0 || n_chan < 1) return -1;
+  const long long tiles = (n_pts + TILE - 1) / TILE;
+  return (int64_t)table_layout(tiles > 0 ? tiles : 1, n_chan).total;
+}
+
+int mwb_delay_table(const double* pts_xyz, int n_pts, const int32_t* d_count, const int32_t* chan_txrx,
+                    int n_chan, const double* ant_xyz, int n_ant, double inv_scale, int interp,
+                    void* table, void* stream) {
+  if (n_pts < 0 || n_chan < 1 || n_ant < 1) return set_err(MWB_EINVAL, "mwb_delay_table: bad sizes");
+  if (n_pts == 0) return MWB_OK;
+  if (n_ant > MAX_ANT) return set_err(MWB_ERANGE, "mwb_delay_table: too many antennas (%d)", n_ant);
+  if (n_chan > MAX_CHAN) return set_err(MWB_ERANGE, "mwb_delay_table: too many channels (%d)", n_chan);
+  if (interp != MWB_INTERP_LINEAR && interp != MWB_INTERP_NEAREST)
+    return set_err(MWB_EINVAL, "mwb_delay_table: bad interpolation");
+  if (!pts_xyz || !chan_txrx || !ant_xyz || !table) return set_err(MWB_EINVAL, "mwb_delay_table: null pointer");
+  if (!(inv_scale > 0.0) || !isfinite(inv_scale)) return set_err(MWB_EINVAL, "mwb_delay_table: inv_scale must be > 0");
+  const long long tiles = (n_pts + TILE - 1) / TILE;
+  const TableLayout T = table_layout(tiles, n_chan);
+  TableParams p;
+  p.pts = pts_xyz;
+  p.P = n_pts;
+  p.d_count = d_count;
+  p.chan = chan_txrx;
+  p.C = n_chan;
+  p.ant = ant_xyz;
+  p.M = n_ant;
+  p.inv_scale = inv_scale;
+  p.interp = interp;
+  unsigned char* base = reinterpret_cast<unsigned char*>(table);
+  p.words = reinterpret_cast<uint32_t*>(base + T.words);
+  p.span = reinterpret_cast<int2*>(base + T.span);
+  p.wide = reinterpret_cast<int*>(base + T.wide);
+  const size_t sm = sizeof(double) * (size_t)n_ant * TILE + sizeof(int) * (2 * (size_t)n_chan + 4);
+  if (sm > 227 * 1024) return set_err(MWB_ERANGE, "mwb_delay_table: shared memory %lld bytes", (long long)sm);
+  cudaError_t e = cudaFuncSetAttribute(delay_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  delay_table_kernel<<<(unsigned)tiles, TPB, sm, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  return check_launch("delay_table_kernel");
+}
+
 int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
                  int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
                  double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
-                 const int32_t* d_count, int kind, int interp, int k0, int window, float* out,
-                 int64_t out_stride, uint64_t* argmax_key, int32_t* flags, int mode,
-                 void* stream) {
+                 const int32_t* d_count, const void* table, int interp, int k0, int window,
+                 float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
+                 uint64_t* key_dmas, int32_t* flags, int mode, void* stream) {
   if (n_pts < 0 || n_scans < 0 || n_chan < 0 || n_ant < 1 || window < 0 || k0 < 0)
     return set_err(MWB_EINVAL, "mwb_energies: negative size");
   if (n_pts == 0 || n_scans == 0) return MWB_OK;
   if (n_chan == 0 || window == 0)
     return set_err(MWB_EINVAL, "mwb_energies: no channels or empty window");
-  if (kind != MWB_DAS && kind != MWB_DMAS) return set_err(MWB_EINVAL, "mwb_energies: bad kind");
+  if (!out_das && !out_dmas) return set_err(MWB_EINVAL, "mwb_energies: no output (kind) requested");
   if (interp != MWB_INTERP_LINEAR && interp != MWB_INTERP_NEAREST)
     return set_err(MWB_EINVAL, "mwb_energies: bad interpolation");
   if (n_ant > MAX_ANT) return set_err(MWB_ERANGE, "mwb_energies: too many antennas (%d)", n_ant);
   if (n_chan > MAX_CHAN) return set_err(MWB_ERANGE, "mwb_energies: too many channels (%d)", n_chan);
   if (ld % 4 != 0 || scan_stride % 4 != 0 || ld < n_samples)
     return set_err(MWB_EINVAL, "mwb_energies: ld and scan_stride must be multiples of 4, ld >= n_samples");
-  if (!sig || !chan_txrx || !ant_xyz || !pts_xyz || !out)
+  if (!sig || !chan_txrx || !ant_xyz || !pts_xyz || !table)
     return set_err(MWB_EINVAL, "mwb_energies: null pointer");
   if (((uintptr_t)sig & 15) != 0) return set_err(MWB_EINVAL, "mwb_energies: sig must be 16-byte aligned");
-  if (inv_scale <= 0.0 || !isfinite(inv_scale)) return set_err(MWB_EINVAL, "mwb_energies: inv_scale must be > 0");
+  if (!(inv_scale > 0.0) || !isfinite(inv_scale)) return set_err(MWB_EINVAL, "mwb_energies: inv_scale must be > 0");
 
+  const long long tiles = (n_pts + TILE - 1) / TILE;
+  const TableLayout T = table_layout(tiles, n_chan);
+  const unsigned char* base = reinterpret_cast<const unsigned char*>(table);
   EnergyParams p;
   p.sig = sig;
   p.scan_stride = scan_stride;
@@ -1026,12 +1210,17 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
   p.out_idx = out_idx;
   p.P = n_pts;
   p.d_count = d_count;
+  p.tab_words = reinterpret_cast<const uint32_t*>(base + T.words);
+  p.tab_span = reinterpret_cast<const int2*>(base + T.span);
+  p.tab_wide = reinterpret_cast<const int*>(base + T.wide);
   p.interp = interp;
   p.k0 = k0;
   p.W = window;
-  p.out = out;
+  p.out_das = out_das;
+  p.out_dmas = out_dmas;
   p.out_stride = out_stride;
-  p.argmax = reinterpret_cast<unsigned long long*>(argmax_key);
+  p.key_das = reinterpret_cast<unsigned long long*>(key_das);
+  p.key_dmas = reinterpret_cast<unsigned long long*>(key_dmas);
   p.flags = flags;
   p.mode = mode;
   // stage capacity: every channel's span for a compact tile, capped at 32 KB
@@ -1040,22 +1229,18 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
   if (cap > CAP_MAX) cap = CAP_MAX;
   if (cap < 256) cap = 256;
   p.cap = (int)cap;
-  const int tiles = (n_pts + TILE - 1) / TILE;
-  p.scans_per_cta = choose_scans_per_cta(tiles, n_scans);
-  const SmemLayout L = smem_layout(n_ant, n_chan, p.cap);
-  if (L.total > 227 * 1024) return set_err(MWB_ERANGE, "mwb_energies: shared memory %lld bytes exceeds 227 KB", (long long)L.total);
-  dim3 grid(tiles, (n_scans + p.scans_per_cta - 1) / p.scans_per_cta);
+  p.scans_per_cta = choose_scans_per_cta((int)tiles, n_scans);
+  const SmemLayout L = smem_layout(n_chan, p.cap);
+  if (L.total > 227 * 1024)
+    return set_err(MWB_ERANGE, "mwb_energies: shared memory %lld bytes exceeds 227 KB", (long long)L.total);
+  dim3 grid((unsigned)tiles, (n_scans + p.scans_per_cta - 1) / p.scans_per_cta);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t e;
-  if (kind == MWB_DAS) {
-    e = cudaFuncSetAttribute(energy_kernel<MWB_DAS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-    if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    energy_kernel<MWB_DAS><<<grid, TPB, L.total, st>>>(p);
-  } else {
-    e = cudaFuncSetAttribute(energy_kernel<MWB_DMAS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-    if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    energy_kernel<MWB_DMAS><<<grid, TPB, L.total, st>>>(p);
-  }
+  const int kind = out_das && out_dmas ? KIND_BOTH : (out_das ? KIND_DAS : KIND_DMAS);
+  void (*fn)(EnergyParams) = kind == KIND_DAS ? energy_kernel<KIND_DAS>
+                             : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS> : energy_kernel<KIND_BOTH>);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  fn<<<grid, TPB, L.total, st>>>(p);
   return check_launch("energy_kernel");
 }
 
@@ -1151,7 +1336,10 @@ int mwb_microbench(int which, double* work, float* ms, void* stream) {
     cudaEventRecord(a, st);
     if (which == 0) mb_lds_kernel<<<blocks, threads, 0, st>>>(sink, 7);
     else if (which == 1) mb_ffma2_kernel<<<blocks, threads, 0, st>>>(sink, 0.5f);
-    else mb_ffma_kernel<<<blocks, threads, 0, st>>>(sink, 0.5f);
+    else if (which == 2) mb_ffma_kernel<<<blocks, threads, 0, st>>>(sink, 0.5f);
+    else if (which >= 100 && which < 110) mb_lds_pattern_kernel<1><<<blocks, threads, 0, st>>>(sink, which - 100);
+    else if (which >= 110 && which < 120) mb_lds_pattern_kernel<2><<<blocks, threads, 0, st>>>(sink, which - 110);
+    else mb_lds_pattern_kernel<4><<<blocks, threads, 0, st>>>(sink, which - 120);
     cudaEventRecord(b, st);
   }
   cudaEventSynchronize(b);
@@ -1159,7 +1347,11 @@ int mwb_microbench(int which, double* work, float* ms, void* stream) {
   const double thr = (double)blocks * threads * MB_ITERS;
   if (which == 0) *work = thr * 32 * 4.0;           // bytes loaded from shared memory
   else if (which == 1) *work = thr * 8 * 2 * 2.0;   // 8 FFMA2 = 16 FMA = 32 flop
-  else *work = thr * 16 * 2.0;
+  else if (which == 2) *work = thr * 16 * 2.0;
+  else {  // bytes delivered to registers by the pattern probe
+    const int words = which < 110 ? 1 : (which < 120 ? 2 : 4);
+    *work = (double)blocks * threads * (MB_ITERS / 4) * 16 * 4.0 * words;
+  }
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(sink);

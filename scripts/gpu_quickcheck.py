@@ -69,50 +69,6 @@ def main():
         ms = ctypes.c_float()
         nat.check(lib.mwb_microbench(which, ctypes.byref(work), ctypes.byref(ms), None), "mb")
         print(f"microbench {name}: {work.value / ms.value / 1e9:.1f} G/ms -> {work.value / (ms.value * 1e-3) / 1e12:.2f} T/s")
-    # batched cfg3-like timing
-    m3 = synth.ScanModel()
-    S = 512
-    sig, tumours = synth.batch_2d(m3, range(S))
-    grid3 = synth.grid_square(0.12, 256)
-    bi = BatchImager(m3.geometry(), m3.pairs(), m3.n_samples, grid3, window=(m3.k0, 32))
-    sig_d = bi.to_device_layout(sig)
-    nxny = 256 * 256
-    for kind in ("das", "dmas"):
-        for mode in (0, 1):
-            bi.mode = mode
-            out = torch.empty((S, nxny), dtype=torch.float32, device="cuda")
-            keys = torch.zeros(S, dtype=torch.int64, device="cuda")
-            for _ in range(2):
-                bi.run_device(sig_d, kind, out, keys)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            reps = 3
-            for _ in range(reps):
-                bi.run_device(sig_d, kind, out, keys)
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / reps
-            pps = S * bi.n_pts * bi.n_chan * 32 / (ms * 1e-3)
-            print(f"batch {kind} mode={mode}: {ms:.2f} ms for {S} scans, {pps / 1e12:.2f} Tpps/s, "
-                  f"{S * bi.n_pts * bi.n_chan / (ms * 1e-3) / 1e9:.1f} G pixel-pair/s")
-        cells = bi.decode_keys(keys.cpu().numpy().view(np.uint64))
-        hits = np.mean([np.abs(np.array(grid3.point_to_cell(*tumours[i])) - cells[i]).max() <= 2 for i in range(S)])
-        print(f"  {kind} argmax within 2 cells of tumour: {hits:.3f}")
-    # batch parity vs oracle for 2 scans
-    bi.mode = 0
-    for kind in ("das", "dmas"):
-        out = torch.empty((S, nxny), dtype=torch.float32, device="cuda")
-        bi.run_device(sig_d, kind, out)
-        o = out.cpu().numpy()
-        for s in (0, 7):
-            ds_s = mw.BackscatterDataset(m3.geometry(), synth.embed_pairs(12, m3.pairs(), sig[s].astype(np.float64)))
-            sub = synth.grid_square(0.12, 256)
-            pts = np.array([sub.cell_center(i, j) for i in range(0, 256, 9) for j in range(0, 256, 11)])
-            ref = orc.windowed_energies(ds_s.geometry.antennas, ds_s.geometry.propagation_speed,
-                                        ds_s.geometry.sample_interval, ds_s.signals, pts, kind, m3.k0, 32)
-            got = np.array([o[s, i * 256 + j] for i in range(0, 256, 9) for j in range(0, 256, 11)])
-            print(f"  batch parity {kind} scan {s}: err {pn(got, ref):.2e}")
 
 
 if __name__ == "__main__":

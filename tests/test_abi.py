@@ -1,0 +1,104 @@
+"""The C-ABI library loads and exports every symbol include/mwb.h declares
+(CPU-only: no compute call needs a GPU; argument validation runs before any
+CUDA call, so error paths are testable here)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_1709_02549_b200 import _build, _native
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "mwb.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mwb_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return _native.load()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = declared_functions()
+    assert len(names) >= 8
+    for name in names:
+        assert hasattr(lib, name), name
+
+
+def test_binding_covers_header():
+    assert set(declared_functions()) == set(_native.EXPORTED)
+
+
+def test_trace_layout_matches_c(lib):
+    assert lib.mwb_trace_bytes() == _native.TRACE_BYTES
+    assert ctypes.sizeof(_native.IterRecord) == 272
+
+
+def test_version(lib):
+    assert lib.mwb_version() >= 1
+
+
+def energies_args(**kw):
+    """Positional argument list of mwb_energies (include/mwb.h) with overrides."""
+    names = ["sig", "n_scans", "scan_stride", "n_chan", "ld", "n_samples", "chan", "ant", "n_ant", "inv_scale",
+             "pts", "out_idx", "n_pts", "d_count", "table", "interp", "k0", "window", "out_das", "out_dmas",
+             "out_stride", "key_das", "key_dmas", "flags", "mode", "stream"]
+    base = dict(sig=None, n_scans=1, scan_stride=0, n_chan=1, ld=4, n_samples=4, chan=None, ant=None, n_ant=2,
+                inv_scale=1.0, pts=None, out_idx=None, n_pts=1, d_count=None, table=None, interp=0, k0=0, window=4,
+                out_das=None, out_dmas=None, out_stride=0, key_das=None, key_dmas=None, flags=None, mode=0,
+                stream=None)
+    base.update(kw)
+    assert len(names) == len(_native._SIGNATURES["mwb_energies"][0])
+    return [base[n] for n in names]
+
+
+def test_argument_errors_set_last_error(lib):
+    assert lib.mwb_energies(*energies_args(n_pts=-1)) == -1
+    assert b"negative" in lib.mwb_last_error()
+    assert lib.mwb_energies(*energies_args()) == -1
+    assert b"no output" in lib.mwb_last_error()
+    assert lib.mwb_energies(*energies_args(out_das=16, interp=5)) == -1
+    assert b"interpolation" in lib.mwb_last_error()
+    assert lib.mwb_energies(*energies_args(out_das=16, ld=6)) == -1
+    assert b"multiples of 4" in lib.mwb_last_error()
+    assert lib.mwb_energies(*energies_args(out_das=16, n_ant=99)) == -3
+    assert lib.mwb_delay_table(None, 10, None, None, 0, None, 2, 1.0, 0, None, None) == -1
+    assert lib.mwb_delay_table_bytes(1000, 66) >= 1000 * 66 * 4
+    assert lib.mwb_delay_table_bytes(-1, 66) == -1
+    rc = lib.mwb_select_roi(None, None, 10, 10, 1, 0, 0, 10, 9, 0.25, 4, None, None, None)
+    assert rc == -1 and b"outside" in lib.mwb_last_error()
+    rc = lib.mwb_select_roi(None, None, 10, 10, 1, 0, 0, 9, 9, 1.5, 4, None, None, None)
+    assert rc == -1 and b"frame_fraction" in lib.mwb_last_error()
+    rc = lib.mwb_enumerate_lattice(0.0, 0.0, 1.0, 10, 10, 0, 0, 9, 9, None, 0, None, 0, None, None, None, None,
+                                   None, None)
+    assert rc == -1
+    assert lib.mwb_lattice_workspace_bytes(0, 5, 1) == -1
+    assert lib.mwb_lattice_workspace_bytes(100, 100, 1) > 0
+
+
+def test_native_check_raises_with_message(lib):
+    lib.mwb_argmax_dense(None, None, -1, None, None)
+    with pytest.raises(RuntimeError, match="bad arguments"):
+        _native.check(-1, "mwb_argmax_dense")
+
+
+def test_sass_is_sm100a():
+    """The built library carries sm_100a SASS with FFMA2 and TMA bulk copies."""
+    import shutil
+    import subprocess
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(tool).exists():
+        pytest.skip("cuobjdump not available")
+    _build.build()
+    out = subprocess.run([tool, "-sass", str(_build.LIB)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "FFMA2" in out
+    assert "UBLKCP" in out
