@@ -27,6 +27,7 @@
 #include <stdarg.h>
 #include <string.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "../../include/mwb.h"
 
@@ -35,9 +36,11 @@ namespace {
 constexpr int TPB = 128;          // threads per energy CTA
 constexpr int TILE = 2 * TPB;     // focal points per CTA
 constexpr int WCH = 32;           // window samples per register chunk
+static_assert(WCH % 4 == 0, "chunk starts must keep the 16-byte span alignment phase");
 constexpr int MAX_ANT = 64;
 constexpr int MAX_CHAN = 4096;
 constexpr int CAP_MAX = 8192;     // floats per stage buffer (32 KB)
+constexpr int NSTAGE = 3;         // stage-buffer ring depth (full/empty mbarrier pairs)
 
 thread_local char g_err[512] = "";
 
@@ -78,6 +81,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -221,7 +228,7 @@ struct EnergyParams {
 };
 
 struct SmemLayout {
-  size_t lo, alloc, off, misc, mbar, stage, total;
+  size_t lo, alloc, off, sb, misc, mbar, stage, total;
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -232,11 +239,12 @@ __host__ __device__ inline SmemLayout smem_layout(int C, int cap) {
   L.lo = o;      o += sizeof(int) * (size_t)C;
   L.alloc = o;   o += sizeof(int) * (size_t)C;
   L.off = o;     o += sizeof(int) * (size_t)C;
+  L.sb = o;      o += sizeof(int) * (size_t)C;
   L.misc = o;    o += sizeof(int) * 16;
   o = align_up(o, 16);
-  L.mbar = o;    o += sizeof(uint64_t) * 2;
+  L.mbar = o;    o += sizeof(uint64_t) * 2 * NSTAGE;
   o = align_up(o, 128);
-  L.stage = o;   o += sizeof(float) * 2 * (size_t)cap;
+  L.stage = o;   o += sizeof(float) * NSTAGE * (size_t)cap;
   L.total = o;
   return L;
 }
@@ -348,11 +356,44 @@ __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
   }
 }
 
+// (1 + f1) as fp32 bits in one LOP3: (w & 0x7FFFFF) | 0x3F800000
+__device__ __forceinline__ float one_plus_f1(uint32_t w) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, 0x7FFFFF, %2, 0xEA;" : "=r"(r) : "r"(w), "r"(0x3F800000u));
+  return __uint_as_float(r);
+}
+
+// Channels [c_begin, c_end) of one step on the smem-staged samples.  The delay
+// words of the next channel are fetched while the current one is processed.
+template <int KIND, bool TAIL>
+__device__ __forceinline__ void channel_loop(float2 (&sacc)[WCH], float2& qe, float2& qo,
+                                             const uint32_t* __restrict__ tw, const int* sb,
+                                             const float* buf, int c_begin, int c_end, int la, int lb,
+                                             int valid) {
+  const uint32_t* wp = tw + (size_t)c_begin * TILE;
+  uint32_t wa = __ldg(wp + la), wb = __ldg(wp + lb);
+  for (int c = c_begin; c < c_end; ++c) {
+    const uint32_t ca = wa, cw = wb;
+    wp += TILE;
+    if (c + 1 < c_end) {
+      wa = __ldg(wp + la);
+      wb = __ldg(wp + lb);
+    }
+    const float2 f1 = __fadd2_rn(make_float2(one_plus_f1(ca), one_plus_f1(cw)), make_float2(-1.f, -1.f));
+    const float2 f0 = __ffma2_rn(f1, make_float2(-1.f, -1.f), make_float2(1.f, 1.f));
+    const float* base = buf + sb[c];
+    const float* ya = base + (ca >> 23);
+    const float* yb = base + (cw >> 23);
+    auto load = [&](int k) { return make_float2(ya[k], yb[k]); };
+    accumulate_channel<KIND, TAIL>(sacc, qe, qo, f0, f1, load, valid);
+  }
+}
+
 // ----------------------------------------------------------------------------
 // K1: staged fractional gather + fused DAS/DMAS window accumulation
 // ----------------------------------------------------------------------------
-template <int KIND>
-__global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
+template <int KIND, int MINB>
+__global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -370,6 +411,7 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
   int* clo = reinterpret_cast<int*>(smem + L.lo);
   int* calloc_ = reinterpret_cast<int*>(smem + L.alloc);
   int* coff = reinterpret_cast<int*>(smem + L.off);
+  int* sb = reinterpret_cast<int*>(smem + L.sb);
   int* misc = reinterpret_cast<int*>(smem + L.misc);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.mbar);
   float* stage = reinterpret_cast<float*>(smem + L.stage);
@@ -393,8 +435,10 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
     calloc_[c] = (sp.y - sp.x + WCH + 8 + 3) & ~3;
   }
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    for (int b = 0; b < NSTAGE; ++b) {
+      mbar_init(&mbar[b], 32);                  // full: the 32 lanes of the producer warp
+      mbar_init(&mbar[NSTAGE + b], TPB / 32);   // empty: one arrival per consumer warp
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -413,37 +457,51 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
     misc[1] = G > 0 ? (p.C + G - 1) / G : 0;
   }
   __syncthreads();
+  // smem slot of sample (k0 + q*WCH + lo_c) in channel c's span: the same for
+  // every chunk q because WCH % 4 == 0
+  for (int c = tid; c < p.C; c += TPB) sb[c] = coff[c] + ((p.k0 + clo[c]) & 3);
+  __syncthreads();
   const int G = misc[0];
   const int n_groups = misc[1];
   const int n_chunks = (p.W + WCH - 1) / WCH;
 
-  // Issue the bulk copies of step t into buffer (t & 1).  Warp 0 only.
+  // Producer (warp 0, all lanes): stage step t into ring slot t % NSTAGE once
+  // the consumers released the slot's previous use.  Zero-fills (spans past
+  // the record) are written before the lanes' arrivals on the full barrier,
+  // whose release/acquire makes them visible with the TMA bytes.
   auto issue = [&](int t) {
+    const int b = t % NSTAGE, use = t / NSTAGE;
+    if (use > 0) mbar_wait(&mbar[NSTAGE + b], (use - 1) & 1);
     const int g = t % n_groups;
     const int r = t / n_groups;
     const int q = r % n_chunks;
     const int s = scan_begin + r / n_chunks;
     const int c_begin = g * G, c_end = min(p.C, c_begin + G);
-    float* buf = stage + (t & 1) * p.cap;
+    float* buf = stage + b * p.cap;
     const float* scan_sig = p.sig + (size_t)s * (size_t)p.scan_stride;
     const int cb = p.k0 + q * WCH;
     uint32_t bytes_lane = 0;
     for (int c = c_begin + lane; c < c_end; c += 32) {
       const long long start4 = ((long long)cb + clo[c]) & ~3LL;
-      const long long n = min((long long)calloc_[c], max((long long)p.ld - start4, 0LL));
+      const int alloc = calloc_[c];
+      const long long n = min((long long)alloc, max((long long)p.ld - start4, 0LL));
       bytes_lane += (uint32_t)(n * 4);
+      float* dst = buf + coff[c];
+      for (long long j = max(n, 0LL); j < alloc; ++j) dst[j] = 0.f;  // past the record: zeros
     }
+    uint32_t bytes = bytes_lane;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bytes_lane += __shfl_xor_sync(0xffffffffu, bytes_lane, o);
-    if (lane == 0) mbar_arrive_expect_tx(&mbar[t & 1], bytes_lane);
+    for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+    if (lane == 0)
+      mbar_arrive_expect_tx(&mbar[b], bytes);
+    else
+      mbar_arrive(&mbar[b]);
     __syncwarp();
     for (int c = c_begin + lane; c < c_end; c += 32) {
       const long long start4 = ((long long)cb + clo[c]) & ~3LL;
-      const int alloc = calloc_[c];
-      const long long n = min((long long)alloc, max((long long)p.ld - start4, 0LL));
-      float* dst = buf + coff[c];
-      if (n > 0) bulk_g2s(dst, scan_sig + (size_t)c * p.ld + start4, (uint32_t)(n * 4), &mbar[t & 1]);
-      for (long long j = max(n, 0LL); j < alloc; ++j) dst[j] = 0.f;  // past the record: zeros
+      const long long n = min((long long)calloc_[c], max((long long)p.ld - start4, 0LL));
+      if (n > 0)
+        bulk_g2s(buf + coff[c], scan_sig + (size_t)c * p.ld + start4, (uint32_t)(n * 4), &mbar[b]);
     }
   };
 
@@ -453,8 +511,8 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
   float2 qe = make_float2(0.f, 0.f), qo = make_float2(0.f, 0.f);
   double eS_a = 0.0, eS_b = 0.0, eQ_a = 0.0, eQ_b = 0.0;
 
-  if (G > 0 && warp == 0) issue(0);
-  __syncthreads();  // thread zero-fills of step 0 are not tracked by the mbarrier
+  if (G > 0 && warp == 0)
+    for (int t = 0; t < NSTAGE - 1 && t < nsteps; ++t) issue(t);
 
   for (int t = 0; t < nsteps; ++t) {
     const int g = G > 0 ? t % n_groups : 0;
@@ -464,10 +522,7 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
     const int valid = min(WCH, p.W - q * WCH);
     const int cb = p.k0 + q * WCH;
 
-    if (G > 0) {
-      if (warp == 0 && t + 1 < nsteps) issue(t + 1);
-      mbar_wait(&mbar[t & 1], (t >> 1) & 1);
-    }
+    if (G > 0) mbar_wait(&mbar[t % NSTAGE], (t / NSTAGE) & 1);
     if (g == 0) {
 #pragma unroll
       for (int k = 0; k < WCH; ++k) sacc[k] = make_float2(0.f, 0.f);
@@ -476,29 +531,15 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
     }
     const int c_begin = G > 0 ? g * G : 0;
     const int c_end = G > 0 ? min(p.C, c_begin + G) : p.C;
-    const float* buf = stage + (t & 1) * p.cap;
+    const float* buf = stage + (t % NSTAGE) * p.cap;
     const float* scan_sig = p.sig + (size_t)s * (size_t)p.scan_stride;
 
     if (G > 0) {
       // fast path: packed delay words (L2-resident table), samples from smem
-      uint32_t wa = __ldg(tw + (size_t)c_begin * TILE + la), wb = __ldg(tw + (size_t)c_begin * TILE + lb);
-      for (int c = c_begin; c < c_end; ++c) {
-        const uint32_t ca = wa, cbw = wb;
-        if (c + 1 < c_end) {
-          wa = __ldg(tw + (size_t)(c + 1) * TILE + la);
-          wb = __ldg(tw + (size_t)(c + 1) * TILE + lb);
-        }
-        const float2 f1 = make_float2(weight_f1(ca), weight_f1(cbw));
-        const float2 f0 = __ffma2_rn(f1, make_float2(-1.f, -1.f), make_float2(1.f, 1.f));
-        const int sbase = coff[c] + ((cb + clo[c]) & 3);  // smem slot of sample cb + lo_c
-        const float* ya = buf + sbase + (int)(ca >> 23);
-        const float* yb = buf + sbase + (int)(cbw >> 23);
-        auto load = [&](int k) { return make_float2(ya[k], yb[k]); };
-        if (valid == WCH)
-          accumulate_channel<KIND, false>(sacc, qe, qo, f0, f1, load, valid);
-        else
-          accumulate_channel<KIND, true>(sacc, qe, qo, f0, f1, load, valid);
-      }
+      if (valid == WCH)
+        channel_loop<KIND, false>(sacc, qe, qo, tw, sb, buf, c_begin, c_end, la, lb, valid);
+      else
+        channel_loop<KIND, true>(sacc, qe, qo, tw, sb, buf, c_begin, c_end, la, lb, valid);
     } else {
       // L1/L2 gather path (mode 1 or a tile whose delay spread exceeds the table):
       // same weights, loads straight from global with a zero tail.
@@ -585,7 +626,11 @@ __global__ void __launch_bounds__(TPB, 3) energy_kernel(const EnergyParams p) {
         eS_a = eS_b = eQ_a = eQ_b = 0.0;
       }
     }
-    if (G > 0) __syncthreads();
+    if (G > 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mbar[NSTAGE + t % NSTAGE]);  // this warp is done with the slot
+      if (warp == 0 && t + NSTAGE - 1 < nsteps) issue(t + NSTAGE - 1);
+    }
   }
 }
 // ----------------------------------------------------------------------------
@@ -1236,8 +1281,18 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
   dim3 grid((unsigned)tiles, (n_scans + p.scans_per_cta - 1) / p.scans_per_cta);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int kind = out_das && out_dmas ? KIND_BOTH : (out_das ? KIND_DAS : KIND_DMAS);
-  void (*fn)(EnergyParams) = kind == KIND_DAS ? energy_kernel<KIND_DAS>
-                             : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS> : energy_kernel<KIND_BOTH>);
+  // MWB_MINB=4 selects the 4-CTA/SM (<=128 registers) build of the kernel
+  static const int minb = [] {
+    const char* e = getenv("MWB_MINB");
+    return (e && atoi(e) == 4) ? 4 : 3;
+  }();
+  void (*fn)(EnergyParams);
+  if (minb == 4)
+    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 4>
+         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 4> : energy_kernel<KIND_BOTH, 4>);
+  else
+    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 3>
+         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 3> : energy_kernel<KIND_BOTH, 3>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   fn<<<grid, TPB, L.total, st>>>(p);
