@@ -18,6 +18,8 @@
  *                             + the skip filter of image(), beamform.py:309-315
  *                             + cell centres, beamform.py:321-323
  *   mwb_select_roi         <- pkg/src/mwbeam/coarse2fine.py:169-256 select_roi
+ *   mwb_enumerate_volume, mwb_select_roi_volume: the same for 3-D voxel grids
+ *                             (BASELINE configs[4]; no reference counterpart)
  *   mwb_argmax_dense       <- pkg/src/mwbeam/beamform.py:101-104  EnergyMap.argmax_cell
  *                             (also fused into mwb_energies through `argmax_key`)
  */
@@ -54,25 +56,30 @@ extern "C" {
 #define MWB_TERM_OVERFLOW (-2)      /* more than MWB_MAX_ITERS iterations */
 
 #define MWB_MAX_ITERS 64
+#define MWB_MAX_CHILDREN 8
+
+/* Regions are inclusive cell boxes {x0, y0, z0, x1, y1, z1} (z0 = z1 = 0 for
+ * 2-D grids).  Dense slots are (ix * ny + iy) * nz + iz (ix * ny + iy in 2-D). */
 
 /* one select_roi iteration (reference IterationRecord, coarse2fine.py:127-152).
- * Regions are inclusive cell bounds {x0, y0, x1, y1}. has_stats: 0 = None
- * (empty quadrant), 1 = {"mu","var"} (first iteration), 2 = full metric parts. */
+ * n_children is 4 (2-D quadrants, reference order) or 8 (3-D octants, index =
+ * xhigh + 2*yhigh + 4*zhigh).  has_stats: 0 = None (empty child), 1 =
+ * {"mu","var"} (first iteration), 2 = full metric parts. */
 typedef struct mwb_iter_record {
   int32_t iteration;
-  int32_t quadrant_counts[4];
+  int32_t n_children;
+  int32_t counts[MWB_MAX_CHILDREN];
   int32_t selected;
   int32_t satisfied;
-  int32_t has_stats[4];
-  int32_t clamped[4];
-  int32_t selected_region[4];
-  int32_t expanded_region[4];
-  int32_t _pad;
-  double scores[4];
-  double mu[4];
-  double var[4];
-  double delta_raw[4];
-  double delta[4];
+  int32_t has_stats[MWB_MAX_CHILDREN];
+  int32_t clamped[MWB_MAX_CHILDREN];
+  int32_t selected_region[6];
+  int32_t expanded_region[6];
+  double scores[MWB_MAX_CHILDREN];
+  double mu[MWB_MAX_CHILDREN];
+  double var[MWB_MAX_CHILDREN];
+  double delta_raw[MWB_MAX_CHILDREN];
+  double delta[MWB_MAX_CHILDREN];
   double w;
   double b;
 } mwb_iter_record_t;
@@ -81,8 +88,7 @@ typedef struct mwb_iter_record {
 typedef struct mwb_trace {
   int32_t termination;
   int32_t n_records;
-  int32_t final_region[4];
-  int32_t _pad[2];
+  int32_t final_region[6];
   mwb_iter_record_t records[MWB_MAX_ITERS];
 } mwb_trace_t;
 
@@ -140,16 +146,17 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
                  float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
                  uint64_t* key_dmas, int32_t* flags, int mode, void* stream);
 
-/* Workspace (bytes) for mwb_enumerate_lattice on an nx x ny grid at `stride`. */
+/* Workspace (bytes) for mwb_enumerate_lattice / mwb_enumerate_volume. */
 int64_t mwb_lattice_workspace_bytes(int nx, int ny, int stride);
+int64_t mwb_volume_workspace_bytes(int nx, int ny, int nz, int stride);
 
 /*
  * Enumerate the stride-`stride` lattice cells of region {x0,y0,x1,y1} (or of
- * the region stored at d_region when non-NULL), keep cells with mask[ix*ny+iy]
- * (mask may be NULL) and drop cells with ix%skip==0 && iy%skip==0 when
- * skip_stride > 0.  Writes fp64 cell centres origin + (i + 0.5) * res
- * (pts_xyz, z = 0), the dense slot ix*ny+iy (out_idx), the count (d_count)
- * and sets valid[slot] = 1.  Points come out in 16x16-lattice-tile order.
+ * the device region d_region, int32[6], when non-NULL), keep cells with
+ * mask[slot] (mask may be NULL) and drop cells whose indices are all
+ * multiples of skip_stride (> 0).  Writes fp64 cell centres origin +
+ * (i + 0.5) * res (pts_xyz, z = 0), the dense slot (out_idx), the count
+ * (d_count) and sets valid[slot] = 1.  Points come out in 16x16 lattice tiles.
  */
 int mwb_enumerate_lattice(double ox, double oy, double res, int nx, int ny, int x0, int y0,
                           int x1, int y1, const int32_t* d_region, int stride,
@@ -157,15 +164,28 @@ int mwb_enumerate_lattice(double ox, double oy, double res, int nx, int ny, int 
                           int32_t* out_idx, int32_t* d_count, uint8_t* valid, void* workspace,
                           void* stream);
 
+/* 3-D voxel variant: box is a HOST int32[6]; points in 8x8x4 voxel tiles;
+ * centres origin + (i + 0.5) * res on all three axes. */
+int mwb_enumerate_volume(double ox, double oy, double oz, double res, int nx, int ny, int nz,
+                         const int32_t* box, const int32_t* d_region, int stride,
+                         const uint8_t* mask, int skip_stride, double* pts_xyz,
+                         int32_t* out_idx, int32_t* d_count, uint8_t* valid, void* workspace,
+                         void* stream);
+
 /*
  * Device-resident iterative quadrant selection on a dense nx x ny energy map
  * whose valid cells lie on multiples of `lattice`.  Region {x0,y0,x1,y1} is
- * the breast region.  Writes the final region to d_region_out (int32[4]) and
+ * the breast region.  Writes the final region to d_region_out (int32[6]) and
  * the full trace to d_trace (mwb_trace_t).  One CTA, no host sync.
  */
 int mwb_select_roi(const float* dense, const uint8_t* valid, int nx, int ny, int lattice,
                    int x0, int y0, int x1, int y1, double frame_fraction, int n_min,
                    int32_t* d_region_out, mwb_trace_t* d_trace, void* stream);
+
+/* 3-D octant selection on an nx x ny x nz map (box: HOST int32[6]). */
+int mwb_select_roi_volume(const float* dense, const uint8_t* valid, int nx, int ny, int nz,
+                          int lattice, const int32_t* box, double frame_fraction, int n_min,
+                          int32_t* d_region_out, mwb_trace_t* d_trace, void* stream);
 
 /* argmax over a dense map (valid cells only); key as in mwb_energies. */
 int mwb_argmax_dense(const float* dense, const uint8_t* valid, int n, uint64_t* key,

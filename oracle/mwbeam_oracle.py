@@ -381,3 +381,143 @@ def cpu_threads() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# 3-D voxels (BASELINE configs[4]).  Energies come from the reference kernel
+# through the exact z-shift adapter (SURVEY.md §8c adapter 3): voxel (x, y, z)
+# = point (x, y) with every antenna shifted by -z (beamform.py:182-185 uses
+# dz = antenna z with points at z = 0).  The octant control flow has no
+# reference counterpart; it restates select_roi (coarse2fine.py:169-256) with
+# 8 children per box (index = xhigh + 2*yhigh + 4*zhigh).
+# ---------------------------------------------------------------------------
+def volume_energies(antennas, v, dt, signals, points3, kind, k0=None, w=None, interpolation="linear"):
+    ants = np.asarray(antennas, dtype=np.float64)
+    pts = np.asarray(points3, dtype=np.float64)
+    out = np.zeros(len(pts))
+    for z in np.unique(pts[:, 2]):
+        sel = pts[:, 2] == z
+        shifted = ants - np.array([0.0, 0.0, z])
+        if w is None:
+            out[sel] = multistatic_energies(shifted, v, dt, signals, pts[sel, :2], kind, interpolation)
+        else:
+            out[sel] = windowed_energies(shifted, v, dt, signals, pts[sel, :2], kind, k0, w, interpolation)
+    return out
+
+
+def octants(box):
+    lo, hi = box
+    if min(h - l + 1 for l, h in zip(lo, hi)) < 2:
+        return None
+    mids = [l + (h - l + 2) // 2 - 1 for l, h in zip(lo, hi)]
+    out = []
+    for k in range(8):
+        a = []
+        b = []
+        for ax in range(3):
+            if (k >> ax) & 1:
+                a.append(mids[ax] + 1)
+                b.append(hi[ax])
+            else:
+                a.append(lo[ax])
+                b.append(mids[ax])
+        out.append((tuple(a), tuple(b)))
+    return out
+
+
+def expand3(box, f, clip):
+    lo, hi = box
+    g = [math.ceil(f * (h - l + 1)) for l, h in zip(lo, hi)]
+    return (tuple(max(l - gg, c) for l, gg, c in zip(lo, g, clip[0])),
+            tuple(min(h + gg, c) for h, gg, c in zip(hi, g, clip[1])))
+
+
+def values_in3(entries, box):
+    lo, hi = box
+    return np.array([v for c, v in entries.items() if all(a <= x <= b for a, x, b in zip(lo, c, hi))])
+
+
+def select_roi_3d(entries, box, frame_fraction=0.25, n_min=4):
+    """select_roi (coarse2fine.py:169-256) with octants."""
+    trace = {"records": [], "termination": "", "warning": None}
+    vals = values_in3(entries, box)
+    if vals.size == 0:
+        raise ValueError("coarse map has no entries in the breast region")
+    if vals.max() == vals.min():
+        trace["termination"] = "degenerate"
+        return box, trace
+    sel, sel_vals = box, vals
+    sigma_prev_sq = float(vals.var())
+    prev_w = prev_b = None
+    it = 0
+    while True:
+        kids = octants(sel)
+        if kids is None:
+            trace["termination"] = "region-floor"
+            return sel, trace
+        scores, counts = [], []
+        for q in kids:
+            v = values_in3(entries, q)
+            counts.append(int(v.size))
+            if v.size == 0:
+                scores.append(-np.inf)
+            elif it == 0:
+                scores.append(float(v.var()))
+            else:
+                scores.append(metric_parts(v, sigma_prev_sq)[0])
+        selected = int(np.argmax(scores))
+        if counts[selected] < n_min:
+            trace["termination"] = "n-min"
+            return sel, trace
+        it += 1
+        expanded = expand3(kids[selected], frame_fraction, sel)
+        new_vals = values_in3(entries, expanded)
+        w, b = class_distances(sel_vals, new_vals)
+        satisfied = prev_w is None or (b > prev_b or w < prev_w)
+        trace["records"].append({"selected": selected, "scores": scores, "quadrant_counts": counts, "W": w, "B": b,
+                                 "selected_region": kids[selected], "expanded_region": expanded,
+                                 "satisfied": satisfied})
+        if not satisfied:
+            trace["termination"] = "distance-metrics"
+            return sel, trace
+        sigma_prev_sq = float(new_vals.var())
+        sel, sel_vals = expanded, new_vals
+        prev_w, prev_b = w, b
+
+
+def hemisphere_mask(origin, res, dims, radius):
+    nx, ny, nz = dims
+    px = origin[0] + (np.arange(nx) + 0.5) * res
+    py = origin[1] + (np.arange(ny) + 0.5) * res
+    pz = origin[2] + (np.arange(nz) + 0.5) * res
+    d2 = px[:, None, None] ** 2 + py[None, :, None] ** 2 + pz[None, None, :] ** 2
+    return (d2 <= radius**2) & (pz[None, None, :] >= 0.0)
+
+
+def run_framework_3d(antennas, v, dt, signals, kind, origin, res, dims, d, radius, frame_fraction=0.25, n_min=4,
+                     window=None):
+    """run_framework (coarse2fine.py:301-350) on voxels with octant selection."""
+    mask = hemisphere_mask(origin, res, dims, radius)
+    full = ((0, 0, 0), tuple(n - 1 for n in dims))
+
+    def evaluate(cells):
+        if not cells:
+            return {}
+        pts = np.array([[origin[a] + (c[a] + 0.5) * res for a in range(3)] for c in cells])
+        k0, w = window if window is not None else (None, None)
+        e = volume_energies(antennas, v, dt, signals, pts, kind, k0, w)
+        return dict(zip(cells, e.tolist()))
+
+    coarse_cells = [(ix, iy, iz) for ix in range(0, dims[0], d) for iy in range(0, dims[1], d)
+                    for iz in range(0, dims[2], d) if mask[ix, iy, iz]]
+    coarse = evaluate(coarse_cells)
+    final, trace = select_roi_3d(coarse, full, frame_fraction, n_min)
+    (x0, y0, z0), (x1, y1, z1) = final
+    fine_cells = [(ix, iy, iz) for ix in range(x0, x1 + 1) for iy in range(y0, y1 + 1) for iz in range(z0, z1 + 1)
+                  if mask[ix, iy, iz] and (ix, iy, iz) not in coarse]
+    fine = evaluate(fine_cells)
+    comp = dict(coarse)
+    comp.update(fine)
+    best = max(comp, key=lambda k: (comp[k], tuple(-x for x in k)))
+    return comp, {"final_region": final, "trace": trace, "argmax_cell": best, "coarse": len(coarse),
+                  "fine": len(fine)}

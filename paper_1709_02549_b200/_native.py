@@ -27,22 +27,25 @@ TERMINATION = {
 }
 
 
+MAX_CHILDREN = 8
+
+
 class IterRecord(C.Structure):
     _fields_ = [
         ("iteration", C.c_int32),
-        ("quadrant_counts", C.c_int32 * 4),
+        ("n_children", C.c_int32),
+        ("counts", C.c_int32 * MAX_CHILDREN),
         ("selected", C.c_int32),
         ("satisfied", C.c_int32),
-        ("has_stats", C.c_int32 * 4),
-        ("clamped", C.c_int32 * 4),
-        ("selected_region", C.c_int32 * 4),
-        ("expanded_region", C.c_int32 * 4),
-        ("_pad", C.c_int32),
-        ("scores", C.c_double * 4),
-        ("mu", C.c_double * 4),
-        ("var", C.c_double * 4),
-        ("delta_raw", C.c_double * 4),
-        ("delta", C.c_double * 4),
+        ("has_stats", C.c_int32 * MAX_CHILDREN),
+        ("clamped", C.c_int32 * MAX_CHILDREN),
+        ("selected_region", C.c_int32 * 6),
+        ("expanded_region", C.c_int32 * 6),
+        ("scores", C.c_double * MAX_CHILDREN),
+        ("mu", C.c_double * MAX_CHILDREN),
+        ("var", C.c_double * MAX_CHILDREN),
+        ("delta_raw", C.c_double * MAX_CHILDREN),
+        ("delta", C.c_double * MAX_CHILDREN),
         ("w", C.c_double),
         ("b", C.c_double),
     ]
@@ -52,8 +55,7 @@ class Trace(C.Structure):
     _fields_ = [
         ("termination", C.c_int32),
         ("n_records", C.c_int32),
-        ("final_region", C.c_int32 * 4),
-        ("_pad", C.c_int32 * 2),
+        ("final_region", C.c_int32 * 6),
         ("records", IterRecord * MAX_ITERS),
     ]
 
@@ -77,6 +79,12 @@ _SIGNATURES = {
         _I,
     ),
     "mwb_lattice_workspace_bytes": ([_I, _I, _I], _I64),
+    "mwb_volume_workspace_bytes": ([_I, _I, _I, _I], _I64),
+    "mwb_enumerate_volume": (
+        [_D, _D, _D, _D, _I, _I, _I, _P, _P, _I, _P, _I, _P, _P, _P, _P, _P, _P],
+        _I,
+    ),
+    "mwb_select_roi_volume": ([_P, _P, _I, _I, _I, _I, _P, _D, _I, _P, _P, _P], _I),
     "mwb_enumerate_lattice": (
         [_D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _P, _P, _P, _P, _P],
         _I,

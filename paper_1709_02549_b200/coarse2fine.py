@@ -231,10 +231,13 @@ class FrameworkReport:
 # trace decoding
 # ---------------------------------------------------------------------------
 def _region(b) -> Region:
-    return Region((int(b[0]), int(b[1])), (int(b[2]), int(b[3])))
+    """2-D Region from a device box {x0, y0, z0, x1, y1, z1}."""
+    return Region((int(b[0]), int(b[1])), (int(b[3]), int(b[4])))
 
 
-def decode_trace(raw: bytes) -> tuple[Region, MetricTrace, int]:
+def decode_trace(raw: bytes, region=_region) -> tuple[Region, MetricTrace, int]:
+    """Device trace -> (final region, MetricTrace, termination code); ``region``
+    converts a device box (2-D Region by default, volume.Box for 3-D)."""
     tr = nat.Trace.from_buffer_copy(raw)
     code = int(tr.termination)
     if code == -1:
@@ -248,7 +251,8 @@ def decode_trace(raw: bytes) -> tuple[Region, MetricTrace, int]:
     for i in range(int(tr.n_records)):
         r = tr.records[i]
         stats: list[dict | None] = []
-        for k in range(4):
+        nk = int(r.n_children)
+        for k in range(nk):
             h = int(r.has_stats[k])
             if h == 0:
                 stats.append(None)
@@ -264,17 +268,17 @@ def decode_trace(raw: bytes) -> tuple[Region, MetricTrace, int]:
                 })
         trace.records.append(IterationRecord(
             iteration=int(r.iteration),
-            quadrant_counts=[int(c) for c in r.quadrant_counts],
-            scores=[float(s) for s in r.scores],
+            quadrant_counts=[int(c) for c in r.counts[:nk]],
+            scores=[float(s) for s in r.scores[:nk]],
             stats=stats,
             selected=int(r.selected),
-            selected_region=_region(r.selected_region),
-            expanded_region=_region(r.expanded_region),
+            selected_region=region(r.selected_region),
+            expanded_region=region(r.expanded_region),
             w=float(r.w),
             b=float(r.b),
             satisfied=bool(r.satisfied),
         ))
-    return _region(tr.final_region), trace, code
+    return region(tr.final_region), trace, code
 
 
 def _launch_select(dense: torch.Tensor, valid: torch.Tensor, grid: ImagingGrid, lattice: int, breast: Region,
@@ -310,7 +314,7 @@ def select_roi(coarse: EnergyMap, breast_region: Region, cfg: FrameworkConfig = 
     dev = dv.device()
     dense_t = torch.from_numpy(np.ascontiguousarray(vals).reshape(-1)).to(dev)
     valid_t = torch.from_numpy(np.ascontiguousarray(valid).view(np.uint8).reshape(-1)).to(dev)
-    region_t = torch.zeros(4, dtype=torch.int32, device=dev)
+    region_t = torch.zeros(6, dtype=torch.int32, device=dev)
     trace_t = torch.zeros(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
     _launch_select(dense_t, valid_t, grid, lattice, breast_region, cfg, region_t, trace_t)
     final, trace, _ = decode_trace(trace_t.cpu().numpy().tobytes())
@@ -333,7 +337,7 @@ class _FrameworkRun:
         self.dense = torch.zeros(nx * ny, dtype=torch.float32, device=dev)
         self.valid = torch.zeros(nx * ny, dtype=torch.uint8, device=dev)
         self.status = _Status()
-        self.region_t = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.region_t = torch.zeros(6, dtype=torch.int32, device=dev)
         self.trace_t = torch.zeros(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
         self.events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 

@@ -634,12 +634,16 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
   }
 }
 // ----------------------------------------------------------------------------
-// lattice enumeration (beamform.py:268-280 + skip filter 309-315 + centres 321-323)
+// lattice enumeration (beamform.py:268-280 + skip filter 309-315 + centres
+// 321-323), generalised to 3-D voxel grids (nz > 1).  Regions on the device
+// are int32[6] {x0, y0, z0, x1, y1, z1}; the dense slot of a cell is
+// (ix * ny + iy) * nz + iz (= ix * ny + iy in 2-D).
 // ----------------------------------------------------------------------------
 struct LatticeParams {
-  double ox, oy, res;
-  int nx, ny;
-  int x0, y0, x1, y1;
+  double ox, oy, oz, res;
+  int nx, ny, nz;
+  int planar;  // 1: 2-D slice, point z = 0 exactly
+  int r[6];
   const int* d_region;
   int stride;
   const uint8_t* mask;
@@ -651,45 +655,50 @@ struct LatticeParams {
   int* tile_counts;
   int* tile_offsets;
   int n_tiles_max;
+  int tx, ty, tz;  // tile shape (tx*ty*tz == 256)
 };
 
 struct LatticeGeom {
-  int sx, sy, Lx, Ly, TX, TY;
+  int s[3], L[3], T[3];
 };
 
 __device__ __forceinline__ LatticeGeom lattice_geom(const LatticeParams& p) {
-  int x0 = p.x0, y0 = p.y0, x1 = p.x1, y1 = p.y1;
-  if (p.d_region) {
-    x0 = p.d_region[0]; y0 = p.d_region[1]; x1 = p.d_region[2]; y1 = p.d_region[3];
-  }
+  int r[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) r[i] = p.d_region ? p.d_region[i] : p.r[i];
   const int D = p.stride;
+  const int tdim[3] = {p.tx, p.ty, p.tz};
   LatticeGeom g;
-  g.sx = (x0 + D - 1) / D * D;
-  g.sy = (y0 + D - 1) / D * D;
-  g.Lx = g.sx <= x1 ? (x1 - g.sx) / D + 1 : 0;
-  g.Ly = g.sy <= y1 ? (y1 - g.sy) / D + 1 : 0;
-  g.TX = (g.Lx + 15) / 16;
-  g.TY = (g.Ly + 15) / 16;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    g.s[a] = (r[a] + D - 1) / D * D;
+    g.L[a] = g.s[a] <= r[3 + a] ? (r[3 + a] - g.s[a]) / D + 1 : 0;
+    g.T[a] = (g.L[a] + tdim[a] - 1) / tdim[a];
+  }
   return g;
 }
 
 __device__ __forceinline__ bool lattice_cell(const LatticeParams& p, const LatticeGeom& g, int tile,
-                                             int t, int& ix, int& iy) {
-  if (tile >= g.TX * g.TY) return false;
-  const int tx = tile / g.TY, ty = tile % g.TY;
-  const int lx = tx * 16 + (t >> 4), ly = ty * 16 + (t & 15);
-  if (lx >= g.Lx || ly >= g.Ly) return false;
-  ix = g.sx + lx * p.stride;
-  iy = g.sy + ly * p.stride;
-  if (p.mask && !p.mask[(size_t)ix * p.ny + iy]) return false;
-  if (p.skip > 0 && ix % p.skip == 0 && iy % p.skip == 0) return false;
+                                             int t, int& ix, int& iy, int& iz) {
+  if (tile >= g.T[0] * g.T[1] * g.T[2]) return false;
+  const int tzi = tile % g.T[2], tyi = (tile / g.T[2]) % g.T[1], txi = tile / (g.T[2] * g.T[1]);
+  const int lz = tzi * p.tz + t % p.tz;
+  const int ly = tyi * p.ty + (t / p.tz) % p.ty;
+  const int lx = txi * p.tx + t / (p.tz * p.ty);
+  if (lx >= g.L[0] || ly >= g.L[1] || lz >= g.L[2]) return false;
+  ix = g.s[0] + lx * p.stride;
+  iy = g.s[1] + ly * p.stride;
+  iz = g.s[2] + lz * p.stride;
+  const size_t slot = ((size_t)ix * p.ny + iy) * p.nz + iz;
+  if (p.mask && !p.mask[slot]) return false;
+  if (p.skip > 0 && ix % p.skip == 0 && iy % p.skip == 0 && iz % p.skip == 0) return false;
   return true;
 }
 
 __global__ void __launch_bounds__(256) lattice_count_kernel(const LatticeParams p) {
   const LatticeGeom g = lattice_geom(p);
-  int ix, iy;
-  const bool ok = lattice_cell(p, g, blockIdx.x, threadIdx.x, ix, iy);
+  int ix, iy, iz;
+  const bool ok = lattice_cell(p, g, blockIdx.x, threadIdx.x, ix, iy, iz);
   const int n = __syncthreads_count(ok);
   if (threadIdx.x == 0) p.tile_counts[blockIdx.x] = n;
 }
@@ -733,8 +742,8 @@ __global__ void __launch_bounds__(1024) lattice_scan_kernel(const LatticeParams 
 __global__ void __launch_bounds__(256) lattice_write_kernel(const LatticeParams p) {
   __shared__ int wsum[8];
   const LatticeGeom g = lattice_geom(p);
-  int ix = 0, iy = 0;
-  const bool ok = lattice_cell(p, g, blockIdx.x, threadIdx.x, ix, iy);
+  int ix = 0, iy = 0, iz = 0;
+  const bool ok = lattice_cell(p, g, blockIdx.x, threadIdx.x, ix, iy, iz);
   const unsigned bal = __ballot_sync(0xffffffffu, ok);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) wsum[warp] = __popc(bal);
@@ -744,46 +753,67 @@ __global__ void __launch_bounds__(256) lattice_write_kernel(const LatticeParams 
   if (!ok) return;
   const int rank = before + __popc(bal & ((1u << lane) - 1u));
   const int pos = p.tile_offsets[blockIdx.x] + rank;
-  const int slot = ix * p.ny + iy;
+  const size_t slot = ((size_t)ix * p.ny + iy) * p.nz + iz;
+  // cell centre origin + (i + 0.5) * res, no FMA contraction (beamform.py:321-322)
   p.pts[3 * (size_t)pos] = __dadd_rn(p.ox, __dmul_rn((double)ix + 0.5, p.res));
   p.pts[3 * (size_t)pos + 1] = __dadd_rn(p.oy, __dmul_rn((double)iy + 0.5, p.res));
-  p.pts[3 * (size_t)pos + 2] = 0.0;
-  p.out_idx[pos] = slot;
+  p.pts[3 * (size_t)pos + 2] = p.planar ? 0.0 : __dadd_rn(p.oz, __dmul_rn((double)iz + 0.5, p.res));
+  p.out_idx[pos] = (int)slot;
   p.valid[slot] = 1;
 }
 
 // ----------------------------------------------------------------------------
-// K2: device-resident select_roi (coarse2fine.py:169-256), one CTA
+// K2: device-resident select_roi (coarse2fine.py:169-256), one CTA.
+// 2-D grids split into the reference's 4 quadrants (geometry.py:225-242);
+// 3-D grids (nz > 1) into 8 octants with the same rules per axis.
 // ----------------------------------------------------------------------------
 constexpr int SEL_TPB = 256;
+constexpr int MAXCH = MWB_MAX_CHILDREN;
 
-struct Reg {
-  int x0, y0, x1, y1;
+struct Box {
+  int lo[3], hi[3];
 };
 
-__device__ __forceinline__ bool reg_contains(const Reg& r, int ix, int iy) {
-  return r.x0 <= ix && ix <= r.x1 && r.y0 <= iy && iy <= r.y1;
+__device__ __forceinline__ bool box_contains(const Box& r, int ix, int iy, int iz) {
+  return r.lo[0] <= ix && ix <= r.hi[0] && r.lo[1] <= iy && iy <= r.hi[1] && r.lo[2] <= iz &&
+         iz <= r.hi[2];
 }
 
-// Region.quadrants (geometry.py:225-242): low half gets the odd cell
-__device__ __forceinline__ bool quadrants(const Reg& r, Reg q[4]) {
-  const int w = r.x1 - r.x0 + 1, h = r.y1 - r.y0 + 1;
-  if (w < 2 || h < 2) return false;
-  const int xm = r.x0 + (w + 1) / 2 - 1;
-  const int ym = r.y0 + (h + 1) / 2 - 1;
-  q[0] = {r.x0, r.y0, xm, ym};
-  q[1] = {xm + 1, r.y0, r.x1, ym};
-  q[2] = {r.x0, ym + 1, xm, r.y1};
-  q[3] = {xm + 1, ym + 1, r.x1, r.y1};
-  return true;
+// children in the reference quadrant order: index = xh + 2*yh (+ 4*zh)
+__device__ __forceinline__ int split_box(const Box& r, int dims, Box q[MAXCH]) {
+  int mid[3];
+  for (int a = 0; a < dims; ++a) {
+    const int w = r.hi[a] - r.lo[a] + 1;
+    if (w < 2) return 0;
+    mid[a] = r.lo[a] + (w + 1) / 2 - 1;  // last cell of the low half
+  }
+  const int n = 1 << dims;
+  for (int k = 0; k < n; ++k) {
+    for (int a = 0; a < 3; ++a) {
+      if (a >= dims) {
+        q[k].lo[a] = r.lo[a];
+        q[k].hi[a] = r.hi[a];
+      } else if ((k >> a) & 1) {
+        q[k].lo[a] = mid[a] + 1;
+        q[k].hi[a] = r.hi[a];
+      } else {
+        q[k].lo[a] = r.lo[a];
+        q[k].hi[a] = mid[a];
+      }
+    }
+  }
+  return n;
 }
 
 // Region.expand (geometry.py:244-257): grow by ceil(f*side), clipped
-__device__ __forceinline__ Reg expand(const Reg& r, double f, const Reg& clip) {
-  const int px = (int)ceil(__dmul_rn(f, (double)(r.x1 - r.x0 + 1)));
-  const int py = (int)ceil(__dmul_rn(f, (double)(r.y1 - r.y0 + 1)));
-  return {max(r.x0 - px, clip.x0), max(r.y0 - py, clip.y0), min(r.x1 + px, clip.x1),
-          min(r.y1 + py, clip.y1)};
+__device__ __forceinline__ Box expand_box(const Box& r, double f, const Box& clip, int dims) {
+  Box e = r;
+  for (int a = 0; a < dims; ++a) {
+    const int g = (int)ceil(__dmul_rn(f, (double)(r.hi[a] - r.lo[a] + 1)));
+    e.lo[a] = max(r.lo[a] - g, clip.lo[a]);
+    e.hi[a] = min(r.hi[a] + g, clip.hi[a]);
+  }
+  return e;
 }
 
 template <int K>
@@ -799,7 +829,7 @@ __device__ void block_sum(double (&v)[K], double* red /* [8][K] */, double* outv
   __syncthreads();
   if (threadIdx.x < K) {
     double x = 0.0;
-    for (int w = 0; w < SEL_TPB / 32; ++w) x += red[w * K + threadIdx.x];
+    for (int w = 0; w < SEL_TPB / 32; ++w) x += red[w * K + threadIdx.x];  // fixed order
     outv[threadIdx.x] = x;
   }
   __syncthreads();
@@ -808,43 +838,53 @@ __device__ void block_sum(double (&v)[K], double* red /* [8][K] */, double* outv
 struct SelectParams {
   const float* dense;
   const uint8_t* valid;
-  int nx, ny, D;
-  Reg breast;
+  int nx, ny, nz, D, dims;
+  Box breast;
   double frac;
   int n_min;
   int* region_out;
   mwb_trace_t* trace;
 };
 
-// visit valid lattice cells of region r
+// visit valid lattice cells of box r
 template <class F>
-__device__ __forceinline__ void for_cells(const SelectParams& p, const Reg& r, F&& f) {
+__device__ __forceinline__ void for_cells(const SelectParams& p, const Box& r, F&& f) {
   const int D = p.D;
-  const int lx0 = (r.x0 + D - 1) / D, ly0 = (r.y0 + D - 1) / D;
-  const int lx1 = r.x1 / D, ly1 = r.y1 / D;
-  if (lx1 < lx0 || ly1 < ly0) return;
-  const int Lx = lx1 - lx0 + 1, Ly = ly1 - ly0 + 1;
-  const long long n = (long long)Lx * Ly;
+  int l0[3], L[3];
+  for (int a = 0; a < 3; ++a) {
+    l0[a] = (r.lo[a] + D - 1) / D;
+    const int l1 = r.hi[a] / D;
+    if (l1 < l0[a]) return;
+    L[a] = l1 - l0[a] + 1;
+  }
+  const long long n = (long long)L[0] * L[1] * L[2];
   for (long long i = threadIdx.x; i < n; i += SEL_TPB) {
-    const int ix = (lx0 + (int)(i / Ly)) * D, iy = (ly0 + (int)(i % Ly)) * D;
-    const size_t slot = (size_t)ix * p.ny + iy;
-    if (p.valid[slot]) f(ix, iy, (double)p.dense[slot]);
+    const int iz = (l0[2] + (int)(i % L[2])) * D;
+    const int iy = (l0[1] + (int)((i / L[2]) % L[1])) * D;
+    const int ix = (l0[0] + (int)(i / ((long long)L[2] * L[1]))) * D;
+    const size_t slot = ((size_t)ix * p.ny + iy) * p.nz + iz;
+    if (p.valid[slot]) f(ix, iy, iz, (double)p.dense[slot]);
   }
 }
 
+__device__ __forceinline__ void put_box(int32_t* dst, const Box& b) {
+  dst[0] = b.lo[0]; dst[1] = b.lo[1]; dst[2] = b.lo[2];
+  dst[3] = b.hi[0]; dst[4] = b.hi[1]; dst[5] = b.hi[2];
+}
+
 __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams p) {
-  __shared__ double red[8 * 16];
-  __shared__ double res[16];
-  __shared__ int ctl[8];
-  __shared__ Reg shared_regs[8];
+  __shared__ double red[8 * 2 * 2 * MAXCH];
+  __shared__ double res[2 * 2 * MAXCH];
+  __shared__ int ctl[2];
+  __shared__ Box next_sel;
   mwb_trace_t* tr = p.trace;
 
-  // breast-region stats: count, sum, min, max
+  // breast-region stats: count, sum, min, max (coarse2fine.py:186-199)
   double n_sel, sum_sel, m2_sel;
   {
     double acc[2] = {0.0, 0.0};
     double mn = INFINITY, mx = -INFINITY;
-    for_cells(p, p.breast, [&](int, int, double v) {
+    for_cells(p, p.breast, [&](int, int, int, double v) {
       acc[0] += 1.0;
       acc[1] += v;
       mn = fmin(mn, v);
@@ -853,7 +893,6 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     block_sum<2>(acc, red, res);
     n_sel = res[0];
     sum_sel = res[1];
-    // min/max via the same scratch
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -879,16 +918,14 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
       if (threadIdx.x == 0) {
         tr->termination = n_sel == 0.0 ? MWB_TERM_EMPTY : MWB_TERM_DEGENERATE;
         tr->n_records = 0;
-        tr->final_region[0] = p.region_out[0] = p.breast.x0;
-        tr->final_region[1] = p.region_out[1] = p.breast.y0;
-        tr->final_region[2] = p.region_out[2] = p.breast.x1;
-        tr->final_region[3] = p.region_out[3] = p.breast.y1;
+        put_box(tr->final_region, p.breast);
+        put_box(p.region_out, p.breast);
       }
       return;
     }
     const double mean = sum_sel / n_sel;
     double d2[1] = {0.0};
-    for_cells(p, p.breast, [&](int, int, double v) {
+    for_cells(p, p.breast, [&](int, int, int, double v) {
       const double d = v - mean;
       d2[0] += d * d;
     });
@@ -896,7 +933,7 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     m2_sel = res[0];
   }
 
-  Reg sel = p.breast;
+  Box sel = p.breast;
   double sigma_prev_sq = m2_sel / n_sel;
   double prev_w = 0.0, prev_b = 0.0;
   bool have_prev = false;
@@ -904,78 +941,76 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
   int term = MWB_TERM_NONE;
 
   while (term == MWB_TERM_NONE) {
-    Reg rg[8];
-    if (!quadrants(sel, rg)) {
+    Box rg[2 * MAXCH];
+    const int nk = split_box(sel, p.dims, rg);
+    if (nk == 0) {
       term = MWB_TERM_REGION_FLOOR;
       break;
     }
-    for (int k = 0; k < 4; ++k) rg[4 + k] = expand(rg[k], p.frac, sel);
+    for (int k = 0; k < nk; ++k) rg[nk + k] = expand_box(rg[k], p.frac, sel, p.dims);
+    const int nreg = 2 * nk;
 
-    // pass 1: count and sum for 4 quadrants + their 4 expansions
-    double a1[16];
+    // pass 1: count and sum of every child and of every child's expansion
+    double a1[4 * MAXCH];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) a1[k] = 0.0;
-    for_cells(p, sel, [&](int ix, int iy, double v) {
+    for (int k = 0; k < 4 * MAXCH; ++k) a1[k] = 0.0;
+    for_cells(p, sel, [&](int ix, int iy, int iz, double v) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (reg_contains(rg[k], ix, iy)) {
+      for (int k = 0; k < 2 * MAXCH; ++k)
+        if (k < nreg && box_contains(rg[k], ix, iy, iz)) {
           a1[2 * k] += 1.0;
           a1[2 * k + 1] += v;
         }
     });
-    block_sum<16>(a1, red, res);
-    double cnt[8], mean[8];
+    block_sum<4 * MAXCH>(a1, red, res);
+    double cnt[2 * MAXCH], mean[2 * MAXCH], sums[2 * MAXCH];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 2 * MAXCH; ++k) {
       cnt[k] = res[2 * k];
-      mean[k] = cnt[k] > 0.0 ? res[2 * k + 1] / cnt[k] : 0.0;
+      sums[k] = res[2 * k + 1];
+      mean[k] = cnt[k] > 0.0 ? sums[k] / cnt[k] : 0.0;
     }
-    double sums[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) sums[k] = res[2 * k + 1];
     __syncthreads();
     // pass 2: Σ (x - mean)^2 (two-pass variance, as numpy's var)
-    double a2[8];
+    double a2[2 * MAXCH];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a2[k] = 0.0;
-    for_cells(p, sel, [&](int ix, int iy, double v) {
+    for (int k = 0; k < 2 * MAXCH; ++k) a2[k] = 0.0;
+    for_cells(p, sel, [&](int ix, int iy, int iz, double v) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (reg_contains(rg[k], ix, iy)) {
+      for (int k = 0; k < 2 * MAXCH; ++k)
+        if (k < nreg && box_contains(rg[k], ix, iy, iz)) {
           const double d = v - mean[k];
           a2[k] += d * d;
         }
     });
-    block_sum<8>(a2, red, res);
-    double m2[8];
+    block_sum<2 * MAXCH>(a2, red, res);
+    double m2[2 * MAXCH];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) m2[k] = res[k];
+    for (int k = 0; k < 2 * MAXCH; ++k) m2[k] = res[k];
     __syncthreads();
 
     if (threadIdx.x == 0) {
-      const int rec_i = iteration;  // record index if accepted
+      const int rec_i = iteration;
       mwb_iter_record_t rec;
       memset(&rec, 0, sizeof(rec));
-      double scores[4];
-      for (int k = 0; k < 4; ++k) {
-        rec.quadrant_counts[k] = (int)cnt[k];
+      rec.n_children = nk;
+      double scores[MAXCH];
+      for (int k = 0; k < nk; ++k) {
+        rec.counts[k] = (int)cnt[k];
         if (cnt[k] == 0.0) {
-          scores[k] = -INFINITY;
+          scores[k] = -INFINITY;  // empty child (coarse2fine.py:215-217)
           rec.has_stats[k] = 0;
         } else {
           const double mu = mean[k], var = m2[k] / cnt[k];
           rec.mu[k] = mu;
           rec.var[k] = var;
-          if (iteration == 0) {
+          if (iteration == 0) {  // first iteration scores by variance (218-220)
             scores[k] = var;
             rec.has_stats[k] = 1;
-          } else {
+          } else {  // Eq. (5) (_metric_parts, 67-91)
             rec.has_stats[k] = 2;
             if (var == 0.0) {
               scores[k] = mu;
-              rec.delta_raw[k] = 0.0;
-              rec.delta[k] = 0.0;
-              rec.clamped[k] = 0;
             } else {
               const double dr = __ddiv_rn(__dsub_rn(var, sigma_prev_sq), var);
               const double dl = fmin(fmax(dr, 0.0), 1.0);
@@ -988,38 +1023,36 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
         }
         rec.scores[k] = scores[k];
       }
-      int selq = 0;
-      for (int k = 1; k < 4; ++k)
+      int selq = 0;  // np.argmax: first maximum
+      for (int k = 1; k < nk; ++k)
         if (scores[k] > scores[selq]) selq = k;
-      if (rec.quadrant_counts[selq] < p.n_min) {
+      if (rec.counts[selq] < p.n_min) {
         ctl[0] = MWB_TERM_N_MIN;
       } else {
-        const int e = 4 + selq;
+        const int e = nk + selq;
         const double n_e = cnt[e], sum_e = sums[e], m2_e = m2[e];
+        // W, B of the previous vs the new selection (class_distances, 94-109)
         const double w = __dadd_rn(m2_sel, m2_e);
         const double ma = sum_sel / n_sel, mb = sum_e / n_e;
         const double grand = __ddiv_rn(__dadd_rn(sum_sel, sum_e), __dadd_rn(n_sel, n_e));
         const double da = __dsub_rn(ma, grand), db = __dsub_rn(mb, grand);
         const double b = __dadd_rn(__dmul_rn(n_sel, __dmul_rn(da, da)), __dmul_rn(n_e, __dmul_rn(db, db)));
-        const bool satisfied = !have_prev || (b > prev_b || w < prev_w);
+        const bool satisfied = !have_prev || (b > prev_b || w < prev_w);  // OR (235)
         rec.iteration = iteration + 1;
         rec.selected = selq;
         rec.satisfied = satisfied;
-        rec.selected_region[0] = rg[selq].x0; rec.selected_region[1] = rg[selq].y0;
-        rec.selected_region[2] = rg[selq].x1; rec.selected_region[3] = rg[selq].y1;
-        rec.expanded_region[0] = rg[e].x0; rec.expanded_region[1] = rg[e].y0;
-        rec.expanded_region[2] = rg[e].x1; rec.expanded_region[3] = rg[e].y1;
+        put_box(rec.selected_region, rg[selq]);
+        put_box(rec.expanded_region, rg[e]);
         rec.w = w;
         rec.b = b;
         if (rec_i < MWB_MAX_ITERS) tr->records[rec_i] = rec;
         ctl[0] = rec_i >= MWB_MAX_ITERS ? MWB_TERM_OVERFLOW : (satisfied ? MWB_TERM_NONE : MWB_TERM_DISTANCE);
-        ctl[1] = selq;
         red[0] = w;
         red[1] = b;
         red[2] = n_e;
         red[3] = sum_e;
         red[4] = m2_e;
-        shared_regs[0] = rg[e];
+        next_sel = rg[e];
       }
     }
     __syncthreads();
@@ -1027,7 +1060,6 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     if (term == MWB_TERM_N_MIN) break;
     iteration += 1;
     if (term != MWB_TERM_NONE) break;
-    // accept the expanded selection
     prev_w = red[0];
     prev_b = red[1];
     have_prev = true;
@@ -1035,19 +1067,16 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     sum_sel = red[3];
     m2_sel = red[4];
     sigma_prev_sq = m2_sel / n_sel;
-    sel = shared_regs[0];
+    sel = next_sel;
     __syncthreads();
   }
   if (threadIdx.x == 0) {
     tr->termination = term;
     tr->n_records = min(iteration, MWB_MAX_ITERS);
-    tr->final_region[0] = p.region_out[0] = sel.x0;
-    tr->final_region[1] = p.region_out[1] = sel.y0;
-    tr->final_region[2] = p.region_out[2] = sel.x1;
-    tr->final_region[3] = p.region_out[3] = sel.y1;
+    put_box(tr->final_region, sel);
+    put_box(p.region_out, sel);
   }
 }
-
 __global__ void argmax_dense_kernel(const float* dense, const uint8_t* valid, int n,
                                     unsigned long long* key) {
   unsigned long long best = 0ull;
@@ -1299,11 +1328,35 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
   return check_launch("energy_kernel");
 }
 
+static long long lattice_tiles(int nx, int ny, int nz, int stride, int tx, int ty, int tz) {
+  const long long Lx = (nx + stride - 1) / stride, Ly = (ny + stride - 1) / stride,
+                  Lz = (nz + stride - 1) / stride;
+  return ((Lx + tx - 1) / tx) * ((Ly + ty - 1) / ty) * ((Lz + tz - 1) / tz);
+}
+
 int64_t mwb_lattice_workspace_bytes(int nx, int ny, int stride) {
   if (nx < 1 || ny < 1 || stride < 1) return -1;
-  const long long Lx = (nx + stride - 1) / stride, Ly = (ny + stride - 1) / stride;
-  const long long tiles = ((Lx + 15) / 16) * ((Ly + 15) / 16);
-  return 2 * tiles * (long long)sizeof(int) + 256;
+  return 2 * lattice_tiles(nx, ny, 1, stride, 16, 16, 1) * (long long)sizeof(int) + 256;
+}
+
+int64_t mwb_volume_workspace_bytes(int nx, int ny, int nz, int stride) {
+  if (nx < 1 || ny < 1 || nz < 1 || stride < 1) return -1;
+  return 2 * lattice_tiles(nx, ny, nz, stride, 8, 8, 4) * (long long)sizeof(int) + 256;
+}
+
+static int enumerate_common(LatticeParams& p, int tx, int ty, int tz, void* workspace, void* stream) {
+  const long long tiles = lattice_tiles(p.nx, p.ny, p.nz, p.stride, tx, ty, tz);
+  p.tx = tx;
+  p.ty = ty;
+  p.tz = tz;
+  p.n_tiles_max = (int)tiles;
+  p.tile_counts = reinterpret_cast<int*>(workspace);
+  p.tile_offsets = p.tile_counts + tiles;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  lattice_count_kernel<<<(unsigned)tiles, 256, 0, st>>>(p);
+  lattice_scan_kernel<<<1, 1024, 0, st>>>(p);
+  lattice_write_kernel<<<(unsigned)tiles, 256, 0, st>>>(p);
+  return check_launch("enumerate_lattice");
 }
 
 int mwb_enumerate_lattice(double ox, double oy, double res, int nx, int ny, int x0, int y0,
@@ -1317,9 +1370,10 @@ int mwb_enumerate_lattice(double ox, double oy, double res, int nx, int ny, int 
   if (!pts_xyz || !out_idx || !d_count || !valid || !workspace)
     return set_err(MWB_EINVAL, "mwb_enumerate_lattice: null pointer");
   LatticeParams p;
-  p.ox = ox; p.oy = oy; p.res = res;
-  p.nx = nx; p.ny = ny;
-  p.x0 = x0; p.y0 = y0; p.x1 = x1; p.y1 = y1;
+  p.ox = ox; p.oy = oy; p.oz = 0.0; p.res = res;
+  p.nx = nx; p.ny = ny; p.nz = 1;
+  p.planar = 1;
+  p.r[0] = x0; p.r[1] = y0; p.r[2] = 0; p.r[3] = x1; p.r[4] = y1; p.r[5] = 0;
   p.d_region = d_region;
   p.stride = stride;
   p.mask = mask;
@@ -1328,17 +1382,42 @@ int mwb_enumerate_lattice(double ox, double oy, double res, int nx, int ny, int 
   p.out_idx = out_idx;
   p.d_count = d_count;
   p.valid = valid;
-  // upper bound on tiles: the lattice of the whole grid
-  const long long Lx = (nx + stride - 1) / stride, Ly = (ny + stride - 1) / stride;
-  const long long tiles = ((Lx + 15) / 16) * ((Ly + 15) / 16);
-  p.n_tiles_max = (int)tiles;
-  p.tile_counts = reinterpret_cast<int*>(workspace);
-  p.tile_offsets = p.tile_counts + tiles;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  lattice_count_kernel<<<(unsigned)tiles, 256, 0, st>>>(p);
-  lattice_scan_kernel<<<1, 1024, 0, st>>>(p);
-  lattice_write_kernel<<<(unsigned)tiles, 256, 0, st>>>(p);
-  return check_launch("enumerate_lattice");
+  return enumerate_common(p, 16, 16, 1, workspace, stream);
+}
+
+int mwb_enumerate_volume(double ox, double oy, double oz, double res, int nx, int ny, int nz,
+                         const int32_t* box, const int32_t* d_region, int stride,
+                         const uint8_t* mask, int skip_stride, double* pts_xyz,
+                         int32_t* out_idx, int32_t* d_count, uint8_t* valid, void* workspace,
+                         void* stream) {
+  if (nx < 1 || ny < 1 || nz < 1 || stride < 1) return set_err(MWB_EINVAL, "mwb_enumerate_volume: bad grid/stride");
+  if ((long long)nx * ny * nz > 0x7FFFFFFFLL) return set_err(MWB_ERANGE, "mwb_enumerate_volume: grid too large");
+  if (!box) return set_err(MWB_EINVAL, "mwb_enumerate_volume: null box");
+  const int dims[3] = {nx, ny, nz};
+  for (int a = 0; a < 3; ++a)
+    if (!d_region && (box[a] < 0 || box[3 + a] >= dims[a] || box[a] > box[3 + a]))
+      return set_err(MWB_EINVAL, "mwb_enumerate_volume: box outside the grid");
+  if (!pts_xyz || !out_idx || !d_count || !valid || !workspace)
+    return set_err(MWB_EINVAL, "mwb_enumerate_volume: null pointer");
+  LatticeParams p;
+  p.ox = ox; p.oy = oy; p.oz = oz; p.res = res;
+  p.nx = nx; p.ny = ny; p.nz = nz;
+  p.planar = 0;
+  for (int i = 0; i < 6; ++i) p.r[i] = box[i];
+  p.d_region = d_region;
+  p.stride = stride;
+  p.mask = mask;
+  p.skip = skip_stride;
+  p.pts = pts_xyz;
+  p.out_idx = out_idx;
+  p.d_count = d_count;
+  p.valid = valid;
+  return enumerate_common(p, 8, 8, 4, workspace, stream);
+}
+
+static int select_common(SelectParams& p, void* stream) {
+  select_roi_kernel<<<1, SEL_TPB, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  return check_launch("select_roi_kernel");
 }
 
 int mwb_select_roi(const float* dense, const uint8_t* valid, int nx, int ny, int lattice,
@@ -1355,14 +1434,42 @@ int mwb_select_roi(const float* dense, const uint8_t* valid, int nx, int ny, int
   p.valid = valid;
   p.nx = nx;
   p.ny = ny;
+  p.nz = 1;
   p.D = lattice;
-  p.breast = {x0, y0, x1, y1};
+  p.dims = 2;
+  p.breast = Box{{x0, y0, 0}, {x1, y1, 0}};
   p.frac = frame_fraction;
   p.n_min = n_min;
   p.region_out = d_region_out;
   p.trace = d_trace;
-  select_roi_kernel<<<1, SEL_TPB, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
-  return check_launch("select_roi_kernel");
+  return select_common(p, stream);
+}
+
+int mwb_select_roi_volume(const float* dense, const uint8_t* valid, int nx, int ny, int nz,
+                          int lattice, const int32_t* box, double frame_fraction, int n_min,
+                          int32_t* d_region_out, mwb_trace_t* d_trace, void* stream) {
+  if (nx < 1 || ny < 1 || nz < 1 || lattice < 1 || !box) return set_err(MWB_EINVAL, "mwb_select_roi_volume: bad grid");
+  const int dims[3] = {nx, ny, nz};
+  for (int a = 0; a < 3; ++a)
+    if (box[a] < 0 || box[3 + a] >= dims[a] || box[a] > box[3 + a])
+      return set_err(MWB_EINVAL, "mwb_select_roi_volume: box outside the grid");
+  if (!(frame_fraction >= 0.0 && frame_fraction < 1.0) || n_min < 1)
+    return set_err(MWB_EINVAL, "mwb_select_roi_volume: bad frame_fraction / n_min");
+  if (!dense || !valid || !d_region_out || !d_trace) return set_err(MWB_EINVAL, "mwb_select_roi_volume: null pointer");
+  SelectParams p;
+  p.dense = dense;
+  p.valid = valid;
+  p.nx = nx;
+  p.ny = ny;
+  p.nz = nz;
+  p.D = lattice;
+  p.dims = 3;
+  p.breast = Box{{box[0], box[1], box[2]}, {box[3], box[4], box[5]}};
+  p.frac = frame_fraction;
+  p.n_min = n_min;
+  p.region_out = d_region_out;
+  p.trace = d_trace;
+  return select_common(p, stream);
 }
 
 int mwb_argmax_dense(const float* dense, const uint8_t* valid, int n, uint64_t* key, void* stream) {

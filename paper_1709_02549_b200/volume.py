@@ -1,0 +1,381 @@
+"""3-D voxel imaging and octant segmentation (BASELINE configs[4]).
+
+The reference images the z = 0 slice only (geometry.py:17-19; 3-D is a
+non-goal).  Its kernel already takes the antenna z into the
+distance, so a voxel (x, y, z) has exactly the energy the reference assigns
+to (x, y) with every antenna shifted by -z (SURVEY.md §8c adapter 3).  The
+same device kernels therefore serve volumes: points carry a real z, the
+lattice enumerator walks 8x8x4 voxel tiles, and the device selection splits
+boxes into octants (index = xhigh + 2*yhigh + 4*zhigh, low half gets the odd
+cell per axis, exactly Region.quadrants' rule, geometry.py:225-242) and
+scores them with the reference's Eq. (5) / W-B / n_min control flow
+(coarse2fine.py:169-256).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _native as nat
+from .beamform import EVAL_COUNTER, _check_interpolation, _kind_code, _Status, _window, build_table, launch_energies
+from .coarse2fine import FrameworkConfig, IterationRecord, MetricTrace, decimation_factor, decode_trace
+
+
+@dataclass(frozen=True)
+class Box:
+    """Inclusive voxel box."""
+
+    min_cell: tuple[int, int, int]
+    max_cell: tuple[int, int, int]
+
+    def __post_init__(self):
+        lo = tuple(int(v) for v in self.min_cell)
+        hi = tuple(int(v) for v in self.max_cell)
+        if len(lo) != 3 or len(hi) != 3 or any(a > b for a, b in zip(lo, hi)):
+            raise ValueError("box bounds must be 3-vectors with min_cell <= max_cell")
+        object.__setattr__(self, "min_cell", lo)
+        object.__setattr__(self, "max_cell", hi)
+
+    @property
+    def shape(self) -> tuple[int, int, int]:
+        return tuple(b - a + 1 for a, b in zip(self.min_cell, self.max_cell))
+
+    @property
+    def n_cells(self) -> int:
+        w, h, d = self.shape
+        return w * h * d
+
+    def bounds(self) -> tuple[int, ...]:
+        return (*self.min_cell, *self.max_cell)
+
+    def contains_cell(self, ix: int, iy: int, iz: int) -> bool:
+        return all(a <= v <= b for a, v, b in zip(self.min_cell, (ix, iy, iz), self.max_cell))
+
+    def contains_box(self, other: "Box") -> bool:
+        return self.contains_cell(*other.min_cell) and self.contains_cell(*other.max_cell)
+
+    def intersection(self, other: "Box") -> "Box | None":
+        lo = tuple(max(a, b) for a, b in zip(self.min_cell, other.min_cell))
+        hi = tuple(min(a, b) for a, b in zip(self.max_cell, other.max_cell))
+        if any(a > b for a, b in zip(lo, hi)):
+            return None
+        return Box(lo, hi)
+
+    def octants(self) -> "list[Box] | None":
+        """8 disjoint children, index = xhigh + 2*yhigh + 4*zhigh; None when a side is 1."""
+        if min(self.shape) < 2:
+            return None
+        halves = []
+        for a, (lo, hi) in enumerate(zip(self.min_cell, self.max_cell)):
+            mid = lo + (hi - lo + 2) // 2 - 1
+            halves.append(((lo, mid), (mid + 1, hi)))
+        out = []
+        for k in range(8):
+            sel = [halves[a][(k >> a) & 1] for a in range(3)]
+            out.append(Box(tuple(s[0] for s in sel), tuple(s[1] for s in sel)))
+        return out
+
+    def expand(self, fraction: float, clip_to: "Box") -> "Box":
+        grow = [math.ceil(fraction * s) for s in self.shape]
+        lo = tuple(max(a - g, c) for a, g, c in zip(self.min_cell, grow, clip_to.min_cell))
+        hi = tuple(min(b + g, c) for b, g, c in zip(self.max_cell, grow, clip_to.max_cell))
+        return Box(lo, hi)
+
+    def to_dict(self) -> dict:
+        return {"min_cell": list(self.min_cell), "max_cell": list(self.max_cell)}
+
+
+def _box(b) -> Box:
+    return Box((int(b[0]), int(b[1]), int(b[2])), (int(b[3]), int(b[4]), int(b[5])))
+
+
+@dataclass(frozen=True)
+class VolumeGrid:
+    """Uniform voxel grid; voxel (ix, iy, iz) is centred at origin + (i + 0.5) * res."""
+
+    origin: tuple[float, float, float]
+    extent: tuple[float, float, float]
+    resolution: float
+    dims: tuple[int, int, int] = field(init=False)
+
+    def __post_init__(self):
+        if not self.resolution > 0:
+            raise ValueError("resolution must be > 0")
+        o = tuple(float(v) for v in self.origin)
+        e = tuple(float(v) for v in self.extent)
+        if len(o) != 3 or len(e) != 3 or min(e) <= 0:
+            raise ValueError("origin and extent must be 3-vectors with a positive extent")
+        res = float(self.resolution)
+        object.__setattr__(self, "origin", o)
+        object.__setattr__(self, "extent", e)
+        object.__setattr__(self, "resolution", res)
+        object.__setattr__(self, "dims", tuple(max(1, math.ceil(round(x / res, 9))) for x in e))
+
+    def cell_center(self, ix: int, iy: int, iz: int) -> tuple[float, float, float]:
+        r = self.resolution
+        return (self.origin[0] + (ix + 0.5) * r, self.origin[1] + (iy + 0.5) * r, self.origin[2] + (iz + 0.5) * r)
+
+    def point_to_cell(self, x: float, y: float, z: float) -> tuple[int, int, int]:
+        r = self.resolution
+        return tuple(int(math.floor((v - o) / r)) for v, o in zip((x, y, z), self.origin))
+
+    def full_box(self) -> Box:
+        nx, ny, nz = self.dims
+        return Box((0, 0, 0), (nx - 1, ny - 1, nz - 1))
+
+
+def hemisphere_mask(grid: VolumeGrid, radius: float, center=(0.0, 0.0, 0.0)) -> np.ndarray:
+    """Voxels whose centres lie in the hemisphere |r - c| <= radius, z >= c_z
+    (the phantom of configs[4]; the 3-D analogue of breast_mask)."""
+    nx, ny, nz = grid.dims
+    r = grid.resolution
+    px = grid.origin[0] + (np.arange(nx) + 0.5) * r - center[0]
+    py = grid.origin[1] + (np.arange(ny) + 0.5) * r - center[1]
+    pz = grid.origin[2] + (np.arange(nz) + 0.5) * r - center[2]
+    d2 = px[:, None, None] ** 2 + py[None, :, None] ** 2 + pz[None, None, :] ** 2
+    return (d2 <= radius**2) & (pz[None, None, :] >= 0.0)
+
+
+class VolumeMap:
+    """Dense-backed voxel energy map (the 3-D counterpart of EnergyMap)."""
+
+    def __init__(self, grid: VolumeGrid, values: np.ndarray, valid: np.ndarray, stride: int = 1, roi: Box | None = None):
+        self.grid, self.stride, self.roi = grid, stride, roi
+        self.values = values
+        self.valid = valid
+        if valid.any() and not np.isfinite(values[valid]).all():
+            raise ValueError("energy map contains non-finite values")
+
+    def __len__(self) -> int:
+        return int(self.valid.sum())
+
+    @property
+    def entries(self) -> dict:
+        ix, iy, iz = np.nonzero(self.valid)
+        vals = self.values[ix, iy, iz].astype(np.float64)
+        return dict(zip(zip(ix.tolist(), iy.tolist(), iz.tolist()), vals.tolist()))
+
+    def argmax_cell(self) -> tuple[int, int, int]:
+        """Max energy, ties to the lowest (ix, iy, iz)."""
+        if not self.valid.any():
+            raise ValueError("energy map is empty")
+        score = np.where(self.valid, self.values.astype(np.float64), -np.inf)
+        return tuple(int(v) for v in np.unravel_index(int(np.argmax(score)), score.shape))
+
+    def argmax_position(self) -> tuple[float, float, float]:
+        return self.grid.cell_center(*self.argmax_cell())
+
+    def values_in(self, box: Box) -> np.ndarray:
+        (x0, y0, z0), (x1, y1, z1) = box.min_cell, box.max_cell
+        v = self.valid[x0 : x1 + 1, y0 : y1 + 1, z0 : z1 + 1]
+        return self.values[x0 : x1 + 1, y0 : y1 + 1, z0 : z1 + 1][v].astype(np.float64)
+
+
+def _volume_pass(scan, grid: VolumeGrid, box: Box, stride: int, mask_t, skip_stride: int, codes: tuple, interp: int,
+                 k0: int, w: int, dense: dict, valid: torch.Tensor, status: _Status, count_slot: int,
+                 d_region: torch.Tensor | None = None, mode: int = 0) -> None:
+    nx, ny, nz = grid.dims
+    p_max = math.prod((n + stride - 1) // stride for n in grid.dims)
+    dev = dv.device()
+    pts = torch.empty((p_max, 3), dtype=torch.float64, device=dev)
+    oidx = torch.empty(p_max, dtype=torch.int32, device=dev)
+    ws = torch.empty(int(nat.load().mwb_volume_workspace_bytes(nx, ny, nz, stride)), dtype=torch.uint8, device=dev)
+    import ctypes
+
+    host_box = (ctypes.c_int32 * 6)(*box.bounds())
+    count_ptr = status.count_ptr(count_slot)
+    nat.call("mwb_enumerate_volume", grid.origin[0], grid.origin[1], grid.origin[2], grid.resolution, nx, ny, nz,
+             ctypes.addressof(host_box), nat.ptr(d_region), stride, nat.ptr(mask_t), skip_stride, pts.data_ptr(),
+             oidx.data_ptr(), count_ptr, valid.data_ptr(), ws.data_ptr(), dv.stream_handle())
+    if w == 0:
+        return
+    table = build_table(scan, pts, p_max, interp, count_ptr)
+    launch_energies(scan, pts, p_max, table, interp, k0, w,
+                    dense.get(nat.MWB_DAS) if nat.MWB_DAS in codes else None,
+                    dense.get(nat.MWB_DMAS) if nat.MWB_DMAS in codes else None,
+                    0, oidx, count_ptr, status.key_ptr(0), status.key_ptr(1), status.flags_ptr, mode)
+
+
+def _upload_mask3(mask, dims) -> torch.Tensor | None:
+    if mask is None:
+        return None
+    m = np.asarray(mask, dtype=bool)
+    if m.shape != tuple(dims):
+        raise ValueError(f"mask must have the grid's dims {tuple(dims)}, got {m.shape}")
+    return torch.from_numpy(np.ascontiguousarray(m).view(np.uint8).reshape(-1)).to(dv.device())
+
+
+def image_volume(ds, kinds, grid: VolumeGrid, box: Box | None = None, stride: int = 1, mask=None,
+                 interpolation: str = "linear", *, window=None, mode: str = "smem") -> dict:
+    """DAS and/or DMAS voxel maps of ``box`` at ``stride`` in one fused pass."""
+    _check_interpolation(interpolation)
+    if isinstance(kinds, str) or not hasattr(kinds, "__iter__"):
+        kinds = (kinds,)
+    codes = tuple(dict.fromkeys(_kind_code(k) for k in kinds))
+    if stride < 1:
+        raise ValueError("stride must be >= 1")
+    box = grid.full_box() if box is None else box
+    if not grid.full_box().contains_box(box):
+        raise ValueError("box lies outside the grid")
+    scan = dv.scan_for(ds)
+    k0, w = _window(scan.n_samples, window)
+    n = math.prod(grid.dims)
+    dev = dv.device()
+    dense = {c: torch.zeros(n, dtype=torch.float32, device=dev) for c in codes}
+    valid = torch.zeros(n, dtype=torch.uint8, device=dev)
+    status = _Status()
+    _volume_pass(scan, grid, box, stride, _upload_mask3(mask, grid.dims), 0, codes, nat.INTERP[interpolation], k0, w,
+                 dense, valid, status, 0, mode={"smem": 0, "gather": 1}[mode])
+    _, counts, flags = status.read()
+    if flags & 1:
+        raise ValueError("energy map contains non-finite values")
+    vmask = valid.view(*grid.dims).cpu().numpy().astype(bool)
+    out = {}
+    for c in codes:
+        EVAL_COUNTER.add(int(counts[0]))
+        out["das" if c == nat.MWB_DAS else "dmas"] = VolumeMap(grid, dense[c].view(*grid.dims).cpu().numpy(), vmask,
+                                                               stride)
+    return out
+
+
+@dataclass
+class VolumeReport:
+    decimation_factor: int
+    iterations: int
+    final_region: Box
+    coarse_points_evaluated: int
+    fine_points_evaluated: int
+    full_equivalent_points: int
+    reduction_ratio: float
+    elapsed: dict
+    trace: MetricTrace
+    argmax_cell: tuple[int, int, int]
+    argmax_position: tuple[float, float, float]
+
+    def to_dict(self) -> dict:
+        return {
+            "decimation_factor": self.decimation_factor,
+            "iterations": self.iterations,
+            "final_region": self.final_region.to_dict(),
+            "coarse_points_evaluated": self.coarse_points_evaluated,
+            "fine_points_evaluated": self.fine_points_evaluated,
+            "full_equivalent_points": self.full_equivalent_points,
+            "reduction_ratio": self.reduction_ratio,
+            "elapsed": self.elapsed,
+            "trace": self.trace.to_dict(),
+            "argmax_cell": list(self.argmax_cell),
+            "argmax_position": list(self.argmax_position),
+        }
+
+
+def select_roi_volume(coarse: VolumeMap, box: Box, cfg: FrameworkConfig = FrameworkConfig()) -> tuple[Box, MetricTrace]:
+    """Octant selection on a voxel map (device kernel)."""
+    grid = coarse.grid
+    nx, ny, nz = grid.dims
+    d = max(1, int(coarse.stride))
+    ix, iy, iz = np.nonzero(coarse.valid)
+    if not coarse.values_in(box).size:
+        raise ValueError("coarse map has no entries in the breast region")
+    lattice = d if (d > 1 and not ((ix % d).any() or (iy % d).any() or (iz % d).any())) else 1
+    dev = dv.device()
+    dense_t = torch.from_numpy(np.ascontiguousarray(coarse.values, dtype=np.float32).reshape(-1)).to(dev)
+    valid_t = torch.from_numpy(np.ascontiguousarray(coarse.valid).view(np.uint8).reshape(-1)).to(dev)
+    region_t = torch.zeros(6, dtype=torch.int32, device=dev)
+    trace_t = torch.zeros(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
+    _launch_select3(dense_t, valid_t, grid, lattice, box, cfg, region_t, trace_t)
+    final, trace, _ = decode_trace(trace_t.cpu().numpy().tobytes(), region=_box)
+    return final, trace
+
+
+def _launch_select3(dense_t, valid_t, grid, lattice, box, cfg, region_t, trace_t):
+    import ctypes
+
+    nx, ny, nz = grid.dims
+    host_box = (ctypes.c_int32 * 6)(*box.bounds())
+    nat.call("mwb_select_roi_volume", dense_t.data_ptr(), valid_t.data_ptr(), nx, ny, nz, lattice,
+             ctypes.addressof(host_box), float(cfg.frame_fraction), int(cfg.n_min), region_t.data_ptr(),
+             trace_t.data_ptr(), dv.stream_handle())
+
+
+def run_framework_volume(ds, kind, grid: VolumeGrid, mode, cfg: FrameworkConfig = FrameworkConfig(), *,
+                         mask=None, phantom_radius: float | None = None, interpolation: str = "linear",
+                         window=None) -> tuple[VolumeMap, VolumeReport]:
+    """Coarse voxel lattice -> device octant selection -> fine pass in the final
+    box -> composite (the configs[4] framework with octant splits).
+
+    The phantom mask is ``mask`` if given, else the hemisphere of
+    ``phantom_radius`` (default: the largest hemisphere inscribed in the grid).
+    """
+    _check_interpolation(interpolation)
+    d = decimation_factor(mode, grid.resolution)
+    if mask is None:
+        if phantom_radius is None:
+            phantom_radius = min(grid.extent[0], grid.extent[1]) / 2.0
+        mask = hemisphere_mask(grid, phantom_radius)
+    mask = np.asarray(mask, dtype=bool)
+    if not mask[::d, ::d, ::d].any():
+        raise ValueError("no coarse focal points inside the phantom mask")
+    kcode = _kind_code(kind)
+    scan = dv.scan_for(ds)
+    k0, w = _window(scan.n_samples, window)
+    interp = nat.INTERP[interpolation]
+    n = math.prod(grid.dims)
+    dev = dv.device()
+    dense = torch.zeros(n, dtype=torch.float32, device=dev)
+    valid = torch.zeros(n, dtype=torch.uint8, device=dev)
+    status = _Status()
+    region_t = torch.zeros(6, dtype=torch.int32, device=dev)
+    trace_t = torch.zeros(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
+    mask_t = _upload_mask3(mask, grid.dims)
+    full = grid.full_box()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record()
+    _volume_pass(scan, grid, full, d, mask_t, 0, (kcode,), interp, k0, w, {kcode: dense}, valid, status, 0)
+    ev[1].record()
+    _launch_select3(dense, valid, grid, d, full, cfg, region_t, trace_t)
+    ev[2].record()
+    _volume_pass(scan, grid, full, 1, mask_t, d, (kcode,), interp, k0, w, {kcode: dense}, valid, status, 1,
+                 d_region=region_t)
+    ev[3].record()
+    keys, counts, flags = status.read()
+    if flags & 1:
+        raise ValueError("energy map contains non-finite values")
+    final, trace, _ = decode_trace(trace_t.cpu().numpy().tobytes(), region=_box)
+    values = dense.view(*grid.dims).cpu().numpy()
+    vmask = valid.view(*grid.dims).cpu().numpy().astype(bool)
+    composite = VolumeMap(grid, values, vmask, stride=d, roi=final)
+    n_c, n_f = int(counts[0]), int(counts[1])
+    EVAL_COUNTER.add(n_c + n_f)
+    key = int(keys[0 if kcode == nat.MWB_DAS else 1])
+    _, ny, nz = grid.dims
+    if key:
+        slot = 0xFFFFFFFF - (key & 0xFFFFFFFF)
+        cell = (slot // (ny * nz), (slot // nz) % ny, slot % nz)
+    else:
+        cell = composite.argmax_cell()
+    t = [ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3, ev[2].elapsed_time(ev[3]) / 1e3]
+    full_eq = int(mask.sum())
+    report = VolumeReport(
+        decimation_factor=d, iterations=len(trace.records), final_region=final, coarse_points_evaluated=n_c,
+        fine_points_evaluated=n_f, full_equivalent_points=full_eq, reduction_ratio=full_eq / (n_c + n_f),
+        elapsed={"coarse": t[0], "select": t[1], "fine": t[2], "total": sum(t)}, trace=trace, argmax_cell=cell,
+        argmax_position=grid.cell_center(*cell))
+    return composite, report
+
+
+__all__ = [
+    "Box",
+    "IterationRecord",
+    "VolumeGrid",
+    "VolumeMap",
+    "VolumeReport",
+    "hemisphere_mask",
+    "image_volume",
+    "run_framework_volume",
+    "select_roi_volume",
+]

@@ -38,7 +38,7 @@ def test_binding_covers_header():
 
 def test_trace_layout_matches_c(lib):
     assert lib.mwb_trace_bytes() == _native.TRACE_BYTES
-    assert ctypes.sizeof(_native.IterRecord) == 272
+    assert ctypes.sizeof(_native.IterRecord) == 496
 
 
 def test_version(lib):

@@ -173,24 +173,26 @@ class TestTraceDecoding:
         tr = nat.Trace()
         tr.termination = 3
         tr.n_records = 1
-        tr.final_region[:] = [1, 2, 30, 40]
+        tr.final_region[:] = [1, 2, 0, 30, 40, 0]
         r = tr.records[0]
         r.iteration = 1
-        r.quadrant_counts[:] = [5, 0, 7, 9]
+        r.n_children = 4
+        r.counts[:4] = [5, 0, 7, 9]
         r.selected = 3
         r.satisfied = 1
-        r.has_stats[:] = [1, 0, 1, 1]
-        r.scores[:] = [1.5, -math.inf, 2.0, 4.0]
-        r.mu[:] = [1.0, 0.0, 2.0, 3.0]
-        r.var[:] = [1.5, 0.0, 2.0, 4.0]
-        r.selected_region[:] = [10, 10, 20, 20]
-        r.expanded_region[:] = [8, 8, 22, 22]
+        r.has_stats[:4] = [1, 0, 1, 1]
+        r.scores[:4] = [1.5, -math.inf, 2.0, 4.0]
+        r.mu[:4] = [1.0, 0.0, 2.0, 3.0]
+        r.var[:4] = [1.5, 0.0, 2.0, 4.0]
+        r.selected_region[:] = [10, 10, 0, 20, 20, 0]
+        r.expanded_region[:] = [8, 8, 0, 22, 22, 0]
         r.w, r.b = 3.25, 1.5
         final, trace, code = decode_trace(bytes(tr))
         assert code == 3 and trace.termination == "n-min" and final == mw.Region((1, 2), (30, 40))
         rec = trace.records[0]
         assert rec.stats[1] is None and rec.stats[0] == {"mu": 1.0, "var": 1.5}
         assert rec.scores[1] == -math.inf and rec.selected_region == mw.Region((10, 10), (20, 20))
+        assert len(rec.scores) == 4 and rec.quadrant_counts == [5, 0, 7, 9]
         json.dumps(trace.to_dict())
 
     def test_decode_errors(self):
