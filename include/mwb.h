@@ -92,6 +92,26 @@ typedef struct mwb_trace {
   mwb_iter_record_t records[MWB_MAX_ITERS];
 } mwb_trace_t;
 
+/* BASELINE configs[2] segmentation trace (no reference counterpart). */
+#define MWB_SEG_MAX_ITERS 32
+typedef struct mwb_seg_record {
+  int32_t iteration;
+  int32_t selected;        /* quadrant index, reference order */
+  int32_t parent[6];       /* region that was split */
+  int32_t selected_region[6];
+  double shift;            /* subtracted before max/mean (DMAS: iteration minimum) */
+  double score[4];         /* max / mean of the shifted sub-grid energies */
+  double emax[4];
+  double emean[4];
+} mwb_seg_record_t;
+
+typedef struct mwb_seg_trace {
+  int32_t n_records;
+  int32_t stopped;         /* 1 when the stop size was reached */
+  int32_t final_region[6];
+  mwb_seg_record_t records[MWB_SEG_MAX_ITERS];
+} mwb_seg_trace_t;
+
 const char* mwb_last_error(void);
 int mwb_version(void);
 /* sizeof(mwb_trace_t), for binding-layout checks */
@@ -186,6 +206,25 @@ int mwb_select_roi(const float* dense, const uint8_t* valid, int nx, int ny, int
 int mwb_select_roi_volume(const float* dense, const uint8_t* valid, int nx, int ny, int nz,
                           int lattice, const int32_t* box, double frame_fraction, int n_min,
                           int32_t* d_region_out, mwb_trace_t* d_trace, void* stream);
+
+/*
+ * BASELINE configs[2] segmentation: starting from region {x0,y0,x1,y1} of an
+ * nx x ny grid (origin, res), split into the 4 reference quadrants, image each
+ * on an n_sub x n_sub sub-grid spanning it (centres corner + (i + 0.5) * side /
+ * n_sub), score each by max/mean of its energies (DMAS energies are shifted by
+ * the iteration minimum so the ratio is defined), keep the argmax (ties to the
+ * lowest index) and repeat until the kept segment's larger side is <=
+ * stop_cells; at most max_iters iterations are enqueued (finished searches
+ * turn the remaining launches into no-ops, so nothing syncs with the host).
+ * The final segment goes to d_region_out (int32[6]); the first iteration's
+ * sub-grids form the (2 n_sub)^2 low-resolution image `lowres` (may be NULL).
+ */
+int64_t mwb_segment_workspace_bytes(int n_sub, int n_chan);
+int mwb_segment(const float* sig, int n_chan, int ld, int n_samples, const int32_t* chan_txrx,
+                const double* ant_xyz, int n_ant, double inv_scale, int interp, int k0, int window,
+                int kind, double ox, double oy, double res, int nx, int ny, int x0, int y0, int x1,
+                int y1, int n_sub, int stop_cells, int max_iters, int32_t* d_region_out,
+                float* lowres, mwb_seg_trace_t* d_trace, void* workspace, void* stream);
 
 /* argmax over a dense map (valid cells only); key as in mwb_energies. */
 int mwb_argmax_dense(const float* dense, const uint8_t* valid, int n, uint64_t* key,

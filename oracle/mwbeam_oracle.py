@@ -521,3 +521,57 @@ def run_framework_3d(antennas, v, dt, signals, kind, origin, res, dims, d, radiu
     best = max(comp, key=lambda k: (comp[k], tuple(-x for x in k)))
     return comp, {"final_region": final, "trace": trace, "argmax_cell": best, "coarse": len(coarse),
                   "fine": len(fine)}
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs[2] segmentation variant: reference
+# energies on per-quadrant n_sub x n_sub sub-grids + a restated control loop
+# (quadrant split = Region.quadrants, geometry.py:225-242; max/mean score,
+# DMAS shifted by the iteration minimum; argmax with first-index ties; stop
+# when the kept segment's larger side <= stop_cells).
+# ---------------------------------------------------------------------------
+def segment_baseline(antennas, v, dt, signals, kind, origin, res, dims, n_sub=16, stop_cells=40, window=None,
+                     region=None, mask=None):
+    def energies(pts):
+        if window is None:
+            return multistatic_energies(antennas, v, dt, signals, pts, kind)
+        return windowed_energies(antennas, v, dt, signals, pts, kind, window[0], window[1])
+
+    sel = region if region is not None else ((0, 0), (dims[0] - 1, dims[1] - 1))
+    records = []
+    lowres = None
+    while True:
+        (x0, y0), (x1, y1) = sel
+        w, h = x1 - x0 + 1, y1 - y0 + 1
+        if max(w, h) <= stop_cells or w < 2 or h < 2:
+            break
+        quads = quadrants(sel)
+        pts = []
+        for (qx0, qy0), (qx1, qy1) in quads:
+            wx, wy = (qx1 - qx0 + 1) * res, (qy1 - qy0 + 1) * res
+            cx, cy = origin[0] + qx0 * res, origin[1] + qy0 * res
+            for i in range(n_sub):
+                for j in range(n_sub):
+                    pts.append((cx + (i + 0.5) * (wx / n_sub), cy + (j + 0.5) * (wy / n_sub)))
+        e = energies(np.array(pts)).reshape(4, n_sub, n_sub)
+        if lowres is None:
+            lowres = np.zeros((2 * n_sub, 2 * n_sub))
+            for k in range(4):
+                lowres[(k & 1) * n_sub:(k & 1) * n_sub + n_sub, (k >> 1) * n_sub:(k >> 1) * n_sub + n_sub] = e[k]
+        shift = float(e.min()) if kind == "dmas" else 0.0
+        scores = []
+        for k in range(4):
+            ek = e[k] - shift
+            mean = float(ek.mean())
+            scores.append(float(ek.max()) / mean if mean > 0 else 0.0)
+        selected = int(np.argmax(scores))
+        records.append({"selected": selected, "scores": scores, "parent": sel, "selected_region": quads[selected]})
+        sel = quads[selected]
+    (x0, y0), (x1, y1) = sel
+    cells = [(ix, iy) for ix in range(x0, x1 + 1) for iy in range(y0, y1 + 1) if mask is None or mask[ix, iy]]
+    fine = {}
+    if cells:
+        pts = np.array([(origin[0] + (ix + 0.5) * res, origin[1] + (iy + 0.5) * res) for ix, iy in cells])
+        fine = dict(zip(cells, energies(pts).tolist()))
+    best = argmax_cell(fine) if fine else None
+    return {"final_region": sel, "records": records, "fine": fine, "argmax_cell": best, "lowres": lowres}

@@ -60,7 +60,33 @@ class Trace(C.Structure):
     ]
 
 
+SEG_MAX_ITERS = 32
+
+
+class SegRecord(C.Structure):
+    _fields_ = [
+        ("iteration", C.c_int32),
+        ("selected", C.c_int32),
+        ("parent", C.c_int32 * 6),
+        ("selected_region", C.c_int32 * 6),
+        ("shift", C.c_double),
+        ("score", C.c_double * 4),
+        ("emax", C.c_double * 4),
+        ("emean", C.c_double * 4),
+    ]
+
+
+class SegTrace(C.Structure):
+    _fields_ = [
+        ("n_records", C.c_int32),
+        ("stopped", C.c_int32),
+        ("final_region", C.c_int32 * 6),
+        ("records", SegRecord * SEG_MAX_ITERS),
+    ]
+
+
 TRACE_BYTES = C.sizeof(Trace)
+SEG_TRACE_BYTES = C.sizeof(SegTrace)
 
 _P = C.c_void_p
 _I = C.c_int
@@ -91,6 +117,12 @@ _SIGNATURES = {
     ),
     "mwb_select_roi": ([_P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P], _I),
     "mwb_argmax_dense": ([_P, _P, _I, _P, _P], _I),
+    "mwb_segment_workspace_bytes": ([_I, _I], _I64),
+    "mwb_segment": (
+        [_P, _I, _I, _I, _P, _P, _I, _D, _I, _I, _I, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P,
+         _P, _P],
+        _I,
+    ),
     "mwb_microbench": ([_I, C.POINTER(C.c_double), C.POINTER(C.c_float), _P], _I),
 }
 

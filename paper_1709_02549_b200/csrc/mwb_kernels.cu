@@ -1077,6 +1077,156 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     put_box(p.region_out, sel);
   }
 }
+// ----------------------------------------------------------------------------
+// K4: BASELINE configs[2] segmentation (quadrants scored on an n_sub x n_sub
+// sub-grid with max/mean, argmax kept, stop at a given segment size).  No
+// reference counterpart; the control flow is restated from BASELINE.json and
+// follows Region.quadrants (geometry.py:225-242) for the split.
+// ----------------------------------------------------------------------------
+struct SegState {
+  int region[6];
+  int done;
+  int iter;
+};
+
+// sub-grid points of the 4 quadrants of the current region (fp64 centres):
+// x = ox + x0*res + (i + 0.5) * (w*res / n_sub), likewise y
+__global__ void seg_points_kernel(SegState* st, double ox, double oy, double res, int n_sub, double* pts) {
+  if (st->done) return;
+  const int per = n_sub * n_sub;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 4 * per) return;
+  Box r;
+  for (int a = 0; a < 3; ++a) {
+    r.lo[a] = st->region[a];
+    r.hi[a] = st->region[3 + a];
+  }
+  Box q[MAXCH];
+  if (split_box(r, 2, q) == 0) return;
+  const int k = t / per, i = (t % per) / n_sub, j = t % n_sub;
+  const double wx = __dmul_rn((double)(q[k].hi[0] - q[k].lo[0] + 1), res);
+  const double wy = __dmul_rn((double)(q[k].hi[1] - q[k].lo[1] + 1), res);
+  const double cx = __dadd_rn(ox, __dmul_rn((double)q[k].lo[0], res));
+  const double cy = __dadd_rn(oy, __dmul_rn((double)q[k].lo[1], res));
+  pts[3 * (size_t)t] = __dadd_rn(cx, __dmul_rn((double)i + 0.5, __ddiv_rn(wx, (double)n_sub)));
+  pts[3 * (size_t)t + 1] = __dadd_rn(cy, __dmul_rn((double)j + 0.5, __ddiv_rn(wy, (double)n_sub)));
+  pts[3 * (size_t)t + 2] = 0.0;
+}
+
+// score the 4 quadrants (max/mean, DMAS shifted by the iteration minimum),
+// keep the argmax (ties -> lowest index), shrink the region, record the trace
+__global__ void __launch_bounds__(256) seg_score_kernel(SegState* st, const float* e, int n_sub, int shift_min,
+                                                         int stop_cells, float* lowres, mwb_seg_trace_t* tr) {
+  __shared__ double red[8][12];
+  __shared__ double fin[12];
+  if (st->done) return;
+  const int it0 = st->iter;  // read before thread 0 advances the state
+  const int per = n_sub * n_sub;
+  Box r;
+  for (int a = 0; a < 3; ++a) {
+    r.lo[a] = st->region[a];
+    r.hi[a] = st->region[3 + a];
+  }
+  Box q[MAXCH];
+  const int nk = split_box(r, 2, q);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // pass 1: global min (for the DMAS shift) and per-quadrant max
+  double mn = INFINITY, mxq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  for (int t = threadIdx.x; t < 4 * per; t += blockDim.x) {
+    const double v = (double)e[t];
+    mn = fmin(mn, v);
+    mxq[t / per] = fmax(mxq[t / per], v);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    for (int k = 0; k < 4; ++k) mxq[k] = fmax(mxq[k], __shfl_xor_sync(0xffffffffu, mxq[k], o));
+  }
+  if (lane == 0) {
+    red[warp][0] = mn;
+    for (int k = 0; k < 4; ++k) red[warp][1 + k] = mxq[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 5; ++k) {
+      double x = red[0][k];
+      for (int w = 1; w < (int)(blockDim.x / 32); ++w) x = k == 0 ? fmin(x, red[w][k]) : fmax(x, red[w][k]);
+      fin[k] = x;
+    }
+  }
+  __syncthreads();
+  const double shift = shift_min ? fin[0] : 0.0;
+  // pass 2: per-quadrant sums of the shifted energies (fixed order)
+  double sq[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int t = threadIdx.x; t < 4 * per; t += blockDim.x) sq[t / per] += (double)e[t] - shift;
+  for (int o = 16; o > 0; o >>= 1)
+    for (int k = 0; k < 4; ++k) sq[k] += __shfl_xor_sync(0xffffffffu, sq[k], o);
+  __syncthreads();
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k) red[warp][k] = sq[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int it = st->iter;
+    mwb_seg_record_t rec;
+    memset(&rec, 0, sizeof(rec));
+    rec.iteration = it + 1;
+    rec.shift = shift;
+    for (int a = 0; a < 6; ++a) rec.parent[a] = st->region[a];
+    double best = -INFINITY;
+    int sel = 0;
+    for (int k = 0; k < 4; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += red[w][k];
+      const double mean = s / (double)per;
+      const double mx = fin[1 + k] - shift;
+      const double score = mean > 0.0 ? mx / mean : 0.0;
+      rec.emax[k] = mx;
+      rec.emean[k] = mean;
+      rec.score[k] = score;
+      if (score > best) {
+        best = score;
+        sel = k;
+      }
+    }
+    rec.selected = sel;
+    put_box(rec.selected_region, q[sel]);
+    if (it < MWB_SEG_MAX_ITERS) tr->records[it] = rec;
+    for (int a = 0; a < 3; ++a) {
+      st->region[a] = q[sel].lo[a];
+      st->region[3 + a] = q[sel].hi[a];
+    }
+    st->iter = it + 1;
+    tr->n_records = min(it + 1, MWB_SEG_MAX_ITERS);
+    const int w = q[sel].hi[0] - q[sel].lo[0] + 1, h = q[sel].hi[1] - q[sel].lo[1] + 1;
+    if (max(w, h) <= stop_cells || w < 2 || h < 2) st->done = 1;
+    put_box(tr->final_region, q[sel]);
+    tr->stopped = st->done;
+  }
+  // the first iteration's sub-grids are the low-resolution background:
+  // a (2 n_sub) x (2 n_sub) image of the starting region, row = x index
+  if (lowres && it0 == 0 && nk == 4) {
+    for (int t = threadIdx.x; t < 4 * per; t += blockDim.x) {
+      const int k = t / per, i = (t % per) / n_sub, j = t % n_sub;
+      const int gx = (k & 1) * n_sub + i, gy = (k >> 1) * n_sub + j;
+      lowres[gx * 2 * n_sub + gy] = e[t];
+    }
+  }
+}
+
+__global__ void seg_init_kernel(SegState* st, int x0, int y0, int x1, int y1, int stop_cells, mwb_seg_trace_t* tr) {
+  st->region[0] = x0; st->region[1] = y0; st->region[2] = 0;
+  st->region[3] = x1; st->region[4] = y1; st->region[5] = 0;
+  st->iter = 0;
+  const int w = x1 - x0 + 1, h = y1 - y0 + 1;
+  st->done = (max(w, h) <= stop_cells || w < 2 || h < 2) ? 1 : 0;
+  tr->n_records = 0;
+  tr->stopped = st->done;
+  for (int a = 0; a < 6; ++a) tr->final_region[a] = st->region[a];
+}
+
+__global__ void seg_region_kernel(const SegState* st, int32_t* region_out) {
+  for (int a = 0; a < 6; ++a) region_out[a] = st->region[a];
+}
+
 __global__ void argmax_dense_kernel(const float* dense, const uint8_t* valid, int n,
                                     unsigned long long* key) {
   unsigned long long best = 0ull;
@@ -1470,6 +1620,55 @@ int mwb_select_roi_volume(const float* dense, const uint8_t* valid, int nx, int 
   p.region_out = d_region_out;
   p.trace = d_trace;
   return select_common(p, stream);
+}
+
+int64_t mwb_segment_workspace_bytes(int n_sub, int n_chan) {
+  if (n_sub < 1 || n_sub > 64 || n_chan < 1) return -1;
+  const long long n = 4LL * n_sub * n_sub;
+  const long long tiles = (n + TILE - 1) / TILE;
+  return (long long)align_up(sizeof(SegState), 256) + (long long)align_up(24 * n, 256) +
+         (long long)align_up(4 * n, 256) + (long long)table_layout(tiles, n_chan).total;
+}
+
+int mwb_segment(const float* sig, int n_chan, int ld, int n_samples, const int32_t* chan_txrx,
+                const double* ant_xyz, int n_ant, double inv_scale, int interp, int k0, int window,
+                int kind, double ox, double oy, double res, int nx, int ny, int x0, int y0, int x1,
+                int y1, int n_sub, int stop_cells, int max_iters, int32_t* d_region_out,
+                float* lowres, mwb_seg_trace_t* d_trace, void* workspace, void* stream) {
+  if (n_sub < 1 || n_sub > 64 || stop_cells < 1 || max_iters < 0 || max_iters > MWB_SEG_MAX_ITERS)
+    return set_err(MWB_EINVAL, "mwb_segment: bad n_sub / stop_cells / max_iters");
+  if (nx < 1 || ny < 1 || x0 < 0 || y0 < 0 || x1 >= nx || y1 >= ny || x0 > x1 || y0 > y1)
+    return set_err(MWB_EINVAL, "mwb_segment: region outside the grid");
+  if (kind != MWB_DAS && kind != MWB_DMAS) return set_err(MWB_EINVAL, "mwb_segment: bad kind");
+  if (!d_region_out || !d_trace || !workspace) return set_err(MWB_EINVAL, "mwb_segment: null pointer");
+  const int n = 4 * n_sub * n_sub;
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  SegState* st = reinterpret_cast<SegState*>(ws);
+  ws += align_up(sizeof(SegState), 256);
+  double* pts = reinterpret_cast<double*>(ws);
+  ws += align_up(24 * (size_t)n, 256);
+  float* e = reinterpret_cast<float*>(ws);
+  ws += align_up(4 * (size_t)n, 256);
+  void* table = ws;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  seg_init_kernel<<<1, 1, 0, cs>>>(st, x0, y0, x1, y1, stop_cells, d_trace);
+  int rc = check_launch("seg_init_kernel");
+  if (rc) return rc;
+  for (int it = 0; it < max_iters; ++it) {
+    // the done flag turns every launch of a finished search into a no-op
+    seg_points_kernel<<<(n + 255) / 256, 256, 0, cs>>>(st, ox, oy, res, n_sub, pts);
+    if ((rc = check_launch("seg_points_kernel"))) return rc;
+    if ((rc = mwb_delay_table(pts, n, nullptr, chan_txrx, n_chan, ant_xyz, n_ant, inv_scale, interp, table, stream)))
+      return rc;
+    if ((rc = mwb_energies(sig, 1, 0, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale, pts, nullptr,
+                           n, nullptr, table, interp, k0, window, kind == MWB_DAS ? e : nullptr,
+                           kind == MWB_DMAS ? e : nullptr, 0, nullptr, nullptr, nullptr, 0, stream)))
+      return rc;
+    seg_score_kernel<<<1, 256, 0, cs>>>(st, e, n_sub, kind == MWB_DMAS, stop_cells, lowres, d_trace);
+    if ((rc = check_launch("seg_score_kernel"))) return rc;
+  }
+  seg_region_kernel<<<1, 1, 0, cs>>>(st, d_region_out);
+  return check_launch("seg_region_kernel");
 }
 
 int mwb_argmax_dense(const float* dense, const uint8_t* valid, int n, uint64_t* key, void* stream) {
