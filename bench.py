@@ -250,7 +250,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_1709_02549_b200 import _native as nat
-    from paper_1709_02549_b200 import synth
+    from paper_1709_02549_b200 import shard, synth
     from paper_1709_02549_b200.batch import BatchImager
 
     rank, local, world = env_rank()
@@ -263,7 +263,7 @@ def run_ours(args):
     model = synth.ScanModel()
     S = args.scans
     t_gen = time.perf_counter()
-    sig, _ = synth.batch_2d(model, range(rank * S, (rank + 1) * S))
+    sig, _ = synth.batch_2d(model, shard.scan_block(rank, world, S))
     t_gen = time.perf_counter() - t_gen
     grid = synth.grid_square(0.12, args.grid)
     bi = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=(model.k0, model.window),
@@ -308,10 +308,7 @@ def run_ours(args):
     clk = clocks.stop()
     elapsed_ms = e0.elapsed_time(e1)
     launch_ms = [a.elapsed_time(b) for a, b in evs]
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t.item())
+    elapsed_ms = shard.max_over_ranks(elapsed_ms, dev)  # device time, max over ranks
     ms_step = elapsed_ms / args.steps
     pair_evals = 2.0 * S * P * C * world
     value = pair_evals / (ms_step * 1e-3)
@@ -357,10 +354,7 @@ def run_ours(args):
             t0 = time.perf_counter()
             bi(host, kinds=("das", "dmas"), chunk=args.chunk, out=out_h)
             times.append(time.perf_counter() - t0)
-        tt = torch.tensor([statistics.median(times)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+        e2e_s = shard.max_over_ranks(statistics.median(times), dev)
         chunks = (S + args.chunk - 1) // args.chunk
         e2e = {"value": pair_evals / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(host.numel() * 4),
                "d2h_bytes_per_step": int(2 * S * nxny * 4 + 2 * S * 8), "seconds_per_step": e2e_s,

@@ -296,12 +296,12 @@ def select_roi(coarse: EnergyMap, breast_region: Region, cfg: FrameworkConfig = 
     nx, ny = grid.dims
     if not grid.full_region().contains_region(breast_region):
         raise ValueError("breast region lies outside the grid")
-    if coarse._entries is None:
+    if getattr(coarse, "_entries", True) is None:  # dense-backed map from this package
         vals, valid = coarse._values.astype(np.float32), coarse._valid
-    else:
+    else:  # dict-backed (this package's or the reference's EnergyMap)
         vals = np.zeros((nx, ny), dtype=np.float32)
         valid = np.zeros((nx, ny), dtype=bool)
-        for (ix, iy), v in coarse._entries.items():
+        for (ix, iy), v in coarse.entries.items():
             if 0 <= ix < nx and 0 <= iy < ny:
                 vals[ix, iy] = v
                 valid[ix, iy] = True
