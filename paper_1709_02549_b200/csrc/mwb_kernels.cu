@@ -35,8 +35,7 @@ namespace {
 
 constexpr int TPB = 128;          // threads per energy CTA
 constexpr int TILE = 2 * TPB;     // focal points per CTA
-constexpr int WCH = 32;           // window samples per register chunk
-static_assert(WCH % 4 == 0, "chunk starts must keep the 16-byte span alignment phase");
+constexpr int WCH = 32;           // default window samples per register chunk (48 for W=48)
 constexpr int MAX_ANT = 64;
 constexpr int MAX_CHAN = 4096;
 constexpr int CAP_MAX = 8192;     // floats per stage buffer (32 KB)
@@ -163,13 +162,14 @@ constexpr int KIND_DAS = 0, KIND_DMAS = 1, KIND_BOTH = 2;
 //   a = f0*y[k] + f1*y[k+1];  s += a            (beamform.py:207-208; DAS 203-205)
 //   q += a*a                                    (DMAS only, beamform.py:209)
 // DAS and DMAS share s, so one pass yields both energies.
-template <int KIND, bool TAIL, class Load>
-__device__ __forceinline__ void accumulate_channel(float2 (&s)[WCH], float2& qe, float2& qo,
+template <int KIND, bool TAIL, int CH, class Load>
+__device__ __forceinline__ void accumulate_channel(float2 (&s)[CH], float2& qe, float2& qo,
                                                    const float2 f0, const float2 f1,
                                                    const Load& load, const int valid) {
+  static_assert(CH % 4 == 0, "chunk starts must keep the 16-byte span alignment phase");
   float2 prev = load(0);
 #pragma unroll
-  for (int k = 0; k < WCH; ++k) {
+  for (int k = 0; k < CH; ++k) {
     const float2 nxt = load(k + 1);
     float2 a = __fmul2_rn(f0, prev);
     a = __ffma2_rn(f1, nxt, a);
@@ -187,10 +187,11 @@ __device__ __forceinline__ void accumulate_channel(float2 (&s)[WCH], float2& qe,
 // Chunk epilogue: S = Σ_k s_k^2 (fp32, fixed order) and Q = Σ q (DMAS);
 // DAS energy = Σ S, DMAS energy = ½ Σ (S − Q), summed over chunks in fp64
 // (beamform.py:210-212).
-__device__ __forceinline__ float2 chunk_sumsq(const float2 (&s)[WCH], const int valid) {
+template <int CH>
+__device__ __forceinline__ float2 chunk_sumsq(const float2 (&s)[CH], const int valid) {
   float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int k = 0; k < WCH; ++k)
+  for (int k = 0; k < CH; ++k)
     if (k < valid) acc = __ffma2_rn(s[k], s[k], acc);
   return acc;
 }
@@ -291,7 +292,9 @@ struct TableParams {
 __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* dist = reinterpret_cast<double*>(smem);                 // [M][TILE]
-  int* lo = reinterpret_cast<int*>(dist + (size_t)p.M * TILE);   // [C]
+  double* amin = dist + (size_t)p.M * TILE;                      // [M]
+  double* amax = amin + p.M;                                     // [M]
+  int* lo = reinterpret_cast<int*>(amax + p.M);                  // [C]
   int* hi = lo + p.C;                                            // [C]
   int* wide = hi + p.C;
   const int tid = threadIdx.x;
@@ -314,25 +317,33 @@ __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
   }
   if (tid == 0) *wide = 0;
   __syncthreads();
-  // exact per-channel i0 range over the tile's valid points
-  for (int c = 0; c < p.C; ++c) {
-    const int tx = __ldg(p.chan + 2 * c), rx = __ldg(p.chan + 2 * c + 1);
-    int ia, ib;
-    uint32_t qa, qb;
-    split_delay_q(pair_delay(dist[tx * TILE + la], dist[rx * TILE + la], p.inv_scale), p.interp, ia, qa);
-    split_delay_q(pair_delay(dist[tx * TILE + lb], dist[rx * TILE + lb], p.inv_scale), p.interp, ib, qb);
-    int mn = 0x7FFFFFFF, mx = -1;
-    if (la < n_in) { mn = min(mn, ia); mx = max(mx, ia); }
-    if (lb < n_in) { mn = min(mn, ib); mx = max(mx, ib); }
+  // per-channel i0 range from per-antenna distance bounds over the tile's
+  // points: fl(+), fl(*), floor and rint are monotone, so every point's i0 for
+  // channel (tx, rx) lies in [i0(dmin_tx + dmin_rx), i0(dmax_tx + dmax_rx)]
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int i = warp; i < p.M; i += TPB / 32) {
+    double mn = INFINITY, mx = -INFINITY;
+    for (int j = lane; j < n_in; j += 32) {
+      const double d = dist[i * TILE + j];
+      mn = fmin(mn, d);
+      mx = fmax(mx, d);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
-    if ((tid & 31) == 0) {
-      atomicMin(&lo[c], mn);
-      atomicMax(&hi[c], mx);
+    if (lane == 0) {
+      amin[i] = mn;
+      amax[i] = mx;
     }
+  }
+  __syncthreads();
+  for (int c = tid; c < p.C; c += TPB) {
+    const int tx = __ldg(p.chan + 2 * c), rx = __ldg(p.chan + 2 * c + 1);
+    uint32_t q;
+    split_delay_q(pair_delay(amin[tx], amin[rx], p.inv_scale), p.interp, lo[c], q);
+    split_delay_q(pair_delay(amax[tx], amax[rx], p.inv_scale), p.interp, hi[c], q);
   }
   __syncthreads();
   const size_t tile = blockIdx.x;
@@ -365,8 +376,8 @@ __device__ __forceinline__ float one_plus_f1(uint32_t w) {
 
 // Channels [c_begin, c_end) of one step on the smem-staged samples.  The delay
 // words of the next channel are fetched while the current one is processed.
-template <int KIND, bool TAIL>
-__device__ __forceinline__ void channel_loop(float2 (&sacc)[WCH], float2& qe, float2& qo,
+template <int KIND, bool TAIL, int CH>
+__device__ __forceinline__ void channel_loop(float2 (&sacc)[CH], float2& qe, float2& qo,
                                              const uint32_t* __restrict__ tw, const int* sb,
                                              const float* buf, int c_begin, int c_end, int la, int lb,
                                              int valid) {
@@ -385,14 +396,14 @@ __device__ __forceinline__ void channel_loop(float2 (&sacc)[WCH], float2& qe, fl
     const float* ya = base + (ca >> 23);
     const float* yb = base + (cw >> 23);
     auto load = [&](int k) { return make_float2(ya[k], yb[k]); };
-    accumulate_channel<KIND, TAIL>(sacc, qe, qo, f0, f1, load, valid);
+    accumulate_channel<KIND, TAIL, CH>(sacc, qe, qo, f0, f1, load, valid);
   }
 }
 
 // ----------------------------------------------------------------------------
 // K1: staged fractional gather + fused DAS/DMAS window accumulation
 // ----------------------------------------------------------------------------
-template <int KIND, int MINB>
+template <int KIND, int MINB, int CH>
 __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
@@ -431,8 +442,8 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
   for (int c = tid; c < p.C; c += TPB) {
     const int2 sp = __ldg(tsp + c);
     clo[c] = sp.x;
-    // samples k0+q*WCH + [lo, hi+WCH] plus up to 3 of alignment slack
-    calloc_[c] = (sp.y - sp.x + WCH + 8 + 3) & ~3;
+    // samples k0+q*CH + [lo, hi+CH] plus up to 3 of alignment slack
+    calloc_[c] = (sp.y - sp.x + CH + 8 + 3) & ~3;
   }
   if (tid == 0) {
     for (int b = 0; b < NSTAGE; ++b) {
@@ -442,28 +453,47 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
+  if (warp == 0) {
+    // largest span -> channels per stage group; then per-group offsets from a
+    // warp-wide exclusive prefix sum of the spans (32 channels per round)
     int mx = 0;
-    for (int c = 0; c < p.C; ++c) mx = max(mx, calloc_[c]);
+    for (int c = lane; c < p.C; c += 32) mx = max(mx, calloc_[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     int G = (!wide && p.mode == 0 && mx <= p.cap) ? p.cap / mx : 0;
     if (G > p.C) G = p.C;
-    int run = 0;
-    for (int c = 0; c < p.C; ++c) {
-      if (G > 0 && c % G == 0) run = 0;
-      coff[c] = run;
-      run += calloc_[c];
+    int carry = 0;
+    for (int base = 0; base < p.C; base += 32) {
+      const int c = base + lane;
+      const int v = c < p.C ? calloc_[c] : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (c < p.C) coff[c] = carry + x - v;  // global exclusive prefix
+      carry += __shfl_sync(0xffffffffu, x, 31);
     }
-    misc[0] = G;
-    misc[1] = G > 0 ? (p.C + G - 1) / G : 0;
+    __syncwarp();
+    if (G > 0)
+      for (int c = lane; c < p.C; c += 32) sb[c] = coff[(c / G) * G];
+    __syncwarp();
+    if (G > 0)
+      for (int c = lane; c < p.C; c += 32) coff[c] -= sb[c];  // offset within the group
+    if (lane == 0) {
+      misc[0] = G;
+      misc[1] = G > 0 ? (p.C + G - 1) / G : 0;
+    }
   }
   __syncthreads();
-  // smem slot of sample (k0 + q*WCH + lo_c) in channel c's span: the same for
-  // every chunk q because WCH % 4 == 0
+  // smem slot of sample (k0 + q*CH + lo_c) in channel c's span: the same for
+  // every chunk q because CH % 4 == 0
   for (int c = tid; c < p.C; c += TPB) sb[c] = coff[c] + ((p.k0 + clo[c]) & 3);
   __syncthreads();
   const int G = misc[0];
   const int n_groups = misc[1];
-  const int n_chunks = (p.W + WCH - 1) / WCH;
+  const int n_chunks = (p.W + CH - 1) / CH;
 
   // Producer (warp 0, all lanes): stage step t into ring slot t % NSTAGE once
   // the consumers released the slot's previous use.  Zero-fills (spans past
@@ -479,7 +509,7 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
     const int c_begin = g * G, c_end = min(p.C, c_begin + G);
     float* buf = stage + b * p.cap;
     const float* scan_sig = p.sig + (size_t)s * (size_t)p.scan_stride;
-    const int cb = p.k0 + q * WCH;
+    const int cb = p.k0 + q * CH;
     uint32_t bytes_lane = 0;
     for (int c = c_begin + lane; c < c_end; c += 32) {
       const long long start4 = ((long long)cb + clo[c]) & ~3LL;
@@ -507,7 +537,7 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
 
   const int nsteps = (n_groups > 0 ? n_groups : 1) * n_chunks * n_my_scans;
 
-  float2 sacc[WCH];
+  float2 sacc[CH];
   float2 qe = make_float2(0.f, 0.f), qo = make_float2(0.f, 0.f);
   double eS_a = 0.0, eS_b = 0.0, eQ_a = 0.0, eQ_b = 0.0;
 
@@ -519,13 +549,13 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
     const int r = G > 0 ? t / n_groups : t;
     const int q = r % n_chunks;
     const int s = scan_begin + r / n_chunks;
-    const int valid = min(WCH, p.W - q * WCH);
-    const int cb = p.k0 + q * WCH;
+    const int valid = min(CH, p.W - q * CH);
+    const int cb = p.k0 + q * CH;
 
     if (G > 0) mbar_wait(&mbar[t % NSTAGE], (t / NSTAGE) & 1);
     if (g == 0) {
 #pragma unroll
-      for (int k = 0; k < WCH; ++k) sacc[k] = make_float2(0.f, 0.f);
+      for (int k = 0; k < CH; ++k) sacc[k] = make_float2(0.f, 0.f);
       qe = make_float2(0.f, 0.f);
       qo = make_float2(0.f, 0.f);
     }
@@ -536,10 +566,10 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
 
     if (G > 0) {
       // fast path: packed delay words (L2-resident table), samples from smem
-      if (valid == WCH)
-        channel_loop<KIND, false>(sacc, qe, qo, tw, sb, buf, c_begin, c_end, la, lb, valid);
+      if (valid == CH)
+        channel_loop<KIND, false, CH>(sacc, qe, qo, tw, sb, buf, c_begin, c_end, la, lb, valid);
       else
-        channel_loop<KIND, true>(sacc, qe, qo, tw, sb, buf, c_begin, c_end, la, lb, valid);
+        channel_loop<KIND, true, CH>(sacc, qe, qo, tw, sb, buf, c_begin, c_end, la, lb, valid);
     } else {
       // L1/L2 gather path (mode 1 or a tile whose delay spread exceeds the table):
       // same weights, loads straight from global with a zero tail.
@@ -575,15 +605,15 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
           const long long xa = ma + k, xb = mb + k;
           return make_float2(xa < ldv ? __ldg(yc + xa) : 0.f, xb < ldv ? __ldg(yc + xb) : 0.f);
         };
-        if (valid == WCH)
-          accumulate_channel<KIND, false>(sacc, qe, qo, f0, f1, load, valid);
+        if (valid == CH)
+          accumulate_channel<KIND, false, CH>(sacc, qe, qo, f0, f1, load, valid);
         else
-          accumulate_channel<KIND, true>(sacc, qe, qo, f0, f1, load, valid);
+          accumulate_channel<KIND, true, CH>(sacc, qe, qo, f0, f1, load, valid);
       }
     }
 
     if (g == (G > 0 ? n_groups - 1 : 0)) {
-      const float2 S = chunk_sumsq(sacc, valid);
+      const float2 S = chunk_sumsq<CH>(sacc, valid);
       eS_a += (double)S.x;
       eS_b += (double)S.y;
       if (KIND != KIND_DAS) {
@@ -1385,7 +1415,7 @@ int mwb_delay_table(const double* pts_xyz, int n_pts, const int32_t* d_count, co
   p.words = reinterpret_cast<uint32_t*>(base + T.words);
   p.span = reinterpret_cast<int2*>(base + T.span);
   p.wide = reinterpret_cast<int*>(base + T.wide);
-  const size_t sm = sizeof(double) * (size_t)n_ant * TILE + sizeof(int) * (2 * (size_t)n_chan + 4);
+  const size_t sm = sizeof(double) * ((size_t)n_ant * TILE + 2 * (size_t)n_ant) + sizeof(int) * (2 * (size_t)n_chan + 4);
   if (sm > 227 * 1024) return set_err(MWB_ERANGE, "mwb_delay_table: shared memory %lld bytes", (long long)sm);
   cudaError_t e = cudaFuncSetAttribute(delay_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -1447,8 +1477,11 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
   p.key_dmas = reinterpret_cast<unsigned long long*>(key_dmas);
   p.flags = flags;
   p.mode = mode;
+  // register chunk: 48 samples for windows that are a multiple of 48 (the
+  // configs[4] W = 48 would waste a third of a 2 x 32 split), else 32
+  const int ch = (window % 48 == 0 && window % 32 != 0) ? 48 : 32;
   // stage capacity: every channel's span for a compact tile, capped at 32 KB
-  long long cap = (long long)n_chan * (WCH + 24);
+  long long cap = (long long)n_chan * (ch + 24);
   cap = (cap + 3) & ~3LL;
   if (cap > CAP_MAX) cap = CAP_MAX;
   if (cap < 256) cap = 256;
@@ -1460,18 +1493,21 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
   dim3 grid((unsigned)tiles, (n_scans + p.scans_per_cta - 1) / p.scans_per_cta);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int kind = out_das && out_dmas ? KIND_BOTH : (out_das ? KIND_DAS : KIND_DMAS);
-  // MWB_MINB=4 selects the 4-CTA/SM (<=128 registers) build of the kernel
+  // MWB_MINB=4 selects the 4-CTA/SM (<=128 registers) build of the 32-sample kernel
   static const int minb = [] {
     const char* e = getenv("MWB_MINB");
     return (e && atoi(e) == 4) ? 4 : 3;
   }();
   void (*fn)(EnergyParams);
-  if (minb == 4)
-    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 4>
-         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 4> : energy_kernel<KIND_BOTH, 4>);
+  if (ch == 48)
+    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 2, 48>
+         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 2, 48> : energy_kernel<KIND_BOTH, 2, 48>);
+  else if (minb == 4)
+    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 4, 32>
+         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 4, 32> : energy_kernel<KIND_BOTH, 4, 32>);
   else
-    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 3>
-         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 3> : energy_kernel<KIND_BOTH, 3>);
+    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 3, 32>
+         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 3, 32> : energy_kernel<KIND_BOTH, 3, 32>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   fn<<<grid, TPB, L.total, st>>>(p);
