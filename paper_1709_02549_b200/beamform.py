@@ -109,14 +109,17 @@ class EnergyMap:
                 raise ValueError("energy map contains non-finite values")
 
     @classmethod
-    def _from_dense(cls, grid, values: np.ndarray, valid: np.ndarray, stride: int = 1, roi=None, split: int = 0):
+    def _from_dense(cls, grid, values: np.ndarray, valid: np.ndarray, stride: int = 1, roi=None, split: int = 0,
+                    checked: bool = False):
+        """Dense-backed map; ``checked`` means the device already verified that
+        every valid value is finite (the energy kernel's flag word)."""
         em = cls.__new__(cls)
         em.grid, em.stride, em.roi = grid, stride, roi
         em._entries = None
         em._values = values
         em._valid = valid
         em._split = split
-        if valid.any() and not np.isfinite(values[valid]).all():
+        if not checked and valid.any() and not np.isfinite(values[valid]).all():
             raise ValueError("energy map contains non-finite values")
         return em
 
@@ -430,7 +433,7 @@ def images(ds, kinds, grid: ImagingGrid, region: Region | None = None, stride: i
     for c in codes:
         EVAL_COUNTER.add(n)
         name = "das" if c == nat.MWB_DAS else "dmas"
-        out[name] = EnergyMap._from_dense(grid, dense[c].view(nx, ny).cpu().numpy(), vmask, stride)
+        out[name] = EnergyMap._from_dense(grid, dense[c].view(nx, ny).cpu().numpy(), vmask, stride, checked=True)
     return out
 
 

@@ -321,29 +321,43 @@ def select_roi(coarse: EnergyMap, breast_region: Region, cfg: FrameworkConfig = 
     return final, trace
 
 
-class _FrameworkRun:
-    """Device state of one framework run (buffers live until ``finish``)."""
+class _FrameworkPlan:
+    """One framework configuration on one device scan, captured as a CUDA graph.
 
-    def __init__(self, ds, kind, grid: ImagingGrid, d: int, cfg: FrameworkConfig, interpolation: str, window, mode: int):
-        self.grid, self.d, self.cfg = grid, d, cfg
-        self.kcode = _kind_code(kind)
-        self.interp = nat.INTERP[interpolation]
-        self.scan = dv.scan_for(ds)
-        self.k0, self.w = _window(self.scan.n_samples, window)
-        self.mode = mode
+    The coarse lattice pass, the select kernel and the ROI-driven fine pass
+    (13 kernels incl. memsets) are enqueued once eagerly, then captured; later
+    calls replay the graph and read the results back into pinned buffers with
+    a single synchronisation.  Buffers persist with the plan, so a replay
+    allocates nothing.
+    """
+
+    def __init__(self, scan: dv.DeviceScan, grid: ImagingGrid, d: int, kcode: int, cfg: FrameworkConfig,
+                 interp: int, k0: int, w: int, mode: int):
+        self.scan, self.grid, self.d, self.kcode, self.cfg = scan, grid, d, kcode, cfg
+        self.interp, self.k0, self.w, self.mode = interp, k0, w, mode
         nx, ny = grid.dims
         self.mask_np, self.mask_t = _breast_mask_device(grid)
         dev = dv.device()
-        self.dense = torch.zeros(nx * ny, dtype=torch.float32, device=dev)
-        self.valid = torch.zeros(nx * ny, dtype=torch.uint8, device=dev)
+        self.dense = torch.empty(nx * ny, dtype=torch.float32, device=dev)  # only valid cells are read
+        self.valid = torch.empty(nx * ny, dtype=torch.uint8, device=dev)
         self.status = _Status()
-        self.region_t = torch.zeros(6, dtype=torch.int32, device=dev)
-        self.trace_t = torch.zeros(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
-        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        self.region_t = torch.empty(6, dtype=torch.int32, device=dev)
+        self.trace_t = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
+        # external events become timestamp nodes inside the captured graph
+        self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
+        pin = torch.cuda.is_available()
+        self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=pin)
+        self.h_trace = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, pin_memory=pin)
+        self.h_dense = torch.empty(nx * ny, dtype=torch.float32, pin_memory=pin)
+        self.h_valid = torch.empty(nx * ny, dtype=torch.uint8, pin_memory=pin)
+        self.graph: torch.cuda.CUDAGraph | None = None
+        self.replays = 0
 
-    def enqueue(self) -> None:
+    def _enqueue(self) -> None:
         g, d = self.grid, self.d
         ev = self.events
+        self.valid.zero_()
+        self.status.t.zero_()
         ev[0].record()
         lattice_pass(self.scan, g, d, self.mask_t, 0, (self.kcode,), self.interp, self.k0, self.w,
                      {self.kcode: self.dense}, self.valid, self.status, 0, mode=self.mode)
@@ -354,19 +368,37 @@ class _FrameworkRun:
                      {self.kcode: self.dense}, self.valid, self.status, 1, d_region=self.region_t, mode=self.mode)
         ev[3].record()
 
+    def launch(self) -> None:
+        """Enqueue one run (graph replay after the first call) and the readback."""
+        if self.graph is None:
+            self._enqueue()  # eager run: kernel attributes set, allocator warmed
+            torch.cuda.current_stream().synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                self._enqueue()
+            self.graph = graph
+        self.graph.replay()
+        self.replays += 1
+        for src, dst in ((self.status.t, self.h_status), (self.trace_t, self.h_trace), (self.dense, self.h_dense),
+                         (self.valid, self.h_valid)):
+            dst.copy_(src, non_blocking=True)
+
     def finish(self) -> tuple[EnergyMap, FrameworkReport]:
+        torch.cuda.current_stream().synchronize()
         nx, ny = self.grid.dims
-        keys, counts, flags = self.status.read()  # synchronises the stream
-        raw = self.trace_t.cpu().numpy().tobytes()
-        vals = self.dense.view(nx, ny).cpu().numpy()
-        vmask = self.valid.view(nx, ny).cpu().numpy().astype(bool)
+        h = self.h_status.numpy()
+        keys = h[:2].view(np.uint64)
+        tail = h[2:].view(np.int32)
+        counts, flags = tail[:2], int(tail[2])
         if flags & 1:
             raise ValueError("energy map contains non-finite values")
-        final, trace, _ = decode_trace(raw)
+        final, trace, _ = decode_trace(self.h_trace.numpy().tobytes())
         n_coarse, n_fine = int(counts[0]), int(counts[1])
         EVAL_COUNTER.add(n_coarse)
         EVAL_COUNTER.add(n_fine)
-        composite = EnergyMap._from_dense(self.grid, vals, vmask, stride=self.d, roi=final, split=self.d)
+        vals = self.h_dense.numpy().reshape(nx, ny).copy()  # the plan's pinned buffers are reused
+        vmask = self.h_valid.numpy().reshape(nx, ny).view(bool).copy()
+        composite = EnergyMap._from_dense(self.grid, vals, vmask, stride=self.d, roi=final, split=self.d, checked=True)
         ev = self.events
         t_c = ev[0].elapsed_time(ev[1]) / 1e3
         t_s = ev[1].elapsed_time(ev[2]) / 1e3
@@ -391,6 +423,36 @@ class _FrameworkRun:
         return composite, report
 
 
+_PLANS: "OrderedDict[tuple, _FrameworkPlan]" = None  # type: ignore[assignment]
+_PLAN_CAPACITY = 8
+
+
+def _plan_for(ds, kind, grid: ImagingGrid, d: int, cfg: FrameworkConfig, interpolation: str, window,
+              mode: int) -> _FrameworkPlan:
+    """Cached plan; a plan is reused only for the same device scan object, so a
+    new (or garbage-collected and re-created) dataset never replays stale data."""
+    global _PLANS
+    from collections import OrderedDict
+
+    if _PLANS is None:
+        _PLANS = OrderedDict()
+    scan = dv.scan_for(ds)
+    k0, w = _window(scan.n_samples, window)
+    kcode = _kind_code(kind)
+    interp = nat.INTERP[interpolation]
+    key = (id(scan), grid.origin, grid.extent, grid.resolution, d, kcode, cfg.frame_fraction, cfg.n_min, interp, k0,
+           w, mode, torch.cuda.current_device())
+    plan = _PLANS.get(key)
+    if plan is not None and plan.scan is scan:
+        _PLANS.move_to_end(key)
+        return plan
+    plan = _FrameworkPlan(scan, grid, d, kcode, cfg, interp, k0, w, mode)
+    _PLANS[key] = plan
+    while len(_PLANS) > _PLAN_CAPACITY:
+        _PLANS.popitem(last=False)
+    return plan
+
+
 def run_framework(
     ds,
     kind,
@@ -406,12 +468,12 @@ def run_framework(
     """Coarse pass, ROI selection, fine pass, composite (coarse2fine.py:301-350)."""
     _check_interpolation(interpolation)
     d = decimation_factor(mode, grid.resolution)
-    mask = breast_mask(grid)
-    if not mask[::d, ::d].any():
+    mask_np, _ = _breast_mask_device(grid)
+    if not mask_np[::d, ::d].any():
         raise ValueError("no coarse focal points inside the breast mask")
-    run = _FrameworkRun(ds, kind, grid, d, cfg, interpolation, window, {"smem": 0, "gather": 1}[kernel_mode])
-    run.enqueue()
-    return run.finish()
+    plan = _plan_for(ds, kind, grid, d, cfg, interpolation, window, {"smem": 0, "gather": 1}[kernel_mode])
+    plan.launch()
+    return plan.finish()
 
 
 @dataclass
@@ -450,13 +512,13 @@ def consistency_check(
     for dd in (d1, d2):
         if dd < 1 or dd > limit:
             raise ValueError(f"decimation factor {dd} outside acceptable range [1, {limit}]")
-    mask = breast_mask(grid)
+    mask, _ = _breast_mask_device(grid)
     for dd in (d1, d2):
         if not mask[::dd, ::dd].any():
             raise ValueError("no coarse focal points inside the breast mask")
-    runs = [_FrameworkRun(ds, kind, grid, dd, cfg, "linear", None, 0) for dd in (d1, d2)]
-    for r in runs:
-        r.enqueue()
-    (_, rep_a), (_, rep_b) = (r.finish() for r in runs)
+    plans = [_plan_for(ds, kind, grid, dd, cfg, "linear", None, 0) for dd in (d1, d2)]
+    for plan in plans:
+        plan.launch()  # both runs are in flight before the first readback
+    (_, rep_a), (_, rep_b) = (plan.finish() for plan in plans)
     inter = rep_a.final_region.intersection(rep_b.final_region)
     return CheckVerdict(inter is not None, inter, rep_a.final_region, rep_b.final_region), rep_a, rep_b

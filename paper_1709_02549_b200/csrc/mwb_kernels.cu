@@ -874,11 +874,16 @@ struct SelectParams {
   int n_min;
   int* region_out;
   mwb_trace_t* trace;
+  int staged;       // 1: the breast box's lattice is staged in shared memory
+  int sl0[3], sL[3];  // staged lattice origin / extent (lattice units)
 };
 
-// visit valid lattice cells of box r
+constexpr int SEL_STAGE_MAX = 24576;  // lattice cells staged in shared memory (96 KB)
+
+// visit valid lattice cells of box r (from the shared-memory copy when staged;
+// entries without a value are NaN there, as energies are always finite)
 template <class F>
-__device__ __forceinline__ void for_cells(const SelectParams& p, const Box& r, F&& f) {
+__device__ __forceinline__ void for_cells(const SelectParams& p, const float* sv, const Box& r, F&& f) {
   const int D = p.D;
   int l0[3], L[3];
   for (int a = 0; a < 3; ++a) {
@@ -887,13 +892,18 @@ __device__ __forceinline__ void for_cells(const SelectParams& p, const Box& r, F
     if (l1 < l0[a]) return;
     L[a] = l1 - l0[a] + 1;
   }
-  const long long n = (long long)L[0] * L[1] * L[2];
-  for (long long i = threadIdx.x; i < n; i += SEL_TPB) {
-    const int iz = (l0[2] + (int)(i % L[2])) * D;
-    const int iy = (l0[1] + (int)((i / L[2]) % L[1])) * D;
-    const int ix = (l0[0] + (int)(i / ((long long)L[2] * L[1]))) * D;
-    const size_t slot = ((size_t)ix * p.ny + iy) * p.nz + iz;
-    if (p.valid[slot]) f(ix, iy, iz, (double)p.dense[slot]);
+  const int n = L[0] * L[1] * L[2];
+  for (int i = threadIdx.x; i < n; i += SEL_TPB) {
+    const int lz = i % L[2], ly = (i / L[2]) % L[1], lx = i / (L[2] * L[1]);
+    const int ix = (l0[0] + lx) * D, iy = (l0[1] + ly) * D, iz = (l0[2] + lz) * D;
+    if (p.staged) {
+      const int si = ((l0[0] + lx - p.sl0[0]) * p.sL[1] + (l0[1] + ly - p.sl0[1])) * p.sL[2] + (l0[2] + lz - p.sl0[2]);
+      const float v = sv[si];
+      if (v == v) f(ix, iy, iz, (double)v);
+    } else {
+      const size_t slot = ((size_t)ix * p.ny + iy) * p.nz + iz;
+      if (p.valid[slot]) f(ix, iy, iz, (double)p.dense[slot]);
+    }
   }
 }
 
@@ -907,14 +917,25 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
   __shared__ double res[2 * 2 * MAXCH];
   __shared__ int ctl[2];
   __shared__ Box next_sel;
+  extern __shared__ float sv[];
   mwb_trace_t* tr = p.trace;
+  if (p.staged) {  // one pass over global memory; every later pass reads shared memory
+    const int n = p.sL[0] * p.sL[1] * p.sL[2];
+    for (int i = threadIdx.x; i < n; i += SEL_TPB) {
+      const int lz = i % p.sL[2], ly = (i / p.sL[2]) % p.sL[1], lx = i / (p.sL[2] * p.sL[1]);
+      const size_t slot = ((size_t)(p.sl0[0] + lx) * p.D * p.ny + (size_t)(p.sl0[1] + ly) * p.D) * p.nz +
+                          (size_t)(p.sl0[2] + lz) * p.D;
+      sv[i] = p.valid[slot] ? p.dense[slot] : __int_as_float(0x7fc00000);
+    }
+    __syncthreads();
+  }
 
   // breast-region stats: count, sum, min, max (coarse2fine.py:186-199)
   double n_sel, sum_sel, m2_sel;
   {
     double acc[2] = {0.0, 0.0};
     double mn = INFINITY, mx = -INFINITY;
-    for_cells(p, p.breast, [&](int, int, int, double v) {
+    for_cells(p, sv, p.breast, [&](int, int, int, double v) {
       acc[0] += 1.0;
       acc[1] += v;
       mn = fmin(mn, v);
@@ -955,7 +976,7 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     }
     const double mean = sum_sel / n_sel;
     double d2[1] = {0.0};
-    for_cells(p, p.breast, [&](int, int, int, double v) {
+    for_cells(p, sv, p.breast, [&](int, int, int, double v) {
       const double d = v - mean;
       d2[0] += d * d;
     });
@@ -984,7 +1005,7 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     double a1[4 * MAXCH];
 #pragma unroll
     for (int k = 0; k < 4 * MAXCH; ++k) a1[k] = 0.0;
-    for_cells(p, sel, [&](int ix, int iy, int iz, double v) {
+    for_cells(p, sv, sel, [&](int ix, int iy, int iz, double v) {
 #pragma unroll
       for (int k = 0; k < 2 * MAXCH; ++k)
         if (k < nreg && box_contains(rg[k], ix, iy, iz)) {
@@ -1005,7 +1026,7 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     double a2[2 * MAXCH];
 #pragma unroll
     for (int k = 0; k < 2 * MAXCH; ++k) a2[k] = 0.0;
-    for_cells(p, sel, [&](int ix, int iy, int iz, double v) {
+    for_cells(p, sv, sel, [&](int ix, int iy, int iz, double v) {
 #pragma unroll
       for (int k = 0; k < 2 * MAXCH; ++k)
         if (k < nreg && box_contains(rg[k], ix, iy, iz)) {
@@ -1602,7 +1623,19 @@ int mwb_enumerate_volume(double ox, double oy, double oz, double res, int nx, in
 }
 
 static int select_common(SelectParams& p, void* stream) {
-  select_roi_kernel<<<1, SEL_TPB, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  long long n = 1;
+  for (int a = 0; a < 3; ++a) {
+    p.sl0[a] = (p.breast.lo[a] + p.D - 1) / p.D;
+    const int l1 = p.breast.hi[a] / p.D;
+    p.sL[a] = l1 >= p.sl0[a] ? l1 - p.sl0[a] + 1 : 0;
+    n *= p.sL[a];
+  }
+  p.staged = n > 0 && n <= SEL_STAGE_MAX;
+  const size_t sm = p.staged ? sizeof(float) * (size_t)n : 0;
+  cudaError_t e = cudaFuncSetAttribute(select_roi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(float) * SEL_STAGE_MAX));
+  if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  select_roi_kernel<<<1, SEL_TPB, sm, reinterpret_cast<cudaStream_t>(stream)>>>(p);
   return check_launch("select_roi_kernel");
 }
 
