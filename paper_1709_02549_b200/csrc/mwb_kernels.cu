@@ -912,9 +912,10 @@ __device__ __forceinline__ void put_box(int32_t* dst, const Box& b) {
   dst[3] = b.hi[0]; dst[4] = b.hi[1]; dst[5] = b.hi[2];
 }
 
+template <int NK>  // 4 children (2-D quadrants) or 8 (3-D octants)
 __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams p) {
-  __shared__ double red[8 * 2 * 2 * MAXCH];
-  __shared__ double res[2 * 2 * MAXCH];
+  __shared__ double red[8 * 2 * 2 * NK];
+  __shared__ double res[2 * 2 * NK];
   __shared__ int ctl[2];
   __shared__ Box next_sel;
   extern __shared__ float sv[];
@@ -993,7 +994,7 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
 
   while (term == MWB_TERM_NONE) {
     Box rg[2 * MAXCH];
-    const int nk = split_box(sel, p.dims, rg);
+    const int nk = split_box(sel, NK == 8 ? 3 : 2, rg);
     if (nk == 0) {
       term = MWB_TERM_REGION_FLOOR;
       break;
@@ -1002,42 +1003,60 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     const int nreg = 2 * nk;
 
     // pass 1: count and sum of every child and of every child's expansion
-    double a1[4 * MAXCH];
+    // children are disjoint: a cell's child index follows from the split point
+    // of each axis (children k have lo = mid+1 on axis a iff bit a of k)
+    int mid[3];
+    for (int a = 0; a < 3; ++a) mid[a] = rg[0].hi[a];
+    double a1[4 * NK];
 #pragma unroll
-    for (int k = 0; k < 4 * MAXCH; ++k) a1[k] = 0.0;
+    for (int k = 0; k < 4 * NK; ++k) a1[k] = 0.0;
     for_cells(p, sv, sel, [&](int ix, int iy, int iz, double v) {
+      const int kc = (ix > mid[0]) | ((iy > mid[1]) << 1) | (NK == 8 ? ((iz > mid[2]) << 2) : 0);
 #pragma unroll
-      for (int k = 0; k < 2 * MAXCH; ++k)
-        if (k < nreg && box_contains(rg[k], ix, iy, iz)) {
+      for (int k = 0; k < NK; ++k)
+        if (k == kc) {
+          a1[2 * k] += 1.0;
+          a1[2 * k + 1] += v;
+        }
+#pragma unroll
+      for (int k = NK; k < 2 * NK; ++k)
+        if (box_contains(rg[k], ix, iy, iz)) {
           a1[2 * k] += 1.0;
           a1[2 * k + 1] += v;
         }
     });
-    block_sum<4 * MAXCH>(a1, red, res);
-    double cnt[2 * MAXCH], mean[2 * MAXCH], sums[2 * MAXCH];
+    block_sum<4 * NK>(a1, red, res);
+    double cnt[2 * NK], mean[2 * NK], sums[2 * NK];
 #pragma unroll
-    for (int k = 0; k < 2 * MAXCH; ++k) {
+    for (int k = 0; k < 2 * NK; ++k) {
       cnt[k] = res[2 * k];
       sums[k] = res[2 * k + 1];
       mean[k] = cnt[k] > 0.0 ? sums[k] / cnt[k] : 0.0;
     }
     __syncthreads();
     // pass 2: Σ (x - mean)^2 (two-pass variance, as numpy's var)
-    double a2[2 * MAXCH];
+    double a2[2 * NK];
 #pragma unroll
-    for (int k = 0; k < 2 * MAXCH; ++k) a2[k] = 0.0;
+    for (int k = 0; k < 2 * NK; ++k) a2[k] = 0.0;
     for_cells(p, sv, sel, [&](int ix, int iy, int iz, double v) {
+      const int kc = (ix > mid[0]) | ((iy > mid[1]) << 1) | (NK == 8 ? ((iz > mid[2]) << 2) : 0);
 #pragma unroll
-      for (int k = 0; k < 2 * MAXCH; ++k)
-        if (k < nreg && box_contains(rg[k], ix, iy, iz)) {
+      for (int k = 0; k < NK; ++k)
+        if (k == kc) {
+          const double d = v - mean[k];
+          a2[k] += d * d;
+        }
+#pragma unroll
+      for (int k = NK; k < 2 * NK; ++k)
+        if (box_contains(rg[k], ix, iy, iz)) {
           const double d = v - mean[k];
           a2[k] += d * d;
         }
     });
-    block_sum<2 * MAXCH>(a2, red, res);
-    double m2[2 * MAXCH];
+    block_sum<2 * NK>(a2, red, res);
+    double m2[2 * NK];
 #pragma unroll
-    for (int k = 0; k < 2 * MAXCH; ++k) m2[k] = res[k];
+    for (int k = 0; k < 2 * NK; ++k) m2[k] = res[k];
     __syncthreads();
 
     if (threadIdx.x == 0) {
@@ -1045,7 +1064,7 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
       mwb_iter_record_t rec;
       memset(&rec, 0, sizeof(rec));
       rec.n_children = nk;
-      double scores[MAXCH];
+      double scores[NK];
       for (int k = 0; k < nk; ++k) {
         rec.counts[k] = (int)cnt[k];
         if (cnt[k] == 0.0) {
@@ -1632,10 +1651,11 @@ static int select_common(SelectParams& p, void* stream) {
   }
   p.staged = n > 0 && n <= SEL_STAGE_MAX;
   const size_t sm = p.staged ? sizeof(float) * (size_t)n : 0;
-  cudaError_t e = cudaFuncSetAttribute(select_roi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  void (*fn)(SelectParams) = p.dims == 3 ? select_roi_kernel<8> : select_roi_kernel<4>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(float) * SEL_STAGE_MAX));
   if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-  select_roi_kernel<<<1, SEL_TPB, sm, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  fn<<<1, SEL_TPB, sm, reinterpret_cast<cudaStream_t>(stream)>>>(p);
   return check_launch("select_roi_kernel");
 }
 
