@@ -575,3 +575,32 @@ def segment_baseline(antennas, v, dt, signals, kind, origin, res, dims, n_sub=16
         fine = dict(zip(cells, energies(pts).tolist()))
     best = argmax_cell(fine) if fine else None
     return {"final_region": sel, "records": records, "fine": fine, "argmax_cell": best, "lowres": lowres}
+
+
+# ---------------------------------------------------------------------------
+# monostatic DAS — beamform.py:215-239 (Eq. (1) delay d / (2 v dt), diagonal
+# channels only)
+# ---------------------------------------------------------------------------
+def monostatic_energies(antennas, v, dt, signals, points):
+    ants = np.asarray(antennas, dtype=np.float64)
+    sig = np.asarray(signals, dtype=np.float64)
+    m, _, nsamp = sig.shape
+    pts = np.asarray(points, dtype=np.float64)
+    dx = pts[:, 0, None] - ants[None, :, 0]
+    dy = pts[:, 1, None] - ants[None, :, 1]
+    dz = ants[None, :, 2]
+    d = np.sqrt(dx * dx + dy * dy + dz * dz)
+    shifts = d / (2.0 * v * dt)
+    i0 = np.floor(shifts).astype(np.int64)
+    frac = shifts - i0
+    diag = sig[np.arange(m), np.arange(m)]
+    ypad = np.zeros((m, nsamp + int(i0.max()) + 2))
+    ypad[:, :nsamp] = diag
+    win = sliding_window_view(ypad, nsamp + 1, axis=1)
+    s = np.zeros((len(pts), nsamp))
+    for ch in range(m):
+        w = win[ch, i0[:, ch]]
+        f1 = frac[:, ch, None]
+        s += (1.0 - f1) * w[:, :nsamp]
+        s += f1 * w[:, 1:]
+    return (s * s).sum(axis=1)

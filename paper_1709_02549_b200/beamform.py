@@ -332,7 +332,8 @@ def lattice_pass(scan: dv.DeviceScan, grid: ImagingGrid, stride: int, mask_t: to
                     0, oidx, count_ptr, status.key_ptr(0), status.key_ptr(1), status.flags_ptr, mode)
 
 
-def energies(ds, points, kind, interpolation: str = "linear", *, window=None, mode: str = "smem") -> np.ndarray:
+def energies(ds, points, kind, interpolation: str = "linear", *, window=None, mode: str = "smem",
+             _scan: dv.DeviceScan | None = None) -> np.ndarray:
     """Energies of an arbitrary (P, 2) or (P, 3) list of focal points [m] (fp64 result)."""
     _check_interpolation(interpolation)
     pts = np.asarray(points, dtype=np.float64)
@@ -345,7 +346,7 @@ def energies(ds, points, kind, interpolation: str = "linear", *, window=None, mo
         return np.zeros(0)
     p3 = np.zeros((n, 3))
     p3[:, : pts.shape[1]] = pts
-    scan = dv.scan_for(ds)
+    scan = dv.scan_for(ds) if _scan is None else _scan
     k0, w = _window(scan.n_samples, window)
     if w == 0:
         return np.zeros(n)
@@ -374,6 +375,35 @@ def dmas_energy(ds, r, interpolation: str = "linear", *, window=None) -> float:
     return float(energies(ds, pt, BeamformerKind.DMAS, interpolation, window=window)[0])
 
 
+def _require_monostatic(ds) -> None:
+    is_mono = getattr(ds, "is_monostatic", None)
+    if is_mono is not None:
+        ok = bool(is_mono())
+    else:
+        sig = np.asarray(ds.signals)
+        off = sig.copy()
+        idx = np.arange(sig.shape[0])
+        off[idx, idx] = 0.0
+        ok = not off.any()
+    if not ok:
+        raise ValueError("dataset is not monostatic (off-diagonal channels present)")
+
+
+def das_energy_monostatic(ds, r, *, window=None) -> float:
+    """Monostatic DAS energy at ``r`` (beamform.py:215-239, 256-261): the diagonal
+    channels aligned with the Eq. (1) delay d / (2 v dt)."""
+    _require_monostatic(ds)
+    pt = np.asarray(r, dtype=np.float64)[:2].reshape(1, 2)
+    return float(energies(ds, pt, BeamformerKind.DAS, window=window, _scan=dv.mono_scan_for(ds))[0])
+
+
+def image_monostatic(ds, grid: ImagingGrid, region: Region | None = None, stride: int = 1, mask=None, skip=None, *,
+                     window=None) -> "EnergyMap":
+    """Monostatic DAS image (extension: the reference only exposes the point form)."""
+    _require_monostatic(ds)
+    return images(ds, ("das",), grid, region, stride, mask, skip, window=window, _scan=dv.mono_scan_for(ds))["das"]
+
+
 def point_energy(ds, kind, r) -> float:
     return das_energy(ds, r) if _kind(kind) is BeamformerKind.DAS else dmas_energy(ds, r)
 
@@ -397,7 +427,7 @@ def _eval_mask(grid: ImagingGrid, mask, skip) -> np.ndarray | None:
 
 def images(ds, kinds, grid: ImagingGrid, region: Region | None = None, stride: int = 1,
            mask: np.ndarray | None = None, skip=None, interpolation: str = "linear", *, window=None,
-           mode: str = "smem") -> dict:
+           mode: str = "smem", _scan: dv.DeviceScan | None = None) -> dict:
     """``image()`` for several kinds in one fused pass: {"das": EnergyMap, "dmas": EnergyMap}.
 
     DAS and DMAS share the per-sample channel sum, so both maps cost one pass
@@ -415,7 +445,7 @@ def images(ds, kinds, grid: ImagingGrid, region: Region | None = None, stride: i
     if not grid.full_region().contains_region(region):
         raise ValueError("region lies outside the grid")
     emask = _eval_mask(grid, mask, skip)
-    scan = dv.scan_for(ds)
+    scan = dv.scan_for(ds) if _scan is None else _scan
     k0, w = _window(scan.n_samples, window)
     nx, ny = grid.dims
     dev = dv.device()

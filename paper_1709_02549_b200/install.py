@@ -26,6 +26,7 @@ REPLACEMENTS = {
     "das_energy": bf.das_energy,
     "dmas_energy": bf.dmas_energy,
     "point_energy": bf.point_energy,
+    "das_energy_monostatic": bf.das_energy_monostatic,
     "select_roi": c2f.select_roi,
     "run_framework": c2f.run_framework,
     "consistency_check": c2f.consistency_check,

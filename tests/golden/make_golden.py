@@ -123,6 +123,21 @@ def main():
                               "das": das, "dmas": dmas})
     (HERE / "points_small.json").write_text(json.dumps(pts_cases))
 
+    # ---- monostatic DAS (beamform.py:215-261) on diagonal-only datasets -------
+    mono = []
+    for trial in range(8):
+        m = int(rng.integers(2, 7))
+        n = int(rng.integers(16, 120))
+        geom = R.ring_array(m, 1.0, propagation_speed=1.0, sample_interval=float(rng.choice([0.05, 0.1])))
+        sig = np.zeros((m, m, n))
+        for i in range(m):
+            sig[i, i] = rng.normal(size=n)
+        rds_m = R.BackscatterDataset(geom, sig)
+        rs = rng.uniform(-0.9, 0.9, (6, 2))
+        mono.append({"m": m, "n": n, "dt": geom.sample_interval, "signals": sig.tolist(), "points": rs.tolist(),
+                     "das": [R.das_energy_monostatic(rds_m, r) for r in rs]})
+    (HERE / "monostatic.json").write_text(json.dumps(mono))
+
     # ---- reference-simulator framework runs (test_coarse2fine.py style) -----
     fw = []
     for name, res, modes in (("dataset2", 0.002, ("auto:0.01", "manual:3", "manual:1")),

@@ -122,3 +122,10 @@ def test_oracle_volume_z_shift():
     got = orc.windowed_energies(shifted, vm.v, vm.dt, full, xy, "dmas", spec["k0"], spec["window"])
     want = np.array(sl["dmas"])[:6]
     assert np.abs(got - want).max() <= 1e-12 * np.abs(np.array(sl["dmas"])).max()
+
+
+def test_oracle_monostatic():
+    for case in load_json("monostatic.json"):
+        ants = orc.ring_antennas(case["m"], 1.0)
+        got = orc.monostatic_energies(ants, 1.0, case["dt"], np.array(case["signals"]), np.array(case["points"]))
+        np.testing.assert_allclose(got, case["das"], rtol=1e-12, atol=1e-12)
