@@ -223,6 +223,17 @@ def main():
     np.savez_compressed(HERE / "volume_cfg4.npz", sig_sha=np.array(sha(sig3)), tumours=tum3)
     (HERE / "volume_cfg4.json").write_text(json.dumps({"seed": 9, "k0": vm.k0, "window": vm.window, "slices": vox}))
 
+    # ---- wire formats (io.py): a small .mwb container and one export ---------
+    from mwbeam import io as RIO
+
+    rng5 = np.random.default_rng(55)
+    g5 = R.ring_array(4, 0.05, propagation_speed=1.2e8, sample_interval=2e-11)
+    ds5 = R.BackscatterDataset(g5, rng5.normal(size=(4, 4, 48)), t0=1.5e-10)
+    RIO.save_dataset(ds5, HERE / "small.mwb")
+    grid5 = R.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 0.01)
+    comp5, _ = R.run_framework(ds5, R.BeamformerKind.DAS, grid5, R.Manual(3))
+    RIO.export_energy_map(comp5, HERE / "export_small")
+
     meta["seconds"] = time.time() - t_start
     (HERE / "META.json").write_text(json.dumps(meta, indent=2))
     print(f"done in {meta['seconds']:.0f}s")
