@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--mode", choices=["smem", "gather"], default="smem")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -235,6 +236,61 @@ def fp32_peak_tflops(lib) -> float:
     return best
 
 
+def other_configs() -> dict:
+    """Latency of the public API on the other BASELINE configurations (device
+    time from CUDA events around whole calls, median of a few repeats)."""
+    import torch
+
+    import paper_1709_02549_b200 as mw
+    from paper_1709_02549_b200 import synth
+    from paper_1709_02549_b200.segment import segment
+    from paper_1709_02549_b200.volume import VolumeGrid, hemisphere_mask, image_volume, run_framework_volume
+
+    def med_ms(fn, reps=7):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    out = {}
+    m0 = synth.ScanModel()
+    ds, _ = synth.dataset_2d(m0, seed=0)
+    win = (m0.k0, m0.window)
+    g0 = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 1e-3)
+    g1 = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 5e-4)
+    t = med_ms(lambda: mw.image(ds, "das", g0, window=win))
+    out["cfg0_das_100x100_image"] = {"ms": t, "pixel_pair_evals_per_s": 1e4 * 66 / (t * 1e-3)}
+    t = med_ms(lambda: mw.image(ds, "dmas", g1, window=win))
+    out["cfg1_dmas_200x200_image"] = {"ms": t, "pixel_pair_evals_per_s": 4e4 * 66 / (t * 1e-3), "images_per_s": 1e3 / t}
+    m2 = synth.ScanModel(n_samples=2048)
+    ds2, _ = synth.dataset_2d(m2, seed=1000, phantom_radius=0.05)
+    g2 = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 2.5e-4)
+    d = g2.dims[0] // 32
+    for kind in ("das", "dmas"):
+        out[f"cfg2_run_framework_{kind}"] = {"ms": med_ms(lambda: mw.run_framework(ds2, kind, g2, mw.Manual(d),
+                                                                                    window=(m2.k0, 32)))}
+        out[f"cfg2_segment_{kind}"] = {"ms": med_ms(lambda: segment(ds2, kind, g2, 16, 0.01, window=(m2.k0, 32)))}
+        out[f"cfg2_full_image_{kind}"] = {"ms": med_ms(lambda: mw.image(ds2, kind, g2, mask=mw.breast_mask(g2),
+                                                                           window=(m2.k0, 32)))}
+    vm = synth.VolumeModel()
+    sig, _ = synth.scan_3d(vm, seed=9)
+    ds4 = mw.BackscatterDataset(vm.geometry(), synth.embed_pairs(vm.n_ant, vm.pairs(), sig))
+    g4 = VolumeGrid((-0.06, -0.06, 0.0), (0.12, 0.12, 0.12), 0.12 / 128)
+    t = med_ms(lambda: image_volume(ds4, "dmas", g4, window=(vm.k0, vm.window)), reps=3)
+    out["cfg4_dmas_128cubed_volume"] = {"ms": t, "voxel_pair_evals_per_s": 128**3 * 496 / (t * 1e-3)}
+    mask = hemisphere_mask(g4, vm.phantom_radius)
+    out["cfg4_octant_framework"] = {"ms": med_ms(lambda: run_framework_volume(
+        ds4, "dmas", g4, mw.Automatic(0.01), mask=mask, window=(vm.k0, vm.window)), reps=3)}
+    return out
+
+
 def load_traffic():
     p = REPO / "profiles" / "ncu_traffic.json"
     if p.exists():
@@ -364,6 +420,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_reference_rate(args.cpu_seconds)
+    others = other_configs() if (rank == 0 and world == 1 and not args.no_configs) else None
 
     if rank == 0:
         line = {
@@ -377,6 +434,7 @@ def run_ours(args):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "other_configs": others,
             "gpu_launches": args.steps,
             "clocks": clk,
             "kernel_mode": args.mode,
