@@ -15,7 +15,7 @@ PKG_DIR = Path(__file__).resolve().parent
 REPO = PKG_DIR.parent
 SRC = PKG_DIR / "csrc" / "mwb_kernels.cu"
 HEADER = REPO / "include" / "mwb.h"
-LIB = PKG_DIR / "libmwb.so"
+LIB = PKG_DIR / ("libmwb_debug.so" if os.environ.get("MWB_DEBUG_BOUNDS") else "libmwb.so")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -45,6 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), *NVCC_FLAGS, "-I", str(REPO / "include"), str(SRC), "-o", str(tmp)]
+    if LIB.name == "libmwb_debug.so":
+        cmd.insert(1, "-DMWB_DEBUG_BOUNDS")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)

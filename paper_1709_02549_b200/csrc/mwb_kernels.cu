@@ -41,6 +41,20 @@ constexpr int MAX_CHAN = 4096;
 constexpr int CAP_MAX = 8192;     // floats per stage buffer (32 KB)
 constexpr int NSTAGE = 3;         // stage-buffer ring depth (full/empty mbarrier pairs)
 
+// Debug builds (-DMWB_DEBUG_BOUNDS, libmwb_debug.so) trap on any shared-memory
+// staging index outside its buffer; compute-sanitizer is not available on the
+// GPU pool, so this is the bounds check the parity suite runs against.
+#ifdef MWB_DEBUG_BOUNDS
+#define MWB_CHECK(cond) \
+  do {                  \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define MWB_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 thread_local char g_err[512] = "";
 
 int set_err(int code, const char* fmt, ...) {
@@ -380,7 +394,7 @@ template <int KIND, bool TAIL, int CH>
 __device__ __forceinline__ void channel_loop(float2 (&sacc)[CH], float2& qe, float2& qo,
                                              const uint32_t* __restrict__ tw, const int* sb,
                                              const float* buf, int c_begin, int c_end, int la, int lb,
-                                             int valid) {
+                                             int valid, int cap) {
   const uint32_t* wp = tw + (size_t)c_begin * TILE;
   uint32_t wa = __ldg(wp + la), wb = __ldg(wp + lb);
   for (int c = c_begin; c < c_end; ++c) {
@@ -393,6 +407,7 @@ __device__ __forceinline__ void channel_loop(float2 (&sacc)[CH], float2& qe, flo
     const float2 f1 = __fadd2_rn(make_float2(one_plus_f1(ca), one_plus_f1(cw)), make_float2(-1.f, -1.f));
     const float2 f0 = __ffma2_rn(f1, make_float2(-1.f, -1.f), make_float2(1.f, 1.f));
     const float* base = buf + sb[c];
+    MWB_CHECK(sb[c] >= 0 && sb[c] + (int)(ca >> 23) + CH < cap && sb[c] + (int)(cw >> 23) + CH < cap);
     const float* ya = base + (ca >> 23);
     const float* yb = base + (cw >> 23);
     auto load = [&](int k) { return make_float2(ya[k], yb[k]); };
@@ -517,6 +532,7 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
       const long long n = min((long long)alloc, max((long long)p.ld - start4, 0LL));
       bytes_lane += (uint32_t)(n * 4);
       float* dst = buf + coff[c];
+      MWB_CHECK(coff[c] >= 0 && coff[c] + alloc <= p.cap);
       for (long long j = max(n, 0LL); j < alloc; ++j) dst[j] = 0.f;  // past the record: zeros
     }
     uint32_t bytes = bytes_lane;
@@ -567,9 +583,9 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
     if (G > 0) {
       // fast path: packed delay words (L2-resident table), samples from smem
       if (valid == CH)
-        channel_loop<KIND, false, CH>(sacc, qe, qo, tw, sb, buf, c_begin, c_end, la, lb, valid);
+        channel_loop<KIND, false, CH>(sacc, qe, qo, tw, sb, buf, c_begin, c_end, la, lb, valid, p.cap);
       else
-        channel_loop<KIND, true, CH>(sacc, qe, qo, tw, sb, buf, c_begin, c_end, la, lb, valid);
+        channel_loop<KIND, true, CH>(sacc, qe, qo, tw, sb, buf, c_begin, c_end, la, lb, valid, p.cap);
     } else {
       // L1/L2 gather path (mode 1 or a tile whose delay spread exceeds the table):
       // same weights, loads straight from global with a zero tail.
