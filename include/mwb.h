@@ -21,6 +21,7 @@
  *   mwb_enumerate_volume, mwb_select_roi_volume: the same for 3-D voxel grids
  *                             (BASELINE configs[4]; no reference counterpart)
  *   mwb_argmax_dense       <- pkg/src/mwbeam/beamform.py:101-104  EnergyMap.argmax_cell
+ *   mwb_simulate           <- pkg/src/mwbeam/simulate.py:111-162 simulate (input producer)
  *                             (also fused into mwb_energies through `argmax_key`)
  */
 #ifndef MWB_H
@@ -225,6 +226,23 @@ int mwb_segment(const float* sig, int n_chan, int ld, int n_samples, const int32
                 int kind, double ox, double oy, double res, int nx, int ny, int x0, int y0, int x1,
                 int y1, int n_sub, int stop_cells, int max_iters, int32_t* d_region_out,
                 float* lowres, mwb_seg_trace_t* d_trace, void* workspace, void* stream);
+
+/*
+ * Device-side scan synthesis (the input producer of the path): writes S scans
+ * [S][n_chan][ld] fp32 (samples >= n_samples zero) for point scatterers
+ * scatterers[S][n_scat][4] = {x, y, z, amplitude}.  model 0 = the reference
+ * simulator's cosine-modulated Gaussian (a = fc, b = envelope width,
+ * c = duration; simulate.py:53-73, 141-156), model 1 = BASELINE's
+ * differentiated Gaussian (a = tau, b = centre t_c).  noise_mode 0 = none,
+ * 1 = absolute sigma (sigma_param[s]), 2 = SNR in dB against the scan's peak
+ * |clean| (sigma_param[s] = SNR, peak_ws = uint32[S] workspace).  Noise is
+ * Philox-4x32-10 (seed, scan, channel, sample) + Box-Muller, reproducible but
+ * not numpy's PCG64 stream.
+ */
+int mwb_simulate(float* out, int n_scans, int n_chan, int n_samples, int ld, const int32_t* chan_txrx,
+                 const double* ant_xyz, int n_ant, const double* scatterers, int n_scat, double v, double dt,
+                 double t0, int model, double a, double b, double c, const double* sigma_param, int noise_mode,
+                 uint64_t seed, uint32_t* peak_ws, void* stream);
 
 /* argmax over a dense map (valid cells only); key as in mwb_energies. */
 int mwb_argmax_dense(const float* dense, const uint8_t* valid, int n, uint64_t* key,

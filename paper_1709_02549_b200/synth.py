@@ -144,6 +144,52 @@ def batch_2d(model: ScanModel, seeds, phantom_radius=(0.04, 0.06), snr_db=(10.0,
     return out, tumours
 
 
+def scan_params_2d(model: ScanModel, seeds, phantom_radius=(0.04, 0.06), snr_db=(10.0, 30.0)):
+    """Per-scan (tumour x, y, SNR) drawn exactly as scan_2d draws them."""
+    out = np.empty((len(seeds), 3))
+    for k, seed in enumerate(seeds):
+        rng = np.random.default_rng(seed)
+        radius = rng.uniform(*phantom_radius) if isinstance(phantom_radius, tuple) else phantom_radius
+        snr = rng.uniform(*snr_db) if isinstance(snr_db, tuple) else snr_db
+        out[k, :2] = uniform_in_disc(rng, radius)
+        out[k, 2] = snr
+    return out
+
+
+def batch_2d_device(model: ScanModel, seeds, phantom_radius=(0.04, 0.06), snr_db=(10.0, 30.0), noise_seed: int = 0,
+                    noise: bool = True):
+    """Device-side twin of batch_2d: (S, C, ld) fp32 CUDA tensor + (S, 2) tumours.
+
+    Tumour positions and SNRs are the host generator's (same seeds, same draws);
+    the clean pulses are evaluated on the GPU in fp64 with the same support;
+    the noise is the device's Philox stream (statistically equivalent, not
+    numpy's PCG64 sequence).  Produces the layout BatchImager.run_device takes.
+    """
+    import torch
+
+    from . import _device as dv
+    from . import _native as nat
+
+    seeds = list(seeds)
+    params = scan_params_2d(model, seeds, phantom_radius, snr_db)
+    dev = dv.device()
+    pairs = model.pairs()
+    ld = dv.round4(model.n_samples)
+    out = torch.empty((len(seeds), pairs.shape[0], ld), dtype=torch.float32, device=dev)
+    scat = np.zeros((len(seeds), 1, 4))
+    scat[:, 0, :2] = params[:, :2]
+    scat[:, 0, 3] = 1.0
+    scat_t = torch.from_numpy(scat).to(dev)
+    snr_t = torch.from_numpy(np.ascontiguousarray(params[:, 2])).to(dev)
+    peak = torch.empty(max(1, len(seeds)), dtype=torch.int32, device=dev)
+    chan = torch.from_numpy(pairs).to(dev)
+    ant = torch.from_numpy(np.array(model.geometry().antennas)).to(dev)
+    nat.call("mwb_simulate", out.data_ptr(), len(seeds), pairs.shape[0], model.n_samples, ld, chan.data_ptr(),
+             ant.data_ptr(), model.n_ant, scat_t.data_ptr(), 1, model.v, model.dt, 0.0, 1, model.tau, model.t_c, 0.0,
+             snr_t.data_ptr(), 2 if noise else 0, noise_seed, peak.data_ptr(), dv.stream_handle())
+    return out, params[:, :2].copy()
+
+
 def grid_square(side: float, n: int) -> ImagingGrid:
     """n x n grid covering [-side/2, side/2]^2."""
     return ImagingGrid((-side / 2, -side / 2), (side, side), side / n)
