@@ -269,6 +269,16 @@ def other_configs() -> dict:
     out["cfg0_das_100x100_image"] = {"ms": t, "pixel_pair_evals_per_s": 1e4 * 66 / (t * 1e-3)}
     t = med_ms(lambda: mw.image(ds, "dmas", g1, window=win))
     out["cfg1_dmas_200x200_image"] = {"ms": t, "pixel_pair_evals_per_s": 4e4 * 66 / (t * 1e-3), "images_per_s": 1e3 / t}
+    # the same configuration for a stream of scans: one launch per 1024 scans
+    from paper_1709_02549_b200.batch import BatchImager
+
+    sig1, _ = synth.batch_2d_device(m0, range(1024), phantom_radius=0.05, snr_db=20.0)
+    bi1 = BatchImager(m0.geometry(), m0.pairs(), m0.n_samples, g1, window=win)
+    o1 = torch.empty((1024, 200 * 200), dtype=torch.float32, device="cuda")
+    t = med_ms(lambda: bi1.run_device(sig1, out_dmas=o1), reps=5)
+    out["cfg1_dmas_200x200_batched_1024_scans"] = {"ms": t, "images_per_s": 1024 / (t * 1e-3),
+                                                   "pixel_pair_evals_per_s": 1024 * 4e4 * 66 / (t * 1e-3)}
+    del sig1, o1
     m2 = synth.ScanModel(n_samples=2048)
     ds2, _ = synth.dataset_2d(m2, seed=1000, phantom_radius=0.05)
     g2 = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 2.5e-4)

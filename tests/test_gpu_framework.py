@@ -303,3 +303,31 @@ class TestAcceptance:  # test_acceptance.py criteria 1, 2 (point counts), 3, 8
         d1, d4 = r1.to_dict(), r4.to_dict()
         d1["elapsed"] = d4["elapsed"] = None
         assert d1 == d4
+
+
+class TestDecimationSafety:  # test_acceptance.py:179-233 (criterion 6)
+    def test_200_trial_sweep(self):
+        resolution, min_diam, radius = 0.002, 0.01, 0.05
+        d = mw.auto_decimation_factor(min_diam, resolution)
+        geom = mw.ring_array(8, radius, sample_interval=1e-11)
+        rng = np.random.default_rng(7)
+        grid = grid_for_geometry(geom, resolution)
+        mask = mw.breast_mask(grid)
+        nx, ny = grid.dims
+        cx, cy = np.arange(0, nx, d), np.arange(0, ny, d)
+        square_hits = roi_hits = 0
+        for _ in range(200):
+            diam = rng.uniform(min_diam, 2 * min_diam)
+            rho = rng.uniform(0.0, radius - diam / 2 - 0.002)
+            ang = rng.uniform(0.0, 2 * np.pi)
+            tc = (rho * np.cos(ang), rho * np.sin(ang))
+            side = diam / np.sqrt(2.0)
+            xs = grid.origin[0] + (cx + 0.5) * resolution
+            ys = grid.origin[1] + (cy + 0.5) * resolution
+            in_x = cx[(xs >= tc[0] - side / 2) & (xs <= tc[0] + side / 2)]
+            in_y = cy[(ys >= tc[1] - side / 2) & (ys <= tc[1] + side / 2)]
+            square_hits += any(mask[ix, iy] for ix in in_x for iy in in_y)
+            sig = orc.simulate(geom.antennas, geom.propagation_speed, 1e-11, 256, [(tc, 1.0)])
+            _, rep = mw.run_framework(mw.BackscatterDataset(geom, sig), "das", grid, mw.Manual(d))
+            roi_hits += rep.final_region.contains_cell(*grid.point_to_cell(*tc))
+        assert square_hits == 200 and roi_hits >= 190
