@@ -289,6 +289,16 @@ def other_configs() -> dict:
         out[f"cfg2_segment_{kind}"] = {"ms": med_ms(lambda: segment(ds2, kind, g2, 16, 0.01, window=(m2.k0, 32)))}
         out[f"cfg2_full_image_{kind}"] = {"ms": med_ms(lambda: mw.image(ds2, kind, g2, mask=mw.breast_mask(g2),
                                                                            window=(m2.k0, 32)))}
+    # the configs[2] framework for a batch of 4096 scans (FrameworkBatch)
+    from paper_1709_02549_b200.fwbatch import FrameworkBatch
+
+    sig2, _ = synth.batch_2d_device(m2, range(4096), phantom_radius=(0.04, 0.05))
+    for kind in ("das", "dmas"):
+        fb = FrameworkBatch(m2.geometry(), m2.pairs(), m2.n_samples, g2, mw.Manual(d), kind, window=(m2.k0, 32))
+        t = med_ms(lambda: fb.run(sig2), reps=5)
+        out[f"cfg2_framework_batch_4096_{kind}"] = {"ms": t, "segmented_images_per_s": 4096 / (t * 1e-3)}
+        del fb
+    del sig2
     vm = synth.VolumeModel()
     sig, _ = synth.scan_3d(vm, seed=9)
     ds4 = mw.BackscatterDataset(vm.geometry(), synth.embed_pairs(vm.n_ant, vm.pairs(), sig))

@@ -167,6 +167,42 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
                  float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
                  uint64_t* key_dmas, int32_t* flags, int mode, void* stream);
 
+/*
+ * Packed multi-scan point lists: tile_info[t] = {scan, valid points} (int32
+ * pairs) for every 256-point tile t of pts_xyz; each tile belongs to one scan.
+ * The table is built per tile; the energy launch evaluates tile t on scan
+ * tile_info[t].x only (one launch for per-scan point lists, e.g. every scan's
+ * fine pass of a framework batch).  Other arguments as above.
+ */
+int mwb_delay_table_tiles(const double* pts_xyz, int n_pts, const int32_t* tile_info,
+                          const int32_t* chan_txrx, int n_chan, const double* ant_xyz, int n_ant,
+                          double inv_scale, int interp, void* table, void* stream);
+int mwb_energies_tiles(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
+                       int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
+                       double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
+                       const int32_t* tile_info, const void* table, int interp, int k0, int window,
+                       float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
+                       uint64_t* key_dmas, int32_t* flags, int mode, void* stream);
+
+/*
+ * Batched fine-pass enumeration: the stride-1 cells of each scan's device
+ * region d_regions[s] (int32[6]) that pass `mask` and are not on the
+ * skip_stride lattice.  _tile_bound writes the largest region's number of
+ * 16x16 enumeration tiles (device int32); with it, _count writes {padded
+ * points, tiles} to d_totals (device int32[2]); after reading them, _write
+ * fills pts_xyz / out_idx (slot ix*ny+iy) / tile_info.  Each scan starts on a
+ * 256-point tile boundary.
+ */
+int mwb_regions_tile_bound(const int32_t* d_regions, int n_scans, int32_t* d_bound, void* stream);
+int64_t mwb_regions_workspace_bytes(int tiles_bound, int n_scans);
+int mwb_enumerate_regions_count(int nx, int ny, const int32_t* d_regions, int n_scans, int tiles_bound,
+                                const uint8_t* mask, int skip_stride, int32_t* d_totals,
+                                void* workspace, void* stream);
+int mwb_enumerate_regions_write(double ox, double oy, double res, int nx, int ny,
+                                const int32_t* d_regions, int n_scans, int tiles_bound,
+                                const uint8_t* mask, int skip_stride, double* pts_xyz,
+                                int32_t* out_idx, int32_t* tile_info, void* workspace, void* stream);
+
 /* Workspace (bytes) for mwb_enumerate_lattice / mwb_enumerate_volume. */
 int64_t mwb_lattice_workspace_bytes(int nx, int ny, int stride);
 int64_t mwb_volume_workspace_bytes(int nx, int ny, int nz, int stride);
@@ -202,6 +238,13 @@ int mwb_enumerate_volume(double ox, double oy, double oz, double res, int nx, in
 int mwb_select_roi(const float* dense, const uint8_t* valid, int nx, int ny, int lattice,
                    int x0, int y0, int x1, int y1, double frame_fraction, int n_min,
                    int32_t* d_region_out, mwb_trace_t* d_trace, void* stream);
+
+/* One select_roi per scan of a batch: CTA s reads dense + s * dense_stride
+ * (the valid mask is shared) and writes d_regions_out[s] / d_traces[s]. */
+int mwb_select_roi_batch(const float* dense, int64_t dense_stride, const uint8_t* valid, int nx,
+                         int ny, int lattice, int x0, int y0, int x1, int y1,
+                         double frame_fraction, int n_min, int n_scans, int32_t* d_regions_out,
+                         mwb_trace_t* d_traces, void* stream);
 
 /* 3-D octant selection on an nx x ny x nz map (box: HOST int32[6]). */
 int mwb_select_roi_volume(const float* dense, const uint8_t* valid, int nx, int ny, int nz,

@@ -225,6 +225,7 @@ struct EnergyParams {
   const int* out_idx;
   int P;
   const int* d_count;
+  const int2* tile_info;      // packed multi-scan lists: {scan, valid points} per tile, or NULL
   const uint32_t* tab_words;  // [tiles][C][TILE]
   const int2* tab_span;       // [tiles][C] {lo, hi}
   const int* tab_wide;        // [tiles]
@@ -301,6 +302,7 @@ struct TableParams {
   uint32_t* words;
   int2* span;
   int* wide;
+  const int2* tile_info;  // packed multi-scan lists: {scan, valid points} per tile, or NULL
 };
 
 __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
@@ -315,7 +317,8 @@ __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
   const int n_pts = p.d_count ? min(*p.d_count, p.P) : p.P;
   const int tile0 = blockIdx.x * TILE;
   if (tile0 >= n_pts) return;
-  const int n_in = min(TILE, n_pts - tile0);
+  const int n_in = p.tile_info ? p.tile_info[blockIdx.x].y : min(TILE, n_pts - tile0);
+  if (n_in <= 0) return;
   const int la = tid, lb = tid + TPB;
   const int ga = tile0 + (la < n_in ? la : 0), gb = tile0 + (lb < n_in ? lb : 0);
   const double pax = p.pts[3 * (size_t)ga], pay = p.pts[3 * (size_t)ga + 1], paz = p.pts[3 * (size_t)ga + 2];
@@ -428,10 +431,17 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
   const int n_pts = p.d_count ? min(*p.d_count, p.P) : p.P;
   const int tile0 = blockIdx.x * TILE;
   if (tile0 >= n_pts) return;
-  const int n_in_tile = min(TILE, n_pts - tile0);
-  const int scan_begin = blockIdx.y * p.scans_per_cta;
+  int n_in_tile = min(TILE, n_pts - tile0);
+  int scan_begin = blockIdx.y * p.scans_per_cta;
+  int n_my_scans = min(p.scans_per_cta, p.n_scans - scan_begin);
+  if (p.tile_info) {  // each tile belongs to one scan (per-scan point lists, packed)
+    const int2 ti = p.tile_info[blockIdx.x];
+    scan_begin = ti.x;
+    n_in_tile = ti.y;
+    n_my_scans = 1;
+    if (n_in_tile <= 0 || scan_begin < 0) return;
+  }
   if (scan_begin >= p.n_scans) return;
-  const int n_my_scans = min(p.scans_per_cta, p.n_scans - scan_begin);
 
   const SmemLayout L = smem_layout(p.C, p.cap);
   int* clo = reinterpret_cast<int*>(smem + L.lo);
@@ -749,15 +759,16 @@ __global__ void __launch_bounds__(256) lattice_count_kernel(const LatticeParams 
   if (threadIdx.x == 0) p.tile_counts[blockIdx.x] = n;
 }
 
-__global__ void __launch_bounds__(1024) lattice_scan_kernel(const LatticeParams p) {
+// exclusive prefix sum of counts[0..n) into offsets (one 1024-thread CTA); total -> *total
+__device__ void block_exclusive_scan(const int* counts, int* offsets, int n, int* total) {
   __shared__ int warp_sums[32];
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int base = 0; base < p.n_tiles_max; base += 1024) {
+  for (int base = 0; base < n; base += 1024) {
     const int i = base + threadIdx.x;
-    const int v = i < p.n_tiles_max ? p.tile_counts[i] : 0;
+    const int v = i < n ? counts[i] : 0;
     int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -777,12 +788,16 @@ __global__ void __launch_bounds__(1024) lattice_scan_kernel(const LatticeParams 
     }
     __syncthreads();
     const int excl = carry + (warp > 0 ? warp_sums[warp - 1] : 0) + x - v;
-    if (i < p.n_tiles_max) p.tile_offsets[i] = excl;
+    if (i < n) offsets[i] = excl;
     __syncthreads();
     if (threadIdx.x == 0) carry += warp_sums[31];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *p.d_count = carry;
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(1024) lattice_scan_kernel(const LatticeParams p) {
+  block_exclusive_scan(p.tile_counts, p.tile_offsets, p.n_tiles_max, p.d_count);
 }
 
 __global__ void __launch_bounds__(256) lattice_write_kernel(const LatticeParams p) {
@@ -806,6 +821,107 @@ __global__ void __launch_bounds__(256) lattice_write_kernel(const LatticeParams 
   p.pts[3 * (size_t)pos + 2] = p.planar ? 0.0 : __dadd_rn(p.oz, __dmul_rn((double)iz + 0.5, p.res));
   p.out_idx[pos] = (int)slot;
   p.valid[slot] = 1;
+}
+
+// ----------------------------------------------------------------------------
+// Batched enumeration of per-scan regions (stride 1, 2-D): every scan's cells
+// go to one packed point list in which each scan starts on a 256-point tile
+// boundary; tile_info[t] = {scan, valid points} drives the table and energy
+// kernels, so one launch serves every scan's fine pass.
+// ----------------------------------------------------------------------------
+struct RegionBatch {
+  int n_scans, tiles_max;
+  int* tile_counts;   // [S][tiles_max]
+  int* tile_offsets;  // [S][tiles_max]
+  int* scan_counts;   // [S]
+  int* scan_offsets;  // [S] first point of each scan (multiple of TILE)
+  int* totals;        // [2] padded points, tiles
+};
+
+__device__ __forceinline__ LatticeParams scan_lattice(LatticeParams p, int s, const RegionBatch& b) {
+  p.d_region += 6 * s;
+  p.tile_counts = b.tile_counts + (size_t)s * b.tiles_max;
+  p.tile_offsets = b.tile_offsets + (size_t)s * b.tiles_max;
+  return p;
+}
+
+__global__ void __launch_bounds__(256) region_count_kernel(const LatticeParams p0, const RegionBatch b) {
+  const LatticeParams p = scan_lattice(p0, blockIdx.y, b);
+  const LatticeGeom g = lattice_geom(p);
+  int ix, iy, iz;
+  const bool ok = lattice_cell(p, g, blockIdx.x, threadIdx.x, ix, iy, iz);
+  const int n = __syncthreads_count(ok);
+  if (threadIdx.x == 0) p.tile_counts[blockIdx.x] = n;
+}
+
+__global__ void __launch_bounds__(1024) region_scan_kernel(const LatticeParams p0, const RegionBatch b) {
+  const LatticeParams p = scan_lattice(p0, blockIdx.x, b);
+  block_exclusive_scan(p.tile_counts, p.tile_offsets, b.tiles_max, b.scan_counts + blockIdx.x);
+}
+
+__global__ void __launch_bounds__(1024) region_offsets_kernel(const RegionBatch b) {
+  // padded sizes -> scan offsets (points); totals = (points, tiles)
+  __shared__ int padded[1024];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < b.n_scans; base += 1024) {
+    const int s = base + threadIdx.x;
+    padded[threadIdx.x] = s < b.n_scans ? (b.scan_counts[s] + TILE - 1) / TILE * TILE : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < 1024 && base + k < b.n_scans; ++k) {
+        b.scan_offsets[base + k] = carry;
+        carry += padded[k];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    b.totals[0] = carry;
+    b.totals[1] = carry / TILE;
+  }
+}
+
+// largest number of 16x16 enumeration tiles over the scans' regions -> *bound
+__global__ void region_bound_kernel(const int* regions, int n_scans, int* bound) {
+  int mx = 0;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_scans; s += gridDim.x * blockDim.x) {
+    const int* r = regions + 6 * s;
+    mx = max(mx, ((r[3] - r[0] + 16) / 16) * ((r[4] - r[1] + 16) / 16));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(bound, mx);
+}
+
+__global__ void region_tiles_kernel(const RegionBatch b, int2* tile_info) {
+  const int s = blockIdx.x;
+  const int count = b.scan_counts[s];
+  const int t0 = b.scan_offsets[s] / TILE;
+  for (int j = threadIdx.x; j * TILE < count; j += blockDim.x)
+    tile_info[t0 + j] = make_int2(s, min(TILE, count - j * TILE));
+}
+
+__global__ void __launch_bounds__(256) region_write_kernel(const LatticeParams p0, const RegionBatch b) {
+  __shared__ int wsum[8];
+  const int s = blockIdx.y;
+  const LatticeParams p = scan_lattice(p0, s, b);
+  const LatticeGeom g = lattice_geom(p);
+  int ix = 0, iy = 0, iz = 0;
+  const bool ok = lattice_cell(p, g, blockIdx.x, threadIdx.x, ix, iy, iz);
+  const unsigned bal = __ballot_sync(0xffffffffu, ok);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) wsum[warp] = __popc(bal);
+  __syncthreads();
+  int before = 0;
+  for (int w = 0; w < warp; ++w) before += wsum[w];
+  if (!ok) return;
+  const int pos = b.scan_offsets[s] + p.tile_offsets[blockIdx.x] + before + __popc(bal & ((1u << lane) - 1u));
+  p.pts[3 * (size_t)pos] = __dadd_rn(p.ox, __dmul_rn((double)ix + 0.5, p.res));
+  p.pts[3 * (size_t)pos + 1] = __dadd_rn(p.oy, __dmul_rn((double)iy + 0.5, p.res));
+  p.pts[3 * (size_t)pos + 2] = 0.0;
+  p.out_idx[pos] = ix * p.ny + iy;
 }
 
 // ----------------------------------------------------------------------------
@@ -890,6 +1006,7 @@ struct SelectParams {
   int n_min;
   int* region_out;
   mwb_trace_t* trace;
+  long long dense_stride;  // batched selection: floats between consecutive scans' maps
   int staged;       // 1: the breast box's lattice is staged in shared memory
   int sl0[3], sL[3];  // staged lattice origin / extent (lattice units)
 };
@@ -929,7 +1046,12 @@ __device__ __forceinline__ void put_box(int32_t* dst, const Box& b) {
 }
 
 template <int NK>  // 4 children (2-D quadrants) or 8 (3-D octants)
-__global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams p) {
+__global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams p0) {
+  // CTA b handles scan b of a batch (maps dense_stride floats apart)
+  SelectParams p = p0;
+  p.dense += (size_t)blockIdx.x * p0.dense_stride;
+  p.region_out += 6 * blockIdx.x;
+  p.trace += blockIdx.x;
   __shared__ double red[8 * 2 * 2 * NK];
   __shared__ double res[2 * 2 * NK];
   __shared__ int ctl[2];
@@ -1545,9 +1667,9 @@ int64_t mwb_delay_table_bytes(int n_pts, int n_chan) {
   return (int64_t)table_layout(tiles > 0 ? tiles : 1, n_chan).total;
 }
 
-int mwb_delay_table(const double* pts_xyz, int n_pts, const int32_t* d_count, const int32_t* chan_txrx,
-                    int n_chan, const double* ant_xyz, int n_ant, double inv_scale, int interp,
-                    void* table, void* stream) {
+static int delay_table_impl(const double* pts_xyz, int n_pts, const int32_t* d_count, const int32_t* tile_info,
+                            const int32_t* chan_txrx, int n_chan, const double* ant_xyz, int n_ant,
+                            double inv_scale, int interp, void* table, void* stream) {
   if (n_pts < 0 || n_chan < 1 || n_ant < 1) return set_err(MWB_EINVAL, "mwb_delay_table: bad sizes");
   if (n_pts == 0) return MWB_OK;
   if (n_ant > MAX_ANT) return set_err(MWB_ERANGE, "mwb_delay_table: too many antennas (%d)", n_ant);
@@ -1568,6 +1690,7 @@ int mwb_delay_table(const double* pts_xyz, int n_pts, const int32_t* d_count, co
   p.M = n_ant;
   p.inv_scale = inv_scale;
   p.interp = interp;
+  p.tile_info = reinterpret_cast<const int2*>(tile_info);
   unsigned char* base = reinterpret_cast<unsigned char*>(table);
   p.words = reinterpret_cast<uint32_t*>(base + T.words);
   p.span = reinterpret_cast<int2*>(base + T.span);
@@ -1580,12 +1703,27 @@ int mwb_delay_table(const double* pts_xyz, int n_pts, const int32_t* d_count, co
   return check_launch("delay_table_kernel");
 }
 
-int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
-                 int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
-                 double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
-                 const int32_t* d_count, const void* table, int interp, int k0, int window,
-                 float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
-                 uint64_t* key_dmas, int32_t* flags, int mode, void* stream) {
+int mwb_delay_table(const double* pts_xyz, int n_pts, const int32_t* d_count, const int32_t* chan_txrx,
+                    int n_chan, const double* ant_xyz, int n_ant, double inv_scale, int interp,
+                    void* table, void* stream) {
+  return delay_table_impl(pts_xyz, n_pts, d_count, nullptr, chan_txrx, n_chan, ant_xyz, n_ant, inv_scale, interp,
+                          table, stream);
+}
+
+int mwb_delay_table_tiles(const double* pts_xyz, int n_pts, const int32_t* tile_info, const int32_t* chan_txrx,
+                          int n_chan, const double* ant_xyz, int n_ant, double inv_scale, int interp,
+                          void* table, void* stream) {
+  if (!tile_info) return set_err(MWB_EINVAL, "mwb_delay_table_tiles: null tile_info");
+  return delay_table_impl(pts_xyz, n_pts, nullptr, tile_info, chan_txrx, n_chan, ant_xyz, n_ant, inv_scale, interp,
+                          table, stream);
+}
+
+static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
+                         int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
+                         double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
+                         const int32_t* d_count, const int32_t* tile_info, const void* table, int interp, int k0,
+                         int window, float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
+                         uint64_t* key_dmas, int32_t* flags, int mode, void* stream) {
   if (n_pts < 0 || n_scans < 0 || n_chan < 0 || n_ant < 1 || window < 0 || k0 < 0)
     return set_err(MWB_EINVAL, "mwb_energies: negative size");
   if (n_pts == 0 || n_scans == 0) return MWB_OK;
@@ -1621,6 +1759,7 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
   p.out_idx = out_idx;
   p.P = n_pts;
   p.d_count = d_count;
+  p.tile_info = reinterpret_cast<const int2*>(tile_info);
   p.tab_words = reinterpret_cast<const uint32_t*>(base + T.words);
   p.tab_span = reinterpret_cast<const int2*>(base + T.span);
   p.tab_wide = reinterpret_cast<const int*>(base + T.wide);
@@ -1643,11 +1782,11 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
   if (cap > CAP_MAX) cap = CAP_MAX;
   if (cap < 256) cap = 256;
   p.cap = (int)cap;
-  p.scans_per_cta = choose_scans_per_cta((int)tiles, n_scans);
+  p.scans_per_cta = tile_info ? 1 : choose_scans_per_cta((int)tiles, n_scans);
   const SmemLayout L = smem_layout(n_chan, p.cap);
   if (L.total > 227 * 1024)
     return set_err(MWB_ERANGE, "mwb_energies: shared memory %lld bytes exceeds 227 KB", (long long)L.total);
-  dim3 grid((unsigned)tiles, (n_scans + p.scans_per_cta - 1) / p.scans_per_cta);
+  dim3 grid((unsigned)tiles, tile_info ? 1 : (n_scans + p.scans_per_cta - 1) / p.scans_per_cta);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int kind = out_das && out_dmas ? KIND_BOTH : (out_das ? KIND_DAS : KIND_DMAS);
   // MWB_MINB=4 selects the 4-CTA/SM (<=128 registers) build of the 32-sample kernel
@@ -1669,6 +1808,29 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
   if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   fn<<<grid, TPB, L.total, st>>>(p);
   return check_launch("energy_kernel");
+}
+
+int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
+                 int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
+                 double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
+                 const int32_t* d_count, const void* table, int interp, int k0, int window,
+                 float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
+                 uint64_t* key_dmas, int32_t* flags, int mode, void* stream) {
+  return energies_impl(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
+                       pts_xyz, out_idx, n_pts, d_count, nullptr, table, interp, k0, window, out_das, out_dmas,
+                       out_stride, key_das, key_dmas, flags, mode, stream);
+}
+
+int mwb_energies_tiles(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
+                       const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale,
+                       const double* pts_xyz, const int32_t* out_idx, int n_pts, const int32_t* tile_info,
+                       const void* table, int interp, int k0, int window, float* out_das, float* out_dmas,
+                       int64_t out_stride, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags, int mode,
+                       void* stream) {
+  if (!tile_info) return set_err(MWB_EINVAL, "mwb_energies_tiles: null tile_info");
+  return energies_impl(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
+                       pts_xyz, out_idx, n_pts, nullptr, tile_info, table, interp, k0, window, out_das, out_dmas,
+                       out_stride, key_das, key_dmas, flags, mode, stream);
 }
 
 static long long lattice_tiles(int nx, int ny, int nz, int stride, int tx, int ty, int tz) {
@@ -1758,7 +1920,88 @@ int mwb_enumerate_volume(double ox, double oy, double oz, double res, int nx, in
   return enumerate_common(p, 8, 8, 4, workspace, stream);
 }
 
-static int select_common(SelectParams& p, void* stream) {
+static RegionBatch region_batch(void* workspace, int tiles_bound, int n_scans) {
+  RegionBatch b;
+  b.n_scans = n_scans;
+  b.tiles_max = tiles_bound;
+  int* w = reinterpret_cast<int*>(workspace);
+  b.tile_counts = w;
+  w += (size_t)n_scans * b.tiles_max;
+  b.tile_offsets = w;
+  w += (size_t)n_scans * b.tiles_max;
+  b.scan_counts = w;
+  w += n_scans;
+  b.scan_offsets = w;
+  w += n_scans;
+  b.totals = w;
+  return b;
+}
+
+int64_t mwb_regions_workspace_bytes(int tiles_bound, int n_scans) {
+  if (tiles_bound < 1 || n_scans < 0) return -1;
+  return (long long)sizeof(int) * (2LL * tiles_bound * n_scans + 2LL * n_scans + 2) + 256;
+}
+
+int mwb_regions_tile_bound(const int32_t* d_regions, int n_scans, int32_t* d_bound, void* stream) {
+  if (n_scans < 1 || !d_regions || !d_bound) return set_err(MWB_EINVAL, "mwb_regions_tile_bound: bad arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(d_bound, 0, sizeof(int32_t), st);
+  region_bound_kernel<<<(n_scans + 255) / 256, 256, 0, st>>>(d_regions, n_scans, d_bound);
+  return check_launch("region_bound_kernel");
+}
+
+static LatticeParams region_params(double ox, double oy, double res, int nx, int ny, const int32_t* d_regions,
+                                   const uint8_t* mask, int skip_stride) {
+  LatticeParams p;
+  memset(&p, 0, sizeof(p));
+  p.ox = ox; p.oy = oy; p.oz = 0.0; p.res = res;
+  p.nx = nx; p.ny = ny; p.nz = 1;
+  p.planar = 1;
+  p.d_region = d_regions;
+  p.stride = 1;
+  p.mask = mask;
+  p.skip = skip_stride;
+  p.tx = 16; p.ty = 16; p.tz = 1;
+  return p;
+}
+
+int mwb_enumerate_regions_count(int nx, int ny, const int32_t* d_regions, int n_scans, int tiles_bound,
+                                const uint8_t* mask, int skip_stride, int32_t* d_totals, void* workspace,
+                                void* stream) {
+  if (nx < 1 || ny < 1 || n_scans < 1 || n_scans > 65535 || tiles_bound < 1)
+    return set_err(MWB_EINVAL, "mwb_enumerate_regions_count: bad sizes");
+  if (!d_regions || !d_totals || !workspace) return set_err(MWB_EINVAL, "mwb_enumerate_regions_count: null pointer");
+  RegionBatch b = region_batch(workspace, tiles_bound, n_scans);
+  LatticeParams p = region_params(0.0, 0.0, 1.0, nx, ny, d_regions, mask, skip_stride);
+  p.n_tiles_max = b.tiles_max;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  region_count_kernel<<<dim3(b.tiles_max, n_scans), 256, 0, st>>>(p, b);
+  region_scan_kernel<<<n_scans, 1024, 0, st>>>(p, b);
+  region_offsets_kernel<<<1, 1024, 0, st>>>(b);
+  cudaMemcpyAsync(d_totals, b.totals, 2 * sizeof(int), cudaMemcpyDeviceToDevice, st);
+  return check_launch("enumerate_regions_count");
+}
+
+int mwb_enumerate_regions_write(double ox, double oy, double res, int nx, int ny, const int32_t* d_regions,
+                                int n_scans, int tiles_bound, const uint8_t* mask, int skip_stride,
+                                double* pts_xyz, int32_t* out_idx, int32_t* tile_info, void* workspace,
+                                void* stream) {
+  if (nx < 1 || ny < 1 || n_scans < 1 || n_scans > 65535 || tiles_bound < 1)
+    return set_err(MWB_EINVAL, "mwb_enumerate_regions_write: bad sizes");
+  if (!d_regions || !pts_xyz || !out_idx || !tile_info || !workspace)
+    return set_err(MWB_EINVAL, "mwb_enumerate_regions_write: null pointer");
+  RegionBatch b = region_batch(workspace, tiles_bound, n_scans);
+  LatticeParams p = region_params(ox, oy, res, nx, ny, d_regions, mask, skip_stride);
+  p.n_tiles_max = b.tiles_max;
+  p.pts = pts_xyz;
+  p.out_idx = out_idx;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  region_tiles_kernel<<<n_scans, 256, 0, st>>>(b, reinterpret_cast<int2*>(tile_info));
+  region_write_kernel<<<dim3(b.tiles_max, n_scans), 256, 0, st>>>(p, b);
+  return check_launch("enumerate_regions_write");
+}
+
+static int select_common(SelectParams& p, void* stream, int n_scans = 1) {
   long long n = 1;
   for (int a = 0; a < 3; ++a) {
     p.sl0[a] = (p.breast.lo[a] + p.D - 1) / p.D;
@@ -1772,7 +2015,7 @@ static int select_common(SelectParams& p, void* stream) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(float) * SEL_STAGE_MAX));
   if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-  fn<<<1, SEL_TPB, sm, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  fn<<<n_scans, SEL_TPB, sm, reinterpret_cast<cudaStream_t>(stream)>>>(p);
   return check_launch("select_roi_kernel");
 }
 
@@ -1798,7 +2041,36 @@ int mwb_select_roi(const float* dense, const uint8_t* valid, int nx, int ny, int
   p.n_min = n_min;
   p.region_out = d_region_out;
   p.trace = d_trace;
+  p.dense_stride = 0;
   return select_common(p, stream);
+}
+
+int mwb_select_roi_batch(const float* dense, int64_t dense_stride, const uint8_t* valid, int nx, int ny,
+                         int lattice, int x0, int y0, int x1, int y1, double frame_fraction, int n_min, int n_scans,
+                         int32_t* d_regions_out, mwb_trace_t* d_traces, void* stream) {
+  if (n_scans < 0 || dense_stride < (int64_t)nx * ny) return set_err(MWB_EINVAL, "mwb_select_roi_batch: bad batch");
+  if (n_scans == 0) return MWB_OK;
+  if (nx < 1 || ny < 1 || lattice < 1) return set_err(MWB_EINVAL, "mwb_select_roi_batch: bad grid");
+  if (x0 < 0 || y0 < 0 || x1 >= nx || y1 >= ny || x0 > x1 || y0 > y1)
+    return set_err(MWB_EINVAL, "mwb_select_roi_batch: region outside the grid");
+  if (!(frame_fraction >= 0.0 && frame_fraction < 1.0) || n_min < 1)
+    return set_err(MWB_EINVAL, "mwb_select_roi_batch: bad frame_fraction / n_min");
+  if (!dense || !valid || !d_regions_out || !d_traces) return set_err(MWB_EINVAL, "mwb_select_roi_batch: null pointer");
+  SelectParams p;
+  p.dense = dense;
+  p.valid = valid;
+  p.nx = nx;
+  p.ny = ny;
+  p.nz = 1;
+  p.D = lattice;
+  p.dims = 2;
+  p.breast = Box{{x0, y0, 0}, {x1, y1, 0}};
+  p.frac = frame_fraction;
+  p.n_min = n_min;
+  p.region_out = d_regions_out;
+  p.trace = d_traces;
+  p.dense_stride = dense_stride;
+  return select_common(p, stream, n_scans);
 }
 
 int mwb_select_roi_volume(const float* dense, const uint8_t* valid, int nx, int ny, int nz,
@@ -1825,6 +2097,7 @@ int mwb_select_roi_volume(const float* dense, const uint8_t* valid, int nx, int 
   p.n_min = n_min;
   p.region_out = d_region_out;
   p.trace = d_trace;
+  p.dense_stride = 0;
   return select_common(p, stream);
 }
 
