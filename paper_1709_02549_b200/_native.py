@@ -7,6 +7,7 @@ There is no CPU fallback: if the library is missing or a call fails, a
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from ._build import LIB
@@ -151,6 +152,8 @@ def load(path: Path | str | None = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
+    if path is None and os.environ.get("MWB_LIB"):  # experiments: an alternative build
+        path = os.environ["MWB_LIB"]
     p = Path(path) if path is not None else LIB
     if not p.exists():
         raise RuntimeError(
@@ -162,7 +165,7 @@ def load(path: Path | str | None = None) -> C.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if path is None:
+    if path is None or os.environ.get("MWB_LIB") == str(path):
         _lib = lib
     return lib
 

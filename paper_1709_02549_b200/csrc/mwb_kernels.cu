@@ -189,10 +189,14 @@ __device__ __forceinline__ void accumulate_channel(float2 (&s)[CH], float2& qe, 
     a = __ffma2_rn(f1, nxt, a);
     s[k] = __fadd2_rn(s[k], a);
     if (KIND != KIND_DAS && (!TAIL || k < valid)) {
+#ifdef MWB_ONE_Q
+      qe = __ffma2_rn(a, a, qe);
+#else
       if (k & 1)
         qo = __ffma2_rn(a, a, qo);
       else
         qe = __ffma2_rn(a, a, qe);
+#endif
     }
     prev = nxt;
   }
@@ -306,7 +310,7 @@ struct TableParams {
 };
 
 __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   double* dist = reinterpret_cast<double*>(smem);                 // [M][TILE]
   double* amin = dist + (size_t)p.M * TILE;                      // [M]
   double* amax = amin + p.M;                                     // [M]
@@ -384,6 +388,11 @@ __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
   }
 }
 
+#ifndef MWB_CH_UNROLL
+#define MWB_CH_UNROLL 2  // two channels in flight per warp: +3.4% on configs[3] (scripts/variants.sh)
+#endif
+constexpr int kChannelUnroll = MWB_CH_UNROLL;  // channel-loop unroll (experiment knob)
+
 // (1 + f1) as fp32 bits in one LOP3: (w & 0x7FFFFF) | 0x3F800000
 __device__ __forceinline__ float one_plus_f1(uint32_t w) {
   uint32_t r;
@@ -400,6 +409,7 @@ __device__ __forceinline__ void channel_loop(float2 (&sacc)[CH], float2& qe, flo
                                              int valid, int cap) {
   const uint32_t* wp = tw + (size_t)c_begin * TILE;
   uint32_t wa = __ldg(wp + la), wb = __ldg(wp + lb);
+#pragma unroll kChannelUnroll
   for (int c = c_begin; c < c_end; ++c) {
     const uint32_t ca = wa, cw = wb;
     wp += TILE;
