@@ -409,14 +409,30 @@ __device__ __forceinline__ void channel_loop(float2 (&sacc)[CH], float2& qe, flo
                                              int valid, int cap) {
   const uint32_t* wp = tw + (size_t)c_begin * TILE;
   uint32_t wa = __ldg(wp + la), wb = __ldg(wp + lb);
+#ifdef MWB_PREFETCH2
+  uint32_t wa2 = 0, wb2 = 0;
+  if (c_begin + 1 < c_end) {
+    wa2 = __ldg(wp + TILE + la);
+    wb2 = __ldg(wp + TILE + lb);
+  }
+#endif
 #pragma unroll kChannelUnroll
   for (int c = c_begin; c < c_end; ++c) {
     const uint32_t ca = wa, cw = wb;
     wp += TILE;
+#ifdef MWB_PREFETCH2
+    wa = wa2;
+    wb = wb2;
+    if (c + 2 < c_end) {
+      wa2 = __ldg(wp + TILE + la);
+      wb2 = __ldg(wp + TILE + lb);
+    }
+#else
     if (c + 1 < c_end) {
       wa = __ldg(wp + la);
       wb = __ldg(wp + lb);
     }
+#endif
     const float2 f1 = __fadd2_rn(make_float2(one_plus_f1(ca), one_plus_f1(cw)), make_float2(-1.f, -1.f));
     const float2 f0 = __ffma2_rn(f1, make_float2(-1.f, -1.f), make_float2(1.f, 1.f));
     const float* base = buf + sb[c];
