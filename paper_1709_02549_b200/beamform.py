@@ -266,8 +266,9 @@ class _Status:
     def flags_ptr(self) -> int:
         return self.t.data_ptr() + 8 * self.N_KEYS + 8
 
-    def read(self) -> tuple[np.ndarray, np.ndarray, int]:
-        h = self.t.cpu().numpy()
+    def read(self, host: np.ndarray | None = None) -> tuple[np.ndarray, np.ndarray, int]:
+        """Decode the block; ``host`` is an already-copied image of ``self.t``."""
+        h = self.t.cpu().numpy() if host is None else host
         keys = h[: self.N_KEYS].view(np.uint64)
         tail = h[self.N_KEYS :].view(np.int32)
         return keys, tail[:2], int(tail[2])
@@ -454,16 +455,17 @@ def images(ds, kinds, grid: ImagingGrid, region: Region | None = None, stride: i
     status = _Status()
     lattice_pass(scan, grid, stride, dv.upload_mask(emask, (nx, ny)), 0, codes, nat.INTERP[interpolation], k0, w,
                  dense, valid, status, 0, bounds=region.bounds(), mode=_MODES[mode])
-    _, counts, flags = status.read()
+    st, vh, *dh = dv.to_host(status.t, valid.view(nx, ny), *(dense[c].view(nx, ny) for c in codes))
+    _, counts, flags = status.read(st)
     if flags & 1:
         raise ValueError("energy map contains non-finite values")
     n = int(counts[0])
-    vmask = valid.view(nx, ny).cpu().numpy().astype(bool)
+    vmask = vh.view(bool)
     out = {}
-    for c in codes:
+    for c, h in zip(codes, dh):
         EVAL_COUNTER.add(n)
         name = "das" if c == nat.MWB_DAS else "dmas"
-        out[name] = EnergyMap._from_dense(grid, dense[c].view(nx, ny).cpu().numpy(), vmask, stride, checked=True)
+        out[name] = EnergyMap._from_dense(grid, h, vmask, stride, checked=True)
     return out
 
 

@@ -142,12 +142,21 @@ __device__ __forceinline__ double antenna_distance(double px, double py, double 
 // fraction (beamform.py:186-190; nearest -> rint, 187-188).  The weights used by
 // every path are f1 = q * 2^-23, f0 = 1 - f1 (both exact in fp32, f0 + f1 == 1),
 // a function of the point alone, so a point's energy never depends on the tile.
+//
+// One conversion does both: n * 2^23 is exact (power-of-two scaling, n <= 2^30),
+// so v = floor(n * 2^23) = floor(n) * 2^23 + trunc((n - floor n) * 2^23), i.e.
+// i0 = v >> 23 and fq = v & (2^23 - 1), bit-identical to the two-step split.
+// (The delay-table kernel evaluates ~10^9 of these per 128^3 volume; this form
+// drops its FRND, one F2I and a DADD per word.)
 __device__ __forceinline__ void split_delay_q(double n, int interp, int& i0, uint32_t& fq) {
   if (interp == MWB_INTERP_NEAREST) n = rint(n);
-  n = fmin(fmax(n, 0.0), 1073741824.0);
-  const double fl = floor(n);
-  i0 = static_cast<int>(fl);
-  fq = static_cast<uint32_t>(__dmul_rn(__dsub_rn(n, fl), 8388608.0));  // trunc, < 2^23
+  // clamp to [0, 2^30] with NaN -> 0 (a failed compare selects the bound):
+  // the same result as fmin(fmax(n, 0), 2^30) without fmax's NaN fix-up code
+  n = n >= 0.0 ? n : 0.0;
+  n = n <= 1073741824.0 ? n : 1073741824.0;
+  const long long v = __double2ll_rd(__dmul_rn(n, 8388608.0));
+  i0 = static_cast<int>(v >> 23);
+  fq = static_cast<uint32_t>(v) & 0x7FFFFFu;
 }
 
 __device__ __forceinline__ float weight_f1(uint32_t fq) {
@@ -309,6 +318,31 @@ struct TableParams {
   const int2* tile_info;  // packed multi-scan lists: {scan, valid points} per tile, or NULL
 };
 
+// Word loop of delay_table_kernel for one thread's two points (da, da + TPB).
+// ~10^9 words per 128^3 volume and the loop is issue-bound, so: channel
+// offsets come pre-scaled to bytes from shared memory, the output pointer
+// advances one tile row per channel (no per-word index arithmetic), the
+// interpolation mode is a template parameter (no if-converted rint on the
+// linear path), and four channels per thread in flight hide fp64 latency.
+template <bool NEAREST>
+__device__ __forceinline__ void table_words(uint32_t* wp, const unsigned char* da, const int2* coff, const int* lo,
+                                            int C, double inv_scale) {
+  const int interp = NEAREST ? MWB_INTERP_NEAREST : MWB_INTERP_LINEAR;
+#pragma unroll 4
+  for (int c = 0; c < C; ++c, wp += TILE) {
+    const int2 o = coff[c];
+    const double* ta = reinterpret_cast<const double*>(da + o.x);
+    const double* ra = reinterpret_cast<const double*>(da + o.y);
+    int ia, ib;
+    uint32_t qa, qb;
+    split_delay_q(pair_delay(ta[0], ra[0], inv_scale), interp, ia, qa);
+    split_delay_q(pair_delay(ta[TPB], ra[TPB], inv_scale), interp, ib, qb);
+    const int l = lo[c];
+    wp[0] = ((uint32_t)min(max(ia - l, 0), SPAN_MAX) << 23) | qa;
+    wp[TPB] = ((uint32_t)min(max(ib - l, 0), SPAN_MAX) << 23) | qb;
+  }
+}
+
 __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* dist = reinterpret_cast<double*>(smem);                 // [M][TILE]
@@ -317,6 +351,7 @@ __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
   int* lo = reinterpret_cast<int*>(amax + p.M);                  // [C]
   int* hi = lo + p.C;                                            // [C]
   int* wide = hi + p.C;
+  int2* coff = reinterpret_cast<int2*>(wide + 2);                // [C] {tx, rx} row offsets in bytes
   const int tid = threadIdx.x;
   const int n_pts = p.d_count ? min(*p.d_count, p.P) : p.P;
   const int tile0 = blockIdx.x * TILE;
@@ -335,6 +370,8 @@ __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
   for (int c = tid; c < p.C; c += TPB) {
     lo[c] = 0x7FFFFFFF;
     hi[c] = -1;
+    coff[c] = make_int2(__ldg(p.chan + 2 * c) * TILE * (int)sizeof(double),
+                        __ldg(p.chan + 2 * c + 1) * TILE * (int)sizeof(double));
   }
   if (tid == 0) *wide = 0;
   __syncthreads();
@@ -375,17 +412,11 @@ __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
   __syncthreads();
   if (tid == 0) p.wide[tile] = *wide;
   if (*wide) return;  // wide tiles are evaluated from the points directly
-  uint32_t* w = p.words + tile * (size_t)p.C * TILE;
-  for (int c = 0; c < p.C; ++c) {
-    const int tx = __ldg(p.chan + 2 * c), rx = __ldg(p.chan + 2 * c + 1);
-    int ia, ib;
-    uint32_t qa, qb;
-    split_delay_q(pair_delay(dist[tx * TILE + la], dist[rx * TILE + la], p.inv_scale), p.interp, ia, qa);
-    split_delay_q(pair_delay(dist[tx * TILE + lb], dist[rx * TILE + lb], p.inv_scale), p.interp, ib, qb);
-    const int l = lo[c];
-    w[(size_t)c * TILE + la] = ((uint32_t)min(max(ia - l, 0), SPAN_MAX) << 23) | qa;
-    w[(size_t)c * TILE + lb] = ((uint32_t)min(max(ib - l, 0), SPAN_MAX) << 23) | qb;
-  }
+  uint32_t* wp = p.words + tile * (size_t)p.C * TILE + la;
+  if (p.interp == MWB_INTERP_NEAREST)
+    table_words<true>(wp, reinterpret_cast<const unsigned char*>(dist + la), coff, lo, p.C, p.inv_scale);
+  else
+    table_words<false>(wp, reinterpret_cast<const unsigned char*>(dist + la), coff, lo, p.C, p.inv_scale);
 }
 
 #ifndef MWB_CH_UNROLL
@@ -1721,7 +1752,8 @@ static int delay_table_impl(const double* pts_xyz, int n_pts, const int32_t* d_c
   p.words = reinterpret_cast<uint32_t*>(base + T.words);
   p.span = reinterpret_cast<int2*>(base + T.span);
   p.wide = reinterpret_cast<int*>(base + T.wide);
-  const size_t sm = sizeof(double) * ((size_t)n_ant * TILE + 2 * (size_t)n_ant) + sizeof(int) * (2 * (size_t)n_chan + 4);
+  const size_t sm = sizeof(double) * ((size_t)n_ant * TILE + 2 * (size_t)n_ant) + sizeof(int) * (2 * (size_t)n_chan + 2) +
+                    sizeof(int2) * (size_t)n_chan;
   if (sm > 227 * 1024) return set_err(MWB_ERANGE, "mwb_delay_table: shared memory %lld bytes", (long long)sm);
   cudaError_t e = cudaFuncSetAttribute(delay_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));

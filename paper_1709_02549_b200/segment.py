@@ -154,10 +154,12 @@ def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.0
     lattice_pass(scan, grid, 1, mask_t, 0, (kcode,), interp, k0, w, {kcode: dense}, valid, status, 0,
                  d_region=region_t)
     ev[2].record()
-    keys, counts, flags = status.read()
+    st, th, dh, vh, lh = dv.to_host(status.t, trace_t, dense.view(nx, ny), valid.view(nx, ny),
+                                    lowres.view(2 * n_sub, 2 * n_sub))
+    keys, counts, flags = status.read(st)
     if flags & 1:
         raise ValueError("energy map contains non-finite values")
-    tr = nat.SegTrace.from_buffer_copy(trace_t.cpu().numpy().tobytes())
+    tr = nat.SegTrace.from_buffer_copy(th.tobytes())
     records = []
     for i in range(int(tr.n_records)):
         r = tr.records[i]
@@ -168,8 +170,7 @@ def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.0
     final = _region(tr.final_region)
     n_fine = int(counts[0])
     EVAL_COUNTER.add(n_fine + 4 * n_sub * n_sub * len(records))
-    fine = EnergyMap._from_dense(grid, dense.view(nx, ny).cpu().numpy(), valid.view(nx, ny).cpu().numpy().astype(bool),
-                                 1, roi=final)
+    fine = EnergyMap._from_dense(grid, dh, vh.view(bool), 1, roi=final)
     key = int(keys[0 if kcode == nat.MWB_DAS else 1])
     if key:
         slot = 0xFFFFFFFF - (key & 0xFFFFFFFF)
@@ -179,7 +180,7 @@ def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.0
     full_eq = int(m.sum()) if m is not None else grid.dims[0] * grid.dims[1]
     report = SegmentReport(
         kind=_kind(kind).value, n_sub=n_sub, stop_cells=stop_cells, records=records, final_region=final,
-        lowres=lowres.view(2 * n_sub, 2 * n_sub).cpu().numpy(),
+        lowres=lh,
         subgrid_points_evaluated=4 * n_sub * n_sub * len(records), fine_points_evaluated=n_fine,
         full_equivalent_points=full_eq, argmax_cell=cell, argmax_position=grid.cell_center(*cell),
         elapsed={"search": ev[0].elapsed_time(ev[1]) / 1e3, "fine": ev[1].elapsed_time(ev[2]) / 1e3,

@@ -144,11 +144,14 @@ def hemisphere_mask(grid: VolumeGrid, radius: float, center=(0.0, 0.0, 0.0)) -> 
 class VolumeMap:
     """Dense-backed voxel energy map (the 3-D counterpart of EnergyMap)."""
 
-    def __init__(self, grid: VolumeGrid, values: np.ndarray, valid: np.ndarray, stride: int = 1, roi: Box | None = None):
+    def __init__(self, grid: VolumeGrid, values: np.ndarray, valid: np.ndarray, stride: int = 1, roi: Box | None = None,
+                 *, checked: bool = False):
+        """``checked``: the producing device pass already raised on its
+        non-finite flag, so the host scan of every voxel is skipped."""
         self.grid, self.stride, self.roi = grid, stride, roi
         self.values = values
         self.valid = valid
-        if valid.any() and not np.isfinite(values[valid]).all():
+        if not checked and valid.any() and not np.isfinite(values[valid]).all():
             raise ValueError("energy map contains non-finite values")
 
     def __len__(self) -> int:
@@ -231,15 +234,15 @@ def image_volume(ds, kinds, grid: VolumeGrid, box: Box | None = None, stride: in
     status = _Status()
     _volume_pass(scan, grid, box, stride, _upload_mask3(mask, grid.dims), 0, codes, nat.INTERP[interpolation], k0, w,
                  dense, valid, status, 0, mode={"smem": 0, "gather": 1}[mode])
-    _, counts, flags = status.read()
+    st, vh, *dh = dv.to_host(status.t, valid.view(*grid.dims), *(dense[c].view(*grid.dims) for c in codes))
+    _, counts, flags = status.read(st)
     if flags & 1:
         raise ValueError("energy map contains non-finite values")
-    vmask = valid.view(*grid.dims).cpu().numpy().astype(bool)
+    vmask = vh.view(bool)
     out = {}
-    for c in codes:
+    for c, h in zip(codes, dh):
         EVAL_COUNTER.add(int(counts[0]))
-        out["das" if c == nat.MWB_DAS else "dmas"] = VolumeMap(grid, dense[c].view(*grid.dims).cpu().numpy(), vmask,
-                                                               stride)
+        out["das" if c == nat.MWB_DAS else "dmas"] = VolumeMap(grid, h, vmask, stride, checked=True)
     return out
 
 
@@ -342,13 +345,13 @@ def run_framework_volume(ds, kind, grid: VolumeGrid, mode, cfg: FrameworkConfig 
     _volume_pass(scan, grid, full, 1, mask_t, d, (kcode,), interp, k0, w, {kcode: dense}, valid, status, 1,
                  d_region=region_t)
     ev[3].record()
-    keys, counts, flags = status.read()
+    st, th, values, vh = dv.to_host(status.t, trace_t, dense.view(*grid.dims), valid.view(*grid.dims))
+    keys, counts, flags = status.read(st)
     if flags & 1:
         raise ValueError("energy map contains non-finite values")
-    final, trace, _ = decode_trace(trace_t.cpu().numpy().tobytes(), region=_box)
-    values = dense.view(*grid.dims).cpu().numpy()
-    vmask = valid.view(*grid.dims).cpu().numpy().astype(bool)
-    composite = VolumeMap(grid, values, vmask, stride=d, roi=final)
+    final, trace, _ = decode_trace(th.tobytes(), region=_box)
+    vmask = vh.view(bool)
+    composite = VolumeMap(grid, values, vmask, stride=d, roi=final, checked=True)
     n_c, n_f = int(counts[0]), int(counts[1])
     EVAL_COUNTER.add(n_c + n_f)
     key = int(keys[0 if kcode == nat.MWB_DAS else 1])
