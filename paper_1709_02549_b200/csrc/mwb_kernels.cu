@@ -35,6 +35,9 @@ namespace {
 
 constexpr int TPB = 128;          // threads per energy CTA
 constexpr int TILE = 2 * TPB;     // focal points per CTA
+#ifndef MWB_W48_CH
+#define MWB_W48_CH 48  // register chunk for W % 48 == 0 windows (experiment knob: 24)
+#endif
 constexpr int WCH = 32;           // default window samples per register chunk (48 for W=48)
 constexpr int MAX_ANT = 64;
 constexpr int MAX_CHAN = 4096;
@@ -112,6 +115,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(addr), "r"(parity)
         : "memory");
   }
+}
+
+// Bulk prefetch of [src, src + bytes) into L2 (16-byte aligned, multiple of 16).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -616,6 +624,12 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
       if (n > 0)
         bulk_g2s(buf + coff[c], scan_sig + (size_t)c * p.ld + start4, (uint32_t)(n * 4), &mbar[b]);
     }
+    // The group's delay words ([c_begin, c_end) x TILE, contiguous) are read
+    // by every consumer thread NSTAGE - 1 steps from now.  A table larger than
+    // L2 (a 128^3 volume: 4.2 GB) would put DRAM latency on each channel's
+    // word load, so each chunk's first use of a group pulls its block into L2
+    // here (later scans of a multi-scan CTA find it there).
+    if (r < n_chunks && lane == 0) bulk_prefetch_l2(tw + (size_t)c_begin * TILE, (uint32_t)(c_end - c_begin) * TILE * 4u);
   };
 
   const int nsteps = (n_groups > 0 ? n_groups : 1) * n_chunks * n_my_scans;
@@ -1833,11 +1847,18 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   p.mode = mode;
   // register chunk: 48 samples for windows that are a multiple of 48 (the
   // configs[4] W = 48 would waste a third of a 2 x 32 split), else 32
-  const int ch = (window % 48 == 0 && window % 32 != 0) ? 48 : 32;
+  const int ch = (window % 48 == 0 && window % 32 != 0) ? MWB_W48_CH : 32;
+  const int resident = ch == 48 ? 2 : 3;  // CTAs per SM the register budget allows
   // stage capacity: every channel's span for a compact tile, capped at 32 KB
+  // and at what leaves `resident` CTAs room in the SM's 228 KB
   long long cap = (long long)n_chan * (ch + 24);
   cap = (cap + 3) & ~3LL;
   if (cap > CAP_MAX) cap = CAP_MAX;
+  {
+    const long long fixed = (long long)smem_layout(n_chan, 0).total + 1024;  // + per-CTA reserve
+    const long long fit = ((228LL * 1024 / resident - fixed) / (4LL * NSTAGE)) & ~3LL;
+    if (cap > fit) cap = fit;
+  }
   if (cap < 256) cap = 256;
   p.cap = (int)cap;
   p.scans_per_cta = tile_info ? 1 : choose_scans_per_cta((int)tiles, n_scans);
@@ -1856,6 +1877,11 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   if (ch == 48)
     fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 2, 48>
          : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 2, 48> : energy_kernel<KIND_BOTH, 2, 48>);
+#if MWB_W48_CH == 24
+  else if (ch == 24)
+    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 3, 24>
+         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 3, 24> : energy_kernel<KIND_BOTH, 3, 24>);
+#endif
   else if (minb == 4)
     fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 4, 32>
          : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 4, 32> : energy_kernel<KIND_BOTH, 4, 32>);
