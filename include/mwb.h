@@ -287,6 +287,26 @@ int mwb_simulate(float* out, int n_scans, int n_chan, int n_samples, int ld, con
                  double t0, int model, double a, double b, double c, const double* sigma_param, int noise_mode,
                  uint64_t seed, uint32_t* peak_ws, void* stream);
 
+/*
+ * One-call lattice image: the reference's image(ds, kind, grid, region,
+ * stride, mask, skip=stride-lattice) (mwbeam/beamform.py:283-342) as
+ * enumerate -> delay table -> one fused DAS/DMAS launch, all stream-ordered,
+ * no host sync.  Region {x0,y0,x1,y1} of an nx x ny grid (origin ox, oy;
+ * cell centres origin + (i + 0.5) * res).  Energies of the evaluated cells go
+ * to out_das / out_dmas (nx * ny dense, either may be NULL) at slot
+ * ix * ny + iy, and valid[slot] = 1; untouched cells keep their contents.
+ * d_count receives the number of evaluated cells.  key_das / key_dmas /
+ * flags are as in mwb_energies and must be zeroed by the caller, like valid.
+ * Workspace: mwb_image_lattice_workspace_bytes(nx, ny, stride, n_chan).
+ */
+int64_t mwb_image_lattice_workspace_bytes(int nx, int ny, int stride, int n_chan);
+int mwb_image_lattice(const float* sig, int n_chan, int ld, int n_samples, const int32_t* chan_txrx,
+                      const double* ant_xyz, int n_ant, double inv_scale, int interp, int k0, int window,
+                      double ox, double oy, double res, int nx, int ny, int x0, int y0, int x1, int y1,
+                      int stride, const uint8_t* mask, int skip_stride, float* out_das, float* out_dmas,
+                      uint8_t* valid, int32_t* d_count, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags,
+                      void* workspace, void* stream);
+
 /* argmax over a dense map (valid cells only); key as in mwb_energies. */
 int mwb_argmax_dense(const float* dense, const uint8_t* valid, int n, uint64_t* key,
                      void* stream);

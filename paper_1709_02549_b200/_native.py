@@ -129,6 +129,12 @@ _SIGNATURES = {
     ),
     "mwb_select_roi": ([_P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P], _I),
     "mwb_argmax_dense": ([_P, _P, _I, _P, _P], _I),
+    "mwb_image_lattice_workspace_bytes": ([_I, _I, _I, _I], _I64),
+    "mwb_image_lattice": (
+        [_P, _I, _I, _I, _P, _P, _I, _D, _I, _I, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _I, _P, _I,
+         _P, _P, _P, _P, _P, _P, _P, _P, _P],
+        _I,
+    ),
     "mwb_segment_workspace_bytes": ([_I, _I], _I64),
     "mwb_simulate": (
         [_P, _I, _I, _I, _I, _P, _P, _I, _P, _I, _D, _D, _D, _I, _D, _D, _D, _P, _I, C.c_uint64, _P, _P],

@@ -2264,6 +2264,53 @@ int mwb_segment(const float* sig, int n_chan, int ld, int n_samples, const int32
   return check_launch("seg_region_kernel");
 }
 
+// One-call lattice image (beamform.py:283-342 as a single C entry point): the
+// enumeration, delay table and fused energy launch of the Python `image()`
+// path, with every buffer supplied by the caller.  Workspace layout:
+// [points fp64 x3 | slots int32 | enumeration scratch | delay table].
+static size_t lattice_points_max(int nx, int ny, int stride) {
+  return (size_t)((nx + stride - 1) / stride) * (size_t)((ny + stride - 1) / stride);
+}
+
+int64_t mwb_image_lattice_workspace_bytes(int nx, int ny, int stride, int n_chan) {
+  if (nx < 1 || ny < 1 || stride < 1 || n_chan < 1) return -1;
+  const size_t pm = lattice_points_max(nx, ny, stride);
+  if (pm > 0x7FFFFFFFu) return -1;
+  const int64_t tb = mwb_delay_table_bytes((int)pm, n_chan);
+  if (tb < 0) return -1;
+  return (int64_t)(align_up(24 * pm, 256) + align_up(4 * pm, 256) +
+                   align_up((size_t)mwb_lattice_workspace_bytes(nx, ny, stride), 256) + (size_t)tb);
+}
+
+int mwb_image_lattice(const float* sig, int n_chan, int ld, int n_samples, const int32_t* chan_txrx,
+                      const double* ant_xyz, int n_ant, double inv_scale, int interp, int k0, int window,
+                      double ox, double oy, double res, int nx, int ny, int x0, int y0, int x1, int y1,
+                      int stride, const uint8_t* mask, int skip_stride, float* out_das, float* out_dmas,
+                      uint8_t* valid, int32_t* d_count, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags,
+                      void* workspace, void* stream) {
+  if (!out_das && !out_dmas) return set_err(MWB_EINVAL, "mwb_image_lattice: no output map");
+  const int64_t need = mwb_image_lattice_workspace_bytes(nx, ny, stride, n_chan);
+  if (need < 0) return set_err(MWB_EINVAL, "mwb_image_lattice: bad grid / stride / channels");
+  if (!workspace) return set_err(MWB_EINVAL, "mwb_image_lattice: null workspace");
+  const size_t pm = lattice_points_max(nx, ny, stride);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  double* pts = reinterpret_cast<double*>(ws);
+  ws += align_up(24 * pm, 256);
+  int32_t* slots = reinterpret_cast<int32_t*>(ws);
+  ws += align_up(4 * pm, 256);
+  void* scratch = ws;
+  ws += align_up((size_t)mwb_lattice_workspace_bytes(nx, ny, stride), 256);
+  void* table = ws;
+  int rc = mwb_enumerate_lattice(ox, oy, res, nx, ny, x0, y0, x1, y1, nullptr, stride, mask, skip_stride, pts, slots,
+                                 d_count, valid, scratch, stream);
+  if (rc) return rc;
+  if ((rc = mwb_delay_table(pts, (int)pm, d_count, chan_txrx, n_chan, ant_xyz, n_ant, inv_scale, interp, table,
+                            stream)))
+    return rc;
+  return mwb_energies(sig, 1, 0, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale, pts, slots, (int)pm,
+                      d_count, table, interp, k0, window, out_das, out_dmas, 0, key_das, key_dmas, flags, 0, stream);
+}
+
 int mwb_argmax_dense(const float* dense, const uint8_t* valid, int n, uint64_t* key, void* stream) {
   if (n < 0 || !dense || !valid || !key) return set_err(MWB_EINVAL, "mwb_argmax_dense: bad arguments");
   if (n == 0) return MWB_OK;

@@ -81,6 +81,11 @@ def test_argument_errors_set_last_error(lib):
     assert rc == -1
     assert lib.mwb_lattice_workspace_bytes(0, 5, 1) == -1
     assert lib.mwb_lattice_workspace_bytes(100, 100, 1) > 0
+    assert lib.mwb_image_lattice_workspace_bytes(100, 100, 0, 66) == -1
+    assert lib.mwb_image_lattice_workspace_bytes(100, 100, 2, 66) >= 50 * 50 * (24 + 4 + 66 * 4)
+    rc = lib.mwb_image_lattice(None, 66, 1024, 1024, None, None, 12, 1.0, 0, 0, 32, 0.0, 0.0, 1e-3, 100, 100,
+                               0, 0, 99, 99, 1, None, 0, None, None, None, None, None, None, None, None, None)
+    assert rc == -1 and b"no output" in lib.mwb_last_error()
 
 
 def test_native_check_raises_with_message(lib):
