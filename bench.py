@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--scans", type=int, default=4096)
     ap.add_argument("--grid", type=int, default=256)
     ap.add_argument("--chunk", type=int, default=128)
-    ap.add_argument("--mode", choices=["smem", "gather"], default="smem")
+    ap.add_argument("--mode", choices=["smem", "gather", "tc", "auto"], default="smem")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-configs", action="store_true")

@@ -288,6 +288,26 @@ int mwb_simulate(float* out, int n_scans, int n_chan, int n_samples, int ld, con
                  uint64_t seed, uint32_t* peak_ws, void* stream);
 
 /*
+ * Tensor-core (tcgen05) variant of mwb_energies for many scans of one
+ * geometry (no tile_info): per channel the tile's interpolation weights
+ * [256 x 16] multiply the Hankel windows of 8 scans [16 x 256] in fp16 hi/lo
+ * split (about fp32 accuracy), accumulated over channels in TMEM; DMAS's
+ * channel self-terms come from windowed Gram entries.  Requirements: window
+ * == 32 and every tile's per-channel delay spread <= 14 samples (check once
+ * per table with mwb_table_max_span); otherwise use mwb_energies.  A tile
+ * found to violate the spread limit sets bit 1 (value 2) of *flags.
+ * Workspace: mwb_energies_tc_workspace_bytes(n_scans) (per-scan scales).
+ */
+int64_t mwb_energies_tc_workspace_bytes(int n_scans);
+int mwb_table_max_span(const void* table, int n_pts, int n_chan, int32_t* d_out, void* stream);
+int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
+                    const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale,
+                    const double* pts_xyz, const int32_t* out_idx, int n_pts, const int32_t* d_count,
+                    const void* table, int interp, int k0, int window, float* out_das, float* out_dmas,
+                    int64_t out_stride, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags, void* workspace,
+                    void* stream);
+
+/*
  * One-call lattice image: the reference's image(ds, kind, grid, region,
  * stride, mask, skip=stride-lattice) (mwbeam/beamform.py:283-342) as
  * enumerate -> delay table -> one fused DAS/DMAS launch, all stream-ordered,

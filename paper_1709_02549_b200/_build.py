@@ -37,7 +37,8 @@ def needs_build() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    return any(p.stat().st_mtime > t for p in (SRC, HEADER, Path(__file__)))
+    deps = [HEADER, Path(__file__), *SRC.parent.glob("*.cu"), *SRC.parent.glob("*.cuh")]
+    return any(p.stat().st_mtime > t for p in deps)
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:

@@ -42,7 +42,9 @@ class BatchImager:
         self.ld = dv.round4(n_samples)
         self.k0, self.w = _window(self.n_samples, window)
         self.interp = nat.INTERP[interpolation]
-        self.mode = {"smem": 0, "gather": 1}[mode]
+        if mode not in ("smem", "gather", "tc", "auto"):
+            raise ValueError(f"unknown mode {mode!r}")
+        self.mode = {"smem": 0, "gather": 1, "tc": 2, "auto": 2}[mode]
         pairs = np.asarray(pairs, dtype=np.int32).reshape(-1, 2)
         m = geometry.n_antennas
         if pairs.size == 0 or pairs.min() < 0 or pairs.max() >= m:
@@ -74,6 +76,34 @@ class BatchImager:
         self.valid_host = self.valid.view(nx, ny).cpu().numpy().astype(bool)
         # per-point delay table: computed once, shared by every scan and kind
         self.table = build_table(self.scan, self.pts, self.n_pts, self.interp) if self.n_pts else None
+        # tensor-core path (mwb_energies_tc): needs W == 32 and every tile's
+        # per-channel delay spread within its 16 taps; checked once per table
+        if self.mode == 2:
+            ok, why = self.tc_eligible()
+            if not ok:
+                if mode == "tc":
+                    raise ValueError(f"tensor-core path unavailable: {why}")
+                self.mode = 0
+        self._tc_ws = None
+
+    TC_WINDOW, TC_MAX_SPAN = 32, 14
+
+    def tc_eligible(self) -> tuple[bool, str]:
+        if self.w != self.TC_WINDOW:
+            return False, f"window {self.w} != {self.TC_WINDOW}"
+        if not self.n_pts:
+            return True, ""
+        out = torch.zeros(1, dtype=torch.int32, device=dv.device())
+        nat.call("mwb_table_max_span", self.table.data_ptr(), self.n_pts, self.n_chan, out.data_ptr(),
+                 dv.stream_handle())
+        span = int(out.item())
+        if span > self.TC_MAX_SPAN:
+            return False, f"tile delay spread {span} > {self.TC_MAX_SPAN} samples"
+        return True, ""
+
+    @property
+    def uses_tensor_cores(self) -> bool:
+        return self.mode == 2
 
     @property
     def n_chan(self) -> int:
@@ -104,6 +134,18 @@ class BatchImager:
             for out in (out_das, out_dmas):
                 if out is not None:
                     out.zero_()
+            return
+        if self.mode == 2:
+            nbytes = int(nat.load().mwb_energies_tc_workspace_bytes(s))
+            if self._tc_ws is None or self._tc_ws.numel() < nbytes:
+                self._tc_ws = torch.empty(nbytes, dtype=torch.uint8, device=sig.device)
+            nat.call(
+                "mwb_energies_tc", sig.data_ptr(), s, self.n_chan * self.ld, self.n_chan, self.ld, self.n_samples,
+                self.scan.chan.data_ptr(), self.scan.ant.data_ptr(), self.scan.n_ant, self.scan.inv_scale,
+                self.pts.data_ptr(), self.oidx.data_ptr(), self.n_pts, None, self.table.data_ptr(), self.interp,
+                self.k0, self.w, nat.ptr(out_das), nat.ptr(out_dmas), nxny, nat.ptr(key_das), nat.ptr(key_dmas),
+                nat.ptr(flags), self._tc_ws.data_ptr(), dv.stream_handle(),
+            )
             return
         nat.call(
             "mwb_energies", sig.data_ptr(), s, self.n_chan * self.ld, self.n_chan, self.ld, self.n_samples,

@@ -22,6 +22,8 @@
 //   * 32 window samples per point live in registers (float2 s[32]); the
 //     per-point accumulation order over channels and samples is fixed.
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <algorithm>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdarg.h>
@@ -1719,6 +1721,8 @@ int choose_scans_per_cta(int tiles, int n_scans) {
   return (int)spc;
 }
 
+#include "mwb_tc.cuh"
+
 }  // namespace
 
 // ============================================================================
@@ -1790,15 +1794,21 @@ int mwb_delay_table_tiles(const double* pts_xyz, int n_pts, const int32_t* tile_
                           table, stream);
 }
 
-static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
-                         int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
-                         double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
-                         const int32_t* d_count, const int32_t* tile_info, const void* table, int interp, int k0,
-                         int window, float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
-                         uint64_t* key_dmas, int32_t* flags, int mode, void* stream) {
+// Argument checks and EnergyParams of mwb_energies / mwb_energies_tiles /
+// mwb_energies_tc.  Returns MWB_OK with *empty set when there is no work.
+static int energy_params(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
+                         const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale,
+                         const double* pts_xyz, const int32_t* out_idx, int n_pts, const int32_t* d_count,
+                         const int32_t* tile_info, const void* table, int interp, int k0, int window,
+                         float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
+                         uint64_t* key_dmas, int32_t* flags, int mode, EnergyParams& p, bool& empty) {
+  empty = false;
   if (n_pts < 0 || n_scans < 0 || n_chan < 0 || n_ant < 1 || window < 0 || k0 < 0)
     return set_err(MWB_EINVAL, "mwb_energies: negative size");
-  if (n_pts == 0 || n_scans == 0) return MWB_OK;
+  if (n_pts == 0 || n_scans == 0) {
+    empty = true;
+    return MWB_OK;
+  }
   if (n_chan == 0 || window == 0)
     return set_err(MWB_EINVAL, "mwb_energies: no channels or empty window");
   if (!out_das && !out_dmas) return set_err(MWB_EINVAL, "mwb_energies: no output (kind) requested");
@@ -1816,7 +1826,6 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   const long long tiles = (n_pts + TILE - 1) / TILE;
   const TableLayout T = table_layout(tiles, n_chan);
   const unsigned char* base = reinterpret_cast<const unsigned char*>(table);
-  EnergyParams p;
   p.sig = sig;
   p.scan_stride = scan_stride;
   p.n_scans = n_scans;
@@ -1845,6 +1854,24 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   p.key_dmas = reinterpret_cast<unsigned long long*>(key_dmas);
   p.flags = flags;
   p.mode = mode;
+  p.scans_per_cta = 1;
+  p.cap = 0;
+  return MWB_OK;
+}
+
+static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
+                         int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
+                         double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
+                         const int32_t* d_count, const int32_t* tile_info, const void* table, int interp, int k0,
+                         int window, float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
+                         uint64_t* key_dmas, int32_t* flags, int mode, void* stream) {
+  EnergyParams p;
+  bool empty;
+  const int rc = energy_params(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant,
+                               inv_scale, pts_xyz, out_idx, n_pts, d_count, tile_info, table, interp, k0, window,
+                               out_das, out_dmas, out_stride, key_das, key_dmas, flags, mode, p, empty);
+  if (rc || empty) return rc;
+  const long long tiles = (n_pts + TILE - 1) / TILE;
   // register chunk: 48 samples for windows that are a multiple of 48 (the
   // configs[4] W = 48 would waste a third of a 2 x 32 split), else 32
   const int ch = (window % 48 == 0 && window % 32 != 0) ? MWB_W48_CH : 32;
@@ -1915,6 +1942,72 @@ int mwb_energies_tiles(const float* sig, int n_scans, int64_t scan_stride, int n
   return energies_impl(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
                        pts_xyz, out_idx, n_pts, nullptr, tile_info, table, interp, k0, window, out_das, out_dmas,
                        out_stride, key_das, key_dmas, flags, mode, stream);
+}
+
+// ---- tensor-core path (mwb_tc.cuh) ----------------------------------------
+int64_t mwb_energies_tc_workspace_bytes(int n_scans) {
+  if (n_scans < 0) return -1;
+  return (int64_t)align_up(sizeof(uint32_t) * (size_t)(n_scans > 0 ? n_scans : 1), 256);
+}
+
+int mwb_table_max_span(const void* table, int n_pts, int n_chan, int32_t* d_out, void* stream) {
+  if (!table || !d_out || n_pts < 0 || n_chan < 1) return set_err(MWB_EINVAL, "mwb_table_max_span: bad arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(d_out, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
+  if (n_pts == 0) return MWB_OK;
+  const long long tiles = (n_pts + TILE - 1) / TILE;
+  const TableLayout T = table_layout(tiles, n_chan);
+  const unsigned char* base = reinterpret_cast<const unsigned char*>(table);
+  long long blocks = (tiles * n_chan + 255) / 256;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  tc::table_max_span_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const int2*>(base + T.span),
+                                                              reinterpret_cast<const int*>(base + T.wide), tiles,
+                                                              n_chan, d_out);
+  return check_launch("table_max_span_kernel");
+}
+
+int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
+                    const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale,
+                    const double* pts_xyz, const int32_t* out_idx, int n_pts, const int32_t* d_count,
+                    const void* table, int interp, int k0, int window, float* out_das, float* out_dmas,
+                    int64_t out_stride, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags, void* workspace,
+                    void* stream) {
+  EnergyParams e;
+  bool empty;
+  int rc = energy_params(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
+                         pts_xyz, out_idx, n_pts, d_count, nullptr, table, interp, k0, window, out_das, out_dmas,
+                         out_stride, key_das, key_dmas, flags, 0, e, empty);
+  if (rc || empty) return rc;
+  if (window != tc::W) return set_err(MWB_EINVAL, "mwb_energies_tc: window must be %d (got %d)", tc::W, window);
+  if (!workspace) return set_err(MWB_EINVAL, "mwb_energies_tc: null workspace");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint32_t* absmax = reinterpret_cast<uint32_t*>(workspace);
+  cudaError_t ce = cudaMemsetAsync(absmax, 0, sizeof(uint32_t) * (size_t)n_scans, st);
+  if (ce != cudaSuccess) return set_err(MWB_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
+  const long long per_scan = (long long)n_chan * ld;
+  const unsigned bx = (unsigned)std::min<long long>(8, (per_scan / 4 + 255) / 256);
+  tc::scan_absmax_kernel<<<dim3(bx, (unsigned)n_scans), 256, 0, st>>>(sig, scan_stride, per_scan, absmax);
+  if ((rc = check_launch("scan_absmax_kernel"))) return rc;
+  tc::Params P;
+  P.e = e;
+  P.absmax = absmax;
+  P.n_tiles = (n_pts + TILE - 1) / TILE;
+  P.n_groups = (n_scans + tc::SPG - 1) / tc::SPG;
+  const tc::Layout L = tc::layout();
+  const int kind = out_das && out_dmas ? KIND_BOTH : (out_das ? KIND_DAS : KIND_DMAS);
+  void (*fn)(tc::Params) = kind == KIND_DAS    ? tc::energy_tc_kernel<KIND_DAS>
+                           : kind == KIND_DMAS ? tc::energy_tc_kernel<KIND_DMAS>
+                                               : tc::energy_tc_kernel<KIND_BOTH>;
+  ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  if (ce != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(ce));
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long items = (long long)P.n_tiles * P.n_groups;
+  const unsigned grid = (unsigned)std::min<long long>(items, sms > 0 ? sms : 148);
+  fn<<<grid, tc::THREADS, L.total, st>>>(P);
+  return check_launch("energy_tc_kernel");
 }
 
 static long long lattice_tiles(int nx, int ny, int nz, int stride, int tx, int ty, int tz) {

@@ -1,0 +1,500 @@
+// Tensor-core (tcgen05 / TMEM / TMA) path of the multi-scan energy kernel.
+// Included by mwb_kernels.cu after the PTX helpers, EnergyParams and the
+// delay-table layout.
+//
+// Restatement of _multistatic_energies (mwbeam/beamform.py:169-212) for a
+// 256-point table tile and a group of SPG scans of one geometry, with the
+// per-sample channel sum on the tensor cores:
+//
+//   S[p, (s, k)] = sum_c sum_m A_c[p, m] * H_{c,s}[m, k]
+//
+//   A_c[p, m]     = f0(p,c) at m = d, f1(p,c) at m = d + 1, else 0, where
+//                   d = i0(p,c) - lo_c is the delay word's offset in the
+//                   tile's span (scan-independent: built once per channel and
+//                   reused by all SPG scans of the group),
+//   H_{c,s}[m, k] = y_{c,s}[k0 + lo_c + m + k]  (Hankel of the staged window).
+//
+// So S is a [256 x 16] x [16 x (SPG * W)] product per channel, accumulated
+// over the channels in TMEM (fp32).  DAS = sum_k S^2 (beamform.py:211).
+// DMAS = 1/2 (sum_k S^2 - Q) (beamform.py:212) with
+//   Q[p, s] = sum_c sum_k a^2 = sum_c f0^2 e(d) + 2 f0 f1 x(d) + f1^2 e(d+1),
+// e(d) = sum_k y[d+k]^2 and x(d) = sum_k y[d+k] y[d+k+1] over the window
+// (windowed Gram entries of the staged samples, one warp prefix scan per
+// (channel, scan)), gathered per point on the CUDA cores.
+//
+// Precision: operands are split hi + lo in fp16 (y scaled per scan by a power
+// of two so |y| < 2^15), and S = A_hi H_hi + A_hi H_lo + A_lo H_hi (the
+// dropped A_lo H_lo term is ~2^-22 relative), i.e. about fp32 accuracy.
+//
+// Roles (576 threads, one CTA per SM, persistent over (tile, group) items):
+//   warps 0-15 builders in two groups of 8 taking alternate channel steps:
+//              thread pt of a group owns point pt (its A row, Q); warp w8 of
+//              a group owns scan w8 (its 32 Hankel rows and Gram entries);
+//              group 0 also runs the TMEM epilogue
+//   warp 16    producer: TMA bulk copies of each channel's window spans
+//   warp 17    MMA issuer: one thread, 6 tcgen05.mma per channel
+// Rings: samples (NS deep, full/empty mbarriers), operands (NO deep, full by
+// the builders, empty by tcgen05.commit), accumulator (full by commit, empty
+// by the builders after the epilogue's tcgen05.ld).
+
+namespace tc {
+
+constexpr int W = 32;                      // window samples (this build)
+constexpr int SPG = 8;                     // scans per group
+constexpr int N = SPG * W;                 // MMA N: 256
+constexpr int K = 16;                      // taps per channel: d + 1 <= K - 1
+constexpr int SPANF = 52;                  // staged floats per (scan, channel): 3 + W + K, rounded to 4
+constexpr int NS = 8;                      // sample ring depth
+constexpr int NO = 4;                      // operand ring depth
+constexpr int NBW = 16;                    // builder warps: two groups of 8 (alternate steps)
+constexpr int NBT = NBW * 32;              // builder threads (2 x TILE)
+constexpr int GW = 8;                      // warps per builder group
+constexpr int THREADS = NBT + 64;          // + producer warp + MMA warp
+constexpr int A_BYTES = TILE * K * 2;      // one of hi/lo, both M-blocks: 8 KB
+constexpr int MB_BYTES = 128 * K * 2;      // one M-block: 4 KB
+constexpr int H_BYTES = N * K * 2;         // 8 KB
+constexpr int OP_BYTES = 2 * A_BYTES + 2 * H_BYTES;
+constexpr int STAGE_BYTES = SPG * SPANF * 4;
+constexpr int TMEM_COLS = 512;             // two M-blocks x N fp32 columns
+constexpr uint32_t LBO = 128, SBO = 256;   // core-matrix strides (bytes)
+constexpr size_t SMEM_MIN = 120 * 1024;    // > half the SM: one CTA per SM (TMEM is sized for one)
+
+struct Layout {
+  size_t ops, stage, g, qx, bar, tmem, total;
+};
+
+__host__ __device__ inline Layout layout() {
+  Layout L;
+  size_t o = 0;
+  L.ops = o;   o += (size_t)NO * OP_BYTES;
+  L.stage = o; o += (size_t)NS * STAGE_BYTES;
+  L.g = o;     o += 4 * (size_t)SPG * 16 * sizeof(float4);  // {e(d), x(d), e(d+1), 0}: 2 groups x 2 steps
+  L.qx = o;    o += (size_t)SPG * TILE * sizeof(float);      // group 1's Q partial sums
+  o = align_up(o, 8);
+  L.bar = o;   o += sizeof(uint64_t) * (2 * NS + 2 * NO + 2);
+  L.tmem = o;  o += 16;
+  L.total = o < SMEM_MIN ? SMEM_MIN : align_up(o, 128);
+  return L;
+}
+
+// byte offset of (row r, tap m) in a K-major, no-swizzle operand of 8 x 16 B
+// core matrices: the two 8-tap halves LBO apart, 8-row groups SBO apart
+__device__ __forceinline__ uint32_t kmajor_off(int r, int half) {
+  return (uint32_t)(r >> 3) * SBO + (uint32_t)half * LBO + (uint32_t)(r & 7) * 16u;
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((LBO >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((SBO >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);  // version 1, no swizzle
+}
+
+// kind::f16 instruction descriptor: f16 x f16 -> f32, both K-major
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void builders_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NBT) : "memory"); }
+__device__ __forceinline__ void group_sync(int gp) {
+  asm volatile("bar.sync %0, %1;" ::"r"(2 + gp), "n"(GW * 32) : "memory");
+}
+
+// 32 consecutive fp32 TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// hi/lo fp16 split of two values, packed as half2 words
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 back = __half22float2(h);
+  const __half2 l = __floats2half2_rn(a - back.x, b - back.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// power-of-two scale putting a scan's max |y| in [2^14, 2^15); 1 for an
+// all-zero or non-finite scan (non-finite energies are flagged downstream)
+__device__ __forceinline__ int scale_exp(uint32_t absmax_bits) {
+  if (absmax_bits == 0u || absmax_bits >= 0x7F800000u) return 0;
+  const int e = (int)(absmax_bits >> 23) - 127;  // floor(log2 max) (subnormals: -127)
+  return max(-100, min(100, 14 - e));
+}
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((e + 127) << 23); }
+
+__device__ __forceinline__ float warp_incl_scan(float v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
+struct Params {
+  EnergyParams e;
+  const uint32_t* absmax;  // [n_scans] bits of max |y| per scan
+  int n_tiles;
+  int n_groups;
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const EnergyParams& p = P.e;
+  const Layout L = layout();
+  unsigned char* ops = smem + L.ops;
+  float* stage = reinterpret_cast<float*>(smem + L.stage);
+  float* gbuf = reinterpret_cast<float*>(smem + L.g);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  uint64_t* s_full = bar;
+  uint64_t* s_empty = bar + NS;
+  uint64_t* o_full = bar + 2 * NS;
+  uint64_t* o_empty = bar + 2 * NS + NO;
+  uint64_t* acc_full = bar + 2 * NS + 2 * NO;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_pts = p.d_count ? min(*p.d_count, p.P) : p.P;
+  const int n_items = P.n_tiles * P.n_groups;
+
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&s_full[i], 32);
+      mbar_init(&s_empty[i], GW);
+    }
+    for (int i = 0; i < NO; ++i) {
+      mbar_init(&o_full[i], GW);
+      mbar_init(&o_empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, GW);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == NBW) {
+    // ===== producer: stage channel c's window span of every scan in the group
+    int t = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int tile = item % P.n_tiles, group = item / P.n_tiles;
+      if (tile * TILE >= n_pts) continue;
+      const int2* tsp = p.tab_span + (size_t)tile * p.C;
+      int lo32 = 0;  // lane i holds lo of channel (c & ~31) + i
+      for (int c = 0; c < p.C; ++c, ++t) {
+        const int slot = t % NS, use = t / NS;
+        if ((c & 31) == 0) lo32 = c + lane < p.C ? __ldg(&tsp[c + lane].x) : 0;
+        const int lo_c = __shfl_sync(0xffffffffu, lo32, c & 31);
+        if (use > 0) mbar_wait(&s_empty[slot], (use - 1) & 1);
+        const long long start4 = ((long long)p.k0 + lo_c) & ~3LL;
+        const int s = group * SPG + lane;
+        float* dst = stage + slot * (STAGE_BYTES / 4) + lane * SPANF;
+        long long n = 0;
+        if (lane < SPG) {
+          if (s < p.n_scans) n = min((long long)SPANF, max((long long)p.ld - start4, 0LL));
+          for (long long j = n; j < SPANF; ++j) dst[j] = 0.f;
+        }
+        uint32_t bytes = (uint32_t)(n * 4);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+        if (lane == 0)
+          mbar_arrive_expect_tx(&s_full[slot], bytes);
+        else
+          mbar_arrive(&s_full[slot]);
+        __syncwarp();
+        if (n > 0)
+          bulk_g2s(dst, p.sig + (size_t)s * (size_t)p.scan_stride + (size_t)c * p.ld + start4, (uint32_t)(n * 4),
+                   &s_full[slot]);
+      }
+    }
+  } else if (warp == NBW + 1) {
+    // ===== MMA issuer (one thread)
+    if (lane == 0) {
+      int t = 0, it = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int tile = item % P.n_tiles;
+        if (tile * TILE >= n_pts) continue;
+        if (it > 0) mbar_wait(acc_empty, (it - 1) & 1);
+        fence_after();
+        for (int c = 0; c < p.C; ++c, ++t) {
+          const int slot = t % NO;
+          mbar_wait(&o_full[slot], (t / NO) & 1);
+          fence_after();
+          const uint32_t base = smem_u32(ops + (size_t)slot * OP_BYTES);
+          const uint64_t b_hi = smem_desc(base + 2 * A_BYTES), b_lo = smem_desc(base + 2 * A_BYTES + H_BYTES);
+#pragma unroll
+          for (int mb = 0; mb < 2; ++mb) {
+            const uint64_t a_hi = smem_desc(base + mb * MB_BYTES), a_lo = smem_desc(base + A_BYTES + mb * MB_BYTES);
+            const uint32_t d = tmem + (uint32_t)(mb * N);
+            mma(d, a_hi, b_hi, c > 0 ? 1u : 0u);
+            mma(d, a_hi, b_lo, 1u);
+            mma(d, a_lo, b_hi, 1u);
+          }
+          commit(&o_empty[slot]);
+        }
+        commit(acc_full);
+        ++it;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===== builders + epilogue: two groups of 8 warps take alternate
+    // pipeline steps (gp = warp >> 3: steps t with t % 2 == gp), so two
+    // channels' operand chains are in flight at once.  Within a group thread
+    // pt (0..255) owns point pt (A row, Q) and warp w8 = warp & 7 owns scan w8
+    // of the group (its 32 Hankel rows and Gram entries).  Group 0 also runs
+    // the epilogue (TMEM lane quarter w8 & 3 of M-block w8 >> 2).
+    const int gp = warp >> 3, w8 = warp & 7;
+    const int pt = w8 * 32 + lane;
+    const int mb = pt >> 7, row = pt & 127;
+    int t = 0, it = 0, my = 0;  // my: this group's step count (Gram buffer parity)
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int tile = item % P.n_tiles, group = item / P.n_tiles;
+      const int tile0 = tile * TILE;
+      if (tile0 >= n_pts) continue;
+      const int n_in = min(TILE, n_pts - tile0);
+      const int nsg = min(SPG, p.n_scans - group * SPG);
+      const uint32_t* tw = p.tab_words + (size_t)tile * p.C * TILE;
+      const int2* tsp = p.tab_span + (size_t)tile * p.C;
+      const int h_scan = group * SPG + w8;
+      const float h_scale = pow2f(h_scan < p.n_scans ? scale_exp(__ldg(P.absmax + h_scan)) : 0);
+      float q[SPG];
+#pragma unroll
+      for (int s = 0; s < SPG; ++s) q[s] = 0.f;
+      bool bad = false, bad_span = false;
+      // first channel of this item handled by this group
+      int c = ((t & 1) == gp) ? 0 : 1;
+      t += c;
+      uint32_t w_next = c < p.C ? __ldg(tw + (size_t)c * TILE + pt) : 0u;
+      int lo_next = c < p.C ? __ldg(&tsp[c].x) : 0;
+      for (; c < p.C; c += 2, t += 2, ++my) {
+        const int slot = t % NS, oslot = t % NO;
+        const uint32_t w = w_next;
+        const int lo_c = lo_next;
+        if (c + 2 < p.C) {
+          w_next = __ldg(tw + (size_t)(c + 2) * TILE + pt);
+          lo_next = __ldg(&tsp[c + 2].x);
+        }
+        int d = (int)(w >> 23);
+        if (d > K - 2) {  // tile span beyond the K taps (the host checks mwb_table_max_span first)
+          bad_span = true;
+          d = K - 2;
+        }
+        const float f1 = weight_f1(w);
+        const float f0 = 1.0f - f1;
+        // ---- A row (weights), once the MMA released this operand slot
+        if (t >= NO) mbar_wait(&o_empty[oslot], (t / NO - 1) & 1);
+        unsigned char* op = ops + (size_t)oslot * OP_BYTES;
+        {
+          uint32_t f0h, f0l;
+          split2(f0, f1, f0h, f0l);  // low half f0, high half f1
+          const uint32_t f1h = f0h >> 16, f1l = f0l >> 16;
+          f0h &= 0xFFFFu;
+          f0l &= 0xFFFFu;
+          // word j holds taps 2j (low) and 2j + 1 (high)
+          const int j0 = d >> 1;
+          const bool odd = d & 1;
+          const uint32_t ph = odd ? (f0h << 16) : (f0h | (f1h << 16));
+          const uint32_t pl = odd ? (f0l << 16) : (f0l | (f1l << 16));
+          const uint32_t nh = odd ? f1h : 0u, nl = odd ? f1l : 0u;
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            hi[j] = j == j0 ? ph : (j == j0 + 1 ? nh : 0u);
+            lo[j] = j == j0 ? pl : (j == j0 + 1 ? nl : 0u);
+          }
+          unsigned char* ah = op + mb * MB_BYTES;
+          unsigned char* al = op + A_BYTES + mb * MB_BYTES;
+          *reinterpret_cast<uint4*>(ah + kmajor_off(row, 0)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(ah + kmajor_off(row, 1)) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+          *reinterpret_cast<uint4*>(al + kmajor_off(row, 0)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          *reinterpret_cast<uint4*>(al + kmajor_off(row, 1)) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+        }
+        // ---- Hankel rows and Gram entries of scan w8, once staged
+        mbar_wait(&s_full[slot], (t / NS) & 1);
+        const float* ys = stage + slot * (STAGE_BYTES / 4) + w8 * SPANF + ((p.k0 + lo_c) & 3);
+        {
+          float v[16];
+#pragma unroll
+          for (int m = 0; m < 16; ++m) v[m] = ys[lane + m] * h_scale;
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) split2(v[2 * j], v[2 * j + 1], hi[j], lo[j]);
+          const int n = w8 * W + lane;  // H row (s, k)
+          unsigned char* hh = op + 2 * A_BYTES;
+          unsigned char* hl = hh + H_BYTES;
+          *reinterpret_cast<uint4*>(hh + kmajor_off(n, 0)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(hh + kmajor_off(n, 1)) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+          *reinterpret_cast<uint4*>(hl + kmajor_off(n, 0)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          *reinterpret_cast<uint4*>(hl + kmajor_off(n, 1)) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+        }
+        float4* gsl = reinterpret_cast<float4*>(gbuf) + ((gp * 2 + (my & 1)) * SPG) * 16;
+        {
+          // e(d) = sum_{i=d}^{d+31} y_i^2 and x(d) = sum y_i y_{i+1} over the
+          // 48 staged samples y_0..y_47 of scan w8, d = 0..15, from inclusive
+          // warp scans of the two 32-sample halves; stored as float4
+          // {e(d), x(d), e(d+1), 0} so a point's gather is one LDS.128
+          const float v0 = ys[lane] * h_scale;
+          const float v1 = lane < 16 ? ys[lane + 32] * h_scale : 0.f;
+          const float dn0 = __shfl_down_sync(0xffffffffu, v0, 1);
+          const float h1 = __shfl_sync(0xffffffffu, v1, 0);
+          const float dn1 = __shfl_down_sync(0xffffffffu, v1, 1);
+          const float n0 = lane == 31 ? h1 : dn0;
+          const float n1 = lane == 31 ? 0.f : dn1;
+          const float S0 = warp_incl_scan(v0 * v0, lane), S1 = warp_incl_scan(v1 * v1, lane);
+          const float X0 = warp_incl_scan(v0 * n0, lane), X1 = warp_incl_scan(v1 * n1, lane);
+          const float Ts = __shfl_sync(0xffffffffu, S0, 31), Tx = __shfl_sync(0xffffffffu, X0, 31);
+          const float ps = __shfl_up_sync(0xffffffffu, S1 - S0, 1);
+          const float px = __shfl_up_sync(0xffffffffu, X1 - X0, 1);
+          const float e = lane == 0 ? Ts : Ts + ps;
+          const float x = lane == 0 ? Tx : Tx + px;
+          const float e_next = __shfl_down_sync(0xffffffffu, e, 1);
+          if (lane < 16) gsl[w8 * 16 + lane] = make_float4(e, x, e_next, 0.f);
+        }
+        fence_async_smem();  // A / H generic writes -> visible to the tensor core
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&o_full[oslot]);
+          mbar_arrive(&s_empty[slot]);
+        }
+        group_sync(gp);  // this group's Gram entries of channel c are in place
+        {
+          const float w0 = f0 * f0, w1 = 2.f * f0 * f1, w2 = f1 * f1;
+          const float4* g = gsl + d;
+#pragma unroll
+          for (int s = 0; s < SPG; ++s) {
+            const float4 gv = g[s * 16];
+            q[s] = fmaf(w0, gv.x, fmaf(w1, gv.y, fmaf(w2, gv.z, q[s])));
+          }
+        }
+      }
+      t -= (c - p.C);  // c overshot C by 0 or 1: t is now the first step of the next item
+      // ---- group 1 hands its Q partial sums to group 0
+      float* qx = reinterpret_cast<float*>(smem + L.qx);
+      if (gp == 1) {
+#pragma unroll
+        for (int s = 0; s < SPG; ++s) qx[s * TILE + pt] = q[s];
+      }
+      builders_sync();
+      if (gp == 1) continue;
+#pragma unroll
+      for (int s = 0; s < SPG; ++s) q[s] += qx[s * TILE + pt];
+      // ---- epilogue (group 0): S rows from TMEM -> energies
+      mbar_wait(acc_full, it & 1);
+      fence_after();
+      const bool valid = pt < n_in;
+      const int g = tile0 + (valid ? pt : 0);
+      const int slot_out = valid ? (p.out_idx ? __ldg(p.out_idx + g) : g) : -1;
+      const uint32_t lane_base = (uint32_t)((w8 & 3) * 32) << 16;
+#pragma unroll
+      for (int s = 0; s < SPG; ++s) {
+        if (s >= nsg) break;  // warp-uniform
+        float v[32];
+        tmem_ld32(tmem + lane_base + (uint32_t)(mb * N + s * W), v);
+        float e0 = 0.f, e1 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          e0 = fmaf(v[k], v[k], e0);
+          e1 = fmaf(v[k + 1], v[k + 1], e1);
+        }
+        const int scan = group * SPG + s;
+        const float inv = pow2f(-scale_exp(__ldg(P.absmax + scan)));
+        const double E = (double)e0 + (double)e1;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const bool want = kk == 0 ? KIND != KIND_DMAS : KIND != KIND_DAS;
+          if (!want) continue;
+          const float raw = kk == 0 ? __double2float_rn(E) : __double2float_rn(0.5 * (E - (double)q[s]));
+          const float en = raw * inv * inv;
+          float* out = (kk == 0 ? p.out_das : p.out_dmas) + (size_t)scan * (size_t)p.out_stride;
+          unsigned long long* keys = kk == 0 ? p.key_das : p.key_dmas;
+          unsigned long long key = 0ull;
+          if (valid) {
+            out[slot_out] = en;
+            if (isfinite(en)) key = argmax_key(en, slot_out); else bad = true;
+          }
+          if (keys) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+            if (lane == 0 && key != 0ull) atomicMax(keys + scan, key);
+          }
+        }
+      }
+      if (p.flags && (bad || bad_span)) atomicOr(p.flags, (bad ? 1 : 0) | (bad_span ? 2 : 0));
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+      ++it;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+// max |y| of each scan (bits; non-negative floats order like their bits)
+__global__ void scan_absmax_kernel(const float* sig, long long scan_stride, long long per_scan, uint32_t* out) {
+  const int s = blockIdx.y;
+  const float* base = sig + (size_t)s * (size_t)scan_stride;
+  uint32_t m = 0u;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < per_scan / 4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(base) + i);
+    m = max(m, max(max(__float_as_uint(fabsf(v.x)), __float_as_uint(fabsf(v.y))),
+                   max(__float_as_uint(fabsf(v.z)), __float_as_uint(fabsf(v.w)))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out + s, m);
+}
+
+// largest per-channel delay spread (hi - lo) over the table's tiles; wide
+// tiles report 1 << 30
+__global__ void table_max_span_kernel(const int2* span, const int* wide, long long tiles, int C, int* out) {
+  int m = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < tiles * C;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long tile = i / C;
+    const int2 sp = span[i];
+    m = max(m, wide[tile] ? (1 << 30) : sp.y - sp.x);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+}  // namespace tc

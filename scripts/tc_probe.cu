@@ -1,0 +1,131 @@
+// Standalone probe of the tcgen05 mechanics the tensor-core energy path uses
+// (development aid, not part of libmwb.so): one CTA computes
+// D[128 x N] = A[128 x 16] * B[N x 16]^T with fp16 operands in the no-swizzle
+// K-major core-matrix layout, fp32 accumulation in TMEM, and checks it on the
+// host.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -o tc_probe tc_probe.cu
+#include <cuda_fp16.h>
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cmath>
+#include <vector>
+
+constexpr int M = 128, K = 16;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// byte offset of element (r, k) of a rows x 16 fp16 K-major operand:
+// core matrices of 8 rows x 16 B; LBO = 128 B (k-half), SBO = 256 B (8-row group)
+__host__ __device__ inline uint32_t kmajor_off(int r, int k) {
+  return (r >> 3) * 256 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
+}
+
+__device__ __forceinline__ uint64_t smem_desc(const void* p, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version 1 (sm_100)
+  return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
+  return (1u << 4)                      // D format f32
+         | (0u << 7) | (0u << 10)       // A, B f16
+         | (0u << 15) | (0u << 16)      // K-major both
+         | ((uint32_t)(n >> 3) << 17)   // N >> 3
+         | ((uint32_t)(m >> 4) << 24);  // M >> 4
+}
+
+template <int N>
+__global__ void probe(const __half* a, const __half* b, float* d, int* err) {
+  __shared__ __align__(1024) unsigned char sa[M * K * 2];
+  __shared__ __align__(1024) unsigned char sb[N * K * 2];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < M * K; i += blockDim.x)
+    *reinterpret_cast<__half*>(sa + kmajor_off(i / K, i % K)) = a[i];
+  for (int i = tid; i < N * K; i += blockDim.x)
+    *reinterpret_cast<__half*>(sb + kmajor_off(i / K, i % K)) = b[i];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    const uint64_t da = smem_desc(sa, 128, 256), db = smem_desc(sb, 128, 256);
+    const uint32_t id = idesc_f16(M, N);
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(id), "r"(0));
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+        smem_u32(&bar)));
+  }
+  // wait for the MMA (phase 0)
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT;\n}\n" ::"r"(
+          smem_u32(&bar)),
+      "r"(0)
+      : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp < 4) {
+    const int row = warp * 32 + (tid & 31);
+    for (int c = 0; c < N; c += 8) {
+      uint32_t v[8];
+      const uint32_t addr = tmem + ((uint32_t)(warp * 32) << 16) + c;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                     "=r"(v[7])
+                   : "r"(addr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int j = 0; j < 8; ++j) d[row * N + c + j] = __uint_as_float(v[j]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  if (tid == 0) *err = 0;
+}
+
+int main() {
+  constexpr int N = 256;
+  std::vector<__half> ha(M * K), hb(N * K);
+  std::vector<float> fa(M * K), fb(N * K);
+  srand(1);
+  for (int i = 0; i < M * K; ++i) { fa[i] = (float)((rand() % 17) - 8) / 4.0f; ha[i] = __float2half(fa[i]); }
+  for (int i = 0; i < N * K; ++i) { fb[i] = (float)((rand() % 13) - 6) / 8.0f; hb[i] = __float2half(fb[i]); }
+  __half *da, *db; float* dd; int* derr;
+  cudaMalloc(&da, M * K * 2); cudaMalloc(&db, N * K * 2); cudaMalloc(&dd, M * N * 4); cudaMalloc(&derr, 4);
+  cudaMemcpy(da, ha.data(), M * K * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(db, hb.data(), N * K * 2, cudaMemcpyHostToDevice);
+  cudaMemset(dd, 0xFF, M * N * 4);
+  probe<N><<<1, 128>>>(da, db, dd, derr);
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("launch: %s\n", cudaGetErrorString(e));
+  std::vector<float> hd(M * N);
+  cudaMemcpy(hd.data(), dd, M * N * 4, cudaMemcpyDeviceToHost);
+  double maxerr = 0; int bad = 0;
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < N; ++j) {
+      double s = 0;
+      for (int k = 0; k < K; ++k) s += (double)fa[i * K + k] * fb[j * K + k];
+      double err = fabs(s - hd[i * N + j]);
+      if (err > maxerr) maxerr = err;
+      if (err > 1e-3 && bad++ < 5) printf("bad (%d,%d): got %f want %f\n", i, j, hd[i * N + j], s);
+    }
+  printf("max abs err %g, bad %d of %d\n", maxerr, bad, M * N);
+  return bad != 0;
+}

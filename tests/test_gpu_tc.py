@@ -1,0 +1,148 @@
+"""Tensor-core energy path (mwb_energies_tc, BatchImager(mode="tc")) against
+the fp32 CUDA-core path and the oracle.
+
+The tensor-core path computes the same energies with a different summation
+(fp16 hi/lo split products accumulated in TMEM, DMAS self-terms from windowed
+Gram entries), so it is compared at tolerance, not bit for bit:
+  * vs the fp32 CUDA-core kernel: max |tc - fp32| / max |fp32| <= 3e-5 per scan
+    (measured ~1e-5: TMEM accumulation over 3 x 66 MMAs rounds toward zero);
+  * vs the oracle (the reference's fp64 algorithm): <= 1e-4 peak-normalised
+    (BASELINE's bound), like every other energy map.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from _mwb_helpers import peak_err
+from oracle import mwbeam_oracle as orc
+from paper_1709_02549_b200 import synth
+from paper_1709_02549_b200.batch import BatchImager
+
+pytestmark = pytest.mark.gpu
+
+TOL_FP32 = 3e-5  # measured: see profiles/r01_tc.md
+TOL_REF = 1e-4
+
+
+@pytest.fixture(scope="module")
+def setup():
+    model = synth.ScanModel()
+    seeds = list(range(37))  # not a multiple of the 8-scan group
+    sig, tumours = synth.batch_2d(model, seeds)
+    grid = synth.grid_square(0.06, 128)  # 0.47 mm pitch, the configs[3] resolution
+    win = (model.k0, model.window)
+    tc = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win, mode="tc")
+    ref = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win)
+    return model, sig, grid, tc, ref
+
+
+def run(bi, sig_d, kinds=("das", "dmas")):
+    s = sig_d.shape[0]
+    n = bi.grid.dims[0] * bi.grid.dims[1]
+    outs = {k: torch.full((s, n), np.nan, dtype=torch.float32, device="cuda") for k in kinds}
+    keys = {k: torch.zeros(s, dtype=torch.int64, device="cuda") for k in kinds}
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    bi.run_device(sig_d, outs.get("das"), outs.get("dmas"), keys.get("das"), keys.get("dmas"), flags)
+    return ({k: v.cpu().numpy() for k, v in outs.items()},
+            {k: bi.decode_keys(v.cpu().numpy().view(np.uint64)) for k, v in keys.items()}, int(flags.item()))
+
+
+def test_tc_is_selected(setup):
+    _, _, _, tc, ref = setup
+    assert tc.uses_tensor_cores and not ref.uses_tensor_cores
+
+
+@pytest.mark.parametrize("kinds", [("das", "dmas"), ("das",), ("dmas",)])
+def test_tc_matches_fp32_path(setup, kinds):
+    _, sig, grid, tc, ref = setup
+    sig_d = tc.to_device_layout(sig)
+    got, gk, gf = run(tc, sig_d, kinds)
+    want, wk, wf = run(ref, sig_d, kinds)
+    assert gf == wf == 0
+    for k in kinds:
+        assert not np.isnan(got[k]).any()
+        for s in range(sig.shape[0]):
+            assert peak_err(got[k][s], want[k][s]) <= TOL_FP32, (k, s)
+        # argmax: identical unless the fp32 map has a near-tie at the top
+        for s in range(sig.shape[0]):
+            if tuple(gk[k][s]) != tuple(wk[k][s]):
+                top = np.sort(want[k][s])[-2:]
+                assert (top[1] - top[0]) <= 1e-5 * abs(top[1]), (k, s)
+
+
+def test_tc_vs_oracle(setup):
+    model, sig, grid, tc, _ = setup
+    got, _, _ = run(tc, tc.to_device_layout(sig))
+    g = model.geometry()
+    ny = grid.dims[1]
+    cells = [(ix, iy) for ix in range(0, 128, 7) for iy in range(3, 128, 9)]
+    pts = np.array([grid.cell_center(*c) for c in cells])
+    slots = np.array([ix * ny + iy for ix, iy in cells])
+    for s in (0, 36):
+        full = synth.embed_pairs(12, model.pairs(), sig[s].astype(np.float64))
+        for kind in ("das", "dmas"):
+            want = orc.windowed_energies(g.antennas, g.propagation_speed, g.sample_interval, full, pts, kind,
+                                         model.k0, model.window)
+            assert peak_err(got[kind][s][slots], want) <= TOL_REF
+
+
+def test_tc_scale_invariance_and_zero_scan(setup):
+    """Per-scan power-of-two scaling: scans 10^6 x larger / smaller give the
+    same relative maps; an all-zero scan images to exactly zero."""
+    _, sig, _, tc, ref = setup
+    x = np.array(sig[:8], dtype=np.float32)
+    x[1] *= 1e6
+    x[2] *= 1e-6
+    x[3] = 0.0
+    sig_d = tc.to_device_layout(x)
+    got, _, _ = run(tc, sig_d)
+    want, _, _ = run(ref, sig_d)
+    for k in ("das", "dmas"):
+        for s in (0, 1, 2):
+            assert peak_err(got[k][s], want[k][s]) <= TOL_FP32
+        assert (got[k][3] == 0).all()
+
+
+def test_tc_flags_non_finite(setup):
+    _, sig, _, tc, _ = setup
+    x = np.array(sig[:3], dtype=np.float32)
+    x[1, 5, :] = np.nan  # inside every window of scan 1
+    got, _, flags = run(tc, tc.to_device_layout(x))
+    assert flags & 1
+    assert np.isfinite(got["das"][0]).all() and np.isfinite(got["das"][2]).all()  # other scans unaffected
+
+
+def test_tc_masked_grid_falls_back():
+    """A breast mask leaves partial lattice tiles, so the 256-point table tiles
+    straddle two lattice tiles and exceed the 16-tap span: "tc" refuses,
+    "auto" falls back to the fp32 kernel (bit-identical to mode "smem")."""
+    import paper_1709_02549_b200 as mw
+
+    model = synth.ScanModel()
+    sig, _ = synth.batch_2d(model, list(range(5)))
+    grid = synth.grid_square(0.05, 107)
+    mask = mw.breast_mask(grid)
+    win = (model.k0, model.window)
+    with pytest.raises(ValueError, match="spread"):
+        BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win, mask=mask, mode="tc")
+    auto = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win, mask=mask, mode="auto")
+    ref = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win, mask=mask)
+    assert not auto.uses_tensor_cores
+    sig_d = auto.to_device_layout(sig)
+    got, _, _ = run(auto, sig_d)
+    want, _, _ = run(ref, sig_d)
+    for k in ("das", "dmas"):
+        assert np.array_equal(got[k], want[k], equal_nan=True)
+
+
+def test_tc_eligibility():
+    model = synth.ScanModel()
+    coarse = synth.grid_square(0.12, 64)  # 1.9 mm pitch: tile spreads exceed 14 samples
+    with pytest.raises(ValueError, match="spread"):
+        BatchImager(model.geometry(), model.pairs(), model.n_samples, coarse, window=(model.k0, 32), mode="tc")
+    auto = BatchImager(model.geometry(), model.pairs(), model.n_samples, coarse, window=(model.k0, 32), mode="auto")
+    assert not auto.uses_tensor_cores
+    fine = synth.grid_square(0.03, 64)
+    with pytest.raises(ValueError, match="window"):
+        BatchImager(model.geometry(), model.pairs(), model.n_samples, fine, window=(model.k0, 48), mode="tc")
