@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--scans", type=int, default=4096)
     ap.add_argument("--grid", type=int, default=256)
     ap.add_argument("--chunk", type=int, default=128)
-    ap.add_argument("--mode", choices=["smem", "gather", "tc", "auto"], default="smem")
+    ap.add_argument("--mode", choices=["smem", "gather", "tc", "auto"], default="auto",
+                    help="auto: tensor-core path when the table qualifies (configs[3] does), else smem")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
@@ -321,6 +322,68 @@ def load_traffic():
     return None
 
 
+def smem_roofline(pps_launch, avg, smem_gbs, fp32_tf, traffic):
+    """CUDA-core kernel: one fp32 sample per point-pair-sample serves both kinds
+    (4 B of LDS), 4 FP32-pipe ops per point-pair-sample."""
+    achieved = pps_launch * 4.0 / (avg * 1e-3) / 1e9
+    fp32_frac = pps_launch * 4.0 / (avg * 1e-3) / (fp32_tf * 1e12 / 2.0)
+    return {
+        "bound": "smem",
+        "kernel": "energy_kernel<BOTH> (fused DAS+DMAS)",
+        "achieved": achieved,
+        "peak": smem_gbs,
+        "unit": "GB/s",
+        "frac": achieved / smem_gbs,
+        "traffic": traffic.get("energy_kernel_both") if isinstance(traffic, dict) else None,
+        "algorithmic_bytes_per_launch": pps_launch * 4.0,
+        "per_unit": "4 B of shared memory per point-pair-sample (one fresh fp32 sample serves DAS and DMAS; "
+                    "the interpolation neighbour is reused in a register)",
+        "peak_source": "LDS.32 bandwidth microbenchmark run live in this process (mwb_microbench 0)",
+        "launch_ms": avg,
+        "fp32_pipe_frac": fp32_frac,
+        "fp32_ops_per_unit": 4,
+        "fp32_peak_tflops": fp32_tf,
+        "co_bound": "smem (1 LDS.32/pps) and FP32 pipe (FMUL+FFMA+FADD+FFMA per pps) peak at the same 32 pps/clk/SM",
+    }
+
+
+def tensor_peak():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["bf16_tflops"]), "MEASURED_PEAKS.json bf16_tflops (burst, cuBLAS)"
+        except (ValueError, KeyError):
+            pass
+    return 1590.0, "fallback 1.59 PFLOP/s of B200_PROFILING.md (MEASURED_PEAKS.json absent)"
+
+
+def tc_roofline(S, P, C, avg, traffic):
+    """Tensor-core kernel: per (256-point tile, 8-scan group, channel) six
+    tcgen05.mma M128 x N256 x K16 f16 (two M-blocks x the hi*hi, hi*lo, lo*hi
+    split) = 6 * 2 * 128 * 256 * 16 FLOP."""
+    tiles, groups = (P + 255) // 256, (S + 7) // 8
+    flop_unit = 6 * 2 * 128 * 256 * 16
+    flops = float(tiles) * groups * C * flop_unit
+    achieved = flops / (avg * 1e-3) / 1e12
+    peak, source = tensor_peak()
+    return {
+        "bound": "tensor",
+        "kernel": "energy_tc_kernel<BOTH> (tcgen05 fp16 hi/lo split, TMEM accumulation; DAS+DMAS fused)",
+        "achieved": achieved,
+        "peak": peak,
+        "unit": "TFLOP/s",
+        "frac": achieved / peak,
+        "traffic": traffic.get("energy_tc_kernel_both") if isinstance(traffic, dict) else None,
+        "algorithmic_flops_per_launch": flops,
+        "per_unit": "6 x 2 x 128 x 256 x 16 FLOP per (256-point tile, 8-scan group, channel): the K=16 tap "
+                    "window per channel x 3 split products x 2 M-blocks",
+        "peak_source": source,
+        "launch_ms": avg,
+        "note": "launch_ms brackets the whole mwb_energies_tc call (a 0.2 ms per-scan |y| max pre-pass and the "
+                "tensor-core kernel); shared memory (operand writes + tensor-core operand reads) is the co-bound",
+    }
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -392,31 +455,14 @@ def run_ours(args):
     value = pair_evals / (ms_step * 1e-3)
     images_s = 2.0 * S * world / (ms_step * 1e-3)
 
-    # roofline of the (single, fused) energy kernel: one fp32 sample per
-    # point-pair-sample serves both kinds; 4 FP32-pipe ops per point-pair-sample
     avg = statistics.mean(launch_ms)
     pps_launch = float(S) * P * C * W
-    achieved = pps_launch * 4.0 / (avg * 1e-3) / 1e9
-    fp32_frac = pps_launch * 4.0 / (avg * 1e-3) / (fp32_tf * 1e12 / 2.0)
     traffic = load_traffic()
-    roofline = {
-        "bound": "smem",
-        "kernel": "energy_kernel<BOTH> (fused DAS+DMAS)",
-        "achieved": achieved,
-        "peak": smem_gbs,
-        "unit": "GB/s",
-        "frac": achieved / smem_gbs,
-        "traffic": traffic.get("energy_kernel_both") if isinstance(traffic, dict) else None,
-        "algorithmic_bytes_per_launch": pps_launch * 4.0,
-        "per_unit": "4 B of shared memory per point-pair-sample (one fresh fp32 sample serves DAS and DMAS; "
-                    "the interpolation neighbour is reused in a register)",
-        "peak_source": "LDS.32 bandwidth microbenchmark run live in this process (mwb_microbench 0)",
-        "launch_ms": avg,
-        "fp32_pipe_frac": fp32_frac,
-        "fp32_ops_per_unit": 4,
-        "fp32_peak_tflops": fp32_tf,
-        "co_bound": "smem (1 LDS.32/pps) and FP32 pipe (FMUL+FFMA+FADD+FFMA per pps) peak at the same 32 pps/clk/SM",
-    }
+    if bi.uses_tensor_cores:
+        roofline = tc_roofline(S, P, C, avg, traffic)
+    else:
+        roofline = smem_roofline(pps_launch, avg, smem_gbs, fp32_tf, traffic)
+
 
     # end to end through the public host API
     e2e = None
@@ -458,7 +504,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "other_configs": others,
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * (2 if bi.uses_tensor_cores else 1),
+            "tensor_cores": bi.uses_tensor_cores,
             "clocks": clk,
             "kernel_mode": args.mode,
             "host_generate_s": t_gen,

@@ -26,13 +26,13 @@
 // of two so |y| < 2^15), and S = A_hi H_hi + A_hi H_lo + A_lo H_hi (the
 // dropped A_lo H_lo term is ~2^-22 relative), i.e. about fp32 accuracy.
 //
-// Roles (576 threads, one CTA per SM, persistent over (tile, group) items):
-//   warps 0-15 builders in two groups of 8 taking alternate channel steps:
+// Roles (8NG + 2 warps, one CTA per SM, persistent over (tile, group) items):
+//   warps 0..8NG-1 builders in NG groups of 8 taking interleaved channel steps:
 //              thread pt of a group owns point pt (its A row, Q); warp w8 of
 //              a group owns scan w8 (its 32 Hankel rows and Gram entries);
 //              group 0 also runs the TMEM epilogue
-//   warp 16    producer: TMA bulk copies of each channel's window spans
-//   warp 17    MMA issuer: one thread, 6 tcgen05.mma per channel
+//   warp 8NG   producer: TMA bulk copies of each channel's window spans
+//   warp 8NG+1 MMA issuer: one thread, 6 tcgen05.mma per channel
 // Rings: samples (NS deep, full/empty mbarriers), operands (NO deep, full by
 // the builders, empty by tcgen05.commit), accumulator (full by commit, empty
 // by the builders after the epilogue's tcgen05.ld).
@@ -44,11 +44,15 @@ constexpr int SPG = 8;                     // scans per group
 constexpr int N = SPG * W;                 // MMA N: 256
 constexpr int K = 16;                      // taps per channel: d + 1 <= K - 1
 constexpr int SPANF = 52;                  // staged floats per (scan, channel): 3 + W + K, rounded to 4
-constexpr int NS = 8;                      // sample ring depth
+constexpr int NS = 16;                     // sample ring depth
 constexpr int NO = 4;                      // operand ring depth
-constexpr int NBW = 16;                    // builder warps: two groups of 8 (alternate steps)
-constexpr int NBT = NBW * 32;              // builder threads (2 x TILE)
+#ifndef MWB_TC_GROUPS
+#define MWB_TC_GROUPS 3
+#endif
+constexpr int NG = MWB_TC_GROUPS;          // builder groups (step t -> group t % NG)
 constexpr int GW = 8;                      // warps per builder group
+constexpr int NBW = NG * GW;               // builder warps
+constexpr int NBT = NBW * 32;              // builder threads
 constexpr int THREADS = NBT + 64;          // + producer warp + MMA warp
 constexpr int A_BYTES = TILE * K * 2;      // one of hi/lo, both M-blocks: 8 KB
 constexpr int MB_BYTES = 128 * K * 2;      // one M-block: 4 KB
@@ -68,8 +72,8 @@ __host__ __device__ inline Layout layout() {
   size_t o = 0;
   L.ops = o;   o += (size_t)NO * OP_BYTES;
   L.stage = o; o += (size_t)NS * STAGE_BYTES;
-  L.g = o;     o += 4 * (size_t)SPG * 16 * sizeof(float4);  // {e(d), x(d), e(d+1), 0}: 2 groups x 2 steps
-  L.qx = o;    o += (size_t)SPG * TILE * sizeof(float);      // group 1's Q partial sums
+  L.g = o;     o += 2 * NG * (size_t)SPG * 16 * sizeof(float4);  // {e(d), x(d), e(d+1), 0}: groups x 2 steps
+  L.qx = o;    o += (NG - 1) * (size_t)SPG * TILE * sizeof(float);  // groups 1.. Q partial sums
   o = align_up(o, 8);
   L.bar = o;   o += sizeof(uint64_t) * (2 * NS + 2 * NO + 2);
   L.tmem = o;  o += 16;
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
-      mbar_init(&s_full[i], 32);
+      mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], GW);
     }
     for (int i = 0; i < NO; ++i) {
@@ -220,24 +224,18 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
         const int lo_c = __shfl_sync(0xffffffffu, lo32, c & 31);
         if (use > 0) mbar_wait(&s_empty[slot], (use - 1) & 1);
         const long long start4 = ((long long)p.k0 + lo_c) & ~3LL;
-        const int s = group * SPG + lane;
+        // every scan of the group stages the same span [start4, start4 + n)
+        const int n = (int)min((long long)SPANF, max((long long)p.ld - start4, 0LL));
+        const int nsg = min(SPG, p.n_scans - group * SPG);
         float* dst = stage + slot * (STAGE_BYTES / 4) + lane * SPANF;
-        long long n = 0;
-        if (lane < SPG) {
-          if (s < p.n_scans) n = min((long long)SPANF, max((long long)p.ld - start4, 0LL));
-          for (long long j = n; j < SPANF; ++j) dst[j] = 0.f;
-        }
-        uint32_t bytes = (uint32_t)(n * 4);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-        if (lane == 0)
-          mbar_arrive_expect_tx(&s_full[slot], bytes);
-        else
-          mbar_arrive(&s_full[slot]);
+        if (lane < SPG && (n < SPANF || lane >= nsg))  // past the record / no such scan: zeros
+          for (int j = lane < nsg ? n : 0; j < SPANF; ++j) dst[j] = 0.f;
+        __syncwarp();  // zero-fills ordered before lane 0's release
+        if (lane == 0) mbar_arrive_expect_tx(&s_full[slot], (uint32_t)(nsg * n * 4));
         __syncwarp();
-        if (n > 0)
-          bulk_g2s(dst, p.sig + (size_t)s * (size_t)p.scan_stride + (size_t)c * p.ld + start4, (uint32_t)(n * 4),
-                   &s_full[slot]);
+        if (lane < nsg && n > 0)
+          bulk_g2s(dst, p.sig + (size_t)(group * SPG + lane) * (size_t)p.scan_stride + (size_t)c * p.ld + start4,
+                   (uint32_t)(n * 4), &s_full[slot]);
       }
     }
   } else if (warp == NBW + 1) {
@@ -271,8 +269,8 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
     }
     __syncwarp();
   } else {
-    // ===== builders + epilogue: two groups of 8 warps take alternate
-    // pipeline steps (gp = warp >> 3: steps t with t % 2 == gp), so two
+    // ===== builders + epilogue: NG groups of 8 warps take interleaved
+    // pipeline steps (gp = warp >> 3: steps t with t % NG == gp), so NG
     // channels' operand chains are in flight at once.  Within a group thread
     // pt (0..255) owns point pt (A row, Q) and warp w8 = warp & 7 owns scan w8
     // of the group (its 32 Hankel rows and Gram entries).  Group 0 also runs
@@ -296,17 +294,17 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
       for (int s = 0; s < SPG; ++s) q[s] = 0.f;
       bool bad = false, bad_span = false;
       // first channel of this item handled by this group
-      int c = ((t & 1) == gp) ? 0 : 1;
+      int c = (gp - t % NG + NG) % NG;
       t += c;
       uint32_t w_next = c < p.C ? __ldg(tw + (size_t)c * TILE + pt) : 0u;
       int lo_next = c < p.C ? __ldg(&tsp[c].x) : 0;
-      for (; c < p.C; c += 2, t += 2, ++my) {
+      for (; c < p.C; c += NG, t += NG, ++my) {
         const int slot = t % NS, oslot = t % NO;
         const uint32_t w = w_next;
         const int lo_c = lo_next;
-        if (c + 2 < p.C) {
-          w_next = __ldg(tw + (size_t)(c + 2) * TILE + pt);
-          lo_next = __ldg(&tsp[c + 2].x);
+        if (c + NG < p.C) {
+          w_next = __ldg(tw + (size_t)(c + NG) * TILE + pt);
+          lo_next = __ldg(&tsp[c + NG].x);
         }
         int d = (int)(w >> 23);
         if (d > K - 2) {  // tile span beyond the K taps (the host checks mwb_table_max_span first)
@@ -401,17 +399,19 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
           }
         }
       }
-      t -= (c - p.C);  // c overshot C by 0 or 1: t is now the first step of the next item
-      // ---- group 1 hands its Q partial sums to group 0
+      t -= (c - p.C);  // c overshot C by 0..NG-1: t is now the first step of the next item
+      // ---- groups 1.. hand their Q partial sums to group 0
       float* qx = reinterpret_cast<float*>(smem + L.qx);
-      if (gp == 1) {
+      if (gp > 0) {
 #pragma unroll
-        for (int s = 0; s < SPG; ++s) qx[s * TILE + pt] = q[s];
+        for (int s = 0; s < SPG; ++s) qx[((gp - 1) * SPG + s) * TILE + pt] = q[s];
       }
       builders_sync();
-      if (gp == 1) continue;
+      if (gp > 0) continue;
+      for (int g2 = 0; g2 < NG - 1; ++g2) {
 #pragma unroll
-      for (int s = 0; s < SPG; ++s) q[s] += qx[s * TILE + pt];
+        for (int s = 0; s < SPG; ++s) q[s] += qx[(g2 * SPG + s) * TILE + pt];
+      }
       // ---- epilogue (group 0): S rows from TMEM -> energies
       mbar_wait(acc_full, it & 1);
       fence_after();

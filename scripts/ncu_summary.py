@@ -66,18 +66,31 @@ def launches(path: str):
     start = next(i for i, l in enumerate(txt) if l.startswith('"ID"'))
     rows = list(csv.DictReader(io.StringIO("\n".join(txt[start:]))))
     per = defaultdict(lambda: [0, 0.0])
-    unit = rows[0].get("Metric Unit", "")
+    dram = defaultdict(lambda: [0, 0.0])  # kernel -> [launches, read + write bytes]
+    unit = ""
     for r in rows:
         name = r["Kernel Name"].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
+        metric = r.get("Metric Name", "gpu__time_duration.sum")
         v = float(r["Metric Value"].replace(",", ""))
-        per[name][0] += 1
-        per[name][1] += v
+        if metric == "gpu__time_duration.sum":
+            unit = r.get("Metric Unit", "")
+            per[name][0] += 1
+            per[name][1] += v
+        elif metric in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            dram[name][1] += v
+            if metric == "dram__bytes_read.sum":
+                dram[name][0] += 1
     total = sum(v for _, v in per.values())
     print(f"# launch list (`gpu__time_duration.sum`, cold-cache, serialised): `{Path(path).name}`\n")
-    print(f"| kernel | launches | total ({unit}) | share |")
-    print("|---|---|---|---|")
+    cols = "| kernel | launches | total (%s) | share |" % unit + (" DRAM bytes / launch |" if dram else "")
+    print(cols)
+    print("|---|---|---|---|" + ("---|" if dram else ""))
     for name, (n, v) in sorted(per.items(), key=lambda kv: -kv[1][1]):
-        print(f"| {name} | {n} | {v:,.0f} | {v / total:.1%} |")
+        extra = ""
+        if dram:
+            dn, db = dram.get(name, [0, 0.0])
+            extra = f" {db / dn:,.0f} |" if dn else " — |"
+        print(f"| {name} | {n} | {v:,.0f} | {v / total:.1%} |{extra}")
 
 
 def traffic(rep: str, key: str = "energy_kernel_both"):
