@@ -42,6 +42,7 @@ namespace tc {
 constexpr int W = 32;                      // window samples (this build)
 constexpr int SPG = 8;                     // scans per group
 constexpr int N = SPG * W;                 // MMA N: 256
+static_assert(SPG % 4 == 0, "Gram entries are interleaved by 4 scans");
 constexpr int K = 16;                      // taps per channel: d + 1 <= K - 1
 constexpr int SPANF = 52;                  // staged floats per (scan, channel): 3 + W + K, rounded to 4
 constexpr int NS = 16;                     // sample ring depth
@@ -72,7 +73,7 @@ __host__ __device__ inline Layout layout() {
   size_t o = 0;
   L.ops = o;   o += (size_t)NO * OP_BYTES;
   L.stage = o; o += (size_t)NS * STAGE_BYTES;
-  L.g = o;     o += 2 * NG * (size_t)SPG * 16 * sizeof(float4);  // {e(d), x(d), e(d+1), 0}: groups x 2 steps
+  L.g = o;     o += 2 * NG * (size_t)SPG * 16 * sizeof(float4);  // [quad][e|x][d] float4: groups x 2 steps
   L.qx = o;    o += (NG - 1) * (size_t)SPG * TILE * sizeof(float);  // groups 1.. Q partial sums
   o = align_up(o, 8);
   L.bar = o;   o += sizeof(uint64_t) * (2 * NS + 2 * NO + 2);
@@ -363,8 +364,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
         {
           // e(d) = sum_{i=d}^{d+31} y_i^2 and x(d) = sum y_i y_{i+1} over the
           // 48 staged samples y_0..y_47 of scan w8, d = 0..15, from inclusive
-          // warp scans of the two 32-sample halves; stored as float4
-          // {e(d), x(d), e(d+1), 0} so a point's gather is one LDS.128
+          // warp scans of the two 32-sample halves
           const float v0 = ys[lane] * h_scale;
           const float v1 = lane < 16 ? ys[lane + 32] * h_scale : 0.f;
           const float dn0 = __shfl_down_sync(0xffffffffu, v0, 1);
@@ -379,8 +379,12 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
           const float px = __shfl_up_sync(0xffffffffu, X1 - X0, 1);
           const float e = lane == 0 ? Ts : Ts + ps;
           const float x = lane == 0 ? Tx : Tx + px;
-          const float e_next = __shfl_down_sync(0xffffffffu, e, 1);
-          if (lane < 16) gsl[w8 * 16 + lane] = make_float4(e, x, e_next, 0.f);
+          // layout [quad][e | x][d] of float4 = 4 scans: e(d) of scans 4q..4q+3
+          float* gq = reinterpret_cast<float*>(gsl + (w8 >> 2) * 32) + (w8 & 3);
+          if (lane < 16) {
+            gq[lane * 4] = e;
+            gq[(16 + lane) * 4] = x;
+          }
         }
         fence_async_smem();  // A / H generic writes -> visible to the tensor core
         __syncwarp();
@@ -391,11 +395,13 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
         group_sync(gp);  // this group's Gram entries of channel c are in place
         {
           const float w0 = f0 * f0, w1 = 2.f * f0 * f1, w2 = f1 * f1;
-          const float4* g = gsl + d;
 #pragma unroll
-          for (int s = 0; s < SPG; ++s) {
-            const float4 gv = g[s * 16];
-            q[s] = fmaf(w0, gv.x, fmaf(w1, gv.y, fmaf(w2, gv.z, q[s])));
+          for (int qd = 0; qd < SPG / 4; ++qd) {
+            const float4 E = gsl[qd * 32 + d], E1 = gsl[qd * 32 + d + 1], X = gsl[qd * 32 + 16 + d];
+            q[4 * qd + 0] = fmaf(w0, E.x, fmaf(w1, X.x, fmaf(w2, E1.x, q[4 * qd + 0])));
+            q[4 * qd + 1] = fmaf(w0, E.y, fmaf(w1, X.y, fmaf(w2, E1.y, q[4 * qd + 1])));
+            q[4 * qd + 2] = fmaf(w0, E.z, fmaf(w1, X.z, fmaf(w2, E1.z, q[4 * qd + 2])));
+            q[4 * qd + 3] = fmaf(w0, E.w, fmaf(w1, X.w, fmaf(w2, E1.w, q[4 * qd + 3])));
           }
         }
       }

@@ -100,6 +100,80 @@ __global__ void probe(const __half* a, const __half* b, float* d, int* err) {
   if (tid == 0) *err = 0;
 }
 
+// Same product with A taken from TMEM: thread r writes row r (16 fp16 = 8
+// packed 32-bit columns) with tcgen05.st, the MMA reads [a_tmem].
+template <int N>
+__global__ void probe_tmem_a(const __half* a, const __half* b, float* d) {
+  __shared__ __align__(1024) unsigned char sb[N * K * 2];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < N * K; i += blockDim.x)
+    *reinterpret_cast<__half*>(sb + kmajor_off(i / K, i % K)) = b[i];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tbase;
+  const uint32_t a_col = 256;  // A operand at columns [256, 264)
+  {
+    const int row = tid;  // 128 threads: warp w writes lanes 32w..32w+31
+    uint32_t r[8];
+    for (int j = 0; j < 8; ++j) {
+      const __half2 h = __halves2half2(a[row * K + 2 * j], a[row * K + 2 * j + 1]);
+      r[j] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    const uint32_t addr = tmem + ((uint32_t)(warp * 32) << 16) + a_col;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0) {
+    const uint64_t db = smem_desc(sb, 128, 256);
+    const uint32_t id = idesc_f16(M, N);
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem),
+        "r"(tmem + a_col), "l"(db), "r"(id), "r"(0));
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+        smem_u32(&bar)));
+  }
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT2:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT2;\n}\n" ::"r"(
+          smem_u32(&bar)),
+      "r"(0)
+      : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  {
+    const int row = warp * 32 + (tid & 31);
+    for (int c = 0; c < N; c += 8) {
+      uint32_t v[8];
+      const uint32_t addr = tmem + ((uint32_t)(warp * 32) << 16) + c;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                     "=r"(v[7])
+                   : "r"(addr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int j = 0; j < 8; ++j) d[row * N + c + j] = __uint_as_float(v[j]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 int main() {
   constexpr int N = 256;
   std::vector<__half> ha(M * K), hb(N * K);
@@ -127,5 +201,22 @@ int main() {
       if (err > 1e-3 && bad++ < 5) printf("bad (%d,%d): got %f want %f\n", i, j, hd[i * N + j], s);
     }
   printf("max abs err %g, bad %d of %d\n", maxerr, bad, M * N);
-  return bad != 0;
+  // A from TMEM
+  constexpr int N2 = 192;
+  cudaMemset(dd, 0xFF, M * N * 4);
+  probe_tmem_a<N2><<<1, 128>>>(da, db, dd);
+  e = cudaDeviceSynchronize();
+  printf("tmem-A launch: %s\n", cudaGetErrorString(e));
+  cudaMemcpy(hd.data(), dd, M * N2 * 4, cudaMemcpyDeviceToHost);
+  double maxerr2 = 0; int bad2 = 0;
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < N2; ++j) {
+      double s = 0;
+      for (int k = 0; k < K; ++k) s += (double)fa[i * K + k] * fb[j * K + k];
+      double err = fabs(s - hd[i * N2 + j]);
+      if (err > maxerr2) maxerr2 = err;
+      if (err > 1e-3 && bad2++ < 5) printf("bad2 (%d,%d): got %f want %f\n", i, j, hd[i * N2 + j], s);
+    }
+  printf("tmem-A: max abs err %g, bad %d of %d\n", maxerr2, bad2, M * N2);
+  return (bad != 0) || (bad2 != 0);
 }
