@@ -274,11 +274,12 @@ def other_configs() -> dict:
     from paper_1709_02549_b200.batch import BatchImager
 
     sig1, _ = synth.batch_2d_device(m0, range(1024), phantom_radius=0.05, snr_db=20.0)
-    bi1 = BatchImager(m0.geometry(), m0.pairs(), m0.n_samples, g1, window=win)
+    bi1 = BatchImager(m0.geometry(), m0.pairs(), m0.n_samples, g1, window=win, mode="auto")
     o1 = torch.empty((1024, 200 * 200), dtype=torch.float32, device="cuda")
     t = med_ms(lambda: bi1.run_device(sig1, out_dmas=o1), reps=5)
     out["cfg1_dmas_200x200_batched_1024_scans"] = {"ms": t, "images_per_s": 1024 / (t * 1e-3),
-                                                   "pixel_pair_evals_per_s": 1024 * 4e4 * 66 / (t * 1e-3)}
+                                                   "pixel_pair_evals_per_s": 1024 * 4e4 * 66 / (t * 1e-3),
+                                                   "tensor_cores": bi1.uses_tensor_cores}
     del sig1, o1
     m2 = synth.ScanModel(n_samples=2048)
     ds2, _ = synth.dataset_2d(m2, seed=1000, phantom_radius=0.05)
@@ -357,11 +358,11 @@ def tensor_peak():
     return 1590.0, "fallback 1.59 PFLOP/s of B200_PROFILING.md (MEASURED_PEAKS.json absent)"
 
 
-def tc_roofline(S, P, C, avg, traffic):
+def tc_roofline(S, slots, C, avg, traffic):
     """Tensor-core kernel: per (256-point tile, 8-scan group, channel) six
     tcgen05.mma M128 x N256 x K16 f16 (two M-blocks x the hi*hi, hi*lo, lo*hi
     split) = 6 * 2 * 128 * 256 * 16 FLOP."""
-    tiles, groups = (P + 255) // 256, (S + 7) // 8
+    tiles, groups = (slots + 255) // 256, (S + 7) // 8
     flop_unit = 6 * 2 * 128 * 256 * 16
     flops = float(tiles) * groups * C * flop_unit
     achieved = flops / (avg * 1e-3) / 1e12
@@ -410,7 +411,7 @@ def run_ours(args):
     grid = synth.grid_square(0.12, args.grid)
     bi = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=(model.k0, model.window),
                      mode=args.mode)
-    P, C, W = bi.n_pts, bi.n_chan, model.window
+    P, C, W = bi.n_valid, bi.n_chan, model.window  # evaluated cells (the padded TC layout has more slots)
     nxny = grid.dims[0] * grid.dims[1]
     outs = {k: torch.empty((S, nxny), dtype=torch.float32, device=dev) for k in ("das", "dmas")}  # 2.1 GB
     keys = {k: torch.zeros(S, dtype=torch.int64, device=dev) for k in ("das", "dmas")}
@@ -459,7 +460,7 @@ def run_ours(args):
     pps_launch = float(S) * P * C * W
     traffic = load_traffic()
     if bi.uses_tensor_cores:
-        roofline = tc_roofline(S, P, C, avg, traffic)
+        roofline = tc_roofline(S, bi.n_pts, C, avg, traffic)
     else:
         roofline = smem_roofline(pps_launch, avg, smem_gbs, fp32_tf, traffic)
 

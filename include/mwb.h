@@ -289,7 +289,8 @@ int mwb_simulate(float* out, int n_scans, int n_chan, int n_samples, int ld, con
 
 /*
  * Tensor-core (tcgen05) variant of mwb_energies for many scans of one
- * geometry (no tile_info): per channel the tile's interpolation weights
+ * geometry (tile_info: NULL, or the padded layout's per-tile {0, count}): per
+ * channel the tile's interpolation weights
  * [256 x 16] multiply the Hankel windows of 8 scans [16 x 256] in fp16 hi/lo
  * split (about fp32 accuracy), accumulated over channels in TMEM; DMAS's
  * channel self-terms come from windowed Gram entries.  Requirements: window
@@ -303,9 +304,24 @@ int mwb_table_max_span(const void* table, int n_pts, int n_chan, int32_t* d_out,
 int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
                     const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale,
                     const double* pts_xyz, const int32_t* out_idx, int n_pts, const int32_t* d_count,
-                    const void* table, int interp, int k0, int window, float* out_das, float* out_dmas,
-                    int64_t out_stride, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags, void* workspace,
-                    void* stream);
+                    const int32_t* tile_info, const void* table, int interp, int k0, int window, float* out_das,
+                    float* out_dmas, int64_t out_stride, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags,
+                    void* workspace, void* stream);
+
+/*
+ * Padded lattice enumeration (for mwb_energies_tc on masked or ragged grids):
+ * like mwb_enumerate_lattice, but lattice tile t's points occupy slots
+ * [256 t, 256 t + count_t) of pts_xyz / out_idx (the list has
+ * 256 * mwb_lattice_tile_count(nx, ny, stride) slots) and tile_info[t] =
+ * {0, count_t} (int32 pairs), the per-tile record mwb_delay_table_tiles and
+ * mwb_energies_tc take.  Table tiles then coincide with 16 x 16 lattice
+ * tiles, whose delay spread is small.  d_count receives the total count.
+ */
+int64_t mwb_lattice_tile_count(int nx, int ny, int stride);
+int mwb_enumerate_lattice_padded(double ox, double oy, double res, int nx, int ny, int x0, int y0, int x1, int y1,
+                                 int stride, const uint8_t* mask, int skip_stride, double* pts_xyz,
+                                 int32_t* out_idx, int32_t* tile_info, int32_t* d_count, uint8_t* valid,
+                                 void* workspace, void* stream);
 
 /*
  * One-call lattice image: the reference's image(ds, kind, grid, region,

@@ -108,8 +108,13 @@ _SIGNATURES = {
     "mwb_energies_tc_workspace_bytes": ([_I], _I64),
     "mwb_table_max_span": ([_P, _I, _I, _P, _P], _I),
     "mwb_energies_tc": (
-        [_P, _I, _I64, _I, _I, _I, _P, _P, _I, _D, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _I64, _P, _P, _P, _P,
-         _P],
+        [_P, _I, _I64, _I, _I, _I, _P, _P, _I, _D, _P, _P, _I, _P, _P, _P, _I, _I, _I, _P, _P, _I64, _P, _P, _P,
+         _P, _P],
+        _I,
+    ),
+    "mwb_lattice_tile_count": ([_I, _I, _I], _I64),
+    "mwb_enumerate_lattice_padded": (
+        [_D, _D, _D, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P],
         _I,
     ),
     "mwb_delay_table_tiles": ([_P, _I, _P, _P, _I, _P, _I, _D, _I, _P, _P], _I),

@@ -59,39 +59,76 @@ class BatchImager:
             n_ant=m,
             chan_host=pairs,
         )
-        nx, ny = grid.dims
-        # enumerate the grid once (device), read the point count once
-        emask = dv.upload_mask(mask, (nx, ny))
-        p_max = nx * ny
-        self.pts = torch.empty((p_max, 3), dtype=torch.float64, device=dev)
-        self.oidx = torch.empty(p_max, dtype=torch.int32, device=dev)
-        self.valid = torch.zeros(p_max, dtype=torch.uint8, device=dev)
-        st = _Status()
-        ws = torch.empty(int(nat.load().mwb_lattice_workspace_bytes(nx, ny, 1)), dtype=torch.uint8, device=dev)
-        nat.call("mwb_enumerate_lattice", grid.origin[0], grid.origin[1], grid.resolution, nx, ny, 0, 0, nx - 1,
-                 ny - 1, None, 1, nat.ptr(emask), 0, self.pts.data_ptr(), self.oidx.data_ptr(), st.count_ptr(0),
-                 self.valid.data_ptr(), ws.data_ptr(), dv.stream_handle())
-        _, counts, _ = st.read()
-        self.n_pts = int(counts[0])
-        self.valid_host = self.valid.view(nx, ny).cpu().numpy().astype(bool)
-        # per-point delay table: computed once, shared by every scan and kind
-        self.table = build_table(self.scan, self.pts, self.n_pts, self.interp) if self.n_pts else None
-        # tensor-core path (mwb_energies_tc): needs W == 32 and every tile's
-        # per-channel delay spread within its 16 taps; checked once per table
+        emask = dv.upload_mask(mask, grid.dims)
+        self.tile_info = None
+        self._tc_ws = None
         if self.mode == 2:
-            ok, why = self.tc_eligible()
+            # tensor-core path (mwb_energies_tc): padded layout (table tiles =
+            # 16 x 16 lattice tiles), W == 32 and every tile's per-channel
+            # delay spread within its 16 taps; checked once per table
+            ok, why = self._setup_padded(emask)
             if not ok:
                 if mode == "tc":
                     raise ValueError(f"tensor-core path unavailable: {why}")
                 self.mode = 0
-        self._tc_ws = None
+        if self.mode != 2:
+            self._setup_compact(emask)
+
+    def _enumerate(self, emask, padded: bool):
+        nx, ny = self.grid.dims
+        dev = dv.device()
+        if padded:
+            tiles = int(nat.load().mwb_lattice_tile_count(nx, ny, 1))
+            p_max = 256 * tiles
+            self.tile_info = torch.zeros((tiles, 2), dtype=torch.int32, device=dev)
+        else:
+            p_max = nx * ny
+            self.tile_info = None
+        self.pts = torch.zeros((p_max, 3), dtype=torch.float64, device=dev)
+        self.oidx = torch.zeros(p_max, dtype=torch.int32, device=dev)
+        self.valid = torch.zeros(nx * ny, dtype=torch.uint8, device=dev)
+        st = _Status()
+        ws = torch.empty(int(nat.load().mwb_lattice_workspace_bytes(nx, ny, 1)), dtype=torch.uint8, device=dev)
+        g = self.grid
+        if padded:
+            nat.call("mwb_enumerate_lattice_padded", g.origin[0], g.origin[1], g.resolution, nx, ny, 0, 0, nx - 1,
+                     ny - 1, 1, nat.ptr(emask), 0, self.pts.data_ptr(), self.oidx.data_ptr(),
+                     self.tile_info.data_ptr(), st.count_ptr(0), self.valid.data_ptr(), ws.data_ptr(),
+                     dv.stream_handle())
+        else:
+            nat.call("mwb_enumerate_lattice", g.origin[0], g.origin[1], g.resolution, nx, ny, 0, 0, nx - 1,
+                     ny - 1, None, 1, nat.ptr(emask), 0, self.pts.data_ptr(), self.oidx.data_ptr(), st.count_ptr(0),
+                     self.valid.data_ptr(), ws.data_ptr(), dv.stream_handle())
+        _, counts, _ = st.read()
+        self.n_valid = int(counts[0])
+        self.n_pts = p_max if padded else self.n_valid
+        self.valid_host = self.valid.view(nx, ny).cpu().numpy().astype(bool)
+
+    def _setup_compact(self, emask) -> None:
+        self._enumerate(emask, padded=False)
+        # per-point delay table: computed once, shared by every scan and kind
+        self.table = build_table(self.scan, self.pts, self.n_pts, self.interp) if self.n_pts else None
+
+    def _setup_padded(self, emask) -> tuple[bool, str]:
+        if self.w != self.TC_WINDOW:
+            return False, f"window {self.w} != {self.TC_WINDOW}"
+        self._enumerate(emask, padded=True)
+        if not self.n_valid:
+            self.table = None
+            return True, ""
+        nbytes = int(nat.load().mwb_delay_table_bytes(self.n_pts, self.n_chan))
+        self.table = torch.empty(nbytes, dtype=torch.uint8, device=self.pts.device)
+        nat.call("mwb_delay_table_tiles", self.pts.data_ptr(), self.n_pts, self.tile_info.data_ptr(),
+                 self.scan.chan.data_ptr(), self.n_chan, self.scan.ant.data_ptr(), self.scan.n_ant,
+                 self.scan.inv_scale, self.interp, self.table.data_ptr(), dv.stream_handle())
+        return self.tc_eligible()
 
     TC_WINDOW, TC_MAX_SPAN = 32, 14
 
     def tc_eligible(self) -> tuple[bool, str]:
         if self.w != self.TC_WINDOW:
             return False, f"window {self.w} != {self.TC_WINDOW}"
-        if not self.n_pts:
+        if not self.n_pts or self.table is None:
             return True, ""
         out = torch.zeros(1, dtype=torch.int32, device=dv.device())
         nat.call("mwb_table_max_span", self.table.data_ptr(), self.n_pts, self.n_chan, out.data_ptr(),
@@ -130,7 +167,7 @@ class BatchImager:
                 raise ValueError(f"outputs must be contiguous float32 (S, {nxny})")
         if out_das is None and out_dmas is None:
             raise ValueError("no output requested")
-        if self.w == 0 or s == 0:
+        if self.w == 0 or s == 0 or self.table is None:
             for out in (out_das, out_dmas):
                 if out is not None:
                     out.zero_()
@@ -142,9 +179,9 @@ class BatchImager:
             nat.call(
                 "mwb_energies_tc", sig.data_ptr(), s, self.n_chan * self.ld, self.n_chan, self.ld, self.n_samples,
                 self.scan.chan.data_ptr(), self.scan.ant.data_ptr(), self.scan.n_ant, self.scan.inv_scale,
-                self.pts.data_ptr(), self.oidx.data_ptr(), self.n_pts, None, self.table.data_ptr(), self.interp,
-                self.k0, self.w, nat.ptr(out_das), nat.ptr(out_dmas), nxny, nat.ptr(key_das), nat.ptr(key_dmas),
-                nat.ptr(flags), self._tc_ws.data_ptr(), dv.stream_handle(),
+                self.pts.data_ptr(), self.oidx.data_ptr(), self.n_pts, None, nat.ptr(self.tile_info),
+                self.table.data_ptr(), self.interp, self.k0, self.w, nat.ptr(out_das), nat.ptr(out_dmas), nxny,
+                nat.ptr(key_das), nat.ptr(key_dmas), nat.ptr(flags), self._tc_ws.data_ptr(), dv.stream_handle(),
             )
             return
         nat.call(

@@ -367,7 +367,11 @@ __global__ void __launch_bounds__(TPB) delay_table_kernel(const TableParams p) {
   const int tile0 = blockIdx.x * TILE;
   if (tile0 >= n_pts) return;
   const int n_in = p.tile_info ? p.tile_info[blockIdx.x].y : min(TILE, n_pts - tile0);
-  if (n_in <= 0) return;
+  if (n_in <= 0) {  // empty padded tile: a zero span, no words
+    for (int c = tid; c < p.C; c += TPB) p.span[(size_t)blockIdx.x * p.C + c] = make_int2(0, 0);
+    if (tid == 0) p.wide[blockIdx.x] = 0;
+    return;
+  }
   const int la = tid, lb = tid + TPB;
   const int ga = tile0 + (la < n_in ? la : 0), gb = tile0 + (lb < n_in ? lb : 0);
   const double pax = p.pts[3 * (size_t)ga], pay = p.pts[3 * (size_t)ga + 1], paz = p.pts[3 * (size_t)ga + 2];
@@ -785,6 +789,7 @@ struct LatticeParams {
   int* tile_offsets;
   int n_tiles_max;
   int tx, ty, tz;  // tile shape (tx*ty*tz == 256)
+  int2* pad_info;  // padded layout: lattice tile t -> points [256 t, 256 t + count), {0, count} here; or NULL
 };
 
 struct LatticeGeom {
@@ -884,9 +889,14 @@ __global__ void __launch_bounds__(256) lattice_write_kernel(const LatticeParams 
   __syncthreads();
   int before = 0;
   for (int w = 0; w < warp; ++w) before += wsum[w];
+  if (p.pad_info && threadIdx.x == 0) {
+    int total = 0;
+    for (int w = 0; w < 8; ++w) total += wsum[w];
+    p.pad_info[blockIdx.x] = make_int2(0, total);
+  }
   if (!ok) return;
   const int rank = before + __popc(bal & ((1u << lane) - 1u));
-  const int pos = p.tile_offsets[blockIdx.x] + rank;
+  const int pos = p.pad_info ? (int)blockIdx.x * 256 + rank : p.tile_offsets[blockIdx.x] + rank;
   const size_t slot = ((size_t)ix * p.ny + iy) * p.nz + iz;
   // cell centre origin + (i + 0.5) * res, no FMA contraction (beamform.py:321-322)
   p.pts[3 * (size_t)pos] = __dadd_rn(p.ox, __dmul_rn((double)ix + 0.5, p.res));
@@ -1970,13 +1980,13 @@ int mwb_table_max_span(const void* table, int n_pts, int n_chan, int32_t* d_out,
 int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
                     const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale,
                     const double* pts_xyz, const int32_t* out_idx, int n_pts, const int32_t* d_count,
-                    const void* table, int interp, int k0, int window, float* out_das, float* out_dmas,
-                    int64_t out_stride, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags, void* workspace,
-                    void* stream) {
+                    const int32_t* tile_info, const void* table, int interp, int k0, int window, float* out_das,
+                    float* out_dmas, int64_t out_stride, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags,
+                    void* workspace, void* stream) {
   EnergyParams e;
   bool empty;
   int rc = energy_params(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
-                         pts_xyz, out_idx, n_pts, d_count, nullptr, table, interp, k0, window, out_das, out_dmas,
+                         pts_xyz, out_idx, n_pts, d_count, tile_info, table, interp, k0, window, out_das, out_dmas,
                          out_stride, key_das, key_dmas, flags, 0, e, empty);
   if (rc || empty) return rc;
   if (window != tc::W) return set_err(MWB_EINVAL, "mwb_energies_tc: window must be %d (got %d)", tc::W, window);
@@ -2052,11 +2062,43 @@ int mwb_enumerate_lattice(double ox, double oy, double res, int nx, int ny, int 
   if (!pts_xyz || !out_idx || !d_count || !valid || !workspace)
     return set_err(MWB_EINVAL, "mwb_enumerate_lattice: null pointer");
   LatticeParams p;
+  p.pad_info = nullptr;
   p.ox = ox; p.oy = oy; p.oz = 0.0; p.res = res;
   p.nx = nx; p.ny = ny; p.nz = 1;
   p.planar = 1;
   p.r[0] = x0; p.r[1] = y0; p.r[2] = 0; p.r[3] = x1; p.r[4] = y1; p.r[5] = 0;
   p.d_region = d_region;
+  p.stride = stride;
+  p.mask = mask;
+  p.skip = skip_stride;
+  p.pts = pts_xyz;
+  p.out_idx = out_idx;
+  p.d_count = d_count;
+  p.valid = valid;
+  return enumerate_common(p, 16, 16, 1, workspace, stream);
+}
+
+int64_t mwb_lattice_tile_count(int nx, int ny, int stride) {
+  if (nx < 1 || ny < 1 || stride < 1) return -1;
+  return lattice_tiles(nx, ny, 1, stride, 16, 16, 1);
+}
+
+int mwb_enumerate_lattice_padded(double ox, double oy, double res, int nx, int ny, int x0, int y0, int x1, int y1,
+                                 int stride, const uint8_t* mask, int skip_stride, double* pts_xyz,
+                                 int32_t* out_idx, int32_t* tile_info, int32_t* d_count, uint8_t* valid,
+                                 void* workspace, void* stream) {
+  if (nx < 1 || ny < 1 || stride < 1) return set_err(MWB_EINVAL, "mwb_enumerate_lattice_padded: bad grid/stride");
+  if (x0 < 0 || y0 < 0 || x1 >= nx || y1 >= ny || x0 > x1 || y0 > y1)
+    return set_err(MWB_EINVAL, "mwb_enumerate_lattice_padded: region outside the grid");
+  if (!pts_xyz || !out_idx || !tile_info || !d_count || !valid || !workspace)
+    return set_err(MWB_EINVAL, "mwb_enumerate_lattice_padded: null pointer");
+  LatticeParams p;
+  p.pad_info = reinterpret_cast<int2*>(tile_info);
+  p.ox = ox; p.oy = oy; p.oz = 0.0; p.res = res;
+  p.nx = nx; p.ny = ny; p.nz = 1;
+  p.planar = 1;
+  p.r[0] = x0; p.r[1] = y0; p.r[2] = 0; p.r[3] = x1; p.r[4] = y1; p.r[5] = 0;
+  p.d_region = nullptr;
   p.stride = stride;
   p.mask = mask;
   p.skip = skip_stride;
@@ -2082,6 +2124,7 @@ int mwb_enumerate_volume(double ox, double oy, double oz, double res, int nx, in
   if (!pts_xyz || !out_idx || !d_count || !valid || !workspace)
     return set_err(MWB_EINVAL, "mwb_enumerate_volume: null pointer");
   LatticeParams p;
+  p.pad_info = nullptr;
   p.ox = ox; p.oy = oy; p.oz = oz; p.res = res;
   p.nx = nx; p.ny = ny; p.nz = nz;
   p.planar = 0;
@@ -2130,6 +2173,7 @@ int mwb_regions_tile_bound(const int32_t* d_regions, int n_scans, int32_t* d_bou
 static LatticeParams region_params(double ox, double oy, double res, int nx, int ny, const int32_t* d_regions,
                                    const uint8_t* mask, int skip_stride) {
   LatticeParams p;
+  p.pad_info = nullptr;
   memset(&p, 0, sizeof(p));
   p.ox = ox; p.oy = oy; p.oz = 0.0; p.res = res;
   p.nx = nx; p.ny = ny; p.nz = 1;

@@ -160,6 +160,13 @@ __device__ __forceinline__ float warp_incl_scan(float v, int lane) {
   return v;
 }
 
+// points of table tile `tile`: the padded layout's {scan, count} record, or
+// the compact list's remainder; <= 0 means nothing to do (every role skips it)
+__device__ __forceinline__ int tile_points(const EnergyParams& p, int tile, int n_pts) {
+  if (p.tile_info) return min(TILE, __ldg(&p.tile_info[tile].y));
+  return min(TILE, n_pts - tile * TILE);
+}
+
 struct Params {
   EnergyParams e;
   const uint32_t* absmax;  // [n_scans] bits of max |y| per scan
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
     int t = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int tile = item % P.n_tiles, group = item / P.n_tiles;
-      if (tile * TILE >= n_pts) continue;
+      if (tile_points(p, tile, n_pts) <= 0) continue;
       const int2* tsp = p.tab_span + (size_t)tile * p.C;
       int lo32 = 0;  // lane i holds lo of channel (c & ~31) + i
       for (int c = 0; c < p.C; ++c, ++t) {
@@ -245,7 +252,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
       int t = 0, it = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int tile = item % P.n_tiles;
-        if (tile * TILE >= n_pts) continue;
+        if (tile_points(p, tile, n_pts) <= 0) continue;
         if (it > 0) mbar_wait(acc_empty, (it - 1) & 1);
         fence_after();
         for (int c = 0; c < p.C; ++c, ++t) {
@@ -283,8 +290,8 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int tile = item % P.n_tiles, group = item / P.n_tiles;
       const int tile0 = tile * TILE;
-      if (tile0 >= n_pts) continue;
-      const int n_in = min(TILE, n_pts - tile0);
+      const int n_in = tile_points(p, tile, n_pts);
+      if (n_in <= 0) continue;
       const int nsg = min(SPG, p.n_scans - group * SPG);
       const uint32_t* tw = p.tab_words + (size_t)tile * p.C * TILE;
       const int2* tsp = p.tab_span + (size_t)tile * p.C;

@@ -113,27 +113,29 @@ def test_tc_flags_non_finite(setup):
     assert np.isfinite(got["das"][0]).all() and np.isfinite(got["das"][2]).all()  # other scans unaffected
 
 
-def test_tc_masked_grid_falls_back():
-    """A breast mask leaves partial lattice tiles, so the 256-point table tiles
-    straddle two lattice tiles and exceed the 16-tap span: "tc" refuses,
-    "auto" falls back to the fp32 kernel (bit-identical to mode "smem")."""
+def test_tc_masked_ragged_grid_padded_tiles():
+    """A breast mask on a ragged grid leaves partial lattice tiles; the padded
+    layout (table tile = 16 x 16 lattice tile, per-tile counts) keeps them on
+    the tensor cores, with cells outside the mask untouched."""
     import paper_1709_02549_b200 as mw
 
     model = synth.ScanModel()
-    sig, _ = synth.batch_2d(model, list(range(5)))
-    grid = synth.grid_square(0.05, 107)
+    sig, _ = synth.batch_2d(model, list(range(11)))
+    grid = synth.grid_square(0.05, 107)  # 0.47 mm, 107 = 6 x 16 + 11
     mask = mw.breast_mask(grid)
     win = (model.k0, model.window)
-    with pytest.raises(ValueError, match="spread"):
-        BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win, mask=mask, mode="tc")
-    auto = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win, mask=mask, mode="auto")
+    tc = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win, mask=mask, mode="tc")
     ref = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win, mask=mask)
-    assert not auto.uses_tensor_cores
-    sig_d = auto.to_device_layout(sig)
-    got, _, _ = run(auto, sig_d)
-    want, _, _ = run(ref, sig_d)
+    assert tc.uses_tensor_cores and tc.n_valid == ref.n_pts == int(mask.sum()) and tc.n_pts % 256 == 0
+    sig_d = tc.to_device_layout(sig)
+    got, gk, _ = run(tc, sig_d)
+    want, wk, _ = run(ref, sig_d)
+    inside = mask.reshape(-1)
     for k in ("das", "dmas"):
-        assert np.array_equal(got[k], want[k], equal_nan=True)
+        assert np.isnan(got[k][:, ~inside]).all()  # untouched outside the mask
+        for s in range(11):
+            assert peak_err(got[k][s][inside], want[k][s][inside]) <= TOL_FP32
+            assert tuple(gk[k][s]) == tuple(wk[k][s])
 
 
 def test_tc_eligibility():
