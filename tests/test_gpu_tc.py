@@ -148,3 +148,40 @@ def test_tc_eligibility():
     fine = synth.grid_square(0.03, 64)
     with pytest.raises(ValueError, match="window"):
         BatchImager(model.geometry(), model.pairs(), model.n_samples, fine, window=(model.k0, 48), mode="tc")
+
+
+def test_tc_nearest_interpolation(setup):
+    model, sig, grid, _, _ = setup
+    win = (model.k0, model.window)
+    tc = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win, mode="tc",
+                     interpolation="nearest")
+    ref = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win, interpolation="nearest")
+    sig_d = tc.to_device_layout(sig[:9])
+    got, _, _ = run(tc, sig_d)
+    want, _, _ = run(ref, sig_d)
+    for k in ("das", "dmas"):
+        for s in range(9):
+            assert peak_err(got[k][s], want[k][s]) <= TOL_FP32
+
+
+def test_tc_window_past_record_end():
+    """Windows that run past the record read zeros (beamform.py:192-193): the
+    producer zero-fills the staged spans beyond ld."""
+    model = synth.ScanModel(n_samples=1024)
+    sig, _ = synth.batch_2d(model, list(range(8)))
+    short = np.ascontiguousarray(sig[:, :, 300:600])  # 300-sample records: late windows overrun
+    grid = synth.grid_square(0.06, 96)
+    win = (180, 32)  # delays 40..100 samples: windows straddle the 300-sample record end
+    tc = BatchImager(model.geometry(), model.pairs(), 300, grid, window=win, mode="tc")
+    ref = BatchImager(model.geometry(), model.pairs(), 300, grid, window=win)
+    sig_d = tc.to_device_layout(short)
+    got, _, _ = run(tc, sig_d)
+    want, _, _ = run(ref, sig_d)
+    # the cut matters: the same scans with 100 more samples image differently
+    longer = np.ascontiguousarray(sig[:, :, 300:700])
+    ref_long = BatchImager(model.geometry(), model.pairs(), 400, grid, window=win)
+    want_long, _, _ = run(ref_long, ref_long.to_device_layout(longer))
+    for k in ("das", "dmas"):
+        assert np.abs(want_long[k] - want[k]).max() > 1e-3 * np.abs(want_long[k]).max()
+        for s in range(8):
+            assert peak_err(got[k][s], want[k][s]) <= TOL_FP32
