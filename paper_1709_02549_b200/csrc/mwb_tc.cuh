@@ -74,7 +74,7 @@ __host__ __device__ inline Layout layout() {
   L.ops = o;   o += (size_t)NO * OP_BYTES;
   L.stage = o; o += (size_t)NS * STAGE_BYTES;
   L.g = o;     o += 2 * NG * (size_t)SPG * 16 * sizeof(float4);  // [quad][e|x][d] float4: groups x 2 steps
-  L.qx = o;    o += (NG - 1) * (size_t)SPG * TILE * sizeof(float);  // groups 1.. Q partial sums
+  L.qx = o;    o += NG * (size_t)SPG * TILE * sizeof(float);  // every group's Q partial sums
   o = align_up(o, 8);
   L.bar = o;   o += sizeof(uint64_t) * (2 * NS + 2 * NO + 2);
   L.tmem = o;  o += 16;
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
       mbar_init(&o_empty[i], 1);
     }
     mbar_init(acc_full, 1);
-    mbar_init(acc_empty, GW);
+    mbar_init(acc_empty, NBW);
     fence_mbar_init();
   }
   if (warp == 0) {
@@ -413,28 +413,23 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
         }
       }
       t -= (c - p.C);  // c overshot C by 0..NG-1: t is now the first step of the next item
-      // ---- groups 1.. hand their Q partial sums to group 0
+      // ---- every group publishes its Q partial sums; group g then runs the
+      // epilogue for the group's scans s = g, g + NG, ... (TMEM lane quarter
+      // w8 & 3 of M-block w8 >> 2 is the same point in every group)
       float* qx = reinterpret_cast<float*>(smem + L.qx);
-      if (gp > 0) {
 #pragma unroll
-        for (int s = 0; s < SPG; ++s) qx[((gp - 1) * SPG + s) * TILE + pt] = q[s];
-      }
+      for (int s = 0; s < SPG; ++s) qx[(gp * SPG + s) * TILE + pt] = q[s];
       builders_sync();
-      if (gp > 0) continue;
-      for (int g2 = 0; g2 < NG - 1; ++g2) {
-#pragma unroll
-        for (int s = 0; s < SPG; ++s) q[s] += qx[(g2 * SPG + s) * TILE + pt];
-      }
-      // ---- epilogue (group 0): S rows from TMEM -> energies
       mbar_wait(acc_full, it & 1);
       fence_after();
       const bool valid = pt < n_in;
       const int g = tile0 + (valid ? pt : 0);
       const int slot_out = valid ? (p.out_idx ? __ldg(p.out_idx + g) : g) : -1;
       const uint32_t lane_base = (uint32_t)((w8 & 3) * 32) << 16;
+      for (int s = gp; s < nsg; s += NG) {  // warp-uniform
+        float qs = 0.f;
 #pragma unroll
-      for (int s = 0; s < SPG; ++s) {
-        if (s >= nsg) break;  // warp-uniform
+        for (int g2 = 0; g2 < NG; ++g2) qs += qx[(g2 * SPG + s) * TILE + pt];
         float v[32];
         tmem_ld32(tmem + lane_base + (uint32_t)(mb * N + s * W), v);
         float e0 = 0.f, e1 = 0.f;
@@ -450,7 +445,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
         for (int kk = 0; kk < 2; ++kk) {
           const bool want = kk == 0 ? KIND != KIND_DMAS : KIND != KIND_DAS;
           if (!want) continue;
-          const float raw = kk == 0 ? __double2float_rn(E) : __double2float_rn(0.5 * (E - (double)q[s]));
+          const float raw = kk == 0 ? __double2float_rn(E) : __double2float_rn(0.5 * (E - (double)qs));
           const float en = raw * inv * inv;
           float* out = (kk == 0 ? p.out_das : p.out_dmas) + (size_t)scan * (size_t)p.out_stride;
           unsigned long long* keys = kk == 0 ? p.key_das : p.key_dmas;
@@ -466,6 +461,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
           }
         }
       }
+      builders_sync();  // every group has read qx before the next item overwrites it
       if (p.flags && (bad || bad_span)) atomicOr(p.flags, (bad ? 1 : 0) | (bad_span ? 2 : 0));
       fence_before();
       __syncwarp();

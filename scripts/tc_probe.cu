@@ -174,6 +174,60 @@ __global__ void probe_tmem_a(const __half* a, const __half* b, float* d) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// Throughput of back-to-back M128 x N x K16 SS MMAs (no-swizzle operands),
+// 6 per iteration with a commit per iteration, as the energy kernel issues them.
+template <int N>
+__global__ void mma_rate(int iters, long long* cycles) {
+  __shared__ __align__(1024) unsigned char sa[2 * M * K * 2];
+  __shared__ __align__(1024) unsigned char sb[2 * N * K * 2];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < (int)sizeof(sa) / 2; i += blockDim.x) reinterpret_cast<__half*>(sa)[i] = __float2half(0.001f);
+  for (int i = tid; i < (int)sizeof(sb) / 2; i += blockDim.x) reinterpret_cast<__half*>(sb)[i] = __float2half(0.001f);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    const uint32_t id = idesc_f16(M, N);
+    const uint64_t a0 = smem_desc(sa, 128, 256), a1 = smem_desc(sa + M * K * 2, 128, 256);
+    const uint64_t b0 = smem_desc(sb, 128, 256), b1 = smem_desc(sb + N * K * 2, 128, 256);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      for (int mb = 0; mb < 2; ++mb) {
+        const uint32_t d = tmem + mb * N;
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+                     ::"r"(d), "l"(mb ? a1 : a0), "l"(b0), "r"(id), "r"(1));
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+                     ::"r"(d), "l"(mb ? a1 : a0), "l"(b1), "r"(id), "r"(1));
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+                     ::"r"(d), "l"(mb ? a0 : a1), "l"(b0), "r"(id), "r"(1));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+    }
+    // wait for the last commit's phase
+    const uint32_t parity = (uint32_t)((iters - 1) & 1);
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT3:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT3;\n}\n" ::"r"(
+            smem_u32(&bar)), "r"(parity) : "memory");
+    *cycles = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 int main() {
   constexpr int N = 256;
   std::vector<__half> ha(M * K), hb(N * K);
@@ -218,5 +272,14 @@ int main() {
       if (err > 1e-3 && bad2++ < 5) printf("bad2 (%d,%d): got %f want %f\n", i, j, hd[i * N2 + j], s);
     }
   printf("tmem-A: max abs err %g, bad %d of %d\n", maxerr2, bad2, M * N2);
+  long long* dcyc; cudaMalloc(&dcyc, 8);
+  for (int iters : {1000, 4000}) {
+    mma_rate<256><<<1, 128>>>(iters, dcyc);
+    cudaDeviceSynchronize();
+    long long cyc; cudaMemcpy(&cyc, dcyc, 8, cudaMemcpyDeviceToHost);
+    const double macs = (double)iters * 6 * 128.0 * 256 * 16;
+    printf("mma_rate N=256 iters=%d: %lld cycles, %.0f MAC/clk (%.1f clk per MMA)\n", iters, cyc, macs / cyc,
+           (double)cyc / (iters * 6.0));
+  }
   return (bad != 0) || (bad2 != 0);
 }
