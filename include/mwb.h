@@ -296,17 +296,26 @@ int mwb_simulate(float* out, int n_scans, int n_chan, int n_samples, int ld, con
  * channel self-terms come from windowed Gram entries.  Requirements: window
  * == 32 and every tile's per-channel delay spread <= 14 samples (check once
  * per table with mwb_table_max_span); otherwise use mwb_energies.  A tile
- * found to violate the spread limit sets bit 1 (value 2) of *flags.
- * Workspace: mwb_energies_tc_workspace_bytes(n_scans) (per-scan scales).
+ * found to violate the spread limit sets bit 1 (value 2) of *flags; a span
+ * start outside [j_lo, j_lo + j_count - 16] sets bit 2 (value 4).  The DMAS
+ * self-terms come from windowed Gram entries precomputed per (scan,
+ * channel, window offset j in [j_lo, j_lo + j_count)) by a pre-pass that also
+ * takes each scan's max |y| (the per-scan fp16 scale).
+ * Workspace: mwb_energies_tc_workspace_bytes(n_scans, n_chan, j_count).
  */
-int64_t mwb_energies_tc_workspace_bytes(int n_scans);
+int64_t mwb_energies_tc_workspace_bytes(int n_scans, int n_chan, int j_count);
 int mwb_table_max_span(const void* table, int n_pts, int n_chan, int32_t* d_out, void* stream);
+/* smallest / largest per-channel span start lo over the table's non-empty
+ * tiles -> d_out[0], d_out[1]; the window-offset range of mwb_energies_tc is
+ * j_lo = d_out[0], j_count = d_out[1] + 16 - d_out[0]. */
+int mwb_table_lo_range(const void* table, int n_pts, int n_chan, const int32_t* tile_info, int32_t* d_out,
+                       void* stream);
 int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
                     const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale,
                     const double* pts_xyz, const int32_t* out_idx, int n_pts, const int32_t* d_count,
                     const int32_t* tile_info, const void* table, int interp, int k0, int window, float* out_das,
                     float* out_dmas, int64_t out_stride, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags,
-                    void* workspace, void* stream);
+                    int j_lo, int j_count, void* workspace, void* stream);
 
 /*
  * Padded lattice enumeration (for mwb_energies_tc on masked or ragged grids):

@@ -121,7 +121,16 @@ class BatchImager:
         nat.call("mwb_delay_table_tiles", self.pts.data_ptr(), self.n_pts, self.tile_info.data_ptr(),
                  self.scan.chan.data_ptr(), self.n_chan, self.scan.ant.data_ptr(), self.scan.n_ant,
                  self.scan.inv_scale, self.interp, self.table.data_ptr(), dv.stream_handle())
-        return self.tc_eligible()
+        ok, why = self.tc_eligible()
+        if ok:
+            # window offsets j = lo_c + d the tiles use: the range of the
+            # precomputed Gram entries (DMAS self-terms)
+            rng = torch.empty(2, dtype=torch.int32, device=self.pts.device)
+            nat.call("mwb_table_lo_range", self.table.data_ptr(), self.n_pts, self.n_chan,
+                     self.tile_info.data_ptr(), rng.data_ptr(), dv.stream_handle())
+            lo_min, lo_max = (int(v) for v in rng.cpu().tolist())
+            self.j_lo, self.j_count = lo_min, lo_max + 16 - lo_min
+        return ok, why
 
     TC_WINDOW, TC_MAX_SPAN = 32, 14
 
@@ -173,7 +182,7 @@ class BatchImager:
                     out.zero_()
             return
         if self.mode == 2:
-            nbytes = int(nat.load().mwb_energies_tc_workspace_bytes(s))
+            nbytes = int(nat.load().mwb_energies_tc_workspace_bytes(s, self.n_chan, self.j_count))
             if self._tc_ws is None or self._tc_ws.numel() < nbytes:
                 self._tc_ws = torch.empty(nbytes, dtype=torch.uint8, device=sig.device)
             nat.call(
@@ -181,7 +190,8 @@ class BatchImager:
                 self.scan.chan.data_ptr(), self.scan.ant.data_ptr(), self.scan.n_ant, self.scan.inv_scale,
                 self.pts.data_ptr(), self.oidx.data_ptr(), self.n_pts, None, nat.ptr(self.tile_info),
                 self.table.data_ptr(), self.interp, self.k0, self.w, nat.ptr(out_das), nat.ptr(out_dmas), nxny,
-                nat.ptr(key_das), nat.ptr(key_dmas), nat.ptr(flags), self._tc_ws.data_ptr(), dv.stream_handle(),
+                nat.ptr(key_das), nat.ptr(key_dmas), nat.ptr(flags), self.j_lo, self.j_count, self._tc_ws.data_ptr(),
+                dv.stream_handle(),
             )
             return
         nat.call(

@@ -21,6 +21,7 @@
 //     whichever tile or call evaluates it;
 //   * 32 window samples per point live in registers (float2 s[32]); the
 //     per-point accumulation order over channels and samples is fixed.
+#include <cuda.h>  // CUtensorMap (types only; the encoder comes through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <algorithm>
@@ -1955,9 +1956,68 @@ int mwb_energies_tiles(const float* sig, int n_scans, int64_t scan_stride, int n
 }
 
 // ---- tensor-core path (mwb_tc.cuh) ----------------------------------------
-int64_t mwb_energies_tc_workspace_bytes(int n_scans) {
-  if (n_scans < 0) return -1;
-  return (int64_t)align_up(sizeof(uint32_t) * (size_t)(n_scans > 0 ? n_scans : 1), 256);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// 3-D fp32 tensor map {d0, d1, d2} (elements; d0 contiguous), row strides in
+// bytes, box {b0, b1, b2}; out-of-bounds elements load as zeros
+static int encode_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1,
+                     uint64_t stride2, uint32_t b0, uint32_t b1, uint32_t b2) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return set_err(MWB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {stride1, stride2};
+  const cuuint32_t box[3] = {b0, b1, b2};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(MWB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return MWB_OK;
+}
+
+// workspace: [absmax u32 x S | gram {E, X} float4 pairs x quads*C*J]
+static size_t tc_ws_absmax(int n_scans) { return align_up(sizeof(uint32_t) * (size_t)(n_scans > 0 ? n_scans : 1), 256); }
+static size_t tc_ws_gram(int n_scans, int n_chan, int j_count) {
+  return 2 * sizeof(float4) * (size_t)((n_scans + 3) / 4) * (size_t)n_chan * (size_t)j_count;
+}
+
+int64_t mwb_energies_tc_workspace_bytes(int n_scans, int n_chan, int j_count) {
+  if (n_scans < 0 || n_chan < 1 || j_count < 16) return -1;
+  return (int64_t)(tc_ws_absmax(n_scans) + align_up(tc_ws_gram(n_scans, n_chan, j_count), 256));
+}
+
+int mwb_table_lo_range(const void* table, int n_pts, int n_chan, const int32_t* tile_info, int32_t* d_out,
+                       void* stream) {
+  if (!table || !d_out || n_pts < 0 || n_chan < 1) return set_err(MWB_EINVAL, "mwb_table_lo_range: bad arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(d_out, 0x7F, sizeof(int32_t), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_out + 1, 0xFF, sizeof(int32_t), st);
+  if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
+  if (n_pts == 0) return MWB_OK;
+  const long long tiles = (n_pts + TILE - 1) / TILE;
+  const TableLayout T = table_layout(tiles, n_chan);
+  const unsigned char* base = reinterpret_cast<const unsigned char*>(table);
+  long long blocks = (tiles * n_chan + 255) / 256;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  tc::table_lo_range_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const int2*>(base + T.span),
+                                                              reinterpret_cast<const int2*>(tile_info), tiles,
+                                                              n_chan, d_out);
+  return check_launch("table_lo_range_kernel");
 }
 
 int mwb_table_max_span(const void* table, int n_pts, int n_chan, int32_t* d_out, void* stream) {
@@ -1982,7 +2042,7 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
                     const double* pts_xyz, const int32_t* out_idx, int n_pts, const int32_t* d_count,
                     const int32_t* tile_info, const void* table, int interp, int k0, int window, float* out_das,
                     float* out_dmas, int64_t out_stride, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags,
-                    void* workspace, void* stream) {
+                    int j_lo, int j_count, void* workspace, void* stream) {
   EnergyParams e;
   bool empty;
   int rc = energy_params(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
@@ -1991,17 +2051,32 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
   if (rc || empty) return rc;
   if (window != tc::W) return set_err(MWB_EINVAL, "mwb_energies_tc: window must be %d (got %d)", tc::W, window);
   if (!workspace) return set_err(MWB_EINVAL, "mwb_energies_tc: null workspace");
+  if (j_lo < 0 || j_count < 16) return set_err(MWB_EINVAL, "mwb_energies_tc: bad window-offset range");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  uint32_t* absmax = reinterpret_cast<uint32_t*>(workspace);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  uint32_t* absmax = reinterpret_cast<uint32_t*>(ws);
+  float4* gx = reinterpret_cast<float4*>(ws + tc_ws_absmax(n_scans));
   cudaError_t ce = cudaMemsetAsync(absmax, 0, sizeof(uint32_t) * (size_t)n_scans, st);
   if (ce != cudaSuccess) return set_err(MWB_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
-  const long long per_scan = (long long)n_chan * ld;
-  const unsigned bx = (unsigned)std::min<long long>(8, (per_scan / 4 + 255) / 256);
-  tc::scan_absmax_kernel<<<dim3(bx, (unsigned)n_scans), 256, 0, st>>>(sig, scan_stride, per_scan, absmax);
-  if ((rc = check_launch("scan_absmax_kernel"))) return rc;
+  {
+    const size_t sm = sizeof(float) * 4 * (size_t)(j_count + tc::W + 1);
+    if (sm > 48 * 1024) return set_err(MWB_ERANGE, "mwb_energies_tc: window-offset range %d too wide", j_count);
+    tc::gram_kernel<<<dim3((unsigned)n_chan, (unsigned)((n_scans + 3) / 4)), 128, sm, st>>>(
+        sig, scan_stride, n_scans, n_chan, ld, k0, j_lo, j_count, gx, absmax);
+    if ((rc = check_launch("gram_kernel"))) return rc;
+  }
   tc::Params P;
   P.e = e;
   P.absmax = absmax;
+  P.j_lo = j_lo;
+  P.J = j_count;
+  const int quads = (n_scans + 3) / 4;
+  if ((rc = encode_3d(&P.tm_sig, sig, (uint64_t)ld, (uint64_t)n_chan, (uint64_t)n_scans, (uint64_t)ld * 4,
+                      (uint64_t)scan_stride * 4, tc::SPANF, 1, tc::SPG)))
+    return rc;
+  if ((rc = encode_3d(&P.tm_gram, gx, (uint64_t)8 * j_count, (uint64_t)n_chan, (uint64_t)quads,
+                      (uint64_t)32 * j_count, (uint64_t)32 * j_count * n_chan, 128, 1, tc::SPG / 4)))
+    return rc;
   P.n_tiles = (n_pts + TILE - 1) / TILE;
   P.n_groups = (n_scans + tc::SPG - 1) / tc::SPG;
   const tc::Layout L = tc::layout();

@@ -60,6 +60,7 @@ constexpr int MB_BYTES = 128 * K * 2;      // one M-block: 4 KB
 constexpr int H_BYTES = N * K * 2;         // 8 KB
 constexpr int OP_BYTES = 2 * A_BYTES + 2 * H_BYTES;
 constexpr int STAGE_BYTES = SPG * SPANF * 4;
+constexpr int GQ_FLOAT4 = (SPG / 4) * 2 * 16;  // per stage: [quad][d = 0..15][e, x] float4
 constexpr int TMEM_COLS = 512;             // two M-blocks x N fp32 columns
 constexpr uint32_t LBO = 128, SBO = 256;   // core-matrix strides (bytes)
 constexpr size_t SMEM_MIN = 120 * 1024;    // > half the SM: one CTA per SM (TMEM is sized for one)
@@ -73,7 +74,7 @@ __host__ __device__ inline Layout layout() {
   size_t o = 0;
   L.ops = o;   o += (size_t)NO * OP_BYTES;
   L.stage = o; o += (size_t)NS * STAGE_BYTES;
-  L.g = o;     o += 2 * NG * (size_t)SPG * 16 * sizeof(float4);  // [quad][e|x][d] float4: groups x 2 steps
+  L.g = o;     o += (size_t)NS * GQ_FLOAT4 * sizeof(float4);  // staged Gram slices, one per sample stage
   L.qx = o;    o += NG * (size_t)SPG * TILE * sizeof(float);  // every group's Q partial sums
   o = align_up(o, 8);
   L.bar = o;   o += sizeof(uint64_t) * (2 * NS + 2 * NO + 2);
@@ -101,6 +102,14 @@ __device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uin
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void commit(uint64_t* bar) {
@@ -167,21 +176,25 @@ __device__ __forceinline__ int tile_points(const EnergyParams& p, int tile, int 
   return min(TILE, n_pts - tile * TILE);
 }
 
-struct Params {
+struct alignas(64) Params {
+  CUtensorMap tm_sig;   // 3-D {ld, C, S} fp32: box {SPANF, 1, SPG} = one channel's spans of a scan group
+  CUtensorMap tm_gram;  // 3-D {8 J, C, quads} fp32 (interleaved {E, X} float4 pairs): box {128, 1, SPG / 4}
   EnergyParams e;
-  const uint32_t* absmax;  // [n_scans] bits of max |y| per scan
+  const uint32_t* absmax;  // [n_scans] bits of max |y| per scan (over the samples any window touches)
+
+  int j_lo, J;             // positions j = lo_c + d, j in [j_lo, j_lo + J)
   int n_tiles;
   int n_groups;
 };
 
 template <int KIND>
-__global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
+__global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const EnergyParams& p = P.e;
   const Layout L = layout();
   unsigned char* ops = smem + L.ops;
   float* stage = reinterpret_cast<float*>(smem + L.stage);
-  float* gbuf = reinterpret_cast<float*>(smem + L.g);
+  float* gstage = reinterpret_cast<float*>(smem + L.g);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
   uint64_t* s_full = bar;
   uint64_t* s_empty = bar + NS;
@@ -231,19 +244,18 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
         if ((c & 31) == 0) lo32 = c + lane < p.C ? __ldg(&tsp[c + lane].x) : 0;
         const int lo_c = __shfl_sync(0xffffffffu, lo32, c & 31);
         if (use > 0) mbar_wait(&s_empty[slot], (use - 1) & 1);
-        const long long start4 = ((long long)p.k0 + lo_c) & ~3LL;
-        // every scan of the group stages the same span [start4, start4 + n)
-        const int n = (int)min((long long)SPANF, max((long long)p.ld - start4, 0LL));
-        const int nsg = min(SPG, p.n_scans - group * SPG);
-        float* dst = stage + slot * (STAGE_BYTES / 4) + lane * SPANF;
-        if (lane < SPG && (n < SPANF || lane >= nsg))  // past the record / no such scan: zeros
-          for (int j = lane < nsg ? n : 0; j < SPANF; ++j) dst[j] = 0.f;
-        __syncwarp();  // zero-fills ordered before lane 0's release
-        if (lane == 0) mbar_arrive_expect_tx(&s_full[slot], (uint32_t)(nsg * n * 4));
+        // one tensor copy stages the group's spans (zeros past the record and
+        // past the last scan), one more the two quads' Gram slices
+        if (lane == 0) {
+          const int start4 = (p.k0 + lo_c) & ~3;
+          const int off = min(max(lo_c - P.j_lo, 0), P.J - 16);  // in range by construction (j_lo, J from the table)
+          if (off != lo_c - P.j_lo && p.flags) atomicOr(p.flags, 4);
+          mbar_arrive_expect_tx(&s_full[slot], (uint32_t)(STAGE_BYTES + GQ_FLOAT4 * 16));
+          tma_load_3d(stage + slot * (STAGE_BYTES / 4), &P.tm_sig, start4, c, group * SPG, &s_full[slot]);
+          tma_load_3d(reinterpret_cast<float4*>(gstage) + slot * GQ_FLOAT4, &P.tm_gram, 8 * off, c,
+                      group * (SPG / 4), &s_full[slot]);
+        }
         __syncwarp();
-        if (lane < nsg && n > 0)
-          bulk_g2s(dst, p.sig + (size_t)(group * SPG + lane) * (size_t)p.scan_stride + (size_t)c * p.ld + start4,
-                   (uint32_t)(n * 4), &s_full[slot]);
       }
     }
   } else if (warp == NBW + 1) {
@@ -367,50 +379,24 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
           *reinterpret_cast<uint4*>(hl + kmajor_off(n, 0)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
           *reinterpret_cast<uint4*>(hl + kmajor_off(n, 1)) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
         }
-        float4* gsl = reinterpret_cast<float4*>(gbuf) + ((gp * 2 + (my & 1)) * SPG) * 16;
-        {
-          // e(d) = sum_{i=d}^{d+31} y_i^2 and x(d) = sum y_i y_{i+1} over the
-          // 48 staged samples y_0..y_47 of scan w8, d = 0..15, from inclusive
-          // warp scans of the two 32-sample halves
-          const float v0 = ys[lane] * h_scale;
-          const float v1 = lane < 16 ? ys[lane + 32] * h_scale : 0.f;
-          const float dn0 = __shfl_down_sync(0xffffffffu, v0, 1);
-          const float h1 = __shfl_sync(0xffffffffu, v1, 0);
-          const float dn1 = __shfl_down_sync(0xffffffffu, v1, 1);
-          const float n0 = lane == 31 ? h1 : dn0;
-          const float n1 = lane == 31 ? 0.f : dn1;
-          const float S0 = warp_incl_scan(v0 * v0, lane), S1 = warp_incl_scan(v1 * v1, lane);
-          const float X0 = warp_incl_scan(v0 * n0, lane), X1 = warp_incl_scan(v1 * n1, lane);
-          const float Ts = __shfl_sync(0xffffffffu, S0, 31), Tx = __shfl_sync(0xffffffffu, X0, 31);
-          const float ps = __shfl_up_sync(0xffffffffu, S1 - S0, 1);
-          const float px = __shfl_up_sync(0xffffffffu, X1 - X0, 1);
-          const float e = lane == 0 ? Ts : Ts + ps;
-          const float x = lane == 0 ? Tx : Tx + px;
-          // layout [quad][e | x][d] of float4 = 4 scans: e(d) of scans 4q..4q+3
-          float* gq = reinterpret_cast<float*>(gsl + (w8 >> 2) * 32) + (w8 & 3);
-          if (lane < 16) {
-            gq[lane * 4] = e;
-            gq[(16 + lane) * 4] = x;
-          }
-        }
         fence_async_smem();  // A / H generic writes -> visible to the tensor core
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&o_full[oslot]);
-          mbar_arrive(&s_empty[slot]);
-        }
-        group_sync(gp);  // this group's Gram entries of channel c are in place
+        if (lane == 0) mbar_arrive(&o_full[oslot]);
         {
+          // Q += f0^2 e(d) + 2 f0 f1 x(d) + f1^2 e(d + 1), 4 scans per LDS.128
           const float w0 = f0 * f0, w1 = 2.f * f0 * f1, w2 = f1 * f1;
+          const float4* gsl = reinterpret_cast<const float4*>(gstage) + slot * GQ_FLOAT4;
 #pragma unroll
           for (int qd = 0; qd < SPG / 4; ++qd) {
-            const float4 E = gsl[qd * 32 + d], E1 = gsl[qd * 32 + d + 1], X = gsl[qd * 32 + 16 + d];
+            const float4 E = gsl[qd * 32 + 2 * d], X = gsl[qd * 32 + 2 * d + 1], E1 = gsl[qd * 32 + 2 * d + 2];
             q[4 * qd + 0] = fmaf(w0, E.x, fmaf(w1, X.x, fmaf(w2, E1.x, q[4 * qd + 0])));
             q[4 * qd + 1] = fmaf(w0, E.y, fmaf(w1, X.y, fmaf(w2, E1.y, q[4 * qd + 1])));
             q[4 * qd + 2] = fmaf(w0, E.z, fmaf(w1, X.z, fmaf(w2, E1.z, q[4 * qd + 2])));
             q[4 * qd + 3] = fmaf(w0, E.w, fmaf(w1, X.w, fmaf(w2, E1.w, q[4 * qd + 3])));
           }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[slot]);  // samples and Gram slices consumed
       }
       t -= (c - p.C);  // c overshot C by 0..NG-1: t is now the first step of the next item
       // ---- every group publishes its Q partial sums; group g then runs the
@@ -440,13 +426,13 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
         }
         const int scan = group * SPG + s;
         const float inv = pow2f(-scale_exp(__ldg(P.absmax + scan)));
-        const double E = (double)e0 + (double)e1;
+        const double E = ((double)e0 + (double)e1) * (double)inv * (double)inv;  // S was in scaled units
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
           const bool want = kk == 0 ? KIND != KIND_DMAS : KIND != KIND_DAS;
           if (!want) continue;
           const float raw = kk == 0 ? __double2float_rn(E) : __double2float_rn(0.5 * (E - (double)qs));
-          const float en = raw * inv * inv;
+          const float en = raw;
           float* out = (kk == 0 ? p.out_das : p.out_dmas) + (size_t)scan * (size_t)p.out_stride;
           unsigned long long* keys = kk == 0 ? p.key_das : p.key_dmas;
           unsigned long long key = 0ull;
@@ -475,20 +461,86 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const Params P) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
-// max |y| of each scan (bits; non-negative floats order like their bits)
-__global__ void scan_absmax_kernel(const float* sig, long long scan_stride, long long per_scan, uint32_t* out) {
-  const int s = blockIdx.y;
-  const float* base = sig + (size_t)s * (size_t)scan_stride;
-  uint32_t m = 0u;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < per_scan / 4;
-       i += (long long)gridDim.x * blockDim.x) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(base) + i);
-    m = max(m, max(max(__float_as_uint(fabsf(v.x)), __float_as_uint(fabsf(v.y))),
-                   max(__float_as_uint(fabsf(v.z)), __float_as_uint(fabsf(v.w)))));
+// Windowed Gram entries of every (scan quad, channel) at window offsets
+// j in [j_lo, j_lo + J) past k0: E(j) = sum_{k<W} y[k0+j+k]^2 and
+// X(j) = sum_{k<W} y[k0+j+k] y[k0+j+k+1] (zeros past the record), the 4
+// scans of the quad interleaved per float4, stored as {E, X} pairs.  They depend on the absolute
+// window start only, so every tile's DMAS self-terms gather from them.  The
+// same pass takes each scan's max |y| over the samples any window touches
+// (bits; non-negative floats order like their bits), the input of the
+// per-scan power-of-two scale.
+__global__ void __launch_bounds__(128) gram_kernel(const float* sig, long long scan_stride, int n_scans, int C,
+                                                   int ld, int k0, int j_lo, int J, float4* gx, uint32_t* absmax) {
+  extern __shared__ float yq[];  // [4][R]
+  __shared__ uint32_t wmax[4][4];
+  const int c = blockIdx.x, quad = blockIdx.y, tid = threadIdx.x;
+  const int R = J + W + 1;
+  const long long base = (long long)k0 + j_lo;
+  uint32_t m[4];
+#pragma unroll
+  for (int sq = 0; sq < 4; ++sq) {
+    m[sq] = 0u;
+    const int s = quad * 4 + sq;
+    const float* row = sig + (size_t)s * (size_t)scan_stride + (size_t)c * ld;
+    for (int r = tid; r < R; r += blockDim.x) {
+      const long long idx = base + r;
+      const float v = (s < n_scans && idx < ld) ? __ldg(row + idx) : 0.f;
+      yq[sq * R + r] = v;
+      m[sq] = max(m[sq], __float_as_uint(fabsf(v)));
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m) atomicMax(out + s, m);
+  for (int sq = 0; sq < 4; ++sq) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m[sq] = max(m[sq], __shfl_xor_sync(0xffffffffu, m[sq], o));
+    if ((tid & 31) == 0) wmax[sq][tid >> 5] = m[sq];
+  }
+  __syncthreads();
+  if (tid < 4) {
+    const uint32_t v = max(max(wmax[tid][0], wmax[tid][1]), max(wmax[tid][2], wmax[tid][3]));
+    if (quad * 4 + tid < n_scans && v) atomicMax(absmax + quad * 4 + tid, v);
+  }
+  const size_t row_out = ((size_t)quad * C + c) * J;
+  for (int jj = tid; jj < J; jj += blockDim.x) {
+    float e[4], x[4];
+#pragma unroll
+    for (int sq = 0; sq < 4; ++sq) {
+      const float* y = yq + sq * R + jj;
+      float a = 0.f, b = 0.f;
+#pragma unroll 8
+      for (int k = 0; k < W; ++k) {
+        a = fmaf(y[k], y[k], a);
+        b = fmaf(y[k], y[k + 1], b);
+      }
+      e[sq] = a;
+      x[sq] = b;
+    }
+    gx[2 * (row_out + jj)] = make_float4(e[0], e[1], e[2], e[3]);
+    gx[2 * (row_out + jj) + 1] = make_float4(x[0], x[1], x[2], x[3]);
+  }
+}
+
+// smallest and largest per-channel span start lo over the table's non-empty
+// tiles (out[0] atomicMin, out[1] atomicMax; the caller presets them)
+__global__ void table_lo_range_kernel(const int2* span, const int2* tile_info, long long tiles, int C, int* out) {
+  int mn = 0x7FFFFFFF, mx = -1;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < tiles * C;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long tile = i / C;
+    if (tile_info && tile_info[tile].y <= 0) continue;
+    const int lo = span[i].x;
+    mn = min(mn, lo);
+    mx = max(mx, lo);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, mn);
+    atomicMax(out + 1, mx);
+  }
 }
 
 // largest per-channel delay spread (hi - lo) over the table's tiles; wide
