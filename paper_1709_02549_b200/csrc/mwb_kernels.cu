@@ -1973,32 +1973,37 @@ static EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-// 3-D fp32 tensor map {d0, d1, d2} (elements; d0 contiguous), row strides in
+// 3-D tensor map {d0, d1, d2} (elements; d0 contiguous), row strides in
 // bytes, box {b0, b1, b2}; out-of-bounds elements load as zeros
 static int encode_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1,
-                     uint64_t stride2, uint32_t b0, uint32_t b1, uint32_t b2) {
+                     uint64_t stride2, uint32_t b0, uint32_t b1, uint32_t b2, CUtensorMapDataType type) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return set_err(MWB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[3] = {d0, d1, d2};
   const cuuint64_t strides[2] = {stride1, stride2};
   const cuuint32_t box[3] = {b0, b1, b2};
   const cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+  const CUresult r = fn(m, type, 3, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(MWB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return MWB_OK;
 }
 
-// workspace: [absmax u32 x S | gram {E, X} float4 pairs x quads*C*J]
+// workspace: [absmax u32 x S | gram {E, X} float4 pairs x quads*C*J | fp16 planes S*C*2*Lp]
 static size_t tc_ws_absmax(int n_scans) { return align_up(sizeof(uint32_t) * (size_t)(n_scans > 0 ? n_scans : 1), 256); }
 static size_t tc_ws_gram(int n_scans, int n_chan, int j_count) {
   return 2 * sizeof(float4) * (size_t)((n_scans + 3) / 4) * (size_t)n_chan * (size_t)j_count;
 }
+static int tc_plane_len(int j_count) { return (j_count + 40 + 7) & ~7; }  // covers offset + 53, 16-B rows
+static size_t tc_ws_planes(int n_scans, int n_chan, int j_count) {
+  return sizeof(__half) * 2 * (size_t)n_scans * (size_t)n_chan * (size_t)tc_plane_len(j_count);
+}
 
 int64_t mwb_energies_tc_workspace_bytes(int n_scans, int n_chan, int j_count) {
   if (n_scans < 0 || n_chan < 1 || j_count < 16) return -1;
-  return (int64_t)(tc_ws_absmax(n_scans) + align_up(tc_ws_gram(n_scans, n_chan, j_count), 256));
+  return (int64_t)(tc_ws_absmax(n_scans) + align_up(tc_ws_gram(n_scans, n_chan, j_count), 256) +
+                   align_up(tc_ws_planes(n_scans, n_chan, j_count), 256));
 }
 
 int mwb_table_lo_range(const void* table, int n_pts, int n_chan, const int32_t* tile_info, int32_t* d_out,
@@ -2056,14 +2061,20 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
   unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
   uint32_t* absmax = reinterpret_cast<uint32_t*>(ws);
   float4* gx = reinterpret_cast<float4*>(ws + tc_ws_absmax(n_scans));
+  __half* planes = reinterpret_cast<__half*>(ws + tc_ws_absmax(n_scans) +
+                                             align_up(tc_ws_gram(n_scans, n_chan, j_count), 256));
+  const int Lp = tc_plane_len(j_count);
   cudaError_t ce = cudaMemsetAsync(absmax, 0, sizeof(uint32_t) * (size_t)n_scans, st);
   if (ce != cudaSuccess) return set_err(MWB_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
   {
-    const size_t sm = sizeof(float) * 4 * (size_t)(j_count + tc::W + 1);
+    const size_t sm = sizeof(float) * 4 * (size_t)Lp;
     if (sm > 48 * 1024) return set_err(MWB_ERANGE, "mwb_energies_tc: window-offset range %d too wide", j_count);
     tc::gram_kernel<<<dim3((unsigned)n_chan, (unsigned)((n_scans + 3) / 4)), 128, sm, st>>>(
-        sig, scan_stride, n_scans, n_chan, ld, k0, j_lo, j_count, gx, absmax);
+        sig, scan_stride, n_scans, n_chan, ld, k0, j_lo, j_count, Lp, gx, absmax);
     if ((rc = check_launch("gram_kernel"))) return rc;
+    tc::planes_kernel<<<dim3((unsigned)n_chan, (unsigned)n_scans), 128, 0, st>>>(sig, scan_stride, n_chan, ld, k0,
+                                                                                  j_lo, Lp, absmax, planes);
+    if ((rc = check_launch("planes_kernel"))) return rc;
   }
   tc::Params P;
   P.e = e;
@@ -2071,11 +2082,13 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
   P.j_lo = j_lo;
   P.J = j_count;
   const int quads = (n_scans + 3) / 4;
-  if ((rc = encode_3d(&P.tm_sig, sig, (uint64_t)ld, (uint64_t)n_chan, (uint64_t)n_scans, (uint64_t)ld * 4,
-                      (uint64_t)scan_stride * 4, tc::SPANF, 1, tc::SPG)))
+  P.Lp = Lp;
+  if ((rc = encode_3d(&P.tm_planes, planes, (uint64_t)Lp, (uint64_t)2 * n_chan, (uint64_t)n_scans, (uint64_t)Lp * 2,
+                      (uint64_t)Lp * 2 * 2 * n_chan, tc::SPANH, 2, tc::SPG, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)))
     return rc;
   if ((rc = encode_3d(&P.tm_gram, gx, (uint64_t)8 * j_count, (uint64_t)n_chan, (uint64_t)quads,
-                      (uint64_t)32 * j_count, (uint64_t)32 * j_count * n_chan, 128, 1, tc::SPG / 4)))
+                      (uint64_t)32 * j_count, (uint64_t)32 * j_count * n_chan, 128, 1, tc::SPG / 4,
+                      CU_TENSOR_MAP_DATA_TYPE_FLOAT32)))
     return rc;
   P.n_tiles = (n_pts + TILE - 1) / TILE;
   P.n_groups = (n_scans + tc::SPG - 1) / tc::SPG;

@@ -44,7 +44,7 @@ constexpr int SPG = 8;                     // scans per group
 constexpr int N = SPG * W;                 // MMA N: 256
 static_assert(SPG % 4 == 0, "Gram entries are interleaved by 4 scans");
 constexpr int K = 16;                      // taps per channel: d + 1 <= K - 1
-constexpr int SPANF = 52;                  // staged floats per (scan, channel): 3 + W + K, rounded to 4
+constexpr int SPANH = 56;                  // staged halves per (scan, channel, plane): 7 + W + K, rounded to 8
 constexpr int NS = 16;                     // sample ring depth
 constexpr int NO = 4;                      // operand ring depth
 #ifndef MWB_TC_GROUPS
@@ -59,7 +59,7 @@ constexpr int A_BYTES = TILE * K * 2;      // one of hi/lo, both M-blocks: 8 KB
 constexpr int MB_BYTES = 128 * K * 2;      // one M-block: 4 KB
 constexpr int H_BYTES = N * K * 2;         // 8 KB
 constexpr int OP_BYTES = 2 * A_BYTES + 2 * H_BYTES;
-constexpr int STAGE_BYTES = SPG * SPANF * 4;
+constexpr int STAGE_BYTES = SPG * 2 * SPANH * 2;  // [scan][hi | lo][SPANH] fp16
 constexpr int GQ_FLOAT4 = (SPG / 4) * 2 * 16;  // per stage: [quad][d = 0..15][e, x] float4
 constexpr int TMEM_COLS = 512;             // two M-blocks x N fp32 columns
 constexpr uint32_t LBO = 128, SBO = 256;   // core-matrix strides (bytes)
@@ -177,12 +177,13 @@ __device__ __forceinline__ int tile_points(const EnergyParams& p, int tile, int 
 }
 
 struct alignas(64) Params {
-  CUtensorMap tm_sig;   // 3-D {ld, C, S} fp32: box {SPANF, 1, SPG} = one channel's spans of a scan group
+  CUtensorMap tm_planes;  // 3-D {Lp, 2 C, S} fp16 (scaled hi | lo planes): box {SPANH, 2, SPG}
   CUtensorMap tm_gram;  // 3-D {8 J, C, quads} fp32 (interleaved {E, X} float4 pairs): box {128, 1, SPG / 4}
   EnergyParams e;
   const uint32_t* absmax;  // [n_scans] bits of max |y| per scan (over the samples any window touches)
 
   int j_lo, J;             // positions j = lo_c + d, j in [j_lo, j_lo + J)
+  int Lp;                  // plane length: samples k0 + j_lo + [0, Lp)
   int n_tiles;
   int n_groups;
 };
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
   const EnergyParams& p = P.e;
   const Layout L = layout();
   unsigned char* ops = smem + L.ops;
-  float* stage = reinterpret_cast<float*>(smem + L.stage);
+  unsigned char* stage_bytes = smem + L.stage;
   float* gstage = reinterpret_cast<float*>(smem + L.g);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
   uint64_t* s_full = bar;
@@ -247,11 +248,10 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
         // one tensor copy stages the group's spans (zeros past the record and
         // past the last scan), one more the two quads' Gram slices
         if (lane == 0) {
-          const int start4 = (p.k0 + lo_c) & ~3;
           const int off = min(max(lo_c - P.j_lo, 0), P.J - 16);  // in range by construction (j_lo, J from the table)
           if (off != lo_c - P.j_lo && p.flags) atomicOr(p.flags, 4);
           mbar_arrive_expect_tx(&s_full[slot], (uint32_t)(STAGE_BYTES + GQ_FLOAT4 * 16));
-          tma_load_3d(stage + slot * (STAGE_BYTES / 4), &P.tm_sig, start4, c, group * SPG, &s_full[slot]);
+          tma_load_3d(stage_bytes + slot * STAGE_BYTES, &P.tm_planes, off & ~7, 2 * c, group * SPG, &s_full[slot]);
           tma_load_3d(reinterpret_cast<float4*>(gstage) + slot * GQ_FLOAT4, &P.tm_gram, 8 * off, c,
                       group * (SPG / 4), &s_full[slot]);
         }
@@ -307,8 +307,6 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
       const int nsg = min(SPG, p.n_scans - group * SPG);
       const uint32_t* tw = p.tab_words + (size_t)tile * p.C * TILE;
       const int2* tsp = p.tab_span + (size_t)tile * p.C;
-      const int h_scan = group * SPG + w8;
-      const float h_scale = pow2f(h_scan < p.n_scans ? scale_exp(__ldg(P.absmax + h_scan)) : 0);
       float q[SPG];
 #pragma unroll
       for (int s = 0; s < SPG; ++s) q[s] = 0.f;
@@ -363,14 +361,27 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
         }
         // ---- Hankel rows and Gram entries of scan w8, once staged
         mbar_wait(&s_full[slot], (t / NS) & 1);
-        const float* ys = stage + slot * (STAGE_BYTES / 4) + w8 * SPANF + ((p.k0 + lo_c) & 3);
         {
-          float v[16];
-#pragma unroll
-          for (int m = 0; m < 16; ++m) v[m] = ys[lane + m] * h_scale;
+          // Hankel row k = lane of scan w8: taps m -> plane element o + m with
+          // o = (lo_c - j_lo) % 8 + k; 9 aligned words per plane, shifted by
+          // one half for odd o
+          const int off = min(max(lo_c - P.j_lo, 0), P.J - 16);
+          const int o = (off & 7) + lane;
+          const uint32_t* hw = reinterpret_cast<const uint32_t*>(stage_bytes + slot * STAGE_BYTES) +
+                               w8 * SPANH + (o >> 1);  // [scan][hi | lo][SPANH halves] = SPANH words per scan
+          const bool odd = o & 1;
           uint32_t hi[8], lo[8];
+          {
+            uint32_t u[9];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) split2(v[2 * j], v[2 * j + 1], hi[j], lo[j]);
+            for (int j = 0; j < 9; ++j) u[j] = hw[j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hi[j] = odd ? __funnelshift_r(u[j], u[j + 1], 16) : u[j];
+#pragma unroll
+            for (int j = 0; j < 9; ++j) u[j] = hw[SPANH / 2 + j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) lo[j] = odd ? __funnelshift_r(u[j], u[j + 1], 16) : u[j];
+          }
           const int n = w8 * W + lane;  // H row (s, k)
           unsigned char* hh = op + 2 * A_BYTES;
           unsigned char* hl = hh + H_BYTES;
@@ -470,11 +481,11 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
 // (bits; non-negative floats order like their bits), the input of the
 // per-scan power-of-two scale.
 __global__ void __launch_bounds__(128) gram_kernel(const float* sig, long long scan_stride, int n_scans, int C,
-                                                   int ld, int k0, int j_lo, int J, float4* gx, uint32_t* absmax) {
-  extern __shared__ float yq[];  // [4][R]
+                                                   int ld, int k0, int j_lo, int J, int R, float4* gx,
+                                                   uint32_t* absmax) {
+  extern __shared__ float yq[];  // [4][R], R >= J + W + 1: the planes' range (the |y| max covers it)
   __shared__ uint32_t wmax[4][4];
   const int c = blockIdx.x, quad = blockIdx.y, tid = threadIdx.x;
-  const int R = J + W + 1;
   const long long base = (long long)k0 + j_lo;
   uint32_t m[4];
 #pragma unroll
@@ -517,6 +528,26 @@ __global__ void __launch_bounds__(128) gram_kernel(const float* sig, long long s
     }
     gx[2 * (row_out + jj)] = make_float4(e[0], e[1], e[2], e[3]);
     gx[2 * (row_out + jj) + 1] = make_float4(x[0], x[1], x[2], x[3]);
+  }
+}
+
+// Scaled fp16 hi / lo planes of each (scan, channel) over the samples the
+// windows touch, k0 + j_lo + [0, Lp): v = y * 2^e_s (the scan's power-of-two
+// scale), hi = fp16(v), lo = fp16(v - hi); zeros past the record.  Layout
+// [S][C][hi | lo][Lp], the tensor-core kernel's staging source.
+__global__ void __launch_bounds__(128) planes_kernel(const float* sig, long long scan_stride, int C, int ld, int k0,
+                                                     int j_lo, int Lp, const uint32_t* absmax, __half* planes) {
+  const int c = blockIdx.x, s = blockIdx.y;
+  const float sc = pow2f(scale_exp(__ldg(absmax + s)));
+  const float* row = sig + (size_t)s * (size_t)scan_stride + (size_t)c * ld;
+  __half* hi = planes + ((size_t)s * C + c) * 2 * (size_t)Lp;
+  __half* lo = hi + Lp;
+  for (int i = threadIdx.x; i < Lp; i += blockDim.x) {
+    const long long idx = (long long)k0 + j_lo + i;
+    const float v = idx < ld ? __ldg(row + idx) * sc : 0.f;
+    const __half h = __float2half_rn(v);
+    hi[i] = h;
+    lo[i] = __float2half_rn(v - __half2float(h));
   }
 }
 
