@@ -17,25 +17,35 @@
 // So S is a [256 x 16] x [16 x (SPG * W)] product per channel, accumulated
 // over the channels in TMEM (fp32).  DAS = sum_k S^2 (beamform.py:211).
 // DMAS = 1/2 (sum_k S^2 - Q) (beamform.py:212) with
-//   Q[p, s] = sum_c sum_k a^2 = sum_c f0^2 e(d) + 2 f0 f1 x(d) + f1^2 e(d+1),
-// e(d) = sum_k y[d+k]^2 and x(d) = sum_k y[d+k] y[d+k+1] over the window
-// (windowed Gram entries of the staged samples, one warp prefix scan per
-// (channel, scan)), gathered per point on the CUDA cores.
+//   Q[p, s] = sum_c sum_k a^2 = sum_c f0^2 E(j) + 2 f0 f1 X(j) + f1^2 E(j+1),
+// j = lo_c + d, E(j) = sum_k y[k0+j+k]^2, X(j) = sum_k y[k0+j+k] y[k0+j+k+1]:
+// windowed Gram entries that depend on the absolute window start only, so a
+// pre-pass (gram_kernel) computes them once per (scan, channel, j) and every
+// tile gathers them per point on the CUDA cores.
 //
 // Precision: operands are split hi + lo in fp16 (y scaled per scan by a power
-// of two so |y| < 2^15), and S = A_hi H_hi + A_hi H_lo + A_lo H_hi (the
-// dropped A_lo H_lo term is ~2^-22 relative), i.e. about fp32 accuracy.
+// of two so |y| < 2^15; planes_kernel writes the scaled hi / lo planes), and
+// S = A_hi H_hi + A_hi H_lo + A_lo H_hi (the dropped A_lo H_lo term is ~2^-22
+// relative), i.e. about fp32 accuracy.
 //
-// Roles (8NG + 2 warps, one CTA per SM, persistent over (tile, group) items):
-//   warps 0..8NG-1 builders in NG groups of 8 taking interleaved channel steps:
-//              thread pt of a group owns point pt (its A row, Q); warp w8 of
-//              a group owns scan w8 (its 32 Hankel rows and Gram entries);
-//              group 0 also runs the TMEM epilogue
-//   warp 8NG   producer: TMA bulk copies of each channel's window spans
-//   warp 8NG+1 MMA issuer: one thread, 6 tcgen05.mma per channel
-// Rings: samples (NS deep, full/empty mbarriers), operands (NO deep, full by
-// the builders, empty by tcgen05.commit), accumulator (full by commit, empty
-// by the builders after the epilogue's tcgen05.ld).
+// Per launch: gram_kernel (Gram entries + per-scan max |y|), planes_kernel
+// (scaled fp16 planes of the sample range the windows touch), then
+// energy_tc_kernel.  Roles of energy_tc_kernel (8 NG + 2 warps, one CTA per
+// SM, persistent over (tile, group) items):
+//   warps 0..8NG-1  builders in NG groups of 8 taking interleaved channel
+//                   steps: thread pt of a group owns point pt (its A row and
+//                   Q partial), warp w8 owns scan w8 (its 32 Hankel rows,
+//                   read from the staged planes); at an item's end every
+//                   group publishes its Q partials and takes part in the
+//                   TMEM epilogue (scans s = g, g + NG, ...)
+//   warp 8NG        producer: per channel step one tensor-map TMA copy of the
+//                   group's planes and one of the two quads' Gram slices
+//   warp 8NG+1      MMA issuer: one thread, 6 tcgen05.mma per channel step
+// Rings: staging (NS deep, full by TMA complete_tx, empty by the builders),
+// operands (NO deep, full by the builders, empty by tcgen05.commit),
+// accumulator (full by commit, empty by the builders after the epilogue's
+// tcgen05.ld).  Measured alternatives (dedicated epilogue warps, A in TMEM,
+// deeper or shallower rings) are recorded in DESIGN.md.
 
 namespace tc {
 
