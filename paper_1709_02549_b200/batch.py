@@ -110,8 +110,8 @@ class BatchImager:
         self.table = build_table(self.scan, self.pts, self.n_pts, self.interp) if self.n_pts else None
 
     def _setup_padded(self, emask) -> tuple[bool, str]:
-        if self.w != self.TC_WINDOW:
-            return False, f"window {self.w} != {self.TC_WINDOW}"
+        if self.w not in self.TC_WINDOWS:
+            return False, f"window {self.w} not in {self.TC_WINDOWS}"
         self._enumerate(emask, padded=True)
         if not self.n_valid:
             self.table = None
@@ -132,11 +132,11 @@ class BatchImager:
             self.j_lo, self.j_count = lo_min, lo_max + 16 - lo_min
         return ok, why
 
-    TC_WINDOW, TC_MAX_SPAN = 32, 14
+    TC_WINDOWS, TC_MAX_SPAN = (32, 48), 14
 
     def tc_eligible(self) -> tuple[bool, str]:
-        if self.w != self.TC_WINDOW:
-            return False, f"window {self.w} != {self.TC_WINDOW}"
+        if self.w not in self.TC_WINDOWS:
+            return False, f"window {self.w} not in {self.TC_WINDOWS}"
         if not self.n_pts or self.table is None:
             return True, ""
         out = torch.zeros(1, dtype=torch.int32, device=dv.device())

@@ -1995,7 +1995,8 @@ static size_t tc_ws_absmax(int n_scans) { return align_up(sizeof(uint32_t) * (si
 static size_t tc_ws_gram(int n_scans, int n_chan, int j_count) {
   return 2 * sizeof(float4) * (size_t)((n_scans + 3) / 4) * (size_t)n_chan * (size_t)j_count;
 }
-static int tc_plane_len(int j_count) { return (j_count + 40 + 7) & ~7; }  // covers offset + 53, 16-B rows
+// plane length: the staged box [x0, x0 + SPANH) with x0 <= J - 16, 16-byte rows
+static int tc_plane_len(int j_count) { return (j_count - 16 + tc::SPANH_MAX + 7) & ~7; }
 static size_t tc_ws_planes(int n_scans, int n_chan, int j_count) {
   return sizeof(__half) * 2 * (size_t)n_scans * (size_t)n_chan * (size_t)tc_plane_len(j_count);
 }
@@ -2042,6 +2043,44 @@ int mwb_table_max_span(const void* table, int n_pts, int n_chan, int32_t* d_out,
   return check_launch("table_max_span_kernel");
 }
 
+// one configuration of the tensor-core kernel: tensor maps, smem, persistent grid
+extern "C++" {
+template <class C>
+static int launch_tc(const EnergyParams& e, int kind, int n_pts, int n_scans, int n_chan, int j_lo, int j_count,
+                     int Lp, const uint32_t* absmax, const float4* gx, const __half* planes, cudaStream_t st) {
+  int rc;
+  tc::Params P;
+  P.e = e;
+  P.absmax = absmax;
+  P.j_lo = j_lo;
+  P.J = j_count;
+  P.Lp = Lp;
+  P.n_tiles = (n_pts + TILE - 1) / TILE;
+  P.n_groups = (n_scans + C::SPG - 1) / C::SPG;
+  const int quads = (n_scans + 3) / 4;
+  if ((rc = encode_3d(&P.tm_planes, planes, (uint64_t)Lp, (uint64_t)2 * n_chan, (uint64_t)n_scans, (uint64_t)Lp * 2,
+                      (uint64_t)Lp * 2 * 2 * n_chan, C::SPANH, 2, C::SPG, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)))
+    return rc;
+  if ((rc = encode_3d(&P.tm_gram, gx, (uint64_t)8 * j_count, (uint64_t)n_chan, (uint64_t)quads,
+                      (uint64_t)32 * j_count, (uint64_t)32 * j_count * n_chan, 128, 1, C::QUADS,
+                      CU_TENSOR_MAP_DATA_TYPE_FLOAT32)))
+    return rc;
+  const tc::Layout L = tc::layout<C>();
+  void (*fn)(tc::Params) = kind == KIND_DAS    ? tc::energy_tc_kernel<KIND_DAS, C>
+                           : kind == KIND_DMAS ? tc::energy_tc_kernel<KIND_DMAS, C>
+                                               : tc::energy_tc_kernel<KIND_BOTH, C>;
+  cudaError_t ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  if (ce != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(ce));
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long items = (long long)P.n_tiles * P.n_groups;
+  const unsigned grid = (unsigned)std::min<long long>(items, sms > 0 ? sms : 148);
+  fn<<<grid, tc::THREADS, L.total, st>>>(P);
+  return check_launch("energy_tc_kernel");
+}
+}  // extern "C++"
+
 int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
                     const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale,
                     const double* pts_xyz, const int32_t* out_idx, int n_pts, const int32_t* d_count,
@@ -2054,7 +2093,8 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
                          pts_xyz, out_idx, n_pts, d_count, tile_info, table, interp, k0, window, out_das, out_dmas,
                          out_stride, key_das, key_dmas, flags, 0, e, empty);
   if (rc || empty) return rc;
-  if (window != tc::W) return set_err(MWB_EINVAL, "mwb_energies_tc: window must be %d (got %d)", tc::W, window);
+  if (window != 32 && window != 48)
+    return set_err(MWB_EINVAL, "mwb_energies_tc: window must be 32 or 48 (got %d)", window);
   if (!workspace) return set_err(MWB_EINVAL, "mwb_energies_tc: null workspace");
   if (j_lo < 0 || j_count < 16) return set_err(MWB_EINVAL, "mwb_energies_tc: bad window-offset range");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -2070,43 +2110,18 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
     const size_t sm = sizeof(float) * 4 * (size_t)Lp;
     if (sm > 48 * 1024) return set_err(MWB_ERANGE, "mwb_energies_tc: window-offset range %d too wide", j_count);
     tc::gram_kernel<<<dim3((unsigned)n_chan, (unsigned)((n_scans + 3) / 4)), 128, sm, st>>>(
-        sig, scan_stride, n_scans, n_chan, ld, k0, j_lo, j_count, Lp, gx, absmax);
+        sig, scan_stride, n_scans, n_chan, ld, k0, window, j_lo, j_count, Lp, gx, absmax);
     if ((rc = check_launch("gram_kernel"))) return rc;
     tc::planes_kernel<<<dim3((unsigned)n_chan, (unsigned)n_scans), 128, 0, st>>>(sig, scan_stride, n_chan, ld, k0,
                                                                                   j_lo, Lp, absmax, planes);
     if ((rc = check_launch("planes_kernel"))) return rc;
   }
-  tc::Params P;
-  P.e = e;
-  P.absmax = absmax;
-  P.j_lo = j_lo;
-  P.J = j_count;
-  const int quads = (n_scans + 3) / 4;
-  P.Lp = Lp;
-  if ((rc = encode_3d(&P.tm_planes, planes, (uint64_t)Lp, (uint64_t)2 * n_chan, (uint64_t)n_scans, (uint64_t)Lp * 2,
-                      (uint64_t)Lp * 2 * 2 * n_chan, tc::SPANH, 2, tc::SPG, CU_TENSOR_MAP_DATA_TYPE_FLOAT16)))
-    return rc;
-  if ((rc = encode_3d(&P.tm_gram, gx, (uint64_t)8 * j_count, (uint64_t)n_chan, (uint64_t)quads,
-                      (uint64_t)32 * j_count, (uint64_t)32 * j_count * n_chan, 128, 1, tc::SPG / 4,
-                      CU_TENSOR_MAP_DATA_TYPE_FLOAT32)))
-    return rc;
-  P.n_tiles = (n_pts + TILE - 1) / TILE;
-  P.n_groups = (n_scans + tc::SPG - 1) / tc::SPG;
-  const tc::Layout L = tc::layout();
   const int kind = out_das && out_dmas ? KIND_BOTH : (out_das ? KIND_DAS : KIND_DMAS);
-  void (*fn)(tc::Params) = kind == KIND_DAS    ? tc::energy_tc_kernel<KIND_DAS>
-                           : kind == KIND_DMAS ? tc::energy_tc_kernel<KIND_DMAS>
-                                               : tc::energy_tc_kernel<KIND_BOTH>;
-  ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-  if (ce != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(ce));
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long items = (long long)P.n_tiles * P.n_groups;
-  const unsigned grid = (unsigned)std::min<long long>(items, sms > 0 ? sms : 148);
-  fn<<<grid, tc::THREADS, L.total, st>>>(P);
-  return check_launch("energy_tc_kernel");
+  if (window == 32) return launch_tc<tc::Cfg32x8>(e, kind, n_pts, n_scans, n_chan, j_lo, j_count, Lp, absmax, gx, planes, st);
+  if (n_scans >= 4) return launch_tc<tc::Cfg48x4>(e, kind, n_pts, n_scans, n_chan, j_lo, j_count, Lp, absmax, gx, planes, st);
+  return launch_tc<tc::Cfg48x1>(e, kind, n_pts, n_scans, n_chan, j_lo, j_count, Lp, absmax, gx, planes, st);
 }
+
 
 static long long lattice_tiles(int nx, int ny, int nz, int stride, int tx, int ty, int tz) {
   const long long Lx = (nx + stride - 1) / stride, Ly = (ny + stride - 1) / stride,

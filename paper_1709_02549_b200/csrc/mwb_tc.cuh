@@ -49,13 +49,8 @@
 
 namespace tc {
 
-constexpr int W = 32;                      // window samples (this build)
-constexpr int SPG = 8;                     // scans per group
-constexpr int N = SPG * W;                 // MMA N: 256
-static_assert(SPG % 4 == 0, "Gram entries are interleaved by 4 scans");
 constexpr int K = 16;                      // taps per channel: d + 1 <= K - 1
-constexpr int SPANH = 56;                  // staged halves per (scan, channel, plane): 7 + W + K, rounded to 8
-constexpr int NS = 16;                     // sample ring depth
+constexpr int NS = 16;                     // staging ring depth
 constexpr int NO = 4;                      // operand ring depth
 #ifndef MWB_TC_GROUPS
 #define MWB_TC_GROUPS 3
@@ -67,25 +62,49 @@ constexpr int NBT = NBW * 32;              // builder threads
 constexpr int THREADS = NBT + 64;          // + producer warp + MMA warp
 constexpr int A_BYTES = TILE * K * 2;      // one of hi/lo, both M-blocks: 8 KB
 constexpr int MB_BYTES = 128 * K * 2;      // one M-block: 4 KB
-constexpr int H_BYTES = N * K * 2;         // 8 KB
-constexpr int OP_BYTES = 2 * A_BYTES + 2 * H_BYTES;
-constexpr int STAGE_BYTES = SPG * 2 * SPANH * 2;  // [scan][hi | lo][SPANH] fp16
-constexpr int GQ_FLOAT4 = (SPG / 4) * 2 * 16;  // per stage: [quad][d = 0..15][e, x] float4
-constexpr int TMEM_COLS = 512;             // two M-blocks x N fp32 columns
 constexpr uint32_t LBO = 128, SBO = 256;   // core-matrix strides (bytes)
 constexpr size_t SMEM_MIN = 120 * 1024;    // > half the SM: one CTA per SM (TMEM is sized for one)
+constexpr int SPANH_MAX = 72;              // largest staged span (W = 48): the planes' length uses it
+
+// Window W and scans per group SPG: everything the kernel derives from them.
+template <int WIN, int SPG_>
+struct Cfg {
+  static constexpr int W = WIN;
+  static constexpr int SPG = SPG_;
+  static constexpr int N = W * SPG;                       // MMA N (scans x window samples)
+  static constexpr int QUADS = (SPG + 3) / 4;             // Gram entries interleave 4 scans per float4
+  static constexpr int SPANH = (W + 22 + 7) & ~7;         // staged halves per (scan, plane): (off & 7) + W + K - 1 + 1
+  static constexpr int H_BYTES = N * K * 2;               // one of hi/lo
+  static constexpr int OP_BYTES = 2 * A_BYTES + 2 * H_BYTES;
+  static constexpr int STAGE_BYTES = (SPG * 2 * SPANH * 2 + 127) & ~127;  // [scan][hi | lo][SPANH] fp16; TMA
+                                                                          // destinations are 128-byte aligned
+  static constexpr int GQ_FLOAT4 = QUADS * 2 * 16;        // per stage: [quad][d = 0..15][e, x] float4
+  static constexpr int D_COLS = 2 * N;                    // two M-blocks x N fp32 accumulator columns
+  static constexpr int TMEM_COLS = D_COLS <= 32 ? 32 : D_COLS <= 64 ? 64 : D_COLS <= 128 ? 128
+                                   : D_COLS <= 256 ? 256 : 512;
+  // kind::f16 instruction descriptor: f16 x f16 -> f32, both K-major, M = 128
+  static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  static_assert(W % 16 == 0 && N % 16 == 0 && N <= 256 && D_COLS <= 512, "tcgen05 shape");
+  static_assert(SPG % 4 == 0 || 4 % SPG == 0, "a group tiles the 4-scan Gram quads");
+  static_assert(SPANH <= SPANH_MAX, "plane length");
+  static_assert(OP_BYTES % 128 == 0 && (GQ_FLOAT4 * 16) % 128 == 0, "128-byte aligned ring slots");
+};
+using Cfg32x8 = Cfg<32, 8>;  // configs[3]: 8 scans x W = 32 (N = 256)
+using Cfg48x4 = Cfg<48, 4>;  // W = 48 batches (N = 192)
+using Cfg48x1 = Cfg<48, 1>;  // configs[4]: one scan, W = 48 (N = 48)
 
 struct Layout {
   size_t ops, stage, g, qx, bar, tmem, total;
 };
 
+template <class C>
 __host__ __device__ inline Layout layout() {
   Layout L;
   size_t o = 0;
-  L.ops = o;   o += (size_t)NO * OP_BYTES;
-  L.stage = o; o += (size_t)NS * STAGE_BYTES;
-  L.g = o;     o += (size_t)NS * GQ_FLOAT4 * sizeof(float4);  // staged Gram slices, one per sample stage
-  L.qx = o;    o += NG * (size_t)SPG * TILE * sizeof(float);  // every group's Q partial sums
+  L.ops = o;   o += (size_t)NO * C::OP_BYTES;
+  L.stage = o; o += (size_t)NS * C::STAGE_BYTES;
+  L.g = o;     o += (size_t)NS * C::GQ_FLOAT4 * sizeof(float4);  // staged Gram slices, one per sample stage
+  L.qx = o;    o += NG * (size_t)C::SPG * TILE * sizeof(float);  // every group's Q partial sums
   o = align_up(o, 8);
   L.bar = o;   o += sizeof(uint64_t) * (2 * NS + 2 * NO + 2);
   L.tmem = o;  o += 16;
@@ -104,14 +123,11 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
          ((uint64_t)((SBO >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);  // version 1, no swizzle
 }
 
-// kind::f16 instruction descriptor: f16 x f16 -> f32, both K-major
-constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-
-__device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+__device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
@@ -152,6 +168,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16 consecutive fp32 TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // hi/lo fp16 split of two values, packed as half2 words
 __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(a, b);
@@ -188,7 +218,7 @@ __device__ __forceinline__ int tile_points(const EnergyParams& p, int tile, int 
 
 struct alignas(64) Params {
   CUtensorMap tm_planes;  // 3-D {Lp, 2 C, S} fp16 (scaled hi | lo planes): box {SPANH, 2, SPG}
-  CUtensorMap tm_gram;  // 3-D {8 J, C, quads} fp32 (interleaved {E, X} float4 pairs): box {128, 1, SPG / 4}
+  CUtensorMap tm_gram;    // 3-D {8 J, C, quads} fp32 (interleaved {E, X} float4 pairs): box {128, 1, QUADS}
   EnergyParams e;
   const uint32_t* absmax;  // [n_scans] bits of max |y| per scan (over the samples any window touches)
 
@@ -198,11 +228,15 @@ struct alignas(64) Params {
   int n_groups;
 };
 
-template <int KIND>
+template <int KIND, class C>
 __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_constant__ Params P) {
+  constexpr int W = C::W, SPG = C::SPG, N = C::N, QUADS = C::QUADS, SPANH = C::SPANH;
+  constexpr int H_BYTES = C::H_BYTES, OP_BYTES = C::OP_BYTES, STAGE_BYTES = C::STAGE_BYTES;
+  constexpr int GQ_FLOAT4 = C::GQ_FLOAT4, TMEM_COLS = C::TMEM_COLS;
+  constexpr uint32_t IDESC = C::IDESC;
   extern __shared__ __align__(1024) unsigned char smem[];
   const EnergyParams& p = P.e;
-  const Layout L = layout();
+  const Layout L = layout<C>();
   unsigned char* ops = smem + L.ops;
   unsigned char* stage_bytes = smem + L.stage;
   float* gstage = reinterpret_cast<float*>(smem + L.g);
@@ -260,10 +294,11 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
         if (lane == 0) {
           const int off = min(max(lo_c - P.j_lo, 0), P.J - 16);  // in range by construction (j_lo, J from the table)
           if (off != lo_c - P.j_lo && p.flags) atomicOr(p.flags, 4);
-          mbar_arrive_expect_tx(&s_full[slot], (uint32_t)(STAGE_BYTES + GQ_FLOAT4 * 16));
+          mbar_arrive_expect_tx(&s_full[slot], (uint32_t)(SPG * 2 * SPANH * 2 + GQ_FLOAT4 * 16));
           tma_load_3d(stage_bytes + slot * STAGE_BYTES, &P.tm_planes, off & ~7, 2 * c, group * SPG, &s_full[slot]);
+          // Gram quads hold scans 4q .. 4q + 3: the group's first scan's quad
           tma_load_3d(reinterpret_cast<float4*>(gstage) + slot * GQ_FLOAT4, &P.tm_gram, 8 * off, c,
-                      group * (SPG / 4), &s_full[slot]);
+                      (group * SPG) / 4, &s_full[slot]);
         }
         __syncwarp();
       }
@@ -287,9 +322,9 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
           for (int mb = 0; mb < 2; ++mb) {
             const uint64_t a_hi = smem_desc(base + mb * MB_BYTES), a_lo = smem_desc(base + A_BYTES + mb * MB_BYTES);
             const uint32_t d = tmem + (uint32_t)(mb * N);
-            mma(d, a_hi, b_hi, c > 0 ? 1u : 0u);
-            mma(d, a_hi, b_lo, 1u);
-            mma(d, a_lo, b_hi, 1u);
+            mma(d, a_hi, b_hi, IDESC, c > 0 ? 1u : 0u);
+            mma(d, a_hi, b_lo, IDESC, 1u);
+            mma(d, a_lo, b_hi, IDESC, 1u);
           }
           commit(&o_empty[slot]);
         }
@@ -317,7 +352,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
       const int nsg = min(SPG, p.n_scans - group * SPG);
       const uint32_t* tw = p.tab_words + (size_t)tile * p.C * TILE;
       const int2* tsp = p.tab_span + (size_t)tile * p.C;
-      float q[SPG];
+      float q[SPG < 4 ? 4 : SPG];
 #pragma unroll
       for (int s = 0; s < SPG; ++s) q[s] = 0.f;
       bool bad = false, bad_span = false;
@@ -371,14 +406,16 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
         }
         // ---- Hankel rows and Gram entries of scan w8, once staged
         mbar_wait(&s_full[slot], (t / NS) & 1);
-        {
-          // Hankel row k = lane of scan w8: taps m -> plane element o + m with
+        const int n_row = w8 * 32 + lane;  // H row (s, k) = (n / W, n % W)
+        if (w8 * 32 < N && n_row < N) {
+          // Hankel row k of scan s: taps m -> plane element o + m with
           // o = (lo_c - j_lo) % 8 + k; 9 aligned words per plane, shifted by
           // one half for odd o
+          const int hs = n_row / W, k = n_row - hs * W;
           const int off = min(max(lo_c - P.j_lo, 0), P.J - 16);
-          const int o = (off & 7) + lane;
+          const int o = (off & 7) + k;
           const uint32_t* hw = reinterpret_cast<const uint32_t*>(stage_bytes + slot * STAGE_BYTES) +
-                               w8 * SPANH + (o >> 1);  // [scan][hi | lo][SPANH halves] = SPANH words per scan
+                               hs * SPANH + (o >> 1);  // [scan][hi | lo][SPANH halves] = SPANH words per scan
           const bool odd = o & 1;
           uint32_t hi[8], lo[8];
           {
@@ -392,13 +429,12 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
 #pragma unroll
             for (int j = 0; j < 8; ++j) lo[j] = odd ? __funnelshift_r(u[j], u[j + 1], 16) : u[j];
           }
-          const int n = w8 * W + lane;  // H row (s, k)
           unsigned char* hh = op + 2 * A_BYTES;
           unsigned char* hl = hh + H_BYTES;
-          *reinterpret_cast<uint4*>(hh + kmajor_off(n, 0)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<uint4*>(hh + kmajor_off(n, 1)) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
-          *reinterpret_cast<uint4*>(hl + kmajor_off(n, 0)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-          *reinterpret_cast<uint4*>(hl + kmajor_off(n, 1)) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+          *reinterpret_cast<uint4*>(hh + kmajor_off(n_row, 0)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(hh + kmajor_off(n_row, 1)) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+          *reinterpret_cast<uint4*>(hl + kmajor_off(n_row, 0)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          *reinterpret_cast<uint4*>(hl + kmajor_off(n_row, 1)) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
         }
         fence_async_smem();  // A / H generic writes -> visible to the tensor core
         __syncwarp();
@@ -407,13 +443,26 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
           // Q += f0^2 e(d) + 2 f0 f1 x(d) + f1^2 e(d + 1), 4 scans per LDS.128
           const float w0 = f0 * f0, w1 = 2.f * f0 * f1, w2 = f1 * f1;
           const float4* gsl = reinterpret_cast<const float4*>(gstage) + slot * GQ_FLOAT4;
+          if constexpr (SPG < 4) {
+            // groups smaller than a quad: this group's scans start at component (group * SPG) % 4
+            const int comp0 = (group * SPG) & 3;
+            const float4 E = gsl[2 * d], X = gsl[2 * d + 1], E1 = gsl[2 * d + 2];
 #pragma unroll
-          for (int qd = 0; qd < SPG / 4; ++qd) {
+            for (int s = 0; s < SPG; ++s) {
+              const int cp = comp0 + s;
+              const float e = cp == 0 ? E.x : cp == 1 ? E.y : cp == 2 ? E.z : E.w;
+              const float x = cp == 0 ? X.x : cp == 1 ? X.y : cp == 2 ? X.z : X.w;
+              const float e1 = cp == 0 ? E1.x : cp == 1 ? E1.y : cp == 2 ? E1.z : E1.w;
+              q[s] = fmaf(w0, e, fmaf(w1, x, fmaf(w2, e1, q[s])));
+            }
+          } else
+#pragma unroll
+          for (int qd = 0; qd < QUADS; ++qd) {
             const float4 E = gsl[qd * 32 + 2 * d], X = gsl[qd * 32 + 2 * d + 1], E1 = gsl[qd * 32 + 2 * d + 2];
-            q[4 * qd + 0] = fmaf(w0, E.x, fmaf(w1, X.x, fmaf(w2, E1.x, q[4 * qd + 0])));
-            q[4 * qd + 1] = fmaf(w0, E.y, fmaf(w1, X.y, fmaf(w2, E1.y, q[4 * qd + 1])));
-            q[4 * qd + 2] = fmaf(w0, E.z, fmaf(w1, X.z, fmaf(w2, E1.z, q[4 * qd + 2])));
-            q[4 * qd + 3] = fmaf(w0, E.w, fmaf(w1, X.w, fmaf(w2, E1.w, q[4 * qd + 3])));
+            if (4 * qd + 0 < SPG) q[4 * qd + 0] = fmaf(w0, E.x, fmaf(w1, X.x, fmaf(w2, E1.x, q[4 * qd + 0])));
+            if (4 * qd + 1 < SPG) q[4 * qd + 1] = fmaf(w0, E.y, fmaf(w1, X.y, fmaf(w2, E1.y, q[4 * qd + 1])));
+            if (4 * qd + 2 < SPG) q[4 * qd + 2] = fmaf(w0, E.z, fmaf(w1, X.z, fmaf(w2, E1.z, q[4 * qd + 2])));
+            if (4 * qd + 3 < SPG) q[4 * qd + 3] = fmaf(w0, E.w, fmaf(w1, X.w, fmaf(w2, E1.w, q[4 * qd + 3])));
           }
         }
         __syncwarp();
@@ -437,13 +486,16 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
         float qs = 0.f;
 #pragma unroll
         for (int g2 = 0; g2 < NG; ++g2) qs += qx[(g2 * SPG + s) * TILE + pt];
-        float v[32];
-        tmem_ld32(tmem + lane_base + (uint32_t)(mb * N + s * W), v);
         float e0 = 0.f, e1 = 0.f;
 #pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          e0 = fmaf(v[k], v[k], e0);
-          e1 = fmaf(v[k + 1], v[k + 1], e1);
+        for (int kc = 0; kc < W; kc += 16) {
+          float v[16];
+          tmem_ld16(tmem + lane_base + (uint32_t)(mb * N + s * W + kc), v);
+#pragma unroll
+          for (int k = 0; k < 16; k += 2) {
+            e0 = fmaf(v[k], v[k], e0);
+            e1 = fmaf(v[k + 1], v[k + 1], e1);
+          }
         }
         const int scan = group * SPG + s;
         const float inv = pow2f(-scale_exp(__ldg(P.absmax + scan)));
@@ -491,9 +543,9 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
 // (bits; non-negative floats order like their bits), the input of the
 // per-scan power-of-two scale.
 __global__ void __launch_bounds__(128) gram_kernel(const float* sig, long long scan_stride, int n_scans, int C,
-                                                   int ld, int k0, int j_lo, int J, int R, float4* gx,
+                                                   int ld, int k0, int win, int j_lo, int J, int R, float4* gx,
                                                    uint32_t* absmax) {
-  extern __shared__ float yq[];  // [4][R], R >= J + W + 1: the planes' range (the |y| max covers it)
+  extern __shared__ float yq[];  // [4][R], R >= J + win + 1: the planes' range (the |y| max covers it)
   __shared__ uint32_t wmax[4][4];
   const int c = blockIdx.x, quad = blockIdx.y, tid = threadIdx.x;
   const long long base = (long long)k0 + j_lo;
@@ -529,7 +581,7 @@ __global__ void __launch_bounds__(128) gram_kernel(const float* sig, long long s
       const float* y = yq + sq * R + jj;
       float a = 0.f, b = 0.f;
 #pragma unroll 8
-      for (int k = 0; k < W; ++k) {
+      for (int k = 0; k < win; ++k) {
         a = fmaf(y[k], y[k], a);
         b = fmaf(y[k], y[k + 1], b);
       }

@@ -147,7 +147,7 @@ def test_tc_eligibility():
     assert not auto.uses_tensor_cores
     fine = synth.grid_square(0.03, 64)
     with pytest.raises(ValueError, match="window"):
-        BatchImager(model.geometry(), model.pairs(), model.n_samples, fine, window=(model.k0, 48), mode="tc")
+        BatchImager(model.geometry(), model.pairs(), model.n_samples, fine, window=(model.k0, 40), mode="tc")
 
 
 def test_tc_nearest_interpolation(setup):
@@ -185,3 +185,21 @@ def test_tc_window_past_record_end():
         assert np.abs(want_long[k] - want[k]).max() > 1e-3 * np.abs(want_long[k]).max()
         for s in range(8):
             assert peak_err(got[k][s], want[k][s]) <= TOL_FP32
+
+
+@pytest.mark.parametrize("n_scans", [1, 3, 9])
+def test_tc_window_48(setup, n_scans):
+    """W = 48 (configs[4]'s window): 4-scan groups (N = 192) for batches, one
+    scan per group (N = 48) below 4 scans."""
+    model, sig, grid, _, _ = setup
+    win = (model.k0, 48)
+    tc = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win, mode="tc")
+    ref = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=win)
+    sig_d = tc.to_device_layout(sig[:n_scans])
+    got, gk, flags = run(tc, sig_d)
+    want, wk, _ = run(ref, sig_d)
+    assert flags == 0
+    for k in ("das", "dmas"):
+        for s in range(n_scans):
+            assert peak_err(got[k][s], want[k][s]) <= TOL_FP32
+            assert tuple(gk[k][s]) == tuple(wk[k][s])
