@@ -107,3 +107,41 @@ def test_sass_is_sm100a():
     assert "sm_100a" in out
     assert "FFMA2" in out
     assert "UBLKCP" in out
+
+
+def tc_args(**kw):
+    """Positional argument list of mwb_energies_tc (include/mwb.h) with overrides;
+    fake non-null pointers pass the null checks (nothing is dereferenced before
+    the argument errors tested here)."""
+    names = ["sig", "n_scans", "scan_stride", "n_chan", "ld", "n_samples", "chan", "ant", "n_ant", "inv_scale",
+             "pts", "out_idx", "n_pts", "d_count", "tile_info", "table", "interp", "k0", "window", "out_das",
+             "out_dmas", "out_stride", "key_das", "key_dmas", "flags", "j_lo", "j_count", "workspace", "stream"]
+    base = dict(sig=256, n_scans=8, scan_stride=4096, n_chan=66, ld=1024, n_samples=1024, chan=256, ant=256,
+                n_ant=12, inv_scale=500.0, pts=256, out_idx=None, n_pts=256, d_count=None, tile_info=None,
+                table=256, interp=0, k0=8, window=32, out_das=256, out_dmas=None, out_stride=0, key_das=None,
+                key_dmas=None, flags=None, j_lo=10, j_count=64, workspace=256, stream=None)
+    base.update(kw)
+    assert len(names) == len(_native._SIGNATURES["mwb_energies_tc"][0])
+    return [base[n] for n in names]
+
+
+def test_tensor_core_entry_argument_errors(lib):
+    assert lib.mwb_energies_tc(*tc_args(window=40)) == -1
+    assert b"window must be 32 or 48" in lib.mwb_last_error()
+    assert lib.mwb_energies_tc(*tc_args(workspace=None)) == -1
+    assert b"workspace" in lib.mwb_last_error()
+    assert lib.mwb_energies_tc(*tc_args(j_count=8)) == -1
+    assert b"window-offset range" in lib.mwb_last_error()
+    assert lib.mwb_energies_tc(*tc_args(out_das=None)) == -1
+    assert b"no output" in lib.mwb_last_error()
+    assert lib.mwb_energies_tc(*tc_args(n_pts=0)) == 0  # nothing to do
+    assert lib.mwb_energies_tc_workspace_bytes(8, 66, 8) == -1
+    small = lib.mwb_energies_tc_workspace_bytes(8, 66, 64)
+    assert small >= 2 * 16 * 2 * 66 * 64 and lib.mwb_energies_tc_workspace_bytes(4096, 66, 152) > 4096 * 66 * 152 * 8
+    assert lib.mwb_table_max_span(None, 10, 66, None, None) == -1
+    assert lib.mwb_table_lo_range(None, 10, 66, None, None, None) == -1
+    assert lib.mwb_lattice_tile_count(256, 256, 1) == 256
+    assert lib.mwb_lattice_tile_count(100, 100, 1) == 49
+    assert lib.mwb_enumerate_lattice_padded(0.0, 0.0, 1.0, 10, 10, 0, 0, 10, 9, 1, None, 0, None, None, None, None,
+                                            None, None, None) == -1
+    assert b"outside" in lib.mwb_last_error()
