@@ -380,8 +380,9 @@ def tc_roofline(S, slots, C, avg, traffic):
                     "window per channel x 3 split products x 2 M-blocks",
         "peak_source": source,
         "launch_ms": avg,
-        "note": "launch_ms brackets the whole mwb_energies_tc call (a 0.2 ms per-scan |y| max pre-pass and the "
-                "tensor-core kernel); shared memory (operand writes + tensor-core operand reads) is the co-bound",
+        "note": "launch_ms brackets the whole mwb_energies_tc call: the windowed-Gram / per-scan |y| max pre-pass "
+                "(~0.29 ms), the fp16-plane pre-pass (~0.17 ms) and the tensor-core kernel; FLOPs count only the "
+                "kernel's MMAs",
     }
 
 
@@ -505,7 +506,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "other_configs": others,
-            "gpu_launches": args.steps * (2 if bi.uses_tensor_cores else 1),
+            "gpu_launches": args.steps * (3 if bi.uses_tensor_cores else 1),  # TC: gram, planes, energy kernels
             "tensor_cores": bi.uses_tensor_cores,
             "clocks": clk,
             "kernel_mode": args.mode,
