@@ -376,6 +376,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
         }
         const float f1 = weight_f1(w);
         const float f0 = 1.0f - f1;
+        MWB_CHECK(d >= 0 && d + 1 < K);
         // ---- A row (weights), once the MMA released this operand slot
         if (t >= NO) mbar_wait(&o_empty[oslot], (t / NO - 1) & 1);
         unsigned char* op = ops + (size_t)oslot * OP_BYTES;
@@ -417,6 +418,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
           const uint32_t* hw = reinterpret_cast<const uint32_t*>(stage_bytes + slot * STAGE_BYTES) +
                                hs * SPANH + (o >> 1);  // [scan][hi | lo][SPANH halves] = SPANH words per scan
           const bool odd = o & 1;
+          MWB_CHECK(hs < SPG && (o >> 1) + 8 < SPANH / 2 && off + 16 <= P.J);  // 9 words inside each plane
           uint32_t hi[8], lo[8];
           {
             uint32_t u[9];
@@ -443,6 +445,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
           // Q += f0^2 e(d) + 2 f0 f1 x(d) + f1^2 e(d + 1), 4 scans per LDS.128
           const float w0 = f0 * f0, w1 = 2.f * f0 * f1, w2 = f1 * f1;
           const float4* gsl = reinterpret_cast<const float4*>(gstage) + slot * GQ_FLOAT4;
+          MWB_CHECK(d >= 0 && d <= K - 2 && (QUADS - 1) * 32 + 2 * d + 2 < GQ_FLOAT4);
           if constexpr (SPG < 4) {
             // groups smaller than a quad: this group's scans start at component (group * SPG) % 4
             const int comp0 = (group * SPG) & 3;
