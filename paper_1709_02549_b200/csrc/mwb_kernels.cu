@@ -38,6 +38,10 @@ namespace {
 
 constexpr int TPB = 128;          // threads per energy CTA
 constexpr int TILE = 2 * TPB;     // focal points per CTA
+#ifndef MWB_W48_MINB
+#define MWB_W48_MINB 3  // CTAs per SM of the W = 48 kernel: 3 (<= 168 registers, one channel in flight) beat 2
+                        // (255 registers, two channels): 7.9 vs 8.4 ms on the configs[4] volume
+#endif
 #ifndef MWB_W48_CH
 #define MWB_W48_CH 48  // register chunk for W % 48 == 0 windows (experiment knob: 24)
 #endif
@@ -462,7 +466,10 @@ __device__ __forceinline__ void channel_loop(float2 (&sacc)[CH], float2& qe, flo
     wb2 = __ldg(wp + TILE + lb);
   }
 #endif
-#pragma unroll kChannelUnroll
+  // two channels in flight for 32-sample chunks; one for 48 (keeps the W = 48
+  // kernel within the 168 registers of 3 CTAs per SM)
+  constexpr int kUnroll = CH == 48 ? 1 : kChannelUnroll;
+#pragma unroll kUnroll
   for (int c = c_begin; c < c_end; ++c) {
     const uint32_t ca = wa, cw = wb;
     wp += TILE;
@@ -1886,7 +1893,7 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   // register chunk: 48 samples for windows that are a multiple of 48 (the
   // configs[4] W = 48 would waste a third of a 2 x 32 split), else 32
   const int ch = (window % 48 == 0 && window % 32 != 0) ? MWB_W48_CH : 32;
-  const int resident = ch == 48 ? 2 : 3;  // CTAs per SM the register budget allows
+  const int resident = ch == 48 ? MWB_W48_MINB : 3;  // CTAs per SM the register budget allows
   // stage capacity: every channel's span for a compact tile, capped at 32 KB
   // and at what leaves `resident` CTAs room in the SM's 228 KB
   long long cap = (long long)n_chan * (ch + 24);
@@ -1913,8 +1920,8 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   }();
   void (*fn)(EnergyParams);
   if (ch == 48)
-    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 2, 48>
-         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 2, 48> : energy_kernel<KIND_BOTH, 2, 48>);
+    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, MWB_W48_MINB, 48>
+         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, MWB_W48_MINB, 48> : energy_kernel<KIND_BOTH, MWB_W48_MINB, 48>);
 #if MWB_W48_CH == 24
   else if (ch == 24)
     fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 3, 24>
