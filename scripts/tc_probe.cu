@@ -228,6 +228,70 @@ __global__ void mma_rate(int iters, long long* cycles) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// 2-CTA (cta_group::2) product D[256 x N] = A[256 x 16] * B[N x 16]^T: CTA r
+// holds A rows 128 r .. 128 r + 127 and B rows (N / 2) r .. (N / 2)(r + 1) - 1
+// at the same shared-memory offsets; the leader issues the MMA; each CTA's
+// TMEM receives its 128 rows of D.
+template <int N>
+__global__ void __cluster_dims__(2, 1, 1) probe_2sm(const __half* a, const __half* b, float* d) {
+  __shared__ __align__(1024) unsigned char sa[128 * K * 2];
+  __shared__ __align__(1024) unsigned char sb[(N / 2) * K * 2];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tbase;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 128 * K; i += blockDim.x)
+    *reinterpret_cast<__half*>(sa + kmajor_off(i / K, i % K)) = a[(rank * 128 + i / K) * K + i % K];
+  for (int i = tid; i < (N / 2) * K; i += blockDim.x)
+    *reinterpret_cast<__half*>(sb + kmajor_off(i / K, i % K)) = b[(rank * (N / 2) + i / K) * K + i % K];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tbase;
+  if (rank == 0 && tid == 0) {
+    const uint64_t da = smem_desc(sa, 128, 256), db = smem_desc(sb, 128, 256);
+    const uint32_t id = idesc_f16(256, N);
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(id), "r"(0));
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(&bar)), "h"((unsigned short)3));
+  }
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT4:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT4;\n}\n" ::"r"(
+          smem_u32(&bar)), "r"(0) : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  {
+    const int row = warp * 32 + (tid & 31);
+    for (int c = 0; c < N; c += 8) {
+      uint32_t v[8];
+      const uint32_t addr = tmem + ((uint32_t)(warp * 32) << 16) + c;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                     "=r"(v[7])
+                   : "r"(addr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int j = 0; j < 8; ++j) d[(rank * 128 + row) * N + c + j] = __uint_as_float(v[j]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
 int main() {
   constexpr int N = 256;
   std::vector<__half> ha(M * K), hb(N * K);
@@ -272,6 +336,29 @@ int main() {
       if (err > 1e-3 && bad2++ < 5) printf("bad2 (%d,%d): got %f want %f\n", i, j, hd[i * N2 + j], s);
     }
   printf("tmem-A: max abs err %g, bad %d of %d\n", maxerr2, bad2, M * N2);
+  {  // 2-CTA pair
+    constexpr int N3 = 256;
+    std::vector<__half> ha3(256 * K); std::vector<float> fa3(256 * K);
+    for (int i = 0; i < 256 * K; ++i) { fa3[i] = (float)((rand() % 15) - 7) / 4.0f; ha3[i] = __float2half(fa3[i]); }
+    __half* da3; float* dd3; cudaMalloc(&da3, 256 * K * 2); cudaMalloc(&dd3, 256 * N3 * 4);
+    cudaMemcpy(da3, ha3.data(), 256 * K * 2, cudaMemcpyHostToDevice);
+    cudaMemset(dd3, 0xFF, 256 * N3 * 4);
+    probe_2sm<N3><<<2, 128>>>(da3, db, dd3);
+    e = cudaDeviceSynchronize();
+    printf("2sm launch: %s\n", cudaGetErrorString(e));
+    std::vector<float> hd3(256 * N3);
+    cudaMemcpy(hd3.data(), dd3, 256 * N3 * 4, cudaMemcpyDeviceToHost);
+    double me = 0; int b3 = 0;
+    for (int i = 0; i < 256; ++i)
+      for (int j = 0; j < N3; ++j) {
+        double sacc = 0;
+        for (int k = 0; k < K; ++k) sacc += (double)fa3[i * K + k] * fb[j * K + k];
+        const double err = fabs(sacc - hd3[i * N3 + j]);
+        if (err > me) me = err;
+        if (err > 1e-3 && b3++ < 5) printf("bad3 (%d,%d): got %f want %f\n", i, j, hd3[i * N3 + j], sacc);
+      }
+    printf("2sm: max abs err %g, bad %d of %d\n", me, b3, 256 * N3);
+  }
   long long* dcyc; cudaMalloc(&dcyc, 8);
   for (int iters : {1000, 4000}) {
     mma_rate<256><<<1, 128>>>(iters, dcyc);
