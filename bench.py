@@ -462,6 +462,12 @@ def run_ours(args):
     traffic = load_traffic()
     if bi.uses_tensor_cores:
         roofline = tc_roofline(S, bi.n_pts, C, avg, traffic)
+        # useful work against the CUDA-core formulation's co-roofline (32 pps/clk/SM)
+        pps_s = pps_launch / (avg * 1e-3)
+        core_peak = smem_gbs * 1e9 / 4.0
+        roofline["useful_pps_per_s"] = pps_s
+        roofline["vs_cuda_core_roofline"] = pps_s / core_peak
+        roofline["cuda_core_roofline_pps_per_s"] = core_peak
     else:
         roofline = smem_roofline(pps_launch, avg, smem_gbs, fp32_tf, traffic)
 
