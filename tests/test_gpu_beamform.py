@@ -349,3 +349,39 @@ class TestGoldenPoints:
                 want = np.array(case[kind])
                 scale = max(np.abs(want).max(), 1.0)
                 assert np.abs(got - want).max() <= 1e-5 * scale, (case["m"], case["n"], kind)
+
+
+def test_lattice_cache_hit_is_identical():
+    """Repeated image() calls on one geometry/grid reuse the cached lattice and
+    delay table: maps, counts and argmax are identical to the uncached call."""
+    from paper_1709_02549_b200.beamform import _LATTICE_CACHE
+
+    model = synth.ScanModel()
+    ds1, _ = synth.dataset_2d(model, seed=11)
+    ds2, _ = synth.dataset_2d(model, seed=12)
+    grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 1e-3)
+    mask = mw.breast_mask(grid)
+    import paper_1709_02549_b200.beamform as bf
+
+    _LATTICE_CACHE.clear()
+    first = mw.images(ds1, ("das", "dmas"), grid, mask=mask, window=(model.k0, model.window))
+    real = bf.lattice_pass
+
+    def no_enumeration(*a, **k):  # a hit must not enumerate again
+        raise AssertionError("cache miss")
+
+    bf.lattice_pass = no_enumeration
+    try:
+        before = mw.EVAL_COUNTER.value
+        again = mw.images(ds1, ("das", "dmas"), grid, mask=mask, window=(model.k0, model.window))  # cache hit
+        assert mw.EVAL_COUNTER.value - before == 2 * int(mask.sum())
+        other = mw.images(ds2, ("das", "dmas"), grid, mask=mask, window=(model.k0, model.window))  # hit, new scan
+    finally:
+        bf.lattice_pass = real
+    _LATTICE_CACHE.clear()
+    fresh = mw.images(ds2, ("das", "dmas"), grid, mask=mask, window=(model.k0, model.window))
+    for k in ("das", "dmas"):
+        assert np.array_equal(first[k].dense(fill=np.nan), again[k].dense(fill=np.nan), equal_nan=True)
+        assert np.array_equal(other[k].dense(fill=np.nan), fresh[k].dense(fill=np.nan), equal_nan=True)
+        assert other[k].argmax_cell() == fresh[k].argmax_cell()
+        assert len(other[k]) == len(fresh[k]) == int(mask.sum())
