@@ -371,8 +371,8 @@ def _lattice_key(ds, scan: dv.DeviceScan, grid: ImagingGrid, bounds, stride: int
     g = ds.geometry
     ants = np.ascontiguousarray(np.asarray(g.antennas, dtype=np.float64)).tobytes()
     mh = None if emask is None else hashlib.blake2b(np.packbits(emask).tobytes(), digest_size=16).digest()
-    return (ants, scan.chan_host.tobytes(), float(scan.inv_scale), tuple(grid.origin), float(grid.resolution),
-            tuple(grid.dims), tuple(bounds), int(stride), mh, int(interp))
+    return (torch.cuda.current_device(), ants, scan.chan_host.tobytes(), float(scan.inv_scale), tuple(grid.origin),
+            float(grid.resolution), tuple(grid.dims), tuple(bounds), int(stride), mh, int(interp))
 
 
 def energies(ds, points, kind, interpolation: str = "linear", *, window=None, mode: str = "smem",
