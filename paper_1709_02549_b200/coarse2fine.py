@@ -235,10 +235,11 @@ def _region(b) -> Region:
     return Region((int(b[0]), int(b[1])), (int(b[3]), int(b[4])))
 
 
-def decode_trace(raw: bytes, region=_region) -> tuple[Region, MetricTrace, int]:
-    """Device trace -> (final region, MetricTrace, termination code); ``region``
-    converts a device box (2-D Region by default, volume.Box for 3-D)."""
-    tr = nat.Trace.from_buffer_copy(raw)
+def decode_trace(raw, region=_region) -> tuple[Region, MetricTrace, int]:
+    """Device trace (bytes, or a writable uint8 array decoded in place) ->
+    (final region, MetricTrace, termination code); ``region`` converts a device
+    box (2-D Region by default, volume.Box for 3-D)."""
+    tr = nat.Trace.from_buffer_copy(raw) if isinstance(raw, (bytes, bytearray)) else nat.Trace.from_buffer(raw)
     code = int(tr.termination)
     if code == -1:
         raise ValueError("coarse map has no entries in the breast region")
@@ -337,6 +338,7 @@ class _FrameworkPlan:
         self.interp, self.k0, self.w, self.mode = interp, k0, w, mode
         nx, ny = grid.dims
         self.mask_np, self.mask_t = _breast_mask_device(grid)
+        self.full_equivalent = int(self.mask_np.sum())  # the report's full-resolution cell count (fixed per plan)
         dev = dv.device()
         self.dense = torch.empty(nx * ny, dtype=torch.float32, device=dev)  # only valid cells are read
         self.valid = torch.empty(nx * ny, dtype=torch.uint8, device=dev)
@@ -392,7 +394,7 @@ class _FrameworkPlan:
         counts, flags = tail[:2], int(tail[2])
         if flags & 1:
             raise ValueError("energy map contains non-finite values")
-        final, trace, _ = decode_trace(self.h_trace.numpy().tobytes())
+        final, trace, _ = decode_trace(self.h_trace.numpy())  # decoded in place: the buffer is reused next call
         n_coarse, n_fine = int(counts[0]), int(counts[1])
         EVAL_COUNTER.add(n_coarse)
         EVAL_COUNTER.add(n_fine)
@@ -403,7 +405,7 @@ class _FrameworkPlan:
         t_c = ev[0].elapsed_time(ev[1]) / 1e3
         t_s = ev[1].elapsed_time(ev[2]) / 1e3
         t_f = ev[2].elapsed_time(ev[3]) / 1e3
-        full_equivalent = int(self.mask_np.sum())
+        full_equivalent = self.full_equivalent
         key = int(keys[0 if self.kcode == nat.MWB_DAS else 1])
         slot = 0xFFFFFFFF - (key & 0xFFFFFFFF)
         cell = (slot // ny, slot % ny) if key != 0 else composite.argmax_cell()
