@@ -147,9 +147,6 @@ __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::be
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void builders_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NBT) : "memory"); }
-__device__ __forceinline__ void group_sync(int gp) {
-  asm volatile("bar.sync %0, %1;" ::"r"(2 + gp), "n"(GW * 32) : "memory");
-}
 
 // 32 consecutive fp32 TMEM columns of this thread's lane
 __device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
@@ -200,14 +197,6 @@ __device__ __forceinline__ int scale_exp(uint32_t absmax_bits) {
 }
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((e + 127) << 23); }
 
-__device__ __forceinline__ float warp_incl_scan(float v, int lane) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const float y = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += y;
-  }
-  return v;
-}
 
 // points of table tile `tile`: the padded layout's {scan, count} record, or
 // the compact list's remainder; <= 0 means nothing to do (every role skips it)
