@@ -45,7 +45,6 @@ constexpr int TILE = 2 * TPB;     // focal points per CTA
 #ifndef MWB_W48_CH
 #define MWB_W48_CH 48  // register chunk for W % 48 == 0 windows (experiment knob: 24)
 #endif
-constexpr int WCH = 32;           // default window samples per register chunk (48 for W=48)
 constexpr int MAX_ANT = 64;
 constexpr int MAX_CHAN = 4096;
 constexpr int CAP_MAX = 8192;     // floats per stage buffer (32 KB)
