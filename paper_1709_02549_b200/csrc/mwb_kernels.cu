@@ -10,17 +10,19 @@
 // Design:
 //   * one CTA = a tile of 256 focal points (128 threads x 2 points; the two
 //     points of a thread are packed into float2 lanes of FFMA2/FADD2/FMUL2);
-//   * per tile, each channel's needed sample span [k0+lo_c, k0+hi_c+WCH] is
-//     staged into shared memory with cp.async.bulk (TMA 1-D) against an
-//     mbarrier, double-buffered across (scan, window-chunk, channel-group)
+//   * per tile, each channel's needed sample span [k0+lo_c, k0+hi_c+CH] is
+//     staged into shared memory with cp.async.bulk (TMA 1-D) into a 3-deep
+//     full/empty mbarrier ring across (scan, window-chunk, channel-group)
 //     steps;
 //   * per-point per-antenna distances are fp64 (exactly the reference's
 //     expression, no FMA contraction), the per-channel delay is
 //     (d_tx + d_rx) * inv_scale in fp64, split into i0 = floor and an fp32
 //     fraction — computed per point only, so a point's energy is bit-identical
 //     whichever tile or call evaluates it;
-//   * 32 window samples per point live in registers (float2 s[32]); the
-//     per-point accumulation order over channels and samples is fixed.
+//   * 32 (or 48) window samples per point live in registers (float2 s[CH]);
+//     the per-point accumulation order over channels and samples is fixed;
+//   * many scans of one geometry (configs[3]) go to the tensor-core kernel
+//     in mwb_tc.cuh instead (mwb_energies_tc).
 #include <cuda.h>  // CUtensorMap (types only; the encoder comes through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
@@ -1228,7 +1230,6 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
       break;
     }
     for (int k = 0; k < nk; ++k) rg[nk + k] = expand_box(rg[k], p.frac, sel, p.dims);
-    const int nreg = 2 * nk;
 
     // pass 1: count and sum of every child and of every child's expansion
     // children are disjoint: a cell's child index follows from the split point
