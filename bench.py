@@ -472,6 +472,27 @@ def run_ours(args):
         roofline = smem_roofline(pps_launch, avg, smem_gbs, fp32_tf, traffic)
 
 
+    # the CUDA-core kernel (north_star's design: shared-memory staging, FP32
+    # pipe) on the same workload, timed in the same run, with its roofline
+    core = None
+    if bi.uses_tensor_cores and not args.no_configs:
+        bk = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=(model.k0, model.window),
+                         mode="smem")
+        for _ in range(2):
+            bk.run_device(sig_d, outs["das"], outs["dmas"], keys["das"], keys["dmas"])
+        torch.cuda.synchronize()
+        k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+        for a, b in k_ev:
+            a.record()
+            bk.run_device(sig_d, outs["das"], outs["dmas"], keys["das"], keys["dmas"])
+            b.record()
+        torch.cuda.synchronize()
+        k_ms = statistics.mean(a.elapsed_time(b) for a, b in k_ev)
+        core = {"kernel": "energy_kernel<BOTH> (CUDA cores, mode smem)", "ms_per_step": k_ms,
+                "value": 2.0 * S * P * C / (k_ms * 1e-3), "unit": UNIT,
+                "roofline": smem_roofline(pps_launch, k_ms, smem_gbs, fp32_tf, traffic)}
+        del bk
+
     # end to end through the public host API
     e2e = None
     if not args.no_e2e:
@@ -509,6 +530,7 @@ def run_ours(args):
             "images_per_s": images_s,
             "pixel_pair_samples_per_s": value * W,
             "roofline": roofline,
+            "cuda_core_path": core,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "other_configs": others,
