@@ -1137,6 +1137,79 @@ __device__ __forceinline__ void put_box(int32_t* dst, const Box& b) {
   dst[3] = b.hi[0]; dst[4] = b.hi[1]; dst[5] = b.hi[2];
 }
 
+// One select_roi decision (coarse2fine.py:207-252) from the children's and
+// expansions' statistics: scores (variance on the first iteration, Eq. (5)
+// after), np.argmax, the n_min stop, W/B of the previous vs the new selection
+// and the record.  Run by one thread; returns the termination code and, when
+// the loop goes on, nxt = {W, B, n, sum, m2} of the new selection.
+template <int NK>
+__device__ int select_score(const SelectParams& p, mwb_trace_t* tr, int iteration, int nk, const Box* rg,
+                            const double* cnt, const double* sums, const double* mean, const double* m2,
+                            double n_sel, double sum_sel, double m2_sel, double sigma_prev_sq, bool have_prev,
+                            double prev_w, double prev_b, double* nxt, Box* next_sel) {
+  const int rec_i = iteration;
+  mwb_iter_record_t rec;
+  memset(&rec, 0, sizeof(rec));
+  rec.n_children = nk;
+  double scores[NK];
+  for (int k = 0; k < nk; ++k) {
+    rec.counts[k] = (int)cnt[k];
+    if (cnt[k] == 0.0) {
+      scores[k] = -INFINITY;  // empty child (coarse2fine.py:215-217)
+      rec.has_stats[k] = 0;
+    } else {
+      const double mu = mean[k], var = m2[k] / cnt[k];
+      rec.mu[k] = mu;
+      rec.var[k] = var;
+      if (iteration == 0) {  // first iteration scores by variance (218-220)
+        scores[k] = var;
+        rec.has_stats[k] = 1;
+      } else {  // Eq. (5) (_metric_parts, 67-91)
+        rec.has_stats[k] = 2;
+        if (var == 0.0) {
+          scores[k] = mu;
+        } else {
+          const double dr = __ddiv_rn(__dsub_rn(var, sigma_prev_sq), var);
+          const double dl = fmin(fmax(dr, 0.0), 1.0);
+          scores[k] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, dl), mu), __dmul_rn(dl, var));
+          rec.delta_raw[k] = dr;
+          rec.delta[k] = dl;
+          rec.clamped[k] = dl != dr;
+        }
+      }
+    }
+    rec.scores[k] = scores[k];
+  }
+  int selq = 0;  // np.argmax: first maximum
+  for (int k = 1; k < nk; ++k)
+    if (scores[k] > scores[selq]) selq = k;
+  if (rec.counts[selq] < p.n_min) return MWB_TERM_N_MIN;
+  const int e = nk + selq;
+  const double n_e = cnt[e], sum_e = sums[e], m2_e = m2[e];
+  // W, B of the previous vs the new selection (class_distances, 94-109)
+  const double w = __dadd_rn(m2_sel, m2_e);
+  const double ma = sum_sel / n_sel, mb = sum_e / n_e;
+  const double grand = __ddiv_rn(__dadd_rn(sum_sel, sum_e), __dadd_rn(n_sel, n_e));
+  const double da = __dsub_rn(ma, grand), db = __dsub_rn(mb, grand);
+  const double b = __dadd_rn(__dmul_rn(n_sel, __dmul_rn(da, da)), __dmul_rn(n_e, __dmul_rn(db, db)));
+  const bool satisfied = !have_prev || (b > prev_b || w < prev_w);  // OR (235)
+  rec.iteration = iteration + 1;
+  rec.selected = selq;
+  rec.satisfied = satisfied;
+  put_box(rec.selected_region, rg[selq]);
+  put_box(rec.expanded_region, rg[e]);
+  rec.w = w;
+  rec.b = b;
+  if (rec_i < MWB_MAX_ITERS) tr->records[rec_i] = rec;
+  nxt[0] = w;
+  nxt[1] = b;
+  nxt[2] = n_e;
+  nxt[3] = sum_e;
+  nxt[4] = m2_e;
+  *next_sel = rg[e];
+  return rec_i >= MWB_MAX_ITERS ? MWB_TERM_OVERFLOW : (satisfied ? MWB_TERM_NONE : MWB_TERM_DISTANCE);
+}
+
 template <int NK>  // 4 children (2-D quadrants) or 8 (3-D octants)
 __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams p0) {
   // CTA b handles scan b of a batch (maps dense_stride floats apart)
@@ -1288,72 +1361,9 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     for (int k = 0; k < 2 * NK; ++k) m2[k] = res[k];
     __syncthreads();
 
-    if (threadIdx.x == 0) {
-      const int rec_i = iteration;
-      mwb_iter_record_t rec;
-      memset(&rec, 0, sizeof(rec));
-      rec.n_children = nk;
-      double scores[NK];
-      for (int k = 0; k < nk; ++k) {
-        rec.counts[k] = (int)cnt[k];
-        if (cnt[k] == 0.0) {
-          scores[k] = -INFINITY;  // empty child (coarse2fine.py:215-217)
-          rec.has_stats[k] = 0;
-        } else {
-          const double mu = mean[k], var = m2[k] / cnt[k];
-          rec.mu[k] = mu;
-          rec.var[k] = var;
-          if (iteration == 0) {  // first iteration scores by variance (218-220)
-            scores[k] = var;
-            rec.has_stats[k] = 1;
-          } else {  // Eq. (5) (_metric_parts, 67-91)
-            rec.has_stats[k] = 2;
-            if (var == 0.0) {
-              scores[k] = mu;
-            } else {
-              const double dr = __ddiv_rn(__dsub_rn(var, sigma_prev_sq), var);
-              const double dl = fmin(fmax(dr, 0.0), 1.0);
-              scores[k] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, dl), mu), __dmul_rn(dl, var));
-              rec.delta_raw[k] = dr;
-              rec.delta[k] = dl;
-              rec.clamped[k] = dl != dr;
-            }
-          }
-        }
-        rec.scores[k] = scores[k];
-      }
-      int selq = 0;  // np.argmax: first maximum
-      for (int k = 1; k < nk; ++k)
-        if (scores[k] > scores[selq]) selq = k;
-      if (rec.counts[selq] < p.n_min) {
-        ctl[0] = MWB_TERM_N_MIN;
-      } else {
-        const int e = nk + selq;
-        const double n_e = cnt[e], sum_e = sums[e], m2_e = m2[e];
-        // W, B of the previous vs the new selection (class_distances, 94-109)
-        const double w = __dadd_rn(m2_sel, m2_e);
-        const double ma = sum_sel / n_sel, mb = sum_e / n_e;
-        const double grand = __ddiv_rn(__dadd_rn(sum_sel, sum_e), __dadd_rn(n_sel, n_e));
-        const double da = __dsub_rn(ma, grand), db = __dsub_rn(mb, grand);
-        const double b = __dadd_rn(__dmul_rn(n_sel, __dmul_rn(da, da)), __dmul_rn(n_e, __dmul_rn(db, db)));
-        const bool satisfied = !have_prev || (b > prev_b || w < prev_w);  // OR (235)
-        rec.iteration = iteration + 1;
-        rec.selected = selq;
-        rec.satisfied = satisfied;
-        put_box(rec.selected_region, rg[selq]);
-        put_box(rec.expanded_region, rg[e]);
-        rec.w = w;
-        rec.b = b;
-        if (rec_i < MWB_MAX_ITERS) tr->records[rec_i] = rec;
-        ctl[0] = rec_i >= MWB_MAX_ITERS ? MWB_TERM_OVERFLOW : (satisfied ? MWB_TERM_NONE : MWB_TERM_DISTANCE);
-        red[0] = w;
-        red[1] = b;
-        red[2] = n_e;
-        red[3] = sum_e;
-        red[4] = m2_e;
-        next_sel = rg[e];
-      }
-    }
+    if (threadIdx.x == 0)
+      ctl[0] = select_score<NK>(p, tr, iteration, nk, rg, cnt, sums, mean, m2, n_sel, sum_sel, m2_sel,
+                                sigma_prev_sq, have_prev, prev_w, prev_b, red, &next_sel);
     __syncthreads();
     term = ctl[0];
     if (term == MWB_TERM_N_MIN) break;
@@ -1376,6 +1386,230 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     put_box(p.region_out, sel);
   }
 }
+// ----------------------------------------------------------------------------
+// K2w: warp-per-scan select_roi for 2-D lattices whose breast box stages in
+// SEL_WARP_STAGE cells (the framework's 16..64-cell-wide low-res lattices).
+// A 256-thread CTA spends most of its time in barriers and 16-double block
+// reductions when every thread visits only ~5 cells per pass; a warp visits
+// ~36 per lane, reduces with shuffles only, and SEL_WPB scans share a CTA.
+// Cells are walked in lattice coordinates (no div/mod per cell) and each
+// cell's child / expansion membership is four range tests per axis (the
+// expansions are per-axis: expand_box grows each axis independently).
+// Same decisions as select_roi_kernel<4>; the summation order is the warp's,
+// so single-scan and batched selection both dispatch here for such lattices
+// and stay bit-identical to each other.
+// ----------------------------------------------------------------------------
+constexpr int SEL_WPB = 4;
+constexpr int SEL_WARP_STAGE = 4096;
+
+struct SelWarpCtl {
+  double nxt[5];
+  Box next;
+  int term;
+};
+
+__device__ __forceinline__ double warp_sum_d(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ int warp_sum_i(int x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// f(lx, ly, v) for every valid cell of box r; lattice cells are i = lane + 32k
+// of the r-lattice in row-major order, advanced incrementally
+template <class F>
+__device__ __forceinline__ void warp_cells(const float* sv, int sLy, int sl0x, int sl0y, int D, const Box& r,
+                                           F&& f) {
+  const int l0x = (r.lo[0] + D - 1) / D, l1x = r.hi[0] / D;
+  const int l0y = (r.lo[1] + D - 1) / D, l1y = r.hi[1] / D;
+  if (l1x < l0x || l1y < l0y) return;
+  const int Ly = l1y - l0y + 1, n = (l1x - l0x + 1) * Ly;
+  const int lane = threadIdx.x & 31;
+  const int q = 32 / Ly, rr = 32 - q * Ly;
+  int lx = lane / Ly, ly = lane - lx * Ly;
+  const float* base = sv + (l0x - sl0x) * sLy + (l0y - sl0y);
+  for (int i = lane; i < n; i += 32) {
+    const float v = base[lx * sLy + ly];
+    if (v == v) f(l0x + lx, l0y + ly, (double)v);
+    lx += q;
+    ly += rr;
+    if (ly >= Ly) {
+      ly -= Ly;
+      ++lx;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(SEL_WPB * 32) select_roi_warp_kernel(const SelectParams p, int n_scans) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * SEL_WPB + warp;
+  if (s >= n_scans) return;
+  extern __shared__ float smem_sel[];
+  __shared__ SelWarpCtl wctl[SEL_WPB];
+  SelWarpCtl& wc = wctl[warp];
+  const int D = p.D, sLx = p.sL[0], sLy = p.sL[1], sl0x = p.sl0[0], sl0y = p.sl0[1];
+  const int nst = sLx * sLy;
+  float* sv = smem_sel + warp * nst;
+  const float* dense = p.dense + (size_t)s * p.dense_stride;
+  int32_t* region_out = p.region_out + 6 * s;
+  mwb_trace_t* tr = p.trace + s;
+
+  {  // stage the breast box's lattice: both loads independent, 4 in flight per lane
+    int lx = lane / sLy, ly = lane - lx * sLy;
+    const int q = 32 / sLy, rr = 32 - q * sLy;
+#pragma unroll 4
+    for (int i = lane; i < nst; i += 32) {
+      const size_t slot = (size_t)(sl0x + lx) * D * p.ny + (size_t)(sl0y + ly) * D;
+      const float v = __ldg(dense + slot);
+      const uint8_t ok = __ldg(p.valid + slot);
+      sv[i] = ok ? v : __int_as_float(0x7fc00000);
+      lx += q;
+      ly += rr;
+      if (ly >= sLy) {
+        ly -= sLy;
+        ++lx;
+      }
+    }
+  }
+  __syncwarp();
+
+  // breast-region stats: count, sum, min, max, then the two-pass m2 (coarse2fine.py:186-199)
+  double n_sel, sum_sel, m2_sel;
+  {
+    int c = 0;
+    double sm = 0.0, mn = INFINITY, mx = -INFINITY;
+    warp_cells(sv, sLy, sl0x, sl0y, D, p.breast, [&](int, int, double v) {
+      ++c;
+      sm += v;
+      mn = fmin(mn, v);
+      mx = fmax(mx, v);
+    });
+    n_sel = (double)warp_sum_i(c);
+    sum_sel = warp_sum_d(sm);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (n_sel == 0.0 || mx == mn) {
+      if (lane == 0) {
+        tr->termination = n_sel == 0.0 ? MWB_TERM_EMPTY : MWB_TERM_DEGENERATE;
+        tr->n_records = 0;
+        put_box(tr->final_region, p.breast);
+        put_box(region_out, p.breast);
+      }
+      return;
+    }
+    const double mean = sum_sel / n_sel;
+    double d2 = 0.0;
+    warp_cells(sv, sLy, sl0x, sl0y, D, p.breast, [&](int, int, double v) {
+      const double d = v - mean;
+      d2 += d * d;
+    });
+    m2_sel = warp_sum_d(d2);
+  }
+
+  Box sel = p.breast;
+  double sigma_prev_sq = m2_sel / n_sel;
+  double prev_w = 0.0, prev_b = 0.0;
+  bool have_prev = false;
+  int iteration = 0;
+  int term = MWB_TERM_NONE;
+
+  while (true) {
+    Box rg[8];
+    const int nk = split_box(sel, 2, rg);
+    if (nk == 0) {
+      term = MWB_TERM_REGION_FLOOR;
+      break;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rg[4 + k] = expand_box(rg[k], p.frac, sel, 2);
+    // lattice thresholds: a cell is in a high-half child iff l * D > mid;
+    // expansion ranges per axis: x from rg[4] (low) / rg[5] (high), y from rg[4] / rg[6]
+    const int mxl = rg[0].hi[0] / D, myl = rg[0].hi[1] / D;
+    const int ex0l = (rg[4].lo[0] + D - 1) / D, ex0h = rg[4].hi[0] / D;
+    const int ex1l = (rg[5].lo[0] + D - 1) / D, ex1h = rg[5].hi[0] / D;
+    const int ey0l = (rg[4].lo[1] + D - 1) / D, ey0h = rg[4].hi[1] / D;
+    const int ey1l = (rg[6].lo[1] + D - 1) / D, ey1h = rg[6].hi[1] / D;
+
+    // pass 1: count and sum of every child and of every child's expansion
+    int ci[8];
+    double a1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      ci[k] = 0;
+      a1[k] = 0.0;
+    }
+    warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, double v) {
+      const int kc = (lx > mxl) | ((ly > myl) << 1);
+      const bool x0 = ex0l <= lx && lx <= ex0h, x1 = ex1l <= lx && lx <= ex1h;
+      const bool y0 = ey0l <= ly && ly <= ey0h, y1 = ey1l <= ly && ly <= ey1h;
+      const bool in[8] = {kc == 0, kc == 1, kc == 2, kc == 3, x0 && y0, x1 && y0, x0 && y1, x1 && y1};
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (in[k]) {
+          ++ci[k];
+          a1[k] += v;
+        }
+    });
+    double cnt[8], sums[8], mean[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      cnt[k] = (double)warp_sum_i(ci[k]);
+      sums[k] = warp_sum_d(a1[k]);
+      mean[k] = cnt[k] > 0.0 ? sums[k] / cnt[k] : 0.0;
+    }
+    // pass 2: sum of (x - mean)^2 (two-pass variance, as numpy's var)
+    double a2[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a2[k] = 0.0;
+    warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, double v) {
+      const int kc = (lx > mxl) | ((ly > myl) << 1);
+      const bool x0 = ex0l <= lx && lx <= ex0h, x1 = ex1l <= lx && lx <= ex1h;
+      const bool y0 = ey0l <= ly && ly <= ey0h, y1 = ey1l <= ly && ly <= ey1h;
+      const bool in[8] = {kc == 0, kc == 1, kc == 2, kc == 3, x0 && y0, x1 && y0, x0 && y1, x1 && y1};
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (in[k]) {
+          const double d = v - mean[k];
+          a2[k] += d * d;
+        }
+    });
+    double m2[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m2[k] = warp_sum_d(a2[k]);
+
+    if (lane == 0)
+      wc.term = select_score<4>(p, tr, iteration, nk, rg, cnt, sums, mean, m2, n_sel, sum_sel, m2_sel,
+                                sigma_prev_sq, have_prev, prev_w, prev_b, wc.nxt, &wc.next);
+    __syncwarp();
+    term = wc.term;
+    if (term == MWB_TERM_N_MIN) break;
+    iteration += 1;
+    if (term != MWB_TERM_NONE) break;
+    prev_w = wc.nxt[0];
+    prev_b = wc.nxt[1];
+    have_prev = true;
+    n_sel = wc.nxt[2];
+    sum_sel = wc.nxt[3];
+    m2_sel = wc.nxt[4];
+    sigma_prev_sq = m2_sel / n_sel;
+    sel = wc.next;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    tr->termination = term;
+    tr->n_records = min(iteration, MWB_MAX_ITERS);
+    put_box(tr->final_region, sel);
+    put_box(region_out, sel);
+  }
+}
+
 // ----------------------------------------------------------------------------
 // K5: device-side scan synthesis (the step before the path)
 //   model 0: the reference simulator (simulate.py:53-73, 141-156): cosine-
@@ -2341,12 +2575,21 @@ static int select_common(SelectParams& p, void* stream, int n_scans = 1) {
     n *= p.sL[a];
   }
   p.staged = n > 0 && n <= SEL_STAGE_MAX;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (p.dims == 2 && n > 0 && n <= SEL_WARP_STAGE) {  // warp per scan (K2w)
+    const size_t smw = sizeof(float) * (size_t)n * SEL_WPB;
+    cudaError_t e = cudaFuncSetAttribute(select_roi_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(float) * SEL_WARP_STAGE * SEL_WPB));
+    if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    select_roi_warp_kernel<<<(n_scans + SEL_WPB - 1) / SEL_WPB, SEL_WPB * 32, smw, st>>>(p, n_scans);
+    return check_launch("select_roi_warp_kernel");
+  }
   const size_t sm = p.staged ? sizeof(float) * (size_t)n : 0;
   void (*fn)(SelectParams) = p.dims == 3 ? select_roi_kernel<8> : select_roi_kernel<4>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(float) * SEL_STAGE_MAX));
   if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-  fn<<<n_scans, SEL_TPB, sm, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  fn<<<n_scans, SEL_TPB, sm, st>>>(p);
   return check_launch("select_roi_kernel");
 }
 
