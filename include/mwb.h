@@ -187,19 +187,18 @@ int mwb_energies_tiles(const float* sig, int n_scans, int64_t scan_stride, int n
 /*
  * Batched fine-pass enumeration: the stride-1 cells of each scan's device
  * region d_regions[s] (int32[6]) that pass `mask` and are not on the
- * skip_stride lattice.  _tile_bound writes the largest region's number of
- * 16x16 enumeration tiles (device int32); with it, _count writes {padded
- * points, tiles} to d_totals (device int32[2]); after reading them, _write
- * fills pts_xyz / out_idx (slot ix*ny+iy) / tile_info.  Each scan starts on a
- * 256-point tile boundary.
+ * skip_stride lattice.  _count writes {padded points, tiles} to d_totals
+ * (device int32[2]) and leaves each scan's cell count in the first n_scans
+ * int32 of the workspace; after reading the totals, _write fills pts_xyz /
+ * out_idx (slot ix*ny+iy) / tile_info.  Each scan starts on a 256-point tile
+ * boundary.
  */
-int mwb_regions_tile_bound(const int32_t* d_regions, int n_scans, int32_t* d_bound, void* stream);
-int64_t mwb_regions_workspace_bytes(int tiles_bound, int n_scans);
-int mwb_enumerate_regions_count(int nx, int ny, const int32_t* d_regions, int n_scans, int tiles_bound,
+int64_t mwb_regions_workspace_bytes(int n_scans);
+int mwb_enumerate_regions_count(int nx, int ny, const int32_t* d_regions, int n_scans,
                                 const uint8_t* mask, int skip_stride, int32_t* d_totals,
                                 void* workspace, void* stream);
 int mwb_enumerate_regions_write(double ox, double oy, double res, int nx, int ny,
-                                const int32_t* d_regions, int n_scans, int tiles_bound,
+                                const int32_t* d_regions, int n_scans,
                                 const uint8_t* mask, int skip_stride, double* pts_xyz,
                                 int32_t* out_idx, int32_t* tile_info, void* workspace, void* stream);
 

@@ -124,10 +124,9 @@ _SIGNATURES = {
          _P],
         _I,
     ),
-    "mwb_regions_tile_bound": ([_P, _I, _P, _P], _I),
-    "mwb_regions_workspace_bytes": ([_I, _I], _I64),
-    "mwb_enumerate_regions_count": ([_I, _I, _P, _I, _I, _P, _I, _P, _P, _P], _I),
-    "mwb_enumerate_regions_write": ([_D, _D, _D, _I, _I, _P, _I, _I, _P, _I, _P, _P, _P, _P, _P], _I),
+    "mwb_regions_workspace_bytes": ([_I], _I64),
+    "mwb_enumerate_regions_count": ([_I, _I, _P, _I, _P, _I, _P, _P, _P], _I),
+    "mwb_enumerate_regions_write": ([_D, _D, _D, _I, _I, _P, _I, _P, _I, _P, _P, _P, _P, _P], _I),
     "mwb_select_roi_batch": ([_P, _I64, _P, _I, _I, _I, _I, _I, _I, _I, _D, _I, _I, _P, _P, _P], _I),
     "mwb_lattice_workspace_bytes": ([_I, _I, _I], _I64),
     "mwb_volume_workspace_bytes": ([_I, _I, _I, _I], _I64),

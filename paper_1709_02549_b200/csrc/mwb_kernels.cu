@@ -919,54 +919,61 @@ __global__ void __launch_bounds__(256) lattice_write_kernel(const LatticeParams 
 // Batched enumeration of per-scan regions (stride 1, 2-D): every scan's cells
 // go to one packed point list in which each scan starts on a 256-point tile
 // boundary; tile_info[t] = {scan, valid points} drives the table and energy
-// kernels, so one launch serves every scan's fine pass.
+// kernels, so one launch serves every scan's fine pass.  One CTA per scan
+// walks its region's 16x16 enumeration tiles in order (a fine-pass region is
+// a handful of tiles: a CTA per (scan, tile) spends its time being scheduled).
 // ----------------------------------------------------------------------------
 struct RegionBatch {
-  int n_scans, tiles_max;
-  int* tile_counts;   // [S][tiles_max]
-  int* tile_offsets;  // [S][tiles_max]
-  int* scan_counts;   // [S]
+  int n_scans;
+  int* scan_counts;   // [S] valid cells of each scan's region
   int* scan_offsets;  // [S] first point of each scan (multiple of TILE)
   int* totals;        // [2] padded points, tiles
 };
 
-__device__ __forceinline__ LatticeParams scan_lattice(LatticeParams p, int s, const RegionBatch& b) {
+__global__ void __launch_bounds__(256) region_count_kernel(LatticeParams p, const RegionBatch b) {
+  const int s = blockIdx.x;
   p.d_region += 6 * s;
-  p.tile_counts = b.tile_counts + (size_t)s * b.tiles_max;
-  p.tile_offsets = b.tile_offsets + (size_t)s * b.tiles_max;
-  return p;
-}
-
-__global__ void __launch_bounds__(256) region_count_kernel(const LatticeParams p0, const RegionBatch b) {
-  const LatticeParams p = scan_lattice(p0, blockIdx.y, b);
   const LatticeGeom g = lattice_geom(p);
-  int ix, iy, iz;
-  const bool ok = lattice_cell(p, g, blockIdx.x, threadIdx.x, ix, iy, iz);
-  const int n = __syncthreads_count(ok);
-  if (threadIdx.x == 0) p.tile_counts[blockIdx.x] = n;
+  const int nt = g.T[0] * g.T[1] * g.T[2];
+  int total = 0;
+  for (int t = 0; t < nt; ++t) {
+    int ix, iy, iz;
+    total += __syncthreads_count(lattice_cell(p, g, t, threadIdx.x, ix, iy, iz));
+  }
+  if (threadIdx.x == 0) b.scan_counts[s] = total;
 }
 
-__global__ void __launch_bounds__(1024) region_scan_kernel(const LatticeParams p0, const RegionBatch b) {
-  const LatticeParams p = scan_lattice(p0, blockIdx.x, b);
-  block_exclusive_scan(p.tile_counts, p.tile_offsets, b.tiles_max, b.scan_counts + blockIdx.x);
-}
-
+// padded per-scan sizes -> scan offsets (points); totals = (points, tiles)
 __global__ void __launch_bounds__(1024) region_offsets_kernel(const RegionBatch b) {
-  // padded sizes -> scan offsets (points); totals = (points, tiles)
-  __shared__ int padded[1024];
+  __shared__ int warp_sums[32];
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int base = 0; base < b.n_scans; base += 1024) {
-    const int s = base + threadIdx.x;
-    padded[threadIdx.x] = s < b.n_scans ? (b.scan_counts[s] + TILE - 1) / TILE * TILE : 0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int k = 0; k < 1024 && base + k < b.n_scans; ++k) {
-        b.scan_offsets[base + k] = carry;
-        carry += padded[k];
-      }
+    const int i = base + threadIdx.x;
+    const int v = i < b.n_scans ? (b.scan_counts[i] + TILE - 1) / TILE * TILE : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_sums[lane] = w;
+    }
+    __syncthreads();
+    if (i < b.n_scans) b.scan_offsets[i] = carry + (warp > 0 ? warp_sums[warp - 1] : 0) + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_sums[31];
     __syncthreads();
   }
   if (threadIdx.x == 0) {
@@ -975,45 +982,40 @@ __global__ void __launch_bounds__(1024) region_offsets_kernel(const RegionBatch 
   }
 }
 
-// largest number of 16x16 enumeration tiles over the scans' regions -> *bound
-__global__ void region_bound_kernel(const int* regions, int n_scans, int* bound) {
-  int mx = 0;
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_scans; s += gridDim.x * blockDim.x) {
-    const int* r = regions + 6 * s;
-    mx = max(mx, ((r[3] - r[0] + 16) / 16) * ((r[4] - r[1] + 16) / 16));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(bound, mx);
-}
-
-__global__ void region_tiles_kernel(const RegionBatch b, int2* tile_info) {
+__global__ void __launch_bounds__(256) region_write_kernel(LatticeParams p, const RegionBatch b, int2* tile_info) {
+  __shared__ int wsum[2][8];
   const int s = blockIdx.x;
-  const int count = b.scan_counts[s];
-  const int t0 = b.scan_offsets[s] / TILE;
-  for (int j = threadIdx.x; j * TILE < count; j += blockDim.x)
-    tile_info[t0 + j] = make_int2(s, min(TILE, count - j * TILE));
-}
-
-__global__ void __launch_bounds__(256) region_write_kernel(const LatticeParams p0, const RegionBatch b) {
-  __shared__ int wsum[8];
-  const int s = blockIdx.y;
-  const LatticeParams p = scan_lattice(p0, s, b);
+  p.d_region += 6 * s;
   const LatticeGeom g = lattice_geom(p);
-  int ix = 0, iy = 0, iz = 0;
-  const bool ok = lattice_cell(p, g, blockIdx.x, threadIdx.x, ix, iy, iz);
-  const unsigned bal = __ballot_sync(0xffffffffu, ok);
+  const int nt = g.T[0] * g.T[1] * g.T[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) wsum[warp] = __popc(bal);
-  __syncthreads();
-  int before = 0;
-  for (int w = 0; w < warp; ++w) before += wsum[w];
-  if (!ok) return;
-  const int pos = b.scan_offsets[s] + p.tile_offsets[blockIdx.x] + before + __popc(bal & ((1u << lane) - 1u));
-  p.pts[3 * (size_t)pos] = __dadd_rn(p.ox, __dmul_rn((double)ix + 0.5, p.res));
-  p.pts[3 * (size_t)pos + 1] = __dadd_rn(p.oy, __dmul_rn((double)iy + 0.5, p.res));
-  p.pts[3 * (size_t)pos + 2] = 0.0;
-  p.out_idx[pos] = ix * p.ny + iy;
+  const int base = b.scan_offsets[s];
+  int carry = 0;
+  for (int t = 0; t < nt; ++t) {
+    int ix = 0, iy = 0, iz = 0;
+    const bool ok = lattice_cell(p, g, t, threadIdx.x, ix, iy, iz);
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    int* ws = wsum[t & 1];  // double-buffered: one barrier per tile
+    if (lane == 0) ws[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      before += w < warp ? ws[w] : 0;
+      all += ws[w];
+    }
+    if (ok) {
+      const int pos = base + carry + before + __popc(bal & ((1u << lane) - 1u));
+      p.pts[3 * (size_t)pos] = __dadd_rn(p.ox, __dmul_rn((double)ix + 0.5, p.res));
+      p.pts[3 * (size_t)pos + 1] = __dadd_rn(p.oy, __dmul_rn((double)iy + 0.5, p.res));
+      p.pts[3 * (size_t)pos + 2] = 0.0;
+      p.out_idx[pos] = ix * p.ny + iy;
+    }
+    carry += all;
+  }
+  const int t0 = base / TILE;
+  for (int j = threadIdx.x; j * TILE < carry; j += blockDim.x)
+    tile_info[t0 + j] = make_int2(s, min(TILE, carry - j * TILE));
 }
 
 // ----------------------------------------------------------------------------
@@ -2484,34 +2486,19 @@ int mwb_enumerate_volume(double ox, double oy, double oz, double res, int nx, in
   return enumerate_common(p, 8, 8, 4, workspace, stream);
 }
 
-static RegionBatch region_batch(void* workspace, int tiles_bound, int n_scans) {
+static RegionBatch region_batch(void* workspace, int n_scans) {
   RegionBatch b;
   b.n_scans = n_scans;
-  b.tiles_max = tiles_bound;
   int* w = reinterpret_cast<int*>(workspace);
-  b.tile_counts = w;
-  w += (size_t)n_scans * b.tiles_max;
-  b.tile_offsets = w;
-  w += (size_t)n_scans * b.tiles_max;
   b.scan_counts = w;
-  w += n_scans;
-  b.scan_offsets = w;
-  w += n_scans;
-  b.totals = w;
+  b.scan_offsets = w + n_scans;
+  b.totals = w + 2 * n_scans;
   return b;
 }
 
-int64_t mwb_regions_workspace_bytes(int tiles_bound, int n_scans) {
-  if (tiles_bound < 1 || n_scans < 0) return -1;
-  return (long long)sizeof(int) * (2LL * tiles_bound * n_scans + 2LL * n_scans + 2) + 256;
-}
-
-int mwb_regions_tile_bound(const int32_t* d_regions, int n_scans, int32_t* d_bound, void* stream) {
-  if (n_scans < 1 || !d_regions || !d_bound) return set_err(MWB_EINVAL, "mwb_regions_tile_bound: bad arguments");
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaMemsetAsync(d_bound, 0, sizeof(int32_t), st);
-  region_bound_kernel<<<(n_scans + 255) / 256, 256, 0, st>>>(d_regions, n_scans, d_bound);
-  return check_launch("region_bound_kernel");
+int64_t mwb_regions_workspace_bytes(int n_scans) {
+  if (n_scans < 0) return -1;
+  return (long long)sizeof(int) * (2LL * n_scans + 2) + 256;
 }
 
 static LatticeParams region_params(double ox, double oy, double res, int nx, int ny, const int32_t* d_regions,
@@ -2530,39 +2517,33 @@ static LatticeParams region_params(double ox, double oy, double res, int nx, int
   return p;
 }
 
-int mwb_enumerate_regions_count(int nx, int ny, const int32_t* d_regions, int n_scans, int tiles_bound,
-                                const uint8_t* mask, int skip_stride, int32_t* d_totals, void* workspace,
-                                void* stream) {
-  if (nx < 1 || ny < 1 || n_scans < 1 || n_scans > 65535 || tiles_bound < 1)
+int mwb_enumerate_regions_count(int nx, int ny, const int32_t* d_regions, int n_scans, const uint8_t* mask,
+                                int skip_stride, int32_t* d_totals, void* workspace, void* stream) {
+  if (nx < 1 || ny < 1 || n_scans < 1 || n_scans > 65535)
     return set_err(MWB_EINVAL, "mwb_enumerate_regions_count: bad sizes");
   if (!d_regions || !d_totals || !workspace) return set_err(MWB_EINVAL, "mwb_enumerate_regions_count: null pointer");
-  RegionBatch b = region_batch(workspace, tiles_bound, n_scans);
+  RegionBatch b = region_batch(workspace, n_scans);
   LatticeParams p = region_params(0.0, 0.0, 1.0, nx, ny, d_regions, mask, skip_stride);
-  p.n_tiles_max = b.tiles_max;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  region_count_kernel<<<dim3(b.tiles_max, n_scans), 256, 0, st>>>(p, b);
-  region_scan_kernel<<<n_scans, 1024, 0, st>>>(p, b);
+  region_count_kernel<<<n_scans, 256, 0, st>>>(p, b);
   region_offsets_kernel<<<1, 1024, 0, st>>>(b);
   cudaMemcpyAsync(d_totals, b.totals, 2 * sizeof(int), cudaMemcpyDeviceToDevice, st);
   return check_launch("enumerate_regions_count");
 }
 
 int mwb_enumerate_regions_write(double ox, double oy, double res, int nx, int ny, const int32_t* d_regions,
-                                int n_scans, int tiles_bound, const uint8_t* mask, int skip_stride,
-                                double* pts_xyz, int32_t* out_idx, int32_t* tile_info, void* workspace,
-                                void* stream) {
-  if (nx < 1 || ny < 1 || n_scans < 1 || n_scans > 65535 || tiles_bound < 1)
+                                int n_scans, const uint8_t* mask, int skip_stride, double* pts_xyz,
+                                int32_t* out_idx, int32_t* tile_info, void* workspace, void* stream) {
+  if (nx < 1 || ny < 1 || n_scans < 1 || n_scans > 65535)
     return set_err(MWB_EINVAL, "mwb_enumerate_regions_write: bad sizes");
   if (!d_regions || !pts_xyz || !out_idx || !tile_info || !workspace)
     return set_err(MWB_EINVAL, "mwb_enumerate_regions_write: null pointer");
-  RegionBatch b = region_batch(workspace, tiles_bound, n_scans);
+  RegionBatch b = region_batch(workspace, n_scans);
   LatticeParams p = region_params(ox, oy, res, nx, ny, d_regions, mask, skip_stride);
-  p.n_tiles_max = b.tiles_max;
   p.pts = pts_xyz;
   p.out_idx = out_idx;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  region_tiles_kernel<<<n_scans, 256, 0, st>>>(b, reinterpret_cast<int2*>(tile_info));
-  region_write_kernel<<<dim3(b.tiles_max, n_scans), 256, 0, st>>>(p, b);
+  region_write_kernel<<<n_scans, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p, b,
+                                                                                 reinterpret_cast<int2*>(tile_info));
   return check_launch("enumerate_regions_write");
 }
 

@@ -165,21 +165,18 @@ class FrameworkBatch:
                  traces.data_ptr(), stream)
         ev[2].record()
         # 3. fine pass: packed per-scan ROI cells, one table and one energy launch
-        bound = torch.zeros(1, dtype=torch.int32, device=dev)
-        nat.call("mwb_regions_tile_bound", regions.data_ptr(), s_n, bound.data_ptr(), stream)
-        tiles_bound = max(1, int(bound.item()))  # host sync 1 of 2: size of the largest ROI
-        ws = torch.empty(int(lib.mwb_regions_workspace_bytes(tiles_bound, s_n)), dtype=torch.uint8, device=dev)
+        ws = torch.empty(int(lib.mwb_regions_workspace_bytes(s_n)), dtype=torch.uint8, device=dev)
         totals = torch.zeros(2, dtype=torch.int32, device=dev)
-        nat.call("mwb_enumerate_regions_count", nx, ny, regions.data_ptr(), s_n, tiles_bound,
-                 self.mask_t.data_ptr(), self.d, totals.data_ptr(), ws.data_ptr(), stream)
-        n_pts, n_tiles = (int(v) for v in totals.cpu().tolist())  # host sync 2 of 2: packed list size
+        nat.call("mwb_enumerate_regions_count", nx, ny, regions.data_ptr(), s_n, self.mask_t.data_ptr(), self.d,
+                 totals.data_ptr(), ws.data_ptr(), stream)
+        n_pts, n_tiles = (int(v) for v in totals.cpu().tolist())  # the one host sync: packed list size
         if n_pts > 0:
             f_pts = torch.empty((n_pts, 3), dtype=torch.float64, device=dev)
             f_idx = torch.empty(n_pts, dtype=torch.int32, device=dev)
             tile_info = torch.empty((n_tiles, 2), dtype=torch.int32, device=dev)
             nat.call("mwb_enumerate_regions_write", grid.origin[0], grid.origin[1], grid.resolution, nx, ny,
-                     regions.data_ptr(), s_n, tiles_bound, self.mask_t.data_ptr(), self.d, f_pts.data_ptr(),
-                     f_idx.data_ptr(), tile_info.data_ptr(), ws.data_ptr(), stream)
+                     regions.data_ptr(), s_n, self.mask_t.data_ptr(), self.d, f_pts.data_ptr(), f_idx.data_ptr(),
+                     tile_info.data_ptr(), ws.data_ptr(), stream)
             f_table = torch.empty(int(lib.mwb_delay_table_bytes(n_pts, self.n_chan)), dtype=torch.uint8, device=dev)
             nat.call("mwb_delay_table_tiles", f_pts.data_ptr(), n_pts, tile_info.data_ptr(), sc.chan.data_ptr(),
                      self.n_chan, sc.ant.data_ptr(), sc.n_ant, sc.inv_scale, self.interp, f_table.data_ptr(), stream)
@@ -190,8 +187,7 @@ class FrameworkBatch:
                      None if das else dense.data_ptr(), nx * ny, keys.data_ptr() if das else None,
                      None if das else keys.data_ptr(), flags.data_ptr(), 0, stream)
         ev[3].record()
-        counts_off = 2 * s_n * tiles_bound  # scan_counts in the region workspace
-        fine_counts = ws.view(torch.int32)[counts_off : counts_off + s_n].cpu().numpy().astype(np.int64)
+        fine_counts = ws.view(torch.int32)[:s_n].cpu().numpy().astype(np.int64)
         if int(flags.item()) & 1:
             raise ValueError("energy map contains non-finite values")
         reg = regions.cpu().numpy()
