@@ -1142,50 +1142,69 @@ __device__ __forceinline__ void put_box(int32_t* dst, const Box& b) {
 // One select_roi decision (coarse2fine.py:207-252) from the children's and
 // expansions' statistics: scores (variance on the first iteration, Eq. (5)
 // after), np.argmax, the n_min stop, W/B of the previous vs the new selection
-// and the record.  Run by one thread; returns the termination code and, when
-// the loop goes on, nxt = {W, B, n, sum, m2} of the new selection.
+// and the record.  Called by all 32 lanes of one warp: lane k scores child k
+// and writes its record fields, the argmax is a shuffle reduction, lane 0
+// does W/B.  Returns the termination code (every lane); lane 0 writes, when
+// the loop goes on, nxt = {W, B, n, sum, m2} of the new selection and next_sel.
 template <int NK>
 __device__ int select_score(const SelectParams& p, mwb_trace_t* tr, int iteration, int nk, const Box* rg,
                             const double* cnt, const double* sums, const double* mean, const double* m2,
                             double n_sel, double sum_sel, double m2_sel, double sigma_prev_sq, bool have_prev,
                             double prev_w, double prev_b, double* nxt, Box* next_sel) {
+  const int lane = threadIdx.x & 31;
   const int rec_i = iteration;
-  mwb_iter_record_t rec;
-  memset(&rec, 0, sizeof(rec));
-  rec.n_children = nk;
-  double scores[NK];
-  for (int k = 0; k < nk; ++k) {
-    rec.counts[k] = (int)cnt[k];
-    if (cnt[k] == 0.0) {
-      scores[k] = -INFINITY;  // empty child (coarse2fine.py:215-217)
-      rec.has_stats[k] = 0;
-    } else {
-      const double mu = mean[k], var = m2[k] / cnt[k];
-      rec.mu[k] = mu;
-      rec.var[k] = var;
+  mwb_iter_record_t* rec = rec_i < MWB_MAX_ITERS ? &tr->records[rec_i] : nullptr;
+  // the record's fields go straight to global memory; entries past
+  // n_children and unset delta fields are zero
+  const int k = lane;
+  int has = 0, clamped = 0, count = 0;
+  double mu = 0.0, var = 0.0, dr = 0.0, dl = 0.0, sc = -INFINITY;
+  if (k < nk) {
+    count = (int)cnt[k];
+    if (cnt[k] != 0.0) {  // else an empty child: -inf (coarse2fine.py:215-217)
+      mu = mean[k];
+      var = m2[k] / cnt[k];
       if (iteration == 0) {  // first iteration scores by variance (218-220)
-        scores[k] = var;
-        rec.has_stats[k] = 1;
+        sc = var;
+        has = 1;
       } else {  // Eq. (5) (_metric_parts, 67-91)
-        rec.has_stats[k] = 2;
+        has = 2;
         if (var == 0.0) {
-          scores[k] = mu;
+          sc = mu;
         } else {
-          const double dr = __ddiv_rn(__dsub_rn(var, sigma_prev_sq), var);
-          const double dl = fmin(fmax(dr, 0.0), 1.0);
-          scores[k] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, dl), mu), __dmul_rn(dl, var));
-          rec.delta_raw[k] = dr;
-          rec.delta[k] = dl;
-          rec.clamped[k] = dl != dr;
+          dr = __ddiv_rn(__dsub_rn(var, sigma_prev_sq), var);
+          dl = fmin(fmax(dr, 0.0), 1.0);
+          sc = __dadd_rn(__dmul_rn(__dsub_rn(1.0, dl), mu), __dmul_rn(dl, var));
+          clamped = dl != dr;
         }
       }
     }
-    rec.scores[k] = scores[k];
   }
-  int selq = 0;  // np.argmax: first maximum
-  for (int k = 1; k < nk; ++k)
-    if (scores[k] > scores[selq]) selq = k;
-  if (rec.counts[selq] < p.n_min) return MWB_TERM_N_MIN;
+  if (rec && k < MWB_MAX_CHILDREN) {
+    rec->counts[k] = count;
+    rec->has_stats[k] = has;
+    rec->clamped[k] = clamped;
+    rec->scores[k] = k < nk ? sc : 0.0;
+    rec->mu[k] = mu;
+    rec->var[k] = var;
+    rec->delta_raw[k] = dr;
+    rec->delta[k] = dl;
+  }
+  // np.argmax (first maximum): the larger score wins, ties go to the lower index
+  double best = sc;
+  int selq = k < nk ? k : 0x7FFF, selc = count;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oq = __shfl_xor_sync(0xffffffffu, selq, o), oc = __shfl_xor_sync(0xffffffffu, selc, o);
+    if (ob > best || (ob == best && oq < selq)) {
+      best = ob;
+      selq = oq;
+      selc = oc;
+    }
+  }
+  if (selq >= nk) selq = 0;  // every score -inf: argmax returns 0
+  if ((selq == 0 ? (int)cnt[0] : selc) < p.n_min) return MWB_TERM_N_MIN;
   const int e = nk + selq;
   const double n_e = cnt[e], sum_e = sums[e], m2_e = m2[e];
   // W, B of the previous vs the new selection (class_distances, 94-109)
@@ -1195,20 +1214,24 @@ __device__ int select_score(const SelectParams& p, mwb_trace_t* tr, int iteratio
   const double da = __dsub_rn(ma, grand), db = __dsub_rn(mb, grand);
   const double b = __dadd_rn(__dmul_rn(n_sel, __dmul_rn(da, da)), __dmul_rn(n_e, __dmul_rn(db, db)));
   const bool satisfied = !have_prev || (b > prev_b || w < prev_w);  // OR (235)
-  rec.iteration = iteration + 1;
-  rec.selected = selq;
-  rec.satisfied = satisfied;
-  put_box(rec.selected_region, rg[selq]);
-  put_box(rec.expanded_region, rg[e]);
-  rec.w = w;
-  rec.b = b;
-  if (rec_i < MWB_MAX_ITERS) tr->records[rec_i] = rec;
-  nxt[0] = w;
-  nxt[1] = b;
-  nxt[2] = n_e;
-  nxt[3] = sum_e;
-  nxt[4] = m2_e;
-  *next_sel = rg[e];
+  if (lane == 0) {
+    if (rec) {
+      rec->iteration = iteration + 1;
+      rec->n_children = nk;
+      rec->selected = selq;
+      rec->satisfied = satisfied;
+      put_box(rec->selected_region, rg[selq]);
+      put_box(rec->expanded_region, rg[e]);
+      rec->w = w;
+      rec->b = b;
+    }
+    nxt[0] = w;
+    nxt[1] = b;
+    nxt[2] = n_e;
+    nxt[3] = sum_e;
+    nxt[4] = m2_e;
+    *next_sel = rg[e];
+  }
   return rec_i >= MWB_MAX_ITERS ? MWB_TERM_OVERFLOW : (satisfied ? MWB_TERM_NONE : MWB_TERM_DISTANCE);
 }
 
@@ -1363,9 +1386,11 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
     for (int k = 0; k < 2 * NK; ++k) m2[k] = res[k];
     __syncthreads();
 
-    if (threadIdx.x == 0)
-      ctl[0] = select_score<NK>(p, tr, iteration, nk, rg, cnt, sums, mean, m2, n_sel, sum_sel, m2_sel,
-                                sigma_prev_sq, have_prev, prev_w, prev_b, red, &next_sel);
+    if (threadIdx.x < 32) {
+      const int t = select_score<NK>(p, tr, iteration, nk, rg, cnt, sums, mean, m2, n_sel, sum_sel, m2_sel,
+                                     sigma_prev_sq, have_prev, prev_w, prev_b, red, &next_sel);
+      if (threadIdx.x == 0) ctl[0] = t;
+    }
     __syncthreads();
     term = ctl[0];
     if (term == MWB_TERM_N_MIN) break;
@@ -1403,6 +1428,7 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
 // ----------------------------------------------------------------------------
 constexpr int SEL_WPB = 4;
 constexpr int SEL_WARP_STAGE = 4096;
+constexpr int SEL_SPLIT_MAX_SCANS = 148;  // below a wave of scans, a CTA of 8 warps per scan
 
 struct SelWarpCtl {
   double nxt[5];
@@ -1422,7 +1448,10 @@ __device__ __forceinline__ int warp_sum_i(int x) {
 }
 
 // f(lx, ly, v) for every valid cell of box r; lattice cells are i = lane + 32k
-// of the r-lattice in row-major order, advanced incrementally
+// of the r-lattice in row-major order, advanced incrementally.  Each lane
+// loads its next SEL_U cells before visiting them in order, so the shared-
+// memory latency overlaps while every accumulator sees the same sequence.
+constexpr int SEL_U = 4;
 template <class F>
 __device__ __forceinline__ void warp_cells(const float* sv, int sLy, int sl0x, int sl0y, int D, const Box& r,
                                            F&& f) {
@@ -1434,37 +1463,63 @@ __device__ __forceinline__ void warp_cells(const float* sv, int sLy, int sl0x, i
   const int q = 32 / Ly, rr = 32 - q * Ly;
   int lx = lane / Ly, ly = lane - lx * Ly;
   const float* base = sv + (l0x - sl0x) * sLy + (l0y - sl0y);
-  for (int i = lane; i < n; i += 32) {
-    const float v = base[lx * sLy + ly];
-    if (v == v) f(l0x + lx, l0y + ly, (double)v);
-    lx += q;
-    ly += rr;
-    if (ly >= Ly) {
-      ly -= Ly;
-      ++lx;
+  for (int i0 = lane; i0 < n; i0 += 32 * SEL_U) {
+    float v[SEL_U];
+    int cx[SEL_U], cy[SEL_U];
+#pragma unroll
+    for (int u = 0; u < SEL_U; ++u) {
+      cx[u] = lx;
+      cy[u] = ly;
+      const bool in = i0 + 32 * u < n;
+      const float x = base[in ? lx * sLy + ly : 0];  // unconditional load: no branch per cell
+      v[u] = in ? x : __int_as_float(0x7fc00000);
+      lx += q;
+      ly += rr;
+      if (ly >= Ly) {
+        ly -= Ly;
+        ++lx;
+      }
     }
+#pragma unroll
+    for (int u = 0; u < SEL_U; ++u)
+      if (v[u] == v[u]) f(l0x + cx[u], l0y + cy[u], v[u]);
   }
 }
 
-__global__ void __launch_bounds__(SEL_WPB * 32) select_roi_warp_kernel(const SelectParams p, int n_scans) {
+// SPLIT = false: SEL_WPB scans per CTA, one warp each (batches).
+// SPLIT = true:  one scan per CTA of SEL_SPLIT_WARPS warps (single scans: a
+//   lone warp is latency bound).  Every warp walks the same cells in the same
+//   lane order, but in the iteration passes warp k accumulates only box k, so
+//   each box's sum sees exactly the additions of the one-warp kernel and the
+//   two modes agree bit for bit.
+constexpr int SEL_SPLIT_WARPS = 8;
+
+template <bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? SEL_SPLIT_WARPS * 32 : SEL_WPB * 32)
+    select_roi_warp_kernel(const SelectParams p, int n_scans) {
+  constexpr int NT = SPLIT ? SEL_SPLIT_WARPS * 32 : 32;  // threads sharing one scan
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = blockIdx.x * SEL_WPB + warp;
+  const int s = SPLIT ? (int)blockIdx.x : (int)blockIdx.x * SEL_WPB + warp;
   if (s >= n_scans) return;
   extern __shared__ float smem_sel[];
   __shared__ SelWarpCtl wctl[SEL_WPB];
-  SelWarpCtl& wc = wctl[warp];
+  __shared__ double box_stat[2][8];  // SPLIT: per-box sums / m2 from the owning warp
+  __shared__ int box_cnt[8];
+  SelWarpCtl& wc = wctl[SPLIT ? 0 : warp];
   const int D = p.D, sLx = p.sL[0], sLy = p.sL[1], sl0x = p.sl0[0], sl0y = p.sl0[1];
   const int nst = sLx * sLy;
-  float* sv = smem_sel + warp * nst;
+  float* sv = smem_sel + (SPLIT ? 0 : warp * nst);
   const float* dense = p.dense + (size_t)s * p.dense_stride;
   int32_t* region_out = p.region_out + 6 * s;
   mwb_trace_t* tr = p.trace + s;
+  const int tid = SPLIT ? (int)threadIdx.x : lane;
+  const bool leader = tid == 0;
 
-  {  // stage the breast box's lattice: both loads independent, 4 in flight per lane
-    int lx = lane / sLy, ly = lane - lx * sLy;
-    const int q = 32 / sLy, rr = 32 - q * sLy;
-#pragma unroll 4
-    for (int i = lane; i < nst; i += 32) {
+  {  // stage the breast box's lattice: both loads independent, 8 in flight per thread
+    int lx = tid / sLy, ly = tid - lx * sLy;
+    const int q = NT / sLy, rr = NT - q * sLy;
+#pragma unroll 8
+    for (int i = tid; i < nst; i += NT) {
       const size_t slot = (size_t)(sl0x + lx) * D * p.ny + (size_t)(sl0y + ly) * D;
       const float v = __ldg(dense + slot);
       const uint8_t ok = __ldg(p.valid + slot);
@@ -1477,28 +1532,33 @@ __global__ void __launch_bounds__(SEL_WPB * 32) select_roi_warp_kernel(const Sel
       }
     }
   }
-  __syncwarp();
+  if (SPLIT)
+    __syncthreads();
+  else
+    __syncwarp();
 
-  // breast-region stats: count, sum, min, max, then the two-pass m2 (coarse2fine.py:186-199)
+  // breast-region stats: count, sum, min, max, then the two-pass m2
+  // (coarse2fine.py:186-199); SPLIT warps all compute them (identically)
   double n_sel, sum_sel, m2_sel;
   {
     int c = 0;
-    double sm = 0.0, mn = INFINITY, mx = -INFINITY;
-    warp_cells(sv, sLy, sl0x, sl0y, D, p.breast, [&](int, int, double v) {
+    double sm = 0.0;
+    float mn = INFINITY, mx = -INFINITY;  // exact in fp32: the values are fp32
+    warp_cells(sv, sLy, sl0x, sl0y, D, p.breast, [&](int, int, float v) {
       ++c;
-      sm += v;
-      mn = fmin(mn, v);
-      mx = fmax(mx, v);
+      sm += (double)v;
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
     });
     n_sel = (double)warp_sum_i(c);
     sum_sel = warp_sum_d(sm);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
     if (n_sel == 0.0 || mx == mn) {
-      if (lane == 0) {
+      if (leader) {
         tr->termination = n_sel == 0.0 ? MWB_TERM_EMPTY : MWB_TERM_DEGENERATE;
         tr->n_records = 0;
         put_box(tr->final_region, p.breast);
@@ -1508,9 +1568,9 @@ __global__ void __launch_bounds__(SEL_WPB * 32) select_roi_warp_kernel(const Sel
     }
     const double mean = sum_sel / n_sel;
     double d2 = 0.0;
-    warp_cells(sv, sLy, sl0x, sl0y, D, p.breast, [&](int, int, double v) {
-      const double d = v - mean;
-      d2 += d * d;
+    warp_cells(sv, sLy, sl0x, sl0y, D, p.breast, [&](int, int, float v) {
+      const double d = (double)v - mean;
+      d2 = __fma_rn(d, d, d2);
     });
     m2_sel = warp_sum_d(d2);
   }
@@ -1538,58 +1598,110 @@ __global__ void __launch_bounds__(SEL_WPB * 32) select_roi_warp_kernel(const Sel
     const int ex1l = (rg[5].lo[0] + D - 1) / D, ex1h = rg[5].hi[0] / D;
     const int ey0l = (rg[4].lo[1] + D - 1) / D, ey0h = rg[4].hi[1] / D;
     const int ey1l = (rg[6].lo[1] + D - 1) / D, ey1h = rg[6].hi[1] / D;
+    double cnt[8], sums[8], mean[8], m2[8];
 
-    // pass 1: count and sum of every child and of every child's expansion
-    int ci[8];
-    double a1[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      ci[k] = 0;
-      a1[k] = 0.0;
-    }
-    warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, double v) {
-      const int kc = (lx > mxl) | ((ly > myl) << 1);
-      const bool x0 = ex0l <= lx && lx <= ex0h, x1 = ex1l <= lx && lx <= ex1h;
-      const bool y0 = ey0l <= ly && ly <= ey0h, y1 = ey1l <= ly && ly <= ey1h;
-      const bool in[8] = {kc == 0, kc == 1, kc == 2, kc == 3, x0 && y0, x1 && y0, x0 && y1, x1 && y1};
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (in[k]) {
-          ++ci[k];
-          a1[k] += v;
+    if constexpr (SPLIT) {
+      // warp k owns box k: the same membership tests as below, as one rectangle
+      const int k = warp;
+      const bool xhi = k < 4 ? (k & 1) : false, yhi = k < 4 ? (k >> 1) & 1 : false;
+      const int rx0 = k < 4 ? (xhi ? mxl + 1 : INT_MIN) : ((k - 4) & 1 ? ex1l : ex0l);
+      const int rx1 = k < 4 ? (xhi ? INT_MAX : mxl) : ((k - 4) & 1 ? ex1h : ex0h);
+      const int ry0 = k < 4 ? (yhi ? myl + 1 : INT_MIN) : ((k - 4) >> 1 ? ey1l : ey0l);
+      const int ry1 = k < 4 ? (yhi ? INT_MAX : myl) : ((k - 4) >> 1 ? ey1h : ey0h);
+      int ci = 0;
+      double a1 = 0.0;
+      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
+        const double v = fv;
+        if (rx0 <= lx && lx <= rx1 && ry0 <= ly && ly <= ry1) {
+          ++ci;
+          a1 += v;
         }
-    });
-    double cnt[8], sums[8], mean[8];
+      });
+      ci = warp_sum_i(ci);
+      a1 = warp_sum_d(a1);
+      if (lane == 0) {
+        box_cnt[k] = ci;
+        box_stat[0][k] = a1;
+      }
+      __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      cnt[k] = (double)warp_sum_i(ci[k]);
-      sums[k] = warp_sum_d(a1[k]);
-      mean[k] = cnt[k] > 0.0 ? sums[k] / cnt[k] : 0.0;
-    }
-    // pass 2: sum of (x - mean)^2 (two-pass variance, as numpy's var)
-    double a2[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a2[k] = 0.0;
-    warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, double v) {
-      const int kc = (lx > mxl) | ((ly > myl) << 1);
-      const bool x0 = ex0l <= lx && lx <= ex0h, x1 = ex1l <= lx && lx <= ex1h;
-      const bool y0 = ey0l <= ly && ly <= ey0h, y1 = ey1l <= ly && ly <= ey1h;
-      const bool in[8] = {kc == 0, kc == 1, kc == 2, kc == 3, x0 && y0, x1 && y0, x0 && y1, x1 && y1};
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (in[k]) {
-          const double d = v - mean[k];
-          a2[k] += d * d;
+      for (int j = 0; j < 8; ++j) {
+        cnt[j] = (double)box_cnt[j];
+        sums[j] = box_stat[0][j];
+        mean[j] = cnt[j] > 0.0 ? sums[j] / cnt[j] : 0.0;
+      }
+      double a2 = 0.0;
+      const double mu = mean[k];
+      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
+        const double v = fv;
+        if (rx0 <= lx && lx <= rx1 && ry0 <= ly && ly <= ry1) {
+          const double d = v - mu;
+          a2 = __fma_rn(d, d, a2);  // explicit: both modes round alike
         }
-    });
-    double m2[8];
+      });
+      a2 = warp_sum_d(a2);
+      if (lane == 0) box_stat[1][k] = a2;
+      __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 8; ++k) m2[k] = warp_sum_d(a2[k]);
+      for (int j = 0; j < 8; ++j) m2[j] = box_stat[1][j];
+    } else {
+      // pass 1: count and sum of every child and of every child's expansion
+      int ci[8];
+      double a1[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        ci[k] = 0;
+        a1[k] = 0.0;
+      }
+      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
+        const double v = fv;
+        const int kc = (lx > mxl) | ((ly > myl) << 1);
+        const bool x0 = ex0l <= lx && lx <= ex0h, x1 = ex1l <= lx && lx <= ex1h;
+        const bool y0 = ey0l <= ly && ly <= ey0h, y1 = ey1l <= ly && ly <= ey1h;
+        const bool in[8] = {kc == 0, kc == 1, kc == 2, kc == 3, x0 && y0, x1 && y0, x0 && y1, x1 && y1};
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (in[k]) {
+            ++ci[k];
+            a1[k] += v;
+          }
+      });
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        cnt[k] = (double)warp_sum_i(ci[k]);
+        sums[k] = warp_sum_d(a1[k]);
+        mean[k] = cnt[k] > 0.0 ? sums[k] / cnt[k] : 0.0;
+      }
+      // pass 2: sum of (x - mean)^2 (two-pass variance, as numpy's var)
+      double a2[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a2[k] = 0.0;
+      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
+        const double v = fv;
+        const int kc = (lx > mxl) | ((ly > myl) << 1);
+        const bool x0 = ex0l <= lx && lx <= ex0h, x1 = ex1l <= lx && lx <= ex1h;
+        const bool y0 = ey0l <= ly && ly <= ey0h, y1 = ey1l <= ly && ly <= ey1h;
+        const bool in[8] = {kc == 0, kc == 1, kc == 2, kc == 3, x0 && y0, x1 && y0, x0 && y1, x1 && y1};
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (in[k]) {
+            const double d = v - mean[k];
+            a2[k] = __fma_rn(d, d, a2[k]);
+          }
+      });
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m2[k] = warp_sum_d(a2[k]);
+    }
 
-    if (lane == 0)
-      wc.term = select_score<4>(p, tr, iteration, nk, rg, cnt, sums, mean, m2, n_sel, sum_sel, m2_sel,
-                                sigma_prev_sq, have_prev, prev_w, prev_b, wc.nxt, &wc.next);
-    __syncwarp();
+    if (!SPLIT || warp == 0) {
+      const int t = select_score<4>(p, tr, iteration, nk, rg, cnt, sums, mean, m2, n_sel, sum_sel, m2_sel,
+                                    sigma_prev_sq, have_prev, prev_w, prev_b, wc.nxt, &wc.next);
+      if (lane == 0) wc.term = t;
+    }
+    if (SPLIT)
+      __syncthreads();
+    else
+      __syncwarp();
     term = wc.term;
     if (term == MWB_TERM_N_MIN) break;
     iteration += 1;
@@ -1602,9 +1714,12 @@ __global__ void __launch_bounds__(SEL_WPB * 32) select_roi_warp_kernel(const Sel
     m2_sel = wc.nxt[4];
     sigma_prev_sq = m2_sel / n_sel;
     sel = wc.next;
-    __syncwarp();
+    if (SPLIT)
+      __syncthreads();
+    else
+      __syncwarp();
   }
-  if (lane == 0) {
+  if (leader) {
     tr->termination = term;
     tr->n_records = min(iteration, MWB_MAX_ITERS);
     put_box(tr->final_region, sel);
@@ -2557,12 +2672,17 @@ static int select_common(SelectParams& p, void* stream, int n_scans = 1) {
   }
   p.staged = n > 0 && n <= SEL_STAGE_MAX;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (p.dims == 2 && n > 0 && n <= SEL_WARP_STAGE) {  // warp per scan (K2w)
-    const size_t smw = sizeof(float) * (size_t)n * SEL_WPB;
-    cudaError_t e = cudaFuncSetAttribute(select_roi_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (p.dims == 2 && n > 0 && n <= SEL_WARP_STAGE) {  // K2w: warp per scan, or one warp per box
+    const bool split = n_scans < SEL_SPLIT_MAX_SCANS;
+    void (*wk)(SelectParams, int) = split ? select_roi_warp_kernel<true> : select_roi_warp_kernel<false>;
+    const size_t smw = sizeof(float) * (size_t)n * (split ? 1 : SEL_WPB);
+    cudaError_t e = cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(sizeof(float) * SEL_WARP_STAGE * SEL_WPB));
     if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    select_roi_warp_kernel<<<(n_scans + SEL_WPB - 1) / SEL_WPB, SEL_WPB * 32, smw, st>>>(p, n_scans);
+    if (split)
+      wk<<<n_scans, SEL_SPLIT_WARPS * 32, smw, st>>>(p, n_scans);
+    else
+      wk<<<(n_scans + SEL_WPB - 1) / SEL_WPB, SEL_WPB * 32, smw, st>>>(p, n_scans);
     return check_launch("select_roi_warp_kernel");
   }
   const size_t sm = p.staged ? sizeof(float) * (size_t)n : 0;
