@@ -340,10 +340,32 @@ struct TableParams {
 // advances one tile row per channel (no per-word index arithmetic), the
 // interpolation mode is a template parameter (no if-converted rint on the
 // linear path), and four channels per thread in flight hide fp64 latency.
+//
+// Linear words skip split_delay_q's [0, 2^30] clamp: this loop only runs for
+// non-wide tiles, where every finite point's i0 lies in the tile's span
+// [lo, hi] (within [0, 2^30]); a NaN point converts to 0 or INT64_MIN, either
+// way i0 = 0, fq = 0, as after the clamp.  q = floor(n 2^23) comes from one
+// DMUL by inv_scale * 2^23 (power-of-two scaling commutes with rounding).
 template <bool NEAREST>
 __device__ __forceinline__ void table_words(uint32_t* wp, const unsigned char* da, const int2* coff, const int* lo,
                                             int C, double inv_scale) {
   const int interp = NEAREST ? MWB_INTERP_NEAREST : MWB_INTERP_LINEAR;
+  if (!NEAREST) {
+    const double inv23 = __dmul_rn(inv_scale, 8388608.0);
+#pragma unroll 4
+    for (int c = 0; c < C; ++c, wp += TILE) {
+      const int2 o = coff[c];
+      const double* ta = reinterpret_cast<const double*>(da + o.x);
+      const double* ra = reinterpret_cast<const double*>(da + o.y);
+      const long long va = __double2ll_rd(__dmul_rn(__dadd_rn(ta[0], ra[0]), inv23));
+      const long long vb = __double2ll_rd(__dmul_rn(__dadd_rn(ta[TPB], ra[TPB]), inv23));
+      const int l = lo[c];
+      const int ia = static_cast<int>(va >> 23), ib = static_cast<int>(vb >> 23);
+      wp[0] = ((uint32_t)min(max(ia - l, 0), SPAN_MAX) << 23) | (static_cast<uint32_t>(va) & 0x7FFFFFu);
+      wp[TPB] = ((uint32_t)min(max(ib - l, 0), SPAN_MAX) << 23) | (static_cast<uint32_t>(vb) & 0x7FFFFFu);
+    }
+    return;
+  }
 #pragma unroll 4
   for (int c = 0; c < C; ++c, wp += TILE) {
     const int2 o = coff[c];
