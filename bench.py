@@ -300,6 +300,14 @@ def other_configs() -> dict:
         t = med_ms(lambda: fb.run(sig2), reps=5)
         out[f"cfg2_framework_batch_4096_{kind}"] = {"ms": t, "segmented_images_per_s": 4096 / (t * 1e-3)}
         del fb
+    # the BASELINE segmentation rule for the same 4096 scans (SegmentBatch)
+    from paper_1709_02549_b200.segment import SegmentBatch
+
+    for kind in ("das", "dmas"):
+        sb = SegmentBatch(m2.geometry(), m2.pairs(), m2.n_samples, g2, kind, 16, 0.01, window=(m2.k0, 32))
+        t = med_ms(lambda: sb.run(sig2), reps=5)
+        out[f"cfg2_segment_batch_4096_{kind}"] = {"ms": t, "segmented_images_per_s": 4096 / (t * 1e-3)}
+        del sb
     del sig2
     vm = synth.VolumeModel()
     sig, _ = synth.scan_3d(vm, seed=9)

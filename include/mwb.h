@@ -270,6 +270,25 @@ int mwb_segment(const float* sig, int n_chan, int ld, int n_samples, const int32
                 float* lowres, mwb_seg_trace_t* d_trace, void* workspace, void* stream);
 
 /*
+ * mwb_segment for S scans [S][n_chan][ld] (scan_stride floats apart) that
+ * share the antenna geometry, grid and start region: each scan runs its own
+ * quadrant search, all scans advancing together (four launches per iteration
+ * for the whole batch; finished scans add no work).  Outputs per scan s:
+ * d_regions_out[6 s..], d_traces[s] and, if lowres != NULL, the (2 n_sub)^2
+ * low-resolution image at lowres + s (2 n_sub)^2.  Every value equals what
+ * mwb_segment returns for that scan alone (same routines, same order).
+ * Replaces a per-scan loop over mwb_segment (no reference counterpart; see
+ * mwb_segment).
+ */
+int64_t mwb_segment_batch_workspace_bytes(int n_scans, int n_sub, int n_chan);
+int mwb_segment_batch(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
+                      int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
+                      double inv_scale, int interp, int k0, int window, int kind, double ox,
+                      double oy, double res, int nx, int ny, int x0, int y0, int x1, int y1,
+                      int n_sub, int stop_cells, int max_iters, int32_t* d_regions_out,
+                      float* lowres, mwb_seg_trace_t* d_traces, void* workspace, void* stream);
+
+/*
  * Device-side scan synthesis (the input producer of the path): writes S scans
  * [S][n_chan][ld] fp32 (samples >= n_samples zero) for point scatterers
  * scatterers[S][n_scat][4] = {x, y, z, amplitude}.  model 0 = the reference

@@ -1862,13 +1862,12 @@ struct SegState {
   int iter;
 };
 
-// sub-grid points of the 4 quadrants of the current region (fp64 centres):
-// x = ox + x0*res + (i + 0.5) * (w*res / n_sub), likewise y
-__global__ void seg_points_kernel(SegState* st, double ox, double oy, double res, int n_sub, double* pts) {
-  if (st->done) return;
+// point t of the 4 sub-grids of the current region (fp64 centres):
+// x = ox + x0*res + (i + 0.5) * (w*res / n_sub), likewise y.  Shared by the
+// single-scan and batched searches, so both place every point bit-identically.
+__device__ __forceinline__ void seg_point(const SegState* st, double ox, double oy, double res, int n_sub, int t,
+                                          double* pts) {
   const int per = n_sub * n_sub;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 4 * per) return;
   Box r;
   for (int a = 0; a < 3; ++a) {
     r.lo[a] = st->region[a];
@@ -1886,10 +1885,35 @@ __global__ void seg_points_kernel(SegState* st, double ox, double oy, double res
   pts[3 * (size_t)t + 2] = 0.0;
 }
 
+__global__ void seg_points_kernel(SegState* st, double ox, double oy, double res, int n_sub, double* pts) {
+  if (st->done) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 4 * n_sub * n_sub) return;
+  seg_point(st, ox, oy, res, n_sub, t, pts);
+}
+
+// Batched search: scan s owns points [s * per_scan, (s + 1) * per_scan) of the
+// packed list (per_scan = 4 n_sub^2 rounded up to whole 256-point tiles).
+// tile_info[t] = {s, valid points}; a finished scan's tiles get 0 valid points,
+// so the table and energy launches skip them.  grid = (tiles per scan, S).
+__global__ void __launch_bounds__(256) seg_points_batch_kernel(const SegState* st, int per_scan, double ox, double oy,
+                                                               double res, int n_sub, double* pts, int2* tile_info) {
+  const int s = blockIdx.y;
+  const int n = 4 * n_sub * n_sub;
+  const int t = blockIdx.x * TILE + threadIdx.x;
+  const bool done = st[s].done != 0;
+  if (threadIdx.x == 0)
+    tile_info[(size_t)s * (per_scan / TILE) + blockIdx.x] = make_int2(s, done ? 0 : min(TILE, n - (int)blockIdx.x * TILE));
+  if (done || t >= n) return;
+  seg_point(st + s, ox, oy, res, n_sub, t, pts + 3 * (size_t)s * per_scan);
+}
+
 // score the 4 quadrants (max/mean, DMAS shifted by the iteration minimum),
 // keep the argmax (ties -> lowest index), shrink the region, record the trace
-__global__ void __launch_bounds__(256) seg_score_kernel(SegState* st, const float* e, int n_sub, int shift_min,
-                                                         int stop_cells, float* lowres, mwb_seg_trace_t* tr) {
+// (one 256-thread CTA per search; the batched kernel runs this same body per
+// scan, so its decisions and trace are bit-identical to the single-scan search)
+__device__ __forceinline__ void seg_score(SegState* st, const float* e, int n_sub, int shift_min, int stop_cells,
+                                          float* lowres, mwb_seg_trace_t* tr) {
   __shared__ double red[8][12];
   __shared__ double fin[12];
   if (st->done) return;
@@ -1985,7 +2009,23 @@ __global__ void __launch_bounds__(256) seg_score_kernel(SegState* st, const floa
   }
 }
 
-__global__ void seg_init_kernel(SegState* st, int x0, int y0, int x1, int y1, int stop_cells, mwb_seg_trace_t* tr) {
+__global__ void __launch_bounds__(256) seg_score_kernel(SegState* st, const float* e, int n_sub, int shift_min,
+                                                         int stop_cells, float* lowres, mwb_seg_trace_t* tr) {
+  seg_score(st, e, n_sub, shift_min, stop_cells, lowres, tr);
+}
+
+// one CTA per scan; e holds per_scan energies per scan
+__global__ void __launch_bounds__(256) seg_score_batch_kernel(SegState* st, const float* e, int per_scan, int n_sub,
+                                                               int shift_min, int stop_cells, float* lowres,
+                                                               mwb_seg_trace_t* tr) {
+  const int s = blockIdx.x;
+  const int lw = 4 * n_sub * n_sub;
+  seg_score(st + s, e + (size_t)s * per_scan, n_sub, shift_min, stop_cells, lowres ? lowres + (size_t)s * lw : nullptr,
+            tr + s);
+}
+
+__device__ __forceinline__ void seg_init(SegState* st, int x0, int y0, int x1, int y1, int stop_cells,
+                                         mwb_seg_trace_t* tr) {
   st->region[0] = x0; st->region[1] = y0; st->region[2] = 0;
   st->region[3] = x1; st->region[4] = y1; st->region[5] = 0;
   st->iter = 0;
@@ -1996,8 +2036,24 @@ __global__ void seg_init_kernel(SegState* st, int x0, int y0, int x1, int y1, in
   for (int a = 0; a < 6; ++a) tr->final_region[a] = st->region[a];
 }
 
+__global__ void seg_init_kernel(SegState* st, int x0, int y0, int x1, int y1, int stop_cells, mwb_seg_trace_t* tr) {
+  seg_init(st, x0, y0, x1, y1, stop_cells, tr);
+}
+
 __global__ void seg_region_kernel(const SegState* st, int32_t* region_out) {
   for (int a = 0; a < 6; ++a) region_out[a] = st->region[a];
+}
+
+__global__ void seg_init_batch_kernel(SegState* st, int n_scans, int x0, int y0, int x1, int y1, int stop_cells,
+                                      mwb_seg_trace_t* tr) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n_scans) seg_init(st + s, x0, y0, x1, y1, stop_cells, tr + s);
+}
+
+__global__ void seg_region_batch_kernel(const SegState* st, int n_scans, int32_t* region_out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n_scans)
+    for (int a = 0; a < 6; ++a) region_out[6 * (size_t)s + a] = st[s].region[a];
 }
 
 __global__ void argmax_dense_kernel(const float* dense, const uint8_t* valid, int n,
@@ -2875,6 +2931,74 @@ int mwb_segment(const float* sig, int n_chan, int ld, int n_samples, const int32
   }
   seg_region_kernel<<<1, 1, 0, cs>>>(st, d_region_out);
   return check_launch("seg_region_kernel");
+}
+
+// Batched configs[2] search: S scans of one geometry, grid and start region,
+// each with its own quadrant sequence.  Every iteration is four launches for
+// the whole batch (points + tile list, delay table, energies, scores); a scan
+// that has finished contributes empty tiles.  Per scan, every value equals
+// mwb_segment's (same point placement, table words, energy routine and
+// scoring body).
+static long long seg_batch_per_scan(int n_sub) {
+  const long long n = 4LL * n_sub * n_sub;
+  return (n + TILE - 1) / TILE * TILE;
+}
+
+int64_t mwb_segment_batch_workspace_bytes(int n_scans, int n_sub, int n_chan) {
+  if (n_scans < 1 || n_scans > 65535 || n_sub < 1 || n_sub > 64 || n_chan < 1) return -1;
+  const long long per = seg_batch_per_scan(n_sub), n = per * n_scans;
+  return (long long)align_up(sizeof(SegState) * (size_t)n_scans, 256) + (long long)align_up(24 * n, 256) +
+         (long long)align_up(4 * n, 256) + (long long)align_up(8 * (n / TILE), 256) +
+         (long long)table_layout(n / TILE, n_chan).total;
+}
+
+int mwb_segment_batch(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
+                      const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale, int interp,
+                      int k0, int window, int kind, double ox, double oy, double res, int nx, int ny, int x0,
+                      int y0, int x1, int y1, int n_sub, int stop_cells, int max_iters, int32_t* d_regions_out,
+                      float* lowres, mwb_seg_trace_t* d_traces, void* workspace, void* stream) {
+  if (n_scans < 1 || n_scans > 65535) return set_err(MWB_EINVAL, "mwb_segment_batch: n_scans must be in [1, 65535]");
+  if (n_sub < 1 || n_sub > 64 || stop_cells < 1 || max_iters < 0 || max_iters > MWB_SEG_MAX_ITERS)
+    return set_err(MWB_EINVAL, "mwb_segment_batch: bad n_sub / stop_cells / max_iters");
+  if (nx < 1 || ny < 1 || x0 < 0 || y0 < 0 || x1 >= nx || y1 >= ny || x0 > x1 || y0 > y1)
+    return set_err(MWB_EINVAL, "mwb_segment_batch: region outside the grid");
+  if (kind != MWB_DAS && kind != MWB_DMAS) return set_err(MWB_EINVAL, "mwb_segment_batch: bad kind");
+  if (!d_regions_out || !d_traces || !workspace) return set_err(MWB_EINVAL, "mwb_segment_batch: null pointer");
+  const long long per = seg_batch_per_scan(n_sub), n = per * n_scans;
+  if (n > 0x7FFFFFFFLL) return set_err(MWB_ERANGE, "mwb_segment_batch: %lld points exceed int32", n);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  SegState* st = reinterpret_cast<SegState*>(ws);
+  ws += align_up(sizeof(SegState) * (size_t)n_scans, 256);
+  double* pts = reinterpret_cast<double*>(ws);
+  ws += align_up(24 * n, 256);
+  float* e = reinterpret_cast<float*>(ws);
+  ws += align_up(4 * n, 256);
+  int2* tile_info = reinterpret_cast<int2*>(ws);
+  ws += align_up(8 * (n / TILE), 256);
+  void* table = ws;
+  const int32_t* ti = reinterpret_cast<const int32_t*>(tile_info);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  seg_init_batch_kernel<<<(n_scans + 255) / 256, 256, 0, cs>>>(st, n_scans, x0, y0, x1, y1, stop_cells, d_traces);
+  int rc = check_launch("seg_init_batch_kernel");
+  if (rc) return rc;
+  for (int it = 0; it < max_iters; ++it) {
+    seg_points_batch_kernel<<<dim3((unsigned)(per / TILE), (unsigned)n_scans), TILE, 0, cs>>>(
+        st, (int)per, ox, oy, res, n_sub, pts, tile_info);
+    if ((rc = check_launch("seg_points_batch_kernel"))) return rc;
+    if ((rc = mwb_delay_table_tiles(pts, (int)n, ti, chan_txrx, n_chan, ant_xyz, n_ant, inv_scale, interp, table,
+                                    stream)))
+      return rc;
+    if ((rc = mwb_energies_tiles(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant,
+                                 inv_scale, pts, nullptr, (int)n, ti, table, interp, k0, window,
+                                 kind == MWB_DAS ? e : nullptr, kind == MWB_DMAS ? e : nullptr, 0, nullptr, nullptr,
+                                 nullptr, 0, stream)))
+      return rc;
+    seg_score_batch_kernel<<<n_scans, 256, 0, cs>>>(st, e, (int)per, n_sub, kind == MWB_DMAS, stop_cells, lowres,
+                                                    d_traces);
+    if ((rc = check_launch("seg_score_batch_kernel"))) return rc;
+  }
+  seg_region_batch_kernel<<<(n_scans + 255) / 256, 256, 0, cs>>>(st, n_scans, d_regions_out);
+  return check_launch("seg_region_batch_kernel");
 }
 
 // One-call lattice image (beamform.py:283-342 as a single C entry point): the

@@ -24,7 +24,9 @@ result once.
 
 from __future__ import annotations
 
+import hashlib
 import math
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -33,8 +35,8 @@ import torch
 from . import _device as dv
 from . import _native as nat
 from .beamform import EVAL_COUNTER, EnergyMap, _check_interpolation, _kind, _kind_code, _Status, _window, lattice_pass
-from .coarse2fine import breast_mask
-from .geometry import ImagingGrid, Region
+from .coarse2fine import _breast_mask_device
+from .geometry import ArrayGeometry, ImagingGrid, Region
 
 
 @dataclass
@@ -110,10 +112,129 @@ def max_iterations(region: Region, stop_cells: int) -> int:
     return n
 
 
+class _SegmentPlan:
+    """One segment() configuration on one device scan, captured as a CUDA graph
+    (the search's 4 launches per iteration and the fine lattice pass); later
+    calls replay it and read the results back into pinned buffers with one
+    synchronisation.  Buffers persist with the plan, so a replay allocates
+    nothing (as coarse2fine._FrameworkPlan)."""
+
+    def __init__(self, scan: dv.DeviceScan, grid: ImagingGrid, region: Region, kcode: int, n_sub: int,
+                 stop_cells: int, n_iter: int, interp: int, k0: int, w: int, mask_np, mask_t):
+        self.scan, self.grid, self.region, self.kcode = scan, grid, region, kcode
+        self.n_sub, self.stop_cells, self.n_iter = n_sub, stop_cells, n_iter
+        self.interp, self.k0, self.w = interp, k0, w
+        self.mask_np, self.mask_t = mask_np, mask_t
+        nx, ny = grid.dims
+        dev = dv.device()
+        n_low = (2 * n_sub) ** 2
+        self.ws = torch.empty(int(nat.load().mwb_segment_workspace_bytes(n_sub, scan.n_chan)), dtype=torch.uint8,
+                              device=dev)
+        self.region_t = torch.zeros(6, dtype=torch.int32, device=dev)
+        self.lowres = torch.zeros(n_low, dtype=torch.float32, device=dev)
+        self.trace_t = torch.zeros(nat.SEG_TRACE_BYTES, dtype=torch.uint8, device=dev)
+        self.dense = torch.empty(nx * ny, dtype=torch.float32, device=dev)  # only valid cells are read
+        self.valid = torch.empty(nx * ny, dtype=torch.uint8, device=dev)
+        self.status = _Status()
+        self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)]
+        pin = torch.cuda.is_available()
+        self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=pin)
+        self.h_trace = torch.empty(nat.SEG_TRACE_BYTES, dtype=torch.uint8, pin_memory=pin)
+        self.h_dense = torch.empty(nx * ny, dtype=torch.float32, pin_memory=pin)
+        self.h_valid = torch.empty(nx * ny, dtype=torch.uint8, pin_memory=pin)
+        self.h_lowres = torch.empty(n_low, dtype=torch.float32, pin_memory=pin)
+        self.graph: torch.cuda.CUDAGraph | None = None
+
+    def _enqueue(self) -> None:
+        sc, grid = self.scan, self.grid
+        nx, ny = grid.dims
+        x0, y0, x1, y1 = self.region.bounds()
+        ev = self.events
+        self.valid.zero_()
+        self.status.t.zero_()
+        self.lowres.zero_()
+        ev[0].record()
+        nat.call("mwb_segment", sc.sig.data_ptr(), sc.n_chan, sc.ld, sc.n_samples, sc.chan.data_ptr(),
+                 sc.ant.data_ptr(), sc.n_ant, sc.inv_scale, self.interp, self.k0, self.w, self.kcode, grid.origin[0],
+                 grid.origin[1], grid.resolution, nx, ny, x0, y0, x1, y1, self.n_sub, self.stop_cells, self.n_iter,
+                 self.region_t.data_ptr(), self.lowres.data_ptr(), self.trace_t.data_ptr(), self.ws.data_ptr(),
+                 dv.stream_handle())
+        ev[1].record()
+        lattice_pass(sc, grid, 1, self.mask_t, 0, (self.kcode,), self.interp, self.k0, self.w,
+                     {self.kcode: self.dense}, self.valid, self.status, 0, d_region=self.region_t)
+        ev[2].record()
+
+    def launch(self) -> None:
+        if self.graph is None:
+            self._enqueue()  # eager run: kernel attributes set, allocator warmed
+            torch.cuda.current_stream().synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                self._enqueue()
+            self.graph = graph
+        self.graph.replay()
+        for src, dst in ((self.status.t, self.h_status), (self.trace_t, self.h_trace), (self.dense, self.h_dense),
+                         (self.valid, self.h_valid), (self.lowres, self.h_lowres)):
+            dst.copy_(src, non_blocking=True)
+
+    def finish(self, kind) -> tuple[EnergyMap, SegmentReport]:
+        torch.cuda.current_stream().synchronize()
+        grid = self.grid
+        nx, ny = grid.dims
+        keys, counts, flags = self.status.read(self.h_status.numpy())
+        if flags & 1:
+            raise ValueError("energy map contains non-finite values")
+        records, final = _decode_seg_trace(self.h_trace.numpy().tobytes())
+        n_fine = int(counts[0])
+        n_sub = self.n_sub
+        EVAL_COUNTER.add(n_fine + 4 * n_sub * n_sub * len(records))
+        vals = self.h_dense.numpy().reshape(nx, ny).copy()  # the plan's pinned buffers are reused
+        vmask = self.h_valid.numpy().reshape(nx, ny).view(bool).copy()
+        fine = EnergyMap._from_dense(grid, vals, vmask, 1, roi=final, checked=True)
+        key = int(keys[0 if self.kcode == nat.MWB_DAS else 1])
+        if key:
+            slot = 0xFFFFFFFF - (key & 0xFFFFFFFF)
+            cell = (slot // ny, slot % ny)
+        else:
+            cell = (final.min_cell[0], final.min_cell[1])
+        full_eq = int(self.mask_np.sum()) if self.mask_np is not None else nx * ny
+        ev = self.events
+        t_s, t_f = ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3
+        report = SegmentReport(
+            kind=_kind(kind).value, n_sub=n_sub, stop_cells=self.stop_cells, records=records, final_region=final,
+            lowres=self.h_lowres.numpy().reshape(2 * n_sub, 2 * n_sub).copy(),
+            subgrid_points_evaluated=4 * n_sub * n_sub * len(records), fine_points_evaluated=n_fine,
+            full_equivalent_points=full_eq, argmax_cell=cell, argmax_position=grid.cell_center(*cell),
+            elapsed={"search": t_s, "fine": t_f, "total": t_s + t_f})
+        return fine, report
+
+
+_SEG_PLANS: "OrderedDict[tuple, _SegmentPlan]" = OrderedDict()
+_SEG_PLAN_CAPACITY = 8
+
+
+def _mask_for(grid: ImagingGrid, mask):
+    """(host mask or None, device mask or None, cache key)."""
+    if isinstance(mask, str):
+        if mask != "breast":
+            raise ValueError(f"unknown mask {mask!r}")
+        m, mt = _breast_mask_device(grid)
+        return m, mt, "breast"
+    if mask is None:
+        return None, None, None
+    m = np.asarray(mask, dtype=bool)
+    if m.shape != grid.dims:
+        raise ValueError(f"mask shape {m.shape} != grid dims {grid.dims}")
+    return m, dv.upload_mask(m, grid.dims), hashlib.sha1(np.packbits(m).tobytes()).hexdigest()
+
+
 def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.01, *, region: Region | None = None,
             mask="breast", window=None, interpolation: str = "linear") -> tuple[EnergyMap, SegmentReport]:
     """Quadrant search scored on n_sub x n_sub sub-grids, then a full-resolution
-    pass over the kept segment.  Returns (fine map of the segment, report)."""
+    pass over the kept segment.  Returns (fine map of the segment, report).
+
+    Repeated calls with one configuration on one dataset replay a captured
+    CUDA graph (the plan is keyed by the device scan object, as run_framework's)."""
     _check_interpolation(interpolation)
     if not stop_size > 0:
         raise ValueError("stop_size must be > 0")
@@ -132,34 +253,23 @@ def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.0
     if w == 0:
         raise ValueError("the segmentation metric needs a non-empty energy window")
     interp = nat.INTERP[interpolation]
-    nx, ny = grid.dims
-    dev = dv.device()
-    ws = torch.empty(int(nat.load().mwb_segment_workspace_bytes(n_sub, scan.n_chan)), dtype=torch.uint8, device=dev)
-    region_t = torch.zeros(6, dtype=torch.int32, device=dev)
-    lowres = torch.zeros((2 * n_sub) ** 2, dtype=torch.float32, device=dev)
-    trace_t = torch.zeros(nat.SEG_TRACE_BYTES, dtype=torch.uint8, device=dev)
-    m = breast_mask(grid) if isinstance(mask, str) and mask == "breast" else mask
-    mask_t = dv.upload_mask(m, grid.dims) if m is not None else None
-    dense = torch.zeros(nx * ny, dtype=torch.float32, device=dev)
-    valid = torch.zeros(nx * ny, dtype=torch.uint8, device=dev)
-    status = _Status()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    x0, y0, x1, y1 = region.bounds()
-    ev[0].record()
-    nat.call("mwb_segment", scan.sig.data_ptr(), scan.n_chan, scan.ld, scan.n_samples, scan.chan.data_ptr(),
-             scan.ant.data_ptr(), scan.n_ant, scan.inv_scale, interp, k0, w, kcode, grid.origin[0], grid.origin[1],
-             grid.resolution, nx, ny, x0, y0, x1, y1, n_sub, stop_cells, n_iter, region_t.data_ptr(),
-             lowres.data_ptr(), trace_t.data_ptr(), ws.data_ptr(), dv.stream_handle())
-    ev[1].record()
-    lattice_pass(scan, grid, 1, mask_t, 0, (kcode,), interp, k0, w, {kcode: dense}, valid, status, 0,
-                 d_region=region_t)
-    ev[2].record()
-    st, th, dh, vh, lh = dv.to_host(status.t, trace_t, dense.view(nx, ny), valid.view(nx, ny),
-                                    lowres.view(2 * n_sub, 2 * n_sub))
-    keys, counts, flags = status.read(st)
-    if flags & 1:
-        raise ValueError("energy map contains non-finite values")
-    tr = nat.SegTrace.from_buffer_copy(th.tobytes())
+    m, mt, mkey = _mask_for(grid, mask)
+    key = (id(scan), grid.origin, grid.extent, grid.resolution, region.bounds(), kcode, n_sub, stop_cells, interp,
+           k0, w, mkey, torch.cuda.current_device())
+    plan = _SEG_PLANS.get(key)
+    if plan is None or plan.scan is not scan:
+        plan = _SegmentPlan(scan, grid, region, kcode, n_sub, stop_cells, n_iter, interp, k0, w, m, mt)
+        _SEG_PLANS[key] = plan
+        while len(_SEG_PLANS) > _SEG_PLAN_CAPACITY:
+            _SEG_PLANS.popitem(last=False)
+    else:
+        _SEG_PLANS.move_to_end(key)
+    plan.launch()
+    return plan.finish(kind)
+
+
+def _decode_seg_trace(raw: bytes) -> tuple[list[SegmentRecord], Region]:
+    tr = nat.SegTrace.from_buffer_copy(raw)
     records = []
     for i in range(int(tr.n_records)):
         r = tr.records[i]
@@ -167,22 +277,176 @@ def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.0
             iteration=int(r.iteration), parent=_region(r.parent), selected=int(r.selected),
             selected_region=_region(r.selected_region), scores=[float(v) for v in r.score],
             maxima=[float(v) for v in r.emax], means=[float(v) for v in r.emean], shift=float(r.shift)))
-    final = _region(tr.final_region)
-    n_fine = int(counts[0])
-    EVAL_COUNTER.add(n_fine + 4 * n_sub * n_sub * len(records))
-    fine = EnergyMap._from_dense(grid, dh, vh.view(bool), 1, roi=final)
-    key = int(keys[0 if kcode == nat.MWB_DAS else 1])
-    if key:
-        slot = 0xFFFFFFFF - (key & 0xFFFFFFFF)
-        cell = (slot // ny, slot % ny)
-    else:
-        cell = (final.min_cell[0], final.min_cell[1])
-    full_eq = int(m.sum()) if m is not None else grid.dims[0] * grid.dims[1]
-    report = SegmentReport(
-        kind=_kind(kind).value, n_sub=n_sub, stop_cells=stop_cells, records=records, final_region=final,
-        lowres=lh,
-        subgrid_points_evaluated=4 * n_sub * n_sub * len(records), fine_points_evaluated=n_fine,
-        full_equivalent_points=full_eq, argmax_cell=cell, argmax_position=grid.cell_center(*cell),
-        elapsed={"search": ev[0].elapsed_time(ev[1]) / 1e3, "fine": ev[1].elapsed_time(ev[2]) / 1e3,
-                 "total": ev[0].elapsed_time(ev[2]) / 1e3})
-    return fine, report
+    return records, _region(tr.final_region)
+
+
+@dataclass
+class SegmentBatchResult:
+    grid: ImagingGrid
+    kind: str
+    n_sub: int
+    final_regions: np.ndarray  # (S, 4) x0, y0, x1, y1
+    argmax_cells: np.ndarray  # (S, 2)
+    iterations: np.ndarray  # (S,)
+    fine_points_evaluated: np.ndarray  # (S,)
+    full_equivalent_points: int
+    dense: torch.Tensor  # (S, nx, ny) fine energies on the device (valid inside each final region only)
+    lowres: torch.Tensor  # (S, 2 n_sub, 2 n_sub) on the device
+    elapsed: dict
+    _traces: torch.Tensor
+    _mask: np.ndarray | None
+
+    @property
+    def n_scans(self) -> int:
+        return int(self.final_regions.shape[0])
+
+    def final_region(self, s: int) -> Region:
+        x0, y0, x1, y1 = (int(v) for v in self.final_regions[s])
+        return Region((x0, y0), (x1, y1))
+
+    def records(self, s: int) -> list[SegmentRecord]:
+        n = nat.SEG_TRACE_BYTES
+        return _decode_seg_trace(self._traces[s * n : (s + 1) * n].cpu().numpy().tobytes())[0]
+
+    def fine(self, s: int) -> EnergyMap:
+        """Scan s's full-resolution map of its final segment, as ``segment`` returns it."""
+        nx, ny = self.grid.dims
+        x0, y0, x1, y1 = (int(v) for v in self.final_regions[s])
+        valid = np.zeros((nx, ny), dtype=bool)
+        valid[x0 : x1 + 1, y0 : y1 + 1] = True
+        if self._mask is not None:
+            valid &= self._mask
+        return EnergyMap._from_dense(self.grid, self.dense[s].cpu().numpy(), valid, 1, roi=self.final_region(s),
+                                     checked=True)
+
+
+class SegmentBatch:
+    """``segment`` for S scans that share the antenna geometry, the grid and the
+    start region (BASELINE configs[2] at batch throughput).
+
+    One ``mwb_segment_batch`` call runs every scan's quadrant search (four
+    launches per iteration for the whole batch); the full-resolution pass over
+    each scan's final segment is one packed launch (``mwb_enumerate_regions_*``
+    + ``mwb_delay_table_tiles`` + ``mwb_energies_tiles``, as in FrameworkBatch).
+    Regions, traces, fine energies and argmax cells are bit-identical to
+    calling ``segment`` once per scan.  One host synchronisation per batch (to
+    size the packed fine list).
+    """
+
+    def __init__(self, geometry: ArrayGeometry, pairs, n_samples: int, grid: ImagingGrid, kind, n_sub: int = 16,
+                 stop_size: float = 0.01, *, region: Region | None = None, mask="breast", window=None,
+                 interpolation: str = "linear"):
+        _check_interpolation(interpolation)
+        if not stop_size > 0:
+            raise ValueError("stop_size must be > 0")
+        if not 1 <= n_sub <= 64:
+            raise ValueError("n_sub must be in [1, 64]")
+        dev = dv.device()
+        self.grid = grid
+        self.kind = _kind(kind)
+        self.kcode = _kind_code(kind)
+        self.n_sub = int(n_sub)
+        self.region = grid.full_region() if region is None else region
+        if not grid.full_region().contains_region(self.region):
+            raise ValueError("region lies outside the grid")
+        self.stop_cells = max(1, int(math.floor(stop_size / grid.resolution + 1e-9)))
+        self.n_iter = max_iterations(self.region, self.stop_cells)
+        if self.n_iter > nat.SEG_MAX_ITERS:
+            raise ValueError("stop_size too small for the segment trace")
+        self.interp = nat.INTERP[interpolation]
+        self.n_samples = int(n_samples)
+        self.ld = dv.round4(n_samples)
+        self.k0, self.w = _window(self.n_samples, window)
+        if self.w == 0:
+            raise ValueError("the segmentation metric needs a non-empty energy window")
+        pairs = np.asarray(pairs, dtype=np.int32).reshape(-1, 2)
+        self.scan = dv.DeviceScan(
+            sig=torch.empty(0, device=dev),
+            chan=torch.from_numpy(pairs).to(dev),
+            ant=torch.from_numpy(np.array(geometry.antennas, dtype=np.float64)).to(dev),
+            inv_scale=1.0 / (float(geometry.propagation_speed) * float(geometry.sample_interval)),
+            n_samples=self.n_samples, ld=self.ld, n_ant=geometry.n_antennas, chan_host=pairs)
+        self.mask_np, self.mask_t, _ = _mask_for(grid, mask)
+        self._ws = None
+
+    @property
+    def n_chan(self) -> int:
+        return self.scan.n_chan
+
+    def run(self, sig: torch.Tensor) -> SegmentBatchResult:
+        """Segment S device-resident scans (S, C, ld) fp32."""
+        s_n = int(sig.shape[0])
+        if sig.dtype != torch.float32 or sig.shape[1:] != (self.n_chan, self.ld) or not sig.is_contiguous():
+            raise ValueError(f"sig must be contiguous float32 (S, {self.n_chan}, {self.ld})")
+        if s_n == 0 or s_n > 65535:
+            raise ValueError("batch size must be in [1, 65535]")
+        grid = self.grid
+        nx, ny = grid.dims
+        dev = dv.device()
+        lib = nat.load()
+        stream = dv.stream_handle()
+        sc = self.scan
+        n_low = (2 * self.n_sub) ** 2
+        ws_bytes = int(lib.mwb_segment_batch_workspace_bytes(s_n, self.n_sub, self.n_chan))
+        if self._ws is None or self._ws.numel() < ws_bytes:
+            self._ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        regions = torch.empty((s_n, 6), dtype=torch.int32, device=dev)
+        traces = torch.empty(s_n * nat.SEG_TRACE_BYTES, dtype=torch.uint8, device=dev)
+        lowres = torch.zeros((s_n, n_low), dtype=torch.float32, device=dev)
+        dense = torch.empty((s_n, nx * ny), dtype=torch.float32, device=dev)
+        keys = torch.zeros(s_n, dtype=torch.int64, device=dev)
+        flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        das = self.kcode == nat.MWB_DAS
+        x0, y0, x1, y1 = self.region.bounds()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        nat.call("mwb_segment_batch", sig.data_ptr(), s_n, self.n_chan * self.ld, self.n_chan, self.ld,
+                 self.n_samples, sc.chan.data_ptr(), sc.ant.data_ptr(), sc.n_ant, sc.inv_scale, self.interp, self.k0,
+                 self.w, self.kcode, grid.origin[0], grid.origin[1], grid.resolution, nx, ny, x0, y0, x1, y1,
+                 self.n_sub, self.stop_cells, self.n_iter, regions.data_ptr(), lowres.data_ptr(), traces.data_ptr(),
+                 self._ws.data_ptr(), stream)
+        ev[1].record()
+        # fine pass over every scan's final segment: one packed list
+        rws = torch.empty(int(lib.mwb_regions_workspace_bytes(s_n)), dtype=torch.uint8, device=dev)
+        totals = torch.zeros(2, dtype=torch.int32, device=dev)
+        mask_p = self.mask_t.data_ptr() if self.mask_t is not None else None
+        nat.call("mwb_enumerate_regions_count", nx, ny, regions.data_ptr(), s_n, mask_p, 0, totals.data_ptr(),
+                 rws.data_ptr(), stream)
+        n_pts, n_tiles = (int(v) for v in totals.cpu().tolist())  # the one host sync: packed list size
+        if n_pts > 0:
+            f_pts = torch.empty((n_pts, 3), dtype=torch.float64, device=dev)
+            f_idx = torch.empty(n_pts, dtype=torch.int32, device=dev)
+            tile_info = torch.empty((n_tiles, 2), dtype=torch.int32, device=dev)
+            nat.call("mwb_enumerate_regions_write", grid.origin[0], grid.origin[1], grid.resolution, nx, ny,
+                     regions.data_ptr(), s_n, mask_p, 0, f_pts.data_ptr(), f_idx.data_ptr(), tile_info.data_ptr(),
+                     rws.data_ptr(), stream)
+            f_table = torch.empty(int(lib.mwb_delay_table_bytes(n_pts, self.n_chan)), dtype=torch.uint8, device=dev)
+            nat.call("mwb_delay_table_tiles", f_pts.data_ptr(), n_pts, tile_info.data_ptr(), sc.chan.data_ptr(),
+                     self.n_chan, sc.ant.data_ptr(), sc.n_ant, sc.inv_scale, self.interp, f_table.data_ptr(), stream)
+            nat.call("mwb_energies_tiles", sig.data_ptr(), s_n, self.n_chan * self.ld, self.n_chan, self.ld,
+                     self.n_samples, sc.chan.data_ptr(), sc.ant.data_ptr(), sc.n_ant, sc.inv_scale,
+                     f_pts.data_ptr(), f_idx.data_ptr(), n_pts, tile_info.data_ptr(), f_table.data_ptr(),
+                     self.interp, self.k0, self.w, dense.data_ptr() if das else None,
+                     None if das else dense.data_ptr(), nx * ny, keys.data_ptr() if das else None,
+                     None if das else keys.data_ptr(), flags.data_ptr(), 0, stream)
+        ev[2].record()
+        fine_counts, st, reg, k, n_rec = dv.to_host(rws.view(torch.int32)[:s_n], flags, regions, keys,
+                                                     traces.view(s_n, -1)[:, :4].contiguous().view(torch.int32))
+        if int(st[0]) & 1:
+            raise ValueError("energy map contains non-finite values")
+        fine_counts = fine_counts.astype(np.int64)
+        k = k.view(np.uint64)
+        slot = (0xFFFFFFFF - (k & np.uint64(0xFFFFFFFF))).astype(np.int64)
+        cells = np.stack([slot // ny, slot % ny], axis=1)
+        none = k == 0  # an empty final segment: segment() reports its first cell
+        cells[none] = reg[none][:, [0, 1]]
+        iters = n_rec.reshape(s_n).astype(np.int64)
+        EVAL_COUNTER.add(int(fine_counts.sum()) + 4 * self.n_sub * self.n_sub * int(iters.sum()))
+        full_eq = int(self.mask_np.sum()) if self.mask_np is not None else nx * ny
+        elapsed = {"search": ev[0].elapsed_time(ev[1]) / 1e3, "fine": ev[1].elapsed_time(ev[2]) / 1e3}
+        elapsed["total"] = elapsed["search"] + elapsed["fine"]
+        return SegmentBatchResult(
+            grid=grid, kind=self.kind.value, n_sub=self.n_sub, final_regions=reg[:, [0, 1, 3, 4]],
+            argmax_cells=cells, iterations=iters, fine_points_evaluated=fine_counts, full_equivalent_points=full_eq,
+            dense=dense.view(s_n, nx, ny), lowres=lowres.view(s_n, 2 * self.n_sub, 2 * self.n_sub), elapsed=elapsed,
+            _traces=traces, _mask=self.mask_np)

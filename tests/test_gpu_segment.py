@@ -71,3 +71,98 @@ def test_search_counts_and_no_refine_when_small():
     assert rep.iterations == 0 and rep.final_region == grid.full_region()
     assert len(fine) == 40 * 40 == rep.fine_points_evaluated
     assert mw.EVAL_COUNTER.value - before == 1600
+
+
+def _records_equal(a, b):
+    return ([(r.iteration, r.selected, r.parent, r.selected_region, r.scores, r.maxima, r.means, r.shift) for r in a]
+            == [(r.iteration, r.selected, r.parent, r.selected_region, r.scores, r.maxima, r.means, r.shift)
+                for r in b])
+
+
+@pytest.mark.parametrize("kind", ["das", "dmas"])
+def test_segment_batch_equals_per_scan_segment(kind):
+    """SegmentBatch reproduces segment() scan by scan, bit for bit: records
+    (scores, maxima, means, shift), final segment, low-res image, fine map,
+    argmax and counters."""
+    import torch
+
+    from paper_1709_02549_b200.segment import SegmentBatch
+
+    model = synth.ScanModel(n_samples=2048)
+    seeds = list(range(900, 910))
+    sig, _ = synth.batch_2d(model, seeds, phantom_radius=(0.04, 0.05), snr_db=(15.0, 30.0))
+    grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 2.5e-4)
+    sb = SegmentBatch(model.geometry(), model.pairs(), model.n_samples, grid, kind, 16, 0.01,
+                      window=(model.k0, model.window))
+    before = mw.EVAL_COUNTER.value
+    res = sb.run(torch.from_numpy(sig).cuda())
+    counted = mw.EVAL_COUNTER.value - before
+    assert res.n_scans == len(seeds)
+    total = 0
+    for s in range(len(seeds)):
+        ds = mw.BackscatterDataset(model.geometry(), synth.embed_pairs(12, model.pairs(), sig[s].astype(np.float64)))
+        fine, rep = segment(ds, kind, grid, 16, 0.01, window=(model.k0, model.window))
+        total += rep.fine_points_evaluated + rep.subgrid_points_evaluated
+        assert res.final_region(s) == rep.final_region
+        assert _records_equal(res.records(s), rep.records)
+        assert res.iterations[s] == rep.iterations
+        assert np.array_equal(res.lowres[s].cpu().numpy(), rep.lowres)
+        assert tuple(res.argmax_cells[s]) == rep.argmax_cell
+        assert res.fine_points_evaluated[s] == rep.fine_points_evaluated
+        assert res.fine(s).entries == fine.entries
+    assert counted == total
+
+
+def test_segment_batch_start_region_already_small_and_no_mask():
+    import torch
+
+    from paper_1709_02549_b200.segment import SegmentBatch
+
+    model = synth.ScanModel(n_samples=512)
+    sig, _ = synth.batch_2d(model, [1, 2, 3], phantom_radius=(0.04, 0.05))
+    grid = mw.ImagingGrid((-0.005, -0.005), (0.01, 0.01), 2.5e-4)  # already a 1 cm segment
+    sb = SegmentBatch(model.geometry(), model.pairs(), model.n_samples, grid, "das", window=(model.k0, 32), mask=None)
+    res = sb.run(torch.from_numpy(sig).cuda())
+    assert (res.iterations == 0).all() and (res.fine_points_evaluated == 1600).all()
+    for s in range(3):
+        assert res.final_region(s) == grid.full_region()
+        ds = mw.BackscatterDataset(model.geometry(), synth.embed_pairs(12, model.pairs(), sig[s].astype(np.float64)))
+        fine, rep = segment(ds, "das", grid, window=(model.k0, 32), mask=None)
+        assert res.fine(s).entries == fine.entries and tuple(res.argmax_cells[s]) == rep.argmax_cell
+
+
+def test_segment_batch_rejects_bad_input():
+    import torch
+
+    from paper_1709_02549_b200.segment import SegmentBatch
+
+    model = synth.ScanModel(n_samples=512)
+    grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 5e-4)
+    with pytest.raises(ValueError):
+        SegmentBatch(model.geometry(), model.pairs(), model.n_samples, grid, "das", n_sub=0)
+    with pytest.raises(ValueError):
+        SegmentBatch(model.geometry(), model.pairs(), model.n_samples, grid, "das", stop_size=0.0)
+    sb = SegmentBatch(model.geometry(), model.pairs(), model.n_samples, grid, "das", window=(model.k0, 32), mask=None)
+    with pytest.raises(ValueError):
+        sb.run(torch.zeros((2, 66, 100), dtype=torch.float32, device="cuda"))
+    bad = torch.zeros((2, 66, sb.ld), dtype=torch.float32, device="cuda")
+    bad[1, 0, :] = float("nan")
+    with pytest.raises(ValueError):
+        sb.run(bad)
+
+
+def test_graph_replay_is_identical_and_per_dataset():
+    """segment() replays a captured graph on repeat calls: the replay must equal
+    the eager first call, and a different dataset must not see stale data."""
+    model = synth.ScanModel(n_samples=1024)
+    grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 5e-4)
+    ds_a, _ = synth.dataset_2d(model, seed=41)
+    ds_b, _ = synth.dataset_2d(model, seed=42)
+    win = (model.k0, model.window)
+    first = [segment(ds, "dmas", grid, 16, 0.01, window=win) for ds in (ds_a, ds_b)]
+    again = [segment(ds, "dmas", grid, 16, 0.01, window=win) for ds in (ds_a, ds_b, ds_a)]
+    for (f0, r0), (f1, r1) in zip(first + first[:1], again):
+        assert f0.entries == f1.entries
+        assert _records_equal(r0.records, r1.records) and r0.argmax_cell == r1.argmax_cell
+        assert np.array_equal(r0.lowres, r1.lowres)
+    assert first[0][1].argmax_cell != first[1][1].argmax_cell or first[0][0].entries != first[1][0].entries
