@@ -289,6 +289,43 @@ int mwb_segment_batch(const float* sig, int n_scans, int64_t scan_stride, int n_
                       float* lowres, mwb_seg_trace_t* d_traces, void* workspace, void* stream);
 
 /*
+ * Batched segmentation over a precomputed region tree.  The regions a search
+ * can visit depend only on the start region {x0,y0,x1,y1}, stop_cells and
+ * max_iters, so a plan holds, for one geometry, grid and mask, the sub-grid
+ * points and delay tables of every region that gets split and the fine-pass
+ * cells (region & mask, stride 1) and tables of every region a search can end
+ * in.  A run then costs two launches per iteration for the whole batch and two
+ * for the fine pass, with no host synchronisation (CUDA-graph capturable).
+ *
+ * mwb_segment_plan_info: info[0] = plan bytes, info[1] = regions split,
+ *   info[2] = terminal regions, info[3] = fine tiles per scan (workspace
+ *   sizing).  MWB_ERANGE when the tree exceeds 16384 regions (use
+ *   mwb_segment_batch then).
+ * mwb_segment_plan_prepare: fills the plan (synchronises `stream` once: the
+ *   node list is copied from the host).
+ * mwb_segment_run: the search for S scans as in mwb_segment_batch, then every
+ *   scan's fine pass into out_fine + s * out_stride (slot ix * ny + iy of the
+ *   final region's cells; other slots untouched), argmax keys keys[s] (as
+ *   mwb_energies; zero them first), fine-cell counts fine_counts[s] (may be
+ *   NULL) and the non-finite flag.  Per scan, identical to mwb_segment + a
+ *   lattice pass over its final region.
+ */
+int mwb_segment_plan_info(int nx, int ny, int x0, int y0, int x1, int y1, int n_sub, int stop_cells,
+                          int max_iters, int n_chan, int64_t* info);
+int mwb_segment_plan_prepare(const int32_t* chan_txrx, int n_chan, const double* ant_xyz, int n_ant,
+                             double inv_scale, int interp, double ox, double oy, double res, int nx,
+                             int ny, int x0, int y0, int x1, int y1, const uint8_t* mask, int n_sub,
+                             int stop_cells, int max_iters, void* plan, void* stream);
+int64_t mwb_segment_run_workspace_bytes(int n_scans, int n_sub, int fine_tiles_per_scan);
+int mwb_segment_run(const void* plan, const float* sig, int n_scans, int64_t scan_stride, int n_chan,
+                    int ld, int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
+                    double inv_scale, int interp, int k0, int window, int kind, int nx, int ny, int x0,
+                    int y0, int x1, int y1, int n_sub, int stop_cells, int max_iters,
+                    int32_t* d_regions_out, float* lowres, mwb_seg_trace_t* d_traces, float* out_fine,
+                    int64_t out_stride, uint64_t* keys, int32_t* fine_counts, int32_t* flags,
+                    void* workspace, void* stream);
+
+/*
  * Device-side scan synthesis (the input producer of the path): writes S scans
  * [S][n_chan][ld] fp32 (samples >= n_samples zero) for point scatterers
  * scatterers[S][n_scat][4] = {x, y, z, amplitude}.  model 0 = the reference

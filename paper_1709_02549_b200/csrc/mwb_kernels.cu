@@ -25,6 +25,7 @@
 //     in mwb_tc.cuh instead (mwb_energies_tc).
 #include <cuda.h>  // CUtensorMap (types only; the encoder comes through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
+#include <vector>
 #include <cuda_fp16.h>
 #include <algorithm>
 #include <stdint.h>
@@ -255,6 +256,7 @@ struct EnergyParams {
   int P;
   const int* d_count;
   const int2* tile_info;      // packed multi-scan lists: {scan, valid points} per tile, or NULL
+  const int* tile_src;        // with tile_info: source tile of the point list / table per launched tile, or NULL
   const uint32_t* tab_words;  // [tiles][C][TILE]
   const int2* tab_span;       // [tiles][C] {lo, hi}
   const int* tab_wide;        // [tiles]
@@ -554,16 +556,19 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.mbar);
   float* stage = reinterpret_cast<float*>(smem + L.stage);
 
-  const size_t tile = blockIdx.x;
+  // source tile of the points / table (a shared, precomputed list) and the
+  // packed output position; the same tile unless tile_src remaps it
+  const size_t tile = p.tile_src ? (size_t)__ldg(p.tile_src + blockIdx.x) : (size_t)blockIdx.x;
+  const int src0 = (int)tile * TILE;
   const bool wide = __ldg(p.tab_wide + tile) != 0;
   const uint32_t* tw = p.tab_words + tile * (size_t)p.C * TILE;
   const int2* tsp = p.tab_span + tile * (size_t)p.C;
 
   const int la = tid, lb = tid + TPB;
   const bool va = la < n_in_tile, vb = lb < n_in_tile;
-  const int ga = tile0 + (va ? la : 0), gb = tile0 + (vb ? lb : 0);
-  const int oa = va ? (p.out_idx ? __ldg(p.out_idx + ga) : ga) : -1;
-  const int ob = vb ? (p.out_idx ? __ldg(p.out_idx + gb) : gb) : -1;
+  const int ga = src0 + (va ? la : 0), gb = src0 + (vb ? lb : 0);
+  const int oa = va ? (p.out_idx ? __ldg(p.out_idx + ga) : tile0 + la) : -1;
+  const int ob = vb ? (p.out_idx ? __ldg(p.out_idx + gb) : tile0 + lb) : -1;
 
   // ---- per-channel spans and stage-buffer groups --------------------------
   for (int c = tid; c < p.C; c += TPB) {
@@ -1058,7 +1063,7 @@ __device__ __forceinline__ bool box_contains(const Box& r, int ix, int iy, int i
 }
 
 // children in the reference quadrant order: index = xh + 2*yh (+ 4*zh)
-__device__ __forceinline__ int split_box(const Box& r, int dims, Box q[MAXCH]) {
+__host__ __device__ __forceinline__ int split_box(const Box& r, int dims, Box q[MAXCH]) {
   int mid[3];
   for (int a = 0; a < dims; ++a) {
     const int w = r.hi[a] - r.lo[a] + 1;
@@ -1860,6 +1865,19 @@ struct SegState {
   int region[6];
   int done;
   int iter;
+  int node;  // batched tree search: index of the current region in the SegNode tree
+};
+
+// Batched search over a precomputed tree: every region a search can reach
+// (the start region, its quadrants, theirs, ... down to the stop size) is a
+// node; search nodes own the 4 n_sub^2 sub-grid points (and delay-table
+// tiles) used to choose among their children, terminal nodes own their
+// full-resolution fine-pass cells.
+struct SegNode {
+  int region[6];
+  int search;    // slot in the search-node list, or -1
+  int term;      // slot in the terminal-node list, or -1
+  int child[4];  // node index of each quadrant (search nodes), else -1
 };
 
 // point t of the 4 sub-grids of the current region (fp64 centres):
@@ -1913,7 +1931,7 @@ __global__ void __launch_bounds__(256) seg_points_batch_kernel(const SegState* s
 // (one 256-thread CTA per search; the batched kernel runs this same body per
 // scan, so its decisions and trace are bit-identical to the single-scan search)
 __device__ __forceinline__ void seg_score(SegState* st, const float* e, int n_sub, int shift_min, int stop_cells,
-                                          float* lowres, mwb_seg_trace_t* tr) {
+                                          float* lowres, mwb_seg_trace_t* tr, const SegNode* nodes = nullptr) {
   __shared__ double red[8][12];
   __shared__ double fin[12];
   if (st->done) return;
@@ -1992,6 +2010,7 @@ __device__ __forceinline__ void seg_score(SegState* st, const float* e, int n_su
       st->region[3 + a] = q[sel].hi[a];
     }
     st->iter = it + 1;
+    if (nodes) st->node = nodes[st->node].child[sel];
     tr->n_records = min(it + 1, MWB_SEG_MAX_ITERS);
     const int w = q[sel].hi[0] - q[sel].lo[0] + 1, h = q[sel].hi[1] - q[sel].lo[1] + 1;
     if (max(w, h) <= stop_cells || w < 2 || h < 2) st->done = 1;
@@ -2029,6 +2048,7 @@ __device__ __forceinline__ void seg_init(SegState* st, int x0, int y0, int x1, i
   st->region[0] = x0; st->region[1] = y0; st->region[2] = 0;
   st->region[3] = x1; st->region[4] = y1; st->region[5] = 0;
   st->iter = 0;
+  st->node = 0;
   const int w = x1 - x0 + 1, h = y1 - y0 + 1;
   st->done = (max(w, h) <= stop_cells || w < 2 || h < 2) ? 1 : 0;
   tr->n_records = 0;
@@ -2054,6 +2074,75 @@ __global__ void seg_region_batch_kernel(const SegState* st, int n_scans, int32_t
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s < n_scans)
     for (int a = 0; a < 6; ++a) region_out[6 * (size_t)s + a] = st[s].region[a];
+}
+
+// ---- tree search (precomputed per-node points and delay tables) ----------
+// sub-grid points of every search node (grid = (tiles per node, search nodes))
+__global__ void __launch_bounds__(256) seg_tree_points_kernel(const SegNode* nodes, const int* search_ids,
+                                                              int per_node, double ox, double oy, double res,
+                                                              int n_sub, double* pts, int2* tile_info) {
+  const int k = blockIdx.y;
+  const int n = 4 * n_sub * n_sub;
+  const int t = blockIdx.x * TILE + threadIdx.x;
+  if (threadIdx.x == 0)
+    tile_info[(size_t)k * (per_node / TILE) + blockIdx.x] = make_int2(k, min(TILE, n - (int)blockIdx.x * TILE));
+  if (t >= n) return;
+  SegState st;
+  const SegNode& nd = nodes[search_ids[k]];
+  for (int a = 0; a < 6; ++a) st.region[a] = nd.region[a];
+  st.done = 0;
+  seg_point(&st, ox, oy, res, n_sub, t, pts + 3 * (size_t)k * per_node);
+}
+
+// launched tile (s, j) of the next search step -> tile j of scan s's node
+__device__ __forceinline__ void seg_tree_map(const SegState& st, const SegNode* nodes, int s, int j, int tps, int n,
+                                             int* tile_src, int2* tile_info) {
+  const int k = st.done ? -1 : nodes[st.node].search;
+  const size_t t = (size_t)s * tps + j;
+  tile_src[t] = k < 0 ? 0 : k * tps + j;
+  tile_info[t] = make_int2(s, k < 0 ? 0 : min(TILE, n - j * TILE));
+}
+
+__global__ void seg_tree_init_kernel(SegState* st, int n_scans, int x0, int y0, int x1, int y1, int stop_cells,
+                                     mwb_seg_trace_t* tr, const SegNode* nodes, int tps, int n, int* tile_src,
+                                     int2* tile_info) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_scans) return;
+  seg_init(st + s, x0, y0, x1, y1, stop_cells, tr + s);
+  for (int j = 0; j < tps; ++j) seg_tree_map(st[s], nodes, s, j, tps, n, tile_src, tile_info);
+}
+
+// score + move to the chosen child + map the next step's tiles (one CTA per scan)
+__global__ void __launch_bounds__(256) seg_tree_score_kernel(SegState* st, const float* e, int per_scan, int n_sub,
+                                                              int shift_min, int stop_cells, float* lowres,
+                                                              mwb_seg_trace_t* tr, const SegNode* nodes,
+                                                              int* tile_src, int2* tile_info) {
+  const int s = blockIdx.x;
+  const int lw = 4 * n_sub * n_sub;
+  seg_score(st + s, e + (size_t)s * per_scan, n_sub, shift_min, stop_cells,
+            lowres ? lowres + (size_t)s * lw : nullptr, tr + s, nodes);
+  __syncthreads();
+  const int tps = per_scan / TILE;
+  for (int j = threadIdx.x; j < tps; j += blockDim.x) seg_tree_map(st[s], nodes, s, j, tps, lw, tile_src, tile_info);
+}
+
+// fine pass: launched tile (s, j) -> tile j of the cell list of scan s's final
+// (terminal) node; regions and fine-cell counts per scan
+__global__ void seg_tree_fine_map_kernel(const SegState* st, int n_scans, const SegNode* nodes,
+                                         const int* term_counts, const int* term_offsets, int fine_tps,
+                                         int* tile_src, int2* tile_info, int32_t* region_out, int32_t* fine_counts) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n_scans * fine_tps) return;
+  const int s = (int)(i / fine_tps), j = (int)(i % fine_tps);
+  const int k = nodes[st[s].node].term;
+  const int cnt = k < 0 ? 0 : term_counts[k];
+  const bool on = j * TILE < cnt;
+  tile_src[i] = on ? term_offsets[k] / TILE + j : 0;
+  tile_info[i] = make_int2(s, on ? min(TILE, cnt - j * TILE) : 0);
+  if (j == 0) {
+    for (int a = 0; a < 6; ++a) region_out[6 * (size_t)s + a] = st[s].region[a];
+    if (fine_counts) fine_counts[s] = cnt;
+  }
 }
 
 __global__ void argmax_dense_kernel(const float* dense, const uint8_t* valid, int n,
@@ -2288,6 +2377,7 @@ static int energy_params(const float* sig, int n_scans, int64_t scan_stride, int
   p.P = n_pts;
   p.d_count = d_count;
   p.tile_info = reinterpret_cast<const int2*>(tile_info);
+  p.tile_src = nullptr;
   p.tab_words = reinterpret_cast<const uint32_t*>(base + T.words);
   p.tab_span = reinterpret_cast<const int2*>(base + T.span);
   p.tab_wide = reinterpret_cast<const int*>(base + T.wide);
@@ -2311,13 +2401,22 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
                          double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
                          const int32_t* d_count, const int32_t* tile_info, const void* table, int interp, int k0,
                          int window, float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
-                         uint64_t* key_dmas, int32_t* flags, int mode, void* stream) {
+                         uint64_t* key_dmas, int32_t* flags, int mode, void* stream,
+                         const int32_t* tile_src = nullptr, int n_src_pts = 0) {
+  // tile_src (with tile_info): launched tile t evaluates source tile tile_src[t]
+  // of a shared point list / table of n_src_pts points; n_pts counts the
+  // launched (packed output) positions
   EnergyParams p;
   bool empty;
   const int rc = energy_params(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant,
-                               inv_scale, pts_xyz, out_idx, n_pts, d_count, tile_info, table, interp, k0, window,
-                               out_das, out_dmas, out_stride, key_das, key_dmas, flags, mode, p, empty);
+                               inv_scale, pts_xyz, out_idx, tile_src ? n_src_pts : n_pts, d_count, tile_info, table,
+                               interp, k0, window, out_das, out_dmas, out_stride, key_das, key_dmas, flags, mode, p,
+                               empty);
   if (rc || empty) return rc;
+  if (tile_src) {
+    p.tile_src = tile_src;
+    p.P = n_pts;
+  }
   const long long tiles = (n_pts + TILE - 1) / TILE;
   // register chunk: 48 samples for windows that are a multiple of 48 (the
   // configs[4] W = 48 would waste a third of a 2 x 32 split), else 32
@@ -2999,6 +3098,248 @@ int mwb_segment_batch(const float* sig, int n_scans, int64_t scan_stride, int n_
   }
   seg_region_batch_kernel<<<(n_scans + 255) / 256, 256, 0, cs>>>(st, n_scans, d_regions_out);
   return check_launch("seg_region_batch_kernel");
+}
+
+// ---- batched search over a precomputed region tree -------------------------
+// The regions a search can visit depend only on the start region, the stop
+// size and the iteration bound, so for a fixed grid the sub-grid points and
+// delay tables of every search node, and the fine-pass cells and tables of
+// every terminal node, are built once (mwb_segment_plan_prepare) and shared
+// by every scan of every batch.  A run is then 2 launches per iteration
+// (energies of each scan's node tiles through tile_src; score + next map)
+// plus 2 for the fine pass, with no host synchronisation.
+struct SegTree {
+  std::vector<SegNode> nodes;
+  std::vector<int> search, term;
+  long long fine_bound = 0;  // padded fine-pass points over terminal nodes
+  int fine_tps = 0;          // most tiles of one terminal node
+};
+
+constexpr int SEG_TREE_MAX_NODES = 1 << 14;
+
+static int build_seg_tree(int x0, int y0, int x1, int y1, int stop_cells, int max_iters, SegTree& T) {
+  T = SegTree();
+  std::vector<int> depth;
+  SegNode root;
+  memset(&root, 0, sizeof(root));
+  root.region[0] = x0; root.region[1] = y0; root.region[3] = x1; root.region[4] = y1;
+  T.nodes.push_back(root);
+  depth.push_back(0);
+  for (size_t i = 0; i < T.nodes.size(); ++i) {
+    SegNode& nd = T.nodes[i];
+    const int w = nd.region[3] - nd.region[0] + 1, h = nd.region[4] - nd.region[1] + 1;
+    const bool done = max(w, h) <= stop_cells || w < 2 || h < 2;
+    for (int k = 0; k < 4; ++k) nd.child[k] = -1;
+    nd.search = nd.term = -1;
+    if (done || depth[i] >= max_iters) {
+      nd.term = (int)T.term.size();
+      T.term.push_back((int)i);
+      const long long tiles = ((long long)w * h + TILE - 1) / TILE;
+      T.fine_bound += tiles * TILE;
+      T.fine_tps = max(T.fine_tps, (int)tiles);
+      continue;
+    }
+    nd.search = (int)T.search.size();
+    T.search.push_back((int)i);
+    Box r, q[MAXCH];
+    for (int a = 0; a < 3; ++a) {
+      r.lo[a] = nd.region[a];
+      r.hi[a] = nd.region[3 + a];
+    }
+    split_box(r, 2, q);  // w, h >= 2: four quadrants
+    const int d = depth[i];
+    for (int k = 0; k < 4; ++k) {
+      if (T.nodes.size() >= (size_t)SEG_TREE_MAX_NODES) return set_err(MWB_ERANGE, "segment tree: too many regions");
+      T.nodes[i].child[k] = (int)T.nodes.size();
+      SegNode c;
+      memset(&c, 0, sizeof(c));
+      for (int a = 0; a < 3; ++a) {
+        c.region[a] = q[k].lo[a];
+        c.region[3 + a] = q[k].hi[a];
+      }
+      T.nodes.push_back(c);  // invalidates nd
+      depth.push_back(d + 1);
+    }
+  }
+  return MWB_OK;
+}
+
+struct SegPlanLayout {
+  size_t nodes, term_regions, search_ids, s_pts, s_info, s_table, r_ws, f_pts, f_idx, f_info, f_table, total;
+};
+
+static SegPlanLayout seg_plan_layout(const SegTree& T, int per_node, int n_chan) {
+  SegPlanLayout L;
+  const long long ns = (long long)T.search.size(), nt = (long long)T.term.size();
+  const long long s_pts = ns * per_node;
+  size_t o = 0;
+  L.nodes = o;        o = align_up(o + sizeof(SegNode) * T.nodes.size(), 256);
+  L.term_regions = o; o = align_up(o + sizeof(int) * 6 * (size_t)nt, 256);
+  L.search_ids = o;   o = align_up(o + sizeof(int) * (size_t)ns, 256);
+  L.s_pts = o;        o = align_up(o + 24 * (size_t)s_pts, 256);
+  L.s_info = o;       o = align_up(o + 8 * (size_t)(s_pts / TILE), 256);
+  L.s_table = o;      o += table_layout(s_pts / TILE, n_chan).total;
+  L.r_ws = o;         o = align_up(o + (size_t)mwb_regions_workspace_bytes((int)nt), 256);
+  L.f_pts = o;        o = align_up(o + 24 * (size_t)T.fine_bound, 256);
+  L.f_idx = o;        o = align_up(o + 4 * (size_t)T.fine_bound, 256);
+  L.f_info = o;       o = align_up(o + 8 * (size_t)(T.fine_bound / TILE), 256);
+  L.f_table = o;      o += table_layout(T.fine_bound / TILE, n_chan).total;
+  L.total = o;
+  return L;
+}
+
+static int seg_tree_args(int nx, int ny, int x0, int y0, int x1, int y1, int n_sub, int stop_cells, int max_iters,
+                         const char* who) {
+  if (n_sub < 1 || n_sub > 64 || stop_cells < 1 || max_iters < 0 || max_iters > MWB_SEG_MAX_ITERS)
+    return set_err(MWB_EINVAL, "%s: bad n_sub / stop_cells / max_iters", who);
+  if (nx < 1 || ny < 1 || x0 < 0 || y0 < 0 || x1 >= nx || y1 >= ny || x0 > x1 || y0 > y1)
+    return set_err(MWB_EINVAL, "%s: region outside the grid", who);
+  return MWB_OK;
+}
+
+int mwb_segment_plan_info(int nx, int ny, int x0, int y0, int x1, int y1, int n_sub, int stop_cells,
+                          int max_iters, int n_chan, int64_t* info) {
+  int rc = seg_tree_args(nx, ny, x0, y0, x1, y1, n_sub, stop_cells, max_iters, "mwb_segment_plan_info");
+  if (rc) return rc;
+  if (n_chan < 1 || !info) return set_err(MWB_EINVAL, "mwb_segment_plan_info: bad n_chan / null info");
+  SegTree T;
+  if ((rc = build_seg_tree(x0, y0, x1, y1, stop_cells, max_iters, T))) return rc;
+  const int per = (int)seg_batch_per_scan(n_sub);
+  info[0] = (int64_t)seg_plan_layout(T, per, n_chan).total;
+  info[1] = (int64_t)T.search.size();
+  info[2] = (int64_t)T.term.size();
+  info[3] = (int64_t)T.fine_tps;
+  return MWB_OK;
+}
+
+int mwb_segment_plan_prepare(const int32_t* chan_txrx, int n_chan, const double* ant_xyz, int n_ant,
+                             double inv_scale, int interp, double ox, double oy, double res, int nx, int ny,
+                             int x0, int y0, int x1, int y1, const uint8_t* mask, int n_sub, int stop_cells,
+                             int max_iters, void* plan, void* stream) {
+  int rc = seg_tree_args(nx, ny, x0, y0, x1, y1, n_sub, stop_cells, max_iters, "mwb_segment_plan_prepare");
+  if (rc) return rc;
+  if (!chan_txrx || !ant_xyz || !plan || n_chan < 1) return set_err(MWB_EINVAL, "mwb_segment_plan_prepare: null pointer");
+  SegTree T;
+  if ((rc = build_seg_tree(x0, y0, x1, y1, stop_cells, max_iters, T))) return rc;
+  const int per = (int)seg_batch_per_scan(n_sub);
+  const SegPlanLayout L = seg_plan_layout(T, per, n_chan);
+  unsigned char* base = reinterpret_cast<unsigned char*>(plan);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  // nodes, search-node ids and terminal regions: one host->device copy
+  std::vector<unsigned char> blob(L.s_pts);
+  memcpy(blob.data() + L.nodes, T.nodes.data(), sizeof(SegNode) * T.nodes.size());
+  int* treg = reinterpret_cast<int*>(blob.data() + L.term_regions);
+  for (size_t k = 0; k < T.term.size(); ++k)
+    for (int a = 0; a < 6; ++a) treg[6 * k + a] = T.nodes[T.term[k]].region[a];
+  if (!T.search.empty()) memcpy(blob.data() + L.search_ids, T.search.data(), sizeof(int) * T.search.size());
+  const int* d_search_ids = reinterpret_cast<const int*>(base + L.search_ids);
+  cudaError_t e = cudaMemcpyAsync(base, blob.data(), blob.size(), cudaMemcpyHostToDevice, cs);
+  if (e != cudaSuccess) return set_err(MWB_ECUDA, "mwb_segment_plan_prepare: %s", cudaGetErrorString(e));
+  const SegNode* nodes = reinterpret_cast<const SegNode*>(base + L.nodes);
+  // search nodes: sub-grid points + delay table
+  const long long s_pts = (long long)T.search.size() * per;
+  if (s_pts > 0) {
+    int2* s_info = reinterpret_cast<int2*>(base + L.s_info);
+    seg_tree_points_kernel<<<dim3((unsigned)(per / TILE), (unsigned)T.search.size()), TILE, 0, cs>>>(
+        nodes, d_search_ids, per, ox, oy, res, n_sub, reinterpret_cast<double*>(base + L.s_pts), s_info);
+    if ((rc = check_launch("seg_tree_points_kernel"))) return rc;
+    if ((rc = mwb_delay_table_tiles(reinterpret_cast<double*>(base + L.s_pts), (int)s_pts,
+                                    reinterpret_cast<const int32_t*>(s_info), chan_txrx, n_chan, ant_xyz, n_ant,
+                                    inv_scale, interp, base + L.s_table, stream)))
+      return rc;
+  }
+  // terminal nodes: fine-pass cells (region & mask) + delay table
+  const int nt = (int)T.term.size();
+  const int32_t* d_treg = reinterpret_cast<const int32_t*>(base + L.term_regions);
+  cudaMemsetAsync(base + L.f_info, 0, 8 * (size_t)(T.fine_bound / TILE), cs);
+  RegionBatch b = region_batch(base + L.r_ws, nt);
+  LatticeParams lp = region_params(ox, oy, res, nx, ny, d_treg, mask, 0);
+  region_count_kernel<<<nt, 256, 0, cs>>>(lp, b);
+  region_offsets_kernel<<<1, 1024, 0, cs>>>(b);
+  lp.pts = reinterpret_cast<double*>(base + L.f_pts);
+  lp.out_idx = reinterpret_cast<int*>(base + L.f_idx);
+  region_write_kernel<<<nt, 256, 0, cs>>>(lp, b, reinterpret_cast<int2*>(base + L.f_info));
+  if ((rc = check_launch("segment plan: terminal cells"))) return rc;
+  if ((rc = mwb_delay_table_tiles(reinterpret_cast<double*>(base + L.f_pts), (int)T.fine_bound,
+                                  reinterpret_cast<const int32_t*>(base + L.f_info), chan_txrx, n_chan, ant_xyz,
+                                  n_ant, inv_scale, interp, base + L.f_table, stream)))
+    return rc;
+  // the host blob must outlive its async copy
+  e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) return set_err(MWB_ECUDA, "mwb_segment_plan_prepare: %s", cudaGetErrorString(e));
+  return MWB_OK;
+}
+
+int64_t mwb_segment_run_workspace_bytes(int n_scans, int n_sub, int fine_tps) {
+  if (n_scans < 1 || n_scans > 65535 || n_sub < 1 || n_sub > 64 || fine_tps < 0) return -1;
+  const long long per = seg_batch_per_scan(n_sub), n = per * n_scans;
+  const long long ft = (long long)n_scans * fine_tps;
+  return (long long)align_up(sizeof(SegState) * (size_t)n_scans, 256) + (long long)align_up(4 * n, 256) +
+         (long long)align_up(4 * (n / TILE), 256) + (long long)align_up(8 * (n / TILE), 256) +
+         (long long)align_up(4 * ft, 256) + (long long)align_up(8 * ft, 256);
+}
+
+int mwb_segment_run(const void* plan, const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
+                    int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale,
+                    int interp, int k0, int window, int kind, int nx, int ny, int x0, int y0, int x1, int y1,
+                    int n_sub, int stop_cells, int max_iters, int32_t* d_regions_out, float* lowres,
+                    mwb_seg_trace_t* d_traces, float* out_fine, int64_t out_stride, uint64_t* keys,
+                    int32_t* fine_counts, int32_t* flags, void* workspace, void* stream) {
+  int rc = seg_tree_args(nx, ny, x0, y0, x1, y1, n_sub, stop_cells, max_iters, "mwb_segment_run");
+  if (rc) return rc;
+  if (n_scans < 1 || n_scans > 65535) return set_err(MWB_EINVAL, "mwb_segment_run: n_scans must be in [1, 65535]");
+  if (kind != MWB_DAS && kind != MWB_DMAS) return set_err(MWB_EINVAL, "mwb_segment_run: bad kind");
+  if (!plan || !d_regions_out || !d_traces || !out_fine || !workspace)
+    return set_err(MWB_EINVAL, "mwb_segment_run: null pointer");
+  if (out_stride < (int64_t)nx * ny) return set_err(MWB_EINVAL, "mwb_segment_run: out_stride < nx * ny");
+  SegTree T;
+  if ((rc = build_seg_tree(x0, y0, x1, y1, stop_cells, max_iters, T))) return rc;
+  const long long per = seg_batch_per_scan(n_sub), n = per * n_scans;
+  const int tps = (int)(per / TILE), lw = 4 * n_sub * n_sub;
+  const long long ft = (long long)n_scans * T.fine_tps;
+  if (n > 0x7FFFFFFFLL || ft * TILE > 0x7FFFFFFFLL) return set_err(MWB_ERANGE, "mwb_segment_run: batch too large");
+  const SegPlanLayout L = seg_plan_layout(T, (int)per, n_chan);
+  const unsigned char* pb = reinterpret_cast<const unsigned char*>(plan);
+  const SegNode* nodes = reinterpret_cast<const SegNode*>(pb + L.nodes);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  SegState* st = reinterpret_cast<SegState*>(ws);
+  ws += align_up(sizeof(SegState) * (size_t)n_scans, 256);
+  float* e = reinterpret_cast<float*>(ws);
+  ws += align_up(4 * n, 256);
+  int* s_src = reinterpret_cast<int*>(ws);
+  ws += align_up(4 * (n / TILE), 256);
+  int2* s_info = reinterpret_cast<int2*>(ws);
+  ws += align_up(8 * (n / TILE), 256);
+  int* f_src = reinterpret_cast<int*>(ws);
+  ws += align_up(4 * ft, 256);
+  int2* f_info = reinterpret_cast<int2*>(ws);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  seg_tree_init_kernel<<<(n_scans + 255) / 256, 256, 0, cs>>>(st, n_scans, x0, y0, x1, y1, stop_cells, d_traces,
+                                                               nodes, tps, lw, s_src, s_info);
+  if ((rc = check_launch("seg_tree_init_kernel"))) return rc;
+  const long long s_pts = (long long)T.search.size() * per;
+  for (int it = 0; it < max_iters && s_pts > 0; ++it) {
+    if ((rc = energies_impl(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
+                            reinterpret_cast<const double*>(pb + L.s_pts), nullptr, (int)n, nullptr,
+                            reinterpret_cast<const int32_t*>(s_info), pb + L.s_table, interp, k0, window,
+                            kind == MWB_DAS ? e : nullptr, kind == MWB_DMAS ? e : nullptr, 0, nullptr, nullptr,
+                            nullptr, 0, stream, s_src, (int)s_pts)))
+      return rc;
+    seg_tree_score_kernel<<<n_scans, 256, 0, cs>>>(st, e, (int)per, n_sub, kind == MWB_DMAS, stop_cells, lowres,
+                                                   d_traces, nodes, s_src, s_info);
+    if ((rc = check_launch("seg_tree_score_kernel"))) return rc;
+  }
+  const RegionBatch b = region_batch(const_cast<unsigned char*>(pb) + L.r_ws, (int)T.term.size());
+  seg_tree_fine_map_kernel<<<(unsigned)((ft + 255) / 256 + (ft == 0)), 256, 0, cs>>>(
+      st, n_scans, nodes, b.scan_counts, b.scan_offsets, T.fine_tps, f_src, f_info, d_regions_out, fine_counts);
+  if ((rc = check_launch("seg_tree_fine_map_kernel"))) return rc;
+  if (ft == 0 || T.fine_bound == 0) return MWB_OK;
+  return energies_impl(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
+                       reinterpret_cast<const double*>(pb + L.f_pts), reinterpret_cast<const int32_t*>(pb + L.f_idx),
+                       (int)(ft * TILE), nullptr, reinterpret_cast<const int32_t*>(f_info), pb + L.f_table, interp,
+                       k0, window, kind == MWB_DAS ? out_fine : nullptr, kind == MWB_DMAS ? out_fine : nullptr,
+                       out_stride, kind == MWB_DAS ? keys : nullptr, kind == MWB_DMAS ? keys : nullptr, flags, 0,
+                       stream, f_src, (int)T.fine_bound);
 }
 
 // One-call lattice image (beamform.py:283-342 as a single C entry point): the

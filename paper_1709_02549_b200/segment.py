@@ -24,6 +24,7 @@ result once.
 
 from __future__ import annotations
 
+import ctypes as C
 import hashlib
 import math
 from collections import OrderedDict
@@ -324,18 +325,27 @@ class SegmentBatch:
     """``segment`` for S scans that share the antenna geometry, the grid and the
     start region (BASELINE configs[2] at batch throughput).
 
-    One ``mwb_segment_batch`` call runs every scan's quadrant search (four
-    launches per iteration for the whole batch); the full-resolution pass over
-    each scan's final segment is one packed launch (``mwb_enumerate_regions_*``
-    + ``mwb_delay_table_tiles`` + ``mwb_energies_tiles``, as in FrameworkBatch).
-    Regions, traces, fine energies and argmax cells are bit-identical to
-    calling ``segment`` once per scan.  One host synchronisation per batch (to
-    size the packed fine list).
+    The regions a search can visit depend only on the grid, start region and
+    stop size, so the constructor builds a region-tree plan once
+    (``mwb_segment_plan_prepare``): the sub-grid points and delay tables of
+    every region that gets split, and the fine-pass cells and tables of every
+    region a search can end in.  ``run`` is then one ``mwb_segment_run`` call:
+    two launches per iteration for the whole batch and two for the fine pass,
+    no host synchronisation until the results are read.
+
+    When the tree is too large (tiny stop sizes), or with ``tree=False``, each
+    iteration builds its own points and tables (``mwb_segment_batch``) and the
+    fine pass is one packed launch (``mwb_enumerate_regions_*`` +
+    ``mwb_delay_table_tiles`` + ``mwb_energies_tiles``, as in FrameworkBatch),
+    with one host synchronisation to size the packed list.
+
+    Either way, regions, traces, low-res images, fine energies and argmax cells
+    are bit-identical to calling ``segment`` once per scan.
     """
 
     def __init__(self, geometry: ArrayGeometry, pairs, n_samples: int, grid: ImagingGrid, kind, n_sub: int = 16,
                  stop_size: float = 0.01, *, region: Region | None = None, mask="breast", window=None,
-                 interpolation: str = "linear"):
+                 interpolation: str = "linear", tree: bool = True):
         _check_interpolation(interpolation)
         if not stop_size > 0:
             raise ValueError("stop_size must be > 0")
@@ -368,6 +378,23 @@ class SegmentBatch:
             n_samples=self.n_samples, ld=self.ld, n_ant=geometry.n_antennas, chan_host=pairs)
         self.mask_np, self.mask_t, _ = _mask_for(grid, mask)
         self._ws = None
+        # region tree plan (search-node points/tables, terminal-node cells/tables),
+        # unless the tree is too large: then every iteration builds its own table
+        lib = nat.load()
+        nx, ny = grid.dims
+        x0, y0, x1, y1 = self.region.bounds()
+        info = (C.c_int64 * 4)()
+        self.plan = None
+        self.fine_tps = 0
+        if tree and lib.mwb_segment_plan_info(nx, ny, x0, y0, x1, y1, self.n_sub, self.stop_cells, self.n_iter, self.n_chan,
+                                     info) == 0:
+            self.plan = torch.empty(int(info[0]), dtype=torch.uint8, device=dev)
+            self.fine_tps = int(info[3])
+            sc = self.scan
+            nat.call("mwb_segment_plan_prepare", sc.chan.data_ptr(), self.n_chan, sc.ant.data_ptr(), sc.n_ant,
+                     sc.inv_scale, self.interp, grid.origin[0], grid.origin[1], grid.resolution, nx, ny, x0, y0, x1,
+                     y1, self.mask_t.data_ptr() if self.mask_t is not None else None, self.n_sub, self.stop_cells,
+                     self.n_iter, self.plan.data_ptr(), dv.stream_handle())
 
     @property
     def n_chan(self) -> int:
@@ -387,7 +414,10 @@ class SegmentBatch:
         stream = dv.stream_handle()
         sc = self.scan
         n_low = (2 * self.n_sub) ** 2
-        ws_bytes = int(lib.mwb_segment_batch_workspace_bytes(s_n, self.n_sub, self.n_chan))
+        if self.plan is not None:
+            ws_bytes = int(lib.mwb_segment_run_workspace_bytes(s_n, self.n_sub, self.fine_tps))
+        else:
+            ws_bytes = int(lib.mwb_segment_batch_workspace_bytes(s_n, self.n_sub, self.n_chan))
         if self._ws is None or self._ws.numel() < ws_bytes:
             self._ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         regions = torch.empty((s_n, 6), dtype=torch.int32, device=dev)
@@ -398,6 +428,8 @@ class SegmentBatch:
         flags = torch.zeros(1, dtype=torch.int32, device=dev)
         das = self.kcode == nat.MWB_DAS
         x0, y0, x1, y1 = self.region.bounds()
+        if self.plan is not None:
+            return self._run_tree(sig, regions, traces, lowres, dense, keys, flags)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record()
         nat.call("mwb_segment_batch", sig.data_ptr(), s_n, self.n_chan * self.ld, self.n_chan, self.ld,
@@ -430,7 +462,29 @@ class SegmentBatch:
                      None if das else dense.data_ptr(), nx * ny, keys.data_ptr() if das else None,
                      None if das else keys.data_ptr(), flags.data_ptr(), 0, stream)
         ev[2].record()
-        fine_counts, st, reg, k, n_rec = dv.to_host(rws.view(torch.int32)[:s_n], flags, regions, keys,
+        return self._result(s_n, rws.view(torch.int32)[:s_n], flags, regions, keys, traces, lowres, dense, ev)
+
+    def _run_tree(self, sig, regions, traces, lowres, dense, keys, flags) -> SegmentBatchResult:
+        s_n = int(sig.shape[0])
+        grid = self.grid
+        nx, ny = grid.dims
+        sc = self.scan
+        x0, y0, x1, y1 = self.region.bounds()
+        counts = torch.empty(s_n, dtype=torch.int32, device=dv.device())
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        nat.call("mwb_segment_run", self.plan.data_ptr(), sig.data_ptr(), s_n, self.n_chan * self.ld, self.n_chan,
+                 self.ld, self.n_samples, sc.chan.data_ptr(), sc.ant.data_ptr(), sc.n_ant, sc.inv_scale, self.interp,
+                 self.k0, self.w, self.kcode, nx, ny, x0, y0, x1, y1, self.n_sub, self.stop_cells, self.n_iter,
+                 regions.data_ptr(), lowres.data_ptr(), traces.data_ptr(), dense.data_ptr(), nx * ny,
+                 keys.data_ptr(), counts.data_ptr(), flags.data_ptr(), self._ws.data_ptr(), dv.stream_handle())
+        ev[1].record()
+        return self._result(s_n, counts, flags, regions, keys, traces, lowres, dense, ev)
+
+    def _result(self, s_n, counts_t, flags, regions, keys, traces, lowres, dense, ev) -> SegmentBatchResult:
+        grid = self.grid
+        nx, ny = grid.dims
+        fine_counts, st, reg, k, n_rec = dv.to_host(counts_t, flags, regions, keys,
                                                      traces.view(s_n, -1)[:, :4].contiguous().view(torch.int32))
         if int(st[0]) & 1:
             raise ValueError("energy map contains non-finite values")
@@ -443,8 +497,11 @@ class SegmentBatch:
         iters = n_rec.reshape(s_n).astype(np.int64)
         EVAL_COUNTER.add(int(fine_counts.sum()) + 4 * self.n_sub * self.n_sub * int(iters.sum()))
         full_eq = int(self.mask_np.sum()) if self.mask_np is not None else nx * ny
-        elapsed = {"search": ev[0].elapsed_time(ev[1]) / 1e3, "fine": ev[1].elapsed_time(ev[2]) / 1e3}
-        elapsed["total"] = elapsed["search"] + elapsed["fine"]
+        if len(ev) == 3:
+            elapsed = {"search": ev[0].elapsed_time(ev[1]) / 1e3, "fine": ev[1].elapsed_time(ev[2]) / 1e3}
+            elapsed["total"] = elapsed["search"] + elapsed["fine"]
+        else:  # tree plan: search and fine pass in one call
+            elapsed = {"total": ev[0].elapsed_time(ev[1]) / 1e3}
         return SegmentBatchResult(
             grid=grid, kind=self.kind.value, n_sub=self.n_sub, final_regions=reg[:, [0, 1, 3, 4]],
             argmax_cells=cells, iterations=iters, fine_points_evaluated=fine_counts, full_equivalent_points=full_eq,

@@ -16,8 +16,8 @@ from paper_1709_02549_b200.segment import SegmentBatch, segment
 m2 = synth.ScanModel(n_samples=2048)
 g2 = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 2.5e-4)
 sig2, _ = synth.batch_2d_device(m2, range(4096), phantom_radius=(0.04, 0.05))
-for kind in ("das", "dmas"):
-    sb = SegmentBatch(m2.geometry(), m2.pairs(), m2.n_samples, g2, kind, 16, 0.01, window=(m2.k0, 32))
+for kind, tree in (("das", True), ("dmas", True), ("das", False)):
+    sb = SegmentBatch(m2.geometry(), m2.pairs(), m2.n_samples, g2, kind, 16, 0.01, window=(m2.k0, 32), tree=tree)
     res = sb.run(sig2)
     torch.cuda.synchronize()
     walls, el = [], []
@@ -26,8 +26,8 @@ for kind in ("das", "dmas"):
         res = sb.run(sig2)
         walls.append((time.perf_counter() - t0) * 1e3)
         el.append(res.elapsed)
-    print(kind, "wall ms", statistics.median(walls), "search ms", statistics.median(e["search"] * 1e3 for e in el),
-          "fine ms", statistics.median(e["fine"] * 1e3 for e in el), "iters", res.iterations[:8].tolist(),
+    print(kind, "tree" if tree else "per-iteration", "wall ms", statistics.median(walls),
+          {k: statistics.median(e[k] * 1e3 for e in el) for k in el[0]}, "iters", res.iterations[:8].tolist(),
           "fine pts mean", float(res.fine_points_evaluated.mean()))
 ds2, _ = synth.dataset_2d(m2, seed=1000, phantom_radius=0.05)
 for kind in ("das", "dmas"):

@@ -79,8 +79,8 @@ def _records_equal(a, b):
                 for r in b])
 
 
-@pytest.mark.parametrize("kind", ["das", "dmas"])
-def test_segment_batch_equals_per_scan_segment(kind):
+@pytest.mark.parametrize("kind,tree", [("das", True), ("dmas", True), ("das", False), ("dmas", False)])
+def test_segment_batch_equals_per_scan_segment(kind, tree):
     """SegmentBatch reproduces segment() scan by scan, bit for bit: records
     (scores, maxima, means, shift), final segment, low-res image, fine map,
     argmax and counters."""
@@ -93,7 +93,8 @@ def test_segment_batch_equals_per_scan_segment(kind):
     sig, _ = synth.batch_2d(model, seeds, phantom_radius=(0.04, 0.05), snr_db=(15.0, 30.0))
     grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 2.5e-4)
     sb = SegmentBatch(model.geometry(), model.pairs(), model.n_samples, grid, kind, 16, 0.01,
-                      window=(model.k0, model.window))
+                      window=(model.k0, model.window), tree=tree)
+    assert (sb.plan is not None) == tree
     before = mw.EVAL_COUNTER.value
     res = sb.run(torch.from_numpy(sig).cuda())
     counted = mw.EVAL_COUNTER.value - before
@@ -113,7 +114,8 @@ def test_segment_batch_equals_per_scan_segment(kind):
     assert counted == total
 
 
-def test_segment_batch_start_region_already_small_and_no_mask():
+@pytest.mark.parametrize("tree", [True, False])
+def test_segment_batch_start_region_already_small_and_no_mask(tree):
     import torch
 
     from paper_1709_02549_b200.segment import SegmentBatch
@@ -121,7 +123,8 @@ def test_segment_batch_start_region_already_small_and_no_mask():
     model = synth.ScanModel(n_samples=512)
     sig, _ = synth.batch_2d(model, [1, 2, 3], phantom_radius=(0.04, 0.05))
     grid = mw.ImagingGrid((-0.005, -0.005), (0.01, 0.01), 2.5e-4)  # already a 1 cm segment
-    sb = SegmentBatch(model.geometry(), model.pairs(), model.n_samples, grid, "das", window=(model.k0, 32), mask=None)
+    sb = SegmentBatch(model.geometry(), model.pairs(), model.n_samples, grid, "das", window=(model.k0, 32), mask=None,
+                      tree=tree)
     res = sb.run(torch.from_numpy(sig).cuda())
     assert (res.iterations == 0).all() and (res.fine_points_evaluated == 1600).all()
     for s in range(3):
@@ -166,3 +169,29 @@ def test_graph_replay_is_identical_and_per_dataset():
         assert _records_equal(r0.records, r1.records) and r0.argmax_cell == r1.argmax_cell
         assert np.array_equal(r0.lowres, r1.lowres)
     assert first[0][1].argmax_cell != first[1][1].argmax_cell or first[0][0].entries != first[1][0].entries
+
+
+def test_segment_batch_odd_region_and_small_stop():
+    """A ragged start region (odd sides: quadrants of unequal size, searches
+    ending at different depths) and a deeper tree, tree plan vs per-iteration
+    path vs segment(); also a region that is not the whole grid."""
+    import torch
+
+    from paper_1709_02549_b200.segment import SegmentBatch
+
+    model = synth.ScanModel(n_samples=1024)
+    seeds = [5, 6, 7, 8]
+    sig, _ = synth.batch_2d(model, seeds, phantom_radius=(0.04, 0.05))
+    grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 5e-4)
+    region = mw.Region((3, 11), (190, 170))
+    win = (model.k0, model.window)
+    res = [SegmentBatch(model.geometry(), model.pairs(), model.n_samples, grid, "dmas", 8, 0.004, region=region,
+                        window=win, tree=t).run(torch.from_numpy(sig).cuda()) for t in (True, False)]
+    for s in range(len(seeds)):
+        ds = mw.BackscatterDataset(model.geometry(), synth.embed_pairs(12, model.pairs(), sig[s].astype(np.float64)))
+        fine, rep = segment(ds, "dmas", grid, 8, 0.004, region=region, window=win)
+        for r in res:
+            assert r.final_region(s) == rep.final_region
+            assert _records_equal(r.records(s), rep.records)
+            assert tuple(r.argmax_cells[s]) == rep.argmax_cell
+            assert r.fine(s).entries == fine.entries
