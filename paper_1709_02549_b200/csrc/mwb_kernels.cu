@@ -559,16 +559,16 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
   // source tile of the points / table (a shared, precomputed list) and the
   // packed output position; the same tile unless tile_src remaps it
   const size_t tile = p.tile_src ? (size_t)__ldg(p.tile_src + blockIdx.x) : (size_t)blockIdx.x;
-  const int src0 = (int)tile * TILE;
   const bool wide = __ldg(p.tab_wide + tile) != 0;
   const uint32_t* tw = p.tab_words + tile * (size_t)p.C * TILE;
   const int2* tsp = p.tab_span + tile * (size_t)p.C;
 
   const int la = tid, lb = tid + TPB;
   const bool va = la < n_in_tile, vb = lb < n_in_tile;
-  const int ga = src0 + (va ? la : 0), gb = src0 + (vb ? lb : 0);
-  const int oa = va ? (p.out_idx ? __ldg(p.out_idx + ga) : tile0 + la) : -1;
-  const int ob = vb ? (p.out_idx ? __ldg(p.out_idx + gb) : tile0 + lb) : -1;
+  // (source point indices are re-derived in the gather path below: keeping
+  // them live across the sample loop costs the register-capped kernels spills)
+  const int oa = va ? (p.out_idx ? __ldg(p.out_idx + (int)tile * TILE + la) : tile0 + la) : -1;
+  const int ob = vb ? (p.out_idx ? __ldg(p.out_idx + (int)tile * TILE + lb) : tile0 + lb) : -1;
 
   // ---- per-channel spans and stage-buffer groups --------------------------
   for (int c = tid; c < p.C; c += TPB) {
@@ -712,6 +712,8 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
     } else {
       // L1/L2 gather path (mode 1 or a tile whose delay spread exceeds the table):
       // same weights, loads straight from global with a zero tail.
+      const int src0 = (p.tile_src ? __ldg(p.tile_src + blockIdx.x) : (int)blockIdx.x) * TILE;
+      const int ga = src0 + (va ? la : 0), gb = src0 + (vb ? lb : 0);
       const double pax = p.pts[3 * (size_t)ga], pay = p.pts[3 * (size_t)ga + 1], paz = p.pts[3 * (size_t)ga + 2];
       const double pbx = p.pts[3 * (size_t)gb], pby = p.pts[3 * (size_t)gb + 1], pbz = p.pts[3 * (size_t)gb + 2];
       for (int c = 0; c < p.C; ++c) {
