@@ -113,24 +113,64 @@ def max_iterations(region: Region, stop_cells: int) -> int:
     return n
 
 
+_TREE_PLANS: "OrderedDict[tuple, tuple]" = OrderedDict()
+_TREE_PLAN_CAPACITY = 4
+
+
+def _tree_plan(scan: dv.DeviceScan, antennas, grid: ImagingGrid, region: Region, mask_key, mask_t, n_sub: int,
+               stop_cells: int, n_iter: int, interp: int):
+    """(plan tensor, fine tiles per scan) of the region tree for one geometry,
+    grid, mask and search configuration, shared by every scan (LRU); None when
+    the tree is too large for a plan."""
+    ants = np.ascontiguousarray(np.asarray(antennas, dtype=np.float64)).tobytes()
+    key = (torch.cuda.current_device(), ants, scan.chan_host.tobytes(), float(scan.inv_scale), tuple(grid.origin),
+           float(grid.resolution), tuple(grid.dims), region.bounds(), mask_key, n_sub, stop_cells, n_iter, interp)
+    if key in _TREE_PLANS:
+        _TREE_PLANS.move_to_end(key)
+        return _TREE_PLANS[key]
+    lib = nat.load()
+    nx, ny = grid.dims
+    x0, y0, x1, y1 = region.bounds()
+    info = (C.c_int64 * 4)()
+    ent = None
+    if lib.mwb_segment_plan_info(nx, ny, x0, y0, x1, y1, n_sub, stop_cells, n_iter, scan.n_chan, info) == 0:
+        plan = torch.empty(int(info[0]), dtype=torch.uint8, device=dv.device())
+        nat.call("mwb_segment_plan_prepare", scan.chan.data_ptr(), scan.n_chan, scan.ant.data_ptr(), scan.n_ant,
+                 scan.inv_scale, interp, grid.origin[0], grid.origin[1], grid.resolution, nx, ny, x0, y0, x1, y1,
+                 mask_t.data_ptr() if mask_t is not None else None, n_sub, stop_cells, n_iter, plan.data_ptr(),
+                 dv.stream_handle())
+        ent = (plan, int(info[3]))
+    _TREE_PLANS[key] = ent
+    while len(_TREE_PLANS) > _TREE_PLAN_CAPACITY:
+        _TREE_PLANS.popitem(last=False)
+    return ent
+
+
 class _SegmentPlan:
-    """One segment() configuration on one device scan, captured as a CUDA graph
-    (the search's 4 launches per iteration and the fine lattice pass); later
-    calls replay it and read the results back into pinned buffers with one
-    synchronisation.  Buffers persist with the plan, so a replay allocates
-    nothing (as coarse2fine._FrameworkPlan)."""
+    """One segment() configuration on one device scan, captured as a CUDA graph;
+    later calls replay it and read the results back into pinned buffers with
+    one synchronisation.  Buffers persist with the plan, so a replay allocates
+    nothing (as coarse2fine._FrameworkPlan).
+
+    With a region-tree plan (shared by every scan of the geometry and grid) the
+    graph is one mwb_segment_run for this scan: two launches per iteration plus
+    two for the fine pass, exactly SegmentBatch's routine for S = 1.  Without
+    one (trees above 16384 regions) it is mwb_segment plus a lattice pass."""
 
     def __init__(self, scan: dv.DeviceScan, grid: ImagingGrid, region: Region, kcode: int, n_sub: int,
-                 stop_cells: int, n_iter: int, interp: int, k0: int, w: int, mask_np, mask_t):
+                 stop_cells: int, n_iter: int, interp: int, k0: int, w: int, mask_np, mask_t, tree):
         self.scan, self.grid, self.region, self.kcode = scan, grid, region, kcode
         self.n_sub, self.stop_cells, self.n_iter = n_sub, stop_cells, n_iter
         self.interp, self.k0, self.w = interp, k0, w
         self.mask_np, self.mask_t = mask_np, mask_t
+        self.tree = tree
         nx, ny = grid.dims
         dev = dv.device()
         n_low = (2 * n_sub) ** 2
-        self.ws = torch.empty(int(nat.load().mwb_segment_workspace_bytes(n_sub, scan.n_chan)), dtype=torch.uint8,
-                              device=dev)
+        lib = nat.load()
+        ws_bytes = (lib.mwb_segment_run_workspace_bytes(1, n_sub, tree[1]) if tree is not None
+                    else lib.mwb_segment_workspace_bytes(n_sub, scan.n_chan))
+        self.ws = torch.empty(int(ws_bytes), dtype=torch.uint8, device=dev)
         self.region_t = torch.zeros(6, dtype=torch.int32, device=dev)
         self.lowres = torch.zeros(n_low, dtype=torch.float32, device=dev)
         self.trace_t = torch.zeros(nat.SEG_TRACE_BYTES, dtype=torch.uint8, device=dev)
@@ -151,9 +191,20 @@ class _SegmentPlan:
         nx, ny = grid.dims
         x0, y0, x1, y1 = self.region.bounds()
         ev = self.events
-        self.valid.zero_()
         self.status.t.zero_()
         self.lowres.zero_()
+        if self.tree is not None:
+            ev[0].record()
+            das = self.kcode == nat.MWB_DAS
+            nat.call("mwb_segment_run", self.tree[0].data_ptr(), sc.sig.data_ptr(), 1, sc.n_chan * sc.ld, sc.n_chan,
+                     sc.ld, sc.n_samples, sc.chan.data_ptr(), sc.ant.data_ptr(), sc.n_ant, sc.inv_scale,
+                     self.interp, self.k0, self.w, self.kcode, nx, ny, x0, y0, x1, y1, self.n_sub, self.stop_cells,
+                     self.n_iter, self.region_t.data_ptr(), self.lowres.data_ptr(), self.trace_t.data_ptr(),
+                     self.dense.data_ptr(), nx * ny, self.status.key_ptr(0 if das else 1), self.status.count_ptr(0),
+                     self.status.flags_ptr, self.ws.data_ptr(), dv.stream_handle())
+            ev[1].record()
+            return
+        self.valid.zero_()
         ev[0].record()
         nat.call("mwb_segment", sc.sig.data_ptr(), sc.n_chan, sc.ld, sc.n_samples, sc.chan.data_ptr(),
                  sc.ant.data_ptr(), sc.n_ant, sc.inv_scale, self.interp, self.k0, self.w, self.kcode, grid.origin[0],
@@ -174,8 +225,11 @@ class _SegmentPlan:
                 self._enqueue()
             self.graph = graph
         self.graph.replay()
-        for src, dst in ((self.status.t, self.h_status), (self.trace_t, self.h_trace), (self.dense, self.h_dense),
-                         (self.valid, self.h_valid), (self.lowres, self.h_lowres)):
+        pairs = [(self.status.t, self.h_status), (self.trace_t, self.h_trace), (self.dense, self.h_dense),
+                 (self.lowres, self.h_lowres)]
+        if self.tree is None:
+            pairs.append((self.valid, self.h_valid))
+        for src, dst in pairs:
             dst.copy_(src, non_blocking=True)
 
     def finish(self, kind) -> tuple[EnergyMap, SegmentReport]:
@@ -190,7 +244,14 @@ class _SegmentPlan:
         n_sub = self.n_sub
         EVAL_COUNTER.add(n_fine + 4 * n_sub * n_sub * len(records))
         vals = self.h_dense.numpy().reshape(nx, ny).copy()  # the plan's pinned buffers are reused
-        vmask = self.h_valid.numpy().reshape(nx, ny).view(bool).copy()
+        if self.tree is None:
+            vmask = self.h_valid.numpy().reshape(nx, ny).view(bool).copy()
+        else:  # the final region's cells that pass the mask
+            vmask = np.zeros((nx, ny), dtype=bool)
+            (fx0, fy0), (fx1, fy1) = final.min_cell, final.max_cell
+            vmask[fx0 : fx1 + 1, fy0 : fy1 + 1] = True
+            if self.mask_np is not None:
+                vmask &= self.mask_np
         fine = EnergyMap._from_dense(grid, vals, vmask, 1, roi=final, checked=True)
         key = int(keys[0 if self.kcode == nat.MWB_DAS else 1])
         if key:
@@ -200,13 +261,17 @@ class _SegmentPlan:
             cell = (final.min_cell[0], final.min_cell[1])
         full_eq = int(self.mask_np.sum()) if self.mask_np is not None else nx * ny
         ev = self.events
-        t_s, t_f = ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3
+        if self.tree is None:
+            t_s, t_f = ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3
+            elapsed = {"search": t_s, "fine": t_f, "total": t_s + t_f}
+        else:  # search and fine pass are one library call
+            elapsed = {"total": ev[0].elapsed_time(ev[1]) / 1e3}
         report = SegmentReport(
             kind=_kind(kind).value, n_sub=n_sub, stop_cells=self.stop_cells, records=records, final_region=final,
             lowres=self.h_lowres.numpy().reshape(2 * n_sub, 2 * n_sub).copy(),
             subgrid_points_evaluated=4 * n_sub * n_sub * len(records), fine_points_evaluated=n_fine,
             full_equivalent_points=full_eq, argmax_cell=cell, argmax_position=grid.cell_center(*cell),
-            elapsed={"search": t_s, "fine": t_f, "total": t_s + t_f})
+            elapsed=elapsed)
         return fine, report
 
 
@@ -230,7 +295,8 @@ def _mask_for(grid: ImagingGrid, mask):
 
 
 def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.01, *, region: Region | None = None,
-            mask="breast", window=None, interpolation: str = "linear") -> tuple[EnergyMap, SegmentReport]:
+            mask="breast", window=None, interpolation: str = "linear",
+            tree: bool = True) -> tuple[EnergyMap, SegmentReport]:
     """Quadrant search scored on n_sub x n_sub sub-grids, then a full-resolution
     pass over the kept segment.  Returns (fine map of the segment, report).
 
@@ -256,10 +322,12 @@ def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.0
     interp = nat.INTERP[interpolation]
     m, mt, mkey = _mask_for(grid, mask)
     key = (id(scan), grid.origin, grid.extent, grid.resolution, region.bounds(), kcode, n_sub, stop_cells, interp,
-           k0, w, mkey, torch.cuda.current_device())
+           k0, w, mkey, bool(tree), torch.cuda.current_device())
     plan = _SEG_PLANS.get(key)
     if plan is None or plan.scan is not scan:
-        plan = _SegmentPlan(scan, grid, region, kcode, n_sub, stop_cells, n_iter, interp, k0, w, m, mt)
+        tree = (_tree_plan(scan, ds.geometry.antennas, grid, region, mkey, mt, n_sub, stop_cells, n_iter, interp)
+                if tree else None)
+        plan = _SegmentPlan(scan, grid, region, kcode, n_sub, stop_cells, n_iter, interp, k0, w, m, mt, tree)
         _SEG_PLANS[key] = plan
         while len(_SEG_PLANS) > _SEG_PLAN_CAPACITY:
             _SEG_PLANS.popitem(last=False)
@@ -376,25 +444,17 @@ class SegmentBatch:
             ant=torch.from_numpy(np.array(geometry.antennas, dtype=np.float64)).to(dev),
             inv_scale=1.0 / (float(geometry.propagation_speed) * float(geometry.sample_interval)),
             n_samples=self.n_samples, ld=self.ld, n_ant=geometry.n_antennas, chan_host=pairs)
-        self.mask_np, self.mask_t, _ = _mask_for(grid, mask)
+        self.mask_np, self.mask_t, mkey = _mask_for(grid, mask)
         self._ws = None
         # region tree plan (search-node points/tables, terminal-node cells/tables),
         # unless the tree is too large: then every iteration builds its own table
-        lib = nat.load()
-        nx, ny = grid.dims
-        x0, y0, x1, y1 = self.region.bounds()
-        info = (C.c_int64 * 4)()
         self.plan = None
         self.fine_tps = 0
-        if tree and lib.mwb_segment_plan_info(nx, ny, x0, y0, x1, y1, self.n_sub, self.stop_cells, self.n_iter, self.n_chan,
-                                     info) == 0:
-            self.plan = torch.empty(int(info[0]), dtype=torch.uint8, device=dev)
-            self.fine_tps = int(info[3])
-            sc = self.scan
-            nat.call("mwb_segment_plan_prepare", sc.chan.data_ptr(), self.n_chan, sc.ant.data_ptr(), sc.n_ant,
-                     sc.inv_scale, self.interp, grid.origin[0], grid.origin[1], grid.resolution, nx, ny, x0, y0, x1,
-                     y1, self.mask_t.data_ptr() if self.mask_t is not None else None, self.n_sub, self.stop_cells,
-                     self.n_iter, self.plan.data_ptr(), dv.stream_handle())
+        if tree:
+            ent = _tree_plan(self.scan, geometry.antennas, grid, self.region, mkey, self.mask_t, self.n_sub,
+                             self.stop_cells, self.n_iter, self.interp)
+            if ent is not None:
+                self.plan, self.fine_tps = ent
 
     @property
     def n_chan(self) -> int:

@@ -102,7 +102,7 @@ def test_segment_batch_equals_per_scan_segment(kind, tree):
     total = 0
     for s in range(len(seeds)):
         ds = mw.BackscatterDataset(model.geometry(), synth.embed_pairs(12, model.pairs(), sig[s].astype(np.float64)))
-        fine, rep = segment(ds, kind, grid, 16, 0.01, window=(model.k0, model.window))
+        fine, rep = segment(ds, kind, grid, 16, 0.01, window=(model.k0, model.window), tree=not tree)
         total += rep.fine_points_evaluated + rep.subgrid_points_evaluated
         assert res.final_region(s) == rep.final_region
         assert _records_equal(res.records(s), rep.records)
@@ -189,7 +189,10 @@ def test_segment_batch_odd_region_and_small_stop():
                         window=win, tree=t).run(torch.from_numpy(sig).cuda()) for t in (True, False)]
     for s in range(len(seeds)):
         ds = mw.BackscatterDataset(model.geometry(), synth.embed_pairs(12, model.pairs(), sig[s].astype(np.float64)))
-        fine, rep = segment(ds, "dmas", grid, 8, 0.004, region=region, window=win)
+        fine, rep = segment(ds, "dmas", grid, 8, 0.004, region=region, window=win, tree=False)
+        fine_t, rep_t = segment(ds, "dmas", grid, 8, 0.004, region=region, window=win)
+        assert fine_t.entries == fine.entries and _records_equal(rep_t.records, rep.records)
+        assert rep_t.argmax_cell == rep.argmax_cell and np.array_equal(rep_t.lowres, rep.lowres)
         for r in res:
             assert r.final_region(s) == rep.final_region
             assert _records_equal(r.records(s), rep.records)
