@@ -56,9 +56,50 @@ class DeviceScan:
     n_ant: int
     chan_host: np.ndarray  # (C, 2) int32
 
+    ant_host: np.ndarray | None = None  # (M, 3) float64, when known
+
     @property
     def n_chan(self) -> int:
         return int(self.chan_host.shape[0])
+
+    def geometry_key(self) -> tuple:
+        """Everything but the samples: scans with equal keys can share device
+        plans (lattices, delay tables, captured graphs)."""
+        ants = self.ant_host if self.ant_host is not None else self.ant.cpu().numpy()
+        return (np.ascontiguousarray(ants, dtype=np.float64).tobytes(), self.chan_host.tobytes(),
+                float(self.inv_scale), int(self.n_samples), int(self.ld), torch.cuda.current_device())
+
+
+_GEOMS: dict[tuple, tuple[torch.Tensor, torch.Tensor]] = {}
+
+
+def geometry_tensors(pairs: np.ndarray, antennas: np.ndarray) -> tuple[torch.Tensor, torch.Tensor]:
+    """Device (C, 2) int32 channel pairs and (M, 3) float64 antennas, cached per
+    geometry so a stream of scans of one scanner uploads them once."""
+    key = (pairs.tobytes(), antennas.tobytes(), torch.cuda.current_device())
+    hit = _GEOMS.get(key)
+    if hit is None:
+        dev = device()
+        hit = (torch.from_numpy(np.array(pairs, dtype=np.int32)).to(dev),
+               torch.from_numpy(np.array(antennas, dtype=np.float64)).to(dev))
+        if len(_GEOMS) > 64:
+            _GEOMS.clear()
+        _GEOMS[key] = hit
+    return hit
+
+
+def upload_rows(rows: np.ndarray, keep: np.ndarray, ld: int) -> torch.Tensor:
+    """Device fp32 [len(keep)][ld] (zero tail) of rows[keep] (any float dtype):
+    cast once into pinned staging, one asynchronous host->device copy."""
+    n = rows.shape[1]
+    pinned = torch.cuda.is_available()
+    h = torch.empty((keep.size, ld), dtype=torch.float32, pin_memory=pinned)
+    hv = h.numpy()
+    if ld > n:
+        hv[:, n:] = 0.0
+    for i, k in enumerate(keep):
+        hv[i, :n] = rows[k]
+    return h.to(device(), non_blocking=pinned)
 
 
 def compact_channels(signals: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
@@ -83,21 +124,25 @@ def _build_scan(ds) -> DeviceScan:
     geom = ds.geometry
     sig = np.asarray(ds.signals)
     m, _, n = sig.shape
-    comp, pairs = compact_channels(sig)
+    flat = sig.reshape(m * m, n)
+    keep = np.flatnonzero(np.any(flat != 0.0, axis=1)) if n > 0 else np.zeros(0, dtype=np.int64)
+    if keep.size == 0:  # as compact_channels: keep channel (0, 0), all zeros
+        keep = np.zeros(1, dtype=np.int64)
+    pairs = np.stack([keep // m, keep % m], axis=1).astype(np.int32)
     ld = round4(n)
-    dev = device()
-    host = np.zeros((comp.shape[0], ld), dtype=np.float32)
-    host[:, :n] = comp
+    ants = np.ascontiguousarray(np.asarray(geom.antennas, dtype=np.float64))
+    chan, ant = geometry_tensors(pairs, ants)
     scale = float(geom.propagation_speed) * float(geom.sample_interval)
     return DeviceScan(
-        sig=torch.from_numpy(host).to(dev),
-        chan=torch.from_numpy(pairs).to(dev),
-        ant=torch.from_numpy(np.array(geom.antennas, dtype=np.float64)).to(dev),
+        sig=upload_rows(flat, keep, ld),
+        chan=chan,
+        ant=ant,
         inv_scale=1.0 / scale,
         n_samples=n,
         ld=ld,
         n_ant=m,
         chan_host=pairs,
+        ant_host=ants,
     )
 
 
@@ -150,10 +195,13 @@ def mono_scan_for(ds) -> DeviceScan:
     pairs = np.stack([keep, keep], axis=1).astype(np.int32)
     geom = ds.geometry
     dev = device()
+    ants = np.ascontiguousarray(np.asarray(geom.antennas, dtype=np.float64))
+    chan, ant = geometry_tensors(pairs, ants)
     scan = DeviceScan(
         sig=torch.from_numpy(host).to(dev),
-        chan=torch.from_numpy(pairs).to(dev),
-        ant=torch.from_numpy(np.array(geom.antennas, dtype=np.float64)).to(dev),
+        chan=chan,
+        ant=ant,
+        ant_host=ants,
         inv_scale=1.0 / (4.0 * float(geom.propagation_speed) * float(geom.sample_interval)),
         n_samples=n,
         ld=ld,

@@ -19,6 +19,7 @@ Drop-in for /root/reference/pkg/src/mwbeam/coarse2fine.py:
 
 from __future__ import annotations
 
+import dataclasses
 import math
 from dataclasses import dataclass, field
 
@@ -323,17 +324,20 @@ def select_roi(coarse: EnergyMap, breast_region: Region, cfg: FrameworkConfig = 
 
 
 class _FrameworkPlan:
-    """One framework configuration on one device scan, captured as a CUDA graph.
+    """One framework configuration for one scanner geometry, captured as a CUDA graph.
 
     The coarse lattice pass, the select kernel and the ROI-driven fine pass
     (13 kernels incl. memsets) are enqueued once eagerly, then captured; later
     calls replay the graph and read the results back into pinned buffers with
     a single synchronisation.  Buffers persist with the plan, so a replay
-    allocates nothing.
+    allocates nothing.  The graph reads the plan's own signal slot: each call
+    first copies its scan into the slot (device to device), so a stream of
+    different scans of one geometry replays one graph.
     """
 
     def __init__(self, scan: dv.DeviceScan, grid: ImagingGrid, d: int, kcode: int, cfg: FrameworkConfig,
                  interp: int, k0: int, w: int, mode: int):
+        scan = dataclasses.replace(scan, sig=torch.empty_like(scan.sig))  # the slot
         self.scan, self.grid, self.d, self.kcode, self.cfg = scan, grid, d, kcode, cfg
         self.interp, self.k0, self.w, self.mode = interp, k0, w, mode
         nx, ny = grid.dims
@@ -350,8 +354,7 @@ class _FrameworkPlan:
         pin = torch.cuda.is_available()
         self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=pin)
         self.h_trace = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, pin_memory=pin)
-        self.h_dense = torch.empty(nx * ny, dtype=torch.float32, pin_memory=pin)
-        self.h_valid = torch.empty(nx * ny, dtype=torch.uint8, pin_memory=pin)
+        self._pin = pin  # map buffers are fresh pinned blocks per call (handed to the EnergyMap, no host copy)
         self.graph: torch.cuda.CUDAGraph | None = None
         self.replays = 0
 
@@ -370,8 +373,9 @@ class _FrameworkPlan:
                      {self.kcode: self.dense}, self.valid, self.status, 1, d_region=self.region_t, mode=self.mode)
         ev[3].record()
 
-    def launch(self) -> None:
-        """Enqueue one run (graph replay after the first call) and the readback."""
+    def launch(self, scan: dv.DeviceScan) -> None:
+        """Enqueue one run on ``scan`` (graph replay after the first call) and the readback."""
+        self.scan.sig.copy_(scan.sig, non_blocking=True)
         if self.graph is None:
             self._enqueue()  # eager run: kernel attributes set, allocator warmed
             torch.cuda.current_stream().synchronize()
@@ -381,6 +385,9 @@ class _FrameworkPlan:
             self.graph = graph
         self.graph.replay()
         self.replays += 1
+        nx, ny = self.grid.dims
+        self.h_dense = torch.empty(nx * ny, dtype=torch.float32, pin_memory=self._pin)
+        self.h_valid = torch.empty(nx * ny, dtype=torch.uint8, pin_memory=self._pin)
         for src, dst in ((self.status.t, self.h_status), (self.trace_t, self.h_trace), (self.dense, self.h_dense),
                          (self.valid, self.h_valid)):
             dst.copy_(src, non_blocking=True)
@@ -398,8 +405,8 @@ class _FrameworkPlan:
         n_coarse, n_fine = int(counts[0]), int(counts[1])
         EVAL_COUNTER.add(n_coarse)
         EVAL_COUNTER.add(n_fine)
-        vals = self.h_dense.numpy().reshape(nx, ny).copy()  # the plan's pinned buffers are reused
-        vmask = self.h_valid.numpy().reshape(nx, ny).view(bool).copy()
+        vals = self.h_dense.numpy().reshape(nx, ny)
+        vmask = self.h_valid.numpy().reshape(nx, ny).view(bool)
         composite = EnergyMap._from_dense(self.grid, vals, vmask, stride=self.d, roi=final, split=self.d, checked=True)
         ev = self.events
         t_c = ev[0].elapsed_time(ev[1]) / 1e3
@@ -430,9 +437,9 @@ _PLAN_CAPACITY = 8
 
 
 def _plan_for(ds, kind, grid: ImagingGrid, d: int, cfg: FrameworkConfig, interpolation: str, window,
-              mode: int) -> _FrameworkPlan:
-    """Cached plan; a plan is reused only for the same device scan object, so a
-    new (or garbage-collected and re-created) dataset never replays stale data."""
+              mode: int) -> tuple[_FrameworkPlan, dv.DeviceScan]:
+    """Cached plan per scanner geometry and configuration (not per dataset: the
+    plan's graph reads a signal slot that every call refills)."""
     global _PLANS
     from collections import OrderedDict
 
@@ -442,17 +449,17 @@ def _plan_for(ds, kind, grid: ImagingGrid, d: int, cfg: FrameworkConfig, interpo
     k0, w = _window(scan.n_samples, window)
     kcode = _kind_code(kind)
     interp = nat.INTERP[interpolation]
-    key = (id(scan), grid.origin, grid.extent, grid.resolution, d, kcode, cfg.frame_fraction, cfg.n_min, interp, k0,
-           w, mode, torch.cuda.current_device())
+    key = (scan.geometry_key(), grid.origin, grid.extent, grid.resolution, d, kcode, cfg.frame_fraction, cfg.n_min,
+           interp, k0, w, mode)
     plan = _PLANS.get(key)
-    if plan is not None and plan.scan is scan:
+    if plan is not None:
         _PLANS.move_to_end(key)
-        return plan
+        return plan, scan
     plan = _FrameworkPlan(scan, grid, d, kcode, cfg, interp, k0, w, mode)
     _PLANS[key] = plan
     while len(_PLANS) > _PLAN_CAPACITY:
         _PLANS.popitem(last=False)
-    return plan
+    return plan, scan
 
 
 def run_framework(
@@ -473,8 +480,8 @@ def run_framework(
     mask_np, _ = _breast_mask_device(grid)
     if not mask_np[::d, ::d].any():
         raise ValueError("no coarse focal points inside the breast mask")
-    plan = _plan_for(ds, kind, grid, d, cfg, interpolation, window, {"smem": 0, "gather": 1}[kernel_mode])
-    plan.launch()
+    plan, scan = _plan_for(ds, kind, grid, d, cfg, interpolation, window, {"smem": 0, "gather": 1}[kernel_mode])
+    plan.launch(scan)
     return plan.finish()
 
 
@@ -519,8 +526,8 @@ def consistency_check(
         if not mask[::dd, ::dd].any():
             raise ValueError("no coarse focal points inside the breast mask")
     plans = [_plan_for(ds, kind, grid, dd, cfg, "linear", None, 0) for dd in (d1, d2)]
-    for plan in plans:
-        plan.launch()  # both runs are in flight before the first readback
-    (_, rep_a), (_, rep_b) = (plan.finish() for plan in plans)
+    for plan, scan in plans:
+        plan.launch(scan)  # both runs are in flight before the first readback
+    (_, rep_a), (_, rep_b) = (plan.finish() for plan, _ in plans)
     inter = rep_a.final_region.intersection(rep_b.final_region)
     return CheckVerdict(inter is not None, inter, rep_a.final_region, rep_b.final_region), rep_a, rep_b

@@ -25,6 +25,7 @@ result once.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import hashlib
 import math
 from collections import OrderedDict
@@ -159,6 +160,7 @@ class _SegmentPlan:
 
     def __init__(self, scan: dv.DeviceScan, grid: ImagingGrid, region: Region, kcode: int, n_sub: int,
                  stop_cells: int, n_iter: int, interp: int, k0: int, w: int, mask_np, mask_t, tree):
+        scan = dataclasses.replace(scan, sig=torch.empty_like(scan.sig))  # the signal slot every call refills
         self.scan, self.grid, self.region, self.kcode = scan, grid, region, kcode
         self.n_sub, self.stop_cells, self.n_iter = n_sub, stop_cells, n_iter
         self.interp, self.k0, self.w = interp, k0, w
@@ -181,8 +183,7 @@ class _SegmentPlan:
         pin = torch.cuda.is_available()
         self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=pin)
         self.h_trace = torch.empty(nat.SEG_TRACE_BYTES, dtype=torch.uint8, pin_memory=pin)
-        self.h_dense = torch.empty(nx * ny, dtype=torch.float32, pin_memory=pin)
-        self.h_valid = torch.empty(nx * ny, dtype=torch.uint8, pin_memory=pin)
+        self._pin = pin  # map buffers are fresh pinned blocks per call (handed to the EnergyMap, no host copy)
         self.h_lowres = torch.empty(n_low, dtype=torch.float32, pin_memory=pin)
         self.graph: torch.cuda.CUDAGraph | None = None
 
@@ -216,7 +217,8 @@ class _SegmentPlan:
                      {self.kcode: self.dense}, self.valid, self.status, 0, d_region=self.region_t)
         ev[2].record()
 
-    def launch(self) -> None:
+    def launch(self, scan: dv.DeviceScan) -> None:
+        self.scan.sig.copy_(scan.sig, non_blocking=True)
         if self.graph is None:
             self._enqueue()  # eager run: kernel attributes set, allocator warmed
             torch.cuda.current_stream().synchronize()
@@ -225,6 +227,10 @@ class _SegmentPlan:
                 self._enqueue()
             self.graph = graph
         self.graph.replay()
+        nx, ny = self.grid.dims
+        self.h_dense = torch.empty(nx * ny, dtype=torch.float32, pin_memory=self._pin)
+        if self.tree is None:
+            self.h_valid = torch.empty(nx * ny, dtype=torch.uint8, pin_memory=self._pin)
         pairs = [(self.status.t, self.h_status), (self.trace_t, self.h_trace), (self.dense, self.h_dense),
                  (self.lowres, self.h_lowres)]
         if self.tree is None:
@@ -243,9 +249,9 @@ class _SegmentPlan:
         n_fine = int(counts[0])
         n_sub = self.n_sub
         EVAL_COUNTER.add(n_fine + 4 * n_sub * n_sub * len(records))
-        vals = self.h_dense.numpy().reshape(nx, ny).copy()  # the plan's pinned buffers are reused
+        vals = self.h_dense.numpy().reshape(nx, ny)
         if self.tree is None:
-            vmask = self.h_valid.numpy().reshape(nx, ny).view(bool).copy()
+            vmask = self.h_valid.numpy().reshape(nx, ny).view(bool)
         else:  # the final region's cells that pass the mask
             vmask = np.zeros((nx, ny), dtype=bool)
             (fx0, fy0), (fx1, fy1) = final.min_cell, final.max_cell
@@ -300,8 +306,8 @@ def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.0
     """Quadrant search scored on n_sub x n_sub sub-grids, then a full-resolution
     pass over the kept segment.  Returns (fine map of the segment, report).
 
-    Repeated calls with one configuration on one dataset replay a captured
-    CUDA graph (the plan is keyed by the device scan object, as run_framework's)."""
+    Calls with one configuration on scans of one geometry replay a captured
+    CUDA graph that reads a signal slot each call refills (as run_framework's)."""
     _check_interpolation(interpolation)
     if not stop_size > 0:
         raise ValueError("stop_size must be > 0")
@@ -321,10 +327,10 @@ def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.0
         raise ValueError("the segmentation metric needs a non-empty energy window")
     interp = nat.INTERP[interpolation]
     m, mt, mkey = _mask_for(grid, mask)
-    key = (id(scan), grid.origin, grid.extent, grid.resolution, region.bounds(), kcode, n_sub, stop_cells, interp,
-           k0, w, mkey, bool(tree), torch.cuda.current_device())
+    key = (scan.geometry_key(), grid.origin, grid.extent, grid.resolution, region.bounds(), kcode, n_sub, stop_cells,
+           interp, k0, w, mkey, bool(tree))
     plan = _SEG_PLANS.get(key)
-    if plan is None or plan.scan is not scan:
+    if plan is None:
         tree = (_tree_plan(scan, ds.geometry.antennas, grid, region, mkey, mt, n_sub, stop_cells, n_iter, interp)
                 if tree else None)
         plan = _SegmentPlan(scan, grid, region, kcode, n_sub, stop_cells, n_iter, interp, k0, w, m, mt, tree)
@@ -333,7 +339,7 @@ def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.0
             _SEG_PLANS.popitem(last=False)
     else:
         _SEG_PLANS.move_to_end(key)
-    plan.launch()
+    plan.launch(scan)
     return plan.finish(kind)
 
 
