@@ -291,6 +291,15 @@ def other_configs() -> dict:
         out[f"cfg2_segment_{kind}"] = {"ms": med_ms(lambda: segment(ds2, kind, g2, 16, 0.01, window=(m2.k0, 32)))}
         out[f"cfg2_full_image_{kind}"] = {"ms": med_ms(lambda: mw.image(ds2, kind, g2, mask=mw.breast_mask(g2),
                                                                            window=(m2.k0, 32)))}
+    # a stream of distinct scans through the drop-in API: every call uploads a new dataset
+    stream1 = [synth.dataset_2d(m0, seed=500 + i)[0] for i in range(8)]
+    stream2 = [synth.dataset_2d(m2, seed=1500 + i, phantom_radius=0.05)[0] for i in range(8)]
+    it1, it2 = iter(stream1), iter(stream2)
+    out["cfg1_dmas_200x200_image_new_dataset_each_call"] = {
+        "ms": med_ms(lambda: mw.image(next(it1), "dmas", g1, window=win))}
+    out["cfg2_run_framework_das_new_dataset_each_call"] = {
+        "ms": med_ms(lambda: mw.run_framework(next(it2), "das", g2, mw.Manual(d), window=(m2.k0, 32)))}
+    del stream1, stream2
     # the configs[2] framework for a batch of 4096 scans (FrameworkBatch)
     from paper_1709_02549_b200.fwbatch import FrameworkBatch
 

@@ -145,3 +145,46 @@ def test_tensor_core_entry_argument_errors(lib):
     assert lib.mwb_enumerate_lattice_padded(0.0, 0.0, 1.0, 10, 10, 0, 0, 10, 9, 1, None, 0, None, None, None, None,
                                             None, None, None) == -1
     assert b"outside" in lib.mwb_last_error()
+
+
+def _tree_counts(region, stop, max_iters):
+    """Python restatement of the region tree (Region.quadrants split,
+    geometry.py:225-242; a region is split while its larger side exceeds the
+    stop size and both sides are >= 2, for at most max_iters levels)."""
+    search = term = 0
+    fine_tps = 0
+    todo = [(region, 0)]
+    while todo:
+        (x0, y0, x1, y1), depth = todo.pop()
+        w, h = x1 - x0 + 1, y1 - y0 + 1
+        if max(w, h) <= stop or w < 2 or h < 2 or depth >= max_iters:
+            term += 1
+            fine_tps = max(fine_tps, -(-(w * h) // 256))
+            continue
+        search += 1
+        mx, my = x0 + (w + 1) // 2 - 1, y0 + (h + 1) // 2 - 1
+        for qx0, qx1 in ((x0, mx), (mx + 1, x1)):
+            for qy0, qy1 in ((y0, my), (my + 1, y1)):
+                todo.append(((qx0, qy0, qx1, qy1), depth + 1))
+    return search, term, fine_tps
+
+
+@pytest.mark.parametrize("region,stop,iters", [((0, 0, 403, 403), 40, 4), ((3, 11, 190, 170), 8, 5),
+                                               ((0, 0, 39, 39), 40, 0), ((0, 0, 480, 100), 40, 4)])
+def test_segment_plan_info_matches_tree(lib, region, stop, iters):
+    """The host-side region tree behind mwb_segment_plan_* (no GPU needed)."""
+    info = (ctypes.c_int64 * 4)()
+    x0, y0, x1, y1 = region
+    assert lib.mwb_segment_plan_info(x1 + 1, y1 + 1, x0, y0, x1, y1, 16, stop, iters, 66, info) == 0
+    search, term, fine_tps = _tree_counts(region, stop, iters)
+    assert (info[1], info[2], info[3]) == (search, term, fine_tps)
+    assert info[0] > 0
+
+
+def test_segment_plan_info_rejects_huge_trees_and_bad_args(lib):
+    info = (ctypes.c_int64 * 4)()
+    assert lib.mwb_segment_plan_info(4096, 4096, 0, 0, 4095, 4095, 16, 1, 12, 66, info) != 0  # > 16384 regions
+    assert b"too many regions" in lib.mwb_last_error()
+    assert lib.mwb_segment_plan_info(100, 100, 0, 0, 100, 99, 16, 8, 4, 66, info) != 0  # region outside the grid
+    assert lib.mwb_segment_plan_info(100, 100, 0, 0, 99, 99, 0, 8, 4, 66, info) != 0  # n_sub
+    assert lib.mwb_segment_run_workspace_bytes(0, 16, 3) == -1
