@@ -1,0 +1,125 @@
+"""BASELINE's full-size configurations, checked through size-independent
+properties (the oracle needs hours at these sizes, so it is spot-checked on a
+sample of points):
+
+* configs[3]: 4096 scans x 256^2 px x (DAS + DMAS) on the default
+  (tensor-core) batch path, exactly as bench.py runs it;
+* configs[4]: the 128^3 DMAS volume, 496 pairs, W = 48.
+
+Properties: every energy finite and DAS >= 0; scaling the signals by 2 scales
+every energy by exactly 4 (power-of-two scaling commutes with every rounding);
+a permuted batch gives every scan bit-identical maps (no cross-scan
+dependence); a sample of pixels agrees with the oracle within BASELINE's 1e-4
+(peak-normalised); the tensor-core maps agree with the fp32 CUDA-core kernel
+on a subset of scans.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from _mwb_helpers import peak_err
+from oracle import mwbeam_oracle as orc
+from paper_1709_02549_b200 import synth
+from paper_1709_02549_b200.batch import BatchImager
+
+pytestmark = pytest.mark.gpu
+
+S = 4096
+
+
+@pytest.fixture(scope="module")
+def cfg3():
+    model = synth.ScanModel()
+    sig, tumours = synth.batch_2d_device(model, range(S))
+    grid = synth.grid_square(0.12, 256)
+    bi = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=(model.k0, model.window),
+                     mode="auto")
+    return model, sig, tumours, grid, bi
+
+
+def _run(bi, sig):
+    n = bi.grid.dims[0] * bi.grid.dims[1]
+    das = torch.empty((sig.shape[0], n), dtype=torch.float32, device="cuda")
+    dmas = torch.empty_like(das)
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    bi.run_device(sig, das, dmas, flags=flags)
+    return das, dmas, int(flags.item())
+
+
+def test_cfg3_full_size_properties(cfg3):
+    model, sig, _, grid, bi = cfg3
+    assert bi.uses_tensor_cores
+    das, dmas, flags = _run(bi, sig)
+    assert flags == 0
+    assert bool(torch.isfinite(das).all()) and bool(torch.isfinite(dmas).all())
+    assert bool((das >= 0).all())
+    # x2 -> x4, bit for bit, on every pixel of every scan
+    das2, dmas2, _ = _run(bi, sig * 2.0)
+    assert torch.equal(das2, das * 4.0) and torch.equal(dmas2, dmas * 4.0)
+    del das2, dmas2
+    # reversed batch order: each scan's maps are bit-identical
+    rev = torch.flip(sig, dims=[0]).contiguous()
+    das_r, dmas_r, _ = _run(bi, rev)
+    assert torch.equal(torch.flip(das_r, dims=[0]), das) and torch.equal(torch.flip(dmas_r, dims=[0]), dmas)
+
+
+def test_cfg3_full_size_vs_oracle_and_fp32(cfg3):
+    model, sig, _, grid, bi = cfg3
+    das, dmas, _ = _run(bi, sig)
+    # oracle: the reference algorithm on a sample of pixels of a few scans
+    g = model.geometry()
+    ny = grid.dims[1]
+    rng = np.random.default_rng(3)
+    cells = [(int(a), int(b)) for a, b in rng.integers(0, 256, size=(96, 2))]
+    pts = np.array([grid.cell_center(*c) for c in cells])
+    slots = np.array([ix * ny + iy for ix, iy in cells])
+    host = sig[[0, 1777, S - 1]].cpu().numpy()
+    for s, row in zip((0, 1777, S - 1), host):
+        full = synth.embed_pairs(12, model.pairs(), row[:, : model.n_samples].astype(np.float64))
+        for kind, got in (("das", das), ("dmas", dmas)):
+            want = orc.windowed_energies(g.antennas, g.propagation_speed, g.sample_interval, full, pts, kind,
+                                         model.k0, model.window)
+            # peak-normalised against the scan's own map peak (the sample may miss the peak)
+            err = np.abs(got[s].cpu().numpy()[slots] - want).max() / float(got[s].abs().max())
+            assert err <= 1e-4, (s, kind, err)
+    # the fp32 CUDA-core kernel on 64 scans spread over the batch
+    ref = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=(model.k0, model.window),
+                      mode="smem")
+    idx = torch.arange(0, S, S // 64, device="cuda")
+    sub = sig.index_select(0, idx).contiguous()
+    rd, rm, _ = _run(ref, sub)
+    for k, (a, b) in enumerate(((das.index_select(0, idx), rd), (dmas.index_select(0, idx), rm))):
+        e = ((a - b).abs().amax(dim=1) / b.abs().amax(dim=1)).max().item()
+        assert e <= 3e-5, (k, e)
+
+
+def test_cfg4_full_size_volume_properties():
+    import paper_1709_02549_b200 as mw
+    from paper_1709_02549_b200.volume import VolumeGrid, image_volume
+
+    vm = synth.VolumeModel()
+    sig, _ = synth.scan_3d(vm, seed=9)
+    full = synth.embed_pairs(vm.n_ant, vm.pairs(), sig)
+    ds = mw.BackscatterDataset(vm.geometry(), full)
+    ds2 = mw.BackscatterDataset(vm.geometry(), full * 2.0)
+    g4 = VolumeGrid((-0.06, -0.06, 0.0), (0.12, 0.12, 0.12), 0.12 / 128)
+    win = (vm.k0, vm.window)
+    a = image_volume(ds, ("das", "dmas"), g4, window=win)
+    b = image_volume(ds2, ("das", "dmas"), g4, window=win)
+    assert a["dmas"].valid.all() and a["das"].valid.all()
+    va, vb = a["dmas"].values, b["dmas"].values
+    assert np.isfinite(va).all() and np.array_equal(vb, va * 4.0)
+    da = a["das"].values
+    assert (da >= 0).all() and np.array_equal(b["das"].values, da * 4.0)
+    # oracle (z-shift adapter) on voxels around the DMAS peak and a random sample
+    g = vm.geometry()
+    peak = np.unravel_index(np.argmax(va), va.shape)
+    rng = np.random.default_rng(4)
+    vox = [tuple(int(v) for v in peak)] + [tuple(int(v) for v in x) for x in rng.integers(0, 128, size=(12, 3))]
+    pts3 = np.array([g4.cell_center(*v) for v in vox])
+    for kind, dense in (("das", da), ("dmas", va)):
+        got = np.array([dense[v] for v in vox], dtype=np.float64)
+        want = orc.volume_energies(g.antennas, g.propagation_speed, g.sample_interval, full, pts3, kind,
+                                   vm.k0, vm.window)
+        assert np.abs(got - want).max() / np.abs(dense).max() <= 1e-4, kind
