@@ -93,3 +93,27 @@ def test_box_octants_partition():
     assert sum(k.n_cells for k in kids) == b.n_cells
     assert [(k.min_cell, k.max_cell) for k in kids] == orc.octants((b.min_cell, b.max_cell))
     assert Box((0, 0, 0), (3, 3, 0)).octants() is None
+
+
+def test_volume_cache_hit_is_identical(vol):
+    """image_volume caches the voxel enumeration and delay table per geometry:
+    a hit (same or a different dataset of the same scanner) equals a fresh run."""
+    from paper_1709_02549_b200 import volume as vmod
+
+    vm, _, ds, _ = vol
+    sig2, _ = synth.scan_3d(vm, seed=77)
+    ds2 = mw.BackscatterDataset(vm.geometry(), synth.embed_pairs(vm.n_ant, vm.pairs(), sig2))
+    grid = VolumeGrid((-0.02, -0.02, 0.0), (0.04, 0.04, 0.02), 0.001)
+    mask = hemisphere_mask(grid, 0.018)
+    win = (vm.k0, vm.window)
+    vmod._VOLUME_CACHE.clear()
+    fresh = [image_volume(d, ("das", "dmas"), grid, mask=mask, window=win) for d in (ds, ds2)]
+    vmod._VOLUME_CACHE.clear()
+    image_volume(ds, "dmas", grid, mask=mask, window=win)  # populates the cache
+    before = mw.EVAL_COUNTER.value
+    hits = [image_volume(d, ("das", "dmas"), grid, mask=mask, window=win) for d in (ds, ds2)]
+    assert mw.EVAL_COUNTER.value - before == 2 * 2 * int(mask.sum())
+    for f, h in zip(fresh, hits):
+        for k in ("das", "dmas"):
+            assert np.array_equal(f[k].valid, h[k].valid)
+            assert np.array_equal(f[k].values[f[k].valid], h[k].values[h[k].valid])
