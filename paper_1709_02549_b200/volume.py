@@ -14,8 +14,11 @@ scores them with the reference's Eq. (5) / W-B / n_min control flow
 
 from __future__ import annotations
 
+import dataclasses
 import hashlib
 import math
+import weakref
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -334,6 +337,120 @@ def _launch_select3(dense_t, valid_t, grid, lattice, box, cfg, region_t, trace_t
              trace_t.data_ptr(), dv.stream_handle())
 
 
+_MASK_KEYS: dict[int, tuple] = {}
+
+
+def _mask_key(mask: np.ndarray) -> tuple:
+    """(content hash, voxel count) of a phantom mask; remembered per array object
+    (while it lives) so a stream of calls with one mask hashes it once."""
+    hit = _MASK_KEYS.get(id(mask))
+    if hit is not None and hit[0]() is mask:
+        return hit[1]
+    val = (hashlib.blake2b(np.packbits(mask).tobytes(), digest_size=16).digest(), int(mask.sum()))
+    try:
+        ref = weakref.ref(mask, lambda _r, k=id(mask): _MASK_KEYS.pop(k, None))
+        _MASK_KEYS[id(mask)] = (ref, val)
+    except TypeError:
+        pass
+    return val
+
+
+class _VolumeFrameworkPlan:
+    """The configs[4] octant framework for one scanner geometry, grid, mask and
+    configuration, captured as a CUDA graph (coarse voxel lattice, octant
+    select, ROI-driven fine pass).  As coarse2fine._FrameworkPlan: buffers live
+    with the plan, the graph reads a signal slot every call refills, so a
+    stream of volumes of one scanner replays one graph and allocates nothing
+    on the device (the fine pass's point list and table are sized for the whole
+    grid, since the ROI is only known on the device)."""
+
+    def __init__(self, scan, grid: VolumeGrid, d: int, kcode: int, cfg: FrameworkConfig, interp: int, k0: int,
+                 w: int, mask: np.ndarray, full_eq: int):
+        self.scan = dataclasses.replace(scan, sig=torch.empty_like(scan.sig))
+        self.grid, self.d, self.kcode, self.cfg = grid, d, kcode, cfg
+        self.interp, self.k0, self.w = interp, k0, w
+        self.full_eq = full_eq
+        n = math.prod(grid.dims)
+        dev = dv.device()
+        self.mask_t = _upload_mask3(mask, grid.dims)
+        self.dense = torch.empty(n, dtype=torch.float32, device=dev)  # only valid voxels are read
+        self.valid = torch.empty(n, dtype=torch.uint8, device=dev)
+        self.status = _Status()
+        self.region_t = torch.empty(6, dtype=torch.int32, device=dev)
+        self.trace_t = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
+        self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
+        self._pin = torch.cuda.is_available()
+        self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=self._pin)
+        self.h_trace = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, pin_memory=self._pin)
+        self.graph: torch.cuda.CUDAGraph | None = None
+
+    def _enqueue(self) -> None:
+        g, d, sc = self.grid, self.d, self.scan
+        ev = self.events
+        full = g.full_box()
+        self.valid.zero_()
+        self.status.t.zero_()
+        ev[0].record()
+        _volume_pass(sc, g, full, d, self.mask_t, 0, (self.kcode,), self.interp, self.k0, self.w,
+                     {self.kcode: self.dense}, self.valid, self.status, 0)
+        ev[1].record()
+        _launch_select3(self.dense, self.valid, g, d, full, self.cfg, self.region_t, self.trace_t)
+        ev[2].record()
+        _volume_pass(sc, g, full, 1, self.mask_t, d, (self.kcode,), self.interp, self.k0, self.w,
+                     {self.kcode: self.dense}, self.valid, self.status, 1, d_region=self.region_t)
+        ev[3].record()
+
+    def launch(self, scan) -> None:
+        self.scan.sig.copy_(scan.sig, non_blocking=True)
+        if self.graph is None:
+            self._enqueue()  # eager run: kernel attributes set, allocator warmed
+            torch.cuda.current_stream().synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                self._enqueue()
+            self.graph = graph
+        self.graph.replay()
+        n = math.prod(self.grid.dims)
+        self.h_dense = torch.empty(n, dtype=torch.float32, pin_memory=self._pin)  # owned by the returned map
+        self.h_valid = torch.empty(n, dtype=torch.uint8, pin_memory=self._pin)
+        for src, dst in ((self.status.t, self.h_status), (self.trace_t, self.h_trace), (self.dense, self.h_dense),
+                         (self.valid, self.h_valid)):
+            dst.copy_(src, non_blocking=True)
+
+    def finish(self) -> tuple[VolumeMap, VolumeReport]:
+        torch.cuda.current_stream().synchronize()
+        grid, d = self.grid, self.d
+        keys, counts, flags = self.status.read(self.h_status.numpy())
+        if flags & 1:
+            raise ValueError("energy map contains non-finite values")
+        final, trace, _ = decode_trace(self.h_trace.numpy().tobytes(), region=_box)
+        values = self.h_dense.numpy().reshape(grid.dims)
+        vmask = self.h_valid.numpy().reshape(grid.dims).view(bool)
+        composite = VolumeMap(grid, values, vmask, stride=d, roi=final, checked=True)
+        n_c, n_f = int(counts[0]), int(counts[1])
+        EVAL_COUNTER.add(n_c + n_f)
+        key = int(keys[0 if self.kcode == nat.MWB_DAS else 1])
+        _, ny, nz = grid.dims
+        if key:
+            slot = 0xFFFFFFFF - (key & 0xFFFFFFFF)
+            cell = (slot // (ny * nz), (slot // nz) % ny, slot % nz)
+        else:
+            cell = composite.argmax_cell()
+        ev = self.events
+        t = [ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3, ev[2].elapsed_time(ev[3]) / 1e3]
+        report = VolumeReport(
+            decimation_factor=d, iterations=len(trace.records), final_region=final, coarse_points_evaluated=n_c,
+            fine_points_evaluated=n_f, full_equivalent_points=self.full_eq,
+            reduction_ratio=self.full_eq / (n_c + n_f),
+            elapsed={"coarse": t[0], "select": t[1], "fine": t[2], "total": sum(t)}, trace=trace, argmax_cell=cell,
+            argmax_position=grid.cell_center(*cell))
+        return composite, report
+
+
+_VOLUME_PLANS: "OrderedDict[tuple, _VolumeFrameworkPlan]" = OrderedDict()
+_VOLUME_PLAN_CAPACITY = 2
+
+
 def run_framework_volume(ds, kind, grid: VolumeGrid, mode, cfg: FrameworkConfig = FrameworkConfig(), *,
                          mask=None, phantom_radius: float | None = None, interpolation: str = "linear",
                          window=None) -> tuple[VolumeMap, VolumeReport]:
@@ -342,6 +459,8 @@ def run_framework_volume(ds, kind, grid: VolumeGrid, mode, cfg: FrameworkConfig 
 
     The phantom mask is ``mask`` if given, else the hemisphere of
     ``phantom_radius`` (default: the largest hemisphere inscribed in the grid).
+    Calls with one configuration on volumes of one scanner replay a captured
+    CUDA graph (``_VolumeFrameworkPlan``).
     """
     _check_interpolation(interpolation)
     d = decimation_factor(mode, grid.resolution)
@@ -349,55 +468,29 @@ def run_framework_volume(ds, kind, grid: VolumeGrid, mode, cfg: FrameworkConfig 
         if phantom_radius is None:
             phantom_radius = min(grid.extent[0], grid.extent[1]) / 2.0
         mask = hemisphere_mask(grid, phantom_radius)
-    mask = np.asarray(mask, dtype=bool)
-    if not mask[::d, ::d, ::d].any():
-        raise ValueError("no coarse focal points inside the phantom mask")
+    if not (isinstance(mask, np.ndarray) and mask.dtype == bool):
+        mask = np.asarray(mask, dtype=bool)
+    if mask.shape != tuple(grid.dims):
+        raise ValueError(f"mask must have the grid's dims {tuple(grid.dims)}, got {mask.shape}")
+    mhash, full_eq = _mask_key(mask)
     kcode = _kind_code(kind)
     scan = dv.scan_for(ds)
     k0, w = _window(scan.n_samples, window)
     interp = nat.INTERP[interpolation]
-    n = math.prod(grid.dims)
-    dev = dv.device()
-    dense = torch.zeros(n, dtype=torch.float32, device=dev)
-    valid = torch.zeros(n, dtype=torch.uint8, device=dev)
-    status = _Status()
-    region_t = torch.zeros(6, dtype=torch.int32, device=dev)
-    trace_t = torch.zeros(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
-    mask_t = _upload_mask3(mask, grid.dims)
-    full = grid.full_box()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    ev[0].record()
-    _volume_pass(scan, grid, full, d, mask_t, 0, (kcode,), interp, k0, w, {kcode: dense}, valid, status, 0)
-    ev[1].record()
-    _launch_select3(dense, valid, grid, d, full, cfg, region_t, trace_t)
-    ev[2].record()
-    _volume_pass(scan, grid, full, 1, mask_t, d, (kcode,), interp, k0, w, {kcode: dense}, valid, status, 1,
-                 d_region=region_t)
-    ev[3].record()
-    st, th, values, vh = dv.to_host(status.t, trace_t, dense.view(*grid.dims), valid.view(*grid.dims))
-    keys, counts, flags = status.read(st)
-    if flags & 1:
-        raise ValueError("energy map contains non-finite values")
-    final, trace, _ = decode_trace(th.tobytes(), region=_box)
-    vmask = vh.view(bool)
-    composite = VolumeMap(grid, values, vmask, stride=d, roi=final, checked=True)
-    n_c, n_f = int(counts[0]), int(counts[1])
-    EVAL_COUNTER.add(n_c + n_f)
-    key = int(keys[0 if kcode == nat.MWB_DAS else 1])
-    _, ny, nz = grid.dims
-    if key:
-        slot = 0xFFFFFFFF - (key & 0xFFFFFFFF)
-        cell = (slot // (ny * nz), (slot // nz) % ny, slot % nz)
+    key = (scan.geometry_key(), tuple(grid.origin), float(grid.resolution), tuple(grid.dims), d, kcode,
+           cfg.frame_fraction, cfg.n_min, interp, k0, w, mhash)
+    plan = _VOLUME_PLANS.get(key)
+    if plan is None:
+        if not mask[::d, ::d, ::d].any():
+            raise ValueError("no coarse focal points inside the phantom mask")
+        plan = _VolumeFrameworkPlan(scan, grid, d, kcode, cfg, interp, k0, w, mask, full_eq)
+        _VOLUME_PLANS[key] = plan
+        while len(_VOLUME_PLANS) > _VOLUME_PLAN_CAPACITY:
+            _VOLUME_PLANS.popitem(last=False)
     else:
-        cell = composite.argmax_cell()
-    t = [ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3, ev[2].elapsed_time(ev[3]) / 1e3]
-    full_eq = int(mask.sum())
-    report = VolumeReport(
-        decimation_factor=d, iterations=len(trace.records), final_region=final, coarse_points_evaluated=n_c,
-        fine_points_evaluated=n_f, full_equivalent_points=full_eq, reduction_ratio=full_eq / (n_c + n_f),
-        elapsed={"coarse": t[0], "select": t[1], "fine": t[2], "total": sum(t)}, trace=trace, argmax_cell=cell,
-        argmax_position=grid.cell_center(*cell))
-    return composite, report
+        _VOLUME_PLANS.move_to_end(key)
+    plan.launch(scan)
+    return plan.finish()
 
 
 __all__ = [

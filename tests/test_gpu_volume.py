@@ -117,3 +117,23 @@ def test_volume_cache_hit_is_identical(vol):
         for k in ("das", "dmas"):
             assert np.array_equal(f[k].valid, h[k].valid)
             assert np.array_equal(f[k].values[f[k].valid], h[k].values[h[k].valid])
+
+
+def test_octant_framework_replay_and_dataset_switch():
+    """run_framework_volume replays one graph per scanner geometry: a second
+    call on a dataset equals the first, after another dataset ran in between."""
+    vm = synth.VolumeModel(n_samples=1024)
+    g = vm.geometry()
+    grid = VolumeGrid((-0.024, -0.024, 0.0), (0.048, 0.048, 0.024), 0.002)
+    dss = []
+    for seed in (21, 22):
+        sig, _ = synth.scan_3d(vm, seed=seed)
+        dss.append(mw.BackscatterDataset(g, synth.embed_pairs(vm.n_ant, vm.pairs(), sig)))
+    win = (vm.k0, vm.window)
+    first = [run_framework_volume(ds, "das", grid, mw.Manual(3), phantom_radius=0.024, window=win) for ds in dss]
+    again = [run_framework_volume(ds, "das", grid, mw.Manual(3), phantom_radius=0.024, window=win)
+             for ds in (dss[1], dss[0])]
+    for (c0, r0), (c1, r1) in zip(first, again[::-1]):
+        assert np.array_equal(c0.valid, c1.valid)
+        assert np.array_equal(c0.values[c0.valid], c1.values[c1.valid])
+        assert r0.final_region == r1.final_region and r0.argmax_cell == r1.argmax_cell
