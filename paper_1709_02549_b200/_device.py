@@ -11,11 +11,19 @@ cross into ``libmwb.so``.
 
 from __future__ import annotations
 
+import threading
 import weakref
 from dataclasses import dataclass
 
 import numpy as np
 import torch
+
+
+# Captured-graph plans (run_framework, segment, run_framework_volume) own their
+# device and pinned buffers; a call holds this lock from the plan lookup to the
+# readback so concurrent host threads (e.g. a web service's worker pool) never
+# interleave on one plan.
+PLAN_LOCK = threading.RLock()
 
 
 def device() -> torch.device:

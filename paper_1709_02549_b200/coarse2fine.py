@@ -480,9 +480,11 @@ def run_framework(
     mask_np, _ = _breast_mask_device(grid)
     if not mask_np[::d, ::d].any():
         raise ValueError("no coarse focal points inside the breast mask")
-    plan, scan = _plan_for(ds, kind, grid, d, cfg, interpolation, window, {"smem": 0, "gather": 1}[kernel_mode])
-    plan.launch(scan)
-    return plan.finish()
+    with dv.PLAN_LOCK:
+        plan, scan = _plan_for(ds, kind, grid, d, cfg, interpolation, window,
+                               {"smem": 0, "gather": 1}[kernel_mode])
+        plan.launch(scan)
+        return plan.finish()
 
 
 @dataclass
@@ -525,9 +527,10 @@ def consistency_check(
     for dd in (d1, d2):
         if not mask[::dd, ::dd].any():
             raise ValueError("no coarse focal points inside the breast mask")
-    plans = [_plan_for(ds, kind, grid, dd, cfg, "linear", None, 0) for dd in (d1, d2)]
-    for plan, scan in plans:
-        plan.launch(scan)  # both runs are in flight before the first readback
-    (_, rep_a), (_, rep_b) = (plan.finish() for plan, _ in plans)
+    with dv.PLAN_LOCK:
+        plans = [_plan_for(ds, kind, grid, dd, cfg, "linear", None, 0) for dd in (d1, d2)]
+        for plan, scan in plans:
+            plan.launch(scan)  # both runs are in flight before the first readback
+        (_, rep_a), (_, rep_b) = (plan.finish() for plan, _ in plans)
     inter = rep_a.final_region.intersection(rep_b.final_region)
     return CheckVerdict(inter is not None, inter, rep_a.final_region, rep_b.final_region), rep_a, rep_b

@@ -327,20 +327,21 @@ def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.0
         raise ValueError("the segmentation metric needs a non-empty energy window")
     interp = nat.INTERP[interpolation]
     m, mt, mkey = _mask_for(grid, mask)
-    key = (scan.geometry_key(), grid.origin, grid.extent, grid.resolution, region.bounds(), kcode, n_sub, stop_cells,
-           interp, k0, w, mkey, bool(tree))
-    plan = _SEG_PLANS.get(key)
-    if plan is None:
-        tree = (_tree_plan(scan, ds.geometry.antennas, grid, region, mkey, mt, n_sub, stop_cells, n_iter, interp)
-                if tree else None)
-        plan = _SegmentPlan(scan, grid, region, kcode, n_sub, stop_cells, n_iter, interp, k0, w, m, mt, tree)
-        _SEG_PLANS[key] = plan
-        while len(_SEG_PLANS) > _SEG_PLAN_CAPACITY:
-            _SEG_PLANS.popitem(last=False)
-    else:
-        _SEG_PLANS.move_to_end(key)
-    plan.launch(scan)
-    return plan.finish(kind)
+    with dv.PLAN_LOCK:
+        key = (scan.geometry_key(), grid.origin, grid.extent, grid.resolution, region.bounds(), kcode, n_sub,
+               stop_cells, interp, k0, w, mkey, bool(tree))
+        plan = _SEG_PLANS.get(key)
+        if plan is None:
+            tree = (_tree_plan(scan, ds.geometry.antennas, grid, region, mkey, mt, n_sub, stop_cells, n_iter, interp)
+                    if tree else None)
+            plan = _SegmentPlan(scan, grid, region, kcode, n_sub, stop_cells, n_iter, interp, k0, w, m, mt, tree)
+            _SEG_PLANS[key] = plan
+            while len(_SEG_PLANS) > _SEG_PLAN_CAPACITY:
+                _SEG_PLANS.popitem(last=False)
+        else:
+            _SEG_PLANS.move_to_end(key)
+        plan.launch(scan)
+        return plan.finish(kind)
 
 
 def _decode_seg_trace(raw: bytes) -> tuple[list[SegmentRecord], Region]:

@@ -477,20 +477,21 @@ def run_framework_volume(ds, kind, grid: VolumeGrid, mode, cfg: FrameworkConfig 
     scan = dv.scan_for(ds)
     k0, w = _window(scan.n_samples, window)
     interp = nat.INTERP[interpolation]
-    key = (scan.geometry_key(), tuple(grid.origin), float(grid.resolution), tuple(grid.dims), d, kcode,
-           cfg.frame_fraction, cfg.n_min, interp, k0, w, mhash)
-    plan = _VOLUME_PLANS.get(key)
-    if plan is None:
-        if not mask[::d, ::d, ::d].any():
-            raise ValueError("no coarse focal points inside the phantom mask")
-        plan = _VolumeFrameworkPlan(scan, grid, d, kcode, cfg, interp, k0, w, mask, full_eq)
-        _VOLUME_PLANS[key] = plan
-        while len(_VOLUME_PLANS) > _VOLUME_PLAN_CAPACITY:
-            _VOLUME_PLANS.popitem(last=False)
-    else:
-        _VOLUME_PLANS.move_to_end(key)
-    plan.launch(scan)
-    return plan.finish()
+    with dv.PLAN_LOCK:
+        key = (scan.geometry_key(), tuple(grid.origin), float(grid.resolution), tuple(grid.dims), d, kcode,
+               cfg.frame_fraction, cfg.n_min, interp, k0, w, mhash)
+        plan = _VOLUME_PLANS.get(key)
+        if plan is None:
+            if not mask[::d, ::d, ::d].any():
+                raise ValueError("no coarse focal points inside the phantom mask")
+            plan = _VolumeFrameworkPlan(scan, grid, d, kcode, cfg, interp, k0, w, mask, full_eq)
+            _VOLUME_PLANS[key] = plan
+            while len(_VOLUME_PLANS) > _VOLUME_PLAN_CAPACITY:
+                _VOLUME_PLANS.popitem(last=False)
+        else:
+            _VOLUME_PLANS.move_to_end(key)
+        plan.launch(scan)
+        return plan.finish()
 
 
 __all__ = [

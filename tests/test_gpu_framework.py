@@ -331,3 +331,28 @@ class TestDecimationSafety:  # test_acceptance.py:179-233 (criterion 6)
             _, rep = mw.run_framework(mw.BackscatterDataset(geom, sig), "das", grid, mw.Manual(d))
             roi_hits += rep.final_region.contains_cell(*grid.point_to_cell(*tc))
         assert square_hits == 200 and roi_hits >= 190
+
+
+def test_concurrent_host_threads_share_plans_safely():
+    """A service's worker threads calling run_framework / segment at once on
+    different scans of one scanner get the results of sequential calls."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1709_02549_b200 import synth
+    from paper_1709_02549_b200.segment import segment
+
+    model = synth.ScanModel(n_samples=1024)
+    grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 5e-4)
+    dss = [synth.dataset_2d(model, seed=600 + i)[0] for i in range(6)]
+    win = (model.k0, model.window)
+    d = grid.dims[0] // 32
+
+    def one(ds):
+        comp, rep = mw.run_framework(ds, "das", grid, mw.Manual(d), window=win)
+        fine, srep = segment(ds, "dmas", grid, 16, 0.01, window=win)
+        return comp.entries, rep.final_region, fine.entries, srep.argmax_cell
+
+    want = [one(ds) for ds in dss]
+    with ThreadPoolExecutor(max_workers=4) as pool:
+        got = list(pool.map(one, dss * 2))
+    assert got == want * 2
