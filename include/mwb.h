@@ -168,6 +168,24 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
                  uint64_t* key_dmas, int32_t* flags, int mode, void* stream);
 
 /*
+ * mwb_energies with a partials workspace: when the launch has few tiles and
+ * the window spans several 32-sample chunks (the reference's full-record
+ * energies, beamform.py:211-212), the chunks are spread over more CTAs and a
+ * second kernel sums each point's chunk partials in chunk order, so every
+ * energy is bit-identical to mwb_energies.  workspace_bytes >=
+ * mwb_energies_split_bytes(n_pts, n_scans, window) enables the split; with a
+ * smaller (or NULL) workspace the call is exactly mwb_energies.
+ */
+int64_t mwb_energies_split_bytes(int n_pts, int n_scans, int window);
+int mwb_energies_split(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
+                       int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
+                       double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
+                       const int32_t* d_count, const void* table, int interp, int k0, int window,
+                       float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
+                       uint64_t* key_dmas, int32_t* flags, int mode, void* workspace,
+                       int64_t workspace_bytes, void* stream);
+
+/*
  * Packed multi-scan point lists: tile_info[t] = {scan, valid points} (int32
  * pairs) for every 256-point tile t of pts_xyz; each tile belongs to one scan.
  * The table is built per tile; the energy launch evaluates tile t on scan

@@ -105,6 +105,12 @@ _SIGNATURES = {
          _P],
         _I,
     ),
+    "mwb_energies_split_bytes": ([_I, _I, _I], _I64),
+    "mwb_energies_split": (
+        [_P, _I, _I64, _I, _I, _I, _P, _P, _I, _D, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _I64, _P, _P, _P, _I,
+         _P, _I64, _P],
+        _I,
+    ),
     "mwb_energies_tc_workspace_bytes": ([_I, _I, _I], _I64),
     "mwb_table_max_span": ([_P, _I, _I, _P, _P], _I),
     "mwb_table_lo_range": ([_P, _I, _I, _P, _P, _P], _I),

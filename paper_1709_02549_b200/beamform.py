@@ -289,15 +289,29 @@ def launch_energies(scan: dv.DeviceScan, pts: torch.Tensor, n_pts: int, table: t
                     out_idx: torch.Tensor | None = None, d_count: int | None = None,
                     key_das: int | None = None, key_dmas: int | None = None, flags_ptr: int | None = None,
                     mode: int = 0, n_scans: int = 1, sig: torch.Tensor | None = None, scan_stride: int = 0) -> None:
-    """One fused launch: DAS and/or DMAS energies (whichever outputs are given)."""
+    """One fused launch: DAS and/or DMAS energies (whichever outputs are given).
+
+    Windows of several 32-sample chunks (the reference's full record) get a
+    partials workspace, so the library may spread a small launch's chunks over
+    more CTAs (mwb_energies_split; results bit-identical to mwb_energies)."""
     sig = scan.sig if sig is None else sig
+    ws, ws_bytes = None, 0
+    if w > 48 and n_pts > 0:
+        need = int(nat.load().mwb_energies_split_bytes(n_pts, n_scans, w))
+        if 0 < need <= _SPLIT_WS_MAX:
+            ws = torch.empty(need, dtype=torch.uint8, device=sig.device)
+            ws_bytes = need
     nat.call(
-        "mwb_energies",
+        "mwb_energies_split",
         sig.data_ptr(), n_scans, scan_stride, scan.n_chan, scan.ld, scan.n_samples,
         scan.chan.data_ptr(), scan.ant.data_ptr(), scan.n_ant, scan.inv_scale,
         pts.data_ptr(), nat.ptr(out_idx), n_pts, d_count, table.data_ptr(), interp, k0, w,
-        nat.ptr(out_das), nat.ptr(out_dmas), out_stride, key_das, key_dmas, flags_ptr, mode, dv.stream_handle(),
+        nat.ptr(out_das), nat.ptr(out_dmas), out_stride, key_das, key_dmas, flags_ptr, mode, nat.ptr(ws), ws_bytes,
+        dv.stream_handle(),
     )
+
+
+_SPLIT_WS_MAX = 256 << 20  # partials workspace cap: larger launches have the tiles to fill the GPU anyway
 
 
 def lattice_pass(scan: dv.DeviceScan, grid: ImagingGrid, stride: int, mask_t: torch.Tensor | None,

@@ -272,6 +272,11 @@ struct EnergyParams {
   int mode;
   int scans_per_cta;
   int cap;  // floats per stage buffer
+  // window split across CTAs (blockIdx.z takes chunks [z*chunks_per_cta, ...)):
+  // each chunk's per-point {S, Q} go to part[(s * P + point) * n_chunks + q]
+  // and energy_reduce_kernel sums them in chunk order, as the unsplit kernel does
+  float2* part;
+  int chunks_per_cta;
 };
 
 struct SmemLayout {
@@ -626,6 +631,8 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
   const int G = misc[0];
   const int n_groups = misc[1];
   const int n_chunks = (p.W + CH - 1) / CH;
+  const int q_begin = p.part ? (int)blockIdx.z * p.chunks_per_cta : 0;
+  const int n_local = p.part ? min(p.chunks_per_cta, n_chunks - q_begin) : n_chunks;
 
   // Producer (warp 0, all lanes): stage step t into ring slot t % NSTAGE once
   // the consumers released the slot's previous use.  Zero-fills (spans past
@@ -636,8 +643,8 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
     if (use > 0) mbar_wait(&mbar[NSTAGE + b], (use - 1) & 1);
     const int g = t % n_groups;
     const int r = t / n_groups;
-    const int q = r % n_chunks;
-    const int s = scan_begin + r / n_chunks;
+    const int q = q_begin + r % n_local;
+    const int s = scan_begin + r / n_local;
     const int c_begin = g * G, c_end = min(p.C, c_begin + G);
     float* buf = stage + b * p.cap;
     const float* scan_sig = p.sig + (size_t)s * (size_t)p.scan_stride;
@@ -671,10 +678,10 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
     // L2 (a 128^3 volume: 4.2 GB) would put DRAM latency on each channel's
     // word load, so each chunk's first use of a group pulls its block into L2
     // here (later scans of a multi-scan CTA find it there).
-    if (r < n_chunks && lane == 0) bulk_prefetch_l2(tw + (size_t)c_begin * TILE, (uint32_t)(c_end - c_begin) * TILE * 4u);
+    if (r < n_local && lane == 0) bulk_prefetch_l2(tw + (size_t)c_begin * TILE, (uint32_t)(c_end - c_begin) * TILE * 4u);
   };
 
-  const int nsteps = (n_groups > 0 ? n_groups : 1) * n_chunks * n_my_scans;
+  const int nsteps = (n_groups > 0 ? n_groups : 1) * n_local * n_my_scans;
 
   float2 sacc[CH];
   float2 qe = make_float2(0.f, 0.f), qo = make_float2(0.f, 0.f);
@@ -686,8 +693,8 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
   for (int t = 0; t < nsteps; ++t) {
     const int g = G > 0 ? t % n_groups : 0;
     const int r = G > 0 ? t / n_groups : t;
-    const int q = r % n_chunks;
-    const int s = scan_begin + r / n_chunks;
+    const int q = q_begin + r % n_local;
+    const int s = scan_begin + r / n_local;
     const int valid = min(CH, p.W - q * CH);
     const int cb = p.k0 + q * CH;
 
@@ -753,7 +760,14 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
       }
     }
 
-    if (g == (G > 0 ? n_groups - 1 : 0)) {
+    if (g == (G > 0 ? n_groups - 1 : 0) && p.part) {
+      // window split: this chunk's sums go to the reduce pass
+      const float2 S = chunk_sumsq<CH>(sacc, valid);
+      const float2 Q = KIND != KIND_DAS ? __fadd2_rn(qe, qo) : make_float2(0.f, 0.f);
+      float2* pp = p.part + ((size_t)s * p.P + tile0) * n_chunks + q;
+      if (va) pp[(size_t)la * n_chunks] = make_float2(S.x, Q.x);
+      if (vb) pp[(size_t)lb * n_chunks] = make_float2(S.y, Q.y);
+    } else if (g == (G > 0 ? n_groups - 1 : 0)) {
       const float2 S = chunk_sumsq<CH>(sacc, valid);
       eS_a += (double)S.x;
       eS_b += (double)S.y;
@@ -2251,6 +2265,47 @@ __global__ void __launch_bounds__(1024) mb_lds_pattern_kernel(float* sink, int p
   if (r == 1234.5f) sink[threadIdx.x] = r;
 }
 
+// Second pass of a window-split launch: per (scan, point), the chunk sums in
+// chunk order (fp64), then exactly the unsplit kernel's epilogue.
+template <int KIND>
+__global__ void __launch_bounds__(256) energy_reduce_kernel(const EnergyParams p, int n_chunks) {
+  const int s = blockIdx.y;
+  const int n_pts = p.d_count ? min(*p.d_count, p.P) : p.P;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool v = i < n_pts;
+  double eS = 0.0, eQ = 0.0;
+  if (v) {
+    const float2* pp = p.part + ((size_t)s * p.P + i) * n_chunks;
+    for (int q = 0; q < n_chunks; ++q) {
+      const float2 sq = pp[q];
+      eS += (double)sq.x;
+      if (KIND != KIND_DAS) eQ += (double)sq.y;
+    }
+  }
+  const int o = v ? (p.out_idx ? __ldg(p.out_idx + i) : i) : -1;
+  const int lane = threadIdx.x & 31;
+  bool bad = false;
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk) {
+    const bool want = kk == 0 ? KIND != KIND_DMAS : KIND != KIND_DAS;
+    if (!want) continue;
+    const float e = kk == 0 ? __double2float_rn(eS) : __double2float_rn(0.5 * (eS - eQ));
+    float* out = (kk == 0 ? p.out_das : p.out_dmas) + (size_t)s * (size_t)p.out_stride;
+    unsigned long long* keys = kk == 0 ? p.key_das : p.key_dmas;
+    unsigned long long key = 0ull;
+    if (v) {
+      out[o] = e;
+      if (isfinite(e)) key = argmax_key(e, o); else bad = true;
+    }
+    if (keys) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, off));
+      if (lane == 0 && key != 0ull) atomicMax(keys + s, key);
+    }
+  }
+  if (bad && p.flags) atomicOr(p.flags, 1);
+}
+
 int choose_scans_per_cta(int tiles, int n_scans) {
   const long long target = 148LL * 3 * 8;  // >= 8 waves of 3 CTAs/SM
   long long spc = (long long)tiles * n_scans / target;
@@ -2395,6 +2450,8 @@ static int energy_params(const float* sig, int n_scans, int64_t scan_stride, int
   p.mode = mode;
   p.scans_per_cta = 1;
   p.cap = 0;
+  p.part = nullptr;
+  p.chunks_per_cta = 0;
   return MWB_OK;
 }
 
@@ -2404,7 +2461,8 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
                          const int32_t* d_count, const int32_t* tile_info, const void* table, int interp, int k0,
                          int window, float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
                          uint64_t* key_dmas, int32_t* flags, int mode, void* stream,
-                         const int32_t* tile_src = nullptr, int n_src_pts = 0) {
+                         const int32_t* tile_src = nullptr, int n_src_pts = 0, void* part_ws = nullptr,
+                         int64_t part_bytes = 0) {
   // tile_src (with tile_info): launched tile t evaluates source tile tile_src[t]
   // of a shared point list / table of n_src_pts points; n_pts counts the
   // launched (packed output) positions
@@ -2441,6 +2499,23 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   if (L.total > 227 * 1024)
     return set_err(MWB_ERANGE, "mwb_energies: shared memory %lld bytes exceeds 227 KB", (long long)L.total);
   dim3 grid((unsigned)tiles, tile_info ? 1 : (n_scans + p.scans_per_cta - 1) / p.scans_per_cta);
+  // Window split: a launch with few tiles and a long window (the reference's
+  // full-record energies) leaves most SMs idle, so the window's chunks are
+  // spread over grid.z when the caller passed a partials workspace.  Launches
+  // over a device count (lattice passes) may hold far fewer points than their
+  // tile bound, so they are treated as small.
+  const int n_chunks = (window + ch - 1) / ch;
+  if (part_ws && !tile_info && n_chunks > 1) {
+    const long long work_ctas = (long long)(d_count ? std::min<long long>(tiles, 16) : tiles) * grid.y;
+    const long long target = 148LL * resident * 4;
+    long long groups = std::min<long long>(n_chunks, (target + work_ctas - 1) / work_ctas);
+    const long long need = (long long)n_scans * n_pts * n_chunks * (long long)sizeof(float2);
+    if (groups > 1 && need <= part_bytes && grid.y * groups <= 65535) {
+      p.chunks_per_cta = (int)((n_chunks + groups - 1) / groups);
+      grid.z = (unsigned)((n_chunks + p.chunks_per_cta - 1) / p.chunks_per_cta);
+      p.part = reinterpret_cast<float2*>(part_ws);
+    }
+  }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int kind = out_das && out_dmas ? KIND_BOTH : (out_das ? KIND_DAS : KIND_DMAS);
   // MWB_MINB=4 selects the 4-CTA/SM (<=128 registers) build of the 32-sample kernel
@@ -2466,7 +2541,12 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   fn<<<grid, TPB, L.total, st>>>(p);
-  return check_launch("energy_kernel");
+  if (!p.part) return check_launch("energy_kernel");
+  if (const int lrc = check_launch("energy_kernel")) return lrc;
+  void (*rk)(EnergyParams, int) = kind == KIND_DAS ? energy_reduce_kernel<KIND_DAS>
+                                  : (kind == KIND_DMAS ? energy_reduce_kernel<KIND_DMAS> : energy_reduce_kernel<KIND_BOTH>);
+  rk<<<dim3((unsigned)((n_pts + 255) / 256), (unsigned)n_scans), 256, 0, st>>>(p, n_chunks);
+  return check_launch("energy_reduce_kernel");
 }
 
 int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
@@ -2478,6 +2558,24 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
   return energies_impl(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
                        pts_xyz, out_idx, n_pts, d_count, nullptr, table, interp, k0, window, out_das, out_dmas,
                        out_stride, key_das, key_dmas, flags, mode, stream);
+}
+
+int64_t mwb_energies_split_bytes(int n_pts, int n_scans, int window) {
+  if (n_pts < 0 || n_scans < 0 || window < 0) return -1;
+  const int ch = (window % 48 == 0 && window % 32 != 0) ? MWB_W48_CH : 32;
+  return (int64_t)n_pts * n_scans * ((window + ch - 1) / ch) * (int64_t)sizeof(float2);
+}
+
+int mwb_energies_split(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
+                       int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
+                       double inv_scale, const double* pts_xyz, const int32_t* out_idx, int n_pts,
+                       const int32_t* d_count, const void* table, int interp, int k0, int window,
+                       float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
+                       uint64_t* key_dmas, int32_t* flags, int mode, void* workspace, int64_t workspace_bytes,
+                       void* stream) {
+  return energies_impl(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
+                       pts_xyz, out_idx, n_pts, d_count, nullptr, table, interp, k0, window, out_das, out_dmas,
+                       out_stride, key_das, key_dmas, flags, mode, stream, nullptr, 0, workspace, workspace_bytes);
 }
 
 int mwb_energies_tiles(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
