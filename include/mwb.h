@@ -321,6 +321,8 @@ int mwb_segment_batch(const float* sig, int n_scans, int64_t scan_stride, int n_
  *   mwb_segment_batch then).
  * mwb_segment_plan_prepare: fills the plan (synchronises `stream` once: the
  *   node list is copied from the host).
+ * mwb_segment_run_workspace_bytes: includes, for small batches with windows
+ *   of several chunks (the full record), room for window-split partials.
  * mwb_segment_run: the search for S scans as in mwb_segment_batch, then every
  *   scan's fine pass into out_fine + s * out_stride (slot ix * ny + iy of the
  *   final region's cells; other slots untouched), argmax keys keys[s] (as
@@ -334,7 +336,7 @@ int mwb_segment_plan_prepare(const int32_t* chan_txrx, int n_chan, const double*
                              double inv_scale, int interp, double ox, double oy, double res, int nx,
                              int ny, int x0, int y0, int x1, int y1, const uint8_t* mask, int n_sub,
                              int stop_cells, int max_iters, void* plan, void* stream);
-int64_t mwb_segment_run_workspace_bytes(int n_scans, int n_sub, int fine_tiles_per_scan);
+int64_t mwb_segment_run_workspace_bytes(int n_scans, int n_sub, int fine_tiles_per_scan, int window);
 int mwb_segment_run(const void* plan, const float* sig, int n_scans, int64_t scan_stride, int n_chan,
                     int ld, int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
                     double inv_scale, int interp, int k0, int window, int kind, int nx, int ny, int x0,

@@ -174,7 +174,7 @@ _SIGNATURES = {
         [_P, _I, _P, _I, _D, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I, _P, _P],
         _I,
     ),
-    "mwb_segment_run_workspace_bytes": ([_I, _I, _I], _I64),
+    "mwb_segment_run_workspace_bytes": ([_I, _I, _I, _I], _I64),
     "mwb_segment_run": (
         [_P, _P, _I, _I64, _I, _I, _I, _P, _P, _I, _D, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P,
          _P, _P, _I64, _P, _P, _P, _P, _P],

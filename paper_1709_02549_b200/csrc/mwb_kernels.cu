@@ -764,7 +764,8 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
       // window split: this chunk's sums go to the reduce pass
       const float2 S = chunk_sumsq<CH>(sacc, valid);
       const float2 Q = KIND != KIND_DAS ? __fadd2_rn(qe, qo) : make_float2(0.f, 0.f);
-      float2* pp = p.part + ((size_t)s * p.P + tile0) * n_chunks + q;
+      // rows: (scan, point) for shared point lists, the launched position for packed per-scan lists
+      float2* pp = p.part + ((p.tile_info ? (size_t)0 : (size_t)s * p.P) + tile0) * n_chunks + q;
       if (va) pp[(size_t)la * n_chunks] = make_float2(S.x, Q.x);
       if (vb) pp[(size_t)lb * n_chunks] = make_float2(S.y, Q.y);
     } else if (g == (G > 0 ? n_groups - 1 : 0)) {
@@ -2269,20 +2270,31 @@ __global__ void __launch_bounds__(1024) mb_lds_pattern_kernel(float* sink, int p
 // chunk order (fp64), then exactly the unsplit kernel's epilogue.
 template <int KIND>
 __global__ void __launch_bounds__(256) energy_reduce_kernel(const EnergyParams p, int n_chunks) {
-  const int s = blockIdx.y;
-  const int n_pts = p.d_count ? min(*p.d_count, p.P) : p.P;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool v = i < n_pts;
+  int s = blockIdx.y, src = i;
+  bool v;
+  size_t row;
+  if (p.tile_info) {  // packed per-scan lists: launched position i, its tile's scan and source point
+    const int2 ti = p.tile_info[i / TILE];
+    s = ti.x;
+    v = i < p.P && (i % TILE) < ti.y && s >= 0;
+    if (p.tile_src) src = __ldg(p.tile_src + i / TILE) * TILE + i % TILE;
+    row = (size_t)i;
+  } else {
+    const int n_pts = p.d_count ? min(*p.d_count, p.P) : p.P;
+    v = i < n_pts;
+    row = (size_t)s * p.P + i;
+  }
   double eS = 0.0, eQ = 0.0;
   if (v) {
-    const float2* pp = p.part + ((size_t)s * p.P + i) * n_chunks;
+    const float2* pp = p.part + row * n_chunks;
     for (int q = 0; q < n_chunks; ++q) {
       const float2 sq = pp[q];
       eS += (double)sq.x;
       if (KIND != KIND_DAS) eQ += (double)sq.y;
     }
   }
-  const int o = v ? (p.out_idx ? __ldg(p.out_idx + i) : i) : -1;
+  const int o = v ? (p.out_idx ? __ldg(p.out_idx + src) : i) : -1;
   const int lane = threadIdx.x & 31;
   bool bad = false;
 #pragma unroll
@@ -2297,7 +2309,7 @@ __global__ void __launch_bounds__(256) energy_reduce_kernel(const EnergyParams p
       out[o] = e;
       if (isfinite(e)) key = argmax_key(e, o); else bad = true;
     }
-    if (keys) {
+    if (keys) {  // a warp's positions lie in one 256-point tile, hence one scan
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, off));
       if (lane == 0 && key != 0ull) atomicMax(keys + s, key);
@@ -2505,11 +2517,12 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   // over a device count (lattice passes) may hold far fewer points than their
   // tile bound, so they are treated as small.
   const int n_chunks = (window + ch - 1) / ch;
-  if (part_ws && !tile_info && n_chunks > 1) {
+  if (part_ws && n_chunks > 1) {
     const long long work_ctas = (long long)(d_count ? std::min<long long>(tiles, 16) : tiles) * grid.y;
     const long long target = 148LL * resident * 4;
     long long groups = std::min<long long>(n_chunks, (target + work_ctas - 1) / work_ctas);
-    const long long need = (long long)n_scans * n_pts * n_chunks * (long long)sizeof(float2);
+    const long long rows = tile_info ? (long long)n_pts : (long long)n_scans * n_pts;
+    const long long need = rows * n_chunks * (long long)sizeof(float2);
     if (groups > 1 && need <= part_bytes && grid.y * groups <= 65535) {
       p.chunks_per_cta = (int)((n_chunks + groups - 1) / groups);
       grid.z = (unsigned)((n_chunks + p.chunks_per_cta - 1) / p.chunks_per_cta);
@@ -2545,7 +2558,7 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   if (const int lrc = check_launch("energy_kernel")) return lrc;
   void (*rk)(EnergyParams, int) = kind == KIND_DAS ? energy_reduce_kernel<KIND_DAS>
                                   : (kind == KIND_DMAS ? energy_reduce_kernel<KIND_DMAS> : energy_reduce_kernel<KIND_BOTH>);
-  rk<<<dim3((unsigned)((n_pts + 255) / 256), (unsigned)n_scans), 256, 0, st>>>(p, n_chunks);
+  rk<<<dim3((unsigned)((n_pts + 255) / 256), tile_info ? 1u : (unsigned)n_scans), 256, 0, st>>>(p, n_chunks);
   return check_launch("energy_reduce_kernel");
 }
 
@@ -3370,13 +3383,28 @@ int mwb_segment_plan_prepare(const int32_t* chan_txrx, int n_chan, const double*
   return MWB_OK;
 }
 
-int64_t mwb_segment_run_workspace_bytes(int n_scans, int n_sub, int fine_tps) {
-  if (n_scans < 1 || n_scans > 65535 || n_sub < 1 || n_sub > 64 || fine_tps < 0) return -1;
+// Chunk partials for window-split launches of a small batch (long windows,
+// e.g. the full record): sized for the larger of the search and fine lists,
+// and only while that stays small (large batches fill the GPU unsplit).
+static long long seg_run_part_bytes(int n_scans, int n_sub, int fine_tps, int window) {
+  const int ch = (window % 48 == 0 && window % 32 != 0) ? MWB_W48_CH : 32;
+  const long long n_chunks = (window + ch - 1) / ch;
+  const long long rows = (long long)n_scans * std::max<long long>(seg_batch_per_scan(n_sub), (long long)fine_tps * TILE);
+  const long long bytes = rows * n_chunks * (long long)sizeof(float2);
+  return (n_chunks > 1 && bytes <= (64LL << 20)) ? bytes : 0;
+}
+
+static long long seg_run_base_bytes(int n_scans, int n_sub, int fine_tps) {
   const long long per = seg_batch_per_scan(n_sub), n = per * n_scans;
   const long long ft = (long long)n_scans * fine_tps;
   return (long long)align_up(sizeof(SegState) * (size_t)n_scans, 256) + (long long)align_up(4 * n, 256) +
          (long long)align_up(4 * (n / TILE), 256) + (long long)align_up(8 * (n / TILE), 256) +
          (long long)align_up(4 * ft, 256) + (long long)align_up(8 * ft, 256);
+}
+
+int64_t mwb_segment_run_workspace_bytes(int n_scans, int n_sub, int fine_tps, int window) {
+  if (n_scans < 1 || n_scans > 65535 || n_sub < 1 || n_sub > 64 || fine_tps < 0 || window < 0) return -1;
+  return seg_run_base_bytes(n_scans, n_sub, fine_tps) + seg_run_part_bytes(n_scans, n_sub, fine_tps, window);
 }
 
 int mwb_segment_run(const void* plan, const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
@@ -3413,6 +3441,8 @@ int mwb_segment_run(const void* plan, const float* sig, int n_scans, int64_t sca
   int* f_src = reinterpret_cast<int*>(ws);
   ws += align_up(4 * ft, 256);
   int2* f_info = reinterpret_cast<int2*>(ws);
+  void* part = reinterpret_cast<unsigned char*>(workspace) + seg_run_base_bytes(n_scans, n_sub, T.fine_tps);
+  const long long part_bytes = seg_run_part_bytes(n_scans, n_sub, T.fine_tps, window);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   seg_tree_init_kernel<<<(n_scans + 255) / 256, 256, 0, cs>>>(st, n_scans, x0, y0, x1, y1, stop_cells, d_traces,
                                                                nodes, tps, lw, s_src, s_info);
@@ -3423,7 +3453,7 @@ int mwb_segment_run(const void* plan, const float* sig, int n_scans, int64_t sca
                             reinterpret_cast<const double*>(pb + L.s_pts), nullptr, (int)n, nullptr,
                             reinterpret_cast<const int32_t*>(s_info), pb + L.s_table, interp, k0, window,
                             kind == MWB_DAS ? e : nullptr, kind == MWB_DMAS ? e : nullptr, 0, nullptr, nullptr,
-                            nullptr, 0, stream, s_src, (int)s_pts)))
+                            nullptr, 0, stream, s_src, (int)s_pts, part_bytes ? part : nullptr, part_bytes)))
       return rc;
     seg_tree_score_kernel<<<n_scans, 256, 0, cs>>>(st, e, (int)per, n_sub, kind == MWB_DMAS, stop_cells, lowres,
                                                    d_traces, nodes, s_src, s_info);
@@ -3439,7 +3469,7 @@ int mwb_segment_run(const void* plan, const float* sig, int n_scans, int64_t sca
                        (int)(ft * TILE), nullptr, reinterpret_cast<const int32_t*>(f_info), pb + L.f_table, interp,
                        k0, window, kind == MWB_DAS ? out_fine : nullptr, kind == MWB_DMAS ? out_fine : nullptr,
                        out_stride, kind == MWB_DAS ? keys : nullptr, kind == MWB_DMAS ? keys : nullptr, flags, 0,
-                       stream, f_src, (int)T.fine_bound);
+                       stream, f_src, (int)T.fine_bound, part_bytes ? part : nullptr, part_bytes);
 }
 
 // One-call lattice image (beamform.py:283-342 as a single C entry point): the

@@ -170,7 +170,7 @@ class _SegmentPlan:
         dev = dv.device()
         n_low = (2 * n_sub) ** 2
         lib = nat.load()
-        ws_bytes = (lib.mwb_segment_run_workspace_bytes(1, n_sub, tree[1]) if tree is not None
+        ws_bytes = (lib.mwb_segment_run_workspace_bytes(1, n_sub, tree[1], w) if tree is not None
                     else lib.mwb_segment_workspace_bytes(n_sub, scan.n_chan))
         self.ws = torch.empty(int(ws_bytes), dtype=torch.uint8, device=dev)
         self.region_t = torch.zeros(6, dtype=torch.int32, device=dev)
@@ -482,7 +482,7 @@ class SegmentBatch:
         sc = self.scan
         n_low = (2 * self.n_sub) ** 2
         if self.plan is not None:
-            ws_bytes = int(lib.mwb_segment_run_workspace_bytes(s_n, self.n_sub, self.fine_tps))
+            ws_bytes = int(lib.mwb_segment_run_workspace_bytes(s_n, self.n_sub, self.fine_tps, self.w))
         else:
             ws_bytes = int(lib.mwb_segment_batch_workspace_bytes(s_n, self.n_sub, self.n_chan))
         if self._ws is None or self._ws.numel() < ws_bytes:

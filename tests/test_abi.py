@@ -187,4 +187,4 @@ def test_segment_plan_info_rejects_huge_trees_and_bad_args(lib):
     assert b"too many regions" in lib.mwb_last_error()
     assert lib.mwb_segment_plan_info(100, 100, 0, 0, 100, 99, 16, 8, 4, 66, info) != 0  # region outside the grid
     assert lib.mwb_segment_plan_info(100, 100, 0, 0, 99, 99, 0, 8, 4, 66, info) != 0  # n_sub
-    assert lib.mwb_segment_run_workspace_bytes(0, 16, 3) == -1
+    assert lib.mwb_segment_run_workspace_bytes(0, 16, 3, 32) == -1

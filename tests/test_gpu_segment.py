@@ -198,3 +198,27 @@ def test_segment_batch_odd_region_and_small_stop():
             assert _records_equal(r.records(s), rep.records)
             assert tuple(r.argmax_cells[s]) == rep.argmax_cell
             assert r.fine(s).entries == fine.entries
+
+
+def test_full_record_split_paths_agree():
+    """The reference's default window (the full record) on the segmentation:
+    the tree path splits its long-window launches over chunk groups
+    (mwb_energies_split semantics inside mwb_segment_run), the per-iteration
+    path does not; both, and a small SegmentBatch, give the same bits."""
+    import torch
+
+    from paper_1709_02549_b200.segment import SegmentBatch
+
+    model = synth.ScanModel(n_samples=1024)
+    seeds = [31, 32, 33]
+    sig, _ = synth.batch_2d(model, seeds, phantom_radius=(0.04, 0.05))
+    grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 5e-4)
+    res = SegmentBatch(model.geometry(), model.pairs(), model.n_samples, grid, "dmas").run(
+        torch.from_numpy(sig).cuda())
+    for s in range(len(seeds)):
+        ds = mw.BackscatterDataset(model.geometry(), synth.embed_pairs(12, model.pairs(), sig[s].astype(np.float64)))
+        f_t, r_t = segment(ds, "dmas", grid)
+        f_n, r_n = segment(ds, "dmas", grid, tree=False)
+        assert f_t.entries == f_n.entries and _records_equal(r_t.records, r_n.records)
+        assert np.array_equal(r_t.lowres, r_n.lowres) and r_t.argmax_cell == r_n.argmax_cell
+        assert res.fine(s).entries == f_t.entries and _records_equal(res.records(s), r_t.records)
