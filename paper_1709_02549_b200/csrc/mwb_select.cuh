@@ -1,0 +1,712 @@
+// mwb_select.cuh — K2 / K2w device select_roi (coarse2fine.py:169-256), quadrants and octants
+// (included by mwb_kernels.cu inside its anonymous namespace; one translation unit)
+#pragma once
+
+// ----------------------------------------------------------------------------
+// K2: device-resident select_roi (coarse2fine.py:169-256), one CTA.
+// 2-D grids split into the reference's 4 quadrants (geometry.py:225-242);
+// 3-D grids (nz > 1) into 8 octants with the same rules per axis.
+// ----------------------------------------------------------------------------
+constexpr int SEL_TPB = 256;
+constexpr int MAXCH = MWB_MAX_CHILDREN;
+
+struct Box {
+  int lo[3], hi[3];
+};
+
+__device__ __forceinline__ bool box_contains(const Box& r, int ix, int iy, int iz) {
+  return r.lo[0] <= ix && ix <= r.hi[0] && r.lo[1] <= iy && iy <= r.hi[1] && r.lo[2] <= iz &&
+         iz <= r.hi[2];
+}
+
+// children in the reference quadrant order: index = xh + 2*yh (+ 4*zh)
+__host__ __device__ __forceinline__ int split_box(const Box& r, int dims, Box q[MAXCH]) {
+  int mid[3];
+  for (int a = 0; a < dims; ++a) {
+    const int w = r.hi[a] - r.lo[a] + 1;
+    if (w < 2) return 0;
+    mid[a] = r.lo[a] + (w + 1) / 2 - 1;  // last cell of the low half
+  }
+  const int n = 1 << dims;
+  for (int k = 0; k < n; ++k) {
+    for (int a = 0; a < 3; ++a) {
+      if (a >= dims) {
+        q[k].lo[a] = r.lo[a];
+        q[k].hi[a] = r.hi[a];
+      } else if ((k >> a) & 1) {
+        q[k].lo[a] = mid[a] + 1;
+        q[k].hi[a] = r.hi[a];
+      } else {
+        q[k].lo[a] = r.lo[a];
+        q[k].hi[a] = mid[a];
+      }
+    }
+  }
+  return n;
+}
+
+// Region.expand (geometry.py:244-257): grow by ceil(f*side), clipped
+__device__ __forceinline__ Box expand_box(const Box& r, double f, const Box& clip, int dims) {
+  Box e = r;
+  for (int a = 0; a < dims; ++a) {
+    const int g = (int)ceil(__dmul_rn(f, (double)(r.hi[a] - r.lo[a] + 1)));
+    e.lo[a] = max(r.lo[a] - g, clip.lo[a]);
+    e.hi[a] = min(r.hi[a] + g, clip.hi[a]);
+  }
+  return e;
+}
+
+template <int K>
+__device__ void block_sum(double (&v)[K], double* red /* [8][K] */, double* outv /* [K] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) red[warp * K + k] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double x = 0.0;
+    for (int w = 0; w < SEL_TPB / 32; ++w) x += red[w * K + threadIdx.x];  // fixed order
+    outv[threadIdx.x] = x;
+  }
+  __syncthreads();
+}
+
+struct SelectParams {
+  const float* dense;
+  const uint8_t* valid;
+  int nx, ny, nz, D, dims;
+  Box breast;
+  double frac;
+  int n_min;
+  int* region_out;
+  mwb_trace_t* trace;
+  long long dense_stride;  // batched selection: floats between consecutive scans' maps
+  int staged;       // 1: the breast box's lattice is staged in shared memory
+  int sl0[3], sL[3];  // staged lattice origin / extent (lattice units)
+};
+
+constexpr int SEL_STAGE_MAX = 24576;  // lattice cells staged in shared memory (96 KB)
+
+// visit valid lattice cells of box r (from the shared-memory copy when staged;
+// entries without a value are NaN there, as energies are always finite)
+template <class F>
+__device__ __forceinline__ void for_cells(const SelectParams& p, const float* sv, const Box& r, F&& f) {
+  const int D = p.D;
+  int l0[3], L[3];
+  for (int a = 0; a < 3; ++a) {
+    l0[a] = (r.lo[a] + D - 1) / D;
+    const int l1 = r.hi[a] / D;
+    if (l1 < l0[a]) return;
+    L[a] = l1 - l0[a] + 1;
+  }
+  const int n = L[0] * L[1] * L[2];
+  for (int i = threadIdx.x; i < n; i += SEL_TPB) {
+    const int lz = i % L[2], ly = (i / L[2]) % L[1], lx = i / (L[2] * L[1]);
+    const int ix = (l0[0] + lx) * D, iy = (l0[1] + ly) * D, iz = (l0[2] + lz) * D;
+    if (p.staged) {
+      const int si = ((l0[0] + lx - p.sl0[0]) * p.sL[1] + (l0[1] + ly - p.sl0[1])) * p.sL[2] + (l0[2] + lz - p.sl0[2]);
+      const float v = sv[si];
+      if (v == v) f(ix, iy, iz, (double)v);
+    } else {
+      const size_t slot = ((size_t)ix * p.ny + iy) * p.nz + iz;
+      if (p.valid[slot]) f(ix, iy, iz, (double)p.dense[slot]);
+    }
+  }
+}
+
+__device__ __forceinline__ void put_box(int32_t* dst, const Box& b) {
+  dst[0] = b.lo[0]; dst[1] = b.lo[1]; dst[2] = b.lo[2];
+  dst[3] = b.hi[0]; dst[4] = b.hi[1]; dst[5] = b.hi[2];
+}
+
+// One select_roi decision (coarse2fine.py:207-252) from the children's and
+// expansions' statistics: scores (variance on the first iteration, Eq. (5)
+// after), np.argmax, the n_min stop, W/B of the previous vs the new selection
+// and the record.  Called by all 32 lanes of one warp: lane k scores child k
+// and writes its record fields, the argmax is a shuffle reduction, lane 0
+// does W/B.  Returns the termination code (every lane); lane 0 writes, when
+// the loop goes on, nxt = {W, B, n, sum, m2} of the new selection and next_sel.
+template <int NK>
+__device__ int select_score(const SelectParams& p, mwb_trace_t* tr, int iteration, int nk, const Box* rg,
+                            const double* cnt, const double* sums, const double* mean, const double* m2,
+                            double n_sel, double sum_sel, double m2_sel, double sigma_prev_sq, bool have_prev,
+                            double prev_w, double prev_b, double* nxt, Box* next_sel) {
+  const int lane = threadIdx.x & 31;
+  const int rec_i = iteration;
+  mwb_iter_record_t* rec = rec_i < MWB_MAX_ITERS ? &tr->records[rec_i] : nullptr;
+  // the record's fields go straight to global memory; entries past
+  // n_children and unset delta fields are zero
+  const int k = lane;
+  int has = 0, clamped = 0, count = 0;
+  double mu = 0.0, var = 0.0, dr = 0.0, dl = 0.0, sc = -INFINITY;
+  if (k < nk) {
+    count = (int)cnt[k];
+    if (cnt[k] != 0.0) {  // else an empty child: -inf (coarse2fine.py:215-217)
+      mu = mean[k];
+      var = m2[k] / cnt[k];
+      if (iteration == 0) {  // first iteration scores by variance (218-220)
+        sc = var;
+        has = 1;
+      } else {  // Eq. (5) (_metric_parts, 67-91)
+        has = 2;
+        if (var == 0.0) {
+          sc = mu;
+        } else {
+          dr = __ddiv_rn(__dsub_rn(var, sigma_prev_sq), var);
+          dl = fmin(fmax(dr, 0.0), 1.0);
+          sc = __dadd_rn(__dmul_rn(__dsub_rn(1.0, dl), mu), __dmul_rn(dl, var));
+          clamped = dl != dr;
+        }
+      }
+    }
+  }
+  if (rec && k < MWB_MAX_CHILDREN) {
+    rec->counts[k] = count;
+    rec->has_stats[k] = has;
+    rec->clamped[k] = clamped;
+    rec->scores[k] = k < nk ? sc : 0.0;
+    rec->mu[k] = mu;
+    rec->var[k] = var;
+    rec->delta_raw[k] = dr;
+    rec->delta[k] = dl;
+  }
+  // np.argmax (first maximum): the larger score wins, ties go to the lower index
+  double best = sc;
+  int selq = k < nk ? k : 0x7FFF, selc = count;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oq = __shfl_xor_sync(0xffffffffu, selq, o), oc = __shfl_xor_sync(0xffffffffu, selc, o);
+    if (ob > best || (ob == best && oq < selq)) {
+      best = ob;
+      selq = oq;
+      selc = oc;
+    }
+  }
+  if (selq >= nk) selq = 0;  // every score -inf: argmax returns 0
+  if ((selq == 0 ? (int)cnt[0] : selc) < p.n_min) return MWB_TERM_N_MIN;
+  const int e = nk + selq;
+  const double n_e = cnt[e], sum_e = sums[e], m2_e = m2[e];
+  // W, B of the previous vs the new selection (class_distances, 94-109)
+  const double w = __dadd_rn(m2_sel, m2_e);
+  const double ma = sum_sel / n_sel, mb = sum_e / n_e;
+  const double grand = __ddiv_rn(__dadd_rn(sum_sel, sum_e), __dadd_rn(n_sel, n_e));
+  const double da = __dsub_rn(ma, grand), db = __dsub_rn(mb, grand);
+  const double b = __dadd_rn(__dmul_rn(n_sel, __dmul_rn(da, da)), __dmul_rn(n_e, __dmul_rn(db, db)));
+  const bool satisfied = !have_prev || (b > prev_b || w < prev_w);  // OR (235)
+  if (lane == 0) {
+    if (rec) {
+      rec->iteration = iteration + 1;
+      rec->n_children = nk;
+      rec->selected = selq;
+      rec->satisfied = satisfied;
+      put_box(rec->selected_region, rg[selq]);
+      put_box(rec->expanded_region, rg[e]);
+      rec->w = w;
+      rec->b = b;
+    }
+    nxt[0] = w;
+    nxt[1] = b;
+    nxt[2] = n_e;
+    nxt[3] = sum_e;
+    nxt[4] = m2_e;
+    *next_sel = rg[e];
+  }
+  return rec_i >= MWB_MAX_ITERS ? MWB_TERM_OVERFLOW : (satisfied ? MWB_TERM_NONE : MWB_TERM_DISTANCE);
+}
+
+template <int NK>  // 4 children (2-D quadrants) or 8 (3-D octants)
+__global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams p0) {
+  // CTA b handles scan b of a batch (maps dense_stride floats apart)
+  SelectParams p = p0;
+  p.dense += (size_t)blockIdx.x * p0.dense_stride;
+  p.region_out += 6 * blockIdx.x;
+  p.trace += blockIdx.x;
+  __shared__ double red[8 * 2 * 2 * NK];
+  __shared__ double res[2 * 2 * NK];
+  __shared__ int ctl[2];
+  __shared__ Box next_sel;
+  extern __shared__ float sv[];
+  mwb_trace_t* tr = p.trace;
+  if (p.staged) {  // one pass over global memory; every later pass reads shared memory
+    const int n = p.sL[0] * p.sL[1] * p.sL[2];
+    for (int i = threadIdx.x; i < n; i += SEL_TPB) {
+      const int lz = i % p.sL[2], ly = (i / p.sL[2]) % p.sL[1], lx = i / (p.sL[2] * p.sL[1]);
+      const size_t slot = ((size_t)(p.sl0[0] + lx) * p.D * p.ny + (size_t)(p.sl0[1] + ly) * p.D) * p.nz +
+                          (size_t)(p.sl0[2] + lz) * p.D;
+      sv[i] = p.valid[slot] ? p.dense[slot] : __int_as_float(0x7fc00000);
+    }
+    __syncthreads();
+  }
+
+  // breast-region stats: count, sum, min, max (coarse2fine.py:186-199)
+  double n_sel, sum_sel, m2_sel;
+  {
+    double acc[2] = {0.0, 0.0};
+    double mn = INFINITY, mx = -INFINITY;
+    for_cells(p, sv, p.breast, [&](int, int, int, double v) {
+      acc[0] += 1.0;
+      acc[1] += v;
+      mn = fmin(mn, v);
+      mx = fmax(mx, v);
+    });
+    block_sum<2>(acc, red, res);
+    n_sel = res[0];
+    sum_sel = res[1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+      red[warp] = mn;
+      red[8 + warp] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < SEL_TPB / 32; ++w) {
+        red[0] = fmin(red[0], red[w]);
+        red[8] = fmax(red[8], red[8 + w]);
+      }
+    }
+    __syncthreads();
+    mn = red[0];
+    mx = red[8];
+    __syncthreads();
+    if (n_sel == 0.0 || mx == mn) {
+      if (threadIdx.x == 0) {
+        tr->termination = n_sel == 0.0 ? MWB_TERM_EMPTY : MWB_TERM_DEGENERATE;
+        tr->n_records = 0;
+        put_box(tr->final_region, p.breast);
+        put_box(p.region_out, p.breast);
+      }
+      return;
+    }
+    const double mean = sum_sel / n_sel;
+    double d2[1] = {0.0};
+    for_cells(p, sv, p.breast, [&](int, int, int, double v) {
+      const double d = v - mean;
+      d2[0] += d * d;
+    });
+    block_sum<1>(d2, red, res);
+    m2_sel = res[0];
+  }
+
+  Box sel = p.breast;
+  double sigma_prev_sq = m2_sel / n_sel;
+  double prev_w = 0.0, prev_b = 0.0;
+  bool have_prev = false;
+  int iteration = 0;
+  int term = MWB_TERM_NONE;
+
+  while (term == MWB_TERM_NONE) {
+    Box rg[2 * MAXCH];
+    const int nk = split_box(sel, NK == 8 ? 3 : 2, rg);
+    if (nk == 0) {
+      term = MWB_TERM_REGION_FLOOR;
+      break;
+    }
+    for (int k = 0; k < nk; ++k) rg[nk + k] = expand_box(rg[k], p.frac, sel, p.dims);
+
+    // pass 1: count and sum of every child and of every child's expansion
+    // children are disjoint: a cell's child index follows from the split point
+    // of each axis (children k have lo = mid+1 on axis a iff bit a of k)
+    int mid[3];
+    for (int a = 0; a < 3; ++a) mid[a] = rg[0].hi[a];
+    double a1[4 * NK];
+#pragma unroll
+    for (int k = 0; k < 4 * NK; ++k) a1[k] = 0.0;
+    for_cells(p, sv, sel, [&](int ix, int iy, int iz, double v) {
+      const int kc = (ix > mid[0]) | ((iy > mid[1]) << 1) | (NK == 8 ? ((iz > mid[2]) << 2) : 0);
+#pragma unroll
+      for (int k = 0; k < NK; ++k)
+        if (k == kc) {
+          a1[2 * k] += 1.0;
+          a1[2 * k + 1] += v;
+        }
+#pragma unroll
+      for (int k = NK; k < 2 * NK; ++k)
+        if (box_contains(rg[k], ix, iy, iz)) {
+          a1[2 * k] += 1.0;
+          a1[2 * k + 1] += v;
+        }
+    });
+    block_sum<4 * NK>(a1, red, res);
+    double cnt[2 * NK], mean[2 * NK], sums[2 * NK];
+#pragma unroll
+    for (int k = 0; k < 2 * NK; ++k) {
+      cnt[k] = res[2 * k];
+      sums[k] = res[2 * k + 1];
+      mean[k] = cnt[k] > 0.0 ? sums[k] / cnt[k] : 0.0;
+    }
+    __syncthreads();
+    // pass 2: Σ (x - mean)^2 (two-pass variance, as numpy's var)
+    double a2[2 * NK];
+#pragma unroll
+    for (int k = 0; k < 2 * NK; ++k) a2[k] = 0.0;
+    for_cells(p, sv, sel, [&](int ix, int iy, int iz, double v) {
+      const int kc = (ix > mid[0]) | ((iy > mid[1]) << 1) | (NK == 8 ? ((iz > mid[2]) << 2) : 0);
+#pragma unroll
+      for (int k = 0; k < NK; ++k)
+        if (k == kc) {
+          const double d = v - mean[k];
+          a2[k] += d * d;
+        }
+#pragma unroll
+      for (int k = NK; k < 2 * NK; ++k)
+        if (box_contains(rg[k], ix, iy, iz)) {
+          const double d = v - mean[k];
+          a2[k] += d * d;
+        }
+    });
+    block_sum<2 * NK>(a2, red, res);
+    double m2[2 * NK];
+#pragma unroll
+    for (int k = 0; k < 2 * NK; ++k) m2[k] = res[k];
+    __syncthreads();
+
+    if (threadIdx.x < 32) {
+      const int t = select_score<NK>(p, tr, iteration, nk, rg, cnt, sums, mean, m2, n_sel, sum_sel, m2_sel,
+                                     sigma_prev_sq, have_prev, prev_w, prev_b, red, &next_sel);
+      if (threadIdx.x == 0) ctl[0] = t;
+    }
+    __syncthreads();
+    term = ctl[0];
+    if (term == MWB_TERM_N_MIN) break;
+    iteration += 1;
+    if (term != MWB_TERM_NONE) break;
+    prev_w = red[0];
+    prev_b = red[1];
+    have_prev = true;
+    n_sel = red[2];
+    sum_sel = red[3];
+    m2_sel = red[4];
+    sigma_prev_sq = m2_sel / n_sel;
+    sel = next_sel;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    tr->termination = term;
+    tr->n_records = min(iteration, MWB_MAX_ITERS);
+    put_box(tr->final_region, sel);
+    put_box(p.region_out, sel);
+  }
+}
+// ----------------------------------------------------------------------------
+// K2w: warp-per-scan select_roi for 2-D lattices whose breast box stages in
+// SEL_WARP_STAGE cells (the framework's 16..64-cell-wide low-res lattices).
+// A 256-thread CTA spends most of its time in barriers and 16-double block
+// reductions when every thread visits only ~5 cells per pass; a warp visits
+// ~36 per lane, reduces with shuffles only, and SEL_WPB scans share a CTA.
+// Cells are walked in lattice coordinates (no div/mod per cell) and each
+// cell's child / expansion membership is four range tests per axis (the
+// expansions are per-axis: expand_box grows each axis independently).
+// Same decisions as select_roi_kernel<4>; the summation order is the warp's,
+// so single-scan and batched selection both dispatch here for such lattices
+// and stay bit-identical to each other.
+// ----------------------------------------------------------------------------
+constexpr int SEL_WPB = 4;
+constexpr int SEL_WARP_STAGE = 4096;
+constexpr int SEL_SPLIT_MAX_SCANS = 148;  // below a wave of scans, a CTA of 8 warps per scan
+
+struct SelWarpCtl {
+  double nxt[5];
+  Box next;
+  int term;
+};
+
+__device__ __forceinline__ double warp_sum_d(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ int warp_sum_i(int x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// f(lx, ly, v) for every valid cell of box r; lattice cells are i = lane + 32k
+// of the r-lattice in row-major order, advanced incrementally.  Each lane
+// loads its next SEL_U cells before visiting them in order, so the shared-
+// memory latency overlaps while every accumulator sees the same sequence.
+constexpr int SEL_U = 4;
+template <class F>
+__device__ __forceinline__ void warp_cells(const float* sv, int sLy, int sl0x, int sl0y, int D, const Box& r,
+                                           F&& f) {
+  const int l0x = (r.lo[0] + D - 1) / D, l1x = r.hi[0] / D;
+  const int l0y = (r.lo[1] + D - 1) / D, l1y = r.hi[1] / D;
+  if (l1x < l0x || l1y < l0y) return;
+  const int Ly = l1y - l0y + 1, n = (l1x - l0x + 1) * Ly;
+  const int lane = threadIdx.x & 31;
+  const int q = 32 / Ly, rr = 32 - q * Ly;
+  int lx = lane / Ly, ly = lane - lx * Ly;
+  const float* base = sv + (l0x - sl0x) * sLy + (l0y - sl0y);
+  for (int i0 = lane; i0 < n; i0 += 32 * SEL_U) {
+    float v[SEL_U];
+    int cx[SEL_U], cy[SEL_U];
+#pragma unroll
+    for (int u = 0; u < SEL_U; ++u) {
+      cx[u] = lx;
+      cy[u] = ly;
+      const bool in = i0 + 32 * u < n;
+      const float x = base[in ? lx * sLy + ly : 0];  // unconditional load: no branch per cell
+      v[u] = in ? x : __int_as_float(0x7fc00000);
+      lx += q;
+      ly += rr;
+      if (ly >= Ly) {
+        ly -= Ly;
+        ++lx;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SEL_U; ++u)
+      if (v[u] == v[u]) f(l0x + cx[u], l0y + cy[u], v[u]);
+  }
+}
+
+// SPLIT = false: SEL_WPB scans per CTA, one warp each (batches).
+// SPLIT = true:  one scan per CTA of SEL_SPLIT_WARPS warps (single scans: a
+//   lone warp is latency bound).  Every warp walks the same cells in the same
+//   lane order, but in the iteration passes warp k accumulates only box k, so
+//   each box's sum sees exactly the additions of the one-warp kernel and the
+//   two modes agree bit for bit.
+constexpr int SEL_SPLIT_WARPS = 8;
+
+template <bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? SEL_SPLIT_WARPS * 32 : SEL_WPB * 32)
+    select_roi_warp_kernel(const SelectParams p, int n_scans) {
+  constexpr int NT = SPLIT ? SEL_SPLIT_WARPS * 32 : 32;  // threads sharing one scan
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = SPLIT ? (int)blockIdx.x : (int)blockIdx.x * SEL_WPB + warp;
+  if (s >= n_scans) return;
+  extern __shared__ float smem_sel[];
+  __shared__ SelWarpCtl wctl[SEL_WPB];
+  __shared__ double box_stat[2][8];  // SPLIT: per-box sums / m2 from the owning warp
+  __shared__ int box_cnt[8];
+  SelWarpCtl& wc = wctl[SPLIT ? 0 : warp];
+  const int D = p.D, sLx = p.sL[0], sLy = p.sL[1], sl0x = p.sl0[0], sl0y = p.sl0[1];
+  const int nst = sLx * sLy;
+  float* sv = smem_sel + (SPLIT ? 0 : warp * nst);
+  const float* dense = p.dense + (size_t)s * p.dense_stride;
+  int32_t* region_out = p.region_out + 6 * s;
+  mwb_trace_t* tr = p.trace + s;
+  const int tid = SPLIT ? (int)threadIdx.x : lane;
+  const bool leader = tid == 0;
+
+  {  // stage the breast box's lattice: both loads independent, 8 in flight per thread
+    int lx = tid / sLy, ly = tid - lx * sLy;
+    const int q = NT / sLy, rr = NT - q * sLy;
+#pragma unroll 8
+    for (int i = tid; i < nst; i += NT) {
+      const size_t slot = (size_t)(sl0x + lx) * D * p.ny + (size_t)(sl0y + ly) * D;
+      const float v = __ldg(dense + slot);
+      const uint8_t ok = __ldg(p.valid + slot);
+      sv[i] = ok ? v : __int_as_float(0x7fc00000);
+      lx += q;
+      ly += rr;
+      if (ly >= sLy) {
+        ly -= sLy;
+        ++lx;
+      }
+    }
+  }
+  if (SPLIT)
+    __syncthreads();
+  else
+    __syncwarp();
+
+  // breast-region stats: count, sum, min, max, then the two-pass m2
+  // (coarse2fine.py:186-199); SPLIT warps all compute them (identically)
+  double n_sel, sum_sel, m2_sel;
+  {
+    int c = 0;
+    double sm = 0.0;
+    float mn = INFINITY, mx = -INFINITY;  // exact in fp32: the values are fp32
+    warp_cells(sv, sLy, sl0x, sl0y, D, p.breast, [&](int, int, float v) {
+      ++c;
+      sm += (double)v;
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    });
+    n_sel = (double)warp_sum_i(c);
+    sum_sel = warp_sum_d(sm);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (n_sel == 0.0 || mx == mn) {
+      if (leader) {
+        tr->termination = n_sel == 0.0 ? MWB_TERM_EMPTY : MWB_TERM_DEGENERATE;
+        tr->n_records = 0;
+        put_box(tr->final_region, p.breast);
+        put_box(region_out, p.breast);
+      }
+      return;
+    }
+    const double mean = sum_sel / n_sel;
+    double d2 = 0.0;
+    warp_cells(sv, sLy, sl0x, sl0y, D, p.breast, [&](int, int, float v) {
+      const double d = (double)v - mean;
+      d2 = __fma_rn(d, d, d2);
+    });
+    m2_sel = warp_sum_d(d2);
+  }
+
+  Box sel = p.breast;
+  double sigma_prev_sq = m2_sel / n_sel;
+  double prev_w = 0.0, prev_b = 0.0;
+  bool have_prev = false;
+  int iteration = 0;
+  int term = MWB_TERM_NONE;
+
+  while (true) {
+    Box rg[8];
+    const int nk = split_box(sel, 2, rg);
+    if (nk == 0) {
+      term = MWB_TERM_REGION_FLOOR;
+      break;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rg[4 + k] = expand_box(rg[k], p.frac, sel, 2);
+    // lattice thresholds: a cell is in a high-half child iff l * D > mid;
+    // expansion ranges per axis: x from rg[4] (low) / rg[5] (high), y from rg[4] / rg[6]
+    const int mxl = rg[0].hi[0] / D, myl = rg[0].hi[1] / D;
+    const int ex0l = (rg[4].lo[0] + D - 1) / D, ex0h = rg[4].hi[0] / D;
+    const int ex1l = (rg[5].lo[0] + D - 1) / D, ex1h = rg[5].hi[0] / D;
+    const int ey0l = (rg[4].lo[1] + D - 1) / D, ey0h = rg[4].hi[1] / D;
+    const int ey1l = (rg[6].lo[1] + D - 1) / D, ey1h = rg[6].hi[1] / D;
+    double cnt[8], sums[8], mean[8], m2[8];
+
+    if constexpr (SPLIT) {
+      // warp k owns box k: the same membership tests as below, as one rectangle
+      const int k = warp;
+      const bool xhi = k < 4 ? (k & 1) : false, yhi = k < 4 ? (k >> 1) & 1 : false;
+      const int rx0 = k < 4 ? (xhi ? mxl + 1 : INT_MIN) : ((k - 4) & 1 ? ex1l : ex0l);
+      const int rx1 = k < 4 ? (xhi ? INT_MAX : mxl) : ((k - 4) & 1 ? ex1h : ex0h);
+      const int ry0 = k < 4 ? (yhi ? myl + 1 : INT_MIN) : ((k - 4) >> 1 ? ey1l : ey0l);
+      const int ry1 = k < 4 ? (yhi ? INT_MAX : myl) : ((k - 4) >> 1 ? ey1h : ey0h);
+      int ci = 0;
+      double a1 = 0.0;
+      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
+        const double v = fv;
+        if (rx0 <= lx && lx <= rx1 && ry0 <= ly && ly <= ry1) {
+          ++ci;
+          a1 += v;
+        }
+      });
+      ci = warp_sum_i(ci);
+      a1 = warp_sum_d(a1);
+      if (lane == 0) {
+        box_cnt[k] = ci;
+        box_stat[0][k] = a1;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        cnt[j] = (double)box_cnt[j];
+        sums[j] = box_stat[0][j];
+        mean[j] = cnt[j] > 0.0 ? sums[j] / cnt[j] : 0.0;
+      }
+      double a2 = 0.0;
+      const double mu = mean[k];
+      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
+        const double v = fv;
+        if (rx0 <= lx && lx <= rx1 && ry0 <= ly && ly <= ry1) {
+          const double d = v - mu;
+          a2 = __fma_rn(d, d, a2);  // explicit: both modes round alike
+        }
+      });
+      a2 = warp_sum_d(a2);
+      if (lane == 0) box_stat[1][k] = a2;
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) m2[j] = box_stat[1][j];
+    } else {
+      // pass 1: count and sum of every child and of every child's expansion
+      int ci[8];
+      double a1[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        ci[k] = 0;
+        a1[k] = 0.0;
+      }
+      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
+        const double v = fv;
+        const int kc = (lx > mxl) | ((ly > myl) << 1);
+        const bool x0 = ex0l <= lx && lx <= ex0h, x1 = ex1l <= lx && lx <= ex1h;
+        const bool y0 = ey0l <= ly && ly <= ey0h, y1 = ey1l <= ly && ly <= ey1h;
+        const bool in[8] = {kc == 0, kc == 1, kc == 2, kc == 3, x0 && y0, x1 && y0, x0 && y1, x1 && y1};
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (in[k]) {
+            ++ci[k];
+            a1[k] += v;
+          }
+      });
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        cnt[k] = (double)warp_sum_i(ci[k]);
+        sums[k] = warp_sum_d(a1[k]);
+        mean[k] = cnt[k] > 0.0 ? sums[k] / cnt[k] : 0.0;
+      }
+      // pass 2: sum of (x - mean)^2 (two-pass variance, as numpy's var)
+      double a2[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a2[k] = 0.0;
+      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
+        const double v = fv;
+        const int kc = (lx > mxl) | ((ly > myl) << 1);
+        const bool x0 = ex0l <= lx && lx <= ex0h, x1 = ex1l <= lx && lx <= ex1h;
+        const bool y0 = ey0l <= ly && ly <= ey0h, y1 = ey1l <= ly && ly <= ey1h;
+        const bool in[8] = {kc == 0, kc == 1, kc == 2, kc == 3, x0 && y0, x1 && y0, x0 && y1, x1 && y1};
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (in[k]) {
+            const double d = v - mean[k];
+            a2[k] = __fma_rn(d, d, a2[k]);
+          }
+      });
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m2[k] = warp_sum_d(a2[k]);
+    }
+
+    if (!SPLIT || warp == 0) {
+      const int t = select_score<4>(p, tr, iteration, nk, rg, cnt, sums, mean, m2, n_sel, sum_sel, m2_sel,
+                                    sigma_prev_sq, have_prev, prev_w, prev_b, wc.nxt, &wc.next);
+      if (lane == 0) wc.term = t;
+    }
+    if (SPLIT)
+      __syncthreads();
+    else
+      __syncwarp();
+    term = wc.term;
+    if (term == MWB_TERM_N_MIN) break;
+    iteration += 1;
+    if (term != MWB_TERM_NONE) break;
+    prev_w = wc.nxt[0];
+    prev_b = wc.nxt[1];
+    have_prev = true;
+    n_sel = wc.nxt[2];
+    sum_sel = wc.nxt[3];
+    m2_sel = wc.nxt[4];
+    sigma_prev_sq = m2_sel / n_sel;
+    sel = wc.next;
+    if (SPLIT)
+      __syncthreads();
+    else
+      __syncwarp();
+  }
+  if (leader) {
+    tr->termination = term;
+    tr->n_records = min(iteration, MWB_MAX_ITERS);
+    put_box(tr->final_region, sel);
+    put_box(region_out, sel);
+  }
+}

@@ -17,7 +17,7 @@ TILE, SPAN_MAX = 256, 511
 
 
 def layout(tiles, c):
-    """Byte offsets of the words, spans and wide flags (table_layout in mwb_kernels.cu)."""
+    """Byte offsets of the words, spans and wide flags (table_layout in csrc/mwb_common.cuh)."""
     span = (4 * tiles * c * TILE + 15) // 16 * 16
     wide = (span + 8 * tiles * c + 15) // 16 * 16
     return 0, span, wide
