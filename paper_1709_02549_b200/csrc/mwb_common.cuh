@@ -221,6 +221,7 @@ struct EnergyParams {
   const int* d_count;
   const int2* tile_info;      // packed multi-scan lists: {scan, valid points} per tile, or NULL
   const int* tile_src;        // with tile_info: source tile of the point list / table per launched tile, or NULL
+  int src_tiles;              // tiles of that source list (bounds checks of the debug build)
   const uint32_t* tab_words;  // [tiles][C][TILE]
   const int2* tab_span;       // [tiles][C] {lo, hi}
   const int* tab_wide;        // [tiles]

@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
   // source tile of the points / table (a shared, precomputed list) and the
   // packed output position; the same tile unless tile_src remaps it
   const size_t tile = p.tile_src ? (size_t)__ldg(p.tile_src + blockIdx.x) : (size_t)blockIdx.x;
+  MWB_CHECK(!p.tile_src || (long long)tile < p.src_tiles);
   const bool wide = __ldg(p.tab_wide + tile) != 0;
   const uint32_t* tw = p.tab_words + tile * (size_t)p.C * TILE;
   const int2* tsp = p.tab_span + tile * (size_t)p.C;
@@ -446,6 +447,7 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
       const float2 S = chunk_sumsq<CH>(sacc, valid);
       const float2 Q = KIND != KIND_DAS ? __fadd2_rn(qe, qo) : make_float2(0.f, 0.f);
       // rows: (scan, point) for shared point lists, the launched position for packed per-scan lists
+      MWB_CHECK(q < n_chunks && s < p.n_scans);
       float2* pp = p.part + ((p.tile_info ? (size_t)0 : (size_t)s * p.P) + tile0) * n_chunks + q;
       if (va) pp[(size_t)la * n_chunks] = make_float2(S.x, Q.x);
       if (vb) pp[(size_t)lb * n_chunks] = make_float2(S.y, Q.y);
@@ -514,6 +516,7 @@ __global__ void __launch_bounds__(256) energy_reduce_kernel(const EnergyParams p
     s = ti.x;
     v = i < p.P && (i % TILE) < ti.y && s >= 0;
     if (p.tile_src) src = __ldg(p.tile_src + i / TILE) * TILE + i % TILE;
+    MWB_CHECK(!p.tile_src || !v || src < p.src_tiles * TILE);
     row = (size_t)i;
   } else {
     const int n_pts = p.d_count ? min(*p.d_count, p.P) : p.P;

@@ -178,6 +178,7 @@ static int energy_params(const float* sig, int n_scans, int64_t scan_stride, int
   p.d_count = d_count;
   p.tile_info = reinterpret_cast<const int2*>(tile_info);
   p.tile_src = nullptr;
+  p.src_tiles = 0;
   p.tab_words = reinterpret_cast<const uint32_t*>(base + T.words);
   p.tab_span = reinterpret_cast<const int2*>(base + T.span);
   p.tab_wide = reinterpret_cast<const int*>(base + T.wide);
@@ -218,6 +219,7 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   if (rc || empty) return rc;
   if (tile_src) {
     p.tile_src = tile_src;
+    p.src_tiles = (n_src_pts + TILE - 1) / TILE;
     p.P = n_pts;
   }
   const long long tiles = (n_pts + TILE - 1) / TILE;
