@@ -385,3 +385,23 @@ def test_lattice_cache_hit_is_identical():
         assert np.array_equal(other[k].dense(fill=np.nan), fresh[k].dense(fill=np.nan), equal_nan=True)
         assert other[k].argmax_cell() == fresh[k].argmax_cell()
         assert len(other[k]) == len(fresh[k]) == int(mask.sum())
+
+
+def test_image_plan_replay_matches_first_pass_across_datasets():
+    """image() replays a captured energy launch once a lattice is cached: maps of
+    several datasets (same scanner; one with a different record length) equal
+    the first, uncached evaluation of each."""
+    from paper_1709_02549_b200 import beamform as bf
+    from paper_1709_02549_b200 import synth
+
+    grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 1e-3)
+    dss = [synth.dataset_2d(synth.ScanModel(n_samples=n), seed=s)[0] for n, s in ((1024, 1), (1024, 2), (512, 3))]
+    fresh = []
+    for ds in dss:
+        bf._LATTICE_CACHE.clear()
+        fresh.append(mw.images(ds, ("das", "dmas"), grid))
+    for _ in range(2):
+        for ds, want in zip(dss, fresh):
+            got = mw.images(ds, ("das", "dmas"), grid)
+            for k in ("das", "dmas"):
+                assert got[k].entries == want[k].entries
