@@ -10,7 +10,7 @@ Parity pin: every function is checked against golden vectors produced by the
 real reference package (``tests/golden/make_golden.py`` imports
 /root/reference/pkg/src in the build container; the fixtures travel, the
 reference does not) and against the reference's own known-answer tests
-(tests/test_oracle_pins.py).
+(tests/test_oracle_pins.py), both on the CPU.
 
 Citations are to /root/reference/pkg/src/mwbeam/<file>:<line>.
 """

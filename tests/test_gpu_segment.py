@@ -222,3 +222,25 @@ def test_full_record_split_paths_agree():
         assert f_t.entries == f_n.entries and _records_equal(r_t.records, r_n.records)
         assert np.array_equal(r_t.lowres, r_n.lowres) and r_t.argmax_cell == r_n.argmax_cell
         assert res.fine(s).entries == f_t.entries and _records_equal(res.records(s), r_t.records)
+
+
+def test_nearest_interpolation_tree_and_batch_paths_agree():
+    import torch
+
+    from paper_1709_02549_b200.segment import SegmentBatch
+
+    model = synth.ScanModel(n_samples=1024)
+    seeds = [51, 52]
+    sig, _ = synth.batch_2d(model, seeds, phantom_radius=(0.04, 0.05))
+    grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 5e-4)
+    win = (model.k0, model.window)
+    res = SegmentBatch(model.geometry(), model.pairs(), model.n_samples, grid, "das", window=win,
+                       interpolation="nearest").run(torch.from_numpy(sig).cuda())
+    for s in range(len(seeds)):
+        ds = mw.BackscatterDataset(model.geometry(), synth.embed_pairs(12, model.pairs(), sig[s].astype(np.float64)))
+        f_t, r_t = segment(ds, "das", grid, window=win, interpolation="nearest")
+        f_n, r_n = segment(ds, "das", grid, window=win, interpolation="nearest", tree=False)
+        f_l, _ = segment(ds, "das", grid, window=win)
+        assert f_t.entries == f_n.entries == res.fine(s).entries
+        assert _records_equal(r_t.records, r_n.records) and _records_equal(r_t.records, res.records(s))
+        assert f_t.entries != f_l.entries  # nearest really differs from linear
