@@ -26,6 +26,37 @@ import torch
 PLAN_LOCK = threading.RLock()
 
 
+class GraphPlan:
+    """Base of the captured-graph plans (image, run_framework, segment,
+    run_framework_volume).  A plan owns a signal slot (a copy of the first
+    scan's DeviceScan with its own ``sig`` buffer) that its graph reads;
+    ``replay(scan)`` refills the slot with ``scan``'s samples (device to
+    device), runs ``_enqueue`` eagerly once and captures it on the first call,
+    then replays the graph.  Subclasses implement ``_enqueue``."""
+
+    graph = None
+
+    def _init_slot(self, scan: "DeviceScan") -> "DeviceScan":
+        import dataclasses
+
+        self.scan = dataclasses.replace(scan, sig=torch.empty_like(scan.sig))
+        return self.scan
+
+    def _enqueue(self) -> None:  # pragma: no cover - abstract
+        raise NotImplementedError
+
+    def replay(self, scan: "DeviceScan") -> None:
+        self.scan.sig.copy_(scan.sig, non_blocking=True)
+        if self.graph is None:
+            self._enqueue()  # eager run: kernel attributes set, allocator warmed
+            torch.cuda.current_stream().synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                self._enqueue()
+            self.graph = graph
+        self.graph.replay()
+
+
 def device() -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError("the B200 imaging path needs a CUDA device (no CPU fallback)")

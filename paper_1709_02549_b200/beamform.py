@@ -22,7 +22,6 @@ ignored: results never depend on it.  Arithmetic is fp32 (delays fp64).
 
 from __future__ import annotations
 
-import dataclasses
 import threading
 from collections import OrderedDict
 from enum import Enum
@@ -484,7 +483,7 @@ def _eval_mask(grid: ImagingGrid, mask, skip) -> np.ndarray | None:
     return m
 
 
-class _ImagePlan:
+class _ImagePlan(dv.GraphPlan):
     """The energy launch of one cached lattice (``_LATTICE_CACHE`` entry) for a
     set of kinds, window and kernel mode, captured as a CUDA graph that reads a
     signal slot each call refills (as the framework plans).  A call is: slot
@@ -495,7 +494,7 @@ class _ImagePlan:
                  mode: int):
         self.ent, self.grid, self.codes = ent, grid, codes
         self.interp, self.k0, self.w, self.mode = interp, k0, w, mode
-        self.scan = dataclasses.replace(scan, sig=torch.empty_like(scan.sig))
+        self._init_slot(scan)
         nx, ny = grid.dims
         dev = dv.device()
         self.dense = {c: torch.zeros(nx * ny, dtype=torch.float32, device=dev) for c in codes}
@@ -503,7 +502,6 @@ class _ImagePlan:
         pts, oidx, table, cnt, valid, self.n = ent
         self.valid_host = valid.view(nx, ny).cpu().numpy().view(bool)
         self._pin = torch.cuda.is_available()
-        self.graph: torch.cuda.CUDAGraph | None = None
 
     def _enqueue(self) -> None:
         pts, oidx, table, cnt, _, _ = self.ent
@@ -514,15 +512,7 @@ class _ImagePlan:
                         st.key_ptr(0), st.key_ptr(1), st.flags_ptr, self.mode)
 
     def run(self, scan: dv.DeviceScan, stride: int) -> dict:
-        self.scan.sig.copy_(scan.sig, non_blocking=True)
-        if self.graph is None:
-            self._enqueue()  # eager run: kernel attributes set, allocator warmed
-            torch.cuda.current_stream().synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                self._enqueue()
-            self.graph = graph
-        self.graph.replay()
+        self.replay(scan)
         nx, ny = self.grid.dims
         st, *dh = dv.to_host(self.status.t, *(self.dense[c].view(nx, ny) for c in self.codes))
         _, _, flags = self.status.read(st)

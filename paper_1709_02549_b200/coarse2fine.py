@@ -19,7 +19,6 @@ Drop-in for /root/reference/pkg/src/mwbeam/coarse2fine.py:
 
 from __future__ import annotations
 
-import dataclasses
 import math
 from dataclasses import dataclass, field
 
@@ -323,7 +322,7 @@ def select_roi(coarse: EnergyMap, breast_region: Region, cfg: FrameworkConfig = 
     return final, trace
 
 
-class _FrameworkPlan:
+class _FrameworkPlan(dv.GraphPlan):
     """One framework configuration for one scanner geometry, captured as a CUDA graph.
 
     The coarse lattice pass, the select kernel and the ROI-driven fine pass
@@ -337,7 +336,7 @@ class _FrameworkPlan:
 
     def __init__(self, scan: dv.DeviceScan, grid: ImagingGrid, d: int, kcode: int, cfg: FrameworkConfig,
                  interp: int, k0: int, w: int, mode: int):
-        scan = dataclasses.replace(scan, sig=torch.empty_like(scan.sig))  # the slot
+        scan = self._init_slot(scan)
         self.scan, self.grid, self.d, self.kcode, self.cfg = scan, grid, d, kcode, cfg
         self.interp, self.k0, self.w, self.mode = interp, k0, w, mode
         nx, ny = grid.dims
@@ -355,7 +354,6 @@ class _FrameworkPlan:
         self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=pin)
         self.h_trace = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, pin_memory=pin)
         self._pin = pin  # map buffers are fresh pinned blocks per call (handed to the EnergyMap, no host copy)
-        self.graph: torch.cuda.CUDAGraph | None = None
         self.replays = 0
 
     def _enqueue(self) -> None:
@@ -375,15 +373,7 @@ class _FrameworkPlan:
 
     def launch(self, scan: dv.DeviceScan) -> None:
         """Enqueue one run on ``scan`` (graph replay after the first call) and the readback."""
-        self.scan.sig.copy_(scan.sig, non_blocking=True)
-        if self.graph is None:
-            self._enqueue()  # eager run: kernel attributes set, allocator warmed
-            torch.cuda.current_stream().synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                self._enqueue()
-            self.graph = graph
-        self.graph.replay()
+        self.replay(scan)
         self.replays += 1
         nx, ny = self.grid.dims
         self.h_dense = torch.empty(nx * ny, dtype=torch.float32, pin_memory=self._pin)

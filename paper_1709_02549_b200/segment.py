@@ -25,7 +25,6 @@ result once.
 from __future__ import annotations
 
 import ctypes as C
-import dataclasses
 import hashlib
 import math
 from collections import OrderedDict
@@ -147,7 +146,7 @@ def _tree_plan(scan: dv.DeviceScan, antennas, grid: ImagingGrid, region: Region,
     return ent
 
 
-class _SegmentPlan:
+class _SegmentPlan(dv.GraphPlan):
     """One segment() configuration on one device scan, captured as a CUDA graph;
     later calls replay it and read the results back into pinned buffers with
     one synchronisation.  Buffers persist with the plan, so a replay allocates
@@ -160,7 +159,7 @@ class _SegmentPlan:
 
     def __init__(self, scan: dv.DeviceScan, grid: ImagingGrid, region: Region, kcode: int, n_sub: int,
                  stop_cells: int, n_iter: int, interp: int, k0: int, w: int, mask_np, mask_t, tree):
-        scan = dataclasses.replace(scan, sig=torch.empty_like(scan.sig))  # the signal slot every call refills
+        scan = self._init_slot(scan)
         self.scan, self.grid, self.region, self.kcode = scan, grid, region, kcode
         self.n_sub, self.stop_cells, self.n_iter = n_sub, stop_cells, n_iter
         self.interp, self.k0, self.w = interp, k0, w
@@ -185,7 +184,6 @@ class _SegmentPlan:
         self.h_trace = torch.empty(nat.SEG_TRACE_BYTES, dtype=torch.uint8, pin_memory=pin)
         self._pin = pin  # map buffers are fresh pinned blocks per call (handed to the EnergyMap, no host copy)
         self.h_lowres = torch.empty(n_low, dtype=torch.float32, pin_memory=pin)
-        self.graph: torch.cuda.CUDAGraph | None = None
 
     def _enqueue(self) -> None:
         sc, grid = self.scan, self.grid
@@ -218,15 +216,7 @@ class _SegmentPlan:
         ev[2].record()
 
     def launch(self, scan: dv.DeviceScan) -> None:
-        self.scan.sig.copy_(scan.sig, non_blocking=True)
-        if self.graph is None:
-            self._enqueue()  # eager run: kernel attributes set, allocator warmed
-            torch.cuda.current_stream().synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                self._enqueue()
-            self.graph = graph
-        self.graph.replay()
+        self.replay(scan)
         nx, ny = self.grid.dims
         self.h_dense = torch.empty(nx * ny, dtype=torch.float32, pin_memory=self._pin)
         if self.tree is None:

@@ -14,7 +14,6 @@ scores them with the reference's Eq. (5) / W-B / n_min control flow
 
 from __future__ import annotations
 
-import dataclasses
 import hashlib
 import math
 import weakref
@@ -355,7 +354,7 @@ def _mask_key(mask: np.ndarray) -> tuple:
     return val
 
 
-class _VolumeFrameworkPlan:
+class _VolumeFrameworkPlan(dv.GraphPlan):
     """The configs[4] octant framework for one scanner geometry, grid, mask and
     configuration, captured as a CUDA graph (coarse voxel lattice, octant
     select, ROI-driven fine pass).  As coarse2fine._FrameworkPlan: buffers live
@@ -366,7 +365,7 @@ class _VolumeFrameworkPlan:
 
     def __init__(self, scan, grid: VolumeGrid, d: int, kcode: int, cfg: FrameworkConfig, interp: int, k0: int,
                  w: int, mask: np.ndarray, full_eq: int):
-        self.scan = dataclasses.replace(scan, sig=torch.empty_like(scan.sig))
+        self._init_slot(scan)
         self.grid, self.d, self.kcode, self.cfg = grid, d, kcode, cfg
         self.interp, self.k0, self.w = interp, k0, w
         self.full_eq = full_eq
@@ -382,7 +381,6 @@ class _VolumeFrameworkPlan:
         self._pin = torch.cuda.is_available()
         self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=self._pin)
         self.h_trace = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, pin_memory=self._pin)
-        self.graph: torch.cuda.CUDAGraph | None = None
 
     def _enqueue(self) -> None:
         g, d, sc = self.grid, self.d, self.scan
@@ -401,15 +399,7 @@ class _VolumeFrameworkPlan:
         ev[3].record()
 
     def launch(self, scan) -> None:
-        self.scan.sig.copy_(scan.sig, non_blocking=True)
-        if self.graph is None:
-            self._enqueue()  # eager run: kernel attributes set, allocator warmed
-            torch.cuda.current_stream().synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                self._enqueue()
-            self.graph = graph
-        self.graph.replay()
+        self.replay(scan)
         n = math.prod(self.grid.dims)
         self.h_dense = torch.empty(n, dtype=torch.float32, pin_memory=self._pin)  # owned by the returned map
         self.h_valid = torch.empty(n, dtype=torch.uint8, pin_memory=self._pin)
