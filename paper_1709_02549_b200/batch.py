@@ -219,7 +219,7 @@ class BatchImager:
         out[:, :, : self.n_samples] = t.to(dev)
         return out
 
-    def __call__(self, signals, kinds=("das", "dmas"), chunk: int = 256, out=None) -> BatchResult:
+    def __call__(self, signals, kinds=("das", "dmas"), chunk: int = 128, out=None) -> BatchResult:
         """End-to-end: host (S, C, N) fp32 scans (pinned torch tensor or numpy) ->
         host (S, nx, ny) fp32 maps per kind + per-scan argmax cells.
 
