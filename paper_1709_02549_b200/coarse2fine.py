@@ -35,6 +35,8 @@ from .beamform import (
     _kind_code,
     _Status,
     _window,
+    build_table,
+    launch_energies,
     lattice_pass,
 )
 from .geometry import ImagingGrid, Region
@@ -325,8 +327,9 @@ def select_roi(coarse: EnergyMap, breast_region: Region, cfg: FrameworkConfig = 
 class _FrameworkPlan(dv.GraphPlan):
     """One framework configuration for one scanner geometry, captured as a CUDA graph.
 
-    The coarse lattice pass, the select kernel and the ROI-driven fine pass
-    (13 kernels incl. memsets) are enqueued once eagerly, then captured; later
+    The coarse energy pass (its lattice and delay table are built once per
+    plan), the select kernel and the ROI-driven fine pass are enqueued once
+    eagerly, then captured; later
     calls replay the graph and read the results back into pinned buffers with
     a single synchronisation.  Buffers persist with the plan, so a replay
     allocates nothing.  The graph reads the plan's own signal slot: each call
@@ -355,15 +358,32 @@ class _FrameworkPlan(dv.GraphPlan):
         self.h_trace = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, pin_memory=pin)
         self._pin = pin  # map buffers are fresh pinned blocks per call (handed to the EnergyMap, no host copy)
         self.replays = 0
+        # The coarse lattice and its delay table depend on the geometry, grid
+        # and mask only: enumerated and tabled once here, outside the graph,
+        # which then holds just the coarse energy launch.
+        p_max = ((nx + d - 1) // d) * ((ny + d - 1) // d)
+        self.c_pts = torch.empty((p_max, 3), dtype=torch.float64, device=dev)
+        self.c_oidx = torch.empty(p_max, dtype=torch.int32, device=dev)
+        self.c_valid = torch.zeros(nx * ny, dtype=torch.uint8, device=dev)
+        self.c_count = torch.zeros(1, dtype=torch.int32, device=dev)
+        ws = torch.empty(int(nat.load().mwb_lattice_workspace_bytes(nx, ny, d)), dtype=torch.uint8, device=dev)
+        nat.call("mwb_enumerate_lattice", grid.origin[0], grid.origin[1], grid.resolution, nx, ny, 0, 0, nx - 1,
+                 ny - 1, None, d, self.mask_t.data_ptr(), 0, self.c_pts.data_ptr(), self.c_oidx.data_ptr(),
+                 self.c_count.data_ptr(), self.c_valid.data_ptr(), ws.data_ptr(), dv.stream_handle())
+        self.c_table = build_table(scan, self.c_pts, p_max, interp, self.c_count.data_ptr())
+        self.n_coarse = int(self.c_count.item())
 
     def _enqueue(self) -> None:
         g, d = self.grid, self.d
         ev = self.events
-        self.valid.zero_()
+        self.valid.copy_(self.c_valid)
         self.status.t.zero_()
+        st = self.status
         ev[0].record()
-        lattice_pass(self.scan, g, d, self.mask_t, 0, (self.kcode,), self.interp, self.k0, self.w,
-                     {self.kcode: self.dense}, self.valid, self.status, 0, mode=self.mode)
+        launch_energies(self.scan, self.c_pts, self.c_pts.shape[0], self.c_table, self.interp, self.k0, self.w,
+                        self.dense if self.kcode == nat.MWB_DAS else None,
+                        self.dense if self.kcode == nat.MWB_DMAS else None, 0, self.c_oidx, self.c_count.data_ptr(),
+                        st.key_ptr(0), st.key_ptr(1), st.flags_ptr, self.mode)
         ev[1].record()
         _launch_select(self.dense, self.valid, g, d, g.full_region(), self.cfg, self.region_t, self.trace_t)
         ev[2].record()
@@ -392,7 +412,7 @@ class _FrameworkPlan(dv.GraphPlan):
         if flags & 1:
             raise ValueError("energy map contains non-finite values")
         final, trace, _ = decode_trace(self.h_trace.numpy())  # decoded in place: the buffer is reused next call
-        n_coarse, n_fine = int(counts[0]), int(counts[1])
+        n_coarse, n_fine = self.n_coarse, int(counts[1])
         EVAL_COUNTER.add(n_coarse)
         EVAL_COUNTER.add(n_fine)
         vals = self.h_dense.numpy().reshape(nx, ny)
