@@ -200,7 +200,7 @@ def _volume_pass(scan, grid: VolumeGrid, box: Box, stride: int, mask_t, skip_str
              ctypes.addressof(host_box), nat.ptr(d_region), stride, nat.ptr(mask_t), skip_stride, pts.data_ptr(),
              oidx.data_ptr(), count_ptr, valid.data_ptr(), ws.data_ptr(), dv.stream_handle())
     if w == 0:
-        return
+        return pts, oidx, None
     table = build_table(scan, pts, p_max, interp, count_ptr)
     launch_energies(scan, pts, p_max, table, interp, k0, w,
                     dense.get(nat.MWB_DAS) if nat.MWB_DAS in codes else None,
@@ -381,16 +381,29 @@ class _VolumeFrameworkPlan(dv.GraphPlan):
         self._pin = torch.cuda.is_available()
         self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=self._pin)
         self.h_trace = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, pin_memory=self._pin)
+        # the coarse voxel lattice and its delay table depend on the geometry,
+        # grid and mask only: built once here, outside the graph
+        self.c_valid = torch.zeros(n, dtype=torch.uint8, device=dev)
+        c_status = _Status()
+        self.c_pts, self.c_oidx, _ = _volume_pass(self.scan, grid, grid.full_box(), d, self.mask_t, 0, (), interp,
+                                                  k0, 0, {}, self.c_valid, c_status, 0)
+        self.c_count = torch.empty(1, dtype=torch.int32, device=dev)
+        self.c_count.copy_(c_status.t.view(torch.int32)[4:5])  # status count slot 0
+        self.c_table = build_table(self.scan, self.c_pts, self.c_pts.shape[0], interp, self.c_count.data_ptr())
+        self.n_coarse = int(self.c_count.item())
 
     def _enqueue(self) -> None:
         g, d, sc = self.grid, self.d, self.scan
         ev = self.events
         full = g.full_box()
-        self.valid.zero_()
+        self.valid.copy_(self.c_valid)
         self.status.t.zero_()
+        st = self.status
         ev[0].record()
-        _volume_pass(sc, g, full, d, self.mask_t, 0, (self.kcode,), self.interp, self.k0, self.w,
-                     {self.kcode: self.dense}, self.valid, self.status, 0)
+        launch_energies(sc, self.c_pts, self.c_pts.shape[0], self.c_table, self.interp, self.k0, self.w,
+                        self.dense if self.kcode == nat.MWB_DAS else None,
+                        self.dense if self.kcode == nat.MWB_DMAS else None, 0, self.c_oidx, self.c_count.data_ptr(),
+                        st.key_ptr(0), st.key_ptr(1), st.flags_ptr, 0)
         ev[1].record()
         _launch_select3(self.dense, self.valid, g, d, full, self.cfg, self.region_t, self.trace_t)
         ev[2].record()
@@ -417,7 +430,7 @@ class _VolumeFrameworkPlan(dv.GraphPlan):
         values = self.h_dense.numpy().reshape(grid.dims)
         vmask = self.h_valid.numpy().reshape(grid.dims).view(bool)
         composite = VolumeMap(grid, values, vmask, stride=d, roi=final, checked=True)
-        n_c, n_f = int(counts[0]), int(counts[1])
+        n_c, n_f = self.n_coarse, int(counts[1])
         EVAL_COUNTER.add(n_c + n_f)
         key = int(keys[0 if self.kcode == nat.MWB_DAS else 1])
         _, ny, nz = grid.dims
