@@ -137,3 +137,16 @@ def test_octant_framework_replay_and_dataset_switch():
         assert np.array_equal(c0.valid, c1.valid)
         assert np.array_equal(c0.values[c0.valid], c1.values[c1.valid])
         assert r0.final_region == r1.final_region and r0.argmax_cell == r1.argmax_cell
+
+
+def test_octant_framework_argument_errors():
+    vm = synth.VolumeModel(n_samples=256)
+    sig, _ = synth.scan_3d(vm, seed=3)
+    ds = mw.BackscatterDataset(vm.geometry(), synth.embed_pairs(vm.n_ant, vm.pairs(), sig))
+    grid = VolumeGrid((-0.012, -0.012, 0.0), (0.024, 0.024, 0.012), 0.002)
+    with pytest.raises(ValueError):  # mask of the wrong shape
+        run_framework_volume(ds, "das", grid, mw.Manual(3), mask=np.ones((3, 3, 3), dtype=bool))
+    with pytest.raises(ValueError):  # no coarse point inside the mask
+        run_framework_volume(ds, "das", grid, mw.Manual(3), mask=np.zeros(grid.dims, dtype=bool))
+    with pytest.raises(ValueError):
+        run_framework_volume(ds, "das", grid, mw.Manual(3), interpolation="cubic")
