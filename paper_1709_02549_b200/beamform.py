@@ -385,7 +385,7 @@ def _lattice_key(ds, scan: dv.DeviceScan, grid: ImagingGrid, bounds, stride: int
 
     g = ds.geometry
     ants = np.ascontiguousarray(np.asarray(g.antennas, dtype=np.float64)).tobytes()
-    mh = None if emask is None else hashlib.blake2b(np.packbits(emask).tobytes(), digest_size=16).digest()
+    mh = None if emask is None else hashlib.sha1(np.packbits(emask)).digest()
     return (torch.cuda.current_device(), ants, scan.chan_host.tobytes(), float(scan.inv_scale), tuple(grid.origin),
             float(grid.resolution), tuple(grid.dims), tuple(bounds), int(stride), mh, int(interp))
 

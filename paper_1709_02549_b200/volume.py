@@ -245,8 +245,7 @@ def image_volume(ds, kinds, grid: VolumeGrid, box: Box | None = None, stride: in
     kmode = {"smem": 0, "gather": 1}[mode]
     dense = {c: torch.zeros(n, dtype=torch.float32, device=dev) for c in codes}
     status = _Status()
-    mh = None if mask is None else hashlib.blake2b(np.packbits(np.asarray(mask, dtype=bool)).tobytes(),
-                                                   digest_size=16).digest()
+    mh = None if mask is None else hashlib.sha1(np.packbits(np.asarray(mask, dtype=bool))).digest()
     key = (scan.geometry_key(), tuple(grid.origin), float(grid.resolution), tuple(grid.dims), box.bounds(), stride,
            mh, interp) if w else None
     ent = _VOLUME_CACHE.get(key) if key is not None else None
@@ -345,7 +344,7 @@ def _mask_key(mask: np.ndarray) -> tuple:
     hit = _MASK_KEYS.get(id(mask))
     if hit is not None and hit[0]() is mask:
         return hit[1]
-    val = (hashlib.blake2b(np.packbits(mask).tobytes(), digest_size=16).digest(), int(mask.sum()))
+    val = (hashlib.sha1(np.packbits(mask)).digest(), int(mask.sum()))
     try:
         ref = weakref.ref(mask, lambda _r, k=id(mask): _MASK_KEYS.pop(k, None))
         _MASK_KEYS[id(mask)] = (ref, val)
