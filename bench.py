@@ -541,7 +541,9 @@ def run_ours(args):
             bi(host, kinds=("das", "dmas"), chunk=args.chunk, out=out_h)
             times.append(time.perf_counter() - t0)
         e2e_s = shard.max_over_ranks(statistics.median(times), dev)
-        chunks = (S + args.chunk - 1) // args.chunk
+        from paper_1709_02549_b200.batch import _chunk_ranges
+
+        chunks = len(_chunk_ranges(S, min(args.chunk, S))) * (3 if bi.uses_tensor_cores else 1)
         e2e = {"value": pair_evals / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(host.numel() * 4),
                "d2h_bytes_per_step": int(2 * S * nxny * 4 + 2 * S * 8), "seconds_per_step": e2e_s,
                "api": "paper_1709_02549_b200.batch.BatchImager.__call__ (pinned host in, host maps out)",

@@ -27,6 +27,27 @@ from .beamform import _Status, _window, build_table
 from .geometry import ArrayGeometry, ImagingGrid
 
 
+def _chunk_ranges(s_total: int, chunk: int) -> list[tuple[int, int]]:
+    """Scan ranges of the end-to-end pipeline: ``chunk`` scans each, with a
+    quarter- and a half-size chunk at both ends when the batch is long enough,
+    so the first kernels start after a short host->device copy and the last
+    device->host copy is short (head and tail of the pipeline)."""
+    if s_total < 6 * chunk or chunk < 4:
+        return [(a, min(s_total, a + chunk)) for a in range(0, s_total, chunk)]
+    ramp = [chunk // 4, chunk // 2]
+    sizes = ramp[:]
+    body = s_total - 2 * sum(ramp)
+    sizes += [chunk] * (body // chunk)
+    if body % chunk:
+        sizes.append(body % chunk)
+    sizes += ramp[::-1]
+    out, a = [], 0
+    for n in sizes:
+        out.append((a, a + n))
+        a += n
+    return out
+
+
 @dataclass
 class BatchResult:
     maps: dict  # kind -> (S, nx, ny) float32 (host or device)
@@ -242,8 +263,9 @@ class BatchImager:
                    for k in kinds}
         dev = dv.device()
         chunk = max(1, min(chunk, s_total))
-        n_chunks = (s_total + chunk - 1) // chunk
-        nbuf = 2
+        ranges = _chunk_ranges(s_total, chunk)
+        n_chunks = len(ranges)
+        nbuf = 4  # chunks in flight: H2D of i+1.., kernels of i, D2H of i-1.. (each buffer set ~chunk x 0.5 MB)
         dev_in = [torch.empty((chunk, self.n_chan, self.ld), dtype=torch.float32, device=dev) for _ in range(nbuf)]
         dev_out = [{k: torch.empty((chunk, nx * ny), dtype=torch.float32, device=dev) for k in kinds}
                    for _ in range(nbuf)]
@@ -255,8 +277,7 @@ class BatchImager:
         ev_in = [torch.cuda.Event() for _ in range(n_chunks)]
         ev_cmp = [torch.cuda.Event() for _ in range(n_chunks)]
         ev_out = [torch.cuda.Event() for _ in range(n_chunks)]
-        for i in range(n_chunks):
-            a, b = i * chunk, min(s_total, (i + 1) * chunk)
+        for i, (a, b) in enumerate(ranges):
             n = b - a
             buf = i % nbuf
             with torch.cuda.stream(s_in):
