@@ -382,8 +382,10 @@ class SegmentBatchResult:
         valid[x0 : x1 + 1, y0 : y1 + 1] = True
         if self._mask is not None:
             valid &= self._mask
-        return EnergyMap._from_dense(self.grid, self.dense[s].cpu().numpy(), valid, 1, roi=self.final_region(s),
-                                     checked=True)
+        # only the final segment's block comes back from the device
+        values = np.zeros((nx, ny), dtype=np.float32)
+        values[x0 : x1 + 1, y0 : y1 + 1] = self.dense[s, x0 : x1 + 1, y0 : y1 + 1].cpu().numpy()
+        return EnergyMap._from_dense(self.grid, values, valid, 1, roi=self.final_region(s), checked=True)
 
 
 class SegmentBatch:
