@@ -51,7 +51,11 @@ class GraphPlan:
             self._enqueue()  # eager run: kernel attributes set, allocator warmed
             torch.cuda.current_stream().synchronize()
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
+            # thread-local capture: scan uploads, mask uploads and plan setup
+            # that other host threads run outside PLAN_LOCK (pinned allocs,
+            # H2D copies, stream syncs) neither invalidate this capture nor
+            # are rejected while it is open
+            with torch.cuda.graph(graph, capture_error_mode="thread_local"):
                 self._enqueue()
             self.graph = graph
         self.graph.replay()

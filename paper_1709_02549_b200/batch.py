@@ -24,7 +24,7 @@ import torch
 from . import _device as dv
 from . import _native as nat
 from .beamform import _Status, _window, build_table
-from .geometry import ArrayGeometry, ImagingGrid
+from .geometry import ArrayGeometry, ImagingGrid, as_grid
 
 
 def _chunk_ranges(s_total: int, chunk: int) -> list[tuple[int, int]]:
@@ -58,6 +58,7 @@ class BatchImager:
     def __init__(self, geometry: ArrayGeometry, pairs, n_samples: int, grid: ImagingGrid, window=None,
                  mask: np.ndarray | None = None, interpolation: str = "linear", mode: str = "smem"):
         dev = dv.device()
+        grid = as_grid(grid)
         self.grid = grid
         self.n_samples = int(n_samples)
         self.ld = dv.round4(n_samples)

@@ -31,7 +31,7 @@ import torch
 
 from . import _device as dv
 from . import _native as nat
-from .geometry import ImagingGrid, Region, delay_multistatic
+from .geometry import ImagingGrid, Region, as_grid, as_region, delay_multistatic
 
 _MODES = {"smem": 0, "gather": 1}
 
@@ -419,6 +419,13 @@ def energies(ds, points, kind, interpolation: str = "linear", *, window=None, mo
     return out.cpu().numpy().astype(np.float64)
 
 
+def _multistatic_energies(ds, points, kind, interpolation: str = "linear") -> np.ndarray:
+    """Drop-in for the reference kernel's own entry (beamform.py:169-212):
+    energies of a (P, 2) batch of focal points over the full record, fp64
+    array out.  One K0 + K1 launch for the whole batch."""
+    return energies(ds, points, kind, interpolation)
+
+
 def das_energy(ds, r, interpolation: str = "linear", *, window=None) -> float:
     """Multistatic DAS synthesized energy at focal point ``r`` (beamform.py:242-246)."""
     _check_interpolation(interpolation)
@@ -540,6 +547,7 @@ def images(ds, kinds, grid: ImagingGrid, region: Region | None = None, stride: i
     for bit; the evaluated-point counter is advanced once per map.
     """
     _check_interpolation(interpolation)
+    grid, region = as_grid(grid), as_region(region)
     codes = tuple(dict.fromkeys(_kind_code(k) for k in kinds))
     if not codes:
         raise ValueError("no beamformer kind requested")

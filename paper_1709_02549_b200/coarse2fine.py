@@ -39,7 +39,7 @@ from .beamform import (
     launch_energies,
     lattice_pass,
 )
-from .geometry import ImagingGrid, Region
+from .geometry import ImagingGrid, Region, as_grid, as_region
 
 
 @dataclass(frozen=True)
@@ -176,6 +176,7 @@ class MetricTrace:
 
 def breast_mask(grid: ImagingGrid) -> np.ndarray:
     """Cells whose centres lie in the circle inscribed in the grid (coarse2fine.py:259-268)."""
+    grid = as_grid(grid)
     nx, ny = grid.dims
     cx, cy = grid.center()
     radius = min(nx, ny) * grid.resolution / 2.0
@@ -295,7 +296,8 @@ def _launch_select(dense: torch.Tensor, valid: torch.Tensor, grid: ImagingGrid, 
 
 def select_roi(coarse: EnergyMap, breast_region: Region, cfg: FrameworkConfig = FrameworkConfig()) -> tuple[Region, MetricTrace]:
     """Iterative quadrant selection (coarse2fine.py:169-256), run by the device kernel."""
-    grid = coarse.grid
+    grid = as_grid(coarse.grid)
+    breast_region = as_region(breast_region)
     nx, ny = grid.dims
     if not grid.full_region().contains_region(breast_region):
         raise ValueError("breast region lies outside the grid")
@@ -486,6 +488,7 @@ def run_framework(
 ) -> tuple[EnergyMap, FrameworkReport]:
     """Coarse pass, ROI selection, fine pass, composite (coarse2fine.py:301-350)."""
     _check_interpolation(interpolation)
+    grid = as_grid(grid)
     d = decimation_factor(mode, grid.resolution)
     mask_np, _ = _breast_mask_device(grid)
     if not mask_np[::d, ::d].any():
@@ -527,6 +530,7 @@ def consistency_check(
     """Confirmed when the final regions of two decimation factors overlap
     (coarse2fine.py:371-402).  Both runs are enqueued back to back on the
     stream before the single synchronisation."""
+    grid = as_grid(grid)
     if d1 == d2:
         raise ValueError("consistency check needs two different decimation factors")
     limit = auto_decimation_factor(cfg.min_tumor_diameter, grid.resolution)

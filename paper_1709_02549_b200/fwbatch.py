@@ -32,7 +32,7 @@ from . import _device as dv
 from . import _native as nat
 from .beamform import EVAL_COUNTER, EnergyMap, _kind, _kind_code, _Status, _window, build_table
 from .coarse2fine import FrameworkConfig, MetricTrace, breast_mask, decimation_factor, decode_trace
-from .geometry import ArrayGeometry, ImagingGrid, Region
+from .geometry import ArrayGeometry, ImagingGrid, Region, as_grid
 
 
 @dataclass
@@ -88,6 +88,7 @@ class FrameworkBatch:
     def __init__(self, geometry: ArrayGeometry, pairs, n_samples: int, grid: ImagingGrid, mode, kind,
                  cfg: FrameworkConfig = FrameworkConfig(), window=None, interpolation: str = "linear"):
         dev = dv.device()
+        grid = as_grid(grid)
         self.grid, self.cfg = grid, cfg
         self.kind = _kind(kind)
         self.kcode = _kind_code(kind)

@@ -7,7 +7,9 @@ the package namespace, __init__.py:3-43).  Patching only
 ``_multistatic_energies`` would be functionally correct but launch-bound
 (one launch per 64 points, beamform.py:325), so every binding of ``image``,
 ``das_energy``, ``dmas_energy``, ``point_energy``, ``select_roi``,
-``run_framework`` and ``consistency_check`` is replaced.
+``run_framework`` and ``consistency_check`` is replaced, together with the
+kernel entry ``_multistatic_energies`` and the ``EVAL_COUNTER`` object the
+GPU ``image()`` adds to.
 
 The GPU functions duck-type the reference's argument objects (grids, regions,
 datasets, kinds, modes, configs) and return this package's result types,
@@ -23,6 +25,8 @@ from . import coarse2fine as c2f
 
 REPLACEMENTS = {
     "image": bf.image,
+    "_multistatic_energies": bf._multistatic_energies,
+    "EVAL_COUNTER": bf.EVAL_COUNTER,  # the counter the GPU image() adds to (beamform.py:74-75, 339)
     "das_energy": bf.das_energy,
     "dmas_energy": bf.dmas_energy,
     "point_energy": bf.point_energy,

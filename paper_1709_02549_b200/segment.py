@@ -37,7 +37,7 @@ from . import _device as dv
 from . import _native as nat
 from .beamform import EVAL_COUNTER, EnergyMap, _check_interpolation, _kind, _kind_code, _Status, _window, lattice_pass
 from .coarse2fine import _breast_mask_device
-from .geometry import ArrayGeometry, ImagingGrid, Region
+from .geometry import ArrayGeometry, ImagingGrid, Region, as_grid, as_region
 
 
 @dataclass
@@ -303,6 +303,7 @@ def segment(ds, kind, grid: ImagingGrid, n_sub: int = 16, stop_size: float = 0.0
         raise ValueError("stop_size must be > 0")
     if not 1 <= n_sub <= 64:
         raise ValueError("n_sub must be in [1, 64]")
+    grid, region = as_grid(grid), as_region(region)
     region = grid.full_region() if region is None else region
     if not grid.full_region().contains_region(region):
         raise ValueError("region lies outside the grid")
@@ -419,6 +420,7 @@ class SegmentBatch:
         if not 1 <= n_sub <= 64:
             raise ValueError("n_sub must be in [1, 64]")
         dev = dv.device()
+        grid, region = as_grid(grid), as_region(region)
         self.grid = grid
         self.kind = _kind(kind)
         self.kcode = _kind_code(kind)

@@ -85,6 +85,23 @@ class TestDmasEnergy:  # test_beamform.py:160-187
             scale = sum(float((a * a).sum()) for a in aligned)
             assert abs(mw.dmas_energy(ds, r) - slow) <= FP32_REL * scale
 
+    def test_acceptance_criterion_4_at_fp32(self):
+        """test_acceptance.py:143-161 (criterion 4) on its own 100 random
+        datasets (seed 2024), with the fp32 bound relative to the channel
+        self-energy sum instead of the fp64 rel 1e-9 on the (zero-crossing)
+        DMAS value itself."""
+        rng = np.random.default_rng(2024)
+        worst = 0.0
+        for _ in range(100):
+            geom = mw.ring_array(4, 1.0, propagation_speed=1.0, sample_interval=1.0)
+            ds = dataset(geom, rng.normal(size=(4, 4, 64)))
+            r = rng.uniform(-0.8, 0.8, 2)
+            aligned = [mw.aligned_channel(ds, i, j, r) for i in range(4) for j in range(4)]
+            slow = sum(float((aligned[k] * aligned[l]).sum()) for k in range(16) for l in range(k + 1, 16))
+            scale = sum(float((a * a).sum()) for a in aligned)
+            worst = max(worst, abs(mw.dmas_energy(ds, r) - slow) / scale)
+        assert worst <= FP32_REL, worst
+
 
 class TestKernelProperties:  # test_beamform.py:190-239
     def make_random(self, seed, m=3, n=48):

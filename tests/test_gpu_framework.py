@@ -15,14 +15,11 @@ import numpy as np
 import pytest
 
 import paper_1709_02549_b200 as mw
-from _mwb_helpers import grid_for_geometry, load_json, peak_err, preset, sha, sim_small
+from _mwb_helpers import divergence_excused, grid_for_geometry, load_json, peak_err, preset, sha, sim_small
 from oracle import mwbeam_oracle as orc
 from paper_1709_02549_b200 import synth
 
 pytestmark = pytest.mark.gpu
-
-NEAR = 1e-4
-
 
 def lattice_map(grid, stride, values):  # test_coarse2fine.py:98-105
     nx, ny = grid.dims
@@ -30,22 +27,25 @@ def lattice_map(grid, stride, values):  # test_coarse2fine.py:98-105
     return mw.EnergyMap(grid, entries, stride)
 
 
-def near_tie(records) -> bool:
-    """True when some oracle decision is within NEAR of flipping."""
-    for r in records:
-        sc = sorted([s for s in r["scores"] if s != -math.inf], reverse=True)
-        if len(sc) >= 2 and abs(sc[0] - sc[1]) <= NEAR * max(abs(sc[0]), 1e-300):
-            return True
-    return False
-
-
 def compare_trace(trace, want_trace, final, want_final):
-    recs = want_trace["records"]
-    got_sel = [r.selected for r in trace.records]
-    want_sel = [r["selected"] for r in recs]
-    same = (got_sel == want_sel and trace.termination == want_trace["termination"]
-            and final.to_dict() == want_final)
-    return same, near_tie(recs)
+    """(same, excused): excused only for a near-tie at the first diverging
+    iteration (_mwb_helpers.divergence_excused)."""
+    same, tie, why = divergence_excused(trace.records, trace.termination, want_trace["records"],
+                                        want_trace["termination"])
+    if same and final.to_dict() != want_final:
+        same, tie = False, False
+    if tie:
+        print("near-tie excused:", why)
+    return same, tie
+
+
+def assert_common_cells(got: dict, want: dict) -> None:
+    """Energies of the cells both composites evaluated agree (peak-normalised
+    by the reference map), whether or not the selections matched."""
+    keys = [k for k in want if k in got]
+    assert len(keys) >= 0.5 * len(want) or len(keys) >= 100
+    ref_peak = max(abs(v) for v in want.values())
+    assert max(abs(got[k] - want[k]) for k in keys) / ref_peak <= 1e-4
 
 
 class TestSelectRoi:  # test_coarse2fine.py:108-169
@@ -213,15 +213,18 @@ class TestGoldenFrameworks:
             comp, rep = mw.run_framework(ds, case["kind"], grid, md)
             want = case["report"]
             same, tie = compare_trace(rep.trace, want["trace"], rep.final_region, want["final_region"])
+            golden = dict(zip(map(tuple, case["cells"]), case["values"]))
             if not same:
                 assert tie, (case["preset"], case["kind"], mode)
                 excused += 1
+                # the selection is excused, not the energies: every cell both
+                # composites hold (at least the whole coarse pass) still agrees
+                assert_common_cells(comp.entries, golden)
                 continue
             assert list(rep.argmax_cell) == want["argmax_cell"]
             assert rep.coarse_points_evaluated == want["coarse_points_evaluated"]
             assert rep.fine_points_evaluated == want["fine_points_evaluated"]
             assert rep.reduction_ratio == want["reduction_ratio"]
-            golden = dict(zip(map(tuple, case["cells"]), case["values"]))
             assert set(comp.entries) == set(golden)
             keys = list(golden)
             assert peak_err([comp.entries[k] for k in keys], [golden[k] for k in keys]) <= 1e-4
@@ -239,9 +242,10 @@ class TestGoldenFrameworks:
             want = case["report"]
             same, tie = compare_trace(rep.trace, want["trace"], rep.final_region, want["final_region"])
             assert same or tie, (case["seed"], case["kind"])
+            golden = dict(zip(map(tuple, case["cells"]), case["values"]))
+            assert_common_cells(comp.entries, golden)
             if same:
                 assert list(rep.argmax_cell) == want["argmax_cell"]
-                golden = dict(zip(map(tuple, case["cells"]), case["values"]))
                 assert set(comp.entries) == set(golden)
                 keys = list(golden)
                 assert peak_err([comp.entries[k] for k in keys], [golden[k] for k in keys]) <= 1e-4
@@ -264,6 +268,7 @@ class TestGoldenFrameworks:
             want_final = {"min_cell": list(orep["final_region"][0]), "max_cell": list(orep["final_region"][1])}
             same, tie = compare_trace(rep.trace, orep["trace"], rep.final_region, want_final)
             assert same or tie, seed
+            assert_common_cells(comp.entries, oc)
             if same:
                 assert rep.argmax_cell == orep["argmax_cell"]
                 keys = list(oc)
@@ -282,6 +287,38 @@ class TestAcceptance:  # test_acceptance.py criteria 1, 2 (point counts), 3, 8
                 assert math.hypot(x - tumour[0], y - tumour[1]) <= 0.005
                 if name == "dataset1" and kind == "das":
                     assert rep.decimation_factor == 7 and rep.reduction_ratio >= 4.0
+
+    def test_criterion_2_on_the_gpu(self):
+        """test_acceptance.py:86-111 restated.  The point-count floor holds
+        exactly (>= 4x at D = 7 on dataset1).  The paper's wall-clock floor
+        (>= 8x) is a CPU property (time ~ points); on the B200 both calls are
+        latency-bound, so the ratio is measured, printed and required > 1:
+        the reference's own formula (median wall time of the full masked DMAS
+        image over the framework report's elapsed total) and wall over wall."""
+        import time
+
+        _, ds = preset("dataset1")
+        grid = grid_for_geometry(ds.geometry, 0.001)
+        _, das = mw.run_framework(ds, "das", grid, mw.Automatic(0.01))
+        assert das.decimation_factor == 7 and das.reduction_ratio >= 4.0
+        mask = mw.breast_mask(grid)
+        mw.image(ds, "dmas", grid, mask=mask)
+        mw.run_framework(ds, "dmas", grid, mw.Automatic(0.01))
+        full, fw, fw_wall = [], [], []
+        for _ in range(7):
+            t0 = time.perf_counter()
+            mw.image(ds, "dmas", grid, mask=mask)
+            full.append(time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            _, rep = mw.run_framework(ds, "dmas", grid, mw.Automatic(0.01))
+            fw_wall.append(time.perf_counter() - t0)
+            fw.append(rep.elapsed["total"])
+        ratio = float(np.median(full) / np.median(fw))
+        wall_ratio = float(np.median(full) / np.median(fw_wall))
+        print(f"criterion 2 on the B200: full {np.median(full) * 1e3:.3f} ms, framework elapsed "
+              f"{np.median(fw) * 1e3:.3f} ms ({ratio:.2f}x), framework wall {np.median(fw_wall) * 1e3:.3f} ms "
+              f"({wall_ratio:.2f}x)")
+        assert ratio > 1.0
 
     def test_coarse_equals_point_kernel_and_manual1(self):
         _, ds = preset("dataset1")
@@ -356,3 +393,34 @@ def test_concurrent_host_threads_share_plans_safely():
     with ThreadPoolExecutor(max_workers=4) as pool:
         got = list(pool.map(one, dss * 2))
     assert got == want * 2
+
+
+def test_concurrent_first_calls_capture_safely():
+    """Worker threads whose FIRST calls race: one thread captures a plan's
+    graph while others upload fresh datasets and masks outside PLAN_LOCK
+    (thread-local capture mode).  Every result equals the sequential one."""
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1709_02549_b200.segment import segment
+
+    model = synth.ScanModel(n_samples=1024)
+    # grids used by no other test: no cached plan exists for them yet
+    grids = [mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), r) for r in (4.75e-4, 5.25e-4)]
+    dss = [synth.dataset_2d(model, seed=900 + i)[0] for i in range(8)]
+    win = (model.k0, model.window)
+    start = threading.Barrier(8)
+
+    def one(i, wait=True):
+        if wait:
+            start.wait()
+        ds, grid = dss[i], grids[i % 2]
+        comp, rep = mw.run_framework(ds, "das", grid, mw.Manual(grid.dims[0] // 32), window=win)
+        fine, srep = segment(ds, "dmas", grid, 16, 0.01, window=win)
+        img = mw.image(ds, "dmas", grid, window=win, mask=mw.breast_mask(grid))
+        return comp.entries, rep.final_region, fine.entries, srep.argmax_cell, img.entries
+
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        got = list(pool.map(one, range(8)))
+    want = [one(i, wait=False) for i in range(8)]
+    assert got == want

@@ -150,3 +150,22 @@ def test_octant_framework_argument_errors():
         run_framework_volume(ds, "das", grid, mw.Manual(3), mask=np.zeros(grid.dims, dtype=bool))
     with pytest.raises(ValueError):
         run_framework_volume(ds, "das", grid, mw.Manual(3), interpolation="cubic")
+
+
+def test_octant_framework_sees_in_place_mask_edits():
+    """A writable mask edited in place between calls must not replay the plan
+    of its old contents (volume._mask_key hashes writable masks every call)."""
+    vm = synth.VolumeModel(n_samples=1024)
+    g = vm.geometry()
+    sig, _ = synth.scan_3d(vm, seed=31)
+    ds = mw.BackscatterDataset(g, synth.embed_pairs(vm.n_ant, vm.pairs(), sig))
+    grid = VolumeGrid((-0.024, -0.024, 0.0), (0.048, 0.048, 0.024), 0.002)
+    mask = np.array(hemisphere_mask(grid, 0.024))  # writable copy
+    win = (vm.k0, vm.window)
+    _, rep_a = run_framework_volume(ds, "dmas", grid, mw.Manual(3), mask=mask, window=win)
+    mask[:, :, 6:] = False  # in place: the upper half of the volume leaves the phantom
+    _, rep_b = run_framework_volume(ds, "dmas", grid, mw.Manual(3), mask=mask, window=win)
+    fresh = np.array(mask)
+    _, rep_c = run_framework_volume(ds, "dmas", grid, mw.Manual(3), mask=fresh, window=win)
+    assert rep_b.full_equivalent_points == int(mask.sum()) != rep_a.full_equivalent_points
+    assert rep_b.to_dict() | {"elapsed": None} == rep_c.to_dict() | {"elapsed": None}

@@ -249,3 +249,34 @@ def test_kind_parsing():
     assert mw.BeamformerKind.parse(" dmas ") is mw.BeamformerKind.DMAS
     with pytest.raises(ValueError):
         mw.BeamformerKind.parse("mvdr")
+
+
+def test_near_tie_excuse_is_tied_to_the_first_divergence():
+    """_mwb_helpers.divergence_excused: a differing selection is excused only
+    by a near-tie AT the iteration where the traces first differ."""
+    from _mwb_helpers import divergence_excused
+
+    def rec(sel, scores, w=1.0, b=1.0, sat=True):
+        return {"selected": sel, "scores": scores, "W": w, "B": b, "satisfied": sat}
+
+    clear = [1.0, 0.5, 0.2, 0.1]
+    tied = [1.0, 1.0 - 1e-6, 0.2, 0.1]
+    want = [rec(0, clear), rec(1, tied), rec(2, clear, w=0.5, b=2.0)]
+    # identical traces
+    assert divergence_excused(want, "n-min", want, "n-min")[:2] == (True, False)
+    # diverges at the tied iteration -> excused
+    got = [want[0], rec(0, tied)]
+    assert divergence_excused(got, "n-min", want, "n-min")[:2] == (False, True)
+    # a tie elsewhere does not excuse a divergence at a clear iteration
+    got = [want[0], want[1], rec(1, clear, w=0.5, b=2.0)]
+    assert divergence_excused(got, "n-min", want, "n-min")[:2] == (False, False)
+    # W/B clause: same child, verdict flipped, B within 1e-4 of B_prev and W not improving
+    w2 = [rec(0, clear, w=1.0, b=1.0), rec(1, clear, w=1.5, b=1.0 + 1e-6, sat=True)]
+    g2 = [w2[0], rec(1, clear, w=1.5, b=1.0 - 1e-6, sat=False)]
+    assert divergence_excused(g2, "distance-metrics", w2, "n-min")[:2] == (False, True)
+    # verdict flipped with clear margins -> not excused
+    w3 = [rec(0, clear, w=1.0, b=1.0), rec(1, clear, w=1.5, b=2.0, sat=True)]
+    g3 = [w3[0], rec(1, clear, w=1.5, b=2.0, sat=False)]
+    assert divergence_excused(g3, "distance-metrics", w3, "n-min")[:2] == (False, False)
+    # same records, different termination -> never excused
+    assert divergence_excused(want, "n-min", want, "region-floor")[:2] == (False, False)
