@@ -22,6 +22,10 @@
  *                             (BASELINE configs[4]; no reference counterpart)
  *   mwb_argmax_dense       <- pkg/src/mwbeam/beamform.py:101-104  EnergyMap.argmax_cell
  *   mwb_simulate           <- pkg/src/mwbeam/simulate.py:111-162 simulate (input producer)
+ *   mwb_compact_payload    <- pkg/src/mwbeam/io.py:65-86 load_dataset (device staging of the
+ *                             .mwb series in the layout the energy entry points take)
+ *   mwb_render_pgm         <- pkg/src/mwbeam/io.py:122-137 export_energy_map's raster
+ *                             over EnergyMap.dense, beamform.py:116-128
  *                             (also fused into mwb_energies through `argmax_key`)
  */
 #ifndef MWB_H
@@ -430,6 +434,31 @@ int mwb_image_lattice(const float* sig, int n_chan, int ld, int n_samples, const
 /* argmax over a dense map (valid cells only); key as in mwb_energies. */
 int mwb_argmax_dense(const float* dense, const uint8_t* valid, int n, uint64_t* key,
                      void* stream);
+
+/*
+ * Device staging of a .mwb container's series.  payload: the file's (m*m, n)
+ * fp64 little-endian series already in device memory (one H2D of the bytes).
+ * Writes the populated channels (any sample != 0; NaN counts as nonzero) in
+ * row-major (i, j) order as fp32 rows of ld >= n floats with a zero tail to
+ * out (capacity m*m rows), their (tx, rx) pairs to pairs (capacity m*m x 2
+ * int32) and the count to *count (device).  An all-zero record keeps channel
+ * (0, 0).  ws: m*m int32 of device workspace.  m in [1, 256].
+ */
+int mwb_compact_payload(const double* payload, int m, int n, int ld, float* out, int32_t* pairs, int32_t* count,
+                        int32_t* ws, void* stream);
+
+/*
+ * 8-bit PGM rasters of n_maps energy maps (export_energy_map's rendering):
+ * values (value_bits 32: float, 64: double) and valid (bytes) are
+ * [n_maps][map_stride] with cell (ix, iy) at ix * ny + iy.  Writes vrange
+ * (2 doubles per map: min and max over the valid cells) and raster
+ * [n_maps][ny][nx] (row r = iy, column c = ix), each byte
+ * rint(255 * clip((v - min) / (max - min), 0, 1)) in IEEE fp64, where v is the
+ * cell's value, else (stride > 1) the value of the stride lattice cell whose
+ * block holds it, else 0; a constant map renders as zeros.
+ */
+int mwb_render_pgm(const void* values, int value_bits, const uint8_t* valid, int n_maps, int nx, int ny,
+                   int64_t map_stride, int stride, double* vrange, uint8_t* raster, void* stream);
 
 /*
  * Roofline microbenchmarks run on the device: which = 0 shared-memory LDS.32

@@ -58,6 +58,7 @@ namespace {
 #include "mwb_segment.cuh"
 #include "mwb_microbench.cuh"
 #include "mwb_tc.cuh"
+#include "mwb_io.cuh"
 
 }  // namespace
 
@@ -1260,6 +1261,51 @@ int mwb_argmax_dense(const float* dense, const uint8_t* valid, int n, uint64_t* 
   argmax_dense_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       dense, valid, n, reinterpret_cast<unsigned long long*>(key));
   return check_launch("argmax_dense_kernel");
+}
+
+int mwb_compact_payload(const double* payload, int m, int n, int ld, float* out, int32_t* pairs, int32_t* count,
+                        int32_t* ws, void* stream) {
+  if (m < 1 || m > 256 || n < 1 || ld < n) return set_err(MWB_EINVAL, "mwb_compact_payload: bad sizes");
+  if (!payload || !out || !pairs || !count || !ws) return set_err(MWB_EINVAL, "mwb_compact_payload: null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  payload_flag_kernel<<<m * m, IO_THREADS, 0, st>>>(payload, n, ws);
+  int rc = check_launch("payload_flag_kernel");
+  if (rc) return rc;
+  payload_rows_kernel<<<1, IO_THREADS, 0, st>>>(ws, m, pairs, count);
+  if ((rc = check_launch("payload_rows_kernel"))) return rc;
+  dim3 g((ld + IO_THREADS - 1) / IO_THREADS < 8 ? (ld + IO_THREADS - 1) / IO_THREADS : 8, m * m);
+  payload_convert_kernel<<<g, IO_THREADS, 0, st>>>(payload, n, ld, ws, out);
+  return check_launch("payload_convert_kernel");
+}
+
+int mwb_render_pgm(const void* values, int value_bits, const uint8_t* valid, int n_maps, int nx, int ny,
+                   int64_t map_stride, int stride, double* vrange, uint8_t* raster, void* stream) {
+  if (n_maps < 0 || nx < 1 || ny < 1 || stride < 1 || map_stride < (int64_t)nx * ny)
+    return set_err(MWB_EINVAL, "mwb_render_pgm: bad sizes");
+  if (value_bits != 32 && value_bits != 64) return set_err(MWB_EINVAL, "mwb_render_pgm: value_bits must be 32 or 64");
+  if (!values || !valid || !vrange || !raster) return set_err(MWB_EINVAL, "mwb_render_pgm: null pointer");
+  if (n_maps == 0) return MWB_OK;
+  if (n_maps > 65535) return set_err(MWB_ERANGE, "mwb_render_pgm: too many maps");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const long long cells = (long long)nx * ny;
+  long long blocks = (cells + IO_THREADS - 1) / IO_THREADS;
+  dim3 g((unsigned)(blocks < 1024 ? blocks : 1024), n_maps);
+  if (value_bits == 32) {
+    render_range_kernel<float><<<n_maps, IO_THREADS, 0, st>>>(static_cast<const float*>(values), valid, cells,
+                                                              map_stride, vrange);
+    int rc = check_launch("render_range_kernel");
+    if (rc) return rc;
+    render_pgm_kernel<float><<<g, IO_THREADS, 0, st>>>(static_cast<const float*>(values), valid, nx, ny, map_stride,
+                                                       stride, vrange, raster);
+  } else {
+    render_range_kernel<double><<<n_maps, IO_THREADS, 0, st>>>(static_cast<const double*>(values), valid, cells,
+                                                               map_stride, vrange);
+    int rc = check_launch("render_range_kernel");
+    if (rc) return rc;
+    render_pgm_kernel<double><<<g, IO_THREADS, 0, st>>>(static_cast<const double*>(values), valid, nx, ny,
+                                                        map_stride, stride, vrange, raster);
+  }
+  return check_launch("render_pgm_kernel");
 }
 
 int mwb_microbench(int which, double* work, float* ms, void* stream) {
