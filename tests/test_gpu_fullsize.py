@@ -123,3 +123,55 @@ def test_cfg4_full_size_volume_properties():
         want = orc.volume_energies(g.antennas, g.propagation_speed, g.sample_interval, full, pts3, kind,
                                    vm.k0, vm.window)
         assert np.abs(got - want).max() / np.abs(dense).max() <= 1e-4, kind
+
+
+def test_cfg4_full_size_octant_framework_vs_oracle():
+    """configs[4] at full size: the 128^3 octant framework (run_framework_volume,
+    exactly as bench.py runs it).  The oracle's octant control flow
+    (select_roi_3d, restating coarse2fine.py:169-256 with 8 children) runs on
+    the GPU's own coarse lattice and must produce the same trace (a divergence
+    is excused only by a near-tie at the first diverging iteration), the same
+    final box and termination; the coarse values are checked against the
+    z-shift oracle on a sample, and the composite's argmax against the oracle
+    over the candidate band (every voxel within 1e-3 of the peak of the
+    GPU maximum; see test_gpu_bench_path.py for why that set suffices)."""
+    import paper_1709_02549_b200 as mw
+    from _mwb_helpers import divergence_excused
+    from paper_1709_02549_b200.volume import VolumeGrid, hemisphere_mask, run_framework_volume
+
+    vm = synth.VolumeModel()
+    sig, _ = synth.scan_3d(vm, seed=9)
+    full = synth.embed_pairs(vm.n_ant, vm.pairs(), sig)
+    g = vm.geometry()
+    ds = mw.BackscatterDataset(g, full)
+    g4 = VolumeGrid((-0.06, -0.06, 0.0), (0.12, 0.12, 0.12), 0.12 / 128)
+    win = (vm.k0, vm.window)
+    mask = hemisphere_mask(g4, vm.phantom_radius)
+    comp, rep = run_framework_volume(ds, "dmas", g4, mw.Automatic(0.01), mask=mask, window=win)
+    d = rep.decimation_factor
+    entries = comp.entries
+    coarse = {c: v for c, v in entries.items() if c[0] % d == 0 and c[1] % d == 0 and c[2] % d == 0}
+    assert len(coarse) == rep.coarse_points_evaluated == int(mask[::d, ::d, ::d].sum())
+    final, trace = orc.select_roi_3d(coarse, ((0, 0, 0), (127, 127, 127)))
+    same, tie, why = divergence_excused(rep.trace.records, rep.trace.termination, trace["records"],
+                                        trace["termination"])
+    assert same or tie, why
+    if same:
+        assert rep.final_region.bounds() == (*final[0], *final[1])
+    # coarse energies against the z-shift oracle (reference kernel)
+    rng = np.random.default_rng(12)
+    keys = list(coarse)
+    pick = [keys[i] for i in rng.choice(len(keys), 24, replace=False)]
+    vals = np.array(list(entries.values()))
+    peak = float(np.abs(vals).max())
+    band = [c for c, v in entries.items() if v >= vals.max() - 1e-3 * peak]
+    assert len(band) < 200
+    cells = sorted(set(pick) | set(band))
+    pts = np.array([g4.cell_center(*c) for c in cells])
+    want = orc.volume_energies(g.antennas, g.propagation_speed, g.sample_interval, full, pts, "dmas", *win)
+    got = np.array([entries[c] for c in cells])
+    assert np.abs(got - want).max() / peak <= 1e-4
+    best = max(range(len(cells)), key=lambda i: (want[i], tuple(-x for x in cells[i])))
+    if tuple(rep.argmax_cell) != cells[best]:
+        gap = abs(want[best] - want[cells.index(tuple(rep.argmax_cell))]) / peak
+        assert gap <= 1e-4, (rep.argmax_cell, cells[best], gap)
