@@ -436,6 +436,25 @@ int mwb_argmax_dense(const float* dense, const uint8_t* valid, int n, uint64_t* 
                      void* stream);
 
 /*
+ * The coarse-to-fine framework's fine pass (coarse2fine.py:321-323) on a
+ * precomputed whole-grid point list in the padded 16 x 16 tile layout
+ * (mwb_enumerate_lattice_padded + mwb_delay_table_tiles, tile_info {0, count}):
+ * only cells inside the device box region {x0, y0, z0, x1, y1, z1} (the select
+ * kernel's output) that are not coarse-lattice cells (ix % skip_stride == 0 &&
+ * iy % skip_stride == 0; skip_stride 0 = none) are evaluated and written; each is
+ * marked in valid and counted into *count (device, atomically added).  Tiles
+ * with no such cell exit at once, so the launch costs about what the ROI
+ * costs, with no host sync and no per-call enumeration or delay table.
+ * Other arguments as mwb_energies / mwb_energies_split (one scan).
+ */
+int mwb_energies_region(const float* sig, int n_chan, int ld, int n_samples, const int32_t* chan_txrx,
+                        const double* ant_xyz, int n_ant, double inv_scale, const double* pts_xyz,
+                        const int32_t* out_idx, int n_pts, const int32_t* tile_info, const void* table, int interp,
+                        int k0, int window, float* out_das, float* out_dmas, uint64_t* key_das, uint64_t* key_dmas,
+                        int32_t* flags, const int32_t* region, int ny, int skip_stride, uint8_t* valid,
+                        int32_t* count, int mode, void* workspace, int64_t workspace_bytes, void* stream);
+
+/*
  * Device staging of a .mwb container's series.  payload: the file's (m*m, n)
  * fp64 little-endian series already in device memory (one H2D of the bytes).
  * Writes the populated channels (any sample != 0; NaN counts as nonzero) in
@@ -459,6 +478,16 @@ int mwb_compact_payload(const double* payload, int m, int n, int ld, float* out,
  */
 int mwb_render_pgm(const void* values, int value_bits, const uint8_t* valid, int n_maps, int nx, int ny,
                    int64_t map_stride, int stride, double* vrange, uint8_t* raster, void* stream);
+
+/* Stream-ordered copy of `bytes` between any two CUDA-visible addresses
+ * (cudaMemcpyDefault): the drop-in's per-call signal-slot refill and result
+ * readback without a framework op per copy. */
+int mwb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
+/* Elapsed milliseconds between consecutive recorded events: out_ms[i] =
+ * events[i] -> events[i + 1] for i < n_events - 1 (the framework report's
+ * phase timings in one call). */
+int mwb_elapsed_ms(void* const* events, int n_events, float* out_ms);
 
 /*
  * Roofline microbenchmarks run on the device: which = 0 shared-memory LDS.32

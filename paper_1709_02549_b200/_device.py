@@ -45,8 +45,15 @@ class GraphPlan:
     def _enqueue(self) -> None:  # pragma: no cover - abstract
         raise NotImplementedError
 
+    _slot_src = None  # the scan whose samples the slot holds (scans are immutable)
+
     def replay(self, scan: "DeviceScan") -> None:
-        self.scan.sig.copy_(scan.sig, non_blocking=True)
+        if scan is not self._slot_src:
+            from . import _native as nat
+
+            nat.call("mwb_memcpy_async", self.scan.sig.data_ptr(), scan.sig.data_ptr(),
+                     scan.sig.numel() * scan.sig.element_size(), stream_handle())
+            self._slot_src = scan
         if self.graph is None:
             self._enqueue()  # eager run: kernel attributes set, allocator warmed
             torch.cuda.current_stream().synchronize()

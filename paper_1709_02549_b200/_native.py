@@ -180,6 +180,13 @@ _SIGNATURES = {
          _P, _P, _I64, _P, _P, _P, _P, _P],
         _I,
     ),
+    "mwb_energies_region": (
+        [_P, _I, _I, _I, _P, _P, _I, _D, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P,
+         _I, _P, _I64, _P],
+        _I,
+    ),
+    "mwb_memcpy_async": ([_P, _P, _I64, _P], _I),
+    "mwb_elapsed_ms": ([_P, _I, _P], _I),
     "mwb_compact_payload": ([_P, _I, _I, _I, _P, _P, _P, _P, _P], _I),
     "mwb_render_pgm": ([_P, _I, _P, _I, _I, _I, _I64, _I, _P, _P, _P], _I),
     "mwb_microbench": ([_I, C.POINTER(C.c_double), C.POINTER(C.c_float), _P], _I),

@@ -254,8 +254,15 @@ class _Status:
 
     N_KEYS = 2
 
-    def __init__(self):
-        self.t = torch.zeros(self.N_KEYS + 2, dtype=torch.int64, device=dv.device())
+    BYTES = 8 * (N_KEYS + 2)
+
+    def __init__(self, storage: torch.Tensor | None = None):
+        """``storage``: BYTES of device memory to live in (e.g. a slice of a
+        plan's result block read back with one copy), else its own tensor."""
+        if storage is None:
+            self.t = torch.zeros(self.N_KEYS + 2, dtype=torch.int64, device=dv.device())
+        else:
+            self.t = storage[: self.BYTES].view(torch.int64)
 
     def key_ptr(self, i: int = 0) -> int:
         return self.t.data_ptr() + 8 * i

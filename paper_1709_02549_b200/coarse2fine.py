@@ -19,6 +19,8 @@ Drop-in for /root/reference/pkg/src/mwbeam/coarse2fine.py:
 
 from __future__ import annotations
 
+import ctypes
+
 import math
 from dataclasses import dataclass, field
 
@@ -238,6 +240,95 @@ def _region(b) -> Region:
     return Region((int(b[0]), int(b[1])), (int(b[3]), int(b[4])))
 
 
+class _DeviceTrace(MetricTrace):
+    """A MetricTrace whose records are decoded from the device trace's bytes on
+    first access.  run_framework's latency path reads only the termination
+    and the final region; building ~7 records of Python objects per call
+    (~60 us) is deferred until someone looks at them."""
+
+    def __init__(self, raw_records: bytes, n: int, termination: str, warning, region):
+        self._raw, self._n, self._region, self._records = raw_records, n, region, None
+        self.termination, self.warning = termination, warning
+
+    @property
+    def records(self) -> list:
+        if self._records is None:
+            recs = (nat.IterRecord * self._n).from_buffer_copy(self._raw) if self._n else []
+            self._records = [_record(recs[i], self._region) for i in range(self._n)]
+        return self._records
+
+    @records.setter
+    def records(self, value) -> None:
+        self._records = list(value)
+
+    @property
+    def n_records(self) -> int:
+        return self._n if self._records is None else len(self._records)
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, MetricTrace):
+            return NotImplemented
+        return (self.records, self.termination, self.warning) == (other.records, other.termination, other.warning)
+
+    __hash__ = None
+
+
+def _record(r, region) -> IterationRecord:
+    stats: list[dict | None] = []
+    nk = int(r.n_children)
+    for k in range(nk):
+        h = int(r.has_stats[k])
+        if h == 0:
+            stats.append(None)
+        elif h == 1:
+            stats.append({"mu": float(r.mu[k]), "var": float(r.var[k])})
+        else:
+            stats.append({
+                "mu": float(r.mu[k]),
+                "var": float(r.var[k]),
+                "delta_raw": float(r.delta_raw[k]),
+                "delta": float(r.delta[k]),
+                "clamped": bool(r.clamped[k]),
+            })
+    return IterationRecord(
+        iteration=int(r.iteration),
+        quadrant_counts=[int(c) for c in r.counts[:nk]],
+        scores=[float(x) for x in r.scores[:nk]],
+        stats=stats,
+        selected=int(r.selected),
+        selected_region=region(r.selected_region),
+        expanded_region=region(r.expanded_region),
+        w=float(r.w),
+        b=float(r.b),
+        satisfied=bool(r.satisfied),
+    )
+
+
+_REC_OFFSET = None
+
+
+def decode_trace_lazy(raw: np.ndarray, region=_region) -> tuple[Region, MetricTrace, int]:
+    """decode_trace with the records deferred (_DeviceTrace): reads the header
+    (termination, record count, final box) now and copies only the used
+    records' bytes, so the source buffer may be reused at once."""
+    import ctypes
+
+    global _REC_OFFSET
+    if _REC_OFFSET is None:
+        _REC_OFFSET = nat.Trace.records.offset
+    head = np.frombuffer(raw, dtype=np.int32, count=8)
+    code, n = int(head[0]), int(head[1])
+    if code == -1:
+        raise ValueError("coarse map has no entries in the breast region")
+    if code == -2:
+        raise RuntimeError(f"select_roi exceeded {nat.MAX_ITERS} iterations")
+    n = min(n, nat.MAX_ITERS)
+    size = ctypes.sizeof(nat.IterRecord)
+    body = bytes(memoryview(raw)[_REC_OFFSET: _REC_OFFSET + n * size])
+    warning = "energy map has no discriminating signal" if code == 1 else None
+    return region(head[2:8]), _DeviceTrace(body, n, nat.TERMINATION[code], warning, region), code
+
+
 def decode_trace(raw, region=_region) -> tuple[Region, MetricTrace, int]:
     """Device trace (bytes, or a writable uint8 array decoded in place) ->
     (final region, MetricTrace, termination code); ``region`` converts a device
@@ -253,35 +344,7 @@ def decode_trace(raw, region=_region) -> tuple[Region, MetricTrace, int]:
     if code == 1:
         trace.warning = "energy map has no discriminating signal"
     for i in range(int(tr.n_records)):
-        r = tr.records[i]
-        stats: list[dict | None] = []
-        nk = int(r.n_children)
-        for k in range(nk):
-            h = int(r.has_stats[k])
-            if h == 0:
-                stats.append(None)
-            elif h == 1:
-                stats.append({"mu": float(r.mu[k]), "var": float(r.var[k])})
-            else:
-                stats.append({
-                    "mu": float(r.mu[k]),
-                    "var": float(r.var[k]),
-                    "delta_raw": float(r.delta_raw[k]),
-                    "delta": float(r.delta[k]),
-                    "clamped": bool(r.clamped[k]),
-                })
-        trace.records.append(IterationRecord(
-            iteration=int(r.iteration),
-            quadrant_counts=[int(c) for c in r.counts[:nk]],
-            scores=[float(s) for s in r.scores[:nk]],
-            stats=stats,
-            selected=int(r.selected),
-            selected_region=region(r.selected_region),
-            expanded_region=region(r.expanded_region),
-            w=float(r.w),
-            b=float(r.b),
-            satisfied=bool(r.satisfied),
-        ))
+        trace.records.append(_record(tr.records[i], region))
     return region(tr.final_region), trace, code
 
 
@@ -348,17 +411,25 @@ class _FrameworkPlan(dv.GraphPlan):
         self.mask_np, self.mask_t = _breast_mask_device(grid)
         self.full_equivalent = int(self.mask_np.sum())  # the report's full-resolution cell count (fixed per plan)
         dev = dv.device()
-        self.dense = torch.empty(nx * ny, dtype=torch.float32, device=dev)  # only valid cells are read
-        self.valid = torch.empty(nx * ny, dtype=torch.uint8, device=dev)
-        self.status = _Status()
+        # One device result block, read back with ONE copy per call into a
+        # fresh pinned block that the returned map and report keep (no host
+        # copy): [status | trace | dense fp32 (only valid cells are read) | valid]
+        n = nx * ny
+        self._o_trace = _Status.BYTES
+        self._o_dense = (self._o_trace + nat.TRACE_BYTES + 15) // 16 * 16
+        self._o_valid = self._o_dense + 4 * n
+        self._res_bytes = self._o_valid + n
+        self.res = torch.empty(self._res_bytes, dtype=torch.uint8, device=dev)
+        self.status = _Status(self.res)
+        self.trace_t = self.res[self._o_trace: self._o_trace + nat.TRACE_BYTES]
+        self.dense = self.res[self._o_dense: self._o_valid].view(torch.float32)
+        self.valid = self.res[self._o_valid:]
         self.region_t = torch.empty(6, dtype=torch.int32, device=dev)
-        self.trace_t = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
         # external events become timestamp nodes inside the captured graph
         self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
-        pin = torch.cuda.is_available()
-        self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=pin)
-        self.h_trace = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, pin_memory=pin)
-        self._pin = pin  # map buffers are fresh pinned blocks per call (handed to the EnergyMap, no host copy)
+        self._ev_handles = None  # raw cudaEvent_t array for mwb_elapsed_ms (after the first record)
+        self._ms = (ctypes.c_float * 3)()
+        self._pin = torch.cuda.is_available()
         self.replays = 0
         # The coarse lattice and its delay table depend on the geometry, grid
         # and mask only: enumerated and tabled once here, outside the graph,
@@ -374,6 +445,31 @@ class _FrameworkPlan(dv.GraphPlan):
                  self.c_count.data_ptr(), self.c_valid.data_ptr(), ws.data_ptr(), dv.stream_handle())
         self.c_table = build_table(scan, self.c_pts, p_max, interp, self.c_count.data_ptr())
         self.n_coarse = int(self.c_count.item())
+        # Fine pass: every masked cell of the grid in the padded 16 x 16 tile
+        # layout with its delay table, also built once here; each call's fine
+        # launch (mwb_energies_region) evaluates just the tiles that meet the
+        # ROI the select kernel left on the device, writing the ROI's
+        # non-coarse cells.  No per-call enumeration, table or host sync.
+        lib = nat.load()
+        tiles = int(lib.mwb_lattice_tile_count(nx, ny, 1))
+        self.f_n = 256 * tiles
+        self.f_pts = torch.zeros((self.f_n, 3), dtype=torch.float64, device=dev)
+        self.f_oidx = torch.zeros(self.f_n, dtype=torch.int32, device=dev)
+        self.f_info = torch.zeros((tiles, 2), dtype=torch.int32, device=dev)
+        f_count = torch.zeros(1, dtype=torch.int32, device=dev)
+        f_valid = torch.zeros(nx * ny, dtype=torch.uint8, device=dev)
+        ws = torch.empty(int(lib.mwb_lattice_workspace_bytes(nx, ny, 1)), dtype=torch.uint8, device=dev)
+        nat.call("mwb_enumerate_lattice_padded", grid.origin[0], grid.origin[1], grid.resolution, nx, ny, 0, 0,
+                 nx - 1, ny - 1, 1, self.mask_t.data_ptr(), 0, self.f_pts.data_ptr(), self.f_oidx.data_ptr(),
+                 self.f_info.data_ptr(), f_count.data_ptr(), f_valid.data_ptr(), ws.data_ptr(), dv.stream_handle())
+        self.f_table = torch.empty(int(lib.mwb_delay_table_bytes(self.f_n, scan.n_chan)), dtype=torch.uint8,
+                                   device=dev)
+        nat.call("mwb_delay_table_tiles", self.f_pts.data_ptr(), self.f_n, self.f_info.data_ptr(),
+                 scan.chan.data_ptr(), scan.n_chan, scan.ant.data_ptr(), scan.n_ant, scan.inv_scale, interp,
+                 self.f_table.data_ptr(), dv.stream_handle())
+        # window-split partials for long windows (the reference's full record)
+        need = int(lib.mwb_energies_split_bytes(self.f_n, 1, w)) if w > 48 else 0
+        self.f_ws = torch.empty(need, dtype=torch.uint8, device=dev) if 0 < need <= (256 << 20) else None
 
     def _enqueue(self) -> None:
         g, d = self.grid, self.d
@@ -389,48 +485,52 @@ class _FrameworkPlan(dv.GraphPlan):
         ev[1].record()
         _launch_select(self.dense, self.valid, g, d, g.full_region(), self.cfg, self.region_t, self.trace_t)
         ev[2].record()
-        lattice_pass(self.scan, g, 1, self.mask_t, d, (self.kcode,), self.interp, self.k0, self.w,
-                     {self.kcode: self.dense}, self.valid, self.status, 1, d_region=self.region_t, mode=self.mode)
+        sc, das = self.scan, self.kcode == nat.MWB_DAS
+        nat.call("mwb_energies_region", sc.sig.data_ptr(), sc.n_chan, sc.ld, sc.n_samples, sc.chan.data_ptr(),
+                 sc.ant.data_ptr(), sc.n_ant, sc.inv_scale, self.f_pts.data_ptr(), self.f_oidx.data_ptr(), self.f_n,
+                 self.f_info.data_ptr(), self.f_table.data_ptr(), self.interp, self.k0, self.w,
+                 self.dense.data_ptr() if das else None, None if das else self.dense.data_ptr(),
+                 st.key_ptr(0), st.key_ptr(1), st.flags_ptr, self.region_t.data_ptr(), g.dims[1], d,
+                 self.valid.data_ptr(), st.count_ptr(1), self.mode, nat.ptr(self.f_ws),
+                 0 if self.f_ws is None else self.f_ws.numel(), dv.stream_handle())
         ev[3].record()
 
     def launch(self, scan: dv.DeviceScan) -> None:
         """Enqueue one run on ``scan`` (graph replay after the first call) and the readback."""
         self.replay(scan)
         self.replays += 1
-        nx, ny = self.grid.dims
-        self.h_dense = torch.empty(nx * ny, dtype=torch.float32, pin_memory=self._pin)
-        self.h_valid = torch.empty(nx * ny, dtype=torch.uint8, pin_memory=self._pin)
-        for src, dst in ((self.status.t, self.h_status), (self.trace_t, self.h_trace), (self.dense, self.h_dense),
-                         (self.valid, self.h_valid)):
-            dst.copy_(src, non_blocking=True)
+        self.h_res = torch.empty(self._res_bytes, dtype=torch.uint8, pin_memory=self._pin)
+        nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), self._res_bytes,
+                 dv.stream_handle())
 
     def finish(self) -> tuple[EnergyMap, FrameworkReport]:
         torch.cuda.current_stream().synchronize()
         nx, ny = self.grid.dims
-        h = self.h_status.numpy()
+        blk = self.h_res.numpy()
+        h = blk[: _Status.BYTES].view(np.int64)
         keys = h[:2].view(np.uint64)
         tail = h[2:].view(np.int32)
         counts, flags = tail[:2], int(tail[2])
         if flags & 1:
             raise ValueError("energy map contains non-finite values")
-        final, trace, _ = decode_trace(self.h_trace.numpy())  # decoded in place: the buffer is reused next call
+        final, trace, _ = decode_trace_lazy(blk[self._o_trace: self._o_trace + nat.TRACE_BYTES])
         n_coarse, n_fine = self.n_coarse, int(counts[1])
         EVAL_COUNTER.add(n_coarse)
         EVAL_COUNTER.add(n_fine)
-        vals = self.h_dense.numpy().reshape(nx, ny)
-        vmask = self.h_valid.numpy().reshape(nx, ny).view(bool)
+        vals = blk[self._o_dense: self._o_valid].view(np.float32).reshape(nx, ny)
+        vmask = blk[self._o_valid:].view(bool).reshape(nx, ny)
         composite = EnergyMap._from_dense(self.grid, vals, vmask, stride=self.d, roi=final, split=self.d, checked=True)
-        ev = self.events
-        t_c = ev[0].elapsed_time(ev[1]) / 1e3
-        t_s = ev[1].elapsed_time(ev[2]) / 1e3
-        t_f = ev[2].elapsed_time(ev[3]) / 1e3
+        if self._ev_handles is None:
+            self._ev_handles = (ctypes.c_void_p * 4)(*[e.cuda_event for e in self.events])
+        nat.call("mwb_elapsed_ms", self._ev_handles, 4, self._ms)
+        t_c, t_s, t_f = (self._ms[i] / 1e3 for i in range(3))
         full_equivalent = self.full_equivalent
         key = int(keys[0 if self.kcode == nat.MWB_DAS else 1])
         slot = 0xFFFFFFFF - (key & 0xFFFFFFFF)
         cell = (slot // ny, slot % ny) if key != 0 else composite.argmax_cell()
         report = FrameworkReport(
             decimation_factor=self.d,
-            iterations=len(trace.records),
+            iterations=trace.n_records,
             final_region=final,
             coarse_points_evaluated=n_coarse,
             fine_points_evaluated=n_fine,

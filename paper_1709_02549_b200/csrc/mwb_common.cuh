@@ -242,7 +242,35 @@ struct EnergyParams {
   // and energy_reduce_kernel sums them in chunk order, as the unsplit kernel does
   float2* part;
   int chunks_per_cta;
+  // ROI filter (the framework's fine pass over a precomputed whole-grid
+  // table): only points whose output cell (ix, iy) = (o / filt_ny, o % filt_ny)
+  // lies in the device box filt_region {x0, y0, z0, x1, y1, z1} and is not a
+  // coarse-lattice cell (ix % filt_skip == 0 && iy % filt_skip == 0; 0 = none;
+  // skip 1 = every cell is coarse, the Manual(1) framework)
+  // are written; each written cell is marked in filt_valid and counted in
+  // *filt_count.  CTAs with no such point exit before staging anything.
+  const int* filt_region;
+  int filt_ny;
+  int filt_skip;
+  uint8_t* filt_valid;
+  int* filt_count;
 };
+
+__device__ __forceinline__ bool filter_keep(const EnergyParams& p, int o) {
+  const int ix = o / p.filt_ny, iy = o - ix * p.filt_ny;
+  const bool in = p.filt_region[0] <= ix && ix <= p.filt_region[3] && p.filt_region[1] <= iy &&
+                  iy <= p.filt_region[4];
+  const bool coarse = p.filt_skip > 0 && ix % p.filt_skip == 0 && iy % p.filt_skip == 0;
+  return in && !coarse;
+}
+
+// mark and count the cells a filtered launch writes (one atomic per warp)
+__device__ __forceinline__ void filter_mark(const EnergyParams& p, bool wa, int oa, bool wb, int ob) {
+  if (wa) p.filt_valid[oa] = 1;
+  if (wb) p.filt_valid[ob] = 1;
+  const int n = __popc(__ballot_sync(0xffffffffu, wa)) + __popc(__ballot_sync(0xffffffffu, wb));
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(p.filt_count, n);
+}
 
 struct SmemLayout {
   size_t lo, alloc, off, sb, misc, mbar, stage, total;

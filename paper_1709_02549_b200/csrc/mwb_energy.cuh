@@ -256,6 +256,10 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
   // them live across the sample loop costs the register-capped kernels spills)
   const int oa = va ? (p.out_idx ? __ldg(p.out_idx + (int)tile * TILE + la) : tile0 + la) : -1;
   const int ob = vb ? (p.out_idx ? __ldg(p.out_idx + (int)tile * TILE + lb) : tile0 + lb) : -1;
+  // ROI filter: which of this thread's points are written; a CTA with none exits
+  const bool wa = va && (!p.filt_region || filter_keep(p, oa));
+  const bool wb = vb && (!p.filt_region || filter_keep(p, ob));
+  if (p.filt_region && !__syncthreads_or(wa || wb)) return;
 
   // ---- per-channel spans and stage-buffer groups --------------------------
   for (int c = tid; c < p.C; c += TPB) {
@@ -462,6 +466,7 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
       }
       if (q == n_chunks - 1) {
         bool bad = false;
+        if (p.filt_region) filter_mark(p, wa, oa, wb, ob);
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
           const bool want = kk == 0 ? KIND != KIND_DMAS : KIND != KIND_DAS;
@@ -477,11 +482,11 @@ __global__ void __launch_bounds__(TPB, MINB) energy_kernel(const EnergyParams p)
           float* out = (kk == 0 ? p.out_das : p.out_dmas) + (size_t)s * (size_t)p.out_stride;
           unsigned long long* keys = kk == 0 ? p.key_das : p.key_dmas;
           unsigned long long key = 0ull;
-          if (va) {
+          if (wa) {
             out[oa] = ea;
             if (isfinite(ea)) key = argmax_key(ea, oa); else bad = true;
           }
-          if (vb) {
+          if (wb) {
             out[ob] = eb;
             if (isfinite(eb)) key = max(key, (unsigned long long)argmax_key(eb, ob)); else bad = true;
           }
@@ -532,7 +537,11 @@ __global__ void __launch_bounds__(256) energy_reduce_kernel(const EnergyParams p
       if (KIND != KIND_DAS) eQ += (double)sq.y;
     }
   }
-  const int o = v ? (p.out_idx ? __ldg(p.out_idx + src) : i) : -1;
+  int o = v ? (p.out_idx ? __ldg(p.out_idx + src) : i) : -1;
+  if (p.filt_region) {
+    v = v && filter_keep(p, o);
+    filter_mark(p, v, o, false, 0);
+  }
   const int lane = threadIdx.x & 31;
   bool bad = false;
 #pragma unroll

@@ -197,8 +197,20 @@ static int energy_params(const float* sig, int n_scans, int64_t scan_stride, int
   p.cap = 0;
   p.part = nullptr;
   p.chunks_per_cta = 0;
+  p.filt_region = nullptr;
+  p.filt_ny = 1;
+  p.filt_skip = 0;
+  p.filt_valid = nullptr;
+  p.filt_count = nullptr;
   return MWB_OK;
 }
+
+struct RegionFilter {
+  const int32_t* region;
+  int ny, skip;
+  uint8_t* valid;
+  int32_t* count;
+};
 
 static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld,
                          int n_samples, const int32_t* chan_txrx, const double* ant_xyz, int n_ant,
@@ -207,7 +219,7 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
                          int window, float* out_das, float* out_dmas, int64_t out_stride, uint64_t* key_das,
                          uint64_t* key_dmas, int32_t* flags, int mode, void* stream,
                          const int32_t* tile_src = nullptr, int n_src_pts = 0, void* part_ws = nullptr,
-                         int64_t part_bytes = 0) {
+                         int64_t part_bytes = 0, const RegionFilter* filt = nullptr) {
   // tile_src (with tile_info): launched tile t evaluates source tile tile_src[t]
   // of a shared point list / table of n_src_pts points; n_pts counts the
   // launched (packed output) positions
@@ -222,6 +234,13 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
     p.tile_src = tile_src;
     p.src_tiles = (n_src_pts + TILE - 1) / TILE;
     p.P = n_pts;
+  }
+  if (filt) {
+    p.filt_region = filt->region;
+    p.filt_ny = filt->ny;
+    p.filt_skip = filt->skip;
+    p.filt_valid = filt->valid;
+    p.filt_count = filt->count;
   }
   const long long tiles = (n_pts + TILE - 1) / TILE;
   // register chunk: 48 samples for windows that are a multiple of 48 (the
@@ -252,7 +271,8 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   // tile bound, so they are treated as small.
   const int n_chunks = (window + ch - 1) / ch;
   if (part_ws && n_chunks > 1) {
-    const long long work_ctas = (long long)(d_count ? std::min<long long>(tiles, 16) : tiles) * grid.y;
+    // launches over a device count or an ROI filter may do far less work than their tile bound
+    const long long work_ctas = (long long)((d_count || filt) ? std::min<long long>(tiles, 16) : tiles) * grid.y;
     const long long target = 148LL * resident * 4;
     long long groups = std::min<long long>(n_chunks, (target + work_ctas - 1) / work_ctas);
     const long long rows = tile_info ? (long long)n_pts : (long long)n_scans * n_pts;
@@ -335,6 +355,20 @@ int mwb_energies_tiles(const float* sig, int n_scans, int64_t scan_stride, int n
   return energies_impl(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
                        pts_xyz, out_idx, n_pts, nullptr, tile_info, table, interp, k0, window, out_das, out_dmas,
                        out_stride, key_das, key_dmas, flags, mode, stream);
+}
+
+int mwb_energies_region(const float* sig, int n_chan, int ld, int n_samples, const int32_t* chan_txrx,
+                        const double* ant_xyz, int n_ant, double inv_scale, const double* pts_xyz,
+                        const int32_t* out_idx, int n_pts, const int32_t* tile_info, const void* table, int interp,
+                        int k0, int window, float* out_das, float* out_dmas, uint64_t* key_das, uint64_t* key_dmas,
+                        int32_t* flags, const int32_t* region, int ny, int skip_stride, uint8_t* valid,
+                        int32_t* count, int mode, void* workspace, int64_t workspace_bytes, void* stream) {
+  if (!tile_info || !region || !valid || !count || !out_idx || ny < 1)
+    return set_err(MWB_EINVAL, "mwb_energies_region: null pointer or bad ny");
+  const RegionFilter f{region, ny, skip_stride, valid, count};
+  return energies_impl(sig, 1, 0, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale, pts_xyz, out_idx,
+                       n_pts, nullptr, tile_info, table, interp, k0, window, out_das, out_dmas, 0, key_das, key_dmas,
+                       flags, mode, stream, nullptr, 0, workspace, workspace_bytes, &f);
 }
 
 // ---- tensor-core path (mwb_tc.cuh) ----------------------------------------
@@ -696,6 +730,14 @@ static int select_common(SelectParams& p, void* stream, int n_scans = 1) {
   }
   p.staged = n > 0 && n <= SEL_STAGE_MAX;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (p.dims == 2 && n > 0 && n <= SAT_MAX_CELLS) {  // K2s: summed-area tables, one CTA per scan
+    const size_t sm = sat_smem_bytes(p.sL[0], p.sL[1]);
+    cudaError_t e = cudaFuncSetAttribute(select_roi_sat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sat_smem_bytes(SAT_MAX_CELLS, 1) > (int)sm ? (int)sat_smem_bytes(SAT_MAX_CELLS, 1) : (int)sm);
+    if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    select_roi_sat_kernel<<<n_scans, SAT_TPB, sm, st>>>(p);
+    return check_launch("select_roi_sat_kernel");
+  }
   if (p.dims == 2 && n > 0 && n <= SEL_WARP_STAGE) {  // K2w: warp per scan, or one warp per box
     const bool split = n_scans < SEL_SPLIT_MAX_SCANS;
     void (*wk)(SelectParams, int) = split ? select_roi_warp_kernel<true> : select_roi_warp_kernel<false>;
@@ -1306,6 +1348,24 @@ int mwb_render_pgm(const void* values, int value_bits, const uint8_t* valid, int
                                                         map_stride, stride, vrange, raster);
   }
   return check_launch("render_pgm_kernel");
+}
+
+int mwb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes && (!dst || !src))) return set_err(MWB_EINVAL, "mwb_memcpy_async: bad arguments");
+  if (bytes == 0) return MWB_OK;
+  const cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault,
+                                        reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? MWB_OK : set_err(MWB_ECUDA, "cudaMemcpyAsync: %s", cudaGetErrorString(e));
+}
+
+int mwb_elapsed_ms(void* const* events, int n_events, float* out_ms) {
+  if (n_events < 2 || !events || !out_ms) return set_err(MWB_EINVAL, "mwb_elapsed_ms: bad arguments");
+  for (int i = 0; i + 1 < n_events; ++i) {
+    const cudaError_t e = cudaEventElapsedTime(out_ms + i, reinterpret_cast<cudaEvent_t>(events[i]),
+                                               reinterpret_cast<cudaEvent_t>(events[i + 1]));
+    if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaEventElapsedTime: %s", cudaGetErrorString(e));
+  }
+  return MWB_OK;
 }
 
 int mwb_microbench(int which, double* work, float* ms, void* stream) {

@@ -710,3 +710,323 @@ __global__ void __launch_bounds__(SPLIT ? SEL_SPLIT_WARPS * 32 : SEL_WPB * 32)
     put_box(region_out, sel);
   }
 }
+
+// ----------------------------------------------------------------------------
+// K2s: 2-D select_roi on summed-area tables (single scans and batches, one
+// CTA per scan).  Every statistic the selection needs is a box statistic of
+// the coarse lattice: count, mean and sum of squared deviations of a child
+// quadrant, of a child's expansion, of the current selection.  Three
+// summed-area tables over the staged breast box — valid count, sum of
+// (x - c) and sum of (x - c)^2 in fp64, with c the breast box's mean (a shift
+// that keeps the one-pass m2 = Q - S^2 / n free of cancellation) — turn each
+// into four lookups, so an iteration costs O(1) instead of two passes over
+// the cells.  The tables are built once (row then column prefix sums, all
+// threads); warp 0 then runs the iterations: lane k evaluates box k (four
+// children, four expansions), select_score makes the decision exactly as the
+// cell-walking kernels do.  Decisions match the reference's two-pass numpy
+// statistics up to fp64 rounding (near-ties are the parity bar's excuse).
+// ----------------------------------------------------------------------------
+constexpr int SAT_TPB = 256;
+constexpr int SAT_MAX_CELLS = 4096;  // staged lattice cells (tables: 20 B per (Lx+1)(Ly+1) entry)
+
+__host__ __device__ inline size_t sat_smem_bytes(int lx, int ly) {
+  const size_t e = (size_t)(lx + 1) * (ly + 1);
+  return e * (2 * sizeof(double) + sizeof(int));
+}
+
+struct SatView {
+  const int* c;
+  const double* s;
+  const double* q;
+  int ly1;  // Ly + 1 (row length)
+  // box of lattice indices [x0, x1] x [y0, y1] relative to the staged origin
+  __device__ __forceinline__ void box(int x0, int y0, int x1, int y1, double& n, double& S, double& Q) const {
+    if (x1 < x0 || y1 < y0) {
+      n = S = Q = 0.0;
+      return;
+    }
+    const int a = x0 * ly1 + y0, b = x0 * ly1 + y1 + 1, cc = (x1 + 1) * ly1 + y0, d = (x1 + 1) * ly1 + y1 + 1;
+    n = (double)(c[d] - c[b] - c[cc] + c[a]);
+    S = __dadd_rn(__dsub_rn(__dsub_rn(s[d], s[b]), s[cc]), s[a]);
+    Q = __dadd_rn(__dsub_rn(__dsub_rn(q[d], q[b]), q[cc]), q[a]);
+  }
+};
+
+__global__ void __launch_bounds__(SAT_TPB) select_roi_sat_kernel(const SelectParams p) {
+  const int s = blockIdx.x;
+  const float* dense = p.dense + (size_t)s * p.dense_stride;
+  int32_t* region_out = p.region_out + 6 * s;
+  mwb_trace_t* tr = p.trace + s;
+  const int D = p.D, Lx = p.sL[0], Ly = p.sL[1], sl0x = p.sl0[0], sl0y = p.sl0[1];
+  const int ly1 = Ly + 1, n_cells = Lx * Ly;
+  extern __shared__ __align__(16) unsigned char smem_sat[];
+  double* ts = reinterpret_cast<double*>(smem_sat);
+  double* tq = ts + (size_t)(Lx + 1) * ly1;
+  int* tc = reinterpret_cast<int*>(tq + (size_t)(Lx + 1) * ly1);
+  __shared__ double red_d[SAT_TPB / 32];
+  __shared__ int red_i[SAT_TPB / 32];
+  __shared__ float red_f[2][SAT_TPB / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // stage: each cell's value (NaN when it holds none) into the sum table's
+  // interior, then the breast box's count, sum (fixed order) and min / max
+  float mn = INFINITY, mx = -INFINITY;
+  double sm = 0.0;
+  int cnt = 0;
+#pragma unroll 4
+  for (int i = tid; i < n_cells; i += SAT_TPB) {
+    const int lx = i / Ly, ly = i - lx * Ly;
+    const size_t slot = (size_t)(sl0x + lx) * D * p.ny + (size_t)(sl0y + ly) * D;
+    const uint8_t okb = __ldg(p.valid + slot);  // both loads issued back to back
+    const float raw = __ldg(dense + slot);       // (unwritten cells are never used)
+    const bool ok = okb != 0;
+    const float v = ok ? raw : 0.f;
+    ts[(lx + 1) * ly1 + ly + 1] = ok ? (double)v : __longlong_as_double(0x7ff8000000000000LL);
+    if (ok) {
+      ++cnt;
+      sm += (double)v;
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) {
+    red_d[warp] = sm;
+    red_i[warp] = cnt;
+    red_f[0][warp] = mn;
+    red_f[1][warp] = mx;
+  }
+  __syncthreads();
+  double n_all = 0.0, s_all = 0.0;
+  mn = INFINITY;
+  mx = -INFINITY;
+  for (int w = 0; w < SAT_TPB / 32; ++w) {  // every thread, same order
+    n_all += (double)red_i[w];
+    s_all += red_d[w];
+    mn = fminf(mn, red_f[0][w]);
+    mx = fmaxf(mx, red_f[1][w]);
+  }
+  if (n_all == 0.0 || mx == mn) {  // coarse2fine.py:186-192
+    if (tid == 0) {
+      tr->termination = n_all == 0.0 ? MWB_TERM_EMPTY : MWB_TERM_DEGENERATE;
+      tr->n_records = 0;
+      put_box(tr->final_region, p.breast);
+      put_box(region_out, p.breast);
+    }
+    return;
+  }
+  const double c0 = s_all / n_all;  // the shift
+  // interior entries -> (count, x - c0, (x - c0)^2); zero borders
+  for (int i = tid; i < (Lx + 1) * ly1; i += SAT_TPB) {
+    const int x = i / ly1, y = i - x * ly1;
+    if (x == 0 || y == 0) {
+      ts[i] = 0.0;
+      tq[i] = 0.0;
+      tc[i] = 0;
+    } else {
+      const double v = ts[i];
+      const bool ok = v == v;
+      const double d = ok ? __dsub_rn(v, c0) : 0.0;
+      ts[i] = d;
+      tq[i] = __dmul_rn(d, d);
+      tc[i] = ok ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  for (int x = tid + 1; x <= Lx; x += SAT_TPB) {  // prefix along y, one row per thread
+    double a = 0.0, b = 0.0;
+    int k = 0;
+    for (int y = 1; y <= Ly; ++y) {
+      const int i = x * ly1 + y;
+      a = __dadd_rn(a, ts[i]);
+      b = __dadd_rn(b, tq[i]);
+      k += tc[i];
+      ts[i] = a;
+      tq[i] = b;
+      tc[i] = k;
+    }
+  }
+  __syncthreads();
+  for (int y = tid + 1; y <= Ly; y += SAT_TPB) {  // then along x, one column per thread
+    double a = 0.0, b = 0.0;
+    int k = 0;
+    for (int x = 1; x <= Lx; ++x) {
+      const int i = x * ly1 + y;
+      a = __dadd_rn(a, ts[i]);
+      b = __dadd_rn(b, tq[i]);
+      k += tc[i];
+      ts[i] = a;
+      tq[i] = b;
+      tc[i] = k;
+    }
+  }
+  __syncthreads();
+  if (warp != 0) return;
+
+  const SatView T{tc, ts, tq, ly1};
+  // lattice-index box of a cell box, relative to the staged origin
+  auto lat = [&](const Box& r, int& x0, int& y0, int& x1, int& y1) {
+    x0 = (r.lo[0] + D - 1) / D - sl0x;
+    x1 = r.hi[0] / D - sl0x;
+    y0 = (r.lo[1] + D - 1) / D - sl0y;
+    y1 = r.hi[1] / D - sl0y;
+  };
+  // the selection's statistics: n, shifted sum, m2 (one-pass on shifted data)
+  double n_sel, sum_sel, m2_sel;
+  {
+    int x0, y0, x1, y1;
+    lat(p.breast, x0, y0, x1, y1);
+    double Q;
+    T.box(x0, y0, x1, y1, n_sel, sum_sel, Q);
+    m2_sel = fmax(__dsub_rn(Q, __dmul_rn(__ddiv_rn(sum_sel, n_sel), sum_sel)), 0.0);
+  }
+  // Iterations, lane-parallel: lane k < 4 owns child quadrant k, lane 4 + k
+  // its expansion (expand_box of child k within the selection); every other
+  // quantity is warp-uniform.  The arithmetic is select_score's (Eq. (5),
+  // np.argmax ties to the lower index, the n_min stop, W/B with the OR test).
+  int sx0 = p.breast.lo[0], sy0 = p.breast.lo[1], sx1 = p.breast.hi[0], sy1 = p.breast.hi[1];
+  double sigma_prev_sq = m2_sel / n_sel;
+  double prev_w = 0.0, prev_b = 0.0;
+  bool have_prev = false;
+  int iteration = 0, term = MWB_TERM_NONE;
+  const int kq = lane & 3;
+  while (true) {
+    const int wx = sx1 - sx0 + 1, wy = sy1 - sy0 + 1;
+    if (wx < 2 || wy < 2) {  // Region.quadrants() is None (geometry.py:233-234)
+      term = MWB_TERM_REGION_FLOOR;
+      break;
+    }
+    const int mxs = sx0 + (wx + 1) / 2 - 1, mys = sy0 + (wy + 1) / 2 - 1;  // last cells of the low halves
+    // child kq (index = xhigh + 2 yhigh, geometry.py:235-240)
+    int bx0 = (kq & 1) ? mxs + 1 : sx0, bx1 = (kq & 1) ? sx1 : mxs;
+    int by0 = (kq & 2) ? mys + 1 : sy0, by1 = (kq & 2) ? sy1 : mys;
+    const int cx0 = bx0, cy0 = by0, cx1 = bx1, cy1 = by1;
+    if (lane >= 4) {  // its expansion: ceil(f * side) per axis, clipped (geometry.py:244-257)
+      const int gx = (int)ceil(__dmul_rn(p.frac, (double)(bx1 - bx0 + 1)));
+      const int gy = (int)ceil(__dmul_rn(p.frac, (double)(by1 - by0 + 1)));
+      bx0 = max(bx0 - gx, sx0);
+      bx1 = min(bx1 + gx, sx1);
+      by0 = max(by0 - gy, sy0);
+      by1 = min(by1 + gy, sy1);
+    }
+    double bn = 0.0, bs = 0.0, bm2 = 0.0, bmu = 0.0;
+    if (lane < 8) {
+      double Q;
+      T.box((bx0 + D - 1) / D - sl0x, (by0 + D - 1) / D - sl0y, bx1 / D - sl0x, by1 / D - sl0y, bn, bs, Q);
+      if (bn > 0.0) {
+        const double ms = __ddiv_rn(bs, bn);  // shifted mean
+        bmu = __dadd_rn(c0, ms);
+        bm2 = fmax(__dsub_rn(Q, __dmul_rn(ms, bs)), 0.0);  // Q - S^2 / n
+      }
+    }
+    // lanes 0..3: scores (coarse2fine.py:212-224)
+    int has = 0, clamped = 0;
+    double var = 0.0, dr = 0.0, dl = 0.0, sc = -INFINITY;
+    if (lane < 4 && bn > 0.0) {
+      var = __ddiv_rn(bm2, bn);
+      if (iteration == 0) {
+        sc = var;
+        has = 1;
+      } else {
+        has = 2;
+        if (var == 0.0) {
+          sc = bmu;
+        } else {
+          dr = __ddiv_rn(__dsub_rn(var, sigma_prev_sq), var);
+          dl = fmin(fmax(dr, 0.0), 1.0);
+          sc = __dadd_rn(__dmul_rn(__dsub_rn(1.0, dl), bmu), __dmul_rn(dl, var));
+          clamped = dl != dr;
+        }
+      }
+    }
+    mwb_iter_record_t* rec = iteration < MWB_MAX_ITERS ? &tr->records[iteration] : nullptr;
+    if (rec && lane < MWB_MAX_CHILDREN) {
+      const bool kid = lane < 4;
+      rec->counts[lane] = kid ? (int)bn : 0;
+      rec->has_stats[lane] = has;
+      rec->clamped[lane] = clamped;
+      rec->scores[lane] = kid ? sc : 0.0;
+      rec->mu[lane] = kid ? bmu : 0.0;
+      rec->var[lane] = var;
+      rec->delta_raw[lane] = dr;
+      rec->delta[lane] = dl;
+    }
+    // np.argmax over the 4 scores: larger wins, ties to the lower index
+    double best = lane < 4 ? sc : -INFINITY;
+    int selq = lane < 4 ? lane : 0x7FFF;
+#pragma unroll
+    for (int o = 2; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oq = __shfl_xor_sync(0xffffffffu, selq, o);
+      if (ob > best || (ob == best && oq < selq)) {
+        best = ob;
+        selq = oq;
+      }
+    }
+    selq = __shfl_sync(0xffffffffu, selq, 0);
+    if (selq >= 4) selq = 0;  // every score -inf: argmax returns 0
+    const double n_q = __shfl_sync(0xffffffffu, bn, selq);
+    if (n_q < (double)p.n_min) {  // coarse2fine.py:227-229
+      term = MWB_TERM_N_MIN;
+      break;
+    }
+    const int e = 4 + selq;
+    const double n_e = __shfl_sync(0xffffffffu, bn, e), sum_e = __shfl_sync(0xffffffffu, bs, e);
+    const double m2_e = __shfl_sync(0xffffffffu, bm2, e);
+    // W, B of the previous vs the new selection (class_distances, 94-109)
+    const double w = __dadd_rn(m2_sel, m2_e);
+    const double ma = __ddiv_rn(sum_sel, n_sel), mb = __ddiv_rn(sum_e, n_e);
+    const double grand = __ddiv_rn(__dadd_rn(sum_sel, sum_e), __dadd_rn(n_sel, n_e));
+    const double da = __dsub_rn(ma, grand), db = __dsub_rn(mb, grand);
+    const double b = __dadd_rn(__dmul_rn(n_sel, __dmul_rn(da, da)), __dmul_rn(n_e, __dmul_rn(db, db)));
+    const bool satisfied = !have_prev || (b > prev_b || w < prev_w);  // OR (235)
+    const int ex0 = __shfl_sync(0xffffffffu, bx0, e), ey0 = __shfl_sync(0xffffffffu, by0, e);
+    const int ex1 = __shfl_sync(0xffffffffu, bx1, e), ey1 = __shfl_sync(0xffffffffu, by1, e);
+    if (rec && lane == selq) {  // the selected child's lane holds its box
+      const Box cb{{cx0, cy0, 0}, {cx1, cy1, 0}};
+      put_box(rec->selected_region, cb);
+    }
+    if (rec && lane == 0) {
+      rec->iteration = iteration + 1;
+      rec->n_children = 4;
+      rec->selected = selq;
+      rec->satisfied = satisfied;
+      put_box(rec->expanded_region, Box{{ex0, ey0, 0}, {ex1, ey1, 0}});
+      rec->w = w;
+      rec->b = b;
+    }
+    if (!rec) {
+      term = MWB_TERM_OVERFLOW;
+      break;
+    }
+    iteration += 1;
+    if (!satisfied) {
+      term = MWB_TERM_DISTANCE;
+      break;
+    }
+    prev_w = w;
+    prev_b = b;
+    have_prev = true;
+    n_sel = n_e;
+    sum_sel = sum_e;
+    m2_sel = m2_e;
+    sigma_prev_sq = m2_sel / n_sel;
+    sx0 = ex0;
+    sy0 = ey0;
+    sx1 = ex1;
+    sy1 = ey1;
+  }
+  const Box sel{{sx0, sy0, 0}, {sx1, sy1, 0}};
+  if (lane == 0) {
+    tr->termination = term;
+    tr->n_records = min(iteration, MWB_MAX_ITERS);
+    put_box(tr->final_region, sel);
+    put_box(region_out, sel);
+  }
+}
