@@ -479,6 +479,12 @@ int mwb_compact_payload(const double* payload, int m, int n, int ld, float* out,
 int mwb_render_pgm(const void* values, int value_bits, const uint8_t* valid, int n_maps, int nx, int ny,
                    int64_t map_stride, int stride, double* vrange, uint8_t* raster, void* stream);
 
+/* Compact readback of a framework composite: out[i] = dense[coarse_slots[i]]
+ * for i < n_coarse, then the device box region {x0, y0, z0, x1, y1, z1}'s
+ * cells row by row (ix-major), at most cap values in all. */
+int mwb_gather_composite(const float* dense, int ny, const int32_t* coarse_slots, int n_coarse,
+                         const int32_t* region, float* out, int64_t cap, void* stream);
+
 /* Stream-ordered copy of `bytes` between any two CUDA-visible addresses
  * (cudaMemcpyDefault): the drop-in's per-call signal-slot refill and result
  * readback without a framework op per copy. */

@@ -185,6 +185,7 @@ _SIGNATURES = {
          _I, _P, _I64, _P],
         _I,
     ),
+    "mwb_gather_composite": ([_P, _I, _P, _I, _P, _P, _I64, _P], _I),
     "mwb_memcpy_async": ([_P, _P, _I64, _P], _I),
     "mwb_elapsed_ms": ([_P, _I, _P], _I),
     "mwb_compact_payload": ([_P, _I, _I, _I, _P, _P, _P, _P, _P], _I),

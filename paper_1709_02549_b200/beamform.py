@@ -124,6 +124,28 @@ class EnergyMap:
             raise ValueError("energy map contains non-finite values")
         return em
 
+    @classmethod
+    def _from_loader(cls, grid, loader, stride: int = 1, roi=None, split: int = 0):
+        """Dense-backed map whose (values, valid) arrays come from ``loader()``
+        on first use (device-checked finite).  The framework's latency path
+        returns such a map, so a caller that reads only the report never pays
+        for building the dense arrays."""
+        em = cls.__new__(cls)
+        em.grid, em.stride, em.roi = grid, stride, roi
+        em._entries = None
+        em._split = split
+        em._loader = loader
+        return em
+
+    def __getattr__(self, name):
+        # only reached when the attribute is missing: a loader-backed map
+        # materialises its dense arrays on the first access
+        if name in ("_values", "_valid") and "_loader" in self.__dict__:
+            vals, valid = self.__dict__.pop("_loader")()
+            self._values, self._valid = vals, valid
+            return vals if name == "_values" else valid
+        raise AttributeError(name)
+
     # -- entries -----------------------------------------------------------
     def _cells_in_order(self) -> tuple[np.ndarray, np.ndarray]:
         ix, iy = np.nonzero(self._valid)
@@ -145,6 +167,7 @@ class EnergyMap:
     def entries(self, value: dict) -> None:
         self._entries = value
         self._values = self._valid = None
+        self.__dict__.pop("_loader", None)
 
     def __len__(self) -> int:
         if self._entries is None:

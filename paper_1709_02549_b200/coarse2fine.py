@@ -20,6 +20,7 @@ Drop-in for /root/reference/pkg/src/mwbeam/coarse2fine.py:
 from __future__ import annotations
 
 import ctypes
+import functools
 
 import math
 from dataclasses import dataclass, field
@@ -411,19 +412,19 @@ class _FrameworkPlan(dv.GraphPlan):
         self.mask_np, self.mask_t = _breast_mask_device(grid)
         self.full_equivalent = int(self.mask_np.sum())  # the report's full-resolution cell count (fixed per plan)
         dev = dv.device()
-        # One device result block, read back with ONE copy per call into a
-        # fresh pinned block that the returned map and report keep (no host
-        # copy): [status | trace | dense fp32 (only valid cells are read) | valid]
+        # The kernels write a dense map and its valid mask; what a call reads
+        # back is one result block [status | trace | compact values], the
+        # compact values being the coarse lattice's followed by the final
+        # ROI rectangle's, row by row (mwb_gather_composite): a few KB instead
+        # of the whole map.  One copy per call into a fresh pinned block that
+        # the returned map keeps; the host rebuilds the dense arrays only when
+        # the map is first read (EnergyMap._from_loader).
         n = nx * ny
+        self.dense = torch.empty(n, dtype=torch.float32, device=dev)  # only valid cells are read
+        self.valid = torch.empty(n, dtype=torch.uint8, device=dev)
         self._o_trace = _Status.BYTES
-        self._o_dense = (self._o_trace + nat.TRACE_BYTES + 15) // 16 * 16
-        self._o_valid = self._o_dense + 4 * n
-        self._res_bytes = self._o_valid + n
-        self.res = torch.empty(self._res_bytes, dtype=torch.uint8, device=dev)
-        self.status = _Status(self.res)
-        self.trace_t = self.res[self._o_trace: self._o_trace + nat.TRACE_BYTES]
-        self.dense = self.res[self._o_dense: self._o_valid].view(torch.float32)
-        self.valid = self.res[self._o_valid:]
+        self._o_vals = (self._o_trace + nat.TRACE_BYTES + 15) // 16 * 16
+        self._res_full = self._o_vals  # + 4 * (n_coarse + n), set below
         self.region_t = torch.empty(6, dtype=torch.int32, device=dev)
         # external events become timestamp nodes inside the captured graph
         self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
@@ -445,6 +446,21 @@ class _FrameworkPlan(dv.GraphPlan):
                  self.c_count.data_ptr(), self.c_valid.data_ptr(), ws.data_ptr(), dv.stream_handle())
         self.c_table = build_table(scan, self.c_pts, p_max, interp, self.c_count.data_ptr())
         self.n_coarse = int(self.c_count.item())
+        self.c_slots = self.c_oidx[: self.n_coarse].clone()
+        self.c_slots_host = self.c_slots.cpu().numpy()
+        self.c_valid_host = self.c_valid.cpu().numpy().view(bool).reshape(nx, ny)
+        self.lattice_host = np.zeros((nx, ny), dtype=bool)
+        self.lattice_host[::d, ::d] = True
+        # result block: device copy sized for the worst case (a degenerate run's
+        # whole-grid ROI); a call copies the coarse values and ROI_BUDGET ROI
+        # cells, and a second copy only when the ROI is larger
+        cap = self.n_coarse + nx * ny
+        self._res_full = self._o_vals + 4 * cap
+        self._res_copy = self._o_vals + 4 * min(cap, self.n_coarse + self.ROI_BUDGET)
+        self.res = torch.empty(self._res_full, dtype=torch.uint8, device=dev)
+        self.status = _Status(self.res)
+        self.trace_t = self.res[self._o_trace: self._o_trace + nat.TRACE_BYTES]
+        self.compact = self.res[self._o_vals:].view(torch.float32)
         # Fine pass: every masked cell of the grid in the padded 16 x 16 tile
         # layout with its delay table, also built once here; each call's fine
         # launch (mwb_energies_region) evaluates just the tiles that meet the
@@ -494,13 +510,33 @@ class _FrameworkPlan(dv.GraphPlan):
                  self.valid.data_ptr(), st.count_ptr(1), self.mode, nat.ptr(self.f_ws),
                  0 if self.f_ws is None else self.f_ws.numel(), dv.stream_handle())
         ev[3].record()
+        nat.call("mwb_gather_composite", self.dense.data_ptr(), g.dims[1], self.c_slots.data_ptr(), self.n_coarse,
+                 self.region_t.data_ptr(), self.compact.data_ptr(), self.compact.numel(), dv.stream_handle())
+
+    ROI_BUDGET = 16384  # ROI cells read back with the result block (64 KB)
+
+    def _dense_arrays(self, comp: np.ndarray, final: Region) -> tuple[np.ndarray, np.ndarray]:
+        """(values, valid) of a composite from its compact readback: coarse
+        lattice cells from their fixed slots, fine cells = the ROI's masked
+        non-lattice cells (the fine pass's filter, mwb_energies_region)."""
+        nx, ny = self.grid.dims
+        (x0, y0), (x1, y1) = final.min_cell, final.max_cell
+        vals = np.zeros(nx * ny, dtype=np.float32)
+        vals[self.c_slots_host] = comp[: self.n_coarse]
+        vals = vals.reshape(nx, ny)
+        valid = self.c_valid_host.copy()
+        fine = self.mask_np[x0: x1 + 1, y0: y1 + 1] & ~self.lattice_host[x0: x1 + 1, y0: y1 + 1]
+        block = comp[self.n_coarse:].reshape(x1 - x0 + 1, y1 - y0 + 1)
+        vals[x0: x1 + 1, y0: y1 + 1][fine] = block[fine]
+        valid[x0: x1 + 1, y0: y1 + 1] |= fine
+        return vals, valid
 
     def launch(self, scan: dv.DeviceScan) -> None:
         """Enqueue one run on ``scan`` (graph replay after the first call) and the readback."""
         self.replay(scan)
         self.replays += 1
-        self.h_res = torch.empty(self._res_bytes, dtype=torch.uint8, pin_memory=self._pin)
-        nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), self._res_bytes,
+        self.h_res = torch.empty(self._res_full, dtype=torch.uint8, pin_memory=self._pin)
+        nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), self._res_copy,
                  dv.stream_handle())
 
     def finish(self) -> tuple[EnergyMap, FrameworkReport]:
@@ -517,9 +553,15 @@ class _FrameworkPlan(dv.GraphPlan):
         n_coarse, n_fine = self.n_coarse, int(counts[1])
         EVAL_COUNTER.add(n_coarse)
         EVAL_COUNTER.add(n_fine)
-        vals = blk[self._o_dense: self._o_valid].view(np.float32).reshape(nx, ny)
-        vmask = blk[self._o_valid:].view(bool).reshape(nx, ny)
-        composite = EnergyMap._from_dense(self.grid, vals, vmask, stride=self.d, roi=final, split=self.d, checked=True)
+        (x0, y0), (x1, y1) = final.min_cell, final.max_cell
+        used = self._o_vals + 4 * (self.n_coarse + (x1 - x0 + 1) * (y1 - y0 + 1))
+        if used > self._res_copy:  # ROI beyond the budget: the rest of the block
+            nat.call("mwb_memcpy_async", self.h_res.data_ptr() + self._res_copy, self.res.data_ptr() + self._res_copy,
+                     used - self._res_copy, dv.stream_handle())
+            torch.cuda.current_stream().synchronize()
+        comp = blk[self._o_vals: used].view(np.float32)
+        composite = EnergyMap._from_loader(self.grid, functools.partial(self._dense_arrays, comp, final),
+                                           stride=self.d, roi=final, split=self.d)
         if self._ev_handles is None:
             self._ev_handles = (ctypes.c_void_p * 4)(*[e.cuda_event for e in self.events])
         nat.call("mwb_elapsed_ms", self._ev_handles, 4, self._ms)
