@@ -226,7 +226,10 @@ def _upload_mask3(mask, dims) -> torch.Tensor | None:
     m = np.asarray(mask, dtype=bool)
     if m.shape != tuple(dims):
         raise ValueError(f"mask must have the grid's dims {tuple(dims)}, got {m.shape}")
-    return torch.from_numpy(np.ascontiguousarray(m).view(np.uint8).reshape(-1)).to(dv.device())
+    flat = np.ascontiguousarray(m).view(np.uint8).reshape(-1)
+    if not flat.flags.writeable:  # read-only masks (hemisphere_mask): torch wants a writable buffer
+        flat = flat.copy()
+    return torch.from_numpy(flat).to(dv.device())
 
 
 def image_volume(ds, kinds, grid: VolumeGrid, box: Box | None = None, stride: int = 1, mask=None,
