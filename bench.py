@@ -721,7 +721,10 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32",
+            "vs_baseline": None,
+            # arithmetic of the measured kernel: tcgen05 kind::f16 with fp16 hi/lo-split operands (3 products)
+            # accumulating in fp32 TMEM, or fp32 FFMA on the CUDA-core path
+            "dtype": "f16x3-split/f32-acc" if bi.uses_tensor_cores else "f32",
             "data": "synthetic: seeded differentiated-Gaussian scans (BASELINE configs[3] signal model) synthesised "
                     "on the device by mwb_simulate, no dataset",
             "config": config_block(args, world),

@@ -135,3 +135,26 @@ def test_images_pair_equals_image():
     pair = mw.images(ds, ("das", "dmas"), grid, stride=2, window=(model.k0, 32))
     for kind in ("das", "dmas"):
         assert pair[kind].entries == mw.image(ds, kind, grid, stride=2, window=(model.k0, 32)).entries
+
+
+def test_end_to_end_ramp_and_buffer_reuse_smem_mode():
+    """__call__ with S >= 6 * chunk (the ramped chunk sizes) and more chunks
+    than buffer sets, on the CUDA-core kernel: bit-identical to run_device
+    (tests/test_gpu_bench_path.py covers the tensor-core mode)."""
+    from paper_1709_02549_b200.batch import _chunk_ranges
+
+    model = synth.ScanModel()
+    sig, _ = synth.batch_2d(model, list(range(100, 196)))
+    grid = synth.grid_square(0.12, 48)
+    bi = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=(model.k0, model.window),
+                     mode="smem")
+    assert len(_chunk_ranges(96, 16)) > 4 and _chunk_ranges(96, 16)[0] == (0, 4)
+    res = bi(torch.from_numpy(sig).pin_memory(), kinds=("das", "dmas"), chunk=16)
+    sig_d = bi.to_device_layout(sig)
+    n = grid.dims[0] * grid.dims[1]
+    for kind in ("das", "dmas"):
+        out = torch.empty((96, n), dtype=torch.float32, device="cuda")
+        keys = torch.zeros(96, dtype=torch.int64, device="cuda")
+        bi.run_device(sig_d, **{f"out_{kind}": out, f"key_{kind}": keys})
+        assert torch.equal(res.maps[kind].reshape(96, -1), out.cpu())
+        assert np.array_equal(res.argmax[kind], bi.decode_keys(keys.cpu().numpy().view(np.uint64)))
