@@ -490,6 +490,18 @@ int mwb_gather_composite(const float* dense, int ny, const int32_t* coarse_slots
  * readback without a framework op per copy. */
 int mwb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
+/* Stream-ordered 2-D copy (cudaMemcpy2DAsync, cudaMemcpyDefault): `height`
+ * rows of `width` bytes, row pitches in bytes. */
+int mwb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
+                       void* stream);
+
+/* The samples mwb_energies_tc reads from each channel row for a window start
+ * k0 and a window-offset range (j_lo, j_count), rows of ld samples: out[0] =
+ * the first sample, out[1] = the count (the Gram and fp16-plane pre-passes
+ * read exactly [out[0], out[0] + out[1]); samples past ld read as zeros).  A
+ * host-to-device pipeline may ship only that range of each row. */
+int mwb_tc_sample_range(int k0, int j_lo, int j_count, int ld, int32_t* out);
+
 /* Elapsed milliseconds between consecutive recorded events: out_ms[i] =
  * events[i] -> events[i + 1] for i < n_events - 1 (the framework report's
  * phase timings in one call). */

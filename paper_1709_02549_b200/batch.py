@@ -16,6 +16,7 @@ CUDA streams.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -224,6 +225,22 @@ class BatchImager:
             self.mode, dv.stream_handle(),
         )
 
+    def input_range(self) -> tuple[int, int]:
+        """(first, count): the samples of each channel row the device path
+        reads.  The tensor-core path reads only the window offsets its delay
+        table uses ([k0 + j_lo, + Lp), mwb_tc_sample_range), so the
+        end-to-end pipeline ships just that part of every row; the CUDA-core
+        path takes whole rows."""
+        if self.mode != 2 or self.table is None:
+            return 0, self.n_samples
+        out = (ctypes.c_int32 * 2)()
+        nat.call("mwb_tc_sample_range", self.k0, self.j_lo, self.j_count, self.ld, out)
+        return int(out[0]), int(out[1])
+
+    def h2d_bytes(self, n_scans: int) -> int:
+        """Host-to-device bytes ``__call__`` copies for ``n_scans`` scans."""
+        return 4 * n_scans * self.n_chan * self.input_range()[1]
+
     def decode_keys(self, keys: np.ndarray) -> np.ndarray:
         ny = self.grid.dims[1]
         slot = 0xFFFFFFFF - (keys.astype(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.int64)
@@ -276,6 +293,11 @@ class BatchImager:
         for st in (s_in, s_cmp, s_out):
             st.wait_stream(main)
         ev_in = [torch.cuda.Event() for _ in range(n_chunks)]
+        first, count = self.input_range()
+        row_floats = self.n_chan * self.n_samples
+        if not host.is_contiguous():
+            host = host.contiguous()
+        st_in = s_in.cuda_stream
         ev_cmp = [torch.cuda.Event() for _ in range(n_chunks)]
         ev_out = [torch.cuda.Event() for _ in range(n_chunks)]
         for i, (a, b) in enumerate(ranges):
@@ -284,7 +306,10 @@ class BatchImager:
             with torch.cuda.stream(s_in):
                 if i >= nbuf:
                     s_in.wait_event(ev_cmp[i - nbuf])
-                dev_in[buf][:n].copy_(host[a:b], non_blocking=True)
+                # the rows' sample range the kernels read, one 2-D copy per chunk
+                nat.call("mwb_memcpy2d_async", dev_in[buf].data_ptr() + 4 * first, 4 * self.ld,
+                         host.data_ptr() + 4 * (a * row_floats + first), 4 * self.n_samples, 4 * count,
+                         n * self.n_chan, st_in)
                 ev_in[i].record(s_in)
             with torch.cuda.stream(s_cmp):
                 s_cmp.wait_event(ev_in[i])

@@ -1367,6 +1367,24 @@ int mwb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
   return e == cudaSuccess ? MWB_OK : set_err(MWB_ECUDA, "cudaMemcpyAsync: %s", cudaGetErrorString(e));
 }
 
+int mwb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
+                       void* stream) {
+  if (width < 0 || height < 0 || dpitch < width || spitch < width || ((width && height) && (!dst || !src)))
+    return set_err(MWB_EINVAL, "mwb_memcpy2d_async: bad arguments");
+  if (!width || !height) return MWB_OK;
+  const cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)height,
+                                          cudaMemcpyDefault, reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? MWB_OK : set_err(MWB_ECUDA, "cudaMemcpy2DAsync: %s", cudaGetErrorString(e));
+}
+
+int mwb_tc_sample_range(int k0, int j_lo, int j_count, int ld, int32_t* out) {
+  if (!out || k0 < 0 || j_lo < 0 || j_count < 16 || ld < 1) return set_err(MWB_EINVAL, "mwb_tc_sample_range: bad arguments");
+  const long long first = (long long)k0 + j_lo, len = tc_plane_len(j_count);
+  out[0] = (int32_t)std::min<long long>(first, ld);
+  out[1] = (int32_t)std::max<long long>(0, std::min<long long>(len, ld - first));
+  return MWB_OK;
+}
+
 int mwb_elapsed_ms(void* const* events, int n_events, float* out_ms) {
   if (n_events < 2 || !events || !out_ms) return set_err(MWB_EINVAL, "mwb_elapsed_ms: bad arguments");
   for (int i = 0; i + 1 < n_events; ++i) {
