@@ -299,9 +299,13 @@ class _Status:
 
     def read(self, host: np.ndarray | None = None) -> tuple[np.ndarray, np.ndarray, int]:
         """Decode the block; ``host`` is an already-copied image of ``self.t``."""
-        h = self.t.cpu().numpy() if host is None else host
-        keys = h[: self.N_KEYS].view(np.uint64)
-        tail = h[self.N_KEYS :].view(np.int32)
+        return self.decode(self.t.cpu().numpy() if host is None else host)
+
+    @classmethod
+    def decode(cls, h: np.ndarray) -> tuple[np.ndarray, np.ndarray, int]:
+        """(argmax keys, counts, flags) from a host int64 image of the block."""
+        keys = h[: cls.N_KEYS].view(np.uint64)
+        tail = h[cls.N_KEYS :].view(np.int32)
         return keys, tail[:2], int(tail[2])
 
 

@@ -25,6 +25,7 @@ result once.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import hashlib
 import math
 from collections import OrderedDict
@@ -177,13 +178,35 @@ class _SegmentPlan(dv.GraphPlan):
         self.trace_t = torch.zeros(nat.SEG_TRACE_BYTES, dtype=torch.uint8, device=dev)
         self.dense = torch.empty(nx * ny, dtype=torch.float32, device=dev)  # only valid cells are read
         self.valid = torch.empty(nx * ny, dtype=torch.uint8, device=dev)
-        self.status = _Status()
         self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)]
         pin = torch.cuda.is_available()
-        self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=pin)
-        self.h_trace = torch.empty(nat.SEG_TRACE_BYTES, dtype=torch.uint8, pin_memory=pin)
-        self._pin = pin  # map buffers are fresh pinned blocks per call (handed to the EnergyMap, no host copy)
-        self.h_lowres = torch.empty(n_low, dtype=torch.float32, pin_memory=pin)
+        self._pin = pin
+        self.full_eq = int(mask_np.sum()) if mask_np is not None else nx * ny
+        # one result block read back with one copy per call (region-tree path):
+        # [status | trace | low-res map | the final region's rectangle, row by
+        # row (mwb_gather_composite)], sized for the worst case (the whole
+        # start region); a call copies up to a budget of rectangle cells
+        self._o_trace = _Status.BYTES
+        self._o_low = (self._o_trace + nat.SEG_TRACE_BYTES + 15) // 16 * 16
+        self._o_roi = self._o_low + 4 * n_low
+        rx0, ry0, rx1, ry1 = region.bounds()
+        cap = (rx1 - rx0 + 1) * (ry1 - ry0 + 1)
+        self._res_full = self._o_roi + 4 * cap
+        self._res_copy = self._o_roi + 4 * min(cap, self.ROI_BUDGET)
+        self.res = torch.empty(self._res_full, dtype=torch.uint8, device=dev)
+        self.status = _Status(self.res)
+        self.roi_t = self.res[self._o_roi:].view(torch.float32)
+        if tree is not None:
+            self.trace_t = self.res[self._o_trace: self._o_trace + nat.SEG_TRACE_BYTES]
+            self.lowres = self.res[self._o_low: self._o_roi].view(torch.float32)
+        else:
+            self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=pin)
+            self.h_trace = torch.empty(nat.SEG_TRACE_BYTES, dtype=torch.uint8, pin_memory=pin)
+            self.h_lowres = torch.empty(n_low, dtype=torch.float32, pin_memory=pin)
+        self._ms = (C.c_float * 2)()
+        self._ev_handles = None
+
+    ROI_BUDGET = 4096  # final-region cells read back with the result block (a 1 cm segment at 0.25 mm: 1600)
 
     def _enqueue(self) -> None:
         sc, grid = self.scan, self.grid
@@ -202,6 +225,8 @@ class _SegmentPlan(dv.GraphPlan):
                      self.dense.data_ptr(), nx * ny, self.status.key_ptr(0 if das else 1), self.status.count_ptr(0),
                      self.status.flags_ptr, self.ws.data_ptr(), dv.stream_handle())
             ev[1].record()
+            nat.call("mwb_gather_composite", self.dense.data_ptr(), ny, None, 0, self.region_t.data_ptr(),
+                     self.roi_t.data_ptr(), self.roi_t.numel(), dv.stream_handle())
             return
         self.valid.zero_()
         ev[0].record()
@@ -218,6 +243,11 @@ class _SegmentPlan(dv.GraphPlan):
     def launch(self, scan: dv.DeviceScan) -> None:
         self.replay(scan)
         nx, ny = self.grid.dims
+        if self.tree is not None:
+            self.h_res = torch.empty(self._res_full, dtype=torch.uint8, pin_memory=self._pin)
+            nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), self._res_copy,
+                     dv.stream_handle())
+            return
         self.h_dense = torch.empty(nx * ny, dtype=torch.float32, pin_memory=self._pin)
         if self.tree is None:
             self.h_valid = torch.empty(nx * ny, dtype=torch.uint8, pin_memory=self._pin)
@@ -228,7 +258,22 @@ class _SegmentPlan(dv.GraphPlan):
         for src, dst in pairs:
             dst.copy_(src, non_blocking=True)
 
+    def _roi_arrays(self, block: np.ndarray, final: Region) -> tuple[np.ndarray, np.ndarray]:
+        """(values, valid) of the fine map from the final region's rectangle:
+        the region's cells that pass the mask."""
+        nx, ny = self.grid.dims
+        (x0, y0), (x1, y1) = final.min_cell, final.max_cell
+        vals = np.zeros((nx, ny), dtype=np.float32)
+        valid = np.zeros((nx, ny), dtype=bool)
+        vals[x0: x1 + 1, y0: y1 + 1] = block.reshape(x1 - x0 + 1, y1 - y0 + 1)
+        valid[x0: x1 + 1, y0: y1 + 1] = True
+        if self.mask_np is not None:
+            valid &= self.mask_np
+        return vals, valid
+
     def finish(self, kind) -> tuple[EnergyMap, SegmentReport]:
+        if self.tree is not None:
+            return self._finish_block(kind)
         torch.cuda.current_stream().synchronize()
         grid = self.grid
         nx, ny = grid.dims
@@ -255,7 +300,7 @@ class _SegmentPlan(dv.GraphPlan):
             cell = (slot // ny, slot % ny)
         else:
             cell = (final.min_cell[0], final.min_cell[1])
-        full_eq = int(self.mask_np.sum()) if self.mask_np is not None else nx * ny
+        full_eq = self.full_eq
         ev = self.events
         if self.tree is None:
             t_s, t_f = ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3
@@ -268,6 +313,44 @@ class _SegmentPlan(dv.GraphPlan):
             subgrid_points_evaluated=4 * n_sub * n_sub * len(records), fine_points_evaluated=n_fine,
             full_equivalent_points=full_eq, argmax_cell=cell, argmax_position=grid.cell_center(*cell),
             elapsed=elapsed)
+        return fine, report
+
+    def _finish_block(self, kind) -> tuple[EnergyMap, SegmentReport]:
+        """The region-tree path: everything from the one result block."""
+        torch.cuda.current_stream().synchronize()
+        grid = self.grid
+        nx, ny = grid.dims
+        blk = self.h_res.numpy()
+        keys, counts, flags = _Status.decode(blk[: _Status.BYTES].view(np.int64))
+        if flags & 1:
+            raise ValueError("energy map contains non-finite values")
+        records, final = _decode_seg_trace(blk[self._o_trace: self._o_trace + nat.SEG_TRACE_BYTES].tobytes())
+        (x0, y0), (x1, y1) = final.min_cell, final.max_cell
+        used = self._o_roi + 4 * (x1 - x0 + 1) * (y1 - y0 + 1)
+        if used > self._res_copy:  # a final region beyond the budget: the rest of the block
+            nat.call("mwb_memcpy_async", self.h_res.data_ptr() + self._res_copy, self.res.data_ptr() + self._res_copy,
+                     used - self._res_copy, dv.stream_handle())
+            torch.cuda.current_stream().synchronize()
+        n_fine = int(counts[0])
+        n_sub = self.n_sub
+        EVAL_COUNTER.add(n_fine + 4 * n_sub * n_sub * len(records))
+        block = blk[self._o_roi: used].view(np.float32)
+        fine = EnergyMap._from_loader(grid, functools.partial(self._roi_arrays, block, final), 1, roi=final)
+        key = int(keys[0 if self.kcode == nat.MWB_DAS else 1])
+        if key:
+            slot = 0xFFFFFFFF - (key & 0xFFFFFFFF)
+            cell = (slot // ny, slot % ny)
+        else:
+            cell = (final.min_cell[0], final.min_cell[1])
+        if self._ev_handles is None:
+            self._ev_handles = (C.c_void_p * 2)(*[e.cuda_event for e in self.events[:2]])
+        nat.call("mwb_elapsed_ms", self._ev_handles, 2, self._ms)
+        report = SegmentReport(
+            kind=_kind(kind).value, n_sub=n_sub, stop_cells=self.stop_cells, records=records, final_region=final,
+            lowres=blk[self._o_low: self._o_roi].view(np.float32).reshape(2 * n_sub, 2 * n_sub).copy(),
+            subgrid_points_evaluated=4 * n_sub * n_sub * len(records), fine_points_evaluated=n_fine,
+            full_equivalent_points=self.full_eq, argmax_cell=cell, argmax_position=grid.cell_center(*cell),
+            elapsed={"total": self._ms[0] / 1e3})
         return fine, report
 
 

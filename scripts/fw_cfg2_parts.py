@@ -63,6 +63,11 @@ for kind in ("das", "dmas"):
         plan.launch(scan)
         torch.cuda.synchronize()
 
+    from paper_1709_02549_b200.segment import segment
+
+    sg = lambda: segment(ds, kind, g2, 16, 0.01, window=w2)
+    sg()
+    print(f"{kind}: segment wall {wall_us(sg):.1f} us (events {dev_ms(sg):.1f})", flush=True)
     print(f"{kind}: run_framework wall {wall_us(fw):.1f} us (events {dev_ms(fw):.1f}), "
           f"launch {wall_us(lambda: plan.launch(scan)):.1f}, launch+sync {wall_us(launch_sync):.1f}; "
           f"elapsed {', '.join(f'{k} {v * 1e6:.1f}' for k, v in rep.elapsed.items())} us; "
