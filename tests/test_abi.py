@@ -188,3 +188,27 @@ def test_segment_plan_info_rejects_huge_trees_and_bad_args(lib):
     assert lib.mwb_segment_plan_info(100, 100, 0, 0, 100, 99, 16, 8, 4, 66, info) != 0  # region outside the grid
     assert lib.mwb_segment_plan_info(100, 100, 0, 0, 99, 99, 0, 8, 4, 66, info) != 0  # n_sub
     assert lib.mwb_segment_run_workspace_bytes(0, 16, 3, 32) == -1
+
+
+def test_round2_entry_points_validate_arguments(lib):
+    """The round-2 entry points reject bad arguments before any CUDA call."""
+    import ctypes
+
+    rc = lib.mwb_energies_region(None, 66, 1024, 1024, None, None, 12, 1.0, None, None, 256, None, None, 0, 0, 32,
+                                 None, None, None, None, None, None, 10, 3, None, None, 0, None, 0, None)
+    assert rc == -1 and b"mwb_energies_region" in lib.mwb_last_error()
+    assert lib.mwb_render_pgm(None, 16, None, 1, 4, 4, 16, 1, None, None, None) == -1
+    assert b"value_bits" in lib.mwb_last_error()
+    assert lib.mwb_render_pgm(None, 32, None, 1, 4, 4, 8, 1, None, None, None) == -1  # map_stride < nx*ny
+    assert lib.mwb_compact_payload(None, 0, 10, 12, None, None, None, None, None) == -1
+    assert lib.mwb_compact_payload(None, 4, 10, 8, None, None, None, None, None) == -1  # ld < n
+    assert lib.mwb_gather_composite(None, 10, None, 0, None, None, 0, None) == -1
+    assert lib.mwb_memcpy2d_async(None, 4, None, 16, 8, 1, None) == -1  # dpitch < width
+    assert lib.mwb_memcpy_async(None, None, 0, None) == 0  # nothing to copy
+    assert lib.mwb_elapsed_ms(None, 1, None) == -1
+    out = (ctypes.c_int32 * 2)()
+    assert lib.mwb_tc_sample_range(477, 10, 150, 1024, out) == 0
+    first, count = out[0], out[1]
+    assert first == 487 and 150 + 32 <= count <= 1024 - first  # covers every window offset plus W
+    assert lib.mwb_tc_sample_range(1000, 10, 150, 1024, out) == 0 and out[0] + out[1] == 1024  # clipped to ld
+    assert lib.mwb_tc_sample_range(0, 0, 8, 1024, out) == -1  # fewer than 16 offsets
