@@ -481,8 +481,9 @@ int mwb_render_pgm(const void* values, int value_bits, const uint8_t* valid, int
 
 /* Compact readback of a framework composite: out[i] = dense[coarse_slots[i]]
  * for i < n_coarse, then the device box region {x0, y0, z0, x1, y1, z1}'s
- * cells row by row (ix-major), at most cap values in all. */
-int mwb_gather_composite(const float* dense, int ny, const int32_t* coarse_slots, int n_coarse,
+ * cells in (ix, iy, iz) order (dense is [nx][ny][nz], nz = 1 in 2-D), at most
+ * cap values in all. */
+int mwb_gather_composite(const float* dense, int ny, int nz, const int32_t* coarse_slots, int n_coarse,
                          const int32_t* region, float* out, int64_t cap, void* stream);
 
 /* Stream-ordered copy of `bytes` between any two CUDA-visible addresses

@@ -510,7 +510,7 @@ class _FrameworkPlan(dv.GraphPlan):
                  self.valid.data_ptr(), st.count_ptr(1), self.mode, nat.ptr(self.f_ws),
                  0 if self.f_ws is None else self.f_ws.numel(), dv.stream_handle())
         ev[3].record()
-        nat.call("mwb_gather_composite", self.dense.data_ptr(), g.dims[1], self.c_slots.data_ptr(), self.n_coarse,
+        nat.call("mwb_gather_composite", self.dense.data_ptr(), g.dims[1], 1, self.c_slots.data_ptr(), self.n_coarse,
                  self.region_t.data_ptr(), self.compact.data_ptr(), self.compact.numel(), dv.stream_handle())
 
     ROI_BUDGET = 16384  # ROI cells read back with the result block (64 KB)
@@ -535,7 +535,7 @@ class _FrameworkPlan(dv.GraphPlan):
         """Enqueue one run on ``scan`` (graph replay after the first call) and the readback."""
         self.replay(scan)
         self.replays += 1
-        self.h_res = torch.empty(self._res_full, dtype=torch.uint8, pin_memory=self._pin)
+        self.h_res = torch.empty(self._res_copy, dtype=torch.uint8, pin_memory=self._pin)
         nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), self._res_copy,
                  dv.stream_handle())
 
@@ -555,10 +555,11 @@ class _FrameworkPlan(dv.GraphPlan):
         EVAL_COUNTER.add(n_fine)
         (x0, y0), (x1, y1) = final.min_cell, final.max_cell
         used = self._o_vals + 4 * (self.n_coarse + (x1 - x0 + 1) * (y1 - y0 + 1))
-        if used > self._res_copy:  # ROI beyond the budget: the rest of the block
-            nat.call("mwb_memcpy_async", self.h_res.data_ptr() + self._res_copy, self.res.data_ptr() + self._res_copy,
-                     used - self._res_copy, dv.stream_handle())
+        if used > self._res_copy:  # ROI beyond the budget: copy the whole used block again
+            self.h_res = torch.empty(used, dtype=torch.uint8, pin_memory=self._pin)
+            nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), used, dv.stream_handle())
             torch.cuda.current_stream().synchronize()
+            blk = self.h_res.numpy()
         comp = blk[self._o_vals: used].view(np.float32)
         composite = EnergyMap._from_loader(self.grid, functools.partial(self._dense_arrays, comp, final),
                                            stride=self.d, roi=final, split=self.d)

@@ -169,23 +169,23 @@ __global__ void __launch_bounds__(IO_THREADS) render_pgm_kernel(const T* __restr
 
 // (3) Compact readback of a framework composite (coarse2fine.py:326-328): the
 //     coarse lattice's values (fixed slots per plan) followed by the ROI
-//     rectangle's values row by row (ix-major), so a call reads back
-//     n_coarse + w*h floats instead of the whole dense map and its mask.
+//     box's values in (ix, iy, iz) order, so a call reads back n_coarse +
+//     |box| floats instead of the whole dense map and its mask (2-D: nz = 1).
 __global__ void __launch_bounds__(IO_THREADS) gather_composite_kernel(const float* __restrict__ dense, int ny,
-                                                                      const int* __restrict__ coarse_slots,
+                                                                      int nz, const int* __restrict__ coarse_slots,
                                                                       int n_coarse, const int* __restrict__ region,
                                                                       float* __restrict__ out, long long cap) {
-  const long long x0 = region[0], y0 = region[1], x1 = region[3], y1 = region[4];
-  const long long h = y1 - y0 + 1, n_roi = (x1 - x0 + 1) * h;
-  const long long total = n_coarse + n_roi;
+  const long long x0 = region[0], y0 = region[1], z0 = region[2];
+  const long long h = region[4] - y0 + 1, dz = region[5] - z0 + 1, plane = h * dz;
+  const long long total = n_coarse + (region[3] - x0 + 1) * plane;
   for (long long i = (long long)blockIdx.x * IO_THREADS + threadIdx.x; i < total && i < cap;
        i += (long long)gridDim.x * IO_THREADS) {
     long long slot;
     if (i < n_coarse) {
       slot = coarse_slots[i];
     } else {
-      const long long r = i - n_coarse, dx = r / h;
-      slot = (x0 + dx) * ny + y0 + (r - dx * h);
+      const long long r = i - n_coarse, ax = r / plane, rem = r - ax * plane, ay = rem / dz;
+      slot = ((x0 + ax) * ny + y0 + ay) * nz + z0 + (rem - ay * dz);
     }
     out[i] = dense[slot];
   }

@@ -1350,12 +1350,12 @@ int mwb_render_pgm(const void* values, int value_bits, const uint8_t* valid, int
   return check_launch("render_pgm_kernel");
 }
 
-int mwb_gather_composite(const float* dense, int ny, const int32_t* coarse_slots, int n_coarse,
+int mwb_gather_composite(const float* dense, int ny, int nz, const int32_t* coarse_slots, int n_coarse,
                          const int32_t* region, float* out, int64_t cap, void* stream) {
-  if (!dense || ny < 1 || n_coarse < 0 || (n_coarse && !coarse_slots) || !region || !out || cap < 0)
+  if (!dense || ny < 1 || nz < 1 || n_coarse < 0 || (n_coarse && !coarse_slots) || !region || !out || cap < 0)
     return set_err(MWB_EINVAL, "mwb_gather_composite: bad arguments");
   gather_composite_kernel<<<64, IO_THREADS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      dense, ny, coarse_slots, n_coarse, region, out, cap);
+      dense, ny, nz, coarse_slots, n_coarse, region, out, cap);
   return check_launch("gather_composite_kernel");
 }
 

@@ -225,7 +225,7 @@ class _SegmentPlan(dv.GraphPlan):
                      self.dense.data_ptr(), nx * ny, self.status.key_ptr(0 if das else 1), self.status.count_ptr(0),
                      self.status.flags_ptr, self.ws.data_ptr(), dv.stream_handle())
             ev[1].record()
-            nat.call("mwb_gather_composite", self.dense.data_ptr(), ny, None, 0, self.region_t.data_ptr(),
+            nat.call("mwb_gather_composite", self.dense.data_ptr(), ny, 1, None, 0, self.region_t.data_ptr(),
                      self.roi_t.data_ptr(), self.roi_t.numel(), dv.stream_handle())
             return
         self.valid.zero_()
@@ -244,7 +244,7 @@ class _SegmentPlan(dv.GraphPlan):
         self.replay(scan)
         nx, ny = self.grid.dims
         if self.tree is not None:
-            self.h_res = torch.empty(self._res_full, dtype=torch.uint8, pin_memory=self._pin)
+            self.h_res = torch.empty(self._res_copy, dtype=torch.uint8, pin_memory=self._pin)
             nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), self._res_copy,
                      dv.stream_handle())
             return
@@ -327,10 +327,11 @@ class _SegmentPlan(dv.GraphPlan):
         records, final = _decode_seg_trace(blk[self._o_trace: self._o_trace + nat.SEG_TRACE_BYTES].tobytes())
         (x0, y0), (x1, y1) = final.min_cell, final.max_cell
         used = self._o_roi + 4 * (x1 - x0 + 1) * (y1 - y0 + 1)
-        if used > self._res_copy:  # a final region beyond the budget: the rest of the block
-            nat.call("mwb_memcpy_async", self.h_res.data_ptr() + self._res_copy, self.res.data_ptr() + self._res_copy,
-                     used - self._res_copy, dv.stream_handle())
+        if used > self._res_copy:  # final region beyond the budget: copy the whole used block again
+            self.h_res = torch.empty(used, dtype=torch.uint8, pin_memory=self._pin)
+            nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), used, dv.stream_handle())
             torch.cuda.current_stream().synchronize()
+            blk = self.h_res.numpy()
         n_fine = int(counts[0])
         n_sub = self.n_sub
         EVAL_COUNTER.add(n_fine + 4 * n_sub * n_sub * len(records))

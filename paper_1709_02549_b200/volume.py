@@ -14,6 +14,8 @@ scores them with the reference's Eq. (5) / W-B / n_min control flow
 
 from __future__ import annotations
 
+import ctypes
+import functools
 import hashlib
 import math
 import weakref
@@ -27,7 +29,8 @@ from . import _device as dv
 from . import _native as nat
 from .beamform import (EVAL_COUNTER, _check_interpolation, _kind_code, _LatticeCache, _Status, _window, build_table,
                        launch_energies)
-from .coarse2fine import FrameworkConfig, IterationRecord, MetricTrace, decimation_factor, decode_trace
+from .coarse2fine import (FrameworkConfig, IterationRecord, MetricTrace, decimation_factor, decode_trace,
+                          decode_trace_lazy)
 
 
 @dataclass(frozen=True)
@@ -162,6 +165,22 @@ class VolumeMap:
         if not checked and valid.any() and not np.isfinite(values[valid]).all():
             raise ValueError("energy map contains non-finite values")
 
+    @classmethod
+    def _from_loader(cls, grid: VolumeGrid, loader, stride: int = 1, roi: Box | None = None):
+        """A map whose (values, valid) arrays come from ``loader()`` on first
+        use (device-checked finite): the octant framework's latency path."""
+        vm = cls.__new__(cls)
+        vm.grid, vm.stride, vm.roi = grid, stride, roi
+        vm._loader = loader
+        return vm
+
+    def __getattr__(self, name):
+        # only reached when the attribute is missing: materialise a loader-backed map
+        if name in ("values", "valid") and "_loader" in self.__dict__:
+            self.values, self.valid = self.__dict__.pop("_loader")()
+            return self.values if name == "values" else self.valid
+        raise AttributeError(name)
+
     def __len__(self) -> int:
         return int(self.valid.sum())
 
@@ -196,8 +215,6 @@ def _volume_pass(scan, grid: VolumeGrid, box: Box, stride: int, mask_t, skip_str
     pts = torch.empty((p_max, 3), dtype=torch.float64, device=dev)
     oidx = torch.empty(p_max, dtype=torch.int32, device=dev)
     ws = torch.empty(int(nat.load().mwb_volume_workspace_bytes(nx, ny, nz, stride)), dtype=torch.uint8, device=dev)
-    import ctypes
-
     host_box = (ctypes.c_int32 * 6)(*box.bounds())
     count_ptr = status.count_ptr(count_slot)
     nat.call("mwb_enumerate_volume", grid.origin[0], grid.origin[1], grid.origin[2], grid.resolution, nx, ny, nz,
@@ -333,8 +350,6 @@ def select_roi_volume(coarse: VolumeMap, box: Box, cfg: FrameworkConfig = Framew
 
 
 def _launch_select3(dense_t, valid_t, grid, lattice, box, cfg, region_t, trace_t):
-    import ctypes
-
     nx, ny, nz = grid.dims
     host_box = (ctypes.c_int32 * 6)(*box.bounds())
     nat.call("mwb_select_roi_volume", dense_t.data_ptr(), valid_t.data_ptr(), nx, ny, nz, lattice,
@@ -384,13 +399,12 @@ class _VolumeFrameworkPlan(dv.GraphPlan):
         self.mask_t = _upload_mask3(mask, grid.dims)
         self.dense = torch.empty(n, dtype=torch.float32, device=dev)  # only valid voxels are read
         self.valid = torch.empty(n, dtype=torch.uint8, device=dev)
-        self.status = _Status()
         self.region_t = torch.empty(6, dtype=torch.int32, device=dev)
-        self.trace_t = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, device=dev)
         self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
+        self._ev_handles = None
+        self._ms = (ctypes.c_float * 3)()
         self._pin = torch.cuda.is_available()
-        self.h_status = torch.empty_like(self.status.t, device="cpu", pin_memory=self._pin)
-        self.h_trace = torch.empty(nat.TRACE_BYTES, dtype=torch.uint8, pin_memory=self._pin)
+        self.mask_np = np.ascontiguousarray(mask, dtype=bool)
         # the coarse voxel lattice and its delay table depend on the geometry,
         # grid and mask only: built once here, outside the graph
         self.c_valid = torch.zeros(n, dtype=torch.uint8, device=dev)
@@ -401,6 +415,22 @@ class _VolumeFrameworkPlan(dv.GraphPlan):
         self.c_count.copy_(c_status.t.view(torch.int32)[4:5])  # status count slot 0
         self.c_table = build_table(self.scan, self.c_pts, self.c_pts.shape[0], interp, self.c_count.data_ptr())
         self.n_coarse = int(self.c_count.item())
+        self.c_slots = self.c_oidx[: self.n_coarse].clone()
+        self.c_slots_host = self.c_slots.cpu().numpy()
+        self.c_valid_host = self.c_valid.cpu().numpy().view(bool).reshape(grid.dims)
+        # one result block per call, as the 2-D plan's: [status | trace | coarse
+        # values, then the final box's voxels (mwb_gather_composite)], a budget
+        # of box voxels copied with it, the rest only for a larger box
+        self._o_trace = _Status.BYTES
+        self._o_vals = (self._o_trace + nat.TRACE_BYTES + 15) // 16 * 16
+        self._res_full = self._o_vals + 4 * (self.n_coarse + n)
+        self._res_copy = min(self._res_full, self._o_vals + 4 * (self.n_coarse + self.BOX_BUDGET))
+        self.res = torch.empty(self._res_full, dtype=torch.uint8, device=dev)
+        self.status = _Status(self.res)
+        self.trace_t = self.res[self._o_trace: self._o_trace + nat.TRACE_BYTES]
+        self.compact = self.res[self._o_vals:].view(torch.float32)
+
+    BOX_BUDGET = 1 << 16  # final-box voxels read back with the result block (256 KB)
 
     def _enqueue(self) -> None:
         g, d, sc = self.grid, self.d, self.scan
@@ -420,26 +450,49 @@ class _VolumeFrameworkPlan(dv.GraphPlan):
         _volume_pass(sc, g, full, 1, self.mask_t, d, (self.kcode,), self.interp, self.k0, self.w,
                      {self.kcode: self.dense}, self.valid, self.status, 1, d_region=self.region_t)
         ev[3].record()
+        _, ny, nz = g.dims
+        nat.call("mwb_gather_composite", self.dense.data_ptr(), ny, nz, self.c_slots.data_ptr(), self.n_coarse,
+                 self.region_t.data_ptr(), self.compact.data_ptr(), self.compact.numel(), dv.stream_handle())
 
     def launch(self, scan) -> None:
         self.replay(scan)
-        n = math.prod(self.grid.dims)
-        self.h_dense = torch.empty(n, dtype=torch.float32, pin_memory=self._pin)  # owned by the returned map
-        self.h_valid = torch.empty(n, dtype=torch.uint8, pin_memory=self._pin)
-        for src, dst in ((self.status.t, self.h_status), (self.trace_t, self.h_trace), (self.dense, self.h_dense),
-                         (self.valid, self.h_valid)):
-            dst.copy_(src, non_blocking=True)
+        self.h_res = torch.empty(self._res_copy, dtype=torch.uint8, pin_memory=self._pin)  # kept by the returned map
+        nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), self._res_copy, dv.stream_handle())
+
+    def _arrays(self, comp: np.ndarray, final: Box) -> tuple[np.ndarray, np.ndarray]:
+        """(values, valid) of the composite: coarse voxels from their slots, fine
+        voxels = the final box's masked voxels off the coarse lattice."""
+        d = self.d
+        (x0, y0, z0), (x1, y1, z1) = final.min_cell, final.max_cell
+        vals = np.zeros(math.prod(self.grid.dims), dtype=np.float32)
+        vals[self.c_slots_host] = comp[: self.n_coarse]
+        vals = vals.reshape(self.grid.dims)
+        valid = self.c_valid_host.copy()
+        ix = np.arange(x0, x1 + 1)[:, None, None] % d == 0
+        iy = np.arange(y0, y1 + 1)[None, :, None] % d == 0
+        iz = np.arange(z0, z1 + 1)[None, None, :] % d == 0
+        fine = self.mask_np[x0: x1 + 1, y0: y1 + 1, z0: z1 + 1] & ~(ix & iy & iz)
+        block = comp[self.n_coarse:].reshape(x1 - x0 + 1, y1 - y0 + 1, z1 - z0 + 1)
+        vals[x0: x1 + 1, y0: y1 + 1, z0: z1 + 1][fine] = block[fine]
+        valid[x0: x1 + 1, y0: y1 + 1, z0: z1 + 1] |= fine
+        return vals, valid
 
     def finish(self) -> tuple[VolumeMap, VolumeReport]:
         torch.cuda.current_stream().synchronize()
         grid, d = self.grid, self.d
-        keys, counts, flags = self.status.read(self.h_status.numpy())
+        blk = self.h_res.numpy()
+        keys, counts, flags = _Status.decode(blk[: _Status.BYTES].view(np.int64))
         if flags & 1:
             raise ValueError("energy map contains non-finite values")
-        final, trace, _ = decode_trace(self.h_trace.numpy().tobytes(), region=_box)
-        values = self.h_dense.numpy().reshape(grid.dims)
-        vmask = self.h_valid.numpy().reshape(grid.dims).view(bool)
-        composite = VolumeMap(grid, values, vmask, stride=d, roi=final, checked=True)
+        final, trace, _ = decode_trace_lazy(blk[self._o_trace: self._o_trace + nat.TRACE_BYTES], region=_box)
+        used = self._o_vals + 4 * (self.n_coarse + final.n_cells)
+        if used > self._res_copy:  # final box beyond the budget: copy the whole used block again
+            self.h_res = torch.empty(used, dtype=torch.uint8, pin_memory=self._pin)
+            nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), used, dv.stream_handle())
+            torch.cuda.current_stream().synchronize()
+            blk = self.h_res.numpy()
+        comp = blk[self._o_vals: used].view(np.float32)
+        composite = VolumeMap._from_loader(grid, functools.partial(self._arrays, comp, final), stride=d, roi=final)
         n_c, n_f = self.n_coarse, int(counts[1])
         EVAL_COUNTER.add(n_c + n_f)
         key = int(keys[0 if self.kcode == nat.MWB_DAS else 1])
@@ -449,10 +502,12 @@ class _VolumeFrameworkPlan(dv.GraphPlan):
             cell = (slot // (ny * nz), (slot // nz) % ny, slot % nz)
         else:
             cell = composite.argmax_cell()
-        ev = self.events
-        t = [ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3, ev[2].elapsed_time(ev[3]) / 1e3]
+        if self._ev_handles is None:
+            self._ev_handles = (ctypes.c_void_p * 4)(*[e.cuda_event for e in self.events])
+        nat.call("mwb_elapsed_ms", self._ev_handles, 4, self._ms)
+        t = [self._ms[i] / 1e3 for i in range(3)]
         report = VolumeReport(
-            decimation_factor=d, iterations=len(trace.records), final_region=final, coarse_points_evaluated=n_c,
+            decimation_factor=d, iterations=trace.n_records, final_region=final, coarse_points_evaluated=n_c,
             fine_points_evaluated=n_f, full_equivalent_points=self.full_eq,
             reduction_ratio=self.full_eq / (n_c + n_f),
             elapsed={"coarse": t[0], "select": t[1], "fine": t[2], "total": sum(t)}, trace=trace, argmax_cell=cell,

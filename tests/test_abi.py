@@ -202,7 +202,7 @@ def test_round2_entry_points_validate_arguments(lib):
     assert lib.mwb_render_pgm(None, 32, None, 1, 4, 4, 8, 1, None, None, None) == -1  # map_stride < nx*ny
     assert lib.mwb_compact_payload(None, 0, 10, 12, None, None, None, None, None) == -1
     assert lib.mwb_compact_payload(None, 4, 10, 8, None, None, None, None, None) == -1  # ld < n
-    assert lib.mwb_gather_composite(None, 10, None, 0, None, None, 0, None) == -1
+    assert lib.mwb_gather_composite(None, 10, 1, None, 0, None, None, 0, None) == -1
     assert lib.mwb_memcpy2d_async(None, 4, None, 16, 8, 1, None) == -1  # dpitch < width
     assert lib.mwb_memcpy_async(None, None, 0, None) == 0  # nothing to copy
     assert lib.mwb_elapsed_ms(None, 1, None) == -1

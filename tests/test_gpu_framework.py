@@ -424,3 +424,24 @@ def test_concurrent_first_calls_capture_safely():
         got = list(pool.map(one, range(8)))
     want = [one(i, wait=False) for i in range(8)]
     assert got == want
+
+
+def test_degenerate_run_reads_back_the_whole_breast_region():
+    """An all-zero scan is degenerate (coarse2fine.py:189-192): the ROI is the
+    whole breast box, larger than the result block's copy budget, so the
+    composite comes back through the overflow copy; it must equal the full
+    masked image (every cell 0) with the reference's counts."""
+    model = synth.ScanModel(n_samples=512)
+    ds, _ = synth.dataset_2d(model, seed=3)
+    zero = mw.BackscatterDataset(ds.geometry, np.zeros_like(ds.signals))
+    grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 2.5e-4)  # 400^2 cells: ROI >> 16384-cell budget
+    comp, rep = mw.run_framework(zero, "das", grid, mw.Manual(12), window=(model.k0, 32))
+    mask = mw.breast_mask(grid)
+    assert rep.trace.termination == "degenerate" and rep.final_region == grid.full_region()
+    assert rep.coarse_points_evaluated + rep.fine_points_evaluated == int(mask.sum())
+    assert set(comp.entries) == {(int(a), int(b)) for a, b in np.argwhere(mask)}
+    assert all(v == 0.0 for v in comp.entries.values())
+    # a real scan right after reuses the plan's buffers correctly
+    comp2, rep2 = mw.run_framework(ds, "das", grid, mw.Manual(12), window=(model.k0, 32))
+    full = mw.image(ds, "das", grid, mask=mask, window=(model.k0, 32))
+    assert all(comp2.entries[c] == full.entries[c] for c in comp2.entries)

@@ -169,3 +169,18 @@ def test_octant_framework_sees_in_place_mask_edits():
     _, rep_c = run_framework_volume(ds, "dmas", grid, mw.Manual(3), mask=fresh, window=win)
     assert rep_b.full_equivalent_points == int(mask.sum()) != rep_a.full_equivalent_points
     assert rep_b.to_dict() | {"elapsed": None} == rep_c.to_dict() | {"elapsed": None}
+
+
+def test_degenerate_octant_run_uses_the_overflow_copy():
+    """An all-zero volume is degenerate: the final box is the whole grid and
+    the composite comes back through the overflow path of the result block."""
+    vm = synth.VolumeModel(n_samples=1024)
+    g = vm.geometry()
+    zero = mw.BackscatterDataset(g, np.zeros((vm.n_ant, vm.n_ant, vm.n_samples)))
+    grid = VolumeGrid((-0.048, -0.048, 0.0), (0.096, 0.096, 0.048), 0.0015)  # 64 x 64 x 32 > the box budget
+    mask = hemisphere_mask(grid, 0.048)
+    comp, rep = run_framework_volume(zero, "dmas", grid, mw.Manual(4), mask=mask, window=(vm.k0, vm.window))
+    assert rep.trace.termination == "degenerate"
+    assert rep.final_region.bounds() == (0, 0, 0, *(n - 1 for n in grid.dims))
+    assert comp.valid.sum() == int(mask.sum()) == rep.coarse_points_evaluated + rep.fine_points_evaluated
+    assert not comp.values[comp.valid].any()
