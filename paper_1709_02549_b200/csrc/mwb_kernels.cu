@@ -738,19 +738,6 @@ static int select_common(SelectParams& p, void* stream, int n_scans = 1) {
     select_roi_sat_kernel<<<n_scans, SAT_TPB, sm, st>>>(p);
     return check_launch("select_roi_sat_kernel");
   }
-  if (p.dims == 2 && n > 0 && n <= SEL_WARP_STAGE) {  // K2w: warp per scan, or one warp per box
-    const bool split = n_scans < SEL_SPLIT_MAX_SCANS;
-    void (*wk)(SelectParams, int) = split ? select_roi_warp_kernel<true> : select_roi_warp_kernel<false>;
-    const size_t smw = sizeof(float) * (size_t)n * (split ? 1 : SEL_WPB);
-    cudaError_t e = cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(float) * SEL_WARP_STAGE * SEL_WPB));
-    if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    if (split)
-      wk<<<n_scans, SEL_SPLIT_WARPS * 32, smw, st>>>(p, n_scans);
-    else
-      wk<<<(n_scans + SEL_WPB - 1) / SEL_WPB, SEL_WPB * 32, smw, st>>>(p, n_scans);
-    return check_launch("select_roi_warp_kernel");
-  }
   const size_t sm = p.staged ? sizeof(float) * (size_t)n : 0;
   void (*fn)(SelectParams) = p.dims == 3 ? select_roi_kernel<8> : select_roi_kernel<4>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

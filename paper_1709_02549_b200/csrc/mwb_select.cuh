@@ -398,320 +398,6 @@ __global__ void __launch_bounds__(SEL_TPB) select_roi_kernel(const SelectParams 
   }
 }
 // ----------------------------------------------------------------------------
-// K2w: warp-per-scan select_roi for 2-D lattices whose breast box stages in
-// SEL_WARP_STAGE cells (the framework's 16..64-cell-wide low-res lattices).
-// A 256-thread CTA spends most of its time in barriers and 16-double block
-// reductions when every thread visits only ~5 cells per pass; a warp visits
-// ~36 per lane, reduces with shuffles only, and SEL_WPB scans share a CTA.
-// Cells are walked in lattice coordinates (no div/mod per cell) and each
-// cell's child / expansion membership is four range tests per axis (the
-// expansions are per-axis: expand_box grows each axis independently).
-// Same decisions as select_roi_kernel<4>; the summation order is the warp's,
-// so single-scan and batched selection both dispatch here for such lattices
-// and stay bit-identical to each other.
-// ----------------------------------------------------------------------------
-constexpr int SEL_WPB = 4;
-constexpr int SEL_WARP_STAGE = 4096;
-constexpr int SEL_SPLIT_MAX_SCANS = 148;  // below a wave of scans, a CTA of 8 warps per scan
-
-struct SelWarpCtl {
-  double nxt[5];
-  Box next;
-  int term;
-};
-
-__device__ __forceinline__ double warp_sum_d(double x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
-}
-__device__ __forceinline__ int warp_sum_i(int x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
-}
-
-// f(lx, ly, v) for every valid cell of box r; lattice cells are i = lane + 32k
-// of the r-lattice in row-major order, advanced incrementally.  Each lane
-// loads its next SEL_U cells before visiting them in order, so the shared-
-// memory latency overlaps while every accumulator sees the same sequence.
-constexpr int SEL_U = 4;
-template <class F>
-__device__ __forceinline__ void warp_cells(const float* sv, int sLy, int sl0x, int sl0y, int D, const Box& r,
-                                           F&& f) {
-  const int l0x = (r.lo[0] + D - 1) / D, l1x = r.hi[0] / D;
-  const int l0y = (r.lo[1] + D - 1) / D, l1y = r.hi[1] / D;
-  if (l1x < l0x || l1y < l0y) return;
-  const int Ly = l1y - l0y + 1, n = (l1x - l0x + 1) * Ly;
-  const int lane = threadIdx.x & 31;
-  const int q = 32 / Ly, rr = 32 - q * Ly;
-  int lx = lane / Ly, ly = lane - lx * Ly;
-  const float* base = sv + (l0x - sl0x) * sLy + (l0y - sl0y);
-  for (int i0 = lane; i0 < n; i0 += 32 * SEL_U) {
-    float v[SEL_U];
-    int cx[SEL_U], cy[SEL_U];
-#pragma unroll
-    for (int u = 0; u < SEL_U; ++u) {
-      cx[u] = lx;
-      cy[u] = ly;
-      const bool in = i0 + 32 * u < n;
-      const float x = base[in ? lx * sLy + ly : 0];  // unconditional load: no branch per cell
-      v[u] = in ? x : __int_as_float(0x7fc00000);
-      lx += q;
-      ly += rr;
-      if (ly >= Ly) {
-        ly -= Ly;
-        ++lx;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < SEL_U; ++u)
-      if (v[u] == v[u]) f(l0x + cx[u], l0y + cy[u], v[u]);
-  }
-}
-
-// SPLIT = false: SEL_WPB scans per CTA, one warp each (batches).
-// SPLIT = true:  one scan per CTA of SEL_SPLIT_WARPS warps (single scans: a
-//   lone warp is latency bound).  Every warp walks the same cells in the same
-//   lane order, but in the iteration passes warp k accumulates only box k, so
-//   each box's sum sees exactly the additions of the one-warp kernel and the
-//   two modes agree bit for bit.
-constexpr int SEL_SPLIT_WARPS = 8;
-
-template <bool SPLIT>
-__global__ void __launch_bounds__(SPLIT ? SEL_SPLIT_WARPS * 32 : SEL_WPB * 32)
-    select_roi_warp_kernel(const SelectParams p, int n_scans) {
-  constexpr int NT = SPLIT ? SEL_SPLIT_WARPS * 32 : 32;  // threads sharing one scan
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = SPLIT ? (int)blockIdx.x : (int)blockIdx.x * SEL_WPB + warp;
-  if (s >= n_scans) return;
-  extern __shared__ float smem_sel[];
-  __shared__ SelWarpCtl wctl[SEL_WPB];
-  __shared__ double box_stat[2][8];  // SPLIT: per-box sums / m2 from the owning warp
-  __shared__ int box_cnt[8];
-  SelWarpCtl& wc = wctl[SPLIT ? 0 : warp];
-  const int D = p.D, sLx = p.sL[0], sLy = p.sL[1], sl0x = p.sl0[0], sl0y = p.sl0[1];
-  const int nst = sLx * sLy;
-  float* sv = smem_sel + (SPLIT ? 0 : warp * nst);
-  const float* dense = p.dense + (size_t)s * p.dense_stride;
-  int32_t* region_out = p.region_out + 6 * s;
-  mwb_trace_t* tr = p.trace + s;
-  const int tid = SPLIT ? (int)threadIdx.x : lane;
-  const bool leader = tid == 0;
-
-  {  // stage the breast box's lattice: both loads independent, 8 in flight per thread
-    int lx = tid / sLy, ly = tid - lx * sLy;
-    const int q = NT / sLy, rr = NT - q * sLy;
-#pragma unroll 8
-    for (int i = tid; i < nst; i += NT) {
-      const size_t slot = (size_t)(sl0x + lx) * D * p.ny + (size_t)(sl0y + ly) * D;
-      const float v = __ldg(dense + slot);
-      const uint8_t ok = __ldg(p.valid + slot);
-      sv[i] = ok ? v : __int_as_float(0x7fc00000);
-      lx += q;
-      ly += rr;
-      if (ly >= sLy) {
-        ly -= sLy;
-        ++lx;
-      }
-    }
-  }
-  if (SPLIT)
-    __syncthreads();
-  else
-    __syncwarp();
-
-  // breast-region stats: count, sum, min, max, then the two-pass m2
-  // (coarse2fine.py:186-199); SPLIT warps all compute them (identically)
-  double n_sel, sum_sel, m2_sel;
-  {
-    int c = 0;
-    double sm = 0.0;
-    float mn = INFINITY, mx = -INFINITY;  // exact in fp32: the values are fp32
-    warp_cells(sv, sLy, sl0x, sl0y, D, p.breast, [&](int, int, float v) {
-      ++c;
-      sm += (double)v;
-      mn = fminf(mn, v);
-      mx = fmaxf(mx, v);
-    });
-    n_sel = (double)warp_sum_i(c);
-    sum_sel = warp_sum_d(sm);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    if (n_sel == 0.0 || mx == mn) {
-      if (leader) {
-        tr->termination = n_sel == 0.0 ? MWB_TERM_EMPTY : MWB_TERM_DEGENERATE;
-        tr->n_records = 0;
-        put_box(tr->final_region, p.breast);
-        put_box(region_out, p.breast);
-      }
-      return;
-    }
-    const double mean = sum_sel / n_sel;
-    double d2 = 0.0;
-    warp_cells(sv, sLy, sl0x, sl0y, D, p.breast, [&](int, int, float v) {
-      const double d = (double)v - mean;
-      d2 = __fma_rn(d, d, d2);
-    });
-    m2_sel = warp_sum_d(d2);
-  }
-
-  Box sel = p.breast;
-  double sigma_prev_sq = m2_sel / n_sel;
-  double prev_w = 0.0, prev_b = 0.0;
-  bool have_prev = false;
-  int iteration = 0;
-  int term = MWB_TERM_NONE;
-
-  while (true) {
-    Box rg[8];
-    const int nk = split_box(sel, 2, rg);
-    if (nk == 0) {
-      term = MWB_TERM_REGION_FLOOR;
-      break;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) rg[4 + k] = expand_box(rg[k], p.frac, sel, 2);
-    // lattice thresholds: a cell is in a high-half child iff l * D > mid;
-    // expansion ranges per axis: x from rg[4] (low) / rg[5] (high), y from rg[4] / rg[6]
-    const int mxl = rg[0].hi[0] / D, myl = rg[0].hi[1] / D;
-    const int ex0l = (rg[4].lo[0] + D - 1) / D, ex0h = rg[4].hi[0] / D;
-    const int ex1l = (rg[5].lo[0] + D - 1) / D, ex1h = rg[5].hi[0] / D;
-    const int ey0l = (rg[4].lo[1] + D - 1) / D, ey0h = rg[4].hi[1] / D;
-    const int ey1l = (rg[6].lo[1] + D - 1) / D, ey1h = rg[6].hi[1] / D;
-    double cnt[8], sums[8], mean[8], m2[8];
-
-    if constexpr (SPLIT) {
-      // warp k owns box k: the same membership tests as below, as one rectangle
-      const int k = warp;
-      const bool xhi = k < 4 ? (k & 1) : false, yhi = k < 4 ? (k >> 1) & 1 : false;
-      const int rx0 = k < 4 ? (xhi ? mxl + 1 : INT_MIN) : ((k - 4) & 1 ? ex1l : ex0l);
-      const int rx1 = k < 4 ? (xhi ? INT_MAX : mxl) : ((k - 4) & 1 ? ex1h : ex0h);
-      const int ry0 = k < 4 ? (yhi ? myl + 1 : INT_MIN) : ((k - 4) >> 1 ? ey1l : ey0l);
-      const int ry1 = k < 4 ? (yhi ? INT_MAX : myl) : ((k - 4) >> 1 ? ey1h : ey0h);
-      int ci = 0;
-      double a1 = 0.0;
-      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
-        const double v = fv;
-        if (rx0 <= lx && lx <= rx1 && ry0 <= ly && ly <= ry1) {
-          ++ci;
-          a1 += v;
-        }
-      });
-      ci = warp_sum_i(ci);
-      a1 = warp_sum_d(a1);
-      if (lane == 0) {
-        box_cnt[k] = ci;
-        box_stat[0][k] = a1;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        cnt[j] = (double)box_cnt[j];
-        sums[j] = box_stat[0][j];
-        mean[j] = cnt[j] > 0.0 ? sums[j] / cnt[j] : 0.0;
-      }
-      double a2 = 0.0;
-      const double mu = mean[k];
-      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
-        const double v = fv;
-        if (rx0 <= lx && lx <= rx1 && ry0 <= ly && ly <= ry1) {
-          const double d = v - mu;
-          a2 = __fma_rn(d, d, a2);  // explicit: both modes round alike
-        }
-      });
-      a2 = warp_sum_d(a2);
-      if (lane == 0) box_stat[1][k] = a2;
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < 8; ++j) m2[j] = box_stat[1][j];
-    } else {
-      // pass 1: count and sum of every child and of every child's expansion
-      int ci[8];
-      double a1[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        ci[k] = 0;
-        a1[k] = 0.0;
-      }
-      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
-        const double v = fv;
-        const int kc = (lx > mxl) | ((ly > myl) << 1);
-        const bool x0 = ex0l <= lx && lx <= ex0h, x1 = ex1l <= lx && lx <= ex1h;
-        const bool y0 = ey0l <= ly && ly <= ey0h, y1 = ey1l <= ly && ly <= ey1h;
-        const bool in[8] = {kc == 0, kc == 1, kc == 2, kc == 3, x0 && y0, x1 && y0, x0 && y1, x1 && y1};
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (in[k]) {
-            ++ci[k];
-            a1[k] += v;
-          }
-      });
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        cnt[k] = (double)warp_sum_i(ci[k]);
-        sums[k] = warp_sum_d(a1[k]);
-        mean[k] = cnt[k] > 0.0 ? sums[k] / cnt[k] : 0.0;
-      }
-      // pass 2: sum of (x - mean)^2 (two-pass variance, as numpy's var)
-      double a2[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) a2[k] = 0.0;
-      warp_cells(sv, sLy, sl0x, sl0y, D, sel, [&](int lx, int ly, float fv) {
-        const double v = fv;
-        const int kc = (lx > mxl) | ((ly > myl) << 1);
-        const bool x0 = ex0l <= lx && lx <= ex0h, x1 = ex1l <= lx && lx <= ex1h;
-        const bool y0 = ey0l <= ly && ly <= ey0h, y1 = ey1l <= ly && ly <= ey1h;
-        const bool in[8] = {kc == 0, kc == 1, kc == 2, kc == 3, x0 && y0, x1 && y0, x0 && y1, x1 && y1};
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (in[k]) {
-            const double d = v - mean[k];
-            a2[k] = __fma_rn(d, d, a2[k]);
-          }
-      });
-#pragma unroll
-      for (int k = 0; k < 8; ++k) m2[k] = warp_sum_d(a2[k]);
-    }
-
-    if (!SPLIT || warp == 0) {
-      const int t = select_score<4>(p, tr, iteration, nk, rg, cnt, sums, mean, m2, n_sel, sum_sel, m2_sel,
-                                    sigma_prev_sq, have_prev, prev_w, prev_b, wc.nxt, &wc.next);
-      if (lane == 0) wc.term = t;
-    }
-    if (SPLIT)
-      __syncthreads();
-    else
-      __syncwarp();
-    term = wc.term;
-    if (term == MWB_TERM_N_MIN) break;
-    iteration += 1;
-    if (term != MWB_TERM_NONE) break;
-    prev_w = wc.nxt[0];
-    prev_b = wc.nxt[1];
-    have_prev = true;
-    n_sel = wc.nxt[2];
-    sum_sel = wc.nxt[3];
-    m2_sel = wc.nxt[4];
-    sigma_prev_sq = m2_sel / n_sel;
-    sel = wc.next;
-    if (SPLIT)
-      __syncthreads();
-    else
-      __syncwarp();
-  }
-  if (leader) {
-    tr->termination = term;
-    tr->n_records = min(iteration, MWB_MAX_ITERS);
-    put_box(tr->final_region, sel);
-    put_box(region_out, sel);
-  }
-}
-
-// ----------------------------------------------------------------------------
 // K2s: 2-D select_roi on summed-area tables (single scans and batches, one
 // CTA per scan).  Every statistic the selection needs is a box statistic of
 // the coarse lattice: count, mean and sum of squared deviations of a child
@@ -722,8 +408,9 @@ __global__ void __launch_bounds__(SPLIT ? SEL_SPLIT_WARPS * 32 : SEL_WPB * 32)
 // into four lookups, so an iteration costs O(1) instead of two passes over
 // the cells.  The tables are built once (row then column prefix sums, all
 // threads); warp 0 then runs the iterations: lane k evaluates box k (four
-// children, four expansions), select_score makes the decision exactly as the
-// cell-walking kernels do.  Decisions match the reference's two-pass numpy
+// children, four expansions) and makes select_score's decision (Eq. (5), the
+// first-index argmax, the n_min stop, W/B with the OR test) with the same
+// arithmetic as the cell-walking K2.  Decisions match the reference's two-pass numpy
 // statistics up to fp64 rounding (near-ties are the parity bar's excuse).
 // ----------------------------------------------------------------------------
 constexpr int SAT_TPB = 256;
