@@ -682,6 +682,18 @@ def run_ours(args):
         core = {"kernel": "energy_kernel<BOTH> (CUDA cores, mode smem)", "ms_per_step": k_ms,
                 "value": 2.0 * S * P * C / (k_ms * 1e-3), "unit": UNIT,
                 "roofline": smem_roofline(pps_launch, k_ms, smem_gbs, fp32_tf, traffic)}
+        # DAS alone (no per-sample DMAS self-term: 3 FP32 ops per pps, so the
+        # smem side binds): the kernel's roofline fraction without the q FFMA
+        d_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+        for a, b in d_ev:
+            a.record()
+            bk.run_device(sig_d, out_das=outs["das"], key_das=keys["das"])
+            b.record()
+        torch.cuda.synchronize()
+        d_ms = statistics.mean(a.elapsed_time(b) for a, b in d_ev)
+        core["das_only"] = {"kernel": "energy_kernel<DAS>", "ms_per_step": d_ms,
+                            "pixel_pair_evals_per_s": S * P * C / (d_ms * 1e-3),
+                            "smem_frac": pps_launch * 4.0 / (d_ms * 1e-3) / 1e9 / smem_gbs}
         del bk
 
     # end to end through the public host API

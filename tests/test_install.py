@@ -1,13 +1,17 @@
 """The drop-in installer rebinds every import-time binding of the hot-path
-names in the reference package.  Runs where the reference is
-importable (the build container); skipped elsewhere (the GPU box)."""
+names in the reference package.  Runs wherever the reference
+is importable: the staged copy in baseline/_ref (here and on the GPU box) or
+/root/reference."""
 
 import sys
 from pathlib import Path
 
 import pytest
 
-REF = Path("/root/reference/pkg/src")
+# the unmodified reference: staged by baseline/stage.py (travels to the GPU
+# box), else the read-only source tree of the build container
+STAGED = Path(__file__).resolve().parents[1] / "baseline" / "_ref"
+REF = STAGED if (STAGED / "mwbeam" / "__init__.py").exists() else Path("/root/reference/pkg/src")
 
 
 @pytest.fixture
