@@ -87,6 +87,9 @@ class EvalCounter:
 EVAL_COUNTER = EvalCounter()
 
 
+_MATERIALISE = threading.Lock()  # loader-backed maps build their dense arrays once
+
+
 class EnergyMap:
     """Sparse map ``(ix, iy) -> energy`` (reference beamform.py:78-128).
 
@@ -139,11 +142,15 @@ class EnergyMap:
 
     def __getattr__(self, name):
         # only reached when the attribute is missing: a loader-backed map
-        # materialises its dense arrays on the first access
-        if name in ("_values", "_valid") and "_loader" in self.__dict__:
-            vals, valid = self.__dict__.pop("_loader")()
-            self._values, self._valid = vals, valid
-            return vals if name == "_values" else valid
+        # materialises its dense arrays on the first access (once, also when
+        # several threads read the map at the same time)
+        if name in ("_values", "_valid"):
+            with _MATERIALISE:
+                d = self.__dict__
+                if name not in d and "_loader" in d:
+                    d["_values"], d["_valid"] = d.pop("_loader")()
+                if name in d:
+                    return d[name]
         raise AttributeError(name)
 
     # -- entries -----------------------------------------------------------

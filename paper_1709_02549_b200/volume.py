@@ -27,8 +27,8 @@ import torch
 
 from . import _device as dv
 from . import _native as nat
-from .beamform import (EVAL_COUNTER, _check_interpolation, _kind_code, _LatticeCache, _Status, _window, build_table,
-                       launch_energies)
+from .beamform import (_MATERIALISE, EVAL_COUNTER, _check_interpolation, _kind_code, _LatticeCache, _Status,
+                       _window, build_table, launch_energies)
 from .coarse2fine import (FrameworkConfig, IterationRecord, MetricTrace, decimation_factor, decode_trace,
                           decode_trace_lazy)
 
@@ -175,10 +175,14 @@ class VolumeMap:
         return vm
 
     def __getattr__(self, name):
-        # only reached when the attribute is missing: materialise a loader-backed map
-        if name in ("values", "valid") and "_loader" in self.__dict__:
-            self.values, self.valid = self.__dict__.pop("_loader")()
-            return self.values if name == "values" else self.valid
+        # only reached when the attribute is missing: materialise a loader-backed map (once)
+        if name in ("values", "valid"):
+            with _MATERIALISE:
+                d = self.__dict__
+                if name not in d and "_loader" in d:
+                    d["values"], d["valid"] = d.pop("_loader")()
+                if name in d:
+                    return d[name]
         raise AttributeError(name)
 
     def __len__(self) -> int:

@@ -445,3 +445,18 @@ def test_degenerate_run_reads_back_the_whole_breast_region():
     comp2, rep2 = mw.run_framework(ds, "das", grid, mw.Manual(12), window=(model.k0, 32))
     full = mw.image(ds, "das", grid, mask=mask, window=(model.k0, 32))
     assert all(comp2.entries[c] == full.entries[c] for c in comp2.entries)
+
+
+def test_lazy_composite_is_materialised_once_under_threads():
+    """run_framework's composite builds its dense arrays on first use
+    (EnergyMap._from_loader); threads reading it at once all see the same map."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    model = synth.ScanModel(n_samples=1024)
+    ds, _ = synth.dataset_2d(model, seed=77)
+    grid = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 5e-4)
+    comp, rep = mw.run_framework(ds, "dmas", grid, mw.Manual(6), window=(model.k0, model.window))
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        got = list(pool.map(lambda _: (comp.argmax_cell(), len(comp), comp.dense()[rep.argmax_cell]), range(16)))
+    assert len(set((a, n) for a, n, _ in got)) == 1
+    assert got[0][0] == rep.argmax_cell and got[0][1] == rep.coarse_points_evaluated + rep.fine_points_evaluated
