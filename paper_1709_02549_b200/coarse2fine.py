@@ -32,7 +32,7 @@ from . import _device as dv
 from . import _native as nat
 from .beamform import (
     EVAL_COUNTER,
-    BeamformerKind,
+    BeamformerKind,  # re-exported, as the reference's coarse2fine namespace has it
     EnergyMap,
     _check_interpolation,
     _kind_code,
@@ -40,7 +40,6 @@ from .beamform import (
     _window,
     build_table,
     launch_energies,
-    lattice_pass,
 )
 from .geometry import ImagingGrid, Region, as_grid, as_region
 
