@@ -549,31 +549,36 @@ def tensor_peak():
     return 1590.0, "fallback 1.59 PFLOP/s of B200_PROFILING.md (MEASURED_PEAKS.json absent)"
 
 
-def tc_roofline(S, slots, C, avg, traffic):
-    """Tensor-core kernel: per (256-point tile, 8-scan group, channel) six
-    tcgen05.mma M128 x N256 x K16 f16 (two M-blocks x the hi*hi, hi*lo, lo*hi
-    split) = 6 * 2 * 128 * 256 * 16 FLOP."""
-    tiles, groups = (slots + 255) // 256, (S + 7) // 8
+def tc_roofline(S, plan_steps, avg, traffic):
+    """Tensor-core kernel (W = 32, energy_tch_kernel): per MMA step of a
+    (128-point M-block, pair of 8-scan groups) item, six tcgen05.mma
+    M128 x N256 x K16 f16 (two scan groups x the hi*hi, hi*lo, lo*hi split) =
+    6 * 2 * 128 * 256 * 16 FLOP.  A step holds two 8-tap K halves, i.e. one
+    channel whose points span <= 7 sample offsets, or half of a wider one;
+    ``plan_steps`` counts the steps of all M-blocks for one pair of groups."""
+    pairs = (S + 15) // 16
     flop_unit = 6 * 2 * 128 * 256 * 16
-    flops = float(tiles) * groups * C * flop_unit
+    flops = float(plan_steps) * pairs * flop_unit
     achieved = flops / (avg * 1e-3) / 1e12
     peak, source = tensor_peak()
     return {
         "bound": "tensor",
-        "kernel": "energy_tc_kernel<BOTH> (tcgen05 fp16 hi/lo split, TMEM accumulation; DAS+DMAS fused)",
+        "kernel": "energy_tch_kernel<BOTH> (tcgen05 fp16 hi/lo split, Hankel operand read in place from the "
+                  "TMA-staged planes, 8-tap K packing; TMEM accumulation; DAS+DMAS fused)",
         "achieved": achieved,
         "peak": peak,
         "unit": "TFLOP/s",
         "frac": achieved / peak,
-        "traffic": traffic.get("energy_tc_kernel_both") if isinstance(traffic, dict) else None,
+        "traffic": traffic.get("energy_tch_kernel_both") if isinstance(traffic, dict) else None,
         "algorithmic_flops_per_launch": flops,
-        "per_unit": "6 x 2 x 128 x 256 x 16 FLOP per (256-point tile, 8-scan group, channel): the K=16 tap "
-                    "window per channel x 3 split products x 2 M-blocks",
+        "mma_steps_per_pair": plan_steps,
+        "per_unit": "6 x 2 x 128 x 256 x 16 FLOP per MMA step of a (128-point M-block, 16-scan pair) item; "
+                    "steps = 8-tap K halves / 2 (one half per channel whose points span <= 7 offsets, else two)",
         "peak_source": source,
         "launch_ms": avg,
-        "note": "launch_ms brackets the whole mwb_energies_tc call: the windowed-Gram / per-scan |y| max pre-pass "
-                "(~0.29 ms), the fp16-plane pre-pass (~0.17 ms) and the tensor-core kernel; FLOPs count only the "
-                "kernel's MMAs",
+        "note": "launch_ms brackets the whole mwb_energies_tc call: the windowed-Gram / per-scan |y| max pre-pass, "
+                "the 8-scan interleaved fp16-plane pre-pass, the per-tile step plan and the tensor-core kernel; "
+                "FLOPs count only the kernel's MMAs",
     }
 
 
@@ -652,7 +657,7 @@ def run_ours(args):
     pps_launch = float(S) * P * C * W
     traffic = load_traffic()
     if bi.uses_tensor_cores:
-        roofline = tc_roofline(S, bi.n_pts, C, avg, traffic)
+        roofline = tc_roofline(S, bi.tc_plan_steps(), avg, traffic)
         # useful work against the CUDA-core formulation's co-roofline (32 pps/clk/SM)
         pps_s = pps_launch / (avg * 1e-3)
         core_peak = smem_gbs * 1e9 / 4.0

@@ -380,9 +380,9 @@ int mwb_simulate(float* out, int n_scans, int n_chan, int n_samples, int ld, con
  * self-terms come from windowed Gram entries precomputed per (scan,
  * channel, window offset j in [j_lo, j_lo + j_count)) by a pre-pass that also
  * takes each scan's max |y| (the per-scan fp16 scale).
- * Workspace: mwb_energies_tc_workspace_bytes(n_scans, n_chan, j_count).
+ * Workspace: mwb_energies_tc_workspace_bytes(n_scans, n_chan, j_count, n_pts).
  */
-int64_t mwb_energies_tc_workspace_bytes(int n_scans, int n_chan, int j_count);
+int64_t mwb_energies_tc_workspace_bytes(int n_scans, int n_chan, int j_count, int n_pts);
 int mwb_table_max_span(const void* table, int n_pts, int n_chan, int32_t* d_out, void* stream);
 /* smallest / largest per-channel span start lo over the table's non-empty
  * tiles -> d_out[0], d_out[1]; the window-offset range of mwb_energies_tc is
@@ -501,6 +501,12 @@ int mwb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitc
  * the first sample, out[1] = the count (the Gram and fp16-plane pre-passes
  * read exactly [out[0], out[0] + out[1]); samples past ld read as zeros).  A
  * host-to-device pipeline may ship only that range of each row. */
+/* K-packing statistics of the last mwb_energies_tc call (window 32) that used
+ * `workspace` with these sizes: the MMA steps of all (table tile, M-block)
+ * items of one scan-group pair (synchronous; for roofline accounting -- each
+ * step is 6 tcgen05.mma M128 x N256 x K16 per pair of 8-scan groups). */
+int mwb_tc_plan_steps(const void* workspace, int n_scans, int n_chan, int j_count, int n_pts, int window,
+                      int64_t* out_steps);
 int mwb_tc_sample_range(int k0, int j_lo, int j_count, int ld, int32_t* out);
 
 /* Elapsed milliseconds between consecutive recorded events: out_ms[i] =

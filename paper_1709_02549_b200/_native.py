@@ -111,7 +111,7 @@ _SIGNATURES = {
          _P, _I64, _P],
         _I,
     ),
-    "mwb_energies_tc_workspace_bytes": ([_I, _I, _I], _I64),
+    "mwb_energies_tc_workspace_bytes": ([_I, _I, _I, _I], _I64),
     "mwb_table_max_span": ([_P, _I, _I, _P, _P], _I),
     "mwb_table_lo_range": ([_P, _I, _I, _P, _P, _P], _I),
     "mwb_energies_tc": (
@@ -188,6 +188,7 @@ _SIGNATURES = {
     "mwb_gather_composite": ([_P, _I, _I, _P, _I, _P, _P, _I64, _P], _I),
     "mwb_memcpy_async": ([_P, _P, _I64, _P], _I),
     "mwb_memcpy2d_async": ([_P, _I64, _P, _I64, _I64, _I64, _P], _I),
+    "mwb_tc_plan_steps": ([_P, _I, _I, _I, _I, _I, _P], _I),
     "mwb_tc_sample_range": ([_I, _I, _I, _I, _P], _I),
     "mwb_elapsed_ms": ([_P, _I, _P], _I),
     "mwb_compact_payload": ([_P, _I, _I, _I, _P, _P, _P, _P, _P], _I),

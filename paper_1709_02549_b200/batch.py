@@ -205,9 +205,10 @@ class BatchImager:
                     out.zero_()
             return
         if self.mode == 2:
-            nbytes = int(nat.load().mwb_energies_tc_workspace_bytes(s, self.n_chan, self.j_count))
+            nbytes = int(nat.load().mwb_energies_tc_workspace_bytes(s, self.n_chan, self.j_count, self.n_pts))
             if self._tc_ws is None or self._tc_ws.numel() < nbytes:
                 self._tc_ws = torch.empty(nbytes, dtype=torch.uint8, device=sig.device)
+            self._tc_last_scans = s
             nat.call(
                 "mwb_energies_tc", sig.data_ptr(), s, self.n_chan * self.ld, self.n_chan, self.ld, self.n_samples,
                 self.scan.chan.data_ptr(), self.scan.ant.data_ptr(), self.scan.n_ant, self.scan.inv_scale,
@@ -224,6 +225,18 @@ class BatchImager:
             self.w, nat.ptr(out_das), nat.ptr(out_dmas), nxny, nat.ptr(key_das), nat.ptr(key_dmas), nat.ptr(flags),
             self.mode, dv.stream_handle(),
         )
+
+    def tc_plan_steps(self) -> int:
+        """MMA steps per scan-group pair of the last tensor-core call (W = 32;
+        mwb_tc_plan_steps): each step is 6 tcgen05.mma M128 x N256 x K16 for
+        two 8-scan groups, so the launch executed
+        ``steps * ceil(S / 16) * 6 * 2 * 128 * 256 * 16`` MMA FLOP."""
+        if self.mode != 2 or self._tc_ws is None or self.w != 32:
+            raise RuntimeError("no tensor-core (W = 32) call on this imager yet")
+        out = ctypes.c_int64()
+        nat.call("mwb_tc_plan_steps", self._tc_ws.data_ptr(), self._tc_last_scans, self.n_chan, self.j_count,
+                 self.n_pts, self.w, ctypes.byref(out))
+        return int(out.value)
 
     def input_range(self) -> tuple[int, int]:
         """(first, count): the samples of each channel row the device path

@@ -58,6 +58,7 @@ namespace {
 #include "mwb_segment.cuh"
 #include "mwb_microbench.cuh"
 #include "mwb_tc.cuh"
+#include "mwb_tch.cuh"
 #include "mwb_io.cuh"
 
 }  // namespace
@@ -406,6 +407,26 @@ static int encode_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1,
   return MWB_OK;
 }
 
+// rank-R tensor map (R <= 5): dims[0] contiguous, byte strides of dims 1..R-1
+static int encode_nd(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                     const uint32_t* box, CUtensorMapDataType type) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return set_err(MWB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i) st[i - 1] = strides[i - 1];
+  }
+  const CUresult r = fn(m, type, (cuuint32_t)rank, const_cast<void*>(base), d, st, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(MWB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return MWB_OK;
+}
+
 // workspace: [absmax u32 x S | gram {E, X} float4 pairs x quads*C*J | fp16 planes S*C*2*Lp]
 static size_t tc_ws_absmax(int n_scans) { return align_up(sizeof(uint32_t) * (size_t)(n_scans > 0 ? n_scans : 1), 256); }
 static size_t tc_ws_gram(int n_scans, int n_chan, int j_count) {
@@ -417,10 +438,21 @@ static size_t tc_ws_planes(int n_scans, int n_chan, int j_count) {
   return sizeof(__half) * 2 * (size_t)n_scans * (size_t)n_chan * (size_t)tc_plane_len(j_count);
 }
 
-int64_t mwb_energies_tc_workspace_bytes(int n_scans, int n_chan, int j_count) {
-  if (n_scans < 0 || n_chan < 1 || j_count < 16) return -1;
+// W = 32 (mwb_tch.cuh): 8-scan interleaved planes [G][C][2][Lp][8] and the step plan
+static size_t tc_ws_planes8(int n_scans, int n_chan, int j_count) {  // whole pairs of 8-scan groups
+  return sizeof(__half) * 2 * 16 * (size_t)((n_scans + 15) / 16) * (size_t)n_chan * (size_t)tc_plane_len(j_count);
+}
+static size_t tc_ws_plan(int n_pts, int n_chan) {  // per (tile, M-block): steps | records | last steps
+  const size_t blocks = 2 * (size_t)(n_pts > 0 ? (n_pts + TILE - 1) / TILE : 1);
+  return align_up(sizeof(int) * blocks, 256) + align_up(sizeof(uint4) * (size_t)n_chan * blocks, 256) +
+         sizeof(int) * (size_t)n_chan * blocks;
+}
+
+int64_t mwb_energies_tc_workspace_bytes(int n_scans, int n_chan, int j_count, int n_pts) {
+  if (n_scans < 0 || n_chan < 1 || j_count < 16 || n_pts < 0) return -1;
+  const size_t planes = std::max(tc_ws_planes(n_scans, n_chan, j_count), tc_ws_planes8(n_scans, n_chan, j_count));
   return (int64_t)(tc_ws_absmax(n_scans) + align_up(tc_ws_gram(n_scans, n_chan, j_count), 256) +
-                   align_up(tc_ws_planes(n_scans, n_chan, j_count), 256));
+                   align_up(planes, 256) + align_up(tc_ws_plan(n_pts, n_chan), 256));
 }
 
 int mwb_table_lo_range(const void* table, int n_pts, int n_chan, const int32_t* tile_info, int32_t* d_out,
@@ -495,6 +527,70 @@ static int launch_tc(const EnergyParams& e, int kind, int n_pts, int n_scans, in
   fn<<<grid, tc::THREADS, L.total, st>>>(P);
   return check_launch("energy_tc_kernel");
 }
+
+// W = 32: the Hankel-in-place kernel (mwb_tch.cuh)
+static int launch_tch(const EnergyParams& e, int kind, int n_pts, int n_scans, int n_chan, int j_lo, int j_count,
+                      int Lp, const uint32_t* absmax, const float4* gx, const __half* planes8, const int* plan_n,
+                      const uint4* plan, const int* plan_last, cudaStream_t st) {
+  int rc;
+  tch::Params P;
+  P.e = e;
+  P.absmax = absmax;
+  P.plan_n = plan_n;
+  P.plan = plan;
+  P.plan_last = plan_last;
+  P.j_lo = j_lo;
+  P.J = j_count;
+  P.Lp = Lp;
+  P.n_tiles = (n_pts + TILE - 1) / TILE;
+  P.n_pairs = (n_scans + tch::NGRP * tch::SPG - 1) / (tch::NGRP * tch::SPG);
+  const int quads = (n_scans + 3) / 4;
+  {
+    // planes [2 n_pairs][C][hi | lo][Lp][8] fp16, viewed as 32-bit words so that a plane's rows
+    // off + [0, ROWS) are one 896 B box row: one box = both groups' hi and lo spans of a channel
+    const uint64_t prow = 16 * (uint64_t)Lp;  // bytes per plane
+    const uint64_t dims[4] = {4 * (uint64_t)Lp, 2, (uint64_t)n_chan, 2 * (uint64_t)P.n_pairs};
+    const uint64_t strides[3] = {prow, prow * 2, prow * 2 * n_chan};
+    const uint32_t box[4] = {4 * tch::ROWS, 2, 1, tch::NGRP};
+    if ((rc = encode_nd(&P.tm_planes, planes8, 4, dims, strides, box, CU_TENSOR_MAP_DATA_TYPE_UINT32))) return rc;
+  }
+  if ((rc = encode_3d(&P.tm_gram, gx, (uint64_t)8 * j_count, (uint64_t)n_chan, (uint64_t)quads,
+                      (uint64_t)32 * j_count, (uint64_t)32 * j_count * n_chan, 128, 1, tch::QUADS,
+                      CU_TENSOR_MAP_DATA_TYPE_FLOAT32)))
+    return rc;
+  const tch::Layout L = tch::layout();
+  void (*fn)(tch::Params) = kind == KIND_DAS    ? tch::energy_tch_kernel<KIND_DAS>
+                            : kind == KIND_DMAS ? tch::energy_tch_kernel<KIND_DMAS>
+                                                : tch::energy_tch_kernel<KIND_BOTH>;
+  cudaError_t ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  if (ce != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(ce));
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long items = 2LL * P.n_tiles * P.n_pairs;
+  const unsigned grid = (unsigned)std::min<long long>(items, sms > 0 ? sms : 148);
+#ifdef MWB_TCH_PROF
+  {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(tch::tch_prof, z, sizeof(z));
+  }
+#endif
+  fn<<<grid, tch::THREADS, L.total, st>>>(P);
+#ifdef MWB_TCH_PROF
+  {
+    cudaDeviceSynchronize();
+    unsigned long long z[16];
+    cudaMemcpyFromSymbol(z, tch::tch_prof, sizeof(z));
+    const double n = (double)grid;
+    fprintf(stderr, "tch prof per CTA (Mclk): issuer total %.2f wait o_full %.2f wait acc_empty %.2f | builder0 "
+            "total %.2f o_empty %.2f s_full %.2f acc_full %.2f epilogue %.2f | producer s_empty %.2f | items %.1f "
+            "steps %.1f | producer issue %.2f total %.2f\n",
+            z[2] / n / 1e6, z[0] / n / 1e6, z[1] / n / 1e6, z[10] / n / 1e6, z[3] / n / 1e6, z[4] / n / 1e6,
+            z[5] / n / 1e6, z[6] / n / 1e6, z[7] / n / 1e6, z[8] / n, z[9] / n, z[11] / n / 1e6, z[12] / n / 1e6);
+  }
+#endif
+  return check_launch("energy_tch_kernel");
+}
 }  // extern "C++"
 
 int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
@@ -513,6 +609,7 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
     return set_err(MWB_EINVAL, "mwb_energies_tc: window must be 32 or 48 (got %d)", window);
   if (!workspace) return set_err(MWB_EINVAL, "mwb_energies_tc: null workspace");
   if (j_lo < 0 || j_count < 16) return set_err(MWB_EINVAL, "mwb_energies_tc: bad window-offset range");
+  if (n_chan > 0xFFFF) return set_err(MWB_ERANGE, "mwb_energies_tc: %d channels (at most 65535)", n_chan);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
   uint32_t* absmax = reinterpret_cast<uint32_t*>(ws);
@@ -522,18 +619,38 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
   const int Lp = tc_plane_len(j_count);
   cudaError_t ce = cudaMemsetAsync(absmax, 0, sizeof(uint32_t) * (size_t)n_scans, st);
   if (ce != cudaSuccess) return set_err(MWB_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
-  {
-    const size_t sm = sizeof(float) * 4 * (size_t)Lp;
-    if (sm > 48 * 1024) return set_err(MWB_ERANGE, "mwb_energies_tc: window-offset range %d too wide", j_count);
-    tc::gram_kernel<<<dim3((unsigned)n_chan, (unsigned)((n_scans + 3) / 4)), 128, sm, st>>>(
-        sig, scan_stride, n_scans, n_chan, ld, k0, window, j_lo, j_count, Lp, gx, absmax);
-    if ((rc = check_launch("gram_kernel"))) return rc;
-    tc::planes_kernel<<<dim3((unsigned)n_chan, (unsigned)n_scans), 128, 0, st>>>(sig, scan_stride, n_chan, ld, k0,
-                                                                                  j_lo, Lp, absmax, planes);
-    if ((rc = check_launch("planes_kernel"))) return rc;
-  }
+  const size_t sm = sizeof(float) * 4 * (size_t)Lp;
+  if (sm > 48 * 1024) return set_err(MWB_ERANGE, "mwb_energies_tc: window-offset range %d too wide", j_count);
+  tc::gram_kernel<<<dim3((unsigned)n_chan, (unsigned)((n_scans + 3) / 4)), 128, sm, st>>>(
+      sig, scan_stride, n_scans, n_chan, ld, k0, window, j_lo, j_count, Lp, gx, absmax);
+  if ((rc = check_launch("gram_kernel"))) return rc;
   const int kind = out_das && out_dmas ? KIND_BOTH : (out_das ? KIND_DAS : KIND_DMAS);
-  if (window == 32) return launch_tc<tc::Cfg32x8>(e, kind, n_pts, n_scans, n_chan, j_lo, j_count, Lp, absmax, gx, planes, st);
+  if (window == 32) {
+    // 8-scan interleaved planes, the per-tile step plan, the Hankel-in-place kernel
+    const int groups = 2 * ((n_scans + 15) / 16);  // whole pairs (the last pair's missing group is zeros)
+    const long long tiles = (n_pts + TILE - 1) / TILE;
+    unsigned char* pl = ws + tc_ws_absmax(n_scans) + align_up(tc_ws_gram(n_scans, n_chan, j_count), 256) +
+                        align_up(std::max(tc_ws_planes(n_scans, n_chan, j_count),
+                                          tc_ws_planes8(n_scans, n_chan, j_count)), 256);
+    int* plan_n = reinterpret_cast<int*>(pl);
+    uint4* plan = reinterpret_cast<uint4*>(pl + align_up(sizeof(int) * 2 * (size_t)tiles, 256));
+    int* plan_last = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(plan) +
+                                            align_up(sizeof(uint4) * (size_t)n_chan * 2 * tiles, 256));
+    tch::planes8_kernel<<<dim3((unsigned)n_chan, (unsigned)groups), 256, 0, st>>>(
+        sig, scan_stride, n_scans, n_chan, ld, k0, j_lo, Lp, absmax, planes);
+    if ((rc = check_launch("planes8_kernel"))) return rc;
+    const TableLayout T = table_layout(tiles, n_chan);
+    const unsigned char* tb = reinterpret_cast<const unsigned char*>(table);
+    tch::plan_kernel<<<(unsigned)(2 * tiles), 256, sizeof(int) * 5 * (size_t)n_chan, st>>>(
+        reinterpret_cast<const uint32_t*>(tb + T.words), reinterpret_cast<const int2*>(tile_info), n_pts, n_chan,
+        plan_n, plan, plan_last);
+    if ((rc = check_launch("plan_kernel"))) return rc;
+    return launch_tch(e, kind, n_pts, n_scans, n_chan, j_lo, j_count, Lp, absmax, gx, planes, plan_n, plan,
+                      plan_last, st);
+  }
+  tc::planes_kernel<<<dim3((unsigned)n_chan, (unsigned)n_scans), 128, 0, st>>>(sig, scan_stride, n_chan, ld, k0,
+                                                                                j_lo, Lp, absmax, planes);
+  if ((rc = check_launch("planes_kernel"))) return rc;
   if (n_scans >= 4) return launch_tc<tc::Cfg48x4>(e, kind, n_pts, n_scans, n_chan, j_lo, j_count, Lp, absmax, gx, planes, st);
   return launch_tc<tc::Cfg48x1>(e, kind, n_pts, n_scans, n_chan, j_lo, j_count, Lp, absmax, gx, planes, st);
 }
@@ -1362,6 +1479,25 @@ int mwb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitc
   const cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)height,
                                           cudaMemcpyDefault, reinterpret_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? MWB_OK : set_err(MWB_ECUDA, "cudaMemcpy2DAsync: %s", cudaGetErrorString(e));
+}
+
+int mwb_tc_plan_steps(const void* workspace, int n_scans, int n_chan, int j_count, int n_pts, int window,
+                      int64_t* out_steps) {
+  if (!workspace || !out_steps || n_scans < 1 || n_chan < 1 || j_count < 16 || n_pts < 1)
+    return set_err(MWB_EINVAL, "mwb_tc_plan_steps: bad arguments");
+  if (window != 32) return set_err(MWB_EINVAL, "mwb_tc_plan_steps: the step plan exists for window 32 only");
+  const long long blocks = 2LL * ((n_pts + TILE - 1) / TILE);
+  const unsigned char* pl = reinterpret_cast<const unsigned char*>(workspace) + tc_ws_absmax(n_scans) +
+                            align_up(tc_ws_gram(n_scans, n_chan, j_count), 256) +
+                            align_up(std::max(tc_ws_planes(n_scans, n_chan, j_count),
+                                              tc_ws_planes8(n_scans, n_chan, j_count)), 256);
+  std::vector<int> n((size_t)blocks);
+  const cudaError_t e = cudaMemcpy(n.data(), pl, sizeof(int) * (size_t)blocks, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaMemcpy: %s", cudaGetErrorString(e));
+  int64_t total = 0;
+  for (int v : n) total += v;
+  *out_steps = total;
+  return MWB_OK;
 }
 
 int mwb_tc_sample_range(int k0, int j_lo, int j_count, int ld, int32_t* out) {

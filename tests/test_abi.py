@@ -135,9 +135,15 @@ def test_tensor_core_entry_argument_errors(lib):
     assert lib.mwb_energies_tc(*tc_args(out_das=None)) == -1
     assert b"no output" in lib.mwb_last_error()
     assert lib.mwb_energies_tc(*tc_args(n_pts=0)) == 0  # nothing to do
-    assert lib.mwb_energies_tc_workspace_bytes(8, 66, 8) == -1
-    small = lib.mwb_energies_tc_workspace_bytes(8, 66, 64)
-    assert small >= 2 * 16 * 2 * 66 * 64 and lib.mwb_energies_tc_workspace_bytes(4096, 66, 152) > 4096 * 66 * 152 * 8
+    assert lib.mwb_energies_tc_workspace_bytes(8, 66, 8, 256) == -1
+    assert lib.mwb_energies_tc_workspace_bytes(8, 66, 64, -1) == -1
+    small = lib.mwb_energies_tc_workspace_bytes(8, 66, 64, 256)
+    assert small >= 2 * 16 * 2 * 66 * 64 + 8 * 66 * 4
+    assert lib.mwb_energies_tc_workspace_bytes(4096, 66, 152, 65536) > 4096 * 66 * 152 * 8 + 256 * 8 * 66 * 4
+    steps = ctypes.c_int64()
+    assert lib.mwb_tc_plan_steps(None, 8, 66, 64, 256, 32, ctypes.byref(steps)) == -1
+    assert lib.mwb_tc_plan_steps(ctypes.c_void_p(16), 8, 66, 64, 256, 48, ctypes.byref(steps)) == -1
+    assert b"window 32" in lib.mwb_last_error()
     assert lib.mwb_table_max_span(None, 10, 66, None, None) == -1
     assert lib.mwb_table_lo_range(None, 10, 66, None, None, None) == -1
     assert lib.mwb_lattice_tile_count(256, 256, 1) == 256
