@@ -61,6 +61,9 @@ static_assert(32 % PCH == 0 && PCH <= NS, "producer rounds");
 constexpr int NG = MWB_TCH_GROUPS;            // builder groups (step t -> builder group t % NG)
 constexpr int GW = 8;
 constexpr int NBW = NG * GW, NBT = NBW * 32;
+// a slot released at step first_c + NG (plan_kernel) is refilled for a channel
+// NS channels later, consumed >= NS / 2 steps after first_c: after the release
+static_assert(NS / 2 > NG, "staging ring too shallow for the Q release slack");
 constexpr int THREADS = NBT + 64;             // + producer warp + MMA warp
 constexpr int ROWS = 56;                      // staged rows per plane: r + m + k <= 22 + 7 + 31 (wide) / 14 + 7 + 31
 constexpr int PLANE_B = ROWS * 16;            // 896 B per plane
@@ -69,7 +72,16 @@ constexpr int STAGE_B = NGRP * GPL_B;         // both groups
 constexpr int A_B = ROWS_M * K * 2;           // one of hi / lo: 4 KB
 constexpr int OP_B = 2 * A_B;
 constexpr int QUADS = NGRP * SPG / 4;         // Gram quads per item
-constexpr int GQ_FLOAT4 = QUADS * 2 * 16;     // quads x 16 positions x {E, X}
+#ifndef MWB_TCH_GREC
+#define MWB_TCH_GREC 8
+#endif
+// Gram record per (quad, position j): {E, X} float4s, padded to 48 bytes so
+// that a warp's LDS.128 of E(d) / X(d) / E(d + 1) over rows whose d spans up
+// to 8 consecutive values hits 8 distinct 16-byte bank groups (a 32-byte
+// record maps d and d + 4 to the same banks)
+constexpr int GREC = MWB_TCH_GREC;            // floats per record (8: unpadded)
+constexpr int GR4 = GREC / 4;                 // float4s per record
+constexpr int GQ_FLOAT4 = QUADS * GR4 * 16;   // quads x 16 positions x record
 constexpr int TMEM_COLS = 512;
 // kind::f16, f32 accumulate, A K-major, B MN-major (bit 16), N = 256, M = 128
 constexpr uint32_t IDESC = (1u << 4) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -94,12 +106,27 @@ __host__ __device__ inline Layout layout() {
   return L;
 }
 
-// plan half word: bit 31 valid, bit 30 the channel's first half, bits 16..21
-// the half's first row r (offset past lo_c), bits 0..15 the channel
+// plan half word: bit 31 valid, bit 30 the channel's first half, bit 27
+// (c / NS) & 1 and bits 22..26 c % NS (the channel's staging-ring position
+// relative to the item's first channel), bits 16..21 the half's first row r
+// (offset past lo_c), bits 0..15 the channel c
 __device__ __forceinline__ bool hv_valid(uint32_t h) { return h >> 31; }
 __device__ __forceinline__ bool hv_first(uint32_t h) { return (h >> 30) & 1u; }
 __device__ __forceinline__ int hv_row(uint32_t h) { return (int)((h >> 16) & 63u); }
 __device__ __forceinline__ int hv_chan(uint32_t h) { return (int)(h & 0xFFFFu); }
+__host__ __device__ constexpr uint32_t hv_ring_bits(int c) {
+  return ((uint32_t)(c % NS) << 22) | ((uint32_t)((c / NS) & 1) << 27);
+}
+// Staging slot of a half's channel and the parity of its fill: the item's
+// channels start at ring position tcb (tr = tcb % NS, tq = (tcb / NS) & 1), so
+// channel c sits at (tcb + c) % NS, filled in phase ((tcb + c) / NS) & 1
+__device__ __forceinline__ int hv_slot(uint32_t h, int tr, int tq, uint32_t& parity) {
+  int s = tr + (int)((h >> 22) & 31u);
+  const int carry = s >= NS ? 1 : 0;
+  s -= carry * NS;
+  parity = (uint32_t)(tq ^ (int)((h >> 27) & 1u) ^ carry);
+  return s;
+}
 
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -114,6 +141,32 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       "[%6];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"(smem_u32(bar))
       : "memory");
+}
+
+#ifndef MWB_TCH_COLLECTOR
+#define MWB_TCH_COLLECTOR 1
+#endif
+// tcgen05.mma with an A-collector usage: FILL reads A from shared memory and
+// keeps it, USE / LASTUSE take the kept A (LASTUSE then frees it); the MMAs of
+// one fill..lastuse run are issued back to back with the same A descriptor
+enum { CA_FILL, CA_USE, CA_LASTUSE };
+template <int U>
+__device__ __forceinline__ void mma_ca(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  if constexpr (U == CA_FILL)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  else if constexpr (U == CA_USE)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16.collector::a::use [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void builders_sync_tch() { asm volatile("bar.sync 1, %0;" ::"n"(NBT) : "memory"); }
@@ -135,11 +188,9 @@ struct alignas(64) Params {
 };
 
 // Stage-relative byte address of a half's first B row (group 0, hi plane).
-__device__ __forceinline__ uint32_t half_addr(uint32_t h, int tcb) {
-  return (uint32_t)(((tcb + hv_chan(h)) % NS) * STAGE_B + hv_row(h) * 16);
-}
-__device__ __forceinline__ bool halves_swapped(uint32_t h0, uint32_t h1, int tcb) {
-  return hv_valid(h1) && half_addr(h1, tcb) < half_addr(h0, tcb);
+__device__ __forceinline__ uint32_t half_addr(uint32_t h, int tr, int tq) {
+  uint32_t par;
+  return (uint32_t)(hv_slot(h, tr, tq, par) * STAGE_B + hv_row(h) * 16);
 }
 
 // points of M-block mb of table tile `tile` (<= 0: nothing to do)
@@ -242,7 +293,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
           if (off != lo_c - P.j_lo && p.flags) atomicOr(p.flags, 4);
           mbar_arrive_expect_tx(&s_full[slot], (uint32_t)(STAGE_B + GQ_FLOAT4 * 16));
           tma_load_4d(stage + slot * STAGE_B, &P.tm_planes, 4 * off, 0, c, NGRP * pair, &s_full[slot]);
-          tc::tma_load_3d(const_cast<float4*>(gstage) + slot * GQ_FLOAT4, &P.tm_gram, 8 * off, c, QUADS * pair,
+          tc::tma_load_3d(const_cast<float4*>(gstage) + slot * GQ_FLOAT4, &P.tm_gram, GREC * off, c, QUADS * pair,
                           &s_full[slot]);
         }
         __syncwarp();
@@ -277,10 +328,27 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
             const uint64_t b_hi = b0 + (uint64_t)((g * GPL_B) >> 4);  // start-address field
             const uint64_t b_lo = b_hi + (PLANE_B >> 4);
             const uint32_t d = tmem + (uint32_t)(g * N);
+#if MWB_TCH_COLLECTOR
+            // A_hi is read from shared memory once for its four products and
+            // A_lo once for its two (the A collector buffer), 64 instead of
+            // 192 operand wavefronts per step
+            if (g == 0) {
+              mma_ca<CA_FILL>(d, a_hi, b_hi, IDESC, i > 0 ? 1u : 0u);
+              mma_ca<CA_USE>(d, a_hi, b_lo, IDESC, 1u);
+            } else {
+              mma_ca<CA_USE>(d, a_hi, b_hi, IDESC, i > 0 ? 1u : 0u);
+              mma_ca<CA_LASTUSE>(d, a_hi, b_lo, IDESC, 1u);
+            }
+#else
             tc::mma(d, a_hi, b_hi, IDESC, i > 0 ? 1u : 0u);
             tc::mma(d, a_hi, b_lo, IDESC, 1u);
             tc::mma(d, a_lo, b_hi, IDESC, 1u);
+#endif
           }
+#if MWB_TCH_COLLECTOR
+          mma_ca<CA_FILL>(tmem, a_lo, b0, IDESC, 1u);
+          mma_ca<CA_LASTUSE>(tmem + (uint32_t)N, a_lo, b0 + (uint64_t)(GPL_B >> 4), IDESC, 1u);
+#endif
           tc::commit(&done[t % DR]);
           if (i + 1 == nst) tc::commit(acc_full);
         }
@@ -305,6 +373,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
       const int nsg = min(SPG, p.n_scans - grp * SPG);
       const int nst = __ldg(P.plan_n + blk);
       const uint4* rec = P.plan + (size_t)blk * p.C;
+      const int tr = tcb % NS, tq = (tcb / NS) & 1;
       float q[SPG];
 #pragma unroll
       for (int s = 0; s < SPG; ++s) q[s] = 0.f;
@@ -340,26 +409,20 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
         const int ts = t + i, oslot = ts % NO;
         if (ts >= NO) PROF_T(3, mbar_wait(&done[(ts - NO) % DR], ((ts - NO) / DR) & 1));
         unsigned char* op = ops + (size_t)oslot * OP_B;
-        const bool swap = halves_swapped(cur.x, cur.y, tcb);
-        if (w8 == 0 && lane == 0) {
-          // the step's B operand (group 0, hi plane): the two halves' rows in
-          // address order, LBO = their distance (a missing second half reads
-          // the next row; its A half is zero)
-          uint32_t a0 = half_addr(cur.x, tcb), a1 = hv_valid(cur.y) ? half_addr(cur.y, tcb) : a0 + 16;
-          if (swap) {
-            const uint32_t x = a0;
-            a0 = a1;
-            a1 = x;
-          }
-          meta[oslot] = desc(smem_u32(stage) + a0, a1 - a0, 16);
-        }
+        // the step's B operand (group 0, hi plane): the two halves' rows in
+        // address order, LBO = their distance (a missing second half reads
+        // the next row; its A half is zero)
+        uint32_t a0 = half_addr(cur.x, tr, tq), a1 = hv_valid(cur.y) ? half_addr(cur.y, tr, tq) : a0 + 16;
+        const bool swap = a1 < a0;
+        if (w8 == 0 && lane == 0) meta[oslot] = desc(smem_u32(stage) + min(a0, a1), swap ? a0 - a1 : a1 - a0, 16);
         // ---- A: K half kh holds plan half kh ^ swap
         {
           const uint32_t hw = (kh ^ (swap ? 1 : 0)) ? cur.y : cur.x;
           uint32_t hi[4] = {0u, 0u, 0u, 0u}, lo[4] = {0u, 0u, 0u, 0u};
           if (hv_valid(hw)) {  // warp-uniform
-            const int c = hv_chan(hw), slot = (tcb + c) % NS;
-            PROF_T(4, mbar_wait(&s_full[slot], ((tcb + c) / NS) & 1));
+            uint32_t par;
+            const int slot = hv_slot(hw, tr, tq, par);
+            PROF_T(4, mbar_wait(&s_full[slot], par));
             const uint32_t w = (kh ^ (swap ? 1 : 0)) ? wh1 : wh0;
             const int rel = (int)(w >> 23) - hv_row(hw);  // f0 at tap rel of this half, f1 at rel + 1
             const float f1 = weight_f1(w);
@@ -382,34 +445,38 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
           *reinterpret_cast<uint4*>(op + tc::kmajor_off(row, kh)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
           *reinterpret_cast<uint4*>(op + A_B + tc::kmajor_off(row, kh)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
         }
-        // ---- Q of the channels starting in this step, for scan group kh (read
-        // before the step is released: its MMAs may free the channel's slot):
+        tc::fence_async_smem();  // A generic writes -> visible to the tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_full[oslot]);
+        // ---- Q of the channels starting in this step, for scan group kh, after
+        // the step's A rows are published (a channel's staging slot is released
+        // no earlier than the step NG after its first, which this group builds
+        // only once these reads are done; plan_kernel):
         // Q += f0^2 e(d) + 2 f0 f1 x(d) + f1^2 e(d + 1), 4 scans per LDS.128
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t hw = h ? cur.y : cur.x;
           if (!hv_valid(hw) || !hv_first(hw)) continue;  // warp-uniform
-          const int c = hv_chan(hw), slot = (tcb + c) % NS;
-          PROF_T(4, mbar_wait(&s_full[slot], ((tcb + c) / NS) & 1));
+          uint32_t par;
+          const int slot = hv_slot(hw, tr, tq, par);
+          PROF_T(4, mbar_wait(&s_full[slot], par));
           const uint32_t w = h ? wh1 : wh0;
           const int d = (int)(w >> 23);
           if (d - hv_row(hw) > K - 2 || d > K - 2) bad_span = true;  // beyond the two halves / the Gram slice
           const int dg = min(d, K - 2);
           const float f1 = weight_f1(w), f0 = 1.0f - f1;
           const float w0 = f0 * f0, w1 = 2.f * f0 * f1, w2 = f1 * f1;
-          const float4* gsl = gstage + slot * GQ_FLOAT4 + kh * 2 * 32;
+          const float4* gsl = gstage + slot * GQ_FLOAT4 + kh * 2 * 16 * GR4;
 #pragma unroll
           for (int qd = 0; qd < 2; ++qd) {
-            const float4 E = gsl[qd * 32 + 2 * dg], X = gsl[qd * 32 + 2 * dg + 1], E1 = gsl[qd * 32 + 2 * dg + 2];
+            const float4* gr = gsl + qd * 16 * GR4 + GR4 * dg;
+            const float4 E = gr[0], X = gr[1], E1 = gr[GR4];
             q[4 * qd + 0] = fmaf(w0, E.x, fmaf(w1, X.x, fmaf(w2, E1.x, q[4 * qd + 0])));
             q[4 * qd + 1] = fmaf(w0, E.y, fmaf(w1, X.y, fmaf(w2, E1.y, q[4 * qd + 1])));
             q[4 * qd + 2] = fmaf(w0, E.z, fmaf(w1, X.z, fmaf(w2, E1.z, q[4 * qd + 2])));
             q[4 * qd + 3] = fmaf(w0, E.w, fmaf(w1, X.w, fmaf(w2, E1.w, q[4 * qd + 3])));
           }
         }
-        tc::fence_async_smem();  // A generic writes -> visible to the tensor core
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&o_full[oslot]);
       }
       t += nst;
       tcb += p.C;
@@ -436,12 +503,15 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
 #pragma unroll
           for (int s = 0; s < SPG; ++s) e[s] = fmaf(v[s + 8], v[s + 8], fmaf(v[s], v[s], e[s]));
         }
+        // this warp's TMEM reads are complete (tcgen05.wait::ld): once every
+        // builder warp has arrived the next item's MMAs may overwrite TMEM
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
 #pragma unroll
         for (int s = 0; s < SPG; ++s) ex[((gp * NGRP + kh) * SPG + s) * ROWS_M + row] = e[s];
       }
-      tc::fence_before();
       builders_sync_tch();
-      if (lane == 0) mbar_arrive(acc_empty);  // TMEM read by every warp: the next item's MMAs may start
       const bool valid = row < n_in;
       const int g = tile * TILE + mb * ROWS_M + (valid ? row : 0);
       const int slot_out = valid ? (p.out_idx ? __ldg(p.out_idx + g) : g) : -1;
@@ -608,11 +678,17 @@ __global__ void __launch_bounds__(256) plan_kernel(const uint32_t* __restrict__ 
         continue;
       }
       const int c = hch[hi_] & 0xFFFF, second = hch[hi_] >> 16;
-      hw[k] = (1u << 31) | (second ? 0u : (1u << 30)) | ((uint32_t)(r0[c] + 8 * second) << 16) | (uint32_t)c;
+      hw[k] = (1u << 31) | (second ? 0u : (1u << 30)) | hv_ring_bits(c) | ((uint32_t)(r0[c] + 8 * second) << 16) |
+              (uint32_t)c;
     }
     out[s] = make_uint4(hw[0], hw[1], 0u, 0u);
   }
-  for (int c = tid; c < C; c += blockDim.x) plan_last[(size_t)blk * C + c] = (h0[c] + cnt[c] - 1) >> 1;
+  // the step whose completion releases channel c's staging slot: its last
+  // step, and no earlier than NG steps after its first (the builder group
+  // that gathers the channel's Q entries after publishing that step's A rows
+  // has then moved on)
+  for (int c = tid; c < C; c += blockDim.x)
+    plan_last[(size_t)blk * C + c] = max((h0[c] + cnt[c] - 1) >> 1, (h0[c] >> 1) + NG);
   if (tid == 0) plan_n[blk] = nst;
 }
 
