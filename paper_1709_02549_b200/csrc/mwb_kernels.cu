@@ -429,10 +429,8 @@ static int encode_nd(CUtensorMap* m, const void* base, int rank, const uint64_t*
 
 // workspace: [absmax u32 x S | gram {E, X} float4 pairs x quads*C*J | fp16 planes S*C*2*Lp]
 static size_t tc_ws_absmax(int n_scans) { return align_up(sizeof(uint32_t) * (size_t)(n_scans > 0 ? n_scans : 1), 256); }
-// Gram records {E, X} float4s per (quad, channel, j): 2 float4s for the W = 48
-// kernel, tch::GR4 (padded) for W = 32
 static size_t tc_ws_gram(int n_scans, int n_chan, int j_count) {
-  return std::max(2, tch::GR4) * sizeof(float4) * (size_t)((n_scans + 3) / 4) * (size_t)n_chan * (size_t)j_count;
+  return 2 * sizeof(float4) * (size_t)((n_scans + 3) / 4) * (size_t)n_chan * (size_t)j_count;
 }
 // plane length: the staged box [x0, x0 + SPANH) with x0 <= J - 16, 16-byte rows
 static int tc_plane_len(int j_count) { return (j_count - 16 + tc::SPANH_MAX + 7) & ~7; }
@@ -556,9 +554,8 @@ static int launch_tch(const EnergyParams& e, int kind, int n_pts, int n_scans, i
     const uint32_t box[4] = {4 * tch::ROWS, 2, 1, tch::NGRP};
     if ((rc = encode_nd(&P.tm_planes, planes8, 4, dims, strides, box, CU_TENSOR_MAP_DATA_TYPE_UINT32))) return rc;
   }
-  if ((rc = encode_3d(&P.tm_gram, gx, (uint64_t)tch::GREC * j_count, (uint64_t)n_chan, (uint64_t)quads,
-                      (uint64_t)4 * tch::GREC * j_count, (uint64_t)4 * tch::GREC * j_count * n_chan, 16 * tch::GREC, 1,
-                      tch::QUADS,
+  if ((rc = encode_3d(&P.tm_gram, gx, (uint64_t)8 * j_count, (uint64_t)n_chan, (uint64_t)quads,
+                      (uint64_t)32 * j_count, (uint64_t)32 * j_count * n_chan, 128, 1, tch::QUADS,
                       CU_TENSOR_MAP_DATA_TYPE_FLOAT32)))
     return rc;
   const tch::Layout L = tch::layout();
@@ -590,6 +587,8 @@ static int launch_tch(const EnergyParams& e, int kind, int n_pts, int n_scans, i
             "steps %.1f | producer issue %.2f total %.2f\n",
             z[2] / n / 1e6, z[0] / n / 1e6, z[1] / n / 1e6, z[10] / n / 1e6, z[3] / n / 1e6, z[4] / n / 1e6,
             z[5] / n / 1e6, z[6] / n / 1e6, z[7] / n / 1e6, z[8] / n, z[9] / n, z[11] / n / 1e6, z[12] / n / 1e6);
+    fprintf(stderr, "tch prof builder0 per item step (clk): A section %.0f  Q + loop section %.0f\n",
+            (double)z[13] / z[9], (double)z[14] / z[9]);
   }
 #endif
   return check_launch("energy_tch_kernel");
@@ -625,7 +624,7 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
   const size_t sm = sizeof(float) * 4 * (size_t)Lp;
   if (sm > 48 * 1024) return set_err(MWB_ERANGE, "mwb_energies_tc: window-offset range %d too wide", j_count);
   tc::gram_kernel<<<dim3((unsigned)n_chan, (unsigned)((n_scans + 3) / 4)), 128, sm, st>>>(
-      sig, scan_stride, n_scans, n_chan, ld, k0, window, j_lo, j_count, Lp, gx, absmax, window == 32 ? tch::GR4 : 2);
+      sig, scan_stride, n_scans, n_chan, ld, k0, window, j_lo, j_count, Lp, gx, absmax);
   if ((rc = check_launch("gram_kernel"))) return rc;
   const int kind = out_das && out_dmas ? KIND_BOTH : (out_das ? KIND_DAS : KIND_DMAS);
   if (window == 32) {

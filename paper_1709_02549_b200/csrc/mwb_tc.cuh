@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tc_kernel(const __grid_cons
 // per-scan power-of-two scale.
 __global__ void __launch_bounds__(128) gram_kernel(const float* sig, long long scan_stride, int n_scans, int C,
                                                    int ld, int k0, int win, int j_lo, int J, int R, float4* gx,
-                                                   uint32_t* absmax, int rec4) {
+                                                   uint32_t* absmax) {
   extern __shared__ float yq[];  // [4][R], R >= J + win + 1: the planes' range (the |y| max covers it)
   __shared__ uint32_t wmax[4][4];
   const int c = blockIdx.x, quad = blockIdx.y, tid = threadIdx.x;
@@ -580,8 +580,8 @@ __global__ void __launch_bounds__(128) gram_kernel(const float* sig, long long s
       e[sq] = a;
       x[sq] = b;
     }
-    gx[rec4 * (row_out + jj)] = make_float4(e[0], e[1], e[2], e[3]);
-    gx[rec4 * (row_out + jj) + 1] = make_float4(x[0], x[1], x[2], x[3]);
+    gx[2 * (row_out + jj)] = make_float4(e[0], e[1], e[2], e[3]);
+    gx[2 * (row_out + jj) + 1] = make_float4(x[0], x[1], x[2], x[3]);
   }
 }
 

@@ -15,8 +15,10 @@
 //     TMA-staged planes (scripts/tc_hankel_probe.cu checks this bit-exactly,
 //     and at the K-major operand's 128 clk per M128 x N256 x K16 MMA);
 //   * the two 8-tap K halves of one MMA may come from two different channels'
-//     staged spans: LBO is set per step to their address difference (the
-//     halves swapped when it would be negative).
+//     staged spans: LBO is set per step to their address difference.  The
+//     halves of a step are consecutive (one channel, or the next one); a
+//     channel staged in ring slot 0 is also copied to a mirror slot past the
+//     ring's end, so the second half always lies above the first (LBO > 0).
 // K is therefore packed in 8-tap halves.  A work item is one M-block (128
 // points of a table tile) and a pair of 8-scan groups.  Per (M-block, channel)
 // the points' exact delay-offset range [dmin, dmax] (from the table words)
@@ -24,14 +26,17 @@
 // pair) and two halves otherwise (<= 14, the tensor-core path's
 // precondition).  Halves are laid out channel after channel and cut into
 // K = 16 steps (plan_kernel), so an item costs ceil(halves / 2) MMA steps
-// instead of one per channel (configs[3]: about 45 instead of 66).
+// instead of one per channel (configs[3]: about 40 instead of 66).
 //
 // Per step the builders write only the A rows (interpolation weights, hi/lo:
 // thread (row, kh) writes K half kh of row `row`, 8 KB per step), used by the
-// MMAs of both scan groups, and add the DMAS self-terms Q of the channels
-// whose first half is in the step (Gram entries, as in mwb_tc.cuh) for their
-// group kh.  The issuer's one commit per step (done[t % DR]) frees the
-// step's operand slot and, at a channel's last step, its staging slot.
+// MMAs of both scan groups (A_hi read once for its four products, A_lo once
+// for its two: the A collector buffer); warp 0 of the step's group also waits
+// for the two staged channels and writes the B descriptor.  After publishing
+// A each builder adds the DMAS self-terms Q of the channels whose first half
+// is in the step (Gram entries, as in mwb_tc.cuh) for its group kh.  The
+// issuer's one commit per step (done[t % DR]) frees the step's operand slot
+// and, at a channel's last step, its staging slot.
 // TMEM: lane = row, column = 256 g + 8 k + s for scan s of group g.
 
 namespace tch {
@@ -72,16 +77,7 @@ constexpr int STAGE_B = NGRP * GPL_B;         // both groups
 constexpr int A_B = ROWS_M * K * 2;           // one of hi / lo: 4 KB
 constexpr int OP_B = 2 * A_B;
 constexpr int QUADS = NGRP * SPG / 4;         // Gram quads per item
-#ifndef MWB_TCH_GREC
-#define MWB_TCH_GREC 8
-#endif
-// Gram record per (quad, position j): {E, X} float4s, padded to 48 bytes so
-// that a warp's LDS.128 of E(d) / X(d) / E(d + 1) over rows whose d spans up
-// to 8 consecutive values hits 8 distinct 16-byte bank groups (a 32-byte
-// record maps d and d + 4 to the same banks)
-constexpr int GREC = MWB_TCH_GREC;            // floats per record (8: unpadded)
-constexpr int GR4 = GREC / 4;                 // float4s per record
-constexpr int GQ_FLOAT4 = QUADS * GR4 * 16;   // quads x 16 positions x record
+constexpr int GQ_FLOAT4 = QUADS * 2 * 16;     // quads x 16 positions x {E, X}
 constexpr int TMEM_COLS = 512;
 // kind::f16, f32 accumulate, A K-major, B MN-major (bit 16), N = 256, M = 128
 constexpr uint32_t IDESC = (1u << 4) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -94,7 +90,7 @@ __host__ __device__ inline Layout layout() {
   Layout L;
   size_t o = 0;
   L.ops = o;   o += (size_t)NO * OP_B;
-  L.stage = o; o += (size_t)NS * STAGE_B;
+  L.stage = o; o += (size_t)(NS + 1) * STAGE_B;              // + the mirror of slot 0 (see the producer)
   L.g = o;     o += (size_t)NS * GQ_FLOAT4 * 16;
   L.qx = o;    o += (size_t)NG * NGRP * SPG * ROWS_M * 4;  // Q partials per builder group
   L.ex = o;    o += (size_t)NG * NGRP * SPG * ROWS_M * 4;  // DAS partial sums per builder group
@@ -187,11 +183,6 @@ struct alignas(64) Params {
   int j_lo, J, Lp, n_tiles, n_pairs;
 };
 
-// Stage-relative byte address of a half's first B row (group 0, hi plane).
-__device__ __forceinline__ uint32_t half_addr(uint32_t h, int tr, int tq) {
-  uint32_t par;
-  return (uint32_t)(hv_slot(h, tr, tq, par) * STAGE_B + hv_row(h) * 16);
-}
 
 // points of M-block mb of table tile `tile` (<= 0: nothing to do)
 __device__ __forceinline__ int block_points(const EnergyParams& p, int tile, int mb, int n_pts) {
@@ -291,9 +282,13 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
           const int c = c0 + lane, slot = (t + lane) % NS;
           const int off = min(max(lo_c - P.j_lo, 0), P.J - 16);
           if (off != lo_c - P.j_lo && p.flags) atomicOr(p.flags, 4);
-          mbar_arrive_expect_tx(&s_full[slot], (uint32_t)(STAGE_B + GQ_FLOAT4 * 16));
+          // a channel in slot 0 also lands in the mirror slot NS: a step whose
+          // second half (the next channel) wraps around the ring reads it there,
+          // above its first half, so that the two halves' LBO is positive
+          mbar_arrive_expect_tx(&s_full[slot], (uint32_t)((slot == 0 ? 2 : 1) * STAGE_B + GQ_FLOAT4 * 16));
           tma_load_4d(stage + slot * STAGE_B, &P.tm_planes, 4 * off, 0, c, NGRP * pair, &s_full[slot]);
-          tc::tma_load_3d(const_cast<float4*>(gstage) + slot * GQ_FLOAT4, &P.tm_gram, GREC * off, c, QUADS * pair,
+          if (slot == 0) tma_load_4d(stage + NS * STAGE_B, &P.tm_planes, 4 * off, 0, c, NGRP * pair, &s_full[0]);
+          tc::tma_load_3d(const_cast<float4*>(gstage) + slot * GQ_FLOAT4, &P.tm_gram, 8 * off, c, QUADS * pair,
                           &s_full[slot]);
         }
         __syncwarp();
@@ -307,7 +302,8 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
   } else if (warp == NBW + 1) {
     // ===== MMA issuer: the whole warp runs the loop (warp-uniform values),
     // one elected lane issues.  Per step 6 MMAs (2 scan groups x 3 split
-    // products) and one commit to done[t % DR]
+    // products; the B descriptor from the step's builders) and one commit to
+    // done[t % DR]
     int t = 0, it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int blk = item % n_blocks;
@@ -408,22 +404,36 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
         }
         const int ts = t + i, oslot = ts % NO;
         if (ts >= NO) PROF_T(3, mbar_wait(&done[(ts - NO) % DR], ((ts - NO) / DR) & 1));
+#ifdef MWB_TCH_PROF
+        const long long _ta = clock64();
+#endif
         unsigned char* op = ops + (size_t)oslot * OP_B;
-        // the step's B operand (group 0, hi plane): the two halves' rows in
-        // address order, LBO = their distance (a missing second half reads
-        // the next row; its A half is zero)
-        uint32_t a0 = half_addr(cur.x, tr, tq), a1 = hv_valid(cur.y) ? half_addr(cur.y, tr, tq) : a0 + 16;
-        const bool swap = a1 < a0;
-        if (w8 == 0 && lane == 0) meta[oslot] = desc(smem_u32(stage) + min(a0, a1), swap ? a0 - a1 : a1 - a0, 16);
-        // ---- A: K half kh holds plan half kh ^ swap
+        if (w8 == 0) {
+          // the step's B operand (group 0, hi plane): the two halves' rows in
+          // address order -- they are consecutive (the same channel, or the
+          // next one, whose slot wraps to the mirror slot NS); a missing
+          // second half reads the next row (its A half is zero).  This warp
+          // waits for both staged channels, so that the step's o_full implies
+          // them.
+          uint32_t p0, p1 = 0u;
+          const int s0 = hv_slot(cur.x, tr, tq, p0);
+          int s1 = s0;
+          if (hv_valid(cur.y)) {
+            s1 = hv_slot(cur.y, tr, tq, p1);
+            if (s1 < s0) s1 += NS;
+          }
+          PROF_T(4, mbar_wait(&s_full[s0], p0));
+          if (s1 != s0) PROF_T(4, mbar_wait(&s_full[s1 == NS ? 0 : s1], p1));
+          const uint32_t a0 = (uint32_t)(s0 * STAGE_B + hv_row(cur.x) * 16);
+          const uint32_t a1 = hv_valid(cur.y) ? (uint32_t)(s1 * STAGE_B + hv_row(cur.y) * 16) : a0 + 16u;
+          if (lane == 0) meta[oslot] = desc(smem_u32(stage) + a0, a1 - a0, 16);
+        }
+        // ---- A: K half kh holds plan half kh (the interpolation weights)
         {
-          const uint32_t hw = (kh ^ (swap ? 1 : 0)) ? cur.y : cur.x;
+          const uint32_t hw = kh ? cur.y : cur.x;
           uint32_t hi[4] = {0u, 0u, 0u, 0u}, lo[4] = {0u, 0u, 0u, 0u};
           if (hv_valid(hw)) {  // warp-uniform
-            uint32_t par;
-            const int slot = hv_slot(hw, tr, tq, par);
-            PROF_T(4, mbar_wait(&s_full[slot], par));
-            const uint32_t w = (kh ^ (swap ? 1 : 0)) ? wh1 : wh0;
+            const uint32_t w = kh ? wh1 : wh0;
             const int rel = (int)(w >> 23) - hv_row(hw);  // f0 at tap rel of this half, f1 at rel + 1
             const float f1 = weight_f1(w);
             uint32_t f0h, f0l;
@@ -448,6 +458,10 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
         tc::fence_async_smem();  // A generic writes -> visible to the tensor core
         __syncwarp();
         if (lane == 0) mbar_arrive(&o_full[oslot]);
+#ifdef MWB_TCH_PROF
+        const long long _tq = clock64();
+        prof[12] += _tq - _ta;
+#endif
         // ---- Q of the channels starting in this step, for scan group kh, after
         // the step's A rows are published (a channel's staging slot is released
         // no earlier than the step NG after its first, which this group builds
@@ -466,17 +480,20 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
           const int dg = min(d, K - 2);
           const float f1 = weight_f1(w), f0 = 1.0f - f1;
           const float w0 = f0 * f0, w1 = 2.f * f0 * f1, w2 = f1 * f1;
-          const float4* gsl = gstage + slot * GQ_FLOAT4 + kh * 2 * 16 * GR4;
+          const float4* gsl = gstage + slot * GQ_FLOAT4 + kh * 2 * 16 * 2;
 #pragma unroll
           for (int qd = 0; qd < 2; ++qd) {
-            const float4* gr = gsl + qd * 16 * GR4 + GR4 * dg;
-            const float4 E = gr[0], X = gr[1], E1 = gr[GR4];
+            const float4* gr = gsl + qd * 32 + 2 * dg;
+            const float4 E = gr[0], X = gr[1], E1 = gr[2];
             q[4 * qd + 0] = fmaf(w0, E.x, fmaf(w1, X.x, fmaf(w2, E1.x, q[4 * qd + 0])));
             q[4 * qd + 1] = fmaf(w0, E.y, fmaf(w1, X.y, fmaf(w2, E1.y, q[4 * qd + 1])));
             q[4 * qd + 2] = fmaf(w0, E.z, fmaf(w1, X.z, fmaf(w2, E1.z, q[4 * qd + 2])));
             q[4 * qd + 3] = fmaf(w0, E.w, fmaf(w1, X.w, fmaf(w2, E1.w, q[4 * qd + 3])));
           }
         }
+#ifdef MWB_TCH_PROF
+        prof[13] += clock64() - _tq;
+#endif
       }
       t += nst;
       tcb += p.C;
@@ -557,7 +574,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
   }
 #ifdef MWB_TCH_PROF
   prof[2] = clock64() - t_start;
-  // issuer lane 0: 0, 1, 2; builder warp 0 lane 0: 3..6, 8, 9, 10; producer lane 0: 7
+  // issuer lane 0: 0, 1, 2; builder warp 0 lane 0: 3..6, 8, 9, 10, 12, 13; producer lane 0: 7
   if (warp == NBW + 1 && lane == 0) {
     atomicAdd(&tch_prof[0], prof[0]);
     atomicAdd(&tch_prof[1], prof[1]);
@@ -565,6 +582,8 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
   }
   if (warp == 0 && lane == 0) {
     for (int k = 3; k <= 6; ++k) atomicAdd(&tch_prof[k], prof[k]);
+    atomicAdd(&tch_prof[13], prof[12]);
+    atomicAdd(&tch_prof[14], prof[13]);
     atomicAdd(&tch_prof[8], prof[8]);
     atomicAdd(&tch_prof[9], prof[9]);
     atomicAdd(&tch_prof[10], prof[2]);
