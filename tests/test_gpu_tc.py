@@ -203,3 +203,33 @@ def test_tc_window_48(setup, n_scans):
         for s in range(n_scans):
             assert peak_err(got[k][s], want[k][s]) <= TOL_FP32
             assert tuple(gk[k][s]) == tuple(wk[k][s])
+
+
+@pytest.mark.parametrize("n_chan,n_scans", [(1, 1), (5, 17), (24, 16), (25, 3), (49, 33)])
+def test_tch_channel_and_scan_counts(setup, n_chan, n_scans):
+    """The W = 32 kernel's step plan and staging ring at the edges: one
+    channel; fewer channels than ring slots (24); exactly one ring lap; a
+    lap plus one (the next item's first channel lands in slot 0 and its
+    mirror); 49 channels with two laps per item; scan counts that leave the
+    last 8-scan group, or the last group pair, partly empty."""
+    model, sig, grid, _, _ = setup
+    win = (model.k0, model.window)
+    pairs = model.pairs()[:n_chan]
+    tc = BatchImager(model.geometry(), pairs, model.n_samples, grid, window=win, mode="tc")
+    ref = BatchImager(model.geometry(), pairs, model.n_samples, grid, window=win)
+    assert tc.uses_tensor_cores
+    sub = np.ascontiguousarray(np.resize(sig, (n_scans,) + sig.shape[1:])[:, :n_chan])
+    sig_d = tc.to_device_layout(sub)
+    got, gk, flags = run(tc, sig_d)
+    want, wk, _ = run(ref, sig_d)
+    assert flags == 0
+    for k in ("das", "dmas"):
+        for s in range(n_scans):
+            if n_chan == 1 and k == "dmas":
+                # one channel: DMAS is 0 up to the rounding of S^2 - Q
+                assert np.abs(got[k][s]).max() <= TOL_FP32 * np.abs(got["das"][s]).max()
+                continue
+            assert peak_err(got[k][s], want[k][s]) <= TOL_FP32, (k, s)
+            top = np.sort(want[k][s])[-2:]
+            if top[1] - top[0] > 2 * TOL_FP32 * abs(top[1]):  # few channels: flat maxima tie within rounding
+                assert tuple(gk[k][s]) == tuple(wk[k][s]), (k, s)
