@@ -485,10 +485,21 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
           for (int qd = 0; qd < 2; ++qd) {
             const float4* gr = gsl + qd * 32 + 2 * dg;
             const float4 E = gr[0], X = gr[1], E1 = gr[2];
-            q[4 * qd + 0] = fmaf(w0, E.x, fmaf(w1, X.x, fmaf(w2, E1.x, q[4 * qd + 0])));
-            q[4 * qd + 1] = fmaf(w0, E.y, fmaf(w1, X.y, fmaf(w2, E1.y, q[4 * qd + 1])));
-            q[4 * qd + 2] = fmaf(w0, E.z, fmaf(w1, X.z, fmaf(w2, E1.z, q[4 * qd + 2])));
-            q[4 * qd + 3] = fmaf(w0, E.w, fmaf(w1, X.w, fmaf(w2, E1.w, q[4 * qd + 3])));
+            // FFMA2: two scans per instruction, each lane the scalar
+            // fma(w0, E, fma(w1, X, fma(w2, E1, q)))
+            const float2 w0v = make_float2(w0, w0), w1v = make_float2(w1, w1), w2v = make_float2(w2, w2);
+            const float2 qa = __ffma2_rn(w0v, make_float2(E.x, E.y),
+                                         __ffma2_rn(w1v, make_float2(X.x, X.y),
+                                                    __ffma2_rn(w2v, make_float2(E1.x, E1.y),
+                                                               make_float2(q[4 * qd + 0], q[4 * qd + 1]))));
+            const float2 qb = __ffma2_rn(w0v, make_float2(E.z, E.w),
+                                         __ffma2_rn(w1v, make_float2(X.z, X.w),
+                                                    __ffma2_rn(w2v, make_float2(E1.z, E1.w),
+                                                               make_float2(q[4 * qd + 2], q[4 * qd + 3]))));
+            q[4 * qd + 0] = qa.x;
+            q[4 * qd + 1] = qa.y;
+            q[4 * qd + 2] = qb.x;
+            q[4 * qd + 3] = qb.y;
           }
         }
 #ifdef MWB_TCH_PROF
@@ -518,7 +529,12 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
           float v[16];
           tc::tmem_ld16(tmem + lane_base + (uint32_t)(kh * N + kc * 16), v);
 #pragma unroll
-          for (int s = 0; s < SPG; ++s) e[s] = fmaf(v[s + 8], v[s + 8], fmaf(v[s], v[s], e[s]));
+          for (int s = 0; s < SPG; s += 2) {  // FFMA2, each lane fma(v8, v8, fma(v, v, e))
+            const float2 a = make_float2(v[s], v[s + 1]), b = make_float2(v[s + 8], v[s + 9]);
+            const float2 r = __ffma2_rn(b, b, __ffma2_rn(a, a, make_float2(e[s], e[s + 1])));
+            e[s] = r.x;
+            e[s + 1] = r.y;
+          }
         }
         // this warp's TMEM reads are complete (tcgen05.wait::ld): once every
         // builder warp has arrived the next item's MMAs may overwrite TMEM
