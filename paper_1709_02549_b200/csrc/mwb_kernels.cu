@@ -442,10 +442,11 @@ static size_t tc_ws_planes(int n_scans, int n_chan, int j_count) {
 static size_t tc_ws_planes8(int n_scans, int n_chan, int j_count) {  // whole pairs of 8-scan groups
   return sizeof(__half) * 2 * 16 * (size_t)((n_scans + 15) / 16) * (size_t)n_chan * (size_t)tc_plane_len(j_count);
 }
-static size_t tc_ws_plan(int n_pts, int n_chan) {  // per (tile, M-block): steps | records | last steps
+// per (tile, M-block): steps | step records | last steps per channel | A operands (<= C steps of 8 KB)
+static size_t tc_ws_plan(int n_pts, int n_chan) {
   const size_t blocks = 2 * (size_t)(n_pts > 0 ? (n_pts + TILE - 1) / TILE : 1);
   return align_up(sizeof(int) * blocks, 256) + align_up(sizeof(uint4) * (size_t)n_chan * blocks, 256) +
-         sizeof(int) * (size_t)n_chan * blocks;
+         align_up(sizeof(int) * (size_t)n_chan * blocks, 256) + (size_t)tch::OP_B * (size_t)n_chan * blocks;
 }
 
 int64_t mwb_energies_tc_workspace_bytes(int n_scans, int n_chan, int j_count, int n_pts) {
@@ -531,7 +532,7 @@ static int launch_tc(const EnergyParams& e, int kind, int n_pts, int n_scans, in
 // W = 32: the Hankel-in-place kernel (mwb_tch.cuh)
 static int launch_tch(const EnergyParams& e, int kind, int n_pts, int n_scans, int n_chan, int j_lo, int j_count,
                       int Lp, const uint32_t* absmax, const float4* gx, const __half* planes8, const int* plan_n,
-                      const uint4* plan, const int* plan_last, cudaStream_t st) {
+                      const uint4* plan, const int* plan_last, const unsigned char* a_ops, cudaStream_t st) {
   int rc;
   tch::Params P;
   P.e = e;
@@ -539,6 +540,7 @@ static int launch_tch(const EnergyParams& e, int kind, int n_pts, int n_scans, i
   P.plan_n = plan_n;
   P.plan = plan;
   P.plan_last = plan_last;
+  P.a_ops = a_ops;
   P.j_lo = j_lo;
   P.J = j_count;
   P.Lp = Lp;
@@ -584,9 +586,10 @@ static int launch_tch(const EnergyParams& e, int kind, int n_pts, int n_scans, i
     const double n = (double)grid;
     fprintf(stderr, "tch prof per CTA (Mclk): issuer total %.2f wait o_full %.2f wait acc_empty %.2f | builder0 "
             "total %.2f o_empty %.2f s_full %.2f acc_full %.2f epilogue %.2f | producer s_empty %.2f | items %.1f "
-            "steps %.1f | producer issue %.2f total %.2f\n",
+            "steps %.1f | producer issue %.2f total %.2f | A producer waits %.2f\n",
             z[2] / n / 1e6, z[0] / n / 1e6, z[1] / n / 1e6, z[10] / n / 1e6, z[3] / n / 1e6, z[4] / n / 1e6,
-            z[5] / n / 1e6, z[6] / n / 1e6, z[7] / n / 1e6, z[8] / n, z[9] / n, z[11] / n / 1e6, z[12] / n / 1e6);
+            z[5] / n / 1e6, z[6] / n / 1e6, z[7] / n / 1e6, z[8] / n, z[9] / n, z[11] / n / 1e6, z[12] / n / 1e6,
+            z[15] / n / 1e6);
     fprintf(stderr, "tch prof builder0 per item step (clk): A section %.0f  Q + loop section %.0f\n",
             (double)z[13] / z[9], (double)z[14] / z[9]);
   }
@@ -638,6 +641,8 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
     uint4* plan = reinterpret_cast<uint4*>(pl + align_up(sizeof(int) * 2 * (size_t)tiles, 256));
     int* plan_last = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(plan) +
                                             align_up(sizeof(uint4) * (size_t)n_chan * 2 * tiles, 256));
+    unsigned char* a_ops =
+        reinterpret_cast<unsigned char*>(plan_last) + align_up(sizeof(int) * (size_t)n_chan * 2 * tiles, 256);
     tch::planes8_kernel<<<dim3((unsigned)n_chan, (unsigned)groups), 256, 0, st>>>(
         sig, scan_stride, n_scans, n_chan, ld, k0, j_lo, Lp, absmax, planes);
     if ((rc = check_launch("planes8_kernel"))) return rc;
@@ -647,8 +652,11 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
         reinterpret_cast<const uint32_t*>(tb + T.words), reinterpret_cast<const int2*>(tile_info), n_pts, n_chan,
         plan_n, plan, plan_last);
     if ((rc = check_launch("plan_kernel"))) return rc;
+    tch::abuild_kernel<<<(unsigned)(2 * tiles), 256, 0, st>>>(reinterpret_cast<const uint32_t*>(tb + T.words), n_chan,
+                                                             plan_n, plan, a_ops);
+    if ((rc = check_launch("abuild_kernel"))) return rc;
     return launch_tch(e, kind, n_pts, n_scans, n_chan, j_lo, j_count, Lp, absmax, gx, planes, plan_n, plan,
-                      plan_last, st);
+                      plan_last, a_ops, st);
   }
   tc::planes_kernel<<<dim3((unsigned)n_chan, (unsigned)n_scans), 128, 0, st>>>(sig, scan_stride, n_chan, ld, k0,
                                                                                 j_lo, Lp, absmax, planes);

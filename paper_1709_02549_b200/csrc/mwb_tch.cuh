@@ -28,15 +28,20 @@
 // K = 16 steps (plan_kernel), so an item costs ceil(halves / 2) MMA steps
 // instead of one per channel (configs[3]: about 40 instead of 66).
 //
-// Per step the builders write only the A rows (interpolation weights, hi/lo:
-// thread (row, kh) writes K half kh of row `row`, 8 KB per step), used by the
-// MMAs of both scan groups (A_hi read once for its four products, A_lo once
-// for its two: the A collector buffer); warp 0 of the step's group also waits
-// for the two staged channels and writes the B descriptor.  After publishing
-// A each builder adds the DMAS self-terms Q of the channels whose first half
-// is in the step (Gram entries, as in mwb_tc.cuh) for its group kh.  The
-// issuer's one commit per step (done[t % DR]) frees the step's operand slot
-// and, at a channel's last step, its staging slot.
+// The A rows (interpolation weights, hi/lo, 8 KB per step) depend on the table
+// and the plan only, so abuild_kernel writes them once per call for every
+// (M-block, step), and an operand-producer warp copies step t's rows into
+// operand slot t % NO (one bulk copy) once the MMAs of step t - NO completed.
+// The MMAs of both scan groups read them (A_hi once for its four products,
+// A_lo once for its two: the A collector buffer).  Three groups of 8 warps
+// take interleaved steps: warp 0 of the step's group waits for the two staged
+// channels and writes the B descriptor, and every thread (row, kh) adds the
+// DMAS self-terms Q of the channels whose first half is in the step (Gram
+// entries, as in mwb_tc.cuh) for its scan group kh; the step's o_full
+// completes with the A copy and the group's 8 arrivals.  The issuer's one
+// commit per step (done[t % DR]) frees the step's operand slot and, at a
+// channel's last step, its staging slot.  Work items run in chunks of BCH
+// M-blocks over all scan-group pairs, so the chunk's A rows stay in L2.
 // TMEM: lane = row, column = 256 g + 8 k + s for scan s of group g.
 
 namespace tch {
@@ -69,7 +74,7 @@ constexpr int NBW = NG * GW, NBT = NBW * 32;
 // a slot released at step first_c + NG (plan_kernel) is refilled for a channel
 // NS channels later, consumed >= NS / 2 steps after first_c: after the release
 static_assert(NS / 2 > NG, "staging ring too shallow for the Q release slack");
-constexpr int THREADS = NBT + 64;             // + producer warp + MMA warp
+constexpr int THREADS = NBT + 96;             // + staging producer, MMA issuer, operand producer
 constexpr int ROWS = 56;                      // staged rows per plane: r + m + k <= 22 + 7 + 31 (wide) / 14 + 7 + 31
 constexpr int PLANE_B = ROWS * 16;            // 896 B per plane
 constexpr int GPL_B = 2 * PLANE_B;            // hi | lo of one scan group
@@ -180,8 +185,27 @@ struct alignas(64) Params {
   const int* plan_n;       // [tiles * 2] steps per M-block
   const uint4* plan;       // [tiles * 2][C] step records {half 0, half 1, 0, 0}
   const int* plan_last;    // [tiles * 2][C] the last step reading each channel
+  const unsigned char* a_ops;  // [tiles * 2][C][OP_B]: every step's A rows (abuild_kernel)
   int j_lo, J, Lp, n_tiles, n_pairs;
 };
+
+// Work items in chunks of BCH M-blocks: every pair of scan groups of a chunk,
+// M-block fastest, so that the CTAs share one chunk's A operands (BCH x ~40
+// steps x 8 KB) and one or two pairs' planes and Gram slices in L2.
+#ifndef MWB_TCH_BCH
+#define MWB_TCH_BCH 64
+#endif
+#ifndef MWB_TCH_APF
+#define MWB_TCH_APF 0  // steps ahead of the operand copy to prefetch A into L2 (0: none)
+#endif
+constexpr int BCH = MWB_TCH_BCH;
+__device__ __forceinline__ void item_coords(int it, int n_blocks, int n_pairs, int& blk, int& pair) {
+  const int per = BCH * n_pairs;
+  const int ch = it / per, rem = it - ch * per;
+  const int bbc = min(BCH, n_blocks - ch * BCH);
+  pair = rem / bbc;
+  blk = ch * BCH + (rem - pair * bbc);
+}
 
 
 // points of M-block mb of table tile `tile` (<= 0: nothing to do)
@@ -226,7 +250,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&s_full[i], 1);
     for (int i = 0; i < DR; ++i) mbar_init(&done[i], 1);
-    for (int i = 0; i < NO; ++i) mbar_init(&o_full[i], GW);
+    for (int i = 0; i < NO; ++i) mbar_init(&o_full[i], 1 + GW);  // the A copy's expect_tx + the step's Q warps
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, NBW);
     fence_mbar_init();
@@ -256,7 +280,9 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
     int t = 0, steps = 0;
     int rel = -1;  // lane s: the global step that releases ring slot s (NS <= 32)
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int blk = item % n_blocks, pair = item / n_blocks, tile = blk >> 1, mb = blk & 1;
+      int blk, pair;
+      item_coords(item, n_blocks, P.n_pairs, blk, pair);
+      const int tile = blk >> 1, mb = blk & 1;
       if (block_points(p, tile, mb, n_pts) <= 0) continue;
       const int2* tsp = p.tab_span + (size_t)tile * p.C;
       const int* last = P.plan_last + (size_t)blk * p.C;
@@ -299,6 +325,32 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
       }
       steps += __ldg(P.plan_n + blk);
     }
+  } else if (warp == NBW + 2) {
+    // ===== operand producer: step t's A rows (hi | lo, 8 KB, built per
+    // (M-block, step) by abuild_kernel: they depend on the table only) into
+    // operand slot t % NO once the MMAs of step t - NO completed
+    int t = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      int blk, pair;
+      item_coords(item, n_blocks, P.n_pairs, blk, pair);
+      if (block_points(p, blk >> 1, blk & 1, n_pts) <= 0) continue;
+      const int nst = __ldg(P.plan_n + blk);
+      const unsigned char* src = P.a_ops + (size_t)blk * p.C * OP_B;
+      for (int i = 0; i < nst; ++i, ++t) {
+        const int slot = t % NO;
+        if (t >= NO) PROF_T(14, mbar_wait(&done[(t - NO) % DR], ((t - NO) / DR) & 1));
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&o_full[slot], (uint32_t)OP_B);
+          bulk_g2s(ops + (size_t)slot * OP_B, src + (size_t)i * OP_B, (uint32_t)OP_B, &o_full[slot]);
+#if MWB_TCH_APF > 0
+          // pull a later step's A rows into L2 (a chunk's A operands may have
+          // been evicted since the previous scan-group pair read them)
+          if (i + MWB_TCH_APF < nst) bulk_prefetch_l2(src + (size_t)(i + MWB_TCH_APF) * OP_B, (uint32_t)OP_B);
+#endif
+        }
+        __syncwarp();
+      }
+    }
   } else if (warp == NBW + 1) {
     // ===== MMA issuer: the whole warp runs the loop (warp-uniform values),
     // one elected lane issues.  Per step 6 MMAs (2 scan groups x 3 split
@@ -306,7 +358,8 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
     // done[t % DR]
     int t = 0, it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int blk = item % n_blocks;
+      int blk, pair;
+      item_coords(item, n_blocks, P.n_pairs, blk, pair);
       if (block_points(p, blk >> 1, blk & 1, n_pts) <= 0) continue;
       const int nst = __ldg(P.plan_n + blk);
       if (it > 0) PROF_T(1, mbar_wait(acc_empty, (it - 1) & 1));
@@ -353,16 +406,19 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
       ++it;
     }
   } else {
-    // ===== builders + epilogue: NG groups of 8 warps take interleaved steps
-    // (item step i -> group i % NG);
-    // thread (row, kh) writes K half kh of A row `row` and owns the Q partials
-    // and the epilogue of point `row` for scan group kh
+    // ===== Q gatherers + epilogue: NG groups of 8 warps take interleaved
+    // steps (item step i -> group i % NG); warp 0 of the step's group waits for
+    // its staged channels and writes its B descriptor; thread (row, kh) owns
+    // the DMAS self-term partials and the epilogue of point `row` for scan
+    // group kh
     const int gp = warp >> 3, w8 = warp & 7;
     const int pt = w8 * 32 + lane;
     const int row = pt & (ROWS_M - 1), kh = pt >> 7;
     int t = 0, tcb = 0, it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int blk = item % n_blocks, pair = item / n_blocks, tile = blk >> 1, mb = blk & 1;
+      int blk, pair;
+      item_coords(item, n_blocks, P.n_pairs, blk, pair);
+      const int tile = blk >> 1, mb = blk & 1;
       const int n_in = block_points(p, tile, mb, n_pts);
       if (n_in <= 0) continue;
       const int grp = NGRP * pair + kh;  // this thread's scan group
@@ -389,13 +445,16 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
         const uint4 x = __ldg(rec + i + NG);
         rn = make_uint2(x.x, x.y);
       }
-      uint32_t wc0 = hv_valid(rc.x) ? __ldg(twb + (size_t)hv_chan(rc.x) * TILE) : 0u;
-      uint32_t wc1 = hv_valid(rc.y) ? __ldg(twb + (size_t)hv_chan(rc.y) * TILE) : 0u;
+      // (the words of the channels whose first half is in the step: the Q gathers')
+      auto first_word = [&](uint32_t h) {
+        return hv_valid(h) && hv_first(h) ? __ldg(twb + (size_t)hv_chan(h) * TILE) : 0u;
+      };
+      uint32_t wc0 = first_word(rc.x), wc1 = first_word(rc.y);
       for (; i < nst; i += NG) {
         const uint2 cur = rc;
         const uint32_t wh0 = wc0, wh1 = wc1;
-        wc0 = hv_valid(rn.x) ? __ldg(twb + (size_t)hv_chan(rn.x) * TILE) : 0u;
-        wc1 = hv_valid(rn.y) ? __ldg(twb + (size_t)hv_chan(rn.y) * TILE) : 0u;
+        wc0 = first_word(rn.x);
+        wc1 = first_word(rn.y);
         rc = rn;
         rn = make_uint2(0u, 0u);
         if (i + 2 * NG < nst) {
@@ -407,7 +466,6 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
 #ifdef MWB_TCH_PROF
         const long long _ta = clock64();
 #endif
-        unsigned char* op = ops + (size_t)oslot * OP_B;
         if (w8 == 0) {
           // the step's B operand (group 0, hi plane): the two halves' rows in
           // address order -- they are consecutive (the same channel, or the
@@ -428,44 +486,12 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
           const uint32_t a1 = hv_valid(cur.y) ? (uint32_t)(s1 * STAGE_B + hv_row(cur.y) * 16) : a0 + 16u;
           if (lane == 0) meta[oslot] = desc(smem_u32(stage) + a0, a1 - a0, 16);
         }
-        // ---- A: K half kh holds plan half kh (the interpolation weights)
-        {
-          const uint32_t hw = kh ? cur.y : cur.x;
-          uint32_t hi[4] = {0u, 0u, 0u, 0u}, lo[4] = {0u, 0u, 0u, 0u};
-          if (hv_valid(hw)) {  // warp-uniform
-            const uint32_t w = kh ? wh1 : wh0;
-            const int rel = (int)(w >> 23) - hv_row(hw);  // f0 at tap rel of this half, f1 at rel + 1
-            const float f1 = weight_f1(w);
-            uint32_t f0h, f0l;
-            tc::split2(1.0f - f1, f1, f0h, f0l);  // low half f0, high half f1
-            const uint32_t f1h = f0h >> 16, f1l = f0l >> 16;
-            f0h &= 0xFFFFu;
-            f0l &= 0xFFFFu;
-            const int j0 = rel >> 1;  // arithmetic: rel may be -1 .. 21
-            const bool odd = rel & 1;
-            const uint32_t ph = odd ? (f0h << 16) : (f0h | (f1h << 16));
-            const uint32_t pl = odd ? (f0l << 16) : (f0l | (f1l << 16));
-            const uint32_t nh = odd ? f1h : 0u, nl = odd ? f1l : 0u;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              hi[j] = j == j0 ? ph : (j == j0 + 1 ? nh : 0u);
-              lo[j] = j == j0 ? pl : (j == j0 + 1 ? nl : 0u);
-            }
-          }
-          *reinterpret_cast<uint4*>(op + tc::kmajor_off(row, kh)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<uint4*>(op + A_B + tc::kmajor_off(row, kh)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-        }
-        tc::fence_async_smem();  // A generic writes -> visible to the tensor core
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&o_full[oslot]);
 #ifdef MWB_TCH_PROF
         const long long _tq = clock64();
         prof[12] += _tq - _ta;
 #endif
-        // ---- Q of the channels starting in this step, for scan group kh, after
-        // the step's A rows are published (a channel's staging slot is released
-        // no earlier than the step NG after its first, which this group builds
-        // only once these reads are done; plan_kernel):
+        // ---- Q of the channels starting in this step, for scan group kh (read
+        // before the step's arrival: the step's MMAs may then release a slot):
         // Q += f0^2 e(d) + 2 f0 f1 x(d) + f1^2 e(d + 1), 4 scans per LDS.128
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -505,6 +531,8 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
 #ifdef MWB_TCH_PROF
         prof[13] += clock64() - _tq;
 #endif
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_full[oslot]);  // this warp's Gram reads of step ts are done
       }
       t += nst;
       tcb += p.C;
@@ -604,6 +632,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
     atomicAdd(&tch_prof[9], prof[9]);
     atomicAdd(&tch_prof[10], prof[2]);
   }
+  if (warp == NBW + 2 && lane == 0) atomicAdd(&tch_prof[15], prof[14]);
   if (warp == NBW && lane == 0) {
     atomicAdd(&tch_prof[7], prof[7]);
     atomicAdd(&tch_prof[11], prof[11]);
@@ -614,6 +643,48 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
   __syncthreads();
   tc::fence_after();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+// The A operands of every (M-block, step), hi | lo in the K-major no-swizzle
+// core-matrix layout the MMA reads (tc::kmajor_off): thread (row, kh) writes
+// K half kh of row `row` -- the interpolation weights f0 at tap d - r and f1
+// at d - r + 1 of the plan half's 8 taps (those inside them).  They depend on
+// the table and the plan only, not on the scans.
+__global__ void __launch_bounds__(256) abuild_kernel(const uint32_t* __restrict__ words, int C,
+                                                     const int* __restrict__ plan_n, const uint4* __restrict__ plan,
+                                                     unsigned char* __restrict__ a_ops) {
+  const int blk = blockIdx.x, tile = blk >> 1, mb = blk & 1;
+  const int row = threadIdx.x & (ROWS_M - 1), kh = threadIdx.x >> 7;
+  const int nst = plan_n[blk];
+  const uint32_t* tw = words + (size_t)tile * C * TILE + mb * ROWS_M + row;
+  for (int i = 0; i < nst; ++i) {
+    const uint4 r = __ldg(plan + (size_t)blk * C + i);
+    const uint32_t hw = kh ? r.y : r.x;
+    uint32_t hi[4] = {0u, 0u, 0u, 0u}, lo[4] = {0u, 0u, 0u, 0u};
+    if (hv_valid(hw)) {
+      const uint32_t w = __ldg(tw + (size_t)hv_chan(hw) * TILE);
+      const int rel = (int)(w >> 23) - hv_row(hw);  // f0 at tap rel of this half, f1 at rel + 1
+      const float f1 = weight_f1(w);
+      uint32_t f0h, f0l;
+      tc::split2(1.0f - f1, f1, f0h, f0l);  // low half f0, high half f1
+      const uint32_t f1h = f0h >> 16, f1l = f0l >> 16;
+      f0h &= 0xFFFFu;
+      f0l &= 0xFFFFu;
+      const int j0 = rel >> 1;  // arithmetic: rel may be -1 .. 21
+      const bool odd = rel & 1;
+      const uint32_t ph = odd ? (f0h << 16) : (f0h | (f1h << 16));
+      const uint32_t pl = odd ? (f0l << 16) : (f0l | (f1l << 16));
+      const uint32_t nh = odd ? f1h : 0u, nl = odd ? f1l : 0u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        hi[j] = j == j0 ? ph : (j == j0 + 1 ? nh : 0u);
+        lo[j] = j == j0 ? pl : (j == j0 + 1 ? nl : 0u);
+      }
+    }
+    unsigned char* op = a_ops + ((size_t)blk * C + i) * OP_B;
+    *reinterpret_cast<uint4*>(op + tc::kmajor_off(row, kh)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4*>(op + A_B + tc::kmajor_off(row, kh)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
 }
 
 // Scaled fp16 hi / lo planes, time-major with the 8 scans of a group
@@ -719,11 +790,9 @@ __global__ void __launch_bounds__(256) plan_kernel(const uint32_t* __restrict__ 
     out[s] = make_uint4(hw[0], hw[1], 0u, 0u);
   }
   // the step whose completion releases channel c's staging slot: its last
-  // step, and no earlier than NG steps after its first (the builder group
-  // that gathers the channel's Q entries after publishing that step's A rows
-  // has then moved on)
+  // (the Q gathers of its first step precede that step's MMAs: o_full)
   for (int c = tid; c < C; c += blockDim.x)
-    plan_last[(size_t)blk * C + c] = max((h0[c] + cnt[c] - 1) >> 1, (h0[c] >> 1) + NG);
+    plan_last[(size_t)blk * C + c] = (h0[c] + cnt[c] - 1) >> 1;
   if (tid == 0) plan_n[blk] = nst;
 }
 
