@@ -577,7 +577,27 @@ static int launch_tch(const EnergyParams& e, int kind, int n_pts, int n_scans, i
     cudaMemcpyToSymbol(tch::tch_prof, z, sizeof(z));
   }
 #endif
+#ifdef MWB_TCH_TRACE
+  {
+    unsigned int z0 = 0;
+    cudaMemcpyToSymbol(tch::tch_trace_n, &z0, sizeof(z0));
+  }
+#endif
   fn<<<grid, tch::THREADS, L.total, st>>>(P);
+#ifdef MWB_TCH_TRACE
+  {
+    cudaDeviceSynchronize();
+    unsigned int nev = 0;
+    cudaMemcpyFromSymbol(&nev, tch::tch_trace_n, sizeof(nev));
+    nev = std::min(nev, 8192u);
+    std::vector<unsigned long long> ev(2 * (size_t)nev);
+    cudaMemcpyFromSymbol(ev.data(), tch::tch_trace, sizeof(unsigned long long) * 2 * nev);
+    FILE* f = fopen(getenv("MWB_TCH_TRACE_FILE") ? getenv("MWB_TCH_TRACE_FILE") : "/tmp/tch_trace.txt", "w");
+    for (unsigned int k = 0; k < nev; ++k)
+      fprintf(f, "%llu %llu %llu\n", ev[2 * k], ev[2 * k + 1] >> 32, ev[2 * k + 1] & 0xFFFFFFFFull);
+    fclose(f);
+  }
+#endif
 #ifdef MWB_TCH_PROF
   {
     cudaDeviceSynchronize();
@@ -590,8 +610,8 @@ static int launch_tch(const EnergyParams& e, int kind, int n_pts, int n_scans, i
             z[2] / n / 1e6, z[0] / n / 1e6, z[1] / n / 1e6, z[10] / n / 1e6, z[3] / n / 1e6, z[4] / n / 1e6,
             z[5] / n / 1e6, z[6] / n / 1e6, z[7] / n / 1e6, z[8] / n, z[9] / n, z[11] / n / 1e6, z[12] / n / 1e6,
             z[15] / n / 1e6);
-    fprintf(stderr, "tch prof builder0 per item step (clk): A section %.0f  Q + loop section %.0f\n",
-            (double)z[13] / z[9], (double)z[14] / z[9]);
+    fprintf(stderr, "tch prof issuer o_full waits (Mclk): item first step %.2f, steps 1-2 %.2f\n", z[15] / n / 1e6,
+            z[14] / n / 1e6);
   }
 #endif
   return check_launch("energy_tch_kernel");

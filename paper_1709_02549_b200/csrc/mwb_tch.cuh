@@ -213,6 +213,23 @@ __device__ __forceinline__ int block_points(const EnergyParams& p, int tile, int
   return min(ROWS_M, tc::tile_points(p, tile, n_pts) - mb * ROWS_M);
 }
 
+#ifdef MWB_TCH_TRACE
+// event log of CTA 0 (development aid): {clock64, code << 32 | arg}
+__device__ unsigned long long tch_trace[2 * 8192];
+__device__ unsigned int tch_trace_n;
+__device__ __forceinline__ void trace_ev(int code, int arg) {
+  if (blockIdx.x != 0) return;
+  const unsigned int k = atomicAdd(&tch_trace_n, 1u);
+  if (k < 8192) {
+    tch_trace[2 * k] = (unsigned long long)clock64();
+    tch_trace[2 * k + 1] = ((unsigned long long)code << 32) | (unsigned int)arg;
+  }
+}
+#define TRACE(code, arg) trace_ev(code, arg)
+#else
+#define TRACE(code, arg)
+#endif
+
 #ifdef MWB_TCH_PROF
 __device__ unsigned long long tch_prof[16];
 #define PROF_T(k, stmt)                  \
@@ -342,6 +359,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
         if (lane == 0) {
           mbar_arrive_expect_tx(&o_full[slot], (uint32_t)OP_B);
           bulk_g2s(ops + (size_t)slot * OP_B, src + (size_t)i * OP_B, (uint32_t)OP_B, &o_full[slot]);
+          TRACE(9, t);
 #if MWB_TCH_APF > 0
           // pull a later step's A rows into L2 (a chunk's A operands may have
           // been evicted since the previous scan-group pair read them)
@@ -363,10 +381,23 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
       if (block_points(p, blk >> 1, blk & 1, n_pts) <= 0) continue;
       const int nst = __ldg(P.plan_n + blk);
       if (it > 0) PROF_T(1, mbar_wait(acc_empty, (it - 1) & 1));
+      if (lane == 0) TRACE(2, it);
       tc::fence_after();
       for (int i = 0; i < nst; ++i, ++t) {
         const int slot = t % NO;
-        PROF_T(0, mbar_wait(&o_full[slot], (t / NO) & 1));
+#ifdef MWB_TCH_PROF
+        {
+          const long long _t0 = clock64();
+          mbar_wait(&o_full[slot], (t / NO) & 1);
+          const long long dt = clock64() - _t0;
+          prof[0] += dt;
+          if (i == 0) prof[15] += dt;        // first step of an item
+          else if (i < 3) prof[5] += dt;     // steps 1, 2
+        }
+#else
+        mbar_wait(&o_full[slot], (t / NO) & 1);
+#endif
+        if (lane == 0) TRACE(1, t);
         tc::fence_after();
         const uint64_t b0 = meta[slot];
         const uint32_t base = smem_u32(ops + (size_t)slot * OP_B);
@@ -463,6 +494,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
         }
         const int ts = t + i, oslot = ts % NO;
         if (ts >= NO) PROF_T(3, mbar_wait(&done[(ts - NO) % DR], ((ts - NO) / DR) & 1));
+        if (w8 == 0 && lane == 0) TRACE(3, (gp << 20) | ts);
 #ifdef MWB_TCH_PROF
         const long long _ta = clock64();
 #endif
@@ -533,6 +565,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
 #endif
         __syncwarp();
         if (lane == 0) mbar_arrive(&o_full[oslot]);  // this warp's Gram reads of step ts are done
+        if (w8 == 0 && lane == 0) TRACE(4, (gp << 20) | ts);
       }
       t += nst;
       tcb += p.C;
@@ -543,7 +576,19 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
       float* ex = reinterpret_cast<float*>(smem + L.ex);
 #pragma unroll
       for (int s = 0; s < SPG; ++s) qx[((gp * NGRP + kh) * SPG + s) * ROWS_M + row] = q[s];
+      // the output stage's global inputs, loaded while the last MMAs run: the
+      // point's output slot and the inverse scales of this thread's scans
+      const bool valid = row < n_in;
+      const int g = tile * TILE + mb * ROWS_M + (valid ? row : 0);
+      const int slot_out = valid ? (p.out_idx ? __ldg(p.out_idx + g) : g) : -1;
+      float inv_s[(SPG + NG - 1) / NG];
+#pragma unroll
+      for (int k = 0; k < (SPG + NG - 1) / NG; ++k) {
+        const int sc = gp + k * NG;
+        inv_s[k] = sc < nsg ? tc::pow2f(-tc::scale_exp(__ldg(P.absmax + grp * SPG + sc))) : 0.f;
+      }
       PROF_T(5, mbar_wait(acc_full, it & 1));
+      if (w8 == 0 && lane == 0) TRACE(5, (gp << 20) | it);
 #ifdef MWB_TCH_PROF
       const long long t_epi = clock64();
 #endif
@@ -569,14 +614,16 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
         tc::fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty);
+        if (w8 == 0 && lane == 0) TRACE(6, (gp << 20) | it);
 #pragma unroll
         for (int s = 0; s < SPG; ++s) ex[((gp * NGRP + kh) * SPG + s) * ROWS_M + row] = e[s];
       }
       builders_sync_tch();
-      const bool valid = row < n_in;
-      const int g = tile * TILE + mb * ROWS_M + (valid ? row : 0);
-      const int slot_out = valid ? (p.out_idx ? __ldg(p.out_idx + g) : g) : -1;
-      for (int s = gp; s < nsg; s += NG) {  // warp-uniform
+      if (w8 == 0 && lane == 0) TRACE(7, (gp << 20) | it);
+#pragma unroll
+      for (int k = 0; k < (SPG + NG - 1) / NG; ++k) {
+        const int s = gp + k * NG;
+        if (s >= nsg) break;  // warp-uniform
         float qs = 0.f;
         double es = 0.0;
 #pragma unroll
@@ -585,7 +632,7 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
           es += (double)ex[((g2 * NGRP + kh) * SPG + s) * ROWS_M + row];
         }
         const int scan = grp * SPG + s;
-        const float inv = tc::pow2f(-tc::scale_exp(__ldg(P.absmax + scan)));
+        const float inv = inv_s[k];
         const double E = es * (double)inv * (double)inv;  // S was in scaled units
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
@@ -599,14 +646,16 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
             out[slot_out] = en;
             if (isfinite(en)) key = argmax_key(en, slot_out); else bad = true;
           }
-          if (keys) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+          if (keys) {  // warp max of the 64-bit keys: the high words, then the low words among the maxima
+            const uint32_t hi = __reduce_max_sync(0xffffffffu, (uint32_t)(key >> 32));
+            const uint32_t lo = __reduce_max_sync(0xffffffffu, (uint32_t)(key >> 32) == hi ? (uint32_t)key : 0u);
+            key = ((unsigned long long)hi << 32) | lo;
             if (lane == 0 && key != 0ull) atomicMax(keys + scan, key);
           }
         }
       }
       builders_sync_tch();  // every group has read qx / ex before the next item overwrites them
+      if (w8 == 0 && lane == 0) TRACE(8, (gp << 20) | it);
       if (p.flags && (bad || bad_span)) atomicOr(p.flags, (bad ? 1 : 0) | (bad_span ? 2 : 0));
 #ifdef MWB_TCH_PROF
       prof[6] += clock64() - t_epi;
@@ -620,19 +669,18 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
   prof[2] = clock64() - t_start;
   // issuer lane 0: 0, 1, 2; builder warp 0 lane 0: 3..6, 8, 9, 10, 12, 13; producer lane 0: 7
   if (warp == NBW + 1 && lane == 0) {
+    atomicAdd(&tch_prof[15], prof[15]);
+    atomicAdd(&tch_prof[14], prof[5]);
     atomicAdd(&tch_prof[0], prof[0]);
     atomicAdd(&tch_prof[1], prof[1]);
     atomicAdd(&tch_prof[2], prof[2]);
   }
   if (warp == 0 && lane == 0) {
     for (int k = 3; k <= 6; ++k) atomicAdd(&tch_prof[k], prof[k]);
-    atomicAdd(&tch_prof[13], prof[12]);
-    atomicAdd(&tch_prof[14], prof[13]);
     atomicAdd(&tch_prof[8], prof[8]);
     atomicAdd(&tch_prof[9], prof[9]);
     atomicAdd(&tch_prof[10], prof[2]);
   }
-  if (warp == NBW + 2 && lane == 0) atomicAdd(&tch_prof[15], prof[14]);
   if (warp == NBW && lane == 0) {
     atomicAdd(&tch_prof[7], prof[7]);
     atomicAdd(&tch_prof[11], prof[11]);
