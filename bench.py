@@ -720,7 +720,7 @@ def run_ours(args):
         e2e_s = shard.max_over_ranks(statistics.median(times), dev)
         from paper_1709_02549_b200.batch import _chunk_ranges
 
-        chunks = len(_chunk_ranges(S, min(args.chunk, S))) * (3 if bi.uses_tensor_cores else 1)
+        chunks = len(_chunk_ranges(S, min(args.chunk, S))) * bi.kernels_per_call
         first, count = bi.input_range()
         e2e = {"value": pair_evals / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "h2d_what": f"samples [{first}, {first + count}) of every channel row (the range the tensor-core "
@@ -756,7 +756,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "other_configs": others,
-            "gpu_launches": args.steps * (3 if bi.uses_tensor_cores else 1),  # TC: gram, planes, energy kernels
+            "gpu_launches": args.steps * bi.kernels_per_call,  # W = 32 TC: gram, planes, plan, A operands, energy
             "tensor_cores": bi.uses_tensor_cores,
             "clocks": clk,
             "kernel_mode": args.mode,

@@ -175,6 +175,16 @@ class BatchImager:
         return self.mode == 2
 
     @property
+    def kernels_per_call(self) -> int:
+        """Kernels of this package one run_device call launches: the CUDA-core
+        energy kernel; or, on the tensor-core path, the Gram and fp16-plane
+        pre-passes and the energy kernel, plus (W = 32) the step plan and the
+        A-operand pre-pass."""
+        if self.mode != 2:
+            return 1
+        return 5 if self.w == 32 else 3
+
+    @property
     def n_chan(self) -> int:
         return self.scan.n_chan
 
