@@ -35,5 +35,5 @@ def test_bench_json_line():
     assert core["roofline"]["bound"] == "smem" and 0 < core["roofline"]["frac"] <= 1.0
     e2e = d["e2e"]
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
-    assert d["gpu_launches"] == 3 * 3
+    assert d["gpu_launches"] == 3 * 5  # per step: Gram, fp16 planes, step plan, A operands, the W = 32 TC kernel
     assert "sm_mhz" in d["clocks"]
