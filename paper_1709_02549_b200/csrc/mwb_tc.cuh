@@ -89,7 +89,6 @@ struct Cfg {
   static_assert(SPANH <= SPANH_MAX, "plane length");
   static_assert(OP_BYTES % 128 == 0 && (GQ_FLOAT4 * 16) % 128 == 0, "128-byte aligned ring slots");
 };
-using Cfg32x8 = Cfg<32, 8>;  // configs[3]: 8 scans x W = 32 (N = 256)
 using Cfg48x4 = Cfg<48, 4>;  // W = 48 batches (N = 192)
 using Cfg48x1 = Cfg<48, 1>;  // configs[4]: one scan, W = 48 (N = 48)
 

@@ -71,9 +71,6 @@ static_assert(32 % PCH == 0 && PCH <= NS, "producer rounds");
 constexpr int NG = MWB_TCH_GROUPS;            // builder groups (step t -> builder group t % NG)
 constexpr int GW = 8;
 constexpr int NBW = NG * GW, NBT = NBW * 32;
-// a slot released at step first_c + NG (plan_kernel) is refilled for a channel
-// NS channels later, consumed >= NS / 2 steps after first_c: after the release
-static_assert(NS / 2 > NG, "staging ring too shallow for the Q release slack");
 constexpr int THREADS = NBT + 96;             // + staging producer, MMA issuer, operand producer
 constexpr int ROWS = 56;                      // staged rows per plane: r + m + k <= 22 + 7 + 31 (wide) / 14 + 7 + 31
 constexpr int PLANE_B = ROWS * 16;            // 896 B per plane
@@ -194,9 +191,6 @@ struct alignas(64) Params {
 // steps x 8 KB) and one or two pairs' planes and Gram slices in L2.
 #ifndef MWB_TCH_BCH
 #define MWB_TCH_BCH 64
-#endif
-#ifndef MWB_TCH_APF
-#define MWB_TCH_APF 0  // steps ahead of the operand copy to prefetch A into L2 (0: none)
 #endif
 constexpr int BCH = MWB_TCH_BCH;
 __device__ __forceinline__ void item_coords(int it, int n_blocks, int n_pairs, int& blk, int& pair) {
@@ -360,11 +354,6 @@ __global__ void __launch_bounds__(THREADS, 1) energy_tch_kernel(const __grid_con
           mbar_arrive_expect_tx(&o_full[slot], (uint32_t)OP_B);
           bulk_g2s(ops + (size_t)slot * OP_B, src + (size_t)i * OP_B, (uint32_t)OP_B, &o_full[slot]);
           TRACE(9, t);
-#if MWB_TCH_APF > 0
-          // pull a later step's A rows into L2 (a chunk's A operands may have
-          // been evicted since the previous scan-group pair read them)
-          if (i + MWB_TCH_APF < nst) bulk_prefetch_l2(src + (size_t)(i + MWB_TCH_APF) * OP_B, (uint32_t)OP_B);
-#endif
         }
         __syncwarp();
       }
