@@ -388,8 +388,9 @@ def other_configs() -> dict:
                                                    "tensor_cores": bi1.uses_tensor_cores}
     del sig1, o1
     # configs[3] with the reference's own semantics: energy over the full
-    # 1024-sample record (beamform.py:211-212), CUDA-core K1 (the tensor-core
-    # kernel is built for 32/48-sample windows); 256 of the 4096 scans
+    # 1024-sample record (beamform.py:211-212); 256 of the 4096 scans, on the
+    # CUDA-core K1 and on the tensor cores (32 chunks of 32 samples,
+    # mwb_energies_tc_record)
     sig3, _ = synth.batch_2d_device(m0, range(256))
     g3 = synth.grid_square(0.12, 256)
     bi3 = BatchImager(m0.geometry(), m0.pairs(), m0.n_samples, g3, window=None, mode="smem")
@@ -400,7 +401,16 @@ def other_configs() -> dict:
                                          "pixel_pair_samples_per_s": 256 * 65536 * 66 * 1024 / (t * 1e-3),
                                          "note": "DAS + DMAS fused (one pass), window = full 1024-sample record, "
                                                  "energy_kernel<BOTH>; pixel_pair_samples counted once per pair"}
-    del sig3, o3, bi3
+    del bi3
+    bi3t = BatchImager(m0.geometry(), m0.pairs(), m0.n_samples, g3, window=None, mode="auto")
+    if bi3t.uses_tensor_cores:
+        t = med_ms(lambda: bi3t.run_device(sig3, o3["das"], o3["dmas"]), reps=3)
+        out["cfg3_full_record_256_scans_tc"] = {
+            "ms": t, "pixel_pair_evals_per_s": pe / (t * 1e-3),
+            "pixel_pair_samples_per_s": 256 * 65536 * 66 * 1024 / (t * 1e-3),
+            "note": "the same on the tensor cores: 32 fused W = 32 K1-TCH passes (one per 32-sample chunk), "
+                    "chunk energies summed in fp64 (mwb_energies_tc_record)"}
+    del sig3, o3, bi3t
     m2 = synth.ScanModel(n_samples=2048)
     ds2, _ = synth.dataset_2d(m2, seed=1000, phantom_radius=0.05)
     g2 = mw.ImagingGrid((-0.05, -0.05), (0.1, 0.1), 2.5e-4)

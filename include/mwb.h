@@ -383,6 +383,22 @@ int mwb_simulate(float* out, int n_scans, int n_chan, int n_samples, int ld, con
  * Workspace: mwb_energies_tc_workspace_bytes(n_scans, n_chan, j_count, n_pts).
  */
 int64_t mwb_energies_tc_workspace_bytes(int n_scans, int n_chan, int j_count, int n_pts);
+/* Windows of any multiple of 32 samples (the reference's full-record energy,
+ * beamform.py:211-212, included) on the tensor cores: one W = 32
+ * mwb_energies_tc call per 32-sample chunk of the window [k0, k0 + window),
+ * the chunk energies summed in fp64 and rounded once; writes the cells
+ * `valid` marks (n_cells = nx * ny = the output stride) of each scan's maps,
+ * their argmax keys and the flags of every chunk call (both kinds in one
+ * fused pass per chunk).  Replaces, for batches of
+ * one geometry, the per-dataset image() of beamform.py:283-342 with its
+ * default full-record window. */
+int64_t mwb_energies_tc_record_workspace_bytes(int n_scans, int n_chan, int j_count, int n_pts, int n_cells);
+int mwb_energies_tc_record(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
+                           const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale,
+                           const double* pts_xyz, const int32_t* out_idx, int n_pts, const int32_t* tile_info,
+                           const void* table, int interp, int k0, int window, const uint8_t* valid, int n_cells,
+                           float* out_das, float* out_dmas, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags,
+                           int j_lo, int j_count, void* workspace, void* stream);
 int mwb_table_max_span(const void* table, int n_pts, int n_chan, int32_t* d_out, void* stream);
 /* smallest / largest per-channel span start lo over the table's non-empty
  * tiles -> d_out[0], d_out[1]; the window-offset range of mwb_energies_tc is

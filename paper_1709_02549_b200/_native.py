@@ -119,6 +119,12 @@ _SIGNATURES = {
          _I, _I, _P, _P],
         _I,
     ),
+    "mwb_energies_tc_record_workspace_bytes": ([_I, _I, _I, _I, _I], _I64),
+    "mwb_energies_tc_record": (
+        [_P, _I, _I64, _I, _I, _I, _P, _P, _I, _D, _P, _P, _I, _P, _P, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P,
+         _I, _I, _P, _P],
+        _I,
+    ),
     "mwb_lattice_tile_count": ([_I, _I, _I], _I64),
     "mwb_enumerate_lattice_padded": (
         [_D, _D, _D, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P],

@@ -132,9 +132,19 @@ class BatchImager:
         # per-point delay table: computed once, shared by every scan and kind
         self.table = build_table(self.scan, self.pts, self.n_pts, self.interp) if self.n_pts else None
 
+    def _tc_window_ok(self) -> bool:
+        # 32 and 48 directly; any other multiple of 32 (the full record
+        # included) as a sum of 32-sample chunks (mwb_energies_tc_record)
+        return self.w in self.TC_WINDOWS or (self.w > 0 and self.w % 32 == 0)
+
+    @property
+    def tc_record(self) -> bool:
+        """Tensor-core path over a window of several 32-sample chunks."""
+        return self.mode == 2 and self.w not in self.TC_WINDOWS
+
     def _setup_padded(self, emask) -> tuple[bool, str]:
-        if self.w not in self.TC_WINDOWS:
-            return False, f"window {self.w} not in {self.TC_WINDOWS}"
+        if not self._tc_window_ok():
+            return False, f"window {self.w} neither in {self.TC_WINDOWS} nor a multiple of 32"
         self._enumerate(emask, padded=True)
         if not self.n_valid:
             self.table = None
@@ -158,8 +168,8 @@ class BatchImager:
     TC_WINDOWS, TC_MAX_SPAN = (32, 48), 14
 
     def tc_eligible(self) -> tuple[bool, str]:
-        if self.w not in self.TC_WINDOWS:
-            return False, f"window {self.w} not in {self.TC_WINDOWS}"
+        if not self._tc_window_ok():
+            return False, f"window {self.w} neither in {self.TC_WINDOWS} nor a multiple of 32"
         if not self.n_pts or self.table is None:
             return True, ""
         out = torch.zeros(1, dtype=torch.int32, device=dv.device())
@@ -182,6 +192,8 @@ class BatchImager:
         A-operand pre-pass."""
         if self.mode != 2:
             return 1
+        if self.tc_record:  # per 32-sample chunk 5 kernels and an accumulation per kind, then a finish per kind
+            return (self.w // 32) * 7 + 2
         return 5 if self.w == 32 else 3
 
     @property
@@ -213,6 +225,20 @@ class BatchImager:
             for out in (out_das, out_dmas):
                 if out is not None:
                     out.zero_()
+            return
+        if self.mode == 2 and self.tc_record:
+            nbytes = int(nat.load().mwb_energies_tc_record_workspace_bytes(s, self.n_chan, self.j_count, self.n_pts,
+                                                                          nxny))
+            if self._tc_ws is None or self._tc_ws.numel() < nbytes:
+                self._tc_ws = torch.empty(nbytes, dtype=torch.uint8, device=sig.device)
+            nat.call(
+                "mwb_energies_tc_record", sig.data_ptr(), s, self.n_chan * self.ld, self.n_chan, self.ld,
+                self.n_samples, self.scan.chan.data_ptr(), self.scan.ant.data_ptr(), self.scan.n_ant,
+                self.scan.inv_scale, self.pts.data_ptr(), self.oidx.data_ptr(), self.n_pts,
+                nat.ptr(self.tile_info), self.table.data_ptr(), self.interp, self.k0, self.w, self.valid.data_ptr(),
+                nxny, nat.ptr(out_das), nat.ptr(out_dmas), nat.ptr(key_das), nat.ptr(key_dmas), nat.ptr(flags),
+                self.j_lo, self.j_count, self._tc_ws.data_ptr(), dv.stream_handle(),
+            )
             return
         if self.mode == 2:
             nbytes = int(nat.load().mwb_energies_tc_workspace_bytes(s, self.n_chan, self.j_count, self.n_pts))
@@ -258,7 +284,11 @@ class BatchImager:
             return 0, self.n_samples
         out = (ctypes.c_int32 * 2)()
         nat.call("mwb_tc_sample_range", self.k0, self.j_lo, self.j_count, self.ld, out)
-        return int(out[0]), int(out[1])
+        first, count = int(out[0]), int(out[1])
+        if self.tc_record:  # the union over the window's 32-sample chunks
+            nat.call("mwb_tc_sample_range", self.k0 + self.w - 32, self.j_lo, self.j_count, self.ld, out)
+            count = int(out[0]) + int(out[1]) - first
+        return first, count
 
     def h2d_bytes(self, n_scans: int) -> int:
         """Host-to-device bytes ``__call__`` copies for ``n_scans`` scans."""

@@ -686,6 +686,104 @@ int mwb_energies_tc(const float* sig, int n_scans, int64_t scan_stride, int n_ch
 }
 
 
+// ---------------------------------------------------------------------------
+// Long windows on the tensor cores: the window's 32-sample chunks one W = 32
+// call each, the chunk energies summed in fp64 (DAS: sum of the chunks' sum of
+// S^2; DMAS: of their (S^2 - Q) / 2 -- both additive over the window), then
+// rounded to fp32 once, with the argmax keys and the non-finite flag of the
+// final maps.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(256) record_accum_kernel(const float* __restrict__ tmp, double* __restrict__ acc,
+                                                           long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    acc[i] += (double)tmp[i];
+}
+
+__global__ void __launch_bounds__(256) record_finish_kernel(const double* __restrict__ acc, int n_cells,
+                                                            const uint8_t* __restrict__ valid, float* out,
+                                                            long long out_stride, unsigned long long* keys,
+                                                            int32_t* flags) {
+  const int s = blockIdx.y;
+  const double* a = acc + (size_t)s * n_cells;
+  float* o = out + (size_t)s * (size_t)out_stride;
+  unsigned long long key = 0ull;
+  bool bad = false;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_cells; i += gridDim.x * blockDim.x) {
+    if (!valid[i]) continue;
+    const float v = __double2float_rn(a[i]);
+    o[i] = v;
+    if (isfinite(v)) key = max(key, (unsigned long long)argmax_key(v, i)); else bad = true;
+  }
+  if (keys) {
+    const uint32_t hi = __reduce_max_sync(0xffffffffu, (uint32_t)(key >> 32));
+    const uint32_t lo = __reduce_max_sync(0xffffffffu, (uint32_t)(key >> 32) == hi ? (uint32_t)key : 0u);
+    key = ((unsigned long long)hi << 32) | lo;
+    if ((threadIdx.x & 31) == 0 && key != 0ull) atomicMax(keys + s, key);
+  }
+  if (bad && flags) atomicOr(flags, 1);
+}
+}  // namespace
+
+// [tmp DAS | tmp DMAS] fp32 chunk maps, then [acc DAS | acc DMAS] fp64
+static size_t record_tmp_bytes(int n_scans, int n_cells) {
+  return align_up(2 * (size_t)n_scans * n_cells * sizeof(float), 256);
+}
+static size_t record_maps_bytes(int n_scans, int n_cells) {
+  return record_tmp_bytes(n_scans, n_cells) + 2 * (size_t)n_scans * n_cells * sizeof(double);
+}
+
+int64_t mwb_energies_tc_record_workspace_bytes(int n_scans, int n_chan, int j_count, int n_pts, int n_cells) {
+  const int64_t tc_bytes = mwb_energies_tc_workspace_bytes(n_scans, n_chan, j_count, n_pts);
+  if (tc_bytes < 0 || n_cells < 1) return -1;
+  return (int64_t)align_up((size_t)tc_bytes, 256) + (int64_t)record_maps_bytes(n_scans, n_cells);
+}
+
+int mwb_energies_tc_record(const float* sig, int n_scans, int64_t scan_stride, int n_chan, int ld, int n_samples,
+                           const int32_t* chan_txrx, const double* ant_xyz, int n_ant, double inv_scale,
+                           const double* pts_xyz, const int32_t* out_idx, int n_pts, const int32_t* tile_info,
+                           const void* table, int interp, int k0, int window, const uint8_t* valid, int n_cells,
+                           float* out_das, float* out_dmas, uint64_t* key_das, uint64_t* key_dmas, int32_t* flags,
+                           int j_lo, int j_count, void* workspace, void* stream) {
+  if (window < 32 || window % 32) return set_err(MWB_EINVAL, "mwb_energies_tc_record: window %d is not a multiple of 32", window);
+  if (!workspace || !valid || n_cells < 1 || n_scans < 0) return set_err(MWB_EINVAL, "mwb_energies_tc_record: bad arguments");
+  if (!out_das && !out_dmas) return set_err(MWB_EINVAL, "mwb_energies_tc_record: no output");
+  if (n_scans == 0 || n_pts == 0) return MWB_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  const int64_t tc_bytes = mwb_energies_tc_workspace_bytes(n_scans, n_chan, j_count, n_pts);
+  if (tc_bytes < 0) return set_err(MWB_EINVAL, "mwb_energies_tc_record: bad sizes");
+  float* tmp = reinterpret_cast<float*>(ws + align_up((size_t)tc_bytes, 256));
+  double* acc = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(tmp) + record_tmp_bytes(n_scans, n_cells));
+  const long long n = (long long)n_scans * n_cells;
+  float* tmp_k[2] = {out_das ? tmp : nullptr, out_dmas ? tmp + n : nullptr};
+  int rc;
+  cudaError_t ce = cudaMemsetAsync(acc, 0, 2 * sizeof(double) * (size_t)n, st);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(tmp, 0, 2 * sizeof(float) * (size_t)n, st);  // cells no point writes
+  if (ce != cudaSuccess) return set_err(MWB_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
+  for (int q = 0; q < window / 32; ++q) {  // both kinds in one fused W = 32 pass per chunk
+    if ((rc = mwb_energies_tc(sig, n_scans, scan_stride, n_chan, ld, n_samples, chan_txrx, ant_xyz, n_ant, inv_scale,
+                              pts_xyz, out_idx, n_pts, nullptr, tile_info, table, interp, k0 + 32 * q, 32, tmp_k[0],
+                              tmp_k[1], n_cells, nullptr, nullptr, flags, j_lo, j_count, workspace, stream)))
+      return rc;
+    for (int kk = 0; kk < 2; ++kk) {
+      if (!tmp_k[kk]) continue;
+      record_accum_kernel<<<4 * 148, 256, 0, st>>>(tmp_k[kk], acc + (size_t)kk * n, n);
+      if ((rc = check_launch("record_accum_kernel"))) return rc;
+    }
+  }
+  for (int kk = 0; kk < 2; ++kk) {
+    float* out = kk == 0 ? out_das : out_dmas;
+    if (!out) continue;
+    const unsigned bx = (unsigned)std::min(64, (n_cells + 255) / 256);
+    record_finish_kernel<<<dim3(bx, (unsigned)n_scans), 256, 0, st>>>(
+        acc + (size_t)kk * n, n_cells, valid, out, n_cells,
+        reinterpret_cast<unsigned long long*>(kk == 0 ? key_das : key_dmas), flags);
+    if ((rc = check_launch("record_finish_kernel"))) return rc;
+  }
+  return MWB_OK;
+}
+
 static long long lattice_tiles(int nx, int ny, int nz, int stride, int tx, int ty, int tz) {
   const long long Lx = (nx + stride - 1) / stride, Ly = (ny + stride - 1) / stride,
                   Lz = (nz + stride - 1) / stride;
