@@ -158,3 +158,26 @@ def test_end_to_end_ramp_and_buffer_reuse_smem_mode():
         bi.run_device(sig_d, **{f"out_{kind}": out, f"key_{kind}": keys})
         assert torch.equal(res.maps[kind].reshape(96, -1), out.cpu())
         assert np.array_equal(res.argmax[kind], bi.decode_keys(keys.cpu().numpy().view(np.uint64)))
+
+
+def test_end_to_end_full_record_tensor_cores():
+    """__call__ over the full record on the tensor-core path
+    (mwb_energies_tc_record): the host pipeline ships the union of the
+    chunks' sample ranges and returns exactly what run_device writes."""
+    model = synth.ScanModel()
+    sig, _ = synth.batch_2d(model, list(range(300, 340)))
+    grid = synth.grid_square(0.024, 48)  # 0.5 mm: every tile within the tensor-core path's delay spread
+    bi = BatchImager(model.geometry(), model.pairs(), model.n_samples, grid, window=(0, model.n_samples),
+                     mode="auto")
+    assert bi.uses_tensor_cores and bi.tc_record
+    first, count = bi.input_range()
+    assert 0 <= first and first + count <= model.n_samples
+    res = bi(torch.from_numpy(sig).pin_memory(), kinds=("das", "dmas"), chunk=16)
+    sig_d = bi.to_device_layout(sig)
+    n = grid.dims[0] * grid.dims[1]
+    outs = {k: torch.zeros((40, n), dtype=torch.float32, device="cuda") for k in ("das", "dmas")}
+    keys = {k: torch.zeros(40, dtype=torch.int64, device="cuda") for k in ("das", "dmas")}
+    bi.run_device(sig_d, outs["das"], outs["dmas"], keys["das"], keys["dmas"])
+    for kind in ("das", "dmas"):
+        assert torch.equal(res.maps[kind].reshape(40, -1), outs[kind].cpu())
+        assert np.array_equal(res.argmax[kind], bi.decode_keys(keys[kind].cpu().numpy().view(np.uint64)))
