@@ -528,6 +528,12 @@ int mwb_tc_sample_range(int k0, int j_lo, int j_count, int ld, int32_t* out);
 /* Elapsed milliseconds between consecutive recorded events: out_ms[i] =
  * events[i] -> events[i + 1] for i < n_events - 1 (the framework report's
  * phase timings in one call). */
+/* Host-side compaction of an (rows, n) fp64 record into fp32 rows of ld
+ * floats (zero tail) for the rows holding a nonzero sample (x != 0.0),
+ * their indices in keep; an all-zero record keeps row 0.  Returns the row
+ * count (>= 1) or a negative status.  The drop-in's upload of a new dataset
+ * (pkg/src/mwbeam/simulate.py:76-108 BackscatterDataset.signals). */
+int mwb_compact_rows_host(const double* src, int rows, int n, int ld, float* dst, int32_t* keep);
 int mwb_elapsed_ms(void* const* events, int n_events, float* out_ms);
 
 /*

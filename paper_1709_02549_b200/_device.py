@@ -170,21 +170,43 @@ def compact_channels(signals: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
 _SCANS: dict[int, tuple[weakref.ref, DeviceScan]] = {}
 
 
+def _upload_record(flat: np.ndarray, ld: int) -> tuple[torch.Tensor, np.ndarray]:
+    """Populated rows of an fp64 (rows, n) record -> device fp32 [C][ld] and
+    their indices: compacted and converted by mwb_compact_rows_host straight
+    into pinned staging (one pass, each row's zero test stopping at its first
+    nonzero word), then one asynchronous host->device copy."""
+    from . import _native as nat
+
+    rows, n = flat.shape
+    pinned = torch.cuda.is_available()
+    h = torch.empty((rows, ld), dtype=torch.float32, pin_memory=pinned)
+    keep = np.empty(rows, dtype=np.int32)
+    count = int(nat.load().mwb_compact_rows_host(flat.ctypes.data, rows, n, ld, h.data_ptr(),
+                                                  keep.ctypes.data))
+    if count < 1:
+        raise RuntimeError(f"mwb_compact_rows_host failed ({count})")
+    return h[:count].to(device(), non_blocking=pinned), keep[:count].astype(np.int64)
+
+
 def _build_scan(ds) -> DeviceScan:
     geom = ds.geometry
     sig = np.asarray(ds.signals)
     m, _, n = sig.shape
     flat = sig.reshape(m * m, n)
-    keep = np.flatnonzero(np.any(flat != 0.0, axis=1)) if n > 0 else np.zeros(0, dtype=np.int64)
-    if keep.size == 0:  # as compact_channels: keep channel (0, 0), all zeros
-        keep = np.zeros(1, dtype=np.int64)
-    pairs = np.stack([keep // m, keep % m], axis=1).astype(np.int32)
     ld = round4(n)
+    if sig.dtype == np.float64 and flat.flags.c_contiguous and n > 0:
+        dev_sig, keep = _upload_record(flat, ld)
+    else:
+        keep = np.flatnonzero(np.any(flat != 0.0, axis=1)) if n > 0 else np.zeros(0, dtype=np.int64)
+        if keep.size == 0:  # as compact_channels: keep channel (0, 0), all zeros
+            keep = np.zeros(1, dtype=np.int64)
+        dev_sig = upload_rows(flat, keep, ld)
+    pairs = np.stack([keep // m, keep % m], axis=1).astype(np.int32)
     ants = np.ascontiguousarray(np.asarray(geom.antennas, dtype=np.float64))
     chan, ant = geometry_tensors(pairs, ants)
     scale = float(geom.propagation_speed) * float(geom.sample_interval)
     return DeviceScan(
-        sig=upload_rows(flat, keep, ld),
+        sig=dev_sig,
         chan=chan,
         ant=ant,
         inv_scale=1.0 / scale,

@@ -125,6 +125,7 @@ _SIGNATURES = {
          _I, _I, _P, _P],
         _I,
     ),
+    "mwb_compact_rows_host": ([_P, _I, _I, _I, _P, _P], _I),
     "mwb_lattice_tile_count": ([_I, _I, _I], _I64),
     "mwb_enumerate_lattice_padded": (
         [_D, _D, _D, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P],

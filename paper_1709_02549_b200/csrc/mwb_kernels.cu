@@ -1636,6 +1636,39 @@ int mwb_tc_sample_range(int k0, int j_lo, int j_count, int ld, int32_t* out) {
   return MWB_OK;
 }
 
+// Host-side compaction of a reference record (the drop-in's upload of a new
+// dataset): the rows of an (rows, n) fp64 array that hold a nonzero sample
+// (x != 0.0: -0.0 counts as zero, NaN as nonzero -- numpy's flat != 0.0 of
+// _device.compact_channels), converted to fp32 rows of ld floats with a zero
+// tail.  A row's scan stops at its first nonzero word; an all-zero record
+// keeps row 0 (zeros).  Returns the row count, or a negative status.
+int mwb_compact_rows_host(const double* src, int rows, int n, int ld, float* dst, int32_t* keep) {
+  if (!src || !dst || !keep || rows < 1 || n < 0 || ld < n) return set_err(MWB_EINVAL, "mwb_compact_rows_host: bad arguments");
+  int count = 0;
+  for (int r = 0; r < rows; ++r) {
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(src + (size_t)r * n);
+    bool nz = false;
+    for (int i = 0; i < n && !nz; i += 64) {
+      uint64_t acc = 0;
+      const int e = std::min(n, i + 64);
+      for (int k = i; k < e; ++k) acc |= w[k] << 1;  // drop the sign: -0.0 is zero
+      nz = acc != 0;
+    }
+    if (!nz) continue;
+    const double* x = src + (size_t)r * n;
+    float* o = dst + (size_t)count * ld;
+    for (int k = 0; k < n; ++k) o[k] = (float)x[k];
+    for (int k = n; k < ld; ++k) o[k] = 0.f;
+    keep[count++] = r;
+  }
+  if (count == 0) {
+    for (int k = 0; k < ld; ++k) dst[k] = 0.f;
+    keep[0] = 0;
+    count = 1;
+  }
+  return count;
+}
+
 int mwb_elapsed_ms(void* const* events, int n_events, float* out_ms) {
   if (n_events < 2 || !events || !out_ms) return set_err(MWB_EINVAL, "mwb_elapsed_ms: bad arguments");
   for (int i = 0; i + 1 < n_events; ++i) {

@@ -218,3 +218,36 @@ def test_round2_entry_points_validate_arguments(lib):
     assert first == 487 and 150 + 32 <= count <= 1024 - first  # covers every window offset plus W
     assert lib.mwb_tc_sample_range(1000, 10, 150, 1024, out) == 0 and out[0] + out[1] == 1024  # clipped to ld
     assert lib.mwb_tc_sample_range(0, 0, 8, 1024, out) == -1  # fewer than 16 offsets
+
+
+def test_compact_rows_host_matches_numpy():
+    """mwb_compact_rows_host (a host function: no GPU needed) keeps exactly the
+    rows numpy's flat != 0.0 keeps (-0.0 is zero, NaN is not), converts them to
+    fp32 with a zero tail, and keeps row 0 for an all-zero record."""
+    import numpy as np
+
+    from paper_1709_02549_b200 import _native as nat
+
+    lib = nat.load()
+    rng = np.random.default_rng(7)
+    for rows, n, ld in ((144, 2048, 2048), (9, 13, 16), (5, 1, 4)):
+        rec = rng.standard_normal((rows, n))
+        rec[rng.random(rows) < 0.5] = 0.0
+        rec[1] = -0.0
+        if rows > 3:
+            rec[3] = 0.0
+            rec[3, n // 2] = np.nan
+        dst = np.full((rows, ld), 7.0, dtype=np.float32)
+        keep = np.zeros(rows, dtype=np.int32)
+        cnt = lib.mwb_compact_rows_host(rec.ctypes.data, rows, n, ld, dst.ctypes.data, keep.ctypes.data)
+        want = np.flatnonzero(np.any(rec != 0.0, axis=1))
+        assert cnt == max(1, want.size)
+        assert np.array_equal(keep[:cnt], want)
+        assert np.array_equal(dst[:cnt, :n], rec[want].astype(np.float32), equal_nan=True)
+        assert not dst[:cnt, n:].any()
+    zero = np.zeros((4, 8))
+    dst = np.ones((4, 8), dtype=np.float32)
+    keep = np.full(4, -1, dtype=np.int32)
+    assert lib.mwb_compact_rows_host(zero.ctypes.data, 4, 8, 8, dst.ctypes.data, keep.ctypes.data) == 1
+    assert keep[0] == 0 and not dst[0].any()
+    assert lib.mwb_compact_rows_host(None, 4, 8, 8, dst.ctypes.data, keep.ctypes.data) < 0
