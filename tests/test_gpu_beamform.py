@@ -316,7 +316,8 @@ class TestGoldenBaselineScans:
     """cfg0 (100x100, DAS/DMAS) and cfg1 (200x200 DMAS) against reference output."""
 
     @pytest.fixture(scope="class")
-    def scan(self):
+    @classmethod
+    def scan(cls):
         z = np.load(GOLDEN / "scan_cfg0.npz")
         model = synth.ScanModel()
         ds, tumour = synth.dataset_2d(model, seed=0)
