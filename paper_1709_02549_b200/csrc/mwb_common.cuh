@@ -172,6 +172,39 @@ __device__ __forceinline__ void accumulate_channel(float2 (&s)[CH], float2& qe, 
                                                    const Load& load, const int valid) {
   static_assert(CH % 4 == 0, "chunk starts must keep the 16-byte span alignment phase");
   float2 prev = load(0);
+#ifdef MWB_RATIO_FORM
+  // a = f0 * a',  a' = y[k] + r*y[k+1],  r = f1/f0  (f0 = 1 - f1 >= 2^-23):
+  //   s += f0*a' is one FFMA, and sum_k a^2 = f0^2 * sum_k a'^2, so the
+  //   channel costs 3 FFMA per sample (2 for DAS) instead of 4 (3).
+  const float2 r = make_float2(__fdividef(f1.x, f0.x), __fdividef(f1.y, f0.y));
+  float2 qce = make_float2(0.f, 0.f);
+#ifdef MWB_RATIO_Q2
+  float2 qco = make_float2(0.f, 0.f);
+#endif
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const float2 nxt = load(k + 1);
+    const float2 ap = __ffma2_rn(r, nxt, prev);
+    s[k] = __ffma2_rn(f0, ap, s[k]);
+    if (KIND != KIND_DAS && (!TAIL || k < valid)) {
+#ifdef MWB_RATIO_Q2
+      if (k & 1)
+        qco = __ffma2_rn(ap, ap, qco);
+      else
+#endif
+        qce = __ffma2_rn(ap, ap, qce);
+    }
+    prev = nxt;
+  }
+  if (KIND != KIND_DAS) {
+    const float2 g = __fmul2_rn(f0, f0);
+    qe = __ffma2_rn(g, qce, qe);
+#ifdef MWB_RATIO_Q2
+    qo = __ffma2_rn(g, qco, qo);
+#endif
+  }
+  return;
+#endif
 #pragma unroll
   for (int k = 0; k < CH; ++k) {
     const float2 nxt = load(k + 1);
