@@ -9,6 +9,12 @@ constexpr int TILE = 2 * TPB;     // focal points per CTA
 #define MWB_W48_MINB 3  // CTAs per SM of the W = 48 kernel: 3 (<= 168 registers, one channel in flight) beat 2
                         // (255 registers, two channels): 7.9 vs 8.4 ms on the configs[4] volume
 #endif
+#ifndef MWB_W32_CH
+#define MWB_W32_CH 32  // register chunk of every other window (experiment knob: 16, with MWB_W32_MINB CTAs per SM)
+#endif
+#ifndef MWB_W32_MINB
+#define MWB_W32_MINB 3
+#endif
 #ifndef MWB_W48_CH
 #define MWB_W48_CH 48  // register chunk for W % 48 == 0 windows (experiment knob: 24)
 #endif

@@ -246,8 +246,8 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
   const long long tiles = (n_pts + TILE - 1) / TILE;
   // register chunk: 48 samples for windows that are a multiple of 48 (the
   // configs[4] W = 48 would waste a third of a 2 x 32 split), else 32
-  const int ch = (window % 48 == 0 && window % 32 != 0) ? MWB_W48_CH : 32;
-  const int resident = ch == 48 ? MWB_W48_MINB : 3;  // CTAs per SM the register budget allows
+  const int ch = (window % 48 == 0 && window % 32 != 0) ? MWB_W48_CH : MWB_W32_CH;
+  const int resident = ch == 48 ? MWB_W48_MINB : MWB_W32_MINB;  // CTAs per SM the register budget allows
   // stage capacity: every channel's span for a compact tile, capped at 32 KB
   // and at what leaves `resident` CTAs room in the SM's 228 KB
   long long cap = (long long)n_chan * (ch + 24);
@@ -304,8 +304,9 @@ static int energies_impl(const float* sig, int n_scans, int64_t scan_stride, int
     fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 4, 32>
          : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 4, 32> : energy_kernel<KIND_BOTH, 4, 32>);
   else
-    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, 3, 32>
-         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, 3, 32> : energy_kernel<KIND_BOTH, 3, 32>);
+    fn = kind == KIND_DAS ? energy_kernel<KIND_DAS, MWB_W32_MINB, MWB_W32_CH>
+         : (kind == KIND_DMAS ? energy_kernel<KIND_DMAS, MWB_W32_MINB, MWB_W32_CH>
+                              : energy_kernel<KIND_BOTH, MWB_W32_MINB, MWB_W32_CH>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return set_err(MWB_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   fn<<<grid, TPB, L.total, st>>>(p);
@@ -330,7 +331,7 @@ int mwb_energies(const float* sig, int n_scans, int64_t scan_stride, int n_chan,
 
 int64_t mwb_energies_split_bytes(int n_pts, int n_scans, int window) {
   if (n_pts < 0 || n_scans < 0 || window < 0) return -1;
-  const int ch = (window % 48 == 0 && window % 32 != 0) ? MWB_W48_CH : 32;
+  const int ch = (window % 48 == 0 && window % 32 != 0) ? MWB_W48_CH : MWB_W32_CH;
   return (int64_t)n_pts * n_scans * ((window + ch - 1) / ch) * (int64_t)sizeof(float2);
 }
 
@@ -1395,7 +1396,7 @@ int mwb_segment_plan_prepare(const int32_t* chan_txrx, int n_chan, const double*
 // e.g. the full record): sized for the larger of the search and fine lists,
 // and only while that stays small (large batches fill the GPU unsplit).
 static long long seg_run_part_bytes(int n_scans, int n_sub, int fine_tps, int window) {
-  const int ch = (window % 48 == 0 && window % 32 != 0) ? MWB_W48_CH : 32;
+  const int ch = (window % 48 == 0 && window % 32 != 0) ? MWB_W48_CH : MWB_W32_CH;
   const long long n_chunks = (window + ch - 1) / ch;
   const long long rows = (long long)n_scans * std::max<long long>(seg_batch_per_scan(n_sub), (long long)fine_tps * TILE);
   const long long bytes = rows * n_chunks * (long long)sizeof(float2);
