@@ -36,6 +36,13 @@ def test_binding_covers_header():
     assert set(declared_functions()) == set(_native.EXPORTED)
 
 
+def test_integration_lists_every_export():
+    """INTEGRATION.md names every entry point a maintainer could bind."""
+    doc = (HEADER.parents[1] / "INTEGRATION.md").read_text()
+    missing = [n for n in declared_functions() if not re.search(rf"\b{n}\b", doc)]
+    assert not missing, missing
+
+
 def test_trace_layout_matches_c(lib):
     assert lib.mwb_trace_bytes() == _native.TRACE_BYTES
     assert ctypes.sizeof(_native.IterRecord) == 496
