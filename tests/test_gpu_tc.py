@@ -292,3 +292,53 @@ def test_tc_record_windows(setup, window):
             top = np.sort(want[k][s][inside])[-2:]
             if top[1] - top[0] > 2 * TOL_FP32 * abs(top[1]):
                 assert tuple(gk[k][s]) == tuple(wk[k][s]), (k, s)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_tch_fuzz_geometries_vs_oracle(seed):
+    """Seeded random set-ups around configs[3]: ring radius, permittivity
+    (sample scale), antenna count, window start, off-centre rectangular grids
+    with ragged dims and pitches up to the tensor-core limit, scan counts that
+    are no multiple of 8 or 16.  Whatever kernel mode="auto" picks, sampled
+    pixels agree with the oracle (reference fp64 algorithm, beamform.py:169-212)
+    within BASELINE's 1e-4 of the oracle's peak; when it picks the tensor
+    cores, the whole maps also agree with the fp32 CUDA-core kernel."""
+    from paper_1709_02549_b200.geometry import ImagingGrid
+
+    rng = np.random.default_rng(1000 + seed)
+    model = synth.ScanModel(n_ant=int(rng.integers(4, 13)), ring_radius=float(rng.uniform(0.06, 0.09)),
+                            eps_r=float(rng.uniform(6.0, 12.0)), t_c=float(rng.uniform(400e-12, 900e-12)))
+    n_scans = int(rng.integers(1, 21))
+    sig, _ = synth.batch_2d(model, [int(s) for s in rng.integers(0, 10_000, n_scans)], phantom_radius=(0.02, 0.03))
+    res = float(rng.uniform(0.25e-3, 0.6e-3))
+    nx, ny = (int(v) for v in rng.integers(20, 90, 2))
+    origin = (float(rng.uniform(-0.03, 0.0)), float(rng.uniform(-0.03, 0.0)))
+    grid = ImagingGrid(origin, (nx * res, ny * res), res)
+    assert grid.dims == (nx, ny)
+    win = (max(0, model.k0 + int(rng.integers(-6, 7))), 32)
+    g, pairs = model.geometry(), model.pairs()
+    auto = BatchImager(g, pairs, model.n_samples, grid, window=win, mode="auto")
+    ref = BatchImager(g, pairs, model.n_samples, grid, window=win)
+    sig_d = auto.to_device_layout(sig)
+    got, gk, flags = run(auto, sig_d)
+    want, wk, _ = run(ref, sig_d)
+    assert flags == 0
+    worst = {"fp32": 0.0, "oracle": 0.0}
+    if auto.uses_tensor_cores:
+        for k in ("das", "dmas"):
+            for s in range(n_scans):
+                worst["fp32"] = max(worst["fp32"], peak_err(got[k][s], want[k][s]))
+                assert peak_err(got[k][s], want[k][s]) <= TOL_FP32, (k, s)
+    cells = [(int(ix), int(iy)) for ix, iy in zip(rng.integers(0, nx, 60), rng.integers(0, ny, 60))]
+    for s in sorted({0, n_scans - 1}):
+        check = cells + [tuple(int(v) for v in wk[k][s]) for k in ("das", "dmas")]
+        pts = np.array([grid.cell_center(*c) for c in check])
+        slots = np.array([ix * ny + iy for ix, iy in check])
+        full = synth.embed_pairs(model.n_ant, pairs, sig[s].astype(np.float64))
+        for kind in ("das", "dmas"):
+            o = orc.windowed_energies(g.antennas, g.propagation_speed, g.sample_interval, full, pts, kind, *win)
+            peak = max(np.abs(o).max(), np.abs(want[kind][s]).max())
+            worst["oracle"] = max(worst["oracle"], np.abs(got[kind][s][slots] - o).max() / peak)
+            assert np.abs(got[kind][s][slots] - o).max() <= TOL_REF * peak
+    print(f"fuzz {seed}: M={model.n_ant} C={len(pairs)} S={n_scans} grid={nx}x{ny} res={res * 1e3:.3f} mm "
+          f"tc={auto.uses_tensor_cores} vs fp32 {worst['fp32']:.2e} vs oracle {worst['oracle']:.2e}")
