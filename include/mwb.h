@@ -507,6 +507,11 @@ int mwb_gather_composite(const float* dense, int ny, int nz, const int32_t* coar
  * readback without a framework op per copy. */
 int mwb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
+/* Blocks the calling host thread until `stream` has drained
+ * (cudaStreamSynchronize): the one wait of a drop-in call before it decodes
+ * the readback (pkg/src/mwbeam/coarse2fine.py:301-350 returns host values). */
+int mwb_stream_synchronize(void* stream);
+
 /* Stream-ordered 2-D copy (cudaMemcpy2DAsync, cudaMemcpyDefault): `height`
  * rows of `width` bytes, row pitches in bytes. */
 int mwb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,

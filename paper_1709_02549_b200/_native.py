@@ -195,6 +195,7 @@ _SIGNATURES = {
     "mwb_gather_composite": ([_P, _I, _I, _P, _I, _P, _P, _I64, _P], _I),
     "mwb_memcpy_async": ([_P, _P, _I64, _P], _I),
     "mwb_memcpy2d_async": ([_P, _I64, _P, _I64, _I64, _I64, _P], _I),
+    "mwb_stream_synchronize": ([_P], _I),
     "mwb_tc_plan_steps": ([_P, _I, _I, _I, _I, _I, _P], _I),
     "mwb_tc_sample_range": ([_I, _I, _I, _I, _P], _I),
     "mwb_elapsed_ms": ([_P, _I, _P], _I),

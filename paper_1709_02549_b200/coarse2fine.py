@@ -539,7 +539,7 @@ class _FrameworkPlan(dv.GraphPlan):
                  dv.stream_handle())
 
     def finish(self) -> tuple[EnergyMap, FrameworkReport]:
-        torch.cuda.current_stream().synchronize()
+        dv.sync_stream()
         nx, ny = self.grid.dims
         blk = self.h_res.numpy()
         h = blk[: _Status.BYTES].view(np.int64)
@@ -557,7 +557,7 @@ class _FrameworkPlan(dv.GraphPlan):
         if used > self._res_copy:  # ROI beyond the budget: copy the whole used block again
             self.h_res = torch.empty(used, dtype=torch.uint8, pin_memory=self._pin)
             nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), used, dv.stream_handle())
-            torch.cuda.current_stream().synchronize()
+            dv.sync_stream()
             blk = self.h_res.numpy()
         comp = blk[self._o_vals: used].view(np.float32)
         composite = EnergyMap._from_loader(self.grid, functools.partial(self._dense_arrays, comp, final),

@@ -1600,6 +1600,11 @@ int mwb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
   return e == cudaSuccess ? MWB_OK : set_err(MWB_ECUDA, "cudaMemcpyAsync: %s", cudaGetErrorString(e));
 }
 
+int mwb_stream_synchronize(void* stream) {
+  const cudaError_t e = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? MWB_OK : set_err(MWB_ECUDA, "cudaStreamSynchronize: %s", cudaGetErrorString(e));
+}
+
 int mwb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
                        void* stream) {
   if (width < 0 || height < 0 || dpitch < width || spitch < width || ((width && height) && (!dst || !src)))

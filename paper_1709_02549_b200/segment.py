@@ -274,7 +274,7 @@ class _SegmentPlan(dv.GraphPlan):
     def finish(self, kind) -> tuple[EnergyMap, SegmentReport]:
         if self.tree is not None:
             return self._finish_block(kind)
-        torch.cuda.current_stream().synchronize()
+        dv.sync_stream()
         grid = self.grid
         nx, ny = grid.dims
         keys, counts, flags = self.status.read(self.h_status.numpy())
@@ -317,7 +317,7 @@ class _SegmentPlan(dv.GraphPlan):
 
     def _finish_block(self, kind) -> tuple[EnergyMap, SegmentReport]:
         """The region-tree path: everything from the one result block."""
-        torch.cuda.current_stream().synchronize()
+        dv.sync_stream()
         grid = self.grid
         nx, ny = grid.dims
         blk = self.h_res.numpy()
@@ -330,7 +330,7 @@ class _SegmentPlan(dv.GraphPlan):
         if used > self._res_copy:  # final region beyond the budget: copy the whole used block again
             self.h_res = torch.empty(used, dtype=torch.uint8, pin_memory=self._pin)
             nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), used, dv.stream_handle())
-            torch.cuda.current_stream().synchronize()
+            dv.sync_stream()
             blk = self.h_res.numpy()
         n_fine = int(counts[0])
         n_sub = self.n_sub

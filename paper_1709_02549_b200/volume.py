@@ -482,7 +482,7 @@ class _VolumeFrameworkPlan(dv.GraphPlan):
         return vals, valid
 
     def finish(self) -> tuple[VolumeMap, VolumeReport]:
-        torch.cuda.current_stream().synchronize()
+        dv.sync_stream()
         grid, d = self.grid, self.d
         blk = self.h_res.numpy()
         keys, counts, flags = _Status.decode(blk[: _Status.BYTES].view(np.int64))
@@ -493,7 +493,7 @@ class _VolumeFrameworkPlan(dv.GraphPlan):
         if used > self._res_copy:  # final box beyond the budget: copy the whole used block again
             self.h_res = torch.empty(used, dtype=torch.uint8, pin_memory=self._pin)
             nat.call("mwb_memcpy_async", self.h_res.data_ptr(), self.res.data_ptr(), used, dv.stream_handle())
-            torch.cuda.current_stream().synchronize()
+            dv.sync_stream()
             blk = self.h_res.numpy()
         comp = blk[self._o_vals: used].view(np.float32)
         composite = VolumeMap._from_loader(grid, functools.partial(self._arrays, comp, final), stride=d, roi=final)
